@@ -1,0 +1,176 @@
+"""ctypes wrapper of the plain CPU oracle (oracle/oracle.c).
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / --impl reference legs.  The product path (paper_1707_03581_b200) never
+imports this package.  See oracle/oracle.h for what is computed and the passages it follows.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+_d = ctypes.c_double
+_i32 = ctypes.c_int32
+_i64 = ctypes.c_int64
+_p = ctypes.c_void_p
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle.c -> liboracle.so with gcc (plain C99, -O2)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", "-std=c99", "-O2", "-fPIC", "-shared", "-o", _LIB, _SRC, "-lm"])
+    return _LIB
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_LIB)
+        L.or_create.restype = _p
+        L.or_create.argtypes = [_i64, _p, _i64, _p, _i64, _p, _p, _i64, _p, _i64, _p, _i64, _p, _p,
+                                _i32, _d, _d, _d]
+        L.or_last_error.restype = ctypes.c_char_p
+        L.or_destroy.argtypes = [_p]
+        L.or_set_robin.argtypes = [_p, _i32, _i32, _d, _d, _d, _d, _d]
+        L.or_n.restype = _i64
+        L.or_n.argtypes = [_p]
+        L.or_n_fixed.restype = _i64
+        L.or_n_fixed.argtypes = [_p]
+        L.or_vol_nnz.restype = _i64
+        L.or_vol_nnz.argtypes = [_p]
+        L.or_get_volume.argtypes = [_p, _p, _p, _p, _p, _p, _p]
+        L.or_assemble_interface.argtypes = [_p, _d, _d, _d, _d]
+        L.or_iface_nnz.restype = _i64
+        L.or_iface_nnz.argtypes = [_p]
+        L.or_get_interface.argtypes = [_p, _p, _p, _p, _p, _p]
+        L.or_step.argtypes = [_p, _d, _d, _i32, _d, _d, _d, _d, _d, _d, _d, _d, _d, _p, _i32, _d, _i32, _p]
+        L.or_ie_residual_rows.argtypes = [_p, _d, _d, _d, _d, _d, _p, _p, _i64, _p, _p, _p]
+        L.or_apply_system.argtypes = [_p, _d, _p, _p]
+        _lib = L
+    return _lib
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+class Oracle:
+    """One coupled two-mesh system (fixed part rows first, then moving part)."""
+
+    def __init__(self, fixed, moving, nu, rho_cp, alpha_iface, iface_tag=4, robin=()):
+        L = lib()
+        self._keep = []
+
+        def arr(a, dt):
+            a = np.ascontiguousarray(a, dtype=dt)
+            self._keep.append(a)
+            return a
+        xf, tf, ff, gf = (arr(fixed.xyz, np.float64), arr(fixed.tets, np.int32),
+                          arr(fixed.bfaces, np.int32), arr(fixed.bface_tag, np.int32))
+        xm, tm, fm, gm = (arr(moving.xyz, np.float64), arr(moving.tets, np.int32),
+                          arr(moving.bfaces, np.int32), arr(moving.bface_tag, np.int32))
+        h = L.or_create(xf.shape[0], _ptr(xf), tf.shape[0], _ptr(tf), ff.shape[0], _ptr(ff), _ptr(gf),
+                        xm.shape[0], _ptr(xm), tm.shape[0], _ptr(tm), fm.shape[0], _ptr(fm), _ptr(gm),
+                        iface_tag, nu, rho_cp, alpha_iface)
+        self._keep = []
+        if not h:
+            raise ValueError("oracle: " + L.or_last_error().decode())
+        self.h = h
+        self.n = int(L.or_n(h))
+        self.nf = int(L.or_n_fixed(h))
+        for r in robin:
+            self.set_robin(r.part, r.tag, r.alpha, r.T_ref, r.grad)
+
+    @classmethod
+    def from_config(cls, cfg):
+        return cls(cfg.fixed, cfg.moving, cfg.nu, cfg.rho_cp, cfg.alpha_iface, cfg.iface_tag, cfg.robin)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().or_destroy(self.h)
+            self.h = None
+
+    def set_robin(self, part, tag, alpha, T_ref, grad=(0.0, 0.0, 0.0)):
+        rc = lib().or_set_robin(self.h, part, tag, alpha, T_ref, *grad)
+        if rc:
+            raise ValueError("oracle: " + lib().or_last_error().decode())
+
+    def volume(self):
+        """(rowptr, col, A, B, ML, benv) of the fixed-pattern volume operator."""
+        L = lib()
+        nnz = int(L.or_vol_nnz(self.h))
+        rowptr = np.zeros(self.n + 1, np.int64)
+        col = np.zeros(nnz, np.int32)
+        A = np.zeros(nnz)
+        B = np.zeros(nnz)
+        ML = np.zeros(self.n)
+        benv = np.zeros(self.n)
+        L.or_get_volume(self.h, _ptr(rowptr), _ptr(col), _ptr(A), _ptr(B), _ptr(ML), _ptr(benv))
+        return rowptr, col, A, B, ML, benv
+
+    def interface(self, offset: Sequence[float], eta: float):
+        """(rowptr, col, val, bG, area) of K_G = M_B + C_B at the given offset."""
+        L = lib()
+        rc = L.or_assemble_interface(self.h, float(offset[0]), float(offset[1]), float(offset[2]), float(eta))
+        if rc:
+            raise ValueError("oracle: " + L.or_last_error().decode())
+        nnz = int(L.or_iface_nnz(self.h))
+        rowptr = np.zeros(self.n + 1, np.int64)
+        col = np.zeros(nnz, np.int32)
+        val = np.zeros(nnz)
+        bG = np.zeros(self.n)
+        area = ctypes.c_double(0.0)
+        L.or_get_interface(self.h, _ptr(rowptr), _ptr(col), _ptr(val), _ptr(bG), ctypes.byref(area))
+        return rowptr, col, val, bG, area.value
+
+    def step(self, T: np.ndarray, t: float, dt: float, nsteps: int, scen, solver: str = "cg",
+             rtol: float = 1e-12, maxit: int = 0):
+        """Advance T (length n, modified copy returned) by nsteps implicit-Euler steps.
+        Returns (T_new, stats[nsteps, 4] = iterations, rel. res, true rel. res, |Gamma_R|)."""
+        T = np.array(T, dtype=np.float64, copy=True)
+        stats = np.zeros((nsteps, 4))
+        rc = lib().or_step(self.h, t, dt, nsteps, scen.s0, scen.amp, scen.period,
+                           scen.dir[0], scen.dir[1], scen.dir[2], scen.eta0, scen.eta_amp,
+                           scen.eta_period, _ptr(T), 1 if solver == "cholesky" else 0, rtol,
+                           maxit, _ptr(stats))
+        if rc:
+            raise RuntimeError(f"oracle step failed rc={rc}: " + lib().or_last_error().decode())
+        return T, stats
+
+    def residual_rows(self, dt, offset, eta, T0, T1, rows):
+        T0 = np.ascontiguousarray(T0, dtype=np.float64)
+        T1 = np.ascontiguousarray(T1, dtype=np.float64)
+        rows = np.ascontiguousarray(rows, dtype=np.int64)
+        res = np.zeros(rows.shape[0])
+        bnorm = ctypes.c_double(0.0)
+        rc = lib().or_ie_residual_rows(self.h, dt, float(offset[0]), float(offset[1]), float(offset[2]),
+                                       float(eta), _ptr(T0), _ptr(T1), rows.shape[0], _ptr(rows),
+                                       _ptr(res), ctypes.byref(bnorm))
+        if rc:
+            raise RuntimeError("oracle residual failed: " + lib().or_last_error().decode())
+        return res, bnorm.value
+
+    def apply_system(self, dt, x):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.zeros_like(x)
+        lib().or_apply_system(self.h, dt, _ptr(x), _ptr(y))
+        return y
+
+
+def run_config(cfg, scen_index: int = 0, T_init: Optional[np.ndarray] = None, nsteps: Optional[int] = None,
+               solver: str = "cg", t0: float = 0.0):
+    """Oracle run of one scenario of a config from T0 (uniform) or T_init."""
+    o = Oracle.from_config(cfg)
+    T = np.full(o.n, cfg.T0) if T_init is None else np.array(T_init, dtype=np.float64)
+    return o.step(T, t0, cfg.dt, cfg.nsteps if nsteps is None else nsteps,
+                  cfg.scenarios[scen_index], solver=solver)

@@ -1,0 +1,753 @@
+/*
+ * oracle.c -- plain CPU oracle for the implicit-Euler hot path of arXiv 1707.03581.
+ *
+ * TEST INFRASTRUCTURE ONLY (see oracle.h).  Plain C99, fp64, single thread, no blocking,
+ * fusion or reordering beyond the definitions cited at each function.  Written
+ * independently of the CUDA library; the two share no code.
+ *
+ * Pins (tests/test_oracle_*.py): volume = sum of lumped mass; stiffness rows sum to 0;
+ * Kuhn 7-point closed form; patch test; Robin sums against exact polynomial integrals;
+ * interface area, row cancellation, friction sum and u^T C_B v = alpha int u v for linear
+ * u, v; matching-mesh C_B = -M_B = alpha * consistent surface mass; dense Cholesky = CG;
+ * uniform state is a fixed point; energy balance; two-slab analytic steady state.
+ */
+#include "oracle.h"
+
+#include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#ifndef M_PI
+#define M_PI 3.14159265358979323846
+#endif
+
+static char g_err[512];
+static void set_err(const char *msg) { snprintf(g_err, sizeof g_err, "%s", msg); }
+const char *or_last_error(void) { return g_err; }
+
+#define MAX_ROBIN 64
+
+typedef struct {
+    int32_t part, tag;
+    double alpha, T_ref, g[3];
+} robin_t;
+
+typedef struct {          /* one surface triangle of Gamma, projected to the plane */
+    int32_t node[3];      /* coupled-system node numbers */
+    double p[3][2];       /* 2-D coordinates, counter-clockwise */
+    double lo[2], hi[2];  /* bounding box */
+} stri_t;
+
+/* growable list of (column, value) of one interface row; linear search on insert */
+typedef struct { int32_t n, cap; int32_t *col; double *val; } rowlist_t;
+
+struct or_sys {
+    int64_t nf, nm, n;
+    double *xyz;          /* [n][3] both parts, coupled numbering */
+    int64_t nt;           /* tets of both parts */
+    int32_t *tets;        /* [nt][4] coupled numbering */
+    int64_t nb;
+    int32_t *faces;       /* [nb][3] coupled numbering */
+    int32_t *ftag;        /* [nb] */
+    int32_t *fpart;       /* [nb] 0 fixed / 1 moving */
+    int32_t iface_tag;
+    double nu, rho_cp, alpha;
+    /* volume operator, fixed pattern */
+    int64_t *rowptr;
+    int32_t *col;
+    double *A, *B, *ML, *benv;
+    int nrobin;
+    robin_t robin[MAX_ROBIN];
+    /* interface geometry */
+    int drop;             /* coordinate dropped by the projection to the plane */
+    int ax0, ax1;         /* kept coordinates */
+    double area_scale;    /* 3-D area = 2-D area * area_scale */
+    double plane_n[3], plane_c;
+    int64_t nsA, nsB;
+    stri_t *sA, *sB;      /* fixed (rail top) / moving (stock bottom) in reference frame */
+    /* interface operator (last assembly) */
+    rowlist_t *rows;      /* per-row accumulation lists of K_G */
+    int64_t inz;
+    int64_t *irowptr;
+    int32_t *icol;
+    double *ival, *bG, iarea;
+};
+
+/* ------------------------------------------------------------------------------------ */
+/* small helpers                                                                        */
+/* ------------------------------------------------------------------------------------ */
+
+static int cmp_i32(const void *a, const void *b) {
+    int32_t x = *(const int32_t *)a, y = *(const int32_t *)b;
+    return (x > y) - (x < y);
+}
+
+/* position of column j in row i of the volume pattern (binary search); -1 if absent */
+static int64_t find_entry(const int64_t *rowptr, const int32_t *col, int64_t i, int32_t j) {
+    int64_t lo = rowptr[i], hi = rowptr[i + 1] - 1;
+    while (lo <= hi) {
+        int64_t mid = (lo + hi) / 2;
+        if (col[mid] == j) return mid;
+        if (col[mid] < j) lo = mid + 1; else hi = mid - 1;
+    }
+    return -1;
+}
+
+/* 3x3 determinant of the columns a, b, c */
+static double det3(const double a[3], const double b[3], const double c[3]) {
+    return a[0] * (b[1] * c[2] - b[2] * c[1]) - a[1] * (b[0] * c[2] - b[2] * c[0]) +
+           a[2] * (b[0] * c[1] - b[1] * c[0]);
+}
+
+/* ------------------------------------------------------------------------------------ */
+/* P1 element matrices on a tetrahedron                                          */
+/* ------------------------------------------------------------------------------------ */
+
+/* Volume V and gradients of the barycentric coordinates lambda_0..3.
+ * J = [x1-x0, x2-x0, x3-x0] (columns); grad lambda_k (k=1..3) = row k-1 of J^{-1};
+ * grad lambda_0 = -(sum of the others).  Returns det J. */
+static double tet_gradients(const double *x0, const double *x1, const double *x2,
+                            const double *x3, double grad[4][3]) {
+    double e1[3], e2[3], e3[3];
+    for (int d = 0; d < 3; d++) {
+        e1[d] = x1[d] - x0[d];
+        e2[d] = x2[d] - x0[d];
+        e3[d] = x3[d] - x0[d];
+    }
+    double detJ = det3(e1, e2, e3);
+    /* rows of J^{-1} = (e2 x e3, e3 x e1, e1 x e2) / det J */
+    double c1[3] = {e2[1] * e3[2] - e2[2] * e3[1], e2[2] * e3[0] - e2[0] * e3[2], e2[0] * e3[1] - e2[1] * e3[0]};
+    double c2[3] = {e3[1] * e1[2] - e3[2] * e1[1], e3[2] * e1[0] - e3[0] * e1[2], e3[0] * e1[1] - e3[1] * e1[0]};
+    double c3[3] = {e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2], e1[0] * e2[1] - e1[1] * e2[0]};
+    for (int d = 0; d < 3; d++) {
+        grad[1][d] = c1[d] / detJ;
+        grad[2][d] = c2[d] / detJ;
+        grad[3][d] = c3[d] / detJ;
+        grad[0][d] = -(grad[1][d] + grad[2][d] + grad[3][d]);
+    }
+    return detJ;
+}
+
+/* ------------------------------------------------------------------------------------ */
+/* sparsity pattern of the volume operator: node adjacency through tetrahedra           */
+/* ------------------------------------------------------------------------------------ */
+
+static int build_pattern(or_sys *s) {
+    int64_t n = s->n, nt = s->nt;
+    /* node -> tet incidence (counting sort) */
+    int64_t *cnt = calloc((size_t)n + 1, sizeof *cnt);
+    if (!cnt) return -1;
+    for (int64_t e = 0; e < nt; e++)
+        for (int a = 0; a < 4; a++) cnt[s->tets[4 * e + a] + 1]++;
+    for (int64_t i = 0; i < n; i++) cnt[i + 1] += cnt[i];
+    int64_t *inc = malloc(sizeof *inc * (size_t)cnt[n]);
+    int64_t *pos = malloc(sizeof *pos * (size_t)n);
+    if (!inc || !pos) return -1;
+    memcpy(pos, cnt, sizeof *pos * (size_t)n);
+    for (int64_t e = 0; e < nt; e++)
+        for (int a = 0; a < 4; a++) inc[pos[s->tets[4 * e + a]]++] = e;
+    /* rows: sorted unique vertices of the incident tets (includes the diagonal) */
+    s->rowptr = malloc(sizeof *s->rowptr * (size_t)(n + 1));
+    int32_t *buf = malloc(sizeof *buf * 4096);
+    if (!s->rowptr || !buf) return -1;
+    int64_t cap = 16 * n + 16, nnz = 0;
+    s->col = malloc(sizeof *s->col * (size_t)cap);
+    if (!s->col) return -1;
+    s->rowptr[0] = 0;
+    for (int64_t i = 0; i < n; i++) {
+        int64_t m = 0;
+        for (int64_t k = cnt[i]; k < cnt[i + 1]; k++) {
+            const int32_t *t = s->tets + 4 * inc[k];
+            for (int a = 0; a < 4; a++) {
+                if (m >= 4096) { set_err("node valence too large"); return -1; }
+                buf[m++] = t[a];
+            }
+        }
+        qsort(buf, (size_t)m, sizeof *buf, cmp_i32);
+        int64_t u = 0;
+        for (int64_t k = 0; k < m; k++)
+            if (u == 0 || buf[k] != buf[u - 1]) buf[u++] = buf[k];
+        if (nnz + u > cap) {
+            cap = 2 * (nnz + u);
+            s->col = realloc(s->col, sizeof *s->col * (size_t)cap);
+            if (!s->col) return -1;
+        }
+        memcpy(s->col + nnz, buf, sizeof *buf * (size_t)u);
+        nnz += u;
+        s->rowptr[i + 1] = nnz;
+    }
+    free(buf);
+    free(cnt);
+    free(inc);
+    free(pos);
+    return 0;
+}
+
+/* ------------------------------------------------------------------------------------ */
+/* element-by-element assembly of A and lumped M                          */
+/* ------------------------------------------------------------------------------------ */
+
+static int assemble_volume(or_sys *s) {
+    int64_t nnz = s->rowptr[s->n];
+    s->A = calloc((size_t)nnz, sizeof *s->A);
+    s->B = calloc((size_t)nnz, sizeof *s->B);
+    s->ML = calloc((size_t)s->n, sizeof *s->ML);
+    s->benv = calloc((size_t)s->n, sizeof *s->benv);
+    if (!s->A || !s->B || !s->ML || !s->benv) return -1;
+    for (int64_t e = 0; e < s->nt; e++) {
+        const int32_t *t = s->tets + 4 * e;
+        double grad[4][3];
+        double detJ = tet_gradients(s->xyz + 3 * t[0], s->xyz + 3 * t[1], s->xyz + 3 * t[2],
+                                    s->xyz + 3 * t[3], grad);
+        if (!(detJ > 0.0)) { set_err("tetrahedron with non-positive det J"); return -1; }
+        double V = detJ / 6.0;
+        for (int a = 0; a < 4; a++) {
+            /* consistent mass rho Cp V/20 (1 + delta_ab), row sum = rho Cp V/4 */
+            s->ML[t[a]] += s->rho_cp * V / 4.0;
+            for (int b = 0; b < 4; b++) {
+                double g = grad[a][0] * grad[b][0] + grad[a][1] * grad[b][1] + grad[a][2] * grad[b][2];
+                int64_t k = find_entry(s->rowptr, s->col, t[a], t[b]);
+                s->A[k] += -s->nu * V * g;   /* A = -nu int grad phi . grad phi */
+            }
+        }
+    }
+    return 0;
+}
+
+/* Robin part B_env, b_env: per face, M_s = S/12 (1 + delta_ab) is the exact
+ * consistent surface mass of P1 on a triangle of area S; T_i is linear, so
+ * int T_i phi_a = sum_b T_i(x_b) M_s[a][b] exactly. */
+static void assemble_robin(or_sys *s) {
+    int64_t nnz = s->rowptr[s->n];
+    memset(s->B, 0, sizeof *s->B * (size_t)nnz);
+    memset(s->benv, 0, sizeof *s->benv * (size_t)s->n);
+    for (int64_t f = 0; f < s->nb; f++) {
+        const robin_t *r = NULL;
+        for (int k = 0; k < s->nrobin; k++)
+            if (s->robin[k].part == s->fpart[f] && s->robin[k].tag == s->ftag[f]) r = &s->robin[k];
+        if (!r || r->alpha == 0.0) continue;
+        if (s->ftag[f] == s->iface_tag) continue;   /* Gamma_R handled by the interface */
+        const int32_t *v = s->faces + 3 * f;
+        const double *x0 = s->xyz + 3 * v[0], *x1 = s->xyz + 3 * v[1], *x2 = s->xyz + 3 * v[2];
+        double u[3], w[3], c[3];
+        for (int d = 0; d < 3; d++) { u[d] = x1[d] - x0[d]; w[d] = x2[d] - x0[d]; }
+        c[0] = u[1] * w[2] - u[2] * w[1];
+        c[1] = u[2] * w[0] - u[0] * w[2];
+        c[2] = u[0] * w[1] - u[1] * w[0];
+        double S = 0.5 * sqrt(c[0] * c[0] + c[1] * c[1] + c[2] * c[2]);
+        double Ta[3];
+        for (int a = 0; a < 3; a++) {
+            const double *x = s->xyz + 3 * v[a];
+            Ta[a] = r->T_ref + r->g[0] * x[0] + r->g[1] * x[1] + r->g[2] * x[2];
+        }
+        for (int a = 0; a < 3; a++) {
+            for (int b = 0; b < 3; b++) {
+                double Ms = S / 12.0 * (a == b ? 2.0 : 1.0);
+                int64_t k = find_entry(s->rowptr, s->col, v[a], v[b]);
+                s->B[k] -= r->alpha * Ms;
+                s->benv[v[a]] += r->alpha * Ms * Ta[b];
+            }
+        }
+    }
+}
+
+/* ------------------------------------------------------------------------------------ */
+/* interface plane and surface triangles                                                */
+/* ------------------------------------------------------------------------------------ */
+
+static void tri_project(const or_sys *s, const int32_t *v, stri_t *t) {
+    for (int a = 0; a < 3; a++) {
+        t->node[a] = v[a];
+        t->p[a][0] = s->xyz[3 * v[a] + s->ax0];
+        t->p[a][1] = s->xyz[3 * v[a] + s->ax1];
+    }
+    double ar = (t->p[1][0] - t->p[0][0]) * (t->p[2][1] - t->p[0][1]) -
+                (t->p[1][1] - t->p[0][1]) * (t->p[2][0] - t->p[0][0]);
+    if (ar < 0.0) {   /* make counter-clockwise */
+        int32_t tn = t->node[1]; t->node[1] = t->node[2]; t->node[2] = tn;
+        for (int d = 0; d < 2; d++) { double tp = t->p[1][d]; t->p[1][d] = t->p[2][d]; t->p[2][d] = tp; }
+    }
+    for (int d = 0; d < 2; d++) {
+        t->lo[d] = fmin(t->p[0][d], fmin(t->p[1][d], t->p[2][d]));
+        t->hi[d] = fmax(t->p[0][d], fmax(t->p[1][d], t->p[2][d]));
+    }
+}
+
+static int setup_interface(or_sys *s) {
+    int64_t first = -1;
+    s->nsA = s->nsB = 0;
+    for (int64_t f = 0; f < s->nb; f++) {
+        if (s->ftag[f] != s->iface_tag) continue;
+        if (first < 0) first = f;
+        if (s->fpart[f] == 0) s->nsA++; else s->nsB++;
+    }
+    s->sA = malloc(sizeof *s->sA * (size_t)(s->nsA + 1));
+    s->sB = malloc(sizeof *s->sB * (size_t)(s->nsB + 1));
+    if (!s->sA || !s->sB) return -1;
+    if (first < 0) { s->drop = 2; s->ax0 = 0; s->ax1 = 1; s->area_scale = 1.0; return 0; }
+    /* plane of the first interface face; drop the coordinate of largest |normal| */
+    const int32_t *v = s->faces + 3 * first;
+    const double *x0 = s->xyz + 3 * v[0], *x1 = s->xyz + 3 * v[1], *x2 = s->xyz + 3 * v[2];
+    double u[3], w[3], nrm[3];
+    for (int d = 0; d < 3; d++) { u[d] = x1[d] - x0[d]; w[d] = x2[d] - x0[d]; }
+    nrm[0] = u[1] * w[2] - u[2] * w[1];
+    nrm[1] = u[2] * w[0] - u[0] * w[2];
+    nrm[2] = u[0] * w[1] - u[1] * w[0];
+    double ln = sqrt(nrm[0] * nrm[0] + nrm[1] * nrm[1] + nrm[2] * nrm[2]);
+    for (int d = 0; d < 3; d++) s->plane_n[d] = nrm[d] / ln;
+    s->plane_c = s->plane_n[0] * x0[0] + s->plane_n[1] * x0[1] + s->plane_n[2] * x0[2];
+    s->drop = 0;
+    for (int d = 1; d < 3; d++) if (fabs(s->plane_n[d]) > fabs(s->plane_n[s->drop])) s->drop = d;
+    s->ax0 = s->drop == 0 ? 1 : 0;
+    s->ax1 = s->drop == 2 ? 1 : 2;
+    s->area_scale = 1.0 / fabs(s->plane_n[s->drop]);
+    double scale = sqrt(ln);
+    int64_t ia = 0, ib = 0;
+    for (int64_t f = 0; f < s->nb; f++) {
+        if (s->ftag[f] != s->iface_tag) continue;
+        const int32_t *fv = s->faces + 3 * f;
+        for (int a = 0; a < 3; a++) {
+            const double *x = s->xyz + 3 * fv[a];
+            double dist = s->plane_n[0] * x[0] + s->plane_n[1] * x[1] + s->plane_n[2] * x[2] - s->plane_c;
+            if (fabs(dist) > 1e-9 * (1.0 + scale)) { set_err("interface faces are not coplanar"); return -1; }
+        }
+        if (s->fpart[f] == 0) tri_project(s, fv, &s->sA[ia++]);
+        else tri_project(s, fv, &s->sB[ib++]);
+    }
+    return 0;
+}
+
+/* ------------------------------------------------------------------------------------ */
+/* create / destroy                                                                     */
+/* ------------------------------------------------------------------------------------ */
+
+or_sys *or_create(int64_t nf, const double *xyz_f, int64_t ntf, const int32_t *tets_f,
+                  int64_t nbf, const int32_t *faces_f, const int32_t *tags_f,
+                  int64_t nm, const double *xyz_m, int64_t ntm, const int32_t *tets_m,
+                  int64_t nbm, const int32_t *faces_m, const int32_t *tags_m,
+                  int32_t iface_tag, double nu, double rho_cp, double alpha_iface) {
+    or_sys *s = calloc(1, sizeof *s);
+    if (!s) return NULL;
+    s->nf = nf; s->nm = nm; s->n = nf + nm;
+    s->nt = ntf + ntm; s->nb = nbf + nbm;
+    s->iface_tag = iface_tag; s->nu = nu; s->rho_cp = rho_cp; s->alpha = alpha_iface;
+    s->xyz = malloc(sizeof *s->xyz * (size_t)(3 * s->n));
+    s->tets = malloc(sizeof *s->tets * (size_t)(4 * s->nt));
+    s->faces = malloc(sizeof *s->faces * (size_t)(3 * s->nb + 1));
+    s->ftag = malloc(sizeof *s->ftag * (size_t)(s->nb + 1));
+    s->fpart = malloc(sizeof *s->fpart * (size_t)(s->nb + 1));
+    if (!s->xyz || !s->tets || !s->faces || !s->ftag || !s->fpart) { or_destroy(s); return NULL; }
+    memcpy(s->xyz, xyz_f, sizeof(double) * (size_t)(3 * nf));
+    memcpy(s->xyz + 3 * nf, xyz_m, sizeof(double) * (size_t)(3 * nm));
+    for (int64_t e = 0; e < ntf; e++)
+        for (int a = 0; a < 4; a++) s->tets[4 * e + a] = tets_f[4 * e + a];
+    for (int64_t e = 0; e < ntm; e++)
+        for (int a = 0; a < 4; a++) s->tets[4 * (ntf + e) + a] = (int32_t)(tets_m[4 * e + a] + nf);
+    for (int64_t f = 0; f < nbf; f++) {
+        for (int a = 0; a < 3; a++) s->faces[3 * f + a] = faces_f[3 * f + a];
+        s->ftag[f] = tags_f[f]; s->fpart[f] = 0;
+    }
+    for (int64_t f = 0; f < nbm; f++) {
+        for (int a = 0; a < 3; a++) s->faces[3 * (nbf + f) + a] = (int32_t)(faces_m[3 * f + a] + nf);
+        s->ftag[nbf + f] = tags_m[f]; s->fpart[nbf + f] = 1;
+    }
+    for (int64_t e = 0; e < 4 * s->nt; e++)
+        if (s->tets[e] < 0 || s->tets[e] >= s->n) { set_err("tet index out of range"); or_destroy(s); return NULL; }
+    if (build_pattern(s) || assemble_volume(s) || setup_interface(s)) { or_destroy(s); return NULL; }
+    s->rows = calloc((size_t)s->n, sizeof *s->rows);
+    s->irowptr = calloc((size_t)(s->n + 1), sizeof *s->irowptr);
+    s->bG = calloc((size_t)s->n, sizeof *s->bG);
+    if (!s->rows || !s->irowptr || !s->bG) { or_destroy(s); return NULL; }
+    assemble_robin(s);
+    return s;
+}
+
+void or_destroy(or_sys *s) {
+    if (!s) return;
+    free(s->xyz); free(s->tets); free(s->faces); free(s->ftag); free(s->fpart);
+    free(s->rowptr); free(s->col); free(s->A); free(s->B); free(s->ML); free(s->benv);
+    free(s->sA); free(s->sB);
+    if (s->rows)
+        for (int64_t i = 0; i < s->n; i++) { free(s->rows[i].col); free(s->rows[i].val); }
+    free(s->rows);
+    free(s->irowptr); free(s->icol); free(s->ival); free(s->bG);
+    free(s);
+}
+
+int or_set_robin(or_sys *s, int32_t part, int32_t tag, double alpha, double T_ref,
+                 double gx, double gy, double gz) {
+    int k;
+    for (k = 0; k < s->nrobin; k++)
+        if (s->robin[k].part == part && s->robin[k].tag == tag) break;
+    if (k == s->nrobin) {
+        if (s->nrobin == MAX_ROBIN) { set_err("too many Robin entries"); return -1; }
+        s->nrobin++;
+    }
+    s->robin[k].part = part; s->robin[k].tag = tag; s->robin[k].alpha = alpha;
+    s->robin[k].T_ref = T_ref;
+    s->robin[k].g[0] = gx; s->robin[k].g[1] = gy; s->robin[k].g[2] = gz;
+    assemble_robin(s);
+    return 0;
+}
+
+int64_t or_n(const or_sys *s) { return s->n; }
+int64_t or_n_fixed(const or_sys *s) { return s->nf; }
+int64_t or_vol_nnz(const or_sys *s) { return s->rowptr[s->n]; }
+
+void or_get_volume(const or_sys *s, int64_t *rowptr, int32_t *col, double *A, double *B,
+                   double *ML, double *benv) {
+    int64_t nnz = s->rowptr[s->n];
+    if (rowptr) memcpy(rowptr, s->rowptr, sizeof *rowptr * (size_t)(s->n + 1));
+    if (col) memcpy(col, s->col, sizeof *col * (size_t)nnz);
+    if (A) memcpy(A, s->A, sizeof *A * (size_t)nnz);
+    if (B) memcpy(B, s->B, sizeof *B * (size_t)nnz);
+    if (ML) memcpy(ML, s->ML, sizeof *ML * (size_t)s->n);
+    if (benv) memcpy(benv, s->benv, sizeof *benv * (size_t)s->n);
+}
+
+/* ------------------------------------------------------------------------------------ */
+/* interface integrals on Gamma_R(t)                                         */
+/* ------------------------------------------------------------------------------------ */
+
+
+static int row_add(rowlist_t *R, int32_t j, double v) {
+    for (int32_t k = 0; k < R->n; k++)
+        if (R->col[k] == j) { R->val[k] += v; return 0; }
+    if (R->n == R->cap) {
+        int32_t nc = R->cap ? 2 * R->cap : 32;
+        int32_t *c = realloc(R->col, sizeof *c * (size_t)nc);
+        double *w = realloc(R->val, sizeof *w * (size_t)nc);
+        if (!c || !w) return -1;
+        R->col = c; R->val = w; R->cap = nc;
+    }
+    R->col[R->n] = j; R->val[R->n] = v; R->n++;
+    return 0;
+}
+
+/* Sutherland-Hodgman: clip the polygon P (n vertices) by the counter-clockwise triangle C.
+ * Inside = left of (or on) every edge of C.  Returns the number of output vertices. */
+static int clip_polygon(double P[][2], int n, const double C[3][2], double out[][2]) {
+    double cur[16][2];
+    int m = n;
+    for (int k = 0; k < n; k++) { cur[k][0] = P[k][0]; cur[k][1] = P[k][1]; }
+    for (int e = 0; e < 3 && m > 0; e++) {
+        const double *c1 = C[e], *c2 = C[(e + 1) % 3];
+        double ex = c2[0] - c1[0], ey = c2[1] - c1[1];
+        double nxt[16][2];
+        int q = 0;
+        for (int k = 0; k < m; k++) {
+            const double *pc = cur[k], *pp = cur[(k + m - 1) % m];
+            double dc = ex * (pc[1] - c1[1]) - ey * (pc[0] - c1[0]);
+            double dp = ex * (pp[1] - c1[1]) - ey * (pp[0] - c1[0]);
+            if (dc >= 0.0) {
+                if (dp < 0.0) {
+                    double t = dp / (dp - dc);
+                    nxt[q][0] = pp[0] + t * (pc[0] - pp[0]);
+                    nxt[q][1] = pp[1] + t * (pc[1] - pp[1]);
+                    q++;
+                }
+                nxt[q][0] = pc[0]; nxt[q][1] = pc[1]; q++;
+            } else if (dp >= 0.0) {
+                double t = dp / (dp - dc);
+                nxt[q][0] = pp[0] + t * (pc[0] - pp[0]);
+                nxt[q][1] = pp[1] + t * (pc[1] - pp[1]);
+                q++;
+            }
+        }
+        m = q;
+        for (int k = 0; k < m; k++) { cur[k][0] = nxt[k][0]; cur[k][1] = nxt[k][1]; }
+    }
+    for (int k = 0; k < m; k++) { out[k][0] = cur[k][0]; out[k][1] = cur[k][1]; }
+    return m;
+}
+
+/* barycentric coordinates of y in the triangle T */
+static void bary(const double T[3][2], const double y[2], double lam[3]) {
+    double D = (T[1][0] - T[0][0]) * (T[2][1] - T[0][1]) - (T[1][1] - T[0][1]) * (T[2][0] - T[0][0]);
+    lam[1] = ((y[0] - T[0][0]) * (T[2][1] - T[0][1]) - (y[1] - T[0][1]) * (T[2][0] - T[0][0])) / D;
+    lam[2] = ((T[1][0] - T[0][0]) * (y[1] - T[0][1]) - (T[1][1] - T[0][1]) * (y[0] - T[0][0])) / D;
+    lam[0] = 1.0 - lam[1] - lam[2];
+}
+
+int or_assemble_interface(or_sys *s, double ox, double oy, double oz, double eta) {
+    double o3[3] = {ox, oy, oz};
+    double od = o3[0] * s->plane_n[0] + o3[1] * s->plane_n[1] + o3[2] * s->plane_n[2];
+    if (fabs(od) > 1e-12 * (1.0 + fabs(ox) + fabs(oy) + fabs(oz))) { set_err("offset leaves the interface plane"); return -1; }
+    double o[2] = {o3[s->ax0], o3[s->ax1]};
+    memset(s->bG, 0, sizeof *s->bG * (size_t)s->n);
+    for (int64_t i = 0; i < s->n; i++) s->rows[i].n = 0;
+    s->iarea = 0.0;
+    double al = s->alpha;
+    /* brute force over all pairs (F in rail top, G in stock bottom) with an AABB test */
+    for (int64_t fa = 0; fa < s->nsA; fa++) {
+        const stri_t *F = &s->sA[fa];
+        for (int64_t gb = 0; gb < s->nsB; gb++) {
+            const stri_t *G = &s->sB[gb];
+            if (G->lo[0] + o[0] > F->hi[0] || G->hi[0] + o[0] < F->lo[0] ||
+                G->lo[1] + o[1] > F->hi[1] || G->hi[1] + o[1] < F->lo[1]) continue;
+            double Gs[3][2], Fp[3][2], poly[16][2];
+            for (int a = 0; a < 3; a++) {
+                Gs[a][0] = G->p[a][0] + o[0]; Gs[a][1] = G->p[a][1] + o[1];
+                Fp[a][0] = F->p[a][0]; Fp[a][1] = F->p[a][1];
+            }
+            int m = clip_polygon(Fp, 3, Gs, poly);
+            /* integrals of this pair: Mff = int phi_F phi_F, Cfg = int phi_F phi_G,
+             * Mgg = int phi_G phi_G, bf = int phi_F, bg = int phi_G over F cap (G + o) */
+            double Mff[3][3] = {{0}}, Cfg[3][3] = {{0}}, Mgg[3][3] = {{0}}, bf[3] = {0}, bg[3] = {0};
+            double pair_area = 0.0;
+            /* fan from vertex 0; 3-point edge-midpoint rule, exact for degree 2 */
+            for (int k = 1; k + 1 < m; k++) {
+                const double *v0 = poly[0], *v1 = poly[k], *v2 = poly[k + 1];
+                double ar2 = 0.5 * ((v1[0] - v0[0]) * (v2[1] - v0[1]) - (v1[1] - v0[1]) * (v2[0] - v0[0]));
+                if (!(ar2 > 0.0)) continue;
+                double area = ar2 * s->area_scale;
+                pair_area += area;
+                double qp[3][2] = {{0.5 * (v0[0] + v1[0]), 0.5 * (v0[1] + v1[1])},
+                                   {0.5 * (v1[0] + v2[0]), 0.5 * (v1[1] + v2[1])},
+                                   {0.5 * (v2[0] + v0[0]), 0.5 * (v2[1] + v0[1])}};
+                for (int q = 0; q < 3; q++) {
+                    double w = area / 3.0;
+                    double lam[3], mu[3], yG[2] = {qp[q][0] - o[0], qp[q][1] - o[1]};
+                    bary(F->p, qp[q], lam);
+                    bary(G->p, yG, mu);
+                    for (int a = 0; a < 3; a++) {
+                        bf[a] += w * lam[a];
+                        bg[a] += w * mu[a];
+                        for (int b = 0; b < 3; b++) {
+                            Mff[a][b] += w * lam[a] * lam[b];
+                            Cfg[a][b] += w * lam[a] * mu[b];
+                            Mgg[a][b] += w * mu[a] * mu[b];
+                        }
+                    }
+                }
+            }
+            if (!(pair_area > 0.0)) continue;
+            s->iarea += pair_area;
+            for (int a = 0; a < 3; a++) {
+                int32_t fi = F->node[a], gi = G->node[a];
+                s->bG[fi] += 0.5 * eta * bf[a];   /* b_fix(t) = int eta/2 phi_fix */
+                s->bG[gi] += 0.5 * eta * bg[a];   /* b_mov(t) */
+                for (int b = 0; b < 3; b++) {
+                    /* M_B,fix = -int alpha phi_fix phi_fix */
+                    if (row_add(&s->rows[fi], F->node[b], -al * Mff[a][b])) return -1;
+                    /* M_B,mov = -int alpha phi_mov phi_mov */
+                    if (row_add(&s->rows[gi], G->node[b], -al * Mgg[a][b])) return -1;
+                    /* C_B = int alpha phi_mov phi_fix (fixed rows) and its
+                     * transpose in the moving rows */
+                    if (row_add(&s->rows[fi], G->node[b], al * Cfg[a][b])) return -1;
+                    if (row_add(&s->rows[G->node[b]], fi, al * Cfg[a][b])) return -1;
+                }
+            }
+        }
+    }
+    /* row lists -> CSR (columns sorted) */
+    int64_t nnz = 0;
+    for (int64_t i = 0; i < s->n; i++) nnz += s->rows[i].n;
+    free(s->icol); free(s->ival);
+    s->icol = malloc(sizeof *s->icol * (size_t)(nnz + 1));
+    s->ival = malloc(sizeof *s->ival * (size_t)(nnz + 1));
+    if (!s->icol || !s->ival) return -1;
+    int64_t u = 0;
+    s->irowptr[0] = 0;
+    for (int64_t i = 0; i < s->n; i++) {
+        rowlist_t *R = &s->rows[i];
+        /* insertion sort by column */
+        for (int32_t k = 1; k < R->n; k++) {
+            int32_t c = R->col[k];
+            double v = R->val[k];
+            int32_t m = k - 1;
+            while (m >= 0 && R->col[m] > c) { R->col[m + 1] = R->col[m]; R->val[m + 1] = R->val[m]; m--; }
+            R->col[m + 1] = c; R->val[m + 1] = v;
+        }
+        for (int32_t k = 0; k < R->n; k++) { s->icol[u] = R->col[k]; s->ival[u] = R->val[k]; u++; }
+        s->irowptr[i + 1] = u;
+    }
+    s->inz = u;
+    return 0;
+}
+
+int64_t or_iface_nnz(const or_sys *s) { return s->inz; }
+
+void or_get_interface(const or_sys *s, int64_t *rowptr, int32_t *col, double *val,
+                      double *bG, double *area) {
+    if (rowptr) memcpy(rowptr, s->irowptr, sizeof *rowptr * (size_t)(s->n + 1));
+    if (col) memcpy(col, s->icol, sizeof *col * (size_t)s->inz);
+    if (val) memcpy(val, s->ival, sizeof *val * (size_t)s->inz);
+    if (bG) memcpy(bG, s->bG, sizeof *bG * (size_t)s->n);
+    if (area) *area = s->iarea;
+}
+
+/* ------------------------------------------------------------------------------------ */
+/* implicit-Euler system K~ = M_L - dt (A + B_env + K_G)             */
+/* ------------------------------------------------------------------------------------ */
+
+void or_apply_system(const or_sys *s, double dt, const double *x, double *y) {
+    for (int64_t i = 0; i < s->n; i++) {
+        double acc = 0.0;
+        for (int64_t k = s->rowptr[i]; k < s->rowptr[i + 1]; k++)
+            acc += (s->A[k] + s->B[k]) * x[s->col[k]];
+        for (int64_t k = s->irowptr[i]; k < s->irowptr[i + 1]; k++)
+            acc += s->ival[k] * x[s->icol[k]];
+        y[i] = s->ML[i] * x[i] - dt * acc;
+    }
+}
+
+static void system_diagonal(const or_sys *s, double dt, double *d) {
+    for (int64_t i = 0; i < s->n; i++) {
+        double kii = 0.0;
+        int64_t k = find_entry(s->rowptr, s->col, i, (int32_t)i);
+        kii += s->A[k] + s->B[k];
+        for (int64_t m = s->irowptr[i]; m < s->irowptr[i + 1]; m++)
+            if (s->icol[m] == i) kii += s->ival[m];
+        d[i] = s->ML[i] - dt * kii;
+    }
+}
+
+static void system_rhs(const or_sys *s, double dt, const double *T, double *b) {
+    for (int64_t i = 0; i < s->n; i++) b[i] = s->ML[i] * T[i] + dt * (s->benv[i] + s->bG[i]);
+}
+
+static double dot(int64_t n, const double *a, const double *b) {
+    double acc = 0.0;
+    for (int64_t i = 0; i < n; i++) acc += a[i] * b[i];
+    return acc;
+}
+
+/* Jacobi-preconditioned CG (textbook; preconditioner = diag of the full K~).
+ * Stops when ||r||_2 <= rtol ||b||_2 (recursive residual).  Returns iterations, or -1. */
+static int64_t pcg(const or_sys *s, double dt, const double *b, double *x, double rtol,
+                   int64_t maxit, double *relres, double *truerel) {
+    int64_t n = s->n;
+    double *r = malloc(sizeof *r * (size_t)n), *z = malloc(sizeof *z * (size_t)n);
+    double *p = malloc(sizeof *p * (size_t)n), *q = malloc(sizeof *q * (size_t)n);
+    double *d = malloc(sizeof *d * (size_t)n);
+    if (!r || !z || !p || !q || !d) return -2;
+    system_diagonal(s, dt, d);
+    or_apply_system(s, dt, x, q);
+    for (int64_t i = 0; i < n; i++) { r[i] = b[i] - q[i]; z[i] = r[i] / d[i]; p[i] = z[i]; }
+    double bnorm = sqrt(dot(n, b, b));
+    double rz = dot(n, r, z);
+    double rnorm = sqrt(dot(n, r, r));
+    int64_t it = 0;
+    while (rnorm > rtol * bnorm && it < maxit) {
+        or_apply_system(s, dt, p, q);
+        double alpha = rz / dot(n, p, q);
+        for (int64_t i = 0; i < n; i++) { x[i] += alpha * p[i]; r[i] -= alpha * q[i]; }
+        for (int64_t i = 0; i < n; i++) z[i] = r[i] / d[i];
+        double rz_new = dot(n, r, z);
+        double beta = rz_new / rz;
+        rz = rz_new;
+        for (int64_t i = 0; i < n; i++) p[i] = z[i] + beta * p[i];
+        rnorm = sqrt(dot(n, r, r));
+        it++;
+    }
+    *relres = bnorm > 0 ? rnorm / bnorm : rnorm;
+    or_apply_system(s, dt, x, q);
+    for (int64_t i = 0; i < n; i++) r[i] = b[i] - q[i];
+    *truerel = bnorm > 0 ? sqrt(dot(n, r, r)) / bnorm : sqrt(dot(n, r, r));
+    free(r); free(z); free(p); free(q); free(d);
+    return rnorm > rtol * bnorm ? -1 : it;
+}
+
+/* dense Cholesky K~ = L L^T, then two triangular solves (brute force for tiny meshes) */
+static int dense_cholesky_solve(const or_sys *s, double dt, const double *b, double *x) {
+    int64_t n = s->n;
+    double *K = calloc((size_t)(n * n), sizeof *K);
+    if (!K) return -2;
+    for (int64_t i = 0; i < n; i++) {
+        for (int64_t k = s->rowptr[i]; k < s->rowptr[i + 1]; k++)
+            K[i * n + s->col[k]] -= dt * (s->A[k] + s->B[k]);
+        for (int64_t k = s->irowptr[i]; k < s->irowptr[i + 1]; k++)
+            K[i * n + s->icol[k]] -= dt * s->ival[k];
+        K[i * n + i] += s->ML[i];
+    }
+    for (int64_t j = 0; j < n; j++) {
+        double dsum = K[j * n + j];
+        for (int64_t k = 0; k < j; k++) dsum -= K[j * n + k] * K[j * n + k];
+        if (!(dsum > 0.0)) { free(K); set_err("Cholesky: matrix not SPD"); return -3; }
+        double ljj = sqrt(dsum);
+        K[j * n + j] = ljj;
+        for (int64_t i = j + 1; i < n; i++) {
+            double v = K[i * n + j];
+            for (int64_t k = 0; k < j; k++) v -= K[i * n + k] * K[j * n + k];
+            K[i * n + j] = v / ljj;
+        }
+    }
+    for (int64_t i = 0; i < n; i++) {   /* L y = b */
+        double v = b[i];
+        for (int64_t k = 0; k < i; k++) v -= K[i * n + k] * x[k];
+        x[i] = v / K[i * n + i];
+    }
+    for (int64_t i = n - 1; i >= 0; i--) {   /* L^T x = y */
+        double v = x[i];
+        for (int64_t k = i + 1; k < n; k++) v -= K[k * n + i] * x[k];
+        x[i] = v / K[i * n + i];
+    }
+    free(K);
+    return 0;
+}
+
+int or_step(or_sys *s, double t, double dt, int32_t nsteps,
+            double s0, double amp, double period, double dx, double dy, double dz,
+            double eta0, double eta_amp, double eta_period,
+            double *T, int32_t solver, double rtol, int32_t maxit, double *stats) {
+    int64_t n = s->n;
+    double *b = malloc(sizeof *b * (size_t)n), *x = malloc(sizeof *x * (size_t)n);
+    if (!b || !x) return -2;
+    int rc = 0;
+    for (int32_t step = 0; step < nsteps; step++) {
+        /* reading R3: fully implicit, K, b_G, eta and s all at t' = t + (n+1) dt */
+        double tp = t + (double)(step + 1) * dt;
+        double sp = s0 + amp * sin(2.0 * M_PI * tp / period);
+        double etap = eta0 * (1.0 + eta_amp * sin(2.0 * M_PI * tp / eta_period));
+        if (or_assemble_interface(s, sp * dx, sp * dy, sp * dz, etap)) { rc = -5; break; }
+        system_rhs(s, dt, T, b);
+        double relres = 0.0, truerel = 0.0;
+        int64_t it = 0;
+        memcpy(x, T, sizeof *x * (size_t)n);   /* x0 = T^n */
+        if (solver == 1) {
+            if (dense_cholesky_solve(s, dt, b, x)) { rc = -3; break; }
+            double *q = malloc(sizeof *q * (size_t)n);
+            or_apply_system(s, dt, x, q);
+            double rr = 0.0, bb = dot(n, b, b);
+            for (int64_t i = 0; i < n; i++) rr += (b[i] - q[i]) * (b[i] - q[i]);
+            free(q);
+            relres = truerel = sqrt(rr / bb);
+        } else {
+            it = pcg(s, dt, b, x, rtol, maxit > 0 ? maxit : 10 * n, &relres, &truerel);
+        }
+        if (stats) {
+            stats[4 * step + 0] = (double)it;
+            stats[4 * step + 1] = relres;
+            stats[4 * step + 2] = truerel;
+            stats[4 * step + 3] = s->iarea;
+        }
+        if (it < 0) { rc = -4; break; }
+        memcpy(T, x, sizeof *T * (size_t)n);
+    }
+    free(b); free(x);
+    return rc;
+}
+
+int or_ie_residual_rows(or_sys *s, double dt, double ox, double oy, double oz, double eta,
+                        const double *T0, const double *T1, int64_t nrows,
+                        const int64_t *rows, double *res, double *bnorm) {
+    if (or_assemble_interface(s, ox, oy, oz, eta)) return -5;
+    int64_t n = s->n;
+    double *b = malloc(sizeof *b * (size_t)n);
+    if (!b) return -2;
+    system_rhs(s, dt, T0, b);
+    *bnorm = sqrt(dot(n, b, b));
+    for (int64_t k = 0; k < nrows; k++) {
+        int64_t i = rows[k];
+        double acc = 0.0;
+        for (int64_t m = s->rowptr[i]; m < s->rowptr[i + 1]; m++)
+            acc += (s->A[m] + s->B[m]) * T1[s->col[m]];
+        for (int64_t m = s->irowptr[i]; m < s->irowptr[i + 1]; m++)
+            acc += s->ival[m] * T1[s->icol[m]];
+        res[k] = s->ML[i] * T1[i] - dt * acc - b[i];
+    }
+    free(b);
+    return 0;
+}
