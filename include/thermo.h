@@ -1,0 +1,165 @@
+/*
+ * thermo.h -- C ABI of the B200 implicit-Euler hot path of arXiv 1707.03581
+ * (Naumann, Ruprecht, Wensch, "Toward transient finite element simulation of thermal
+ * deformation of machine tools in real-time").  P:n = /root/reference/PAPER.md line n.
+ *
+ * The library advances the semi-discrete, two-mesh P1 finite-element heat system
+ *
+ *   M dT/dt = (A + B_env + M_B(t)) T + C_B(t) T_other + b_env + b(t)
+ *
+ * of a fixed stand/rail (part 0) and a stock (part 1) sliding along it with implicit Euler
+ * (P:211-213): per step n, with t' = t + (n+1) dt,
+ *
+ *   (M_L - dt K(t')) T^{n+1} = M_L T^n + dt (b_env + b_G(t'))
+ *
+ * where M_L is the row-sum lumped mass scaled by rho*Cp, K(t') = blockdiag(A + B_env)
+ * + [[M_B,fix, C_B],[C_B^T, M_B,mov]](t') and b_G(t') the friction source eta(t')/2.
+ * The interface terms are re-integrated every step on the exact intersection of the two
+ * non-matching surface triangulations at the stock's current offset, and the
+ * coupled system is solved monolithically by Jacobi-preconditioned CG in fp64 until
+ * ||b - K~ x||_2 <= rtol ||b||_2 (default 1e-12), from x0 = T^n.
+ *
+ * Everything runs in hand-written sm_100a CUDA kernels on the caller's stream; there is no
+ * CPU fallback.  Several independent scenarios (different motion / friction laws) may be
+ * advanced together (batched mode, BASELINE.json config 4).
+ *
+ * Conventions for every entry point:
+ *  - Return value: THERMO_OK (0) or a negative THERMO_E* code; functions never abort and
+ *    never throw.  thermo_last_error(ctx) (or thermo_last_error(NULL) for a failed create)
+ *    returns a human-readable message of the last failure on that context / thread.
+ *  - Arrays are plain host pointers unless stated; all input arrays are copied during the
+ *    call, so the caller may free them on return.  Indices are 0-based int32.
+ *  - A context owns all device memory it allocates until thermo_destroy.  One context must
+ *    not be used from two host threads at the same time.
+ */
+#ifndef THERMO_H
+#define THERMO_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    THERMO_OK = 0,
+    THERMO_EINVAL = -1,   /* bad argument: sizes, indices, inverted tet, non-planar interface */
+    THERMO_ENOMEM = -2,   /* device or host allocation failed */
+    THERMO_ECUDA = -3,    /* CUDA runtime error (message has the CUDA error string) */
+    THERMO_ENOCONV = -4,  /* CG did not reach rtol within maxit; see thermo_get_stats */
+    THERMO_EGEOM = -5     /* interface capacity exceeded or intersection area inconsistent */
+};
+
+/* One part's tetrahedral P1 mesh.
+ *  xyz[n_nodes][3]   node coordinates (m), fp64, row-major
+ *  tets[n_tets][4]   vertex indices; every tet must have positive det J (else EINVAL)
+ *  bfaces[n_bfaces][3], bface_tag[n_bfaces]: boundary triangles and their tags.  Tags select
+ *  Robin data (thermo_set_bc); tag 0 (or any tag without Robin data) is insulated.
+ *  The moving part's coordinates are its reference position (offset s = 0). */
+typedef struct {
+    int64_t n_nodes;
+    const double *xyz;
+    int64_t n_tets;
+    const int32_t *tets;
+    int64_t n_bfaces;
+    const int32_t *bfaces;
+    const int32_t *bface_tag;
+} thermo_mesh;
+
+/* Motion and friction law of one scenario:
+ *   offset s(t) = s0 + amp * sin(2 pi t / period)  along the unit vector dir (in the plane)
+ *   eta(t)      = eta0 * (1 + eta_amp * sin(2 pi t / eta_period))   [W/m^2]            */
+typedef struct {
+    double s0, amp, period;
+    double dir[3];
+    double eta0, eta_amp, eta_period;
+} thermo_scenario;
+
+/* Create a context: copies both meshes to the device, assembles M_L and A
+ * element by element on the device, extracts the interface triangulations (faces tagged
+ * iface_tag_fixed on part 0 and iface_tag_moving on part 1; they must be coplanar), sizes
+ * the per-step interface storage by sweeping each scenario's motion range, and sets the
+ * state of every scenario to the uniform temperature T_init.
+ *  nu [W/mK], rho_cp [J/m^3K], alpha_iface [W/m^2K]
+ *  n_scen >= 1 scenarios, scen[n_scen]
+ *  cuda_stream: a cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream) or NULL for
+ *  the legacy default stream; every later call enqueues its work on this stream.
+ * On failure *out is NULL; message via thermo_last_error(NULL). */
+int thermo_create_mesh(void **out, const thermo_mesh *fixed, const thermo_mesh *moving,
+                       int32_t iface_tag_fixed, int32_t iface_tag_moving,
+                       double nu, double rho_cp, double alpha_iface,
+                       int32_t n_scen, const thermo_scenario *scen, double T_init,
+                       void *cuda_stream);
+
+/* Robin boundary data for faces of `part` (0 fixed, 1 moving) carrying `tag`:
+ *   nu grad T . n = alpha (T_a(x) - T),   T_a(x) = T_ref + grad_T . x
+ * Assembles B_env = -int alpha phi phi dS and b_env = int alpha T_a phi dS on the
+ * device.  alpha = 0 removes the condition.  For part 1 grad_T must be orthogonal to every
+ * scenario's motion direction (b_env of the stock is then time-independent), else EINVAL.
+ * Interface tags cannot carry Robin data (EINVAL). */
+int thermo_set_bc(void *ctx, int32_t part, int32_t tag, double alpha, double T_ref,
+                  const double grad_T[3]);
+
+/* Advance every scenario by nsteps implicit-Euler steps of size dt from time t:
+ * step n uses t' = t + (n+1) dt for s, eta, M_B, C_B and b_G (fully implicit).
+ * Work is enqueued on the context stream; the call synchronises that stream once at the
+ * end to report status.  Returns THERMO_ENOCONV if some scenario's CG did not converge
+ * within maxit (steps before the failing one are committed; the failing step and its
+ * residual are in thermo_get_stats), THERMO_EGEOM if the interface storage overflowed. */
+int thermo_step(void *ctx, double t, double dt, int32_t nsteps);
+
+/* Copy the temperature of one scenario and part (0 fixed, 1 moving, -1 both: fixed nodes
+ * first) into out[n]; n must equal the node count of the selection (EINVAL otherwise).
+ * out_on_device != 0: out is a device pointer (e.g. a torch tensor's data_ptr()), the copy
+ * is asynchronous on the context stream.  Otherwise out is host memory and the call
+ * synchronises the stream. */
+int thermo_get_T(void *ctx, int32_t scen, int32_t part, double *out, int64_t n,
+                 int32_t out_on_device);
+
+/* Overwrite the temperature of one scenario and part (same selection rules as get_T). */
+int thermo_set_T(void *ctx, int32_t scen, int32_t part, const double *in, int64_t n,
+                 int32_t in_on_device);
+
+/* CG stopping rule ||r||_2 <= rtol ||b||_2 (default 1e-12) and iteration cap
+ * (default 0 = min(10 N, 10000)).  EINVAL if rtol <= 0 or maxit < 0. */
+int thermo_set_solver(void *ctx, double rtol, int32_t maxit);
+
+typedef struct {
+    int64_t n_fixed, n_moving;       /* node counts */
+    int64_t nnz_volume;              /* stored nonzeros of the volume operator (unpadded) */
+    int64_t nnz_volume_padded;       /* stored sliced-ELL entries incl. padding */
+    int32_t n_scen;
+    int32_t n_iface_rows;            /* rail-top + stock-bottom nodes */
+    int32_t iface_capacity;          /* interface entries per row per scenario */
+    int32_t last_nsteps;             /* nsteps of the last thermo_step */
+    int64_t total_iters;             /* CG iterations of the last thermo_step, all scenarios */
+    int32_t max_iters;               /* max over steps/scenarios of the last thermo_step */
+    int32_t failed_step;             /* -1, or the first step (0-based, last call) that failed */
+    int32_t failed_scen;
+    double failed_relres;            /* achieved relative residual of the failing solve */
+    double last_relres;              /* max over scenarios, last step */
+    int64_t steps_done;              /* committed steps since create */
+    double iface_area;               /* |Gamma_R| of scenario 0 at the last step (m^2) */
+    double ms_iface;                 /* device time of the interface kernels, last call (ms) */
+    double ms_solve;                 /* device time of the CG solve kernels, last call (ms) */
+    int32_t solve_grid;              /* CTAs of the persistent CG kernel */
+    int32_t solve_block;             /* threads per CTA */
+} thermo_stats;
+
+int thermo_get_stats(const void *ctx, thermo_stats *out);
+
+/* enable != 0: record CUDA events on the context stream around every interface and solve
+ * kernel of thermo_step, so that thermo_get_stats reports ms_iface / ms_solve of the last
+ * call (small overhead per step).  Default off. */
+int thermo_set_timing(void *ctx, int32_t enable);
+
+/* Per-step CG iteration counts of the last thermo_step: out[nsteps * n_scen], step-major. */
+int thermo_get_step_iters(const void *ctx, int32_t *out, int64_t n);
+
+const char *thermo_last_error(const void *ctx);
+void thermo_destroy(void *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* THERMO_H */

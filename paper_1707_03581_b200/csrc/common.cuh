@@ -1,0 +1,144 @@
+// common.cuh -- shared device helpers and parameter blocks of the thermo library.
+// Part of the CUDA product path; never includes anything from oracle/.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#ifndef THERMO_BLOCK
+#define THERMO_BLOCK 256
+#endif
+#define THERMO_WARPS (THERMO_BLOCK / 32)
+#define THERMO_NRED 8  // reduction slots per CTA
+
+namespace thermo {
+
+// ---------------------------------------------------------------------------------
+// memory helpers
+// ---------------------------------------------------------------------------------
+
+// L2 eviction policy for data streamed once per sweep (matrix values / columns).
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
+// Streaming read: non-coherent path, no L1 allocation, L2 evict-first policy.
+__device__ __forceinline__ double ld_stream(const double *p, uint64_t pol) {
+    double v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ int ld_stream(const int *p, uint64_t pol) {
+    int v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
+
+// ---------------------------------------------------------------------------------
+// deterministic reductions: xor-butterfly inside a warp (every lane ends with the same
+// bits), fixed-order combination across warps and CTAs.
+// ---------------------------------------------------------------------------------
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Reduce NV values over the CTA and store them to partials[blockIdx.x * THERMO_NRED + slot + j].
+template <int NV>
+__device__ __forceinline__ void cta_reduce_store(double (&v)[NV], double *smem, double *partials,
+                                                 int slot) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) v[j] = warp_sum(v[j]);
+    if (lane == 0) {
+#pragma unroll
+        for (int j = 0; j < NV; ++j) smem[warp * NV + j] = v[j];
+    }
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+            double x = lane < THERMO_WARPS ? smem[lane * NV + j] : 0.0;
+            x = warp_sum(x);
+            if (lane == 0) partials[blockIdx.x * THERMO_NRED + slot + j] = x;
+        }
+    }
+    __syncthreads();
+}
+
+// Sum the per-CTA partials of G CTAs (fixed order); every thread of every CTA returns the
+// identical value.  Must be called by all threads of the CTA after a grid-wide barrier.
+template <int NV>
+__device__ __forceinline__ void grid_total(const double *partials, int G, int slot, double *smem,
+                                           double (&out)[NV]) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (warp == 0) {
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+            double x = 0.0;
+            for (int g = lane; g < G; g += 32) x += partials[g * THERMO_NRED + slot + j];
+            x = warp_sum(x);
+            if (lane == 0) smem[64 + j] = x;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < NV; ++j) out[j] = smem[64 + j];
+    __syncthreads();
+}
+
+// ---------------------------------------------------------------------------------
+// parameter blocks
+// ---------------------------------------------------------------------------------
+
+struct BinGrid {      // uniform bin grid over one surface triangulation (2-D, own frame)
+    double x0, y0, inv_h;
+    int nx, ny;
+    const int32_t *ptr;   // [nx*ny + 1]
+    const int32_t *ids;   // triangle ids, ascending within a bin
+};
+
+struct PairRec {       // one overlapping (rail-top, stock-bottom) triangle pair, one side's view
+    int other;         // triangle of the other surface
+    int pad_;
+    double own[6];     // int phi_own_a phi_own_b, symmetric 3x3 (00 01 02 11 12 22)
+    double cross[9];   // int phi_own_a phi_other_b, [a*3 + b]
+    double b[3];       // int phi_own_a
+};
+
+struct IfaceParams {
+    int nTA, nTB;         // rail-top / stock-bottom triangles
+    int pcap;             // pair records per triangle
+    PairRec *pairs;       // [(side A: S*nTA | side B: S*nTB) * pcap]
+    int32_t *pcnt;        // [S*nTA + S*nTB]
+    int n_if;             // interface rows: [0, nA) rail top (fixed), [nA, n_if) stock bottom
+    int nA;
+    int S;                // scenarios
+    int cap;              // ELL capacity per row
+    const int32_t *if_rows;   // [n_if] global row of each interface node
+    const double2 *uv;        // [n_if] in-plane coordinates (fixed frame / stock reference frame)
+    const int32_t *star_ptr;  // [n_if + 1]
+    const int32_t *star_tri;  // own-surface triangles around each node, ascending
+    const int4 *triA;         // [nTA] (k0, k1, k2, -) interface-row indices, counter-clockwise
+    const int4 *triB;
+    const double4 *boxA;      // [nTA] (lo.x, lo.y, hi.x, hi.y)
+    const double4 *boxB;
+    BinGrid binA, binB;
+    double alpha, dt;
+    const double *step_sc;    // [S][4] this step: (o.x, o.y, eta, s)
+    const double *Dvol;       // [N] volume diagonal of K~
+    // outputs, per scenario s: ell_cnt[s*n_if + k], ell_col/val[(s*cap + c)*n_if + k]
+    int32_t *ell_cnt;
+    int32_t *ell_col;
+    double *ell_val;
+    double *if_b;             // [S][n_if] dt-free friction source eta/2 int phi
+    double *if_phi;           // [S][n_if] int_{Gamma_R} phi
+    double *Dinv;             // S == 1: [N] Jacobi inverse diagonal, interface rows rewritten
+    double *if_dinv;          // S > 1: [S][n_if]
+    int *status;              // status[1] |= overflow
+};
+
+}  // namespace thermo

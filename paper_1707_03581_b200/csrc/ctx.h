@@ -1,0 +1,124 @@
+// ctx.h -- host-side context of the thermo library (see include/thermo.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace thermo {
+
+#define THERMO_MAX_ROW 96   // max distinct neighbours of one node in the volume pattern
+
+struct Robin {
+    int part, tag;
+    double alpha, T_ref, g[3];
+};
+
+struct Scen {
+    double s0, amp, period, dir[3], eta0, eta_amp, eta_period;
+    double d2[2];  // in-plane motion direction
+};
+
+struct Ctx {
+    cudaStream_t stream = nullptr;
+    int dev = 0, num_sms = 0;
+    std::string err;
+
+    int64_t nf = 0, nm = 0, N = 0;
+    int S = 1;
+    double nu = 0, rho_cp = 0, alpha = 0;
+    int iface_tag_f = 0, iface_tag_m = 0;
+    std::vector<Scen> scen;
+    std::vector<Robin> robin;
+
+    // mesh on the device (coupled numbering: fixed nodes first)
+    int64_t ntets = 0, nfaces = 0;
+    double *d_xyz = nullptr;         // [N][3]
+    int32_t *d_tets = nullptr;       // [ntets][4]
+    int32_t *d_faces = nullptr;      // [nfaces][3]
+    int32_t *d_fkey = nullptr;       // [nfaces] part * 65536 + tag
+    int64_t *d_tinc_ptr = nullptr;   // node -> tet incidence
+    int32_t *d_tinc = nullptr;
+    int64_t *d_finc_ptr = nullptr;   // node -> boundary face incidence
+    int32_t *d_finc = nullptr;
+
+    // volume operator in sliced ELL (slice height 32)
+    int64_t nslices = 0, nnz = 0, nnz_pad = 0;
+    int64_t *d_slice_ptr = nullptr;  // [nslices + 1] entry offsets
+    int32_t *d_col = nullptr;        // [nnz_pad]
+    double *d_A = nullptr;           // stiffness  -nu int grad phi grad phi
+    double *d_R = nullptr;           // Robin      -int alpha phi phi
+    double *d_val = nullptr;         // K~ = M_L - dt (A + R) (volume part)
+    int64_t *d_diagpos = nullptr;    // [N]
+    double *d_ML = nullptr, *d_benv = nullptr, *d_Dvol = nullptr, *d_Dinv = nullptr;
+    double *d_robin_tab = nullptr;   // [nrobin][8]
+    double built_dt = -1.0;
+    bool robin_dirty = true;
+
+    // interface
+    int n_if = 0, nA = 0, nTA = 0, nTB = 0, cap = 0, pcap = 0;
+    PairRec *d_pairs = nullptr;
+    int32_t *d_pcnt = nullptr;
+    int32_t *d_if_rows = nullptr;
+    double2 *d_uv = nullptr;
+    int32_t *d_star_ptr = nullptr, *d_star_tri = nullptr;
+    int4 *d_triA = nullptr, *d_triB = nullptr;
+    double4 *d_boxA = nullptr, *d_boxB = nullptr;
+    BinGrid binA{}, binB{};
+    int32_t *d_binA_ptr = nullptr, *d_binA_ids = nullptr, *d_binB_ptr = nullptr, *d_binB_ids = nullptr;
+    int32_t *d_slice_if = nullptr;   // [nslices + 1]
+    int32_t *d_ell_cnt = nullptr, *d_ell_col = nullptr;
+    double *d_ell_val = nullptr, *d_if_b = nullptr, *d_if_phi = nullptr, *d_if_dinv = nullptr;
+    double plane_n[3] = {0, 0, 1}, e1[3] = {1, 0, 0}, e2[3] = {0, 1, 0};
+    double min_edge = 0.0;
+
+    // state and CG workspace (N x S, row-major)
+    double *d_T[2] = {nullptr, nullptr};
+    int cur = 0;                     // index of the buffer holding the committed state
+    double *d_z = nullptr, *d_p[2] = {nullptr, nullptr}, *d_q = nullptr;
+    double *d_partials = nullptr;    // [grid][THERMO_NRED]
+    int *d_status = nullptr;         // [0] failure, [1] overflow, [2] failed step, [3] failed scen
+    double *d_fail_relres = nullptr;
+    double *d_step_sc = nullptr;     // [steps][S][4]
+    int32_t *d_iters = nullptr;      // [steps][S]
+    double *d_relres = nullptr;      // [steps][S]
+    double *d_area = nullptr;        // [steps]
+    int64_t step_cap = 0;
+    int cg_grid = 0;
+
+    double rtol = 1e-12;
+    int maxit = 0;
+    bool timing = false;
+    std::vector<cudaEvent_t> events;   // 2 * nsteps + 1 when timing
+    double ms_iface = 0.0, ms_solve = 0.0;
+
+    // stats of the last thermo_step
+    int last_nsteps = 0;
+    std::vector<int32_t> h_iters;
+    std::vector<double> h_relres, h_area;
+    int64_t steps_done = 0;
+    int failed_step = -1, failed_scen = -1;
+    double failed_relres = 0.0;
+};
+
+// assemble.cu
+int assemble_create(Ctx &c, const double *xyz, const int32_t *tets, const int32_t *faces,
+                    const int32_t *fkey);
+int assemble_robin(Ctx &c);
+int build_operator(Ctx &c, double dt);
+
+// iface.cu
+int iface_setup(Ctx &c, const double *h_xyz, const std::vector<int32_t> &facesA,
+                const std::vector<int32_t> &facesB);
+void iface_params(Ctx &c, IfaceParams &p, const double *step_sc, double dt);
+int iface_launch(Ctx &c, const IfaceParams &p);
+
+// cg.cu
+int cg_setup(Ctx &c);
+int cg_launch_step(Ctx &c, int step, double dt);
+
+}  // namespace thermo

@@ -1,0 +1,637 @@
+// iface.cu -- per-step re-integration of the interface terms on Gamma_R(t).
+//
+// K2a (k_pairs, twice: once per surface): one thread per surface triangle finds every
+// triangle of the other surface whose box overlaps (uniform bin grid, each pair visited
+// once), cuts the overlap polygon F cap (G + o) by Sutherland-Hodgman (F = rail-top
+// triangle, G = stock-bottom triangle, o = in-plane offset of the stock), fans it from
+// vertex 0 and integrates the products of the two P1 fields exactly with the P1 mass formula
+//   int_tau g h = |tau|/12 (sum_i g_i h_i + sum_i g_i sum_i h_i)
+// on every fan triangle tau; the result is one record per overlapping pair.
+// K2b (k_rows): one warp per interface node sums the records of its star into its row of
+// K~_G = -dt [[M_B,fix, C_B], [C_B^T, M_B,mov]] and its friction source
+// eta/2 int phi, and refreshes its Jacobi diagonal.
+// Every sum runs in a fixed order, so results are deterministic; no floating-point atomics.
+//
+// Host part (iface_setup): plane and in-plane basis, interface node numbering, stars, bin
+// grids, and the per-row capacity of the interface rows (swept over the motion range).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "ctx.h"
+
+namespace thermo {
+
+#define CK(x)                                                                    \
+    do {                                                                         \
+        cudaError_t e_ = (x);                                                    \
+        if (e_ != cudaSuccess) {                                                 \
+            c.err = std::string("CUDA: ") + cudaGetErrorString(e_) + " at " #x; \
+            return -3;                                                           \
+        }                                                                        \
+    } while (0)
+
+#define IF_MAXV 12   // polygon vertices (triangle clipped by 3 half-planes: <= 6, + slack)
+
+__device__ __forceinline__ double cross2(double ax, double ay, double bx, double by) {
+    return ax * by - ay * bx;
+}
+
+// Clip triangle F (counter-clockwise) by the counter-clockwise triangle G; inclusive
+// inside test.  Returns the vertex count of F cap G.
+__device__ int clip_tri(const double2 F[3], const double2 G[3], double2 *out) {
+    double2 a[IF_MAXV], b[IF_MAXV];
+    int n = 3;
+    a[0] = F[0]; a[1] = F[1]; a[2] = F[2];
+    double2 *cur = a, *nxt = b;
+    for (int e = 0; e < 3; ++e) {
+        double2 c1 = G[e], c2 = G[e == 2 ? 0 : e + 1];
+        double ex = c2.x - c1.x, ey = c2.y - c1.y;
+        int m = 0;
+        double2 prev = cur[n - 1];
+        double dprev = cross2(ex, ey, prev.x - c1.x, prev.y - c1.y);
+        for (int k = 0; k < n; ++k) {
+            double2 p = cur[k];
+            double dp = cross2(ex, ey, p.x - c1.x, p.y - c1.y);
+            if (dp >= 0.0) {
+                if (dprev < 0.0 && m < IF_MAXV) {
+                    double t = dprev / (dprev - dp);
+                    nxt[m++] = make_double2(prev.x + t * (p.x - prev.x), prev.y + t * (p.y - prev.y));
+                }
+                if (m < IF_MAXV) nxt[m++] = p;
+            } else if (dprev >= 0.0 && m < IF_MAXV) {
+                double t = dprev / (dprev - dp);
+                nxt[m++] = make_double2(prev.x + t * (p.x - prev.x), prev.y + t * (p.y - prev.y));
+            }
+            prev = p;
+            dprev = dp;
+        }
+        double2 *tmp = cur; cur = nxt; nxt = tmp;
+        n = m;
+        if (n == 0) break;
+    }
+    for (int k = 0; k < n; ++k) out[k] = cur[k];
+    return n;
+}
+
+__device__ __forceinline__ void bary(const double2 T[3], double2 y, double l[3]) {
+    double D = cross2(T[1].x - T[0].x, T[1].y - T[0].y, T[2].x - T[0].x, T[2].y - T[0].y);
+    double inv = 1.0 / D;
+    l[1] = cross2(y.x - T[0].x, y.y - T[0].y, T[2].x - T[0].x, T[2].y - T[0].y) * inv;
+    l[2] = cross2(T[1].x - T[0].x, T[1].y - T[0].y, y.x - T[0].x, y.y - T[0].y) * inv;
+    l[0] = 1.0 - l[1] - l[2];
+}
+
+__device__ __forceinline__ int bin_coord(double v, double v0, double inv_h, int n) {
+    int b = (int)floor((v - v0) * inv_h);
+    return b < 0 ? 0 : (b >= n ? n - 1 : b);
+}
+
+// ------------------------------------------------------------------------------ K2a: pairs
+
+// Integrals over one overlap polygon F cap (G + o) (both triangles given in the fixed frame),
+// seen from side `ownIsF`: own[] = int phi_own_a phi_own_b (symmetric, 00 01 02 11 12 22),
+// cross[a*3+b] = int phi_own_a phi_other_b, b[a] = int phi_own_a.  The polygon is always F
+// clipped by G and every product is formed in the same order from both sides, so the F-side
+// and G-side records of a pair hold bitwise-transposed cross blocks.
+__device__ bool pair_integrals(const double2 F[3], const double2 G[3], bool ownIsF, PairRec &r) {
+    double2 poly[IF_MAXV];
+    const int nv = clip_tri(F, G, poly);
+    if (nv < 3) return false;
+    double lf[IF_MAXV][3], lg[IF_MAXV][3];
+    for (int v = 0; v < nv; ++v) {
+        bary(F, poly[v], lf[v]);
+        bary(G, poly[v], lg[v]);
+    }
+    double(*own)[3] = ownIsF ? lf : lg;
+    double(*oth)[3] = ownIsF ? lg : lf;
+    for (int q = 0; q < 6; ++q) r.own[q] = 0.0;
+    for (int q = 0; q < 9; ++q) r.cross[q] = 0.0;
+    for (int q = 0; q < 3; ++q) r.b[q] = 0.0;
+    double area = 0.0;
+    for (int f = 1; f + 1 < nv; ++f) {
+        const int i0 = 0, i1 = f, i2 = f + 1;
+        const double ar = 0.5 * cross2(poly[i1].x - poly[i0].x, poly[i1].y - poly[i0].y,
+                                       poly[i2].x - poly[i0].x, poly[i2].y - poly[i0].y);
+        if (!(ar > 0.0)) continue;
+        area += ar;
+        const double w12 = ar * (1.0 / 12.0), w3 = ar * (1.0 / 3.0);
+        double so[3], st[3];
+        for (int a = 0; a < 3; ++a) {
+            so[a] = own[i0][a] + own[i1][a] + own[i2][a];
+            st[a] = oth[i0][a] + oth[i1][a] + oth[i2][a];
+        }
+        int q = 0;
+        for (int a = 0; a < 3; ++a) {
+            r.b[a] += w3 * so[a];
+            for (int b = a; b < 3; ++b, ++q)
+                r.own[q] += w12 * (own[i0][a] * own[i0][b] + own[i1][a] * own[i1][b] + own[i2][a] * own[i2][b] + so[a] * so[b]);
+            for (int b = 0; b < 3; ++b)
+                r.cross[a * 3 + b] += w12 * (own[i0][a] * oth[i0][b] + own[i1][a] * oth[i1][b] + own[i2][a] * oth[i2][b] + so[a] * st[b]);
+        }
+    }
+    return area > 0.0;
+}
+
+// Thread per (own triangle t of side `side`, scenario s): every overlapping pair with the
+// other surface, in a fixed order (bins row-major, ascending ids, each pair once).
+__global__ void __launch_bounds__(128) k_pairs(IfaceParams P, int side) {
+    const int nT = side == 0 ? P.nTA : P.nTB;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int s = blockIdx.y;
+    if (t >= nT) return;
+    const double ox = P.step_sc[4 * s + 0], oy = P.step_sc[4 * s + 1];
+    const int4 T = (side == 0 ? P.triA : P.triB)[t];
+    const int4 *oth_tri = side == 0 ? P.triB : P.triA;
+    const double4 *oth_box = side == 0 ? P.boxB : P.boxA;
+    const BinGrid &G = side == 0 ? P.binB : P.binA;
+    const double sx_own = side == 0 ? 0.0 : ox, sy_own = side == 0 ? 0.0 : oy;
+    const double sx_oth = side == 0 ? ox : 0.0, sy_oth = side == 0 ? oy : 0.0;
+    const int tv[3] = {T.x, T.y, T.z};
+    double2 Tp[3];
+    double lox = 1e300, loy = 1e300, hix = -1e300, hiy = -1e300;
+    for (int v = 0; v < 3; ++v) {
+        const double2 u = P.uv[tv[v]];
+        Tp[v] = make_double2(u.x + sx_own, u.y + sy_own);
+        lox = fmin(lox, Tp[v].x); hix = fmax(hix, Tp[v].x);
+        loy = fmin(loy, Tp[v].y); hiy = fmax(hiy, Tp[v].y);
+    }
+    const double qlx = lox - sx_oth, qhx = hix - sx_oth, qly = loy - sy_oth, qhy = hiy - sy_oth;
+    const int bx0 = bin_coord(qlx, G.x0, G.inv_h, G.nx), bx1 = bin_coord(qhx, G.x0, G.inv_h, G.nx);
+    const int by0 = bin_coord(qly, G.y0, G.inv_h, G.ny), by1 = bin_coord(qhy, G.y0, G.inv_h, G.ny);
+    PairRec *out = P.pairs + ((int64_t)(side == 0 ? 0 : P.nTA * (int64_t)P.S) + (int64_t)s * nT + t) * P.pcap;
+    int j = 0;
+    bool ok = true;
+    for (int by = by0; by <= by1; ++by)
+        for (int bx = bx0; bx <= bx1; ++bx) {
+            const int bin = by * G.nx + bx;
+            for (int m = G.ptr[bin]; m < G.ptr[bin + 1]; ++m) {
+                const int u = G.ids[m];
+                const double4 ub = oth_box[u];
+                if (ub.x > qhx || ub.z < qlx || ub.y > qhy || ub.w < qly) continue;
+                if (bin_coord(fmax(qlx, ub.x), G.x0, G.inv_h, G.nx) != bx ||
+                    bin_coord(fmax(qly, ub.y), G.y0, G.inv_h, G.ny) != by) continue;
+                const int4 W = oth_tri[u];
+                const int wv[3] = {W.x, W.y, W.z};
+                double2 Up[3];
+                for (int v = 0; v < 3; ++v) {
+                    const double2 q = P.uv[wv[v]];
+                    Up[v] = make_double2(q.x + sx_oth, q.y + sy_oth);
+                }
+                PairRec r;
+                const bool hit = side == 0 ? pair_integrals(Tp, Up, true, r) : pair_integrals(Up, Tp, false, r);
+                if (!hit) continue;
+                if (j == P.pcap) { ok = false; continue; }
+                r.other = u;
+                out[j++] = r;
+            }
+        }
+    if (!ok) atomicOr(&P.status[1], 1);
+    P.pcnt[(side == 0 ? 0 : P.nTA * (int64_t)P.S) + (int64_t)s * nT + t] = j;
+}
+
+// ------------------------------------------------------------------------------ K2b: rows
+
+// Warp per (interface node k, scenario s): sum the pair records of the node's star into its
+// ELL row of K~_G in a fixed order (star triangles ascending, pairs in record order, the six
+// contributions of a record in order own b=0..2, other b=0..2).  Shared-memory row buffer,
+// warp-ballot search for the column.
+__global__ void __launch_bounds__(128) k_rows(IfaceParams P) {
+    extern __shared__ unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int k = blockIdx.x * 4 + wib;
+    const int s = blockIdx.y;
+    double *vals = reinterpret_cast<double *>(smem_raw) + (size_t)wib * P.cap;
+    int *cols = reinterpret_cast<int *>(reinterpret_cast<double *>(smem_raw) + 4 * (size_t)P.cap) + (size_t)wib * P.cap;
+    if (k >= P.n_if) return;
+    const bool sideA = k < P.nA;
+    const int nT = sideA ? P.nTA : P.nTB;
+    const int64_t base_rec = sideA ? 0 : (int64_t)P.nTA * P.S;
+    const int4 *own_tri = sideA ? P.triA : P.triB;
+    const int4 *oth_tri = sideA ? P.triB : P.triA;
+    const int32_t row = P.if_rows[k];
+    const double scale = P.dt * P.alpha;
+    int count = 0;
+    bool ok = true;
+    double phi = 0.0;
+    for (int st = P.star_ptr[k]; st < P.star_ptr[k + 1]; ++st) {
+        const int t = P.star_tri[st];
+        const int4 T = own_tri[t];
+        const int a = (T.x == k) ? 0 : ((T.y == k) ? 1 : 2);
+        const int64_t rid = base_rec + (int64_t)s * nT + t;
+        const int np = P.pcnt[rid];
+        const PairRec *rec = P.pairs + rid * P.pcap;
+        // own-row index pattern into the symmetric 3x3 (00 01 02 11 12 22)
+        const int sym[3][3] = {{0, 1, 2}, {1, 3, 4}, {2, 4, 5}};
+        for (int j = 0; j < np; ++j) {
+            const PairRec &r = rec[j];
+            int col = 0;
+            double v = 0.0;
+            if (lane < 3) {
+                const int tv = lane == 0 ? T.x : (lane == 1 ? T.y : T.z);
+                col = P.if_rows[tv];
+                v = scale * r.own[sym[a][lane]];          // -dt * (-alpha int phi phi)
+            } else if (lane < 6) {
+                const int4 W = oth_tri[r.other];
+                const int wv = lane == 3 ? W.x : (lane == 4 ? W.y : W.z);
+                col = P.if_rows[wv];
+                v = -scale * r.cross[a * 3 + (lane - 3)];  // -dt * (+alpha int phi phi)
+            }
+            phi += r.b[a];
+            for (int q = 0; q < 6; ++q) {
+                const int cq = __shfl_sync(0xffffffffu, col, q);
+                const double vq = __shfl_sync(0xffffffffu, v, q);
+                int idx = -1;
+                for (int c = lane; c < count; c += 32)
+                    if (cols[c] == cq) idx = c;
+                const unsigned m = __ballot_sync(0xffffffffu, idx >= 0);
+                if (m) {
+                    if (lane == __ffs(m) - 1) vals[idx] += vq;
+                } else if (count < P.cap) {
+                    if (lane == 0) { cols[count] = cq; vals[count] = vq; }
+                    ++count;
+                } else {
+                    ok = false;
+                }
+                __syncwarp();
+            }
+        }
+    }
+    double dself = 0.0;
+    for (int c = 0; c < count; ++c)
+        if (cols[c] == row) dself += vals[c];
+    for (int c = lane; c < count; c += 32) {
+        const int64_t e = ((int64_t)s * P.cap + c) * P.n_if + k;
+        P.ell_col[e] = cols[c];
+        P.ell_val[e] = vals[c];
+    }
+    if (lane == 0) {
+        if (!ok) atomicOr(&P.status[1], 1);
+        P.ell_cnt[(int64_t)s * P.n_if + k] = count;
+        P.if_phi[(int64_t)s * P.n_if + k] = phi;
+        P.if_b[(int64_t)s * P.n_if + k] = 0.5 * P.step_sc[4 * s + 2] * phi;
+        const double dinv = 1.0 / (P.Dvol[row] + dself);
+        if (P.S == 1) P.Dinv[row] = dinv;
+        else P.if_dinv[(int64_t)s * P.n_if + k] = dinv;
+    }
+}
+
+// Conservative count of overlapping-candidate triangles of the other surface for each
+// triangle of `side` at offset o (boxes padded by pad).
+__global__ void k_tri_count(IfaceParams P, int side, const double2 *offs, double pad, int *maxcnt) {
+    const int nT = side == 0 ? P.nTA : P.nTB;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nT) return;
+    const double2 o = offs[blockIdx.y];
+    const double4 b = (side == 0 ? P.boxA : P.boxB)[t];
+    const double4 *oth_box = side == 0 ? P.boxB : P.boxA;
+    const BinGrid &G = side == 0 ? P.binB : P.binA;
+    const double sx = side == 0 ? -o.x : o.x, sy = side == 0 ? -o.y : o.y;
+    const double lx = b.x + sx - pad, hx = b.z + sx + pad, ly = b.y + sy - pad, hy = b.w + sy + pad;
+    const int bx0 = bin_coord(lx, G.x0, G.inv_h, G.nx), bx1 = bin_coord(hx, G.x0, G.inv_h, G.nx);
+    const int by0 = bin_coord(ly, G.y0, G.inv_h, G.ny), by1 = bin_coord(hy, G.y0, G.inv_h, G.ny);
+    int n = 0;
+    for (int by = by0; by <= by1; ++by)
+        for (int bx = bx0; bx <= bx1; ++bx) {
+            const int bin = by * G.nx + bx;
+            for (int m = G.ptr[bin]; m < G.ptr[bin + 1]; ++m) {
+                const double4 ub = oth_box[G.ids[m]];
+                if (ub.x > hx || ub.z < lx || ub.y > hy || ub.w < ly) continue;
+                if (bin_coord(fmax(lx, ub.x), G.x0, G.inv_h, G.nx) != bx ||
+                    bin_coord(fmax(ly, ub.y), G.y0, G.inv_h, G.ny) != by) continue;
+                ++n;
+            }
+        }
+    atomicMax(maxcnt, n);
+}
+
+// Conservative count of the interface entries of row k for an offset o (expanded by pad):
+// distinct own-star nodes + distinct nodes of other-surface triangles whose box overlaps.
+__global__ void k_iface_count(IfaceParams P, const double2 *offs, double pad, int *maxcnt) {
+    int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= P.n_if) return;
+    const double2 o = offs[blockIdx.y];
+    const bool sideA = k < P.nA;
+    const int4 *own_tri = sideA ? P.triA : P.triB;
+    const int4 *oth_tri = sideA ? P.triB : P.triA;
+    const double4 *oth_box = sideA ? P.boxB : P.boxA;
+    const BinGrid &G = sideA ? P.binB : P.binA;
+    const double sx = sideA ? -o.x : o.x, sy = sideA ? -o.y : o.y;   // own frame -> other frame
+    int ids[512];
+    int n = 0;
+    bool over = false;
+    auto add = [&](int v) {
+        for (int q = 0; q < n; ++q) if (ids[q] == v) return;
+        if (n < 512) ids[n++] = v; else over = true;
+    };
+    for (int st = P.star_ptr[k]; st < P.star_ptr[k + 1]; ++st) {
+        const int4 t = own_tri[P.star_tri[st]];
+        add(t.x); add(t.y); add(t.z);
+        double lox = 1e300, loy = 1e300, hix = -1e300, hiy = -1e300;
+        const int tv[3] = {t.x, t.y, t.z};
+        for (int v = 0; v < 3; ++v) {
+            double2 u = P.uv[tv[v]];
+            lox = fmin(lox, u.x + sx); hix = fmax(hix, u.x + sx);
+            loy = fmin(loy, u.y + sy); hiy = fmax(hiy, u.y + sy);
+        }
+        lox -= pad; loy -= pad; hix += pad; hiy += pad;
+        const int bx0 = bin_coord(lox, G.x0, G.inv_h, G.nx), bx1 = bin_coord(hix, G.x0, G.inv_h, G.nx);
+        const int by0 = bin_coord(loy, G.y0, G.inv_h, G.ny), by1 = bin_coord(hiy, G.y0, G.inv_h, G.ny);
+        for (int by = by0; by <= by1; ++by)
+            for (int bx = bx0; bx <= bx1; ++bx) {
+                const int bin = by * G.nx + bx;
+                for (int m = G.ptr[bin]; m < G.ptr[bin + 1]; ++m) {
+                    const double4 ub = oth_box[G.ids[m]];
+                    if (ub.x > hix || ub.z < lox || ub.y > hiy || ub.w < loy) continue;
+                    const int4 w = oth_tri[G.ids[m]];
+                    add(w.x); add(w.y); add(w.z);
+                }
+            }
+    }
+    atomicMax(maxcnt, over ? (1 << 30) : n);
+}
+
+// ------------------------------------------------------------------------------ host
+
+static void make_bins(const std::vector<double4> &box, std::vector<int32_t> &ptr, std::vector<int32_t> &ids,
+                      BinGrid &g) {
+    double lx = 1e300, ly = 1e300, hx = -1e300, hy = -1e300, area = 0.0;
+    for (auto &b : box) {
+        lx = std::min(lx, b.x); ly = std::min(ly, b.y);
+        hx = std::max(hx, b.z); hy = std::max(hy, b.w);
+        area += (b.z - b.x) * (b.w - b.y);
+    }
+    int nt = (int)box.size();
+    double h = nt ? std::sqrt(std::max(area, 1e-300) / nt) : 1.0;
+    if (!(h > 0)) h = 1.0;
+    int nx = std::max(1, std::min(4096, (int)std::ceil((hx - lx) / h)));
+    int ny = std::max(1, std::min(4096, (int)std::ceil((hy - ly) / h)));
+    h = std::max((hx - lx) / nx, (hy - ly) / ny);
+    if (!(h > 0)) h = 1.0;
+    g.x0 = nt ? lx : 0.0;
+    g.y0 = nt ? ly : 0.0;
+    g.inv_h = 1.0 / h;
+    g.nx = nx;
+    g.ny = ny;
+    auto bc = [&](double v, double v0, int n) {
+        int b = (int)std::floor((v - v0) * g.inv_h);
+        return b < 0 ? 0 : (b >= n ? n - 1 : b);
+    };
+    std::vector<int32_t> cnt((size_t)nx * ny + 1, 0);
+    for (int t = 0; t < nt; ++t)
+        for (int by = bc(box[t].y, g.y0, ny); by <= bc(box[t].w, g.y0, ny); ++by)
+            for (int bx = bc(box[t].x, g.x0, nx); bx <= bc(box[t].z, g.x0, nx); ++bx) cnt[by * nx + bx + 1]++;
+    for (size_t i = 1; i < cnt.size(); ++i) cnt[i] += cnt[i - 1];
+    ptr = cnt;
+    ids.assign(cnt.back() + 1, 0);
+    std::vector<int32_t> pos(cnt.begin(), cnt.end() - 1);
+    for (int t = 0; t < nt; ++t)   // ascending t -> ascending ids within each bin
+        for (int by = bc(box[t].y, g.y0, ny); by <= bc(box[t].w, g.y0, ny); ++by)
+            for (int bx = bc(box[t].x, g.x0, nx); bx <= bc(box[t].z, g.x0, nx); ++bx) ids[pos[by * nx + bx]++] = t;
+}
+
+template <class T>
+static int upload(Ctx &c, T **d, const std::vector<T> &h) {
+    CK(cudaMalloc(d, sizeof(T) * (h.size() + 1)));
+    if (!h.empty()) CK(cudaMemcpyAsync(*d, h.data(), sizeof(T) * h.size(), cudaMemcpyHostToDevice, c.stream));
+    return 0;
+}
+
+int iface_setup(Ctx &c, const double *X, const std::vector<int32_t> &fA, const std::vector<int32_t> &fB) {
+    const int nTA = (int)(fA.size() / 3), nTB = (int)(fB.size() / 3);
+    c.nTA = nTA;
+    c.nTB = nTB;
+    // slice -> interface-row range map (needed even without an interface)
+    std::vector<int32_t> rows;
+    {
+        std::vector<int32_t> ra(fA), rb(fB);
+        std::sort(ra.begin(), ra.end());
+        ra.erase(std::unique(ra.begin(), ra.end()), ra.end());
+        std::sort(rb.begin(), rb.end());
+        rb.erase(std::unique(rb.begin(), rb.end()), rb.end());
+        for (int32_t r : ra) if (r >= c.nf) { c.err = "interface face of part 0 references a part-1 node"; return -1; }
+        for (int32_t r : rb) if (r < c.nf) { c.err = "interface face of part 1 references a part-0 node"; return -1; }
+        c.nA = (int)ra.size();
+        rows = ra;
+        rows.insert(rows.end(), rb.begin(), rb.end());
+    }
+    c.n_if = (int)rows.size();
+    std::vector<int32_t> slice_if(c.nslices + 1);
+    for (int64_t s = 0; s <= c.nslices; ++s)
+        slice_if[s] = (int32_t)(std::lower_bound(rows.begin(), rows.end(), (int32_t)std::min<int64_t>(32 * s, INT32_MAX)) - rows.begin());
+    if (int rc = upload(c, &c.d_slice_if, slice_if)) return rc;
+    if (c.n_if == 0) return 0;
+    if (nTA == 0 || nTB == 0) { c.err = "interface tag present on only one part"; return -1; }
+
+    // plane of the first rail-top face, in-plane orthonormal basis (e1, e2)
+    const double *p0 = X + 3 * (int64_t)fA[0], *p1 = X + 3 * (int64_t)fA[1], *p2 = X + 3 * (int64_t)fA[2];
+    double u[3], w[3], n[3];
+    for (int d = 0; d < 3; ++d) { u[d] = p1[d] - p0[d]; w[d] = p2[d] - p0[d]; }
+    n[0] = u[1] * w[2] - u[2] * w[1];
+    n[1] = u[2] * w[0] - u[0] * w[2];
+    n[2] = u[0] * w[1] - u[1] * w[0];
+    double ln = std::sqrt(n[0] * n[0] + n[1] * n[1] + n[2] * n[2]);
+    if (!(ln > 0)) { c.err = "degenerate interface face"; return -1; }
+    for (int d = 0; d < 3; ++d) n[d] /= ln;
+    int ax = 0;
+    for (int d = 1; d < 3; ++d) if (std::fabs(n[d]) < std::fabs(n[ax])) ax = d;
+    double e1[3] = {0, 0, 0};
+    e1[ax] = 1.0;
+    double dn = e1[0] * n[0] + e1[1] * n[1] + e1[2] * n[2];
+    for (int d = 0; d < 3; ++d) e1[d] -= dn * n[d];
+    double l1 = std::sqrt(e1[0] * e1[0] + e1[1] * e1[1] + e1[2] * e1[2]);
+    for (int d = 0; d < 3; ++d) e1[d] /= l1;
+    double e2[3] = {n[1] * e1[2] - n[2] * e1[1], n[2] * e1[0] - n[0] * e1[2], n[0] * e1[1] - n[1] * e1[0]};
+    memcpy(c.plane_n, n, sizeof n);
+    memcpy(c.e1, e1, sizeof e1);
+    memcpy(c.e2, e2, sizeof e2);
+
+    // interface nodes: coordinates, coplanarity
+    std::vector<int32_t> kmap;   // global row -> k, via binary search on `rows`
+    auto kof = [&](int32_t r) { return (int32_t)(std::lower_bound(rows.begin(), rows.end(), r) - rows.begin()); };
+    std::vector<double2> uv(c.n_if);
+    double diam = 0.0;
+    for (int k = 0; k < c.n_if; ++k) {
+        const double *x = X + 3 * (int64_t)rows[k];
+        double d[3] = {x[0] - p0[0], x[1] - p0[1], x[2] - p0[2]};
+        uv[k] = make_double2(d[0] * e1[0] + d[1] * e1[1] + d[2] * e1[2], d[0] * e2[0] + d[1] * e2[1] + d[2] * e2[2]);
+        diam = std::max(diam, std::fabs(uv[k].x) + std::fabs(uv[k].y));
+    }
+    for (int k = 0; k < c.n_if; ++k) {
+        const double *x = X + 3 * (int64_t)rows[k];
+        double dist = (x[0] - p0[0]) * n[0] + (x[1] - p0[1]) * n[1] + (x[2] - p0[2]) * n[2];
+        if (std::fabs(dist) > 1e-9 * std::max(1.0, diam)) { c.err = "interface faces are not coplanar"; return -1; }
+    }
+    // triangles (counter-clockwise in (e1, e2)), boxes, stars, min edge
+    auto mk = [&](const std::vector<int32_t> &f, int nt, std::vector<int4> &tri, std::vector<double4> &box) -> int {
+        tri.resize(nt);
+        box.resize(nt);
+        for (int t = 0; t < nt; ++t) {
+            int k0 = kof(f[3 * t]), k1 = kof(f[3 * t + 1]), k2 = kof(f[3 * t + 2]);
+            double ar = (uv[k1].x - uv[k0].x) * (uv[k2].y - uv[k0].y) - (uv[k1].y - uv[k0].y) * (uv[k2].x - uv[k0].x);
+            if (ar == 0.0) { c.err = "degenerate interface triangle"; return -1; }
+            if (ar < 0) std::swap(k1, k2);
+            tri[t] = make_int4(k0, k1, k2, 0);
+            int kk[3] = {k0, k1, k2};
+            double4 b = make_double4(1e300, 1e300, -1e300, -1e300);
+            for (int v = 0; v < 3; ++v) {
+                b.x = std::min(b.x, uv[kk[v]].x); b.y = std::min(b.y, uv[kk[v]].y);
+                b.z = std::max(b.z, uv[kk[v]].x); b.w = std::max(b.w, uv[kk[v]].y);
+                double2 q = uv[kk[(v + 1) % 3]];
+                double le = std::hypot(q.x - uv[kk[v]].x, q.y - uv[kk[v]].y);
+                if (c.min_edge == 0.0 || le < c.min_edge) c.min_edge = le;
+            }
+            box[t] = b;
+        }
+        return 0;
+    };
+    std::vector<int4> triA, triB;
+    std::vector<double4> boxA, boxB;
+    if (mk(fA, nTA, triA, boxA) || mk(fB, nTB, triB, boxB)) return -1;
+    std::vector<int32_t> sptr(c.n_if + 1, 0), stri;
+    for (auto &t : triA) { sptr[t.x + 1]++; sptr[t.y + 1]++; sptr[t.z + 1]++; }
+    for (auto &t : triB) { sptr[t.x + 1]++; sptr[t.y + 1]++; sptr[t.z + 1]++; }
+    for (int k = 0; k < c.n_if; ++k) sptr[k + 1] += sptr[k];
+    stri.assign(sptr[c.n_if] + 1, 0);
+    {
+        std::vector<int32_t> pos(sptr.begin(), sptr.end() - 1);
+        for (int t = 0; t < nTA; ++t) { stri[pos[triA[t].x]++] = t; stri[pos[triA[t].y]++] = t; stri[pos[triA[t].z]++] = t; }
+        for (int t = 0; t < nTB; ++t) { stri[pos[triB[t].x]++] = t; stri[pos[triB[t].y]++] = t; stri[pos[triB[t].z]++] = t; }
+    }
+    std::vector<int32_t> bAp, bAi, bBp, bBi;
+    make_bins(boxA, bAp, bAi, c.binA);
+    make_bins(boxB, bBp, bBi, c.binB);
+    if (upload(c, &c.d_if_rows, rows) || upload(c, &c.d_uv, uv) || upload(c, &c.d_star_ptr, sptr) ||
+        upload(c, &c.d_star_tri, stri) || upload(c, &c.d_triA, triA) || upload(c, &c.d_triB, triB) ||
+        upload(c, &c.d_boxA, boxA) || upload(c, &c.d_boxB, boxB) || upload(c, &c.d_binA_ptr, bAp) ||
+        upload(c, &c.d_binA_ids, bAi) || upload(c, &c.d_binB_ptr, bBp) || upload(c, &c.d_binB_ids, bBi))
+        return -3;
+    c.binA.ptr = c.d_binA_ptr; c.binA.ids = c.d_binA_ids;
+    c.binB.ptr = c.d_binB_ptr; c.binB.ids = c.d_binB_ids;
+
+    // in-plane motion of every scenario; the offset must stay in the plane
+    for (auto &sc : c.scen) {
+        double dnn = sc.dir[0] * n[0] + sc.dir[1] * n[1] + sc.dir[2] * n[2];
+        double dl = std::fabs(sc.dir[0]) + std::fabs(sc.dir[1]) + std::fabs(sc.dir[2]);
+        if (std::fabs(dnn) > 1e-12 * std::max(1.0, dl)) { c.err = "motion direction leaves the interface plane"; return -1; }
+        sc.d2[0] = sc.dir[0] * e1[0] + sc.dir[1] * e1[1] + sc.dir[2] * e1[2];
+        sc.d2[1] = sc.dir[0] * e2[0] + sc.dir[1] * e2[1] + sc.dir[2] * e2[2];
+    }
+
+    // capacity: sweep every scenario's motion range [s0 - |amp|, s0 + |amp|] in steps of
+    // min_edge / 2 with boxes padded by the step (conservative superset at any offset)
+    const double step = 0.5 * c.min_edge;
+    std::vector<double2> offs;
+    for (auto &sc : c.scen) {
+        double lo = sc.s0 - std::fabs(sc.amp), hi = sc.s0 + std::fabs(sc.amp);
+        int64_t ns = std::min<int64_t>(200000, (int64_t)std::ceil((hi - lo) / step) + 1);
+        for (int64_t i = 0; i < ns; ++i) {
+            double s = ns == 1 ? lo : lo + (hi - lo) * (double)i / (double)(ns - 1);
+            double2 o = make_double2(s * sc.d2[0], s * sc.d2[1]);
+            bool dup = false;
+            for (size_t q = offs.size() > 64 ? offs.size() - 64 : 0; q < offs.size(); ++q)
+                if (offs[q].x == o.x && offs[q].y == o.y) { dup = true; break; }
+            if (!dup) offs.push_back(o);
+        }
+    }
+    if (offs.size() > 400000) offs.resize(400000);
+    double2 *d_offs = nullptr;
+    int *d_max = nullptr;
+    if (upload(c, &d_offs, offs)) return -3;
+    CK(cudaMalloc(&d_max, sizeof(int)));
+    CK(cudaMemsetAsync(d_max, 0, sizeof(int), c.stream));
+    IfaceParams P;
+    memset(&P, 0, sizeof P);
+    iface_params(c, P, nullptr, 0.0);
+    for (size_t b0 = 0; b0 < offs.size(); b0 += 60000) {
+        unsigned ny = (unsigned)std::min<size_t>(60000, offs.size() - b0);
+        dim3 grid((unsigned)((c.n_if + 127) / 128), ny);
+        k_iface_count<<<grid, 128, 0, c.stream>>>(P, d_offs + b0, step, d_max);
+        CK(cudaGetLastError());
+    }
+    int *d_pmax = nullptr;
+    CK(cudaMalloc(&d_pmax, sizeof(int)));
+    CK(cudaMemsetAsync(d_pmax, 0, sizeof(int), c.stream));
+    for (int side = 0; side < 2; ++side) {
+        const int nT = side == 0 ? c.nTA : c.nTB;
+        for (size_t b0 = 0; b0 < offs.size(); b0 += 60000) {
+            unsigned ny = (unsigned)std::min<size_t>(60000, offs.size() - b0);
+            dim3 grid((unsigned)((nT + 127) / 128), ny);
+            k_tri_count<<<grid, 128, 0, c.stream>>>(P, side, d_offs + b0, step, d_pmax);
+            CK(cudaGetLastError());
+        }
+    }
+    int mx = 0, pmx = 0;
+    CK(cudaMemcpyAsync(&pmx, d_pmax, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaMemcpyAsync(&mx, d_max, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    cudaFree(d_offs);
+    cudaFree(d_max);
+    cudaFree(d_pmax);
+    if (mx > 2048) { c.err = "interface rows too dense (capacity > 2048)"; return -5; }
+    c.cap = ((mx + 4) + 3) / 4 * 4;
+    c.pcap = pmx + 2;
+    CK(cudaMalloc(&c.d_pairs, sizeof(PairRec) * (size_t)c.S * (c.nTA + c.nTB) * c.pcap));
+    CK(cudaMalloc(&c.d_pcnt, sizeof(int32_t) * (size_t)c.S * (c.nTA + c.nTB)));
+
+    const int64_t S = c.S, nif = c.n_if;
+    CK(cudaMalloc(&c.d_ell_cnt, sizeof(int32_t) * S * nif));
+    CK(cudaMalloc(&c.d_ell_col, sizeof(int32_t) * S * c.cap * nif));
+    CK(cudaMalloc(&c.d_ell_val, sizeof(double) * S * c.cap * nif));
+    CK(cudaMalloc(&c.d_if_b, sizeof(double) * S * nif));
+    CK(cudaMalloc(&c.d_if_phi, sizeof(double) * S * nif));
+    CK(cudaMalloc(&c.d_if_dinv, sizeof(double) * S * nif));
+    CK(cudaMemsetAsync(c.d_ell_cnt, 0, sizeof(int32_t) * S * nif, c.stream));
+    CK(cudaMemsetAsync(c.d_if_b, 0, sizeof(double) * S * nif, c.stream));
+    CK(cudaMemsetAsync(c.d_if_phi, 0, sizeof(double) * S * nif, c.stream));
+    return 0;
+}
+
+void iface_params(Ctx &c, IfaceParams &P, const double *step_sc, double dt) {
+    P.nTA = c.nTA;
+    P.nTB = c.nTB;
+    P.pcap = c.pcap;
+    P.pairs = c.d_pairs;
+    P.pcnt = c.d_pcnt;
+    P.n_if = c.n_if;
+    P.nA = c.nA;
+    P.S = c.S;
+    P.cap = c.cap;
+    P.if_rows = c.d_if_rows;
+    P.uv = c.d_uv;
+    P.star_ptr = c.d_star_ptr;
+    P.star_tri = c.d_star_tri;
+    P.triA = c.d_triA;
+    P.triB = c.d_triB;
+    P.boxA = c.d_boxA;
+    P.boxB = c.d_boxB;
+    P.binA = c.binA;
+    P.binB = c.binB;
+    P.alpha = c.alpha;
+    P.dt = dt;
+    P.step_sc = step_sc;
+    P.Dvol = c.d_Dvol;
+    P.ell_cnt = c.d_ell_cnt;
+    P.ell_col = c.d_ell_col;
+    P.ell_val = c.d_ell_val;
+    P.if_b = c.d_if_b;
+    P.if_phi = c.d_if_phi;
+    P.Dinv = c.d_Dinv;
+    P.if_dinv = c.d_if_dinv;
+    P.status = c.d_status;
+}
+
+int iface_launch(Ctx &c, const IfaceParams &P) {
+    if (c.n_if == 0) return 0;
+    k_pairs<<<dim3((unsigned)((c.nTA + 127) / 128), (unsigned)c.S), 128, 0, c.stream>>>(P, 0);
+    CK(cudaGetLastError());
+    k_pairs<<<dim3((unsigned)((c.nTB + 127) / 128), (unsigned)c.S), 128, 0, c.stream>>>(P, 1);
+    CK(cudaGetLastError());
+    const size_t smem = 4 * (size_t)c.cap * (sizeof(double) + sizeof(int));
+    if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_rows<<<dim3((unsigned)((c.n_if + 3) / 4), (unsigned)c.S), 128, smem, c.stream>>>(P);
+    CK(cudaGetLastError());
+    return 0;
+}
+
+}  // namespace thermo

@@ -1,0 +1,425 @@
+// thermo.cu -- C ABI of the thermo library (include/thermo.h).
+//
+// Host control only: argument checks, allocation, the per-step time scalars
+// t' = t + (n+1) dt, s(t'), eta(t') (reading R3) and kernel launches.
+// Every arithmetic step of the hot path runs in the kernels of assemble.cu, iface.cu and
+// cg.cu.  No CPU fallback exists.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/thermo.h"
+#include "ctx.h"
+
+using thermo::Ctx;
+
+static thread_local std::string g_create_err;
+
+#define API_CK(x)                                                                \
+    do {                                                                         \
+        cudaError_t e_ = (x);                                                    \
+        if (e_ != cudaSuccess) {                                                 \
+            c->err = std::string("CUDA: ") + cudaGetErrorString(e_) + " at " #x; \
+            return THERMO_ECUDA;                                                 \
+        }                                                                        \
+    } while (0)
+
+static int fail(Ctx *c, int code, const std::string &msg) {
+    c->err = msg;
+    return code;
+}
+
+static void free_ctx(Ctx *c) {
+    if (!c) return;
+    void *ptrs[] = {c->d_xyz, c->d_tets, c->d_faces, c->d_fkey, c->d_tinc_ptr, c->d_tinc, c->d_finc_ptr,
+                    c->d_finc, c->d_slice_ptr, c->d_col, c->d_A, c->d_R, c->d_val, c->d_diagpos, c->d_ML,
+                    c->d_benv, c->d_Dvol, c->d_Dinv, c->d_robin_tab, c->d_if_rows, c->d_uv, c->d_star_ptr,
+                    c->d_star_tri, c->d_triA, c->d_triB, c->d_boxA, c->d_boxB, c->d_binA_ptr, c->d_binA_ids,
+                    c->d_binB_ptr, c->d_binB_ids, c->d_slice_if, c->d_ell_cnt, c->d_ell_col, c->d_ell_val,
+                    c->d_if_b, c->d_if_phi, c->d_if_dinv, c->d_T[0], c->d_T[1], c->d_z, c->d_p[0], c->d_p[1],
+                    c->d_q, c->d_partials, c->d_status, c->d_fail_relres, c->d_step_sc, c->d_iters,
+                    c->d_relres, c->d_area, c->d_pairs, c->d_pcnt};
+    for (void *p : ptrs)
+        if (p) cudaFree(p);
+    for (cudaEvent_t e : c->events) cudaEventDestroy(e);
+    delete c;
+}
+
+static bool mesh_ok(const thermo_mesh *m) {
+    return m && m->n_nodes > 0 && m->xyz && m->n_tets > 0 && m->tets && m->n_bfaces >= 0 &&
+           (m->n_bfaces == 0 || (m->bfaces && m->bface_tag)) && m->n_nodes < (1LL << 31) &&
+           m->n_tets < (1LL << 31);
+}
+
+__global__ void k_fill_value(double *p, int64_t n, double v) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+
+extern "C" int thermo_create_mesh(void **out, const thermo_mesh *fixed, const thermo_mesh *moving,
+                                  int32_t iface_tag_fixed, int32_t iface_tag_moving, double nu,
+                                  double rho_cp, double alpha_iface, int32_t n_scen,
+                                  const thermo_scenario *scen, double T_init, void *cuda_stream) {
+    if (!out) { g_create_err = "out is NULL"; return THERMO_EINVAL; }
+    *out = nullptr;
+    if (!mesh_ok(fixed) || !mesh_ok(moving)) { g_create_err = "invalid mesh arrays or sizes"; return THERMO_EINVAL; }
+    if (!(nu > 0) || !(rho_cp > 0) || !(alpha_iface >= 0) || n_scen < 1 || !scen || !std::isfinite(T_init)) {
+        g_create_err = "invalid material parameters or scenarios";
+        return THERMO_EINVAL;
+    }
+    Ctx *c = new (std::nothrow) Ctx();
+    if (!c) { g_create_err = "host allocation failed"; return THERMO_ENOMEM; }
+    try {
+        c->stream = (cudaStream_t)cuda_stream;
+        if (cudaGetDevice(&c->dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->dev) != cudaSuccess) {
+            g_create_err = "no CUDA device";
+            free_ctx(c);
+            return THERMO_ECUDA;
+        }
+        int coop = 0;
+        cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, c->dev);
+        if (!coop) { g_create_err = "device lacks cooperative launch"; free_ctx(c); return THERMO_ECUDA; }
+        c->nf = fixed->n_nodes;
+        c->nm = moving->n_nodes;
+        c->N = c->nf + c->nm;
+        if (c->N >= (1LL << 31)) { g_create_err = "too many nodes"; free_ctx(c); return THERMO_EINVAL; }
+        c->S = n_scen;
+        c->nu = nu;
+        c->rho_cp = rho_cp;
+        c->alpha = alpha_iface;
+        c->iface_tag_f = iface_tag_fixed;
+        c->iface_tag_m = iface_tag_moving;
+        for (int s = 0; s < n_scen; ++s) {
+            thermo::Scen q;
+            q.s0 = scen[s].s0; q.amp = scen[s].amp; q.period = scen[s].period;
+            for (int d = 0; d < 3; ++d) q.dir[d] = scen[s].dir[d];
+            q.eta0 = scen[s].eta0; q.eta_amp = scen[s].eta_amp; q.eta_period = scen[s].eta_period;
+            q.d2[0] = q.d2[1] = 0.0;
+            if (!(q.period != 0.0) || !(q.eta_period != 0.0) || !std::isfinite(q.s0) || !std::isfinite(q.amp)) {
+                g_create_err = "invalid scenario (zero period or non-finite values)";
+                free_ctx(c);
+                return THERMO_EINVAL;
+            }
+            c->scen.push_back(q);
+        }
+        // coupled host arrays: fixed part first
+        const int64_t N = c->N;
+        c->ntets = fixed->n_tets + moving->n_tets;
+        c->nfaces = fixed->n_bfaces + moving->n_bfaces;
+        std::vector<double> xyz(3 * N);
+        memcpy(xyz.data(), fixed->xyz, sizeof(double) * 3 * c->nf);
+        memcpy(xyz.data() + 3 * c->nf, moving->xyz, sizeof(double) * 3 * c->nm);
+        std::vector<int32_t> tets(4 * c->ntets);
+        for (int64_t e = 0; e < 4 * fixed->n_tets; ++e) {
+            if (fixed->tets[e] < 0 || fixed->tets[e] >= c->nf) { g_create_err = "fixed tet index out of range"; free_ctx(c); return THERMO_EINVAL; }
+            tets[e] = fixed->tets[e];
+        }
+        for (int64_t e = 0; e < 4 * moving->n_tets; ++e) {
+            if (moving->tets[e] < 0 || moving->tets[e] >= c->nm) { g_create_err = "moving tet index out of range"; free_ctx(c); return THERMO_EINVAL; }
+            tets[4 * fixed->n_tets + e] = (int32_t)(moving->tets[e] + c->nf);
+        }
+        std::vector<int32_t> faces(3 * c->nfaces), fkey(c->nfaces);
+        std::vector<int32_t> fA, fB;
+        for (int64_t f = 0; f < fixed->n_bfaces; ++f) {
+            for (int a = 0; a < 3; ++a) {
+                int32_t v = fixed->bfaces[3 * f + a];
+                if (v < 0 || v >= c->nf) { g_create_err = "fixed face index out of range"; free_ctx(c); return THERMO_EINVAL; }
+                faces[3 * f + a] = v;
+            }
+            fkey[f] = fixed->bface_tag[f];
+            if (fixed->bface_tag[f] == iface_tag_fixed) fA.insert(fA.end(), &faces[3 * f], &faces[3 * f] + 3);
+        }
+        for (int64_t f = 0; f < moving->n_bfaces; ++f) {
+            int64_t g = fixed->n_bfaces + f;
+            for (int a = 0; a < 3; ++a) {
+                int32_t v = moving->bfaces[3 * f + a];
+                if (v < 0 || v >= c->nm) { g_create_err = "moving face index out of range"; free_ctx(c); return THERMO_EINVAL; }
+                faces[3 * g + a] = (int32_t)(v + c->nf);
+            }
+            fkey[g] = 65536 + moving->bface_tag[f];
+            if (moving->bface_tag[f] == iface_tag_moving) fB.insert(fB.end(), &faces[3 * g], &faces[3 * g] + 3);
+        }
+        int rc = thermo::assemble_create(*c, xyz.data(), tets.data(), faces.data(), fkey.data());
+        if (!rc) rc = thermo::iface_setup(*c, xyz.data(), fA, fB);
+        if (rc) {
+            g_create_err = c->err;
+            free_ctx(c);
+            return rc == -1 ? THERMO_EINVAL : (rc == -5 ? THERMO_EGEOM : THERMO_ECUDA);
+        }
+        // state and workspace
+        const int64_t NS = N * c->S;
+        bool ok = true;
+        for (double **p : {&c->d_T[0], &c->d_T[1], &c->d_z, &c->d_p[0], &c->d_p[1], &c->d_q})
+            ok &= cudaMalloc(p, sizeof(double) * NS) == cudaSuccess;
+        ok &= cudaMalloc(&c->d_status, sizeof(int) * 8) == cudaSuccess;
+        ok &= cudaMalloc(&c->d_fail_relres, sizeof(double)) == cudaSuccess;
+        if (!ok) { g_create_err = "device allocation failed"; free_ctx(c); return THERMO_ENOMEM; }
+        k_fill_value<<<(unsigned)((NS + 255) / 256), 256, 0, c->stream>>>(c->d_T[0], NS, T_init);
+        cudaMemsetAsync(c->d_p[0], 0, sizeof(double) * NS, c->stream);
+        cudaMemsetAsync(c->d_p[1], 0, sizeof(double) * NS, c->stream);
+        cudaMemsetAsync(c->d_status, 0, sizeof(int) * 8, c->stream);
+        rc = thermo::assemble_robin(*c);
+        if (!rc) rc = thermo::cg_setup(*c);
+        if (!rc && cudaStreamSynchronize(c->stream) != cudaSuccess) { c->err = "CUDA error during create"; rc = -3; }
+        if (rc) { g_create_err = c->err; free_ctx(c); return THERMO_ECUDA; }
+        *out = c;
+        return THERMO_OK;
+    } catch (const std::exception &e) {
+        g_create_err = std::string("exception: ") + e.what();
+        free_ctx(c);
+        return THERMO_ENOMEM;
+    }
+}
+
+extern "C" int thermo_set_bc(void *ctx, int32_t part, int32_t tag, double alpha, double T_ref,
+                             const double grad_T[3]) {
+    Ctx *c = (Ctx *)ctx;
+    if (!c) return THERMO_EINVAL;
+    if (part != 0 && part != 1) return fail(c, THERMO_EINVAL, "part must be 0 or 1");
+    if (tag < 0 || tag >= 65536) return fail(c, THERMO_EINVAL, "tag out of range [0, 65536)");
+    if ((part == 0 && tag == c->iface_tag_f) || (part == 1 && tag == c->iface_tag_m))
+        return fail(c, THERMO_EINVAL, "interface faces cannot carry Robin data");
+    if (!(alpha >= 0) || !std::isfinite(T_ref)) return fail(c, THERMO_EINVAL, "invalid alpha or T_ref");
+    double g[3] = {0, 0, 0};
+    if (grad_T) for (int d = 0; d < 3; ++d) g[d] = grad_T[d];
+    if (part == 1) {
+        for (auto &s : c->scen) {
+            double gd = g[0] * s.dir[0] + g[1] * s.dir[1] + g[2] * s.dir[2];
+            double gn = std::fabs(g[0]) + std::fabs(g[1]) + std::fabs(g[2]);
+            if (std::fabs(gd) > 1e-12 * (gn + 1e-300) && gn > 0 && s.amp != 0.0)
+                return fail(c, THERMO_EINVAL, "moving-part T_a gradient must be orthogonal to the motion");
+        }
+    }
+    try {
+        bool found = false;
+        for (auto &r : c->robin)
+            if (r.part == part && r.tag == tag) {
+                r.alpha = alpha; r.T_ref = T_ref;
+                for (int d = 0; d < 3; ++d) r.g[d] = g[d];
+                found = true;
+            }
+        if (!found) {
+            thermo::Robin r{part, tag, alpha, T_ref, {g[0], g[1], g[2]}};
+            c->robin.push_back(r);
+        }
+        int rc = thermo::assemble_robin(*c);
+        return rc ? THERMO_ECUDA : THERMO_OK;
+    } catch (...) {
+        return fail(c, THERMO_ENOMEM, "host allocation failed");
+    }
+}
+
+extern "C" int thermo_set_solver(void *ctx, double rtol, int32_t maxit) {
+    Ctx *c = (Ctx *)ctx;
+    if (!c) return THERMO_EINVAL;
+    if (!(rtol > 0) || maxit < 0) return fail(c, THERMO_EINVAL, "rtol must be > 0 and maxit >= 0");
+    c->rtol = rtol;
+    c->maxit = maxit;
+    return THERMO_OK;
+}
+
+extern "C" int thermo_step(void *ctx, double t, double dt, int32_t nsteps) {
+    Ctx *c = (Ctx *)ctx;
+    if (!c) return THERMO_EINVAL;
+    if (!(dt > 0) || !std::isfinite(t) || nsteps < 0) return fail(c, THERMO_EINVAL, "dt must be > 0, nsteps >= 0");
+    if (nsteps == 0) return THERMO_OK;
+    try {
+        const int S = c->S;
+        if (c->built_dt != dt) {
+            if (thermo::build_operator(*c, dt)) return THERMO_ECUDA;
+        }
+        if ((int64_t)nsteps > c->step_cap) {
+            for (void *p : {(void *)c->d_step_sc, (void *)c->d_iters, (void *)c->d_relres, (void *)c->d_area})
+                if (p) cudaFree(p);
+            c->step_cap = nsteps;
+            API_CK(cudaMalloc(&c->d_step_sc, sizeof(double) * 4 * S * (size_t)nsteps));
+            API_CK(cudaMalloc(&c->d_iters, sizeof(int32_t) * S * (size_t)nsteps));
+            API_CK(cudaMalloc(&c->d_relres, sizeof(double) * S * (size_t)nsteps));
+            API_CK(cudaMalloc(&c->d_area, sizeof(double) * (size_t)nsteps));
+        }
+        // time scalars, fully implicit: everything at t' = t + (n+1) dt (reading R3)
+        std::vector<double> sc(4 * (size_t)S * nsteps);
+        for (int n = 0; n < nsteps; ++n) {
+            const double tp = t + (double)(n + 1) * dt;
+            for (int s = 0; s < S; ++s) {
+                const thermo::Scen &q = c->scen[s];
+                const double sv = q.s0 + q.amp * std::sin(2.0 * M_PI * tp / q.period);
+                const double eta = q.eta0 * (1.0 + q.eta_amp * std::sin(2.0 * M_PI * tp / q.eta_period));
+                double *o = &sc[4 * ((size_t)n * S + s)];
+                o[0] = sv * q.d2[0];
+                o[1] = sv * q.d2[1];
+                o[2] = eta;
+                o[3] = sv;
+            }
+        }
+        API_CK(cudaMemcpyAsync(c->d_step_sc, sc.data(), sizeof(double) * sc.size(), cudaMemcpyHostToDevice, c->stream));
+        API_CK(cudaMemsetAsync(c->d_status, 0, sizeof(int) * 8, c->stream));
+        if (S != 1) return fail(c, THERMO_EINVAL, "batched scenarios not enabled in this build");
+        if (c->timing) {
+            while (c->events.size() < 2 * (size_t)nsteps + 1) {
+                cudaEvent_t e;
+                API_CK(cudaEventCreate(&e));
+                c->events.push_back(e);
+            }
+        }
+        for (int n = 0; n < nsteps; ++n) {
+            thermo::IfaceParams P;
+            memset(&P, 0, sizeof P);
+            thermo::iface_params(*c, P, c->d_step_sc + 4 * (size_t)n * S, dt);
+            if (c->timing) API_CK(cudaEventRecord(c->events[2 * n], c->stream));
+            if (thermo::iface_launch(*c, P)) return THERMO_ECUDA;
+            if (c->timing) API_CK(cudaEventRecord(c->events[2 * n + 1], c->stream));
+            if (thermo::cg_launch_step(*c, n, dt)) return THERMO_ECUDA;
+        }
+        if (c->timing) API_CK(cudaEventRecord(c->events[2 * nsteps], c->stream));
+        int status[8];
+        c->h_iters.assign((size_t)nsteps * S, 0);
+        c->h_relres.assign((size_t)nsteps * S, 0.0);
+        c->h_area.assign(nsteps, 0.0);
+        API_CK(cudaMemcpyAsync(status, c->d_status, sizeof status, cudaMemcpyDeviceToHost, c->stream));
+        API_CK(cudaMemcpyAsync(c->h_iters.data(), c->d_iters, sizeof(int32_t) * c->h_iters.size(), cudaMemcpyDeviceToHost, c->stream));
+        API_CK(cudaMemcpyAsync(c->h_relres.data(), c->d_relres, sizeof(double) * c->h_relres.size(), cudaMemcpyDeviceToHost, c->stream));
+        API_CK(cudaMemcpyAsync(c->h_area.data(), c->d_area, sizeof(double) * c->h_area.size(), cudaMemcpyDeviceToHost, c->stream));
+        double frel = 0.0;
+        API_CK(cudaMemcpyAsync(&frel, c->d_fail_relres, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        API_CK(cudaStreamSynchronize(c->stream));
+        c->last_nsteps = nsteps;
+        c->ms_iface = c->ms_solve = 0.0;
+        if (c->timing) {
+            for (int n = 0; n < nsteps; ++n) {
+                float a = 0.f, b = 0.f;
+                API_CK(cudaEventElapsedTime(&a, c->events[2 * n], c->events[2 * n + 1]));
+                API_CK(cudaEventElapsedTime(&b, c->events[2 * n + 1], c->events[2 * n + 2]));
+                c->ms_iface += a;
+                c->ms_solve += b;
+            }
+        }
+        if (status[0]) {
+            const int f = status[2];
+            c->failed_step = f;
+            c->failed_scen = status[3];
+            c->failed_relres = status[0] == 1 ? frel : NAN;
+            c->cur = (c->cur + f) & 1;
+            c->steps_done += f;
+            c->last_nsteps = f;
+            if (status[0] == 2)
+                return fail(c, THERMO_EGEOM, "interface row capacity exceeded at step " + std::to_string(f));
+            char buf[160];
+            snprintf(buf, sizeof buf, "CG did not converge at step %d (scenario %d), relres %.3e", f, status[3], frel);
+            return fail(c, THERMO_ENOCONV, buf);
+        }
+        c->failed_step = -1;
+        c->failed_scen = -1;
+        c->cur = (c->cur + nsteps) & 1;
+        c->steps_done += nsteps;
+        return THERMO_OK;
+    } catch (...) {
+        return fail(c, THERMO_ENOMEM, "host allocation failed");
+    }
+}
+
+static int selection(Ctx *c, int32_t scen, int32_t part, int64_t n, int64_t *off, int64_t *cnt) {
+    if (scen < 0 || scen >= c->S) return fail(c, THERMO_EINVAL, "scenario index out of range");
+    if (part == 0) { *off = 0; *cnt = c->nf; }
+    else if (part == 1) { *off = c->nf; *cnt = c->nm; }
+    else if (part == -1) { *off = 0; *cnt = c->N; }
+    else return fail(c, THERMO_EINVAL, "part must be 0, 1 or -1");
+    if (n != *cnt) return fail(c, THERMO_EINVAL, "n does not match the node count of the selection");
+    return THERMO_OK;
+}
+
+extern "C" int thermo_get_T(void *ctx, int32_t scen, int32_t part, double *out, int64_t n,
+                            int32_t out_on_device) {
+    Ctx *c = (Ctx *)ctx;
+    if (!c || !out) return c ? fail(c, THERMO_EINVAL, "out is NULL") : THERMO_EINVAL;
+    int64_t off, cnt;
+    if (int rc = selection(c, scen, part, n, &off, &cnt)) return rc;
+    const double *src = c->d_T[c->cur] + off * c->S + scen;
+    cudaMemcpyKind kind = out_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    if (c->S == 1) API_CK(cudaMemcpyAsync(out, src, sizeof(double) * cnt, kind, c->stream));
+    else API_CK(cudaMemcpy2DAsync(out, sizeof(double), src, sizeof(double) * c->S, sizeof(double), cnt, kind, c->stream));
+    if (!out_on_device) API_CK(cudaStreamSynchronize(c->stream));
+    return THERMO_OK;
+}
+
+extern "C" int thermo_set_T(void *ctx, int32_t scen, int32_t part, const double *in, int64_t n,
+                            int32_t in_on_device) {
+    Ctx *c = (Ctx *)ctx;
+    if (!c || !in) return c ? fail(c, THERMO_EINVAL, "in is NULL") : THERMO_EINVAL;
+    int64_t off, cnt;
+    if (int rc = selection(c, scen, part, n, &off, &cnt)) return rc;
+    double *dst = c->d_T[c->cur] + off * c->S + scen;
+    cudaMemcpyKind kind = in_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    if (c->S == 1) API_CK(cudaMemcpyAsync(dst, in, sizeof(double) * cnt, kind, c->stream));
+    else API_CK(cudaMemcpy2DAsync(dst, sizeof(double) * c->S, in, sizeof(double), sizeof(double), cnt, kind, c->stream));
+    if (!in_on_device) API_CK(cudaStreamSynchronize(c->stream));
+    return THERMO_OK;
+}
+
+extern "C" int thermo_get_stats(const void *ctx, thermo_stats *out) {
+    const Ctx *c = (const Ctx *)ctx;
+    if (!c || !out) return THERMO_EINVAL;
+    memset(out, 0, sizeof *out);
+    out->n_fixed = c->nf;
+    out->n_moving = c->nm;
+    out->nnz_volume = c->nnz;
+    out->nnz_volume_padded = c->nnz_pad;
+    out->n_scen = c->S;
+    out->n_iface_rows = c->n_if;
+    out->iface_capacity = c->cap;
+    out->last_nsteps = c->last_nsteps;
+    int64_t tot = 0;
+    int mx = 0;
+    for (size_t k = 0; k < c->h_iters.size() && k < (size_t)c->last_nsteps * c->S; ++k) {
+        tot += c->h_iters[k];
+        mx = c->h_iters[k] > mx ? c->h_iters[k] : mx;
+    }
+    out->total_iters = tot;
+    out->max_iters = mx;
+    out->failed_step = c->failed_step;
+    out->failed_scen = c->failed_scen;
+    out->failed_relres = c->failed_relres;
+    double lr = 0.0;
+    if (c->last_nsteps > 0)
+        for (int s = 0; s < c->S; ++s) lr = fmax(lr, c->h_relres[(size_t)(c->last_nsteps - 1) * c->S + s]);
+    out->last_relres = lr;
+    out->steps_done = c->steps_done;
+    out->iface_area = c->last_nsteps > 0 ? c->h_area[c->last_nsteps - 1] : 0.0;
+    out->ms_iface = c->ms_iface;
+    out->ms_solve = c->ms_solve;
+    out->solve_grid = c->cg_grid;
+    out->solve_block = THERMO_BLOCK;
+    return THERMO_OK;
+}
+
+extern "C" int thermo_set_timing(void *ctx, int32_t enable) {
+    Ctx *c = (Ctx *)ctx;
+    if (!c) return THERMO_EINVAL;
+    c->timing = enable != 0;
+    return THERMO_OK;
+}
+
+extern "C" int thermo_get_step_iters(const void *ctx, int32_t *out, int64_t n) {
+    const Ctx *c = (const Ctx *)ctx;
+    if (!c || !out) return THERMO_EINVAL;
+    int64_t m = (int64_t)c->h_iters.size();
+    if (n < m) m = n;
+    for (int64_t k = 0; k < m; ++k) out[k] = c->h_iters[k];
+    return THERMO_OK;
+}
+
+extern "C" const char *thermo_last_error(const void *ctx) {
+    const Ctx *c = (const Ctx *)ctx;
+    return c ? c->err.c_str() : g_create_err.c_str();
+}
+
+extern "C" void thermo_destroy(void *ctx) {
+    Ctx *c = (Ctx *)ctx;
+    if (!c) return;
+    cudaStreamSynchronize(c->stream);
+    free_ctx(c);
+}

@@ -328,18 +328,19 @@ def lshape_pair(h_fixed, h_stock, jitter=0.1, seed=1707):
     return fixed, moving
 
 
-def make_config(name: str, n_scen: Optional[int] = None) -> Config:
+def make_config(name: str, n_scen: Optional[int] = None, jitter: Optional[float] = None) -> Config:
     """Build one named configuration.
 
     cfg0..cfg4 are BASELINE.json configs[0..4]; "small" and "medium" are extra parity
-    sizes (same geometry as cfg 0/1, several SELL slices + a ragged tail)."""
+    sizes (same geometry as cfg 0/1, several SELL slices + a ragged tail).  `jitter`
+    overrides the configuration's node jitter (fraction of h)."""
     if name in ("cfg0", "small", "medium", "cfg1", "cfg4"):
         cells = {"cfg0": ((16, 4, 2), (5, 3, 2)),
                  "small": ((32, 8, 4), (10, 6, 3)),
                  "medium": ((64, 16, 8), (20, 12, 6)),
                  "cfg1": ((128, 32, 16), (40, 24, 12)),
                  "cfg4": ((128, 32, 16), (40, 24, 12))}[name]
-        fixed, moving = rail_pair(*cells)
+        fixed, moving = rail_pair(*cells, jitter=0.0 if jitter is None else jitter)
         if name == "cfg4":
             S = 64 if n_scen is None else n_scen
             scen = [Scenario(0.375, 0.375, 20.0 + k, 100.0 + 15.0 * k) for k in range(S)]
@@ -357,7 +358,7 @@ def make_config(name: str, n_scen: Optional[int] = None) -> Config:
                       24.0, dt, nsteps, description=f"rail pair {cells}")
     if name in ("cfg2", "cfg3"):
         hf, hs, nsteps = {"cfg2": (0.01, 0.004, 3600), "cfg3": (0.005, 0.002, 200)}[name]
-        fixed, moving = lshape_pair(hf, hs)
+        fixed, moving = lshape_pair(hf, hs, jitter=0.1 if jitter is None else jitter)
         scen = [Scenario(1.15, 0.5, 30.0, 500.0)]
         return Config(name, fixed, moving, NU, RHO_CP, ALPHA_IFACE, _std_robin(), scen,
                       24.0, 1.0, nsteps, description=f"L-shape stand h={hf}, stock h={hs}")

@@ -1,0 +1,146 @@
+"""GPU parity: the CUDA path through the C ABI against the CPU oracle on the same seeded
+inputs (max-norm relative error <= 1e-9 after the run, BASELINE.json north star), plus the
+invariants of the method evaluated on the GPU output.
+
+All calls go through paper_1707_03581_b200.thermo (ctypes -> libthermo.so).
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_1707_03581_b200 import inputs as I
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-9   # north star: max-norm relative error after the full run
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    import __graft_entry__ as g
+    g.build()
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+
+
+def _thermo(cfg, **kw):
+    from paper_1707_03581_b200.thermo import Thermo
+    return Thermo.from_config(cfg, **kw)
+
+
+def rel(a, b):
+    return float(np.abs(a - b).max() / np.abs(b).max())
+
+
+def test_cfg0_full_run_vs_dense_cholesky():
+    """BASELINE config 0, 100 steps: GPU CG vs oracle dense Cholesky."""
+    cfg = I.make_config("cfg0")
+    th = _thermo(cfg)
+    th.step(0.0, cfg.dt, cfg.nsteps)
+    Tg = th.get_T()
+    Tr, st = O.run_config(cfg, solver="cholesky")
+    assert rel(Tg, Tr) <= TOL
+    s = th.stats()
+    assert s["steps_done"] == cfg.nsteps and s["failed_step"] == -1
+    assert abs(s["iface_area"] - 0.05) < 1e-14
+
+
+@pytest.mark.parametrize("name,jitter", [("small", 0.0), ("small", 0.1), ("medium", 0.1)])
+def test_parity_vs_oracle_cg(name, jitter):
+    """Several slices + a ragged tail, jittered non-matching meshes, a non-uniform seeded
+    start field, time-varying friction; full configured run length."""
+    cfg = I.make_config(name, jitter=jitter)
+    T0 = I.initial_field(cfg)[0]
+    th = _thermo(cfg)
+    th.set_T(T0)
+    th.step(0.0, cfg.dt, cfg.nsteps)
+    Tg = th.get_T()
+    Tr, st = O.run_config(cfg, T_init=T0)
+    assert rel(Tg, Tr) <= TOL
+    it = th.step_iters()[:, 0]
+    # same stopping rule on both sides: iteration counts agree to +-1
+    assert np.abs(it - st[:, 0]).max() <= 1
+
+
+def test_parts_and_device_copy():
+    import torch
+    cfg = I.make_config("small")
+    th = _thermo(cfg)
+    th.step(0.0, cfg.dt, 3)
+    full = th.get_T()
+    assert np.array_equal(th.get_T(part=0), full[:cfg.fixed.n_nodes])
+    assert np.array_equal(th.get_T(part=1), full[cfg.fixed.n_nodes:])
+    out = torch.empty(cfg.n_dof, dtype=torch.float64, device="cuda")
+    th.get_T(out=out)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), full)
+
+
+def test_deterministic_and_step_splitting():
+    """Deterministic reductions: two runs are bitwise equal, and 10 steps in one call equal
+    5 + 5 steps in two calls."""
+    cfg = I.make_config("small", jitter=0.1)
+    a = _thermo(cfg)
+    a.step(0.0, cfg.dt, 10)
+    b = _thermo(cfg)
+    b.step(0.0, cfg.dt, 5)
+    b.step(5 * cfg.dt, cfg.dt, 5)
+    c = _thermo(cfg)
+    c.step(0.0, cfg.dt, 10)
+    assert np.array_equal(a.get_T(), c.get_T())
+    assert np.array_equal(a.get_T(), b.get_T())
+
+
+def test_uniform_state_fixed_point_gpu():
+    cfg = I.make_config("small", jitter=0.1)
+    cfg.robin = [I.Robin(0, 1, 10.0, 24.0), I.Robin(1, 1, 10.0, 24.0), I.Robin(0, 3, 50.0, 24.0),
+                 I.Robin(1, 2, 200.0, 24.0)]
+    cfg.scenarios = [I.Scenario(0.375, 0.375, 20.0, 0.0)]
+    th = _thermo(cfg)
+    th.step(0.0, 1.0, 10)
+    assert np.abs(th.get_T() - 24.0).max() < 1e-9
+
+
+def test_energy_balance_gpu():
+    """Robin off: sum M_L dT = dt eta(t_{n+1}) |Gamma_R| per step (north star invariant)."""
+    cfg = I.make_config("medium", jitter=0.1)
+    cfg.robin = []
+    ML = O.Oracle.from_config(cfg).volume()[4]
+    sc = cfg.scenarios[0]
+    th = _thermo(cfg)
+    T = th.get_T()
+    for n in range(4):
+        th.step(n * cfg.dt, cfg.dt, 1)
+        T1 = th.get_T()
+        eta = sc.eta0 * (1 + sc.eta_amp * math.sin(2 * math.pi * (n + 1) * cfg.dt / sc.eta_period))
+        dE = float(ML @ (T1 - T))
+        assert abs(dE - cfg.dt * eta * 0.05) < 1e-7 * cfg.dt * eta * 0.05
+        T = T1
+
+
+def test_noconv_reports_and_keeps_state():
+    from paper_1707_03581_b200.thermo import ThermoError, THERMO_ENOCONV
+    cfg = I.make_config("small")
+    th = _thermo(cfg)
+    th.step(0.0, cfg.dt, 2)
+    T2 = th.get_T()
+    th.set_solver(1e-12, 1)
+    with pytest.raises(ThermoError) as e:
+        th.step(2 * cfg.dt, cfg.dt, 3)
+    assert e.value.code == THERMO_ENOCONV
+    s = th.stats()
+    assert s["failed_step"] == 0 and s["failed_relres"] > 1e-12
+    assert np.array_equal(th.get_T(), T2)
+
+
+@pytest.mark.slow
+def test_cfg1_full_run():
+    """BASELINE config 1: 85,694 DoF, 1000 steps of 0.5 s, eta(t) varying."""
+    cfg = I.make_config("cfg1")
+    th = _thermo(cfg)
+    th.step(0.0, cfg.dt, cfg.nsteps)
+    Tg = th.get_T()
+    Tr, st = O.run_config(cfg)
+    assert rel(Tg, Tr) <= TOL
