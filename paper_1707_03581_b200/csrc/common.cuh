@@ -37,6 +37,52 @@ __device__ __forceinline__ int ld_stream(const int *p, uint64_t pol) {
 }
 
 // ---------------------------------------------------------------------------------
+// mbarrier + bulk-copy (TMA engine) helpers
+// ---------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// global -> shared bulk copy on the TMA engine, completion signalled on `bar` (tx bytes)
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar,
+                                         uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+
+// L2 prefetch of a contiguous range on the TMA engine (16-byte aligned, size % 16 == 0)
+__device__ __forceinline__ void bulk_prefetch_l2(const void *src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
+// ---------------------------------------------------------------------------------
 // deterministic reductions: xor-butterfly inside a warp (every lane ends with the same
 // bits), fixed-order combination across warps and CTAs.
 // ---------------------------------------------------------------------------------
@@ -46,11 +92,15 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
+// smem scratch of the reductions: >= 144 doubles (warp partials [0, 32*NV), totals at 136).
+#define THERMO_RED_SMEM 160
+
 // Reduce NV values over the CTA and store them to partials[blockIdx.x * THERMO_NRED + slot + j].
 template <int NV>
 __device__ __forceinline__ void cta_reduce_store(double (&v)[NV], double *smem, double *partials,
                                                  int slot) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nwarps = blockDim.x >> 5;
 #pragma unroll
     for (int j = 0; j < NV; ++j) v[j] = warp_sum(v[j]);
     if (lane == 0) {
@@ -61,7 +111,7 @@ __device__ __forceinline__ void cta_reduce_store(double (&v)[NV], double *smem, 
     if (warp == 0) {
 #pragma unroll
         for (int j = 0; j < NV; ++j) {
-            double x = lane < THERMO_WARPS ? smem[lane * NV + j] : 0.0;
+            double x = lane < nwarps ? smem[lane * NV + j] : 0.0;
             x = warp_sum(x);
             if (lane == 0) partials[blockIdx.x * THERMO_NRED + slot + j] = x;
         }
@@ -81,12 +131,12 @@ __device__ __forceinline__ void grid_total(const double *partials, int G, int sl
             double x = 0.0;
             for (int g = lane; g < G; g += 32) x += partials[g * THERMO_NRED + slot + j];
             x = warp_sum(x);
-            if (lane == 0) smem[64 + j] = x;
+            if (lane == 0) smem[136 + j] = x;
         }
     }
     __syncthreads();
 #pragma unroll
-    for (int j = 0; j < NV; ++j) out[j] = smem[64 + j];
+    for (int j = 0; j < NV; ++j) out[j] = smem[136 + j];
     __syncthreads();
 }
 
@@ -112,6 +162,7 @@ struct PairRec {       // one overlapping (rail-top, stock-bottom) triangle pair
 struct IfaceParams {
     int nTA, nTB;         // rail-top / stock-bottom triangles
     int pcap;             // pair records per triangle
+    int cmax;             // contributions per interface row (6 x records of its star)
     PairRec *pairs;       // [(side A: S*nTA | side B: S*nTB) * pcap]
     int32_t *pcnt;        // [S*nTA + S*nTB]
     int n_if;             // interface rows: [0, nA) rail top (fixed), [nA, n_if) stock bottom

@@ -60,7 +60,7 @@ struct Ctx {
     bool robin_dirty = true;
 
     // interface
-    int n_if = 0, nA = 0, nTA = 0, nTB = 0, cap = 0, pcap = 0;
+    int n_if = 0, nA = 0, nTA = 0, nTB = 0, cap = 0, pcap = 0, cmax = 0;
     PairRec *d_pairs = nullptr;
     int32_t *d_pcnt = nullptr;
     int32_t *d_if_rows = nullptr;
@@ -88,7 +88,12 @@ struct Ctx {
     double *d_relres = nullptr;      // [steps][S]
     double *d_area = nullptr;        // [steps]
     int64_t step_cap = 0;
-    int cg_grid = 0;
+    int cg_grid = 0, cg_block = 0, cg_stage_entries = 0;
+    size_t cg_smem = 0;
+    bool cg_tma = false;
+    int cg_variant = 0, cg_chunk = 8;
+    int32_t *d_chunk_hi = nullptr;
+    int *d_chunk_ctr = nullptr;
 
     double rtol = 1e-12;
     int maxit = 0;

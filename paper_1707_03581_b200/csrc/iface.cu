@@ -133,11 +133,23 @@ __device__ bool pair_integrals(const double2 F[3], const double2 G[3], bool ownI
     return area > 0.0;
 }
 
-// Thread per (own triangle t of side `side`, scenario s): every overlapping pair with the
-// other surface, in a fixed order (bins row-major, ascending ids, each pair once).
+__device__ __forceinline__ int warp_excl_scan(int v, int lane) {
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    return x - v;
+}
+
+// Warp per (own triangle t of side `side`, scenario s): the candidates of all bins under the
+// triangle's box are flattened (bins row-major, ascending ids) and spread over the lanes;
+// hits are written in that order (ballot prefix), so the record list is deterministic.
 __global__ void __launch_bounds__(128) k_pairs(IfaceParams P, int side) {
+    const int lane = threadIdx.x & 31;
     const int nT = side == 0 ? P.nTA : P.nTB;
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int t = blockIdx.x * 4 + (threadIdx.x >> 5);
     const int s = blockIdx.y;
     if (t >= nT) return;
     const double ox = P.step_sc[4 * s + 0], oy = P.step_sc[4 * s + 1];
@@ -159,51 +171,99 @@ __global__ void __launch_bounds__(128) k_pairs(IfaceParams P, int side) {
     const double qlx = lox - sx_oth, qhx = hix - sx_oth, qly = loy - sy_oth, qhy = hiy - sy_oth;
     const int bx0 = bin_coord(qlx, G.x0, G.inv_h, G.nx), bx1 = bin_coord(qhx, G.x0, G.inv_h, G.nx);
     const int by0 = bin_coord(qly, G.y0, G.inv_h, G.ny), by1 = bin_coord(qhy, G.y0, G.inv_h, G.ny);
-    PairRec *out = P.pairs + ((int64_t)(side == 0 ? 0 : P.nTA * (int64_t)P.S) + (int64_t)s * nT + t) * P.pcap;
+    const int nbx = bx1 - bx0 + 1, nbins = nbx * (by1 - by0 + 1);
+    const int64_t rid = (side == 0 ? 0 : (int64_t)P.nTA * P.S) + (int64_t)s * nT + t;
+    PairRec *out = P.pairs + rid * P.pcap;
     int j = 0;
     bool ok = true;
-    for (int by = by0; by <= by1; ++by)
-        for (int bx = bx0; bx <= bx1; ++bx) {
-            const int bin = by * G.nx + bx;
-            for (int m = G.ptr[bin]; m < G.ptr[bin + 1]; ++m) {
-                const int u = G.ids[m];
-                const double4 ub = oth_box[u];
-                if (ub.x > qhx || ub.z < qlx || ub.y > qhy || ub.w < qly) continue;
-                if (bin_coord(fmax(qlx, ub.x), G.x0, G.inv_h, G.nx) != bx ||
-                    bin_coord(fmax(qly, ub.y), G.y0, G.inv_h, G.ny) != by) continue;
-                const int4 W = oth_tri[u];
-                const int wv[3] = {W.x, W.y, W.z};
-                double2 Up[3];
-                for (int v = 0; v < 3; ++v) {
-                    const double2 q = P.uv[wv[v]];
-                    Up[v] = make_double2(q.x + sx_oth, q.y + sy_oth);
-                }
-                PairRec r;
-                const bool hit = side == 0 ? pair_integrals(Tp, Up, true, r) : pair_integrals(Up, Tp, false, r);
-                if (!hit) continue;
-                if (j == P.pcap) { ok = false; continue; }
-                r.other = u;
-                out[j++] = r;
-            }
+    for (int b0 = 0; b0 < nbins; b0 += 32) {   // up to 32 bins per round
+        const int bl = b0 + lane;
+        int bin = -1, cnt = 0;
+        if (bl < nbins) {
+            bin = (by0 + bl / nbx) * G.nx + bx0 + bl % nbx;
+            cnt = G.ptr[bin + 1] - G.ptr[bin];
         }
-    if (!ok) atomicOr(&P.status[1], 1);
-    P.pcnt[(side == 0 ? 0 : P.nTA * (int64_t)P.S) + (int64_t)s * nT + t] = j;
+        const int off = warp_excl_scan(cnt, lane);
+        const int total = __shfl_sync(0xffffffffu, off + cnt, 31);
+        for (int base = 0; base < total; base += 32) {
+            const int idx = base + lane;
+            bool hit = false;
+            PairRec r;
+            int u = -1;
+            // bin slot q holding candidate idx (every lane takes part in the shuffles)
+            int q = 0;
+            for (int l = 1; l < 32; ++l) {
+                const int ol = __shfl_sync(0xffffffffu, off, l);
+                if (l < nbins - b0 && ol <= idx) q = l;
+            }
+            const int binq = __shfl_sync(0xffffffffu, bin, q);
+            const int offq = __shfl_sync(0xffffffffu, off, q);
+            if (idx < total) {
+                const int m = G.ptr[binq] + (idx - offq);
+                u = G.ids[m];
+                const double4 ub = oth_box[u];
+                const int bx = bx0 + (b0 + q) % nbx, by = by0 + (b0 + q) / nbx;
+                if (!(ub.x > qhx || ub.z < qlx || ub.y > qhy || ub.w < qly) &&
+                    bin_coord(fmax(qlx, ub.x), G.x0, G.inv_h, G.nx) == bx &&
+                    bin_coord(fmax(qly, ub.y), G.y0, G.inv_h, G.ny) == by) {
+                    const int4 W = oth_tri[u];
+                    const int wv[3] = {W.x, W.y, W.z};
+                    double2 Up[3];
+                    for (int v = 0; v < 3; ++v) {
+                        const double2 c2 = P.uv[wv[v]];
+                        Up[v] = make_double2(c2.x + sx_oth, c2.y + sy_oth);
+                    }
+                    hit = side == 0 ? pair_integrals(Tp, Up, true, r) : pair_integrals(Up, Tp, false, r);
+                }
+            }
+            const unsigned mask = __ballot_sync(0xffffffffu, hit);
+            if (hit) {
+                const int pos = j + __popc(mask & ((1u << lane) - 1u));
+                if (pos < P.pcap) {
+                    r.other = u;
+                    out[pos] = r;
+                } else {
+                    ok = false;
+                }
+            }
+            j += __popc(mask);
+        }
+    }
+    if (!__all_sync(0xffffffffu, ok) || j > P.pcap) {
+        if (lane == 0) atomicOr(&P.status[1], 1);
+    }
+    if (lane == 0) P.pcnt[rid] = min(j, P.pcap);
 }
 
 // ------------------------------------------------------------------------------ K2b: rows
 
-// Warp per (interface node k, scenario s): sum the pair records of the node's star into its
-// ELL row of K~_G in a fixed order (star triangles ascending, pairs in record order, the six
-// contributions of a record in order own b=0..2, other b=0..2).  Shared-memory row buffer,
-// warp-ballot search for the column.
-__global__ void __launch_bounds__(128) k_rows(IfaceParams P) {
-    extern __shared__ unsigned char smem_raw[];
+// Warp per (interface node k, scenario s).  The node's contributions (6 per pair record of
+// its star: own columns b=0..2, other b=0..2) are streamed in a fixed order -- rounds of 32
+// records, then q = 0..5, then lane -- and merged into a shared-memory row:
+//  - a column gets its slot on first appearance (new keys ranked by lane within the round),
+//    found again through a small shared-memory hash table;
+//  - contributions to one slot inside a round are summed in lane order by the group leader,
+//    then added to the slot.
+// Every floating-point sum therefore runs in a fixed order: deterministic, no FP atomics.
+#define ROW_HS 256   // hash table size per warp (power of two, >= 2 x capacity)
+#define ROW_WPB 4    // warps per block
+
+struct RowSmem {
+    int hkey[ROW_HS], hslot_[ROW_HS];
+    int ucol[ROW_HS / 2];
+    double val[ROW_HS / 2];
+    double tmp[32];
+};
+
+__device__ __forceinline__ int hslot(int key) { return (int)(((unsigned)key * 2654435761u) >> 24) & (ROW_HS - 1); }
+
+__global__ void __launch_bounds__(32 * ROW_WPB) k_rows(IfaceParams P) {
+    __shared__ RowSmem sm_all[ROW_WPB];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int k = blockIdx.x * 4 + wib;
+    const int k = blockIdx.x * ROW_WPB + wib;
     const int s = blockIdx.y;
-    double *vals = reinterpret_cast<double *>(smem_raw) + (size_t)wib * P.cap;
-    int *cols = reinterpret_cast<int *>(reinterpret_cast<double *>(smem_raw) + 4 * (size_t)P.cap) + (size_t)wib * P.cap;
     if (k >= P.n_if) return;
+    RowSmem &W = sm_all[wib];
     const bool sideA = k < P.nA;
     const int nT = sideA ? P.nTA : P.nTB;
     const int64_t base_rec = sideA ? 0 : (int64_t)P.nTA * P.S;
@@ -211,63 +271,112 @@ __global__ void __launch_bounds__(128) k_rows(IfaceParams P) {
     const int4 *oth_tri = sideA ? P.triB : P.triA;
     const int32_t row = P.if_rows[k];
     const double scale = P.dt * P.alpha;
+    const int st0 = P.star_ptr[k], nstar = P.star_ptr[k + 1] - st0;   // <= 32 (checked at setup)
+    const unsigned lt = (1u << lane) - 1u;
+    for (int h = lane; h < ROW_HS; h += 32) W.hkey[h] = -1;
+    __syncwarp();
+
+    int t_l = 0, np_l = 0, a_l = 0;
+    if (lane < nstar) {
+        t_l = P.star_tri[st0 + lane];
+        const int4 T = own_tri[t_l];
+        a_l = (T.x == k) ? 0 : ((T.y == k) ? 1 : 2);
+        np_l = P.pcnt[base_rec + (int64_t)s * nT + t_l];
+    }
+    const int roff = warp_excl_scan(np_l, lane);
+    const int R = __shfl_sync(0xffffffffu, roff + np_l, 31);
     int count = 0;
     bool ok = true;
     double phi = 0.0;
-    for (int st = P.star_ptr[k]; st < P.star_ptr[k + 1]; ++st) {
-        const int t = P.star_tri[st];
-        const int4 T = own_tri[t];
-        const int a = (T.x == k) ? 0 : ((T.y == k) ? 1 : 2);
-        const int64_t rid = base_rec + (int64_t)s * nT + t;
-        const int np = P.pcnt[rid];
-        const PairRec *rec = P.pairs + rid * P.pcap;
-        // own-row index pattern into the symmetric 3x3 (00 01 02 11 12 22)
-        const int sym[3][3] = {{0, 1, 2}, {1, 3, 4}, {2, 4, 5}};
-        for (int j = 0; j < np; ++j) {
-            const PairRec &r = rec[j];
-            int col = 0;
-            double v = 0.0;
-            if (lane < 3) {
-                const int tv = lane == 0 ? T.x : (lane == 1 ? T.y : T.z);
-                col = P.if_rows[tv];
-                v = scale * r.own[sym[a][lane]];          // -dt * (-alpha int phi phi)
-            } else if (lane < 6) {
-                const int4 W = oth_tri[r.other];
-                const int wv = lane == 3 ? W.x : (lane == 4 ? W.y : W.z);
-                col = P.if_rows[wv];
-                v = -scale * r.cross[a * 3 + (lane - 3)];  // -dt * (+alpha int phi phi)
+    for (int r0 = 0; r0 < R; r0 += 32) {
+        const int r = r0 + lane;
+        int q = 0;
+        for (int l = 1; l < 32; ++l) {
+            const int ol = __shfl_sync(0xffffffffu, roff, l);
+            if (l < nstar && ol <= r) q = l;
+        }
+        const int tq = __shfl_sync(0xffffffffu, t_l, q);
+        const int aq = __shfl_sync(0xffffffffu, a_l, q);
+        const int oq = __shfl_sync(0xffffffffu, roff, q);
+        const bool valid = r < R;
+        int cc[6];
+        double cv[6];
+        if (valid) {
+            const PairRec &rec = P.pairs[(base_rec + (int64_t)s * nT + tq) * P.pcap + (r - oq)];
+            const int4 Tq = own_tri[tq];
+            const int4 Wq = oth_tri[rec.other];
+            const int sym[3][3] = {{0, 1, 2}, {1, 3, 4}, {2, 4, 5}};
+            const int tv[3] = {Tq.x, Tq.y, Tq.z}, wv[3] = {Wq.x, Wq.y, Wq.z};
+#pragma unroll
+            for (int b = 0; b < 3; ++b) {
+                cc[b] = P.if_rows[tv[b]];
+                cv[b] = scale * rec.own[sym[aq][b]];          // -dt * (-alpha int phi phi)
+                cc[3 + b] = P.if_rows[wv[b]];
+                cv[3 + b] = -scale * rec.cross[aq * 3 + b];   // -dt * (+alpha int phi phi)
             }
-            phi += r.b[a];
-            for (int q = 0; q < 6; ++q) {
-                const int cq = __shfl_sync(0xffffffffu, col, q);
-                const double vq = __shfl_sync(0xffffffffu, v, q);
-                int idx = -1;
-                for (int c = lane; c < count; c += 32)
-                    if (cols[c] == cq) idx = c;
-                const unsigned m = __ballot_sync(0xffffffffu, idx >= 0);
-                if (m) {
-                    if (lane == __ffs(m) - 1) vals[idx] += vq;
-                } else if (count < P.cap) {
-                    if (lane == 0) { cols[count] = cq; vals[count] = vq; }
-                    ++count;
-                } else {
-                    ok = false;
+            phi += rec.b[aq];
+        }
+#pragma unroll
+        for (int qq = 0; qq < 6; ++qq) {
+            const int key = valid ? cc[qq] : -1;
+            // existing slot?
+            int slot = -1;
+            if (valid) {
+                int h = hslot(key);
+                for (int pr = 0; pr < ROW_HS; ++pr) {
+                    const int kk = W.hkey[h];
+                    if (kk == key) { slot = W.hslot_[h]; break; }
+                    if (kk == -1) break;
+                    h = (h + 1) & (ROW_HS - 1);
                 }
-                __syncwarp();
             }
+            // new keys: one leader per distinct key, slots by leader lane order
+            const bool isnew = valid && slot < 0;
+            const unsigned grp = __match_any_sync(0xffffffffu, isnew ? key : (valid ? -2 : -3 - lane));
+            const bool leader_new = isnew && (grp & lt) == 0;
+            const unsigned lm = __ballot_sync(0xffffffffu, leader_new);
+            if (leader_new) {
+                slot = count + __popc(lm & lt);
+                if (slot < ROW_HS / 2) {
+                    W.ucol[slot] = key;
+                    W.val[slot] = 0.0;
+                    int h = hslot(key);
+                    for (int pr = 0; pr < ROW_HS; ++pr) {
+                        if (atomicCAS(&W.hkey[h], -1, key) == -1) { W.hslot_[h] = slot; break; }
+                        h = (h + 1) & (ROW_HS - 1);
+                    }
+                }
+            }
+            count += __popc(lm);
+            if (isnew) slot = __shfl_sync(grp, slot, __ffs(grp) - 1);
+            __syncwarp();
+            // sum per slot in lane order, leader adds to the row
+            W.tmp[lane] = valid ? cv[qq] : 0.0;
+            __syncwarp();
+            const unsigned g2 = __match_any_sync(0xffffffffu, valid ? slot : -3 - lane);
+            if (valid && (g2 & lt) == 0 && slot < ROW_HS / 2) {
+                double acc = 0.0;
+                for (unsigned m = g2; m; m &= m - 1) acc += W.tmp[__ffs(m) - 1];
+                W.val[slot] += acc;
+            }
+            __syncwarp();
         }
     }
+    phi = warp_sum(phi);
+    if (count > P.cap || count > ROW_HS / 2) ok = false;
     double dself = 0.0;
-    for (int c = 0; c < count; ++c)
-        if (cols[c] == row) dself += vals[c];
-    for (int c = lane; c < count; c += 32) {
-        const int64_t e = ((int64_t)s * P.cap + c) * P.n_if + k;
-        P.ell_col[e] = cols[c];
-        P.ell_val[e] = vals[c];
+    if (ok) {
+        for (int u = lane; u < count; u += 32) {
+            const int64_t idx = ((int64_t)s * P.cap + u) * P.n_if + k;
+            P.ell_col[idx] = W.ucol[u];
+            P.ell_val[idx] = W.val[u];
+            if (W.ucol[u] == row) dself = W.val[u];
+        }
     }
+    dself = warp_sum(dself);   // exactly one lane holds the diagonal (others add 0)
     if (lane == 0) {
         if (!ok) atomicOr(&P.status[1], 1);
-        P.ell_cnt[(int64_t)s * P.n_if + k] = count;
+        P.ell_cnt[(int64_t)s * P.n_if + k] = ok ? count : 0;
         P.if_phi[(int64_t)s * P.n_if + k] = phi;
         P.if_b[(int64_t)s * P.n_if + k] = 0.5 * P.step_sc[4 * s + 2] * phi;
         const double dinv = 1.0 / (P.Dvol[row] + dself);
@@ -571,6 +680,12 @@ int iface_setup(Ctx &c, const double *X, const std::vector<int32_t> &fA, const s
     if (mx > 2048) { c.err = "interface rows too dense (capacity > 2048)"; return -5; }
     c.cap = ((mx + 4) + 3) / 4 * 4;
     c.pcap = pmx + 2;
+    // contributions per row: 6 per record, records <= star size x pcap
+    int max_star = 0;
+    for (int k = 0; k < c.n_if; ++k) max_star = std::max(max_star, sptr[k + 1] - sptr[k]);
+    if (max_star > 32) { c.err = "interface node with more than 32 surface triangles"; return -1; }
+    if (c.cap > ROW_HS / 2) { c.err = "interface rows too dense for the row merge (capacity > 128)"; return -5; }
+    c.cmax = 6 * max_star * c.pcap;
     CK(cudaMalloc(&c.d_pairs, sizeof(PairRec) * (size_t)c.S * (c.nTA + c.nTB) * c.pcap));
     CK(cudaMalloc(&c.d_pcnt, sizeof(int32_t) * (size_t)c.S * (c.nTA + c.nTB)));
 
@@ -593,6 +708,7 @@ void iface_params(Ctx &c, IfaceParams &P, const double *step_sc, double dt) {
     P.pcap = c.pcap;
     P.pairs = c.d_pairs;
     P.pcnt = c.d_pcnt;
+    P.cmax = c.cmax;
     P.n_if = c.n_if;
     P.nA = c.nA;
     P.S = c.S;
@@ -623,13 +739,11 @@ void iface_params(Ctx &c, IfaceParams &P, const double *step_sc, double dt) {
 
 int iface_launch(Ctx &c, const IfaceParams &P) {
     if (c.n_if == 0) return 0;
-    k_pairs<<<dim3((unsigned)((c.nTA + 127) / 128), (unsigned)c.S), 128, 0, c.stream>>>(P, 0);
+    k_pairs<<<dim3((unsigned)((c.nTA + 3) / 4), (unsigned)c.S), 128, 0, c.stream>>>(P, 0);
     CK(cudaGetLastError());
-    k_pairs<<<dim3((unsigned)((c.nTB + 127) / 128), (unsigned)c.S), 128, 0, c.stream>>>(P, 1);
+    k_pairs<<<dim3((unsigned)((c.nTB + 3) / 4), (unsigned)c.S), 128, 0, c.stream>>>(P, 1);
     CK(cudaGetLastError());
-    const size_t smem = 4 * (size_t)c.cap * (sizeof(double) + sizeof(int));
-    if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_rows<<<dim3((unsigned)((c.n_if + 3) / 4), (unsigned)c.S), 128, smem, c.stream>>>(P);
+    k_rows<<<dim3((unsigned)((c.n_if + ROW_WPB - 1) / ROW_WPB), (unsigned)c.S), 32 * ROW_WPB, 0, c.stream>>>(P);
     CK(cudaGetLastError());
     return 0;
 }

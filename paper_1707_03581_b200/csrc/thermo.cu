@@ -41,7 +41,7 @@ static void free_ctx(Ctx *c) {
                     c->d_binB_ptr, c->d_binB_ids, c->d_slice_if, c->d_ell_cnt, c->d_ell_col, c->d_ell_val,
                     c->d_if_b, c->d_if_phi, c->d_if_dinv, c->d_T[0], c->d_T[1], c->d_z, c->d_p[0], c->d_p[1],
                     c->d_q, c->d_partials, c->d_status, c->d_fail_relres, c->d_step_sc, c->d_iters,
-                    c->d_relres, c->d_area, c->d_pairs, c->d_pcnt};
+                    c->d_relres, c->d_area, c->d_pairs, c->d_pcnt, c->d_chunk_hi, c->d_chunk_ctr};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     for (cudaEvent_t e : c->events) cudaEventDestroy(e);
@@ -392,7 +392,7 @@ extern "C" int thermo_get_stats(const void *ctx, thermo_stats *out) {
     out->ms_iface = c->ms_iface;
     out->ms_solve = c->ms_solve;
     out->solve_grid = c->cg_grid;
-    out->solve_block = THERMO_BLOCK;
+    out->solve_block = c->cg_block;
     return THERMO_OK;
 }
 

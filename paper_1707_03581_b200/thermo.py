@@ -173,6 +173,12 @@ class Thermo:
         self._check(load().thermo_get_T(self.h, scen, part, a.ctypes.data_as(ctypes.c_void_p), n, 0))
         return a
 
+    def get_T_host_ptr(self, ptr: int, scen: int = 0, part: int = -1):
+        """Copy into caller-owned host memory at address `ptr` (e.g. a pinned torch tensor);
+        synchronises the context stream."""
+        n = self._count(part)
+        self._check(load().thermo_get_T(self.h, scen, part, ctypes.c_void_p(ptr), n, 0))
+
     def set_T(self, T, scen: int = 0, part: int = -1):
         n = self._count(part)
         if hasattr(T, "is_cuda") and T.is_cuda:

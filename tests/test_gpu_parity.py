@@ -144,3 +144,16 @@ def test_cfg1_full_run():
     Tg = th.get_T()
     Tr, st = O.run_config(cfg)
     assert rel(Tg, Tr) <= TOL
+
+
+def test_register_path_matches_tma_path(monkeypatch):
+    """The TMA-ring sweep and the register-streaming fallback compute identical row sums;
+    only the order of the CTA-level dot-product partials differs."""
+    cfg = I.make_config("medium", jitter=0.1)
+    a = _thermo(cfg)
+    a.step(0.0, cfg.dt, 5)
+    monkeypatch.setenv("THERMO_CG_PATH", "0")
+    b = _thermo(cfg)
+    b.step(0.0, cfg.dt, 5)
+    assert a.stats()["solve_block"] != b.stats()["solve_block"]
+    assert rel(a.get_T(), b.get_T()) < 1e-12
