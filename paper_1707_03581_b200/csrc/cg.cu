@@ -11,19 +11,24 @@
 // Every value of every reduction is combined in a fixed order (deterministic, identical in
 // all CTAs), so all CTAs take the same control-flow decisions.
 //
-// Two variants of the sliced-ELL sweeps (phase 0 and S):
-//  kTMA = true  (default): one CTA per SM, CG_W consumer warps + 1 producer warp.  The
-//    producer streams chunks of CG_W consecutive slices (values + columns, contiguous in HBM)
-//    into a CG_NS-stage shared-memory ring with cp.async.bulk on the TMA engine
-//    (mbarrier complete_tx); consumers read the matrix from shared memory and only gather
-//    the vector entries from L1/L2.  HBM streaming is thereby decoupled from gather latency.
-//  kTMA = false: every warp streams its slices with L1-bypassing, L2-evict-first loads
-//    (fallback when a chunk does not fit the shared-memory ring).
+// Sliced-ELL sweeps (phase 0 and S) come in three kinds:
+//  KIND 0  register streaming: every warp streams its slices with L1-bypassing,
+//          L2-evict-first loads and gathers the vector entries from L1/L2 (fallback).
+//  KIND 1  TMA matrix ring: a producer warp streams chunks of W consecutive slices (values +
+//          int32 columns, contiguous in HBM) into an NS-stage shared-memory ring with
+//          cp.async.bulk (mbarrier complete_tx); NG groups of W consumer warps take every
+//          NG-th chunk and gather the vector entries from L1/L2.
+//  KIND 2  TMA matrix + vector windows: as KIND 1, but the columns are stored as 16-bit
+//          indices local to the chunk, and the producer also bulk-copies the chunk's column
+//          window (<= 32 contiguous runs of the gathered vectors, precomputed at setup) into
+//          shared memory, so every gather is a shared-memory load.  10 instead of 12 bytes
+//          per stored entry, and no gather latency on the critical path.
 #include <cooperative_groups.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "ctx.h"
@@ -41,19 +46,16 @@ namespace thermo {
         }                                                                        \
     } while (0)
 
-// TMA-ring geometry variants: CG_W slices per chunk = consumer warps per group, CG_G consumer
-// groups (group g consumes chunks n with n % CG_G == g), CG_NS pipeline stages.
-#define CG_HDR 128  // stage header bytes: chunk-relative slice offsets + interface ranges
-#define CG_NVARIANT 3
-__host__ __device__ constexpr int cg_w(int v) { return v == 2 ? 4 : 8; }
-__host__ __device__ constexpr int cg_g(int v) { return v == 2 ? 4 : 2; }
-__host__ __device__ constexpr int cg_ns(int v) { return v == 0 ? 4 : (v == 1 ? 3 : 6); }
-__host__ __device__ constexpr int cg_threads(int v) { return (cg_w(v) * cg_g(v) + 1) * 32; }
+#define CG_HDR 128      // stage header bytes (int32): [0..W] slice offsets, [16..16+W] interface
+                        // ranges, [30] end-marker position, [31] chunk id (< 0: end marker)
+#define CG_MAXR 32      // max window runs per chunk (one per producer lane)
+#define CG_GAP 32       // column gaps up to this size are bridged inside one run
 
 struct CGParams {
     int64_t N, nslices, nchunks;
     const int64_t *slice_ptr;
     const int32_t *col;
+    const uint16_t *lcol;      // KIND 2: chunk-local 16-bit columns (same layout as col)
     const double *val;
     const double *ML, *benv, *Dinv;
     int n_if, nA;
@@ -68,76 +70,92 @@ struct CGParams {
     double *relres_out, *area_out;
     double dt, rtol2;
     int maxit, step;
-    int stage_entries;   // TMA: entries per stage buffer
+    int stage_entries;         // TMA: matrix entries per stage
+    int nstages;               // TMA: ring stages (<= 8)
+    int win_cap;               // KIND 2: window entries per vector per stage
     const int32_t *chunk_hi;   // TMA: largest column index referenced by each chunk
-    int *chunk_ctr;            // TMA: two chunk-claim counters (zero between launches)
-    const double *pf[4];       // TMA: vectors whose leading edge is prefetched into L2
+    const int2 *chunk_runs;    // KIND 2: [nchunks][CG_MAXR] (start, length) of the window runs
+    const int32_t *chunk_nruns;
+    const int32_t *chunk_lown;  // KIND 2: window-local index of the chunk's first row
+    const double *pf[4];       // vectors whose leading edge is prefetched into L2
     int npf;
+    const double *wv[2];       // KIND 2: vectors staged through the window
+    int nwv;
+    unsigned long long *trace; // optional: %globaltimer after every grid barrier (CTA 0)
 };
 
-// Prefetch into L2 the leading edge of the column window of a chunk: rows
-// [hi - len + 1, hi] of each vector in pf (len = rows of the chunk, clamped, 16-B aligned).
-template <int CG_W>
-__device__ __forceinline__ void prefetch_edge(const CGParams &P, int64_t ch) {
-    if (ch >= P.nchunks) return;
-    const int64_t rows = (int64_t)CG_W * 32;
-    int64_t hi = (int64_t)P.chunk_hi[ch] + 1;
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Prefetch into L2 the leading edge of the column window of a chunk whose largest column
+// index is hi_col: rows [hi_col - len + 1, hi_col] of each vector in pf (len = rows of the
+// chunk, 16-B aligned).  hi_col < 0: nothing.
+template <int W>
+__device__ __forceinline__ void prefetch_edge(const CGParams &P, int hi_col) {
+    if (hi_col < 0) return;
+    const int64_t rows = (int64_t)W * 32;
+    int64_t hi = (int64_t)hi_col + 1;
     int64_t lo = hi - rows;
     if (lo < 0) lo = 0;
     lo &= ~(int64_t)1;
     hi = (hi + 1) & ~(int64_t)1;
     if (hi > P.N) hi = P.N & ~(int64_t)1;
     if (hi <= lo) return;
-    for (int v = 0; v < P.npf; ++v) bulk_prefetch_l2(P.pf[v] + lo, (uint32_t)((hi - lo) * 8));
+#pragma unroll
+    for (int v = 0; v < 4; ++v)
+        if (v < P.npf) bulk_prefetch_l2(P.pf[v] + lo, (uint32_t)((hi - lo) * 8));
 }
 
-// sum_k val * (x1[col] + beta * x2[col]) over one sliced-ELL row (entries at stride 32).
-// kSmem: the slice lives in shared memory (TMA ring); else in global memory (streamed).
-template <bool kSmem, bool kTwo>
-__device__ __forceinline__ double row_dot(const int32_t *cp, const double *vp, int w, const double *x1,
-                                          const double *x2, double beta, uint64_t pol) {
-    constexpr int B = kSmem ? 16 : 8;   // gathers issued together
-    double acc = 0.0;
-    int k = 0;
-    for (; k + B <= w; k += B) {
-        int c[B];
-        double v[B], y[B];
-#pragma unroll
-        for (int u = 0; u < B; ++u) c[u] = kSmem ? cp[32 * (k + u)] : ld_stream(cp + 32 * (k + u), pol);
-#pragma unroll
-        for (int u = 0; u < B; ++u) y[u] = x1[c[u]];
-        if (kTwo) {
-#pragma unroll
-            for (int u = 0; u < B; ++u) y[u] = fma(beta, x2[c[u]], y[u]);
-        }
-#pragma unroll
-        for (int u = 0; u < B; ++u) v[u] = kSmem ? vp[32 * (k + u)] : ld_stream(vp + 32 * (k + u), pol);
-#pragma unroll
-        for (int u = 0; u < B; ++u) acc = fma(v[u], y[u], acc);
+// Producer-side metadata of one chunk, loaded one chunk ahead of its use so that the
+// producer never waits on global-memory latency (lane l holds slice offset l, interface
+// range l and window run l).
+struct ChunkMeta {
+    int64_t ptr;
+    int sif, nruns, hi_own, hi_pf, lown;
+    int2 run;
+};
+
+template <int KIND, int W>
+__device__ __forceinline__ ChunkMeta load_meta(const CGParams &P, int64_t ch, int lane, int G) {
+    ChunkMeta m;
+    m.ptr = 0; m.sif = 0; m.nruns = 0; m.hi_own = -1; m.hi_pf = -1; m.lown = 0;
+    m.run = make_int2(0, 0);
+    if (ch >= P.nchunks) return m;
+    const int64_t s0 = ch * W, s1 = min(s0 + (int64_t)W, P.nslices);
+    const int64_t sl = min(s0 + lane, s1);
+    if (lane <= W) {
+        m.ptr = P.slice_ptr[sl];
+        m.sif = P.slice_if[sl];
     }
-    if (kSmem && k < w) {   // remainder: all loads first, then the ordered FMA chain
-        int c[B];
-        double y[B];
-#pragma unroll
-        for (int u = 0; u < B; ++u) c[u] = (k + u < w) ? cp[32 * (k + u)] : -1;
-#pragma unroll
-        for (int u = 0; u < B; ++u) {
-            y[u] = c[u] >= 0 ? x1[c[u]] : 0.0;
-            if (kTwo && c[u] >= 0) y[u] = fma(beta, x2[c[u]], y[u]);
-        }
-#pragma unroll
-        for (int u = 0; u < B; ++u)
-            if (k + u < w) acc = fma(vp[32 * (k + u)], y[u], acc);
-        return acc;
+    if (KIND == 2) {
+        m.nruns = P.chunk_nruns[ch];
+        m.lown = P.chunk_lown[ch];
+        m.run = P.chunk_runs[ch * CG_MAXR + lane];   // lanes >= nruns ignore theirs
     }
-    for (; k < w; ++k) {
-        const int c0 = kSmem ? cp[32 * k] : ld_stream(cp + 32 * k, pol);
-        double y0 = x1[c0];
-        if (kTwo) y0 = fma(beta, x2[c0], y0);
-        const double v0 = kSmem ? vp[32 * k] : ld_stream(vp + 32 * k, pol);
-        acc = fma(v0, y0, acc);
+    if (lane == 0) {
+        // leading edge of the column window two chunk waves ahead (and the chunk itself
+        // during the first waves)
+        if (ch < 2 * G) m.hi_own = P.chunk_hi[ch];
+        if (ch + 2 * G < P.nchunks) m.hi_pf = P.chunk_hi[ch + 2 * G];
     }
-    return acc;
+    return m;
+}
+
+// Interface index of the row owned by this lane (-1 if none), given the slice's range
+// [b, e) in if_rows.  Warp-uniform call.
+__device__ __forceinline__ int iface_index_r(const CGParams &P, int b, int e, int64_t i, int lane) {
+    if (b == e) return -1;
+    const int m = e - b;
+    const int mine = lane < m ? P.if_rows[b + lane] : -1;
+    int ik = -1;
+    for (int j = 0; j < m; ++j) {
+        int rj = __shfl_sync(0xffffffffu, mine, j);
+        if (rj == (int)i) ik = b + j;
+    }
+    return ik;
 }
 
 template <bool kTwo>
@@ -156,139 +174,257 @@ __device__ __forceinline__ double ell_row(const CGParams &P, int ik, const doubl
 }
 
 // ---------------------------------------------------------------------------------
-// slice sweep: calls body(s, cp, vp, w) for every slice owned by this warp, with the slice's
-// columns / values (already offset by the lane) either in the shared-memory ring (kTMA) or
-// in global memory.
+// row sources: sum_k val_k * (x1[col_k] + beta * x2[col_k]) over one sliced-ELL row whose
+// entries sit at stride 32.  All sources add in the same order (k ascending, fused
+// multiply-add), so the three kinds produce bitwise-identical row sums.
+// ---------------------------------------------------------------------------------
+struct SrcGlobal {   // KIND 0: matrix streamed from HBM, gathers from L1/L2
+    const int32_t *cp;
+    const double *vp;
+    uint64_t pol;
+    // own-row value of the first / second gathered vector
+    __device__ __forceinline__ double own1(const double *g, int64_t i) const { return g[i]; }
+    __device__ __forceinline__ double own2(const double *g, int64_t i) const { return g[i]; }
+    template <bool kTwo>
+    __device__ __forceinline__ double dot(int w, const double *x1, const double *x2, double beta) const {
+        double acc = 0.0;
+        int k = 0;
+        for (; k + 8 <= w; k += 8) {
+            int c[8];
+            double v[8], y[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) c[u] = ld_stream(cp + 32 * (k + u), pol);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) y[u] = kTwo ? fma(beta, x2[c[u]], x1[c[u]]) : x1[c[u]];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = ld_stream(vp + 32 * (k + u), pol);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc = fma(v[u], y[u], acc);
+        }
+        for (; k < w; ++k) {
+            const int c0 = ld_stream(cp + 32 * k, pol);
+            const double y0 = kTwo ? fma(beta, x2[c0], x1[c0]) : x1[c0];
+            acc = fma(ld_stream(vp + 32 * k, pol), y0, acc);
+        }
+        return acc;
+    }
+};
+
+struct SrcRing {     // KIND 1: matrix in the shared-memory ring, gathers from L1/L2
+    const int32_t *cp;
+    const double *vp;
+    __device__ __forceinline__ double own1(const double *g, int64_t i) const { return g[i]; }
+    __device__ __forceinline__ double own2(const double *g, int64_t i) const { return g[i]; }
+    template <bool kTwo>
+    __device__ __forceinline__ double dot(int w, const double *x1, const double *x2, double beta) const {
+        constexpr int B = 16;
+        double acc = 0.0;
+        for (int k = 0; k < w; k += B) {
+            int c[B];
+            double y[B];
+#pragma unroll
+            for (int u = 0; u < B; ++u) c[u] = (k + u < w) ? cp[32 * (k + u)] : -1;
+#pragma unroll
+            for (int u = 0; u < B; ++u) y[u] = c[u] >= 0 ? (kTwo ? fma(beta, x2[c[u]], x1[c[u]]) : x1[c[u]]) : 0.0;
+#pragma unroll
+            for (int u = 0; u < B; ++u)
+                if (k + u < w) acc = fma(vp[32 * (k + u)], y[u], acc);
+        }
+        return acc;
+    }
+};
+
+struct SrcWin {      // KIND 2: matrix and gathered vectors in shared memory
+    const uint16_t *lp;
+    const double *vp;
+    const double *w1, *w2;
+    int lown;            // window-local index of this lane's own row (the chunk's rows form
+                         // one contiguous block of its column set)
+    __device__ __forceinline__ double own1(const double *, int64_t) const { return w1[lown]; }
+    __device__ __forceinline__ double own2(const double *, int64_t) const { return w2[lown]; }
+    template <bool kTwo>
+    __device__ __forceinline__ double dot(int w, const double *, const double *, double beta) const {
+        double acc = 0.0;
+        int k = 0;
+        for (; k + 8 <= w; k += 8) {
+            int c[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) c[u] = lp[32 * (k + u)];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const double y = kTwo ? fma(beta, w2[c[u]], w1[c[u]]) : w1[c[u]];
+                acc = fma(vp[32 * (k + u)], y, acc);
+            }
+        }
+        for (; k < w; ++k) {
+            const int c0 = lp[32 * k];
+            const double y = kTwo ? fma(beta, w2[c0], w1[c0]) : w1[c0];
+            acc = fma(vp[32 * k], y, acc);
+        }
+        return acc;
+    }
+};
+
+// ---------------------------------------------------------------------------------
+// TMA ring
 // ---------------------------------------------------------------------------------
 struct Ring {
     uint64_t *full, *empty;
-    unsigned char *stage;   // CG_NS stages of [header | values | columns]
-    size_t stage_bytes;
-    uint32_t n;             // chunks passed through the ring so far (same count in every warp)
+    unsigned char *stage;   // NS stages of [header | values | columns | windows]
+    size_t stage_bytes, col_off, win_off;
+    uint32_t n;             // stages passed through the ring so far (same count in every warp)
 };
 
-// Interface index of the row owned by this lane (-1 if none), given the slice's range
-// [b, e) in if_rows.  Warp-uniform call.
-__device__ __forceinline__ int iface_index_r(const CGParams &P, int b, int e, int64_t i, int lane) {
-    if (b == e) return -1;
-    const int m = e - b;
-    const int mine = lane < m ? P.if_rows[b + lane] : -1;
-    int ik = -1;
-    for (int j = 0; j < m; ++j) {
-        int rj = __shfl_sync(0xffffffffu, mine, j);
-        if (rj == (int)i) ik = b + j;
-    }
-    return ik;
-}
+__host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
 
-// Chunk order (TMA variant): CTA b takes chunks b, b + G, b + 2G, ... (static, so that every
-// CTA's dot-product partial -- and hence every result bit -- is reproducible; dynamic claiming
-// from a global counter was measured slower and breaks determinism).  The chunk id travels in
-// the stage header; an id < 0 is the end marker (one per consumer group).
-template <bool kTMA, int V, class Body>
-__device__ __forceinline__ void sweep(const CGParams &P, Ring &R, int *ctr, Body &&body) {
-    constexpr int CG_W = cg_w(V), CG_G = cg_g(V), CG_NS = cg_ns(V);
+// Sweep over all slices: calls body(s, src, w, ib, ie) for every slice owned by this warp.
+// TMA kinds: CTA b takes chunks b, b + G, b + 2G, ... (static order: every CTA's dot-product
+// partial -- and so every result bit -- is reproducible); the chunk id travels in the stage
+// header; an id < 0 is the end marker (one per consumer group).
+template <int KIND, int W, int NG, class Body>
+__device__ __forceinline__ void sweep(const CGParams &P, Ring &R, Body &&body) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (kTMA) {
-        const int G = gridDim.x;
-        const int E = P.stage_entries;
-        if (warp == CG_W * CG_G) {   // producer warp
-            const uint64_t pol = policy_evict_first();
-            int64_t next = blockIdx.x;   // static grid-stride order: deterministic partials
-            while (true) {
-                const uint32_t st = R.n % CG_NS, ph = (R.n / CG_NS) & 1u;
-                const int64_t ch = next;
-                next += G;
-                if (ch >= P.nchunks) {   // end markers for every consumer group
-                    const uint32_t m0 = R.n;
-                    for (int q = 0; q < CG_G; ++q) {
-                        const uint32_t sq = R.n % CG_NS, pq = (R.n / CG_NS) & 1u;
-                        if (lane == 0) {
-                            mbar_wait(&R.empty[sq], pq ^ 1u);
-                            int *hdr = reinterpret_cast<int *>(R.stage + (size_t)sq * R.stage_bytes);
-                            hdr[31] = -1;
-                            hdr[30] = (int)m0;
-                            mbar_arrive(&R.full[sq]);
-                        }
-                        __syncwarp();
-                        ++R.n;
-                    }
-                    break;
-                }
-                const int64_t s0 = ch * CG_W, s1 = min(s0 + (int64_t)CG_W, P.nslices);
-                const int64_t sl = min(s0 + lane, s1);
-                const int64_t ptr = lane <= CG_W ? P.slice_ptr[sl] : 0;
-                const int sif = lane <= CG_W ? P.slice_if[sl] : 0;
-                const int64_t e0 = __shfl_sync(0xffffffffu, ptr, 0);
-                const int64_t e1 = __shfl_sync(0xffffffffu, ptr, CG_W);
-                if (lane == 0) mbar_wait(&R.empty[st], ph ^ 1u);
-                __syncwarp();
-                unsigned char *sb = R.stage + (size_t)st * R.stage_bytes;
-                int *hdr = reinterpret_cast<int *>(sb);
-                if (lane <= CG_W) {
-                    hdr[lane] = (int)(ptr - e0);
-                    hdr[16 + lane] = sif;
-                }
-                if (lane == 0) hdr[31] = (int)ch;
-                __syncwarp();
-                if (lane == 0) {
-                    // leading edge of the column window two claim rounds ahead (and the
-                    // current chunk during the first rounds)
-                    if (ch < 2 * G) prefetch_edge<CG_W>(P, ch);
-                    prefetch_edge<CG_W>(P, ch + 2 * G);
-                    const uint32_t cnt = (uint32_t)(e1 - e0);
-                    double *vals = reinterpret_cast<double *>(sb + CG_HDR);
-                    int32_t *cols = reinterpret_cast<int32_t *>(vals + E);
-                    mbar_arrive_expect_tx(&R.full[st], cnt * 12u);
-                    bulk_g2s(vals, P.val + e0, cnt * 8u, &R.full[st], pol);
-                    bulk_g2s(cols, P.col + e0, cnt * 4u, &R.full[st], pol);
-                }
-                __syncwarp();
-                ++R.n;
-            }
-        } else {                     // consumer warps: group g takes every CG_G-th stage
-            const int g = warp / CG_W, wg = warp % CG_W;
-            while (true) {
-                const uint32_t st = R.n % CG_NS, ph = (R.n / CG_NS) & 1u;
-                if ((int)(R.n % CG_G) == g) {
-                    mbar_wait(&R.full[st], ph);
-                    const unsigned char *sb = R.stage + (size_t)st * R.stage_bytes;
-                    const int *hdr = reinterpret_cast<const int *>(sb);
-                    const int ch = hdr[31];
-                    if (ch < 0) {
-                        const uint32_t m0 = (uint32_t)hdr[30];
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive(&R.empty[st]);
-                        R.n = m0 + CG_G;
-                        break;
-                    }
-                    const int64_t s = (int64_t)ch * CG_W + wg;
-                    if (s < P.nslices) {
-                        const double *vals = reinterpret_cast<const double *>(sb + CG_HDR);
-                        const int32_t *cols = reinterpret_cast<const int32_t *>(vals + E);
-                        const int o0 = hdr[wg], o1 = hdr[wg + 1];
-                        body(s, cols + o0 + lane, vals + o0 + lane, (o1 - o0) >> 5, hdr[16 + wg], hdr[17 + wg]);
-                    }
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&R.empty[st]);
-                }
-                ++R.n;
-            }
-        }
-    } else {
+    const uint32_t NS = (uint32_t)P.nstages;
+    if (KIND == 0) {
         const int nw = blockDim.x >> 5;
         const int gw = blockIdx.x * nw + warp;
         const int TW = gridDim.x * nw;
+        const uint64_t pol = policy_evict_first();
         for (int64_t s = gw; s < P.nslices; s += TW) {
             const int64_t b0 = P.slice_ptr[s], b1 = P.slice_ptr[s + 1];
-            body(s, P.col + b0 + lane, P.val + b0 + lane, (int)((b1 - b0) >> 5), P.slice_if[s], P.slice_if[s + 1]);
+            SrcGlobal src{P.col + b0 + lane, P.val + b0 + lane, pol};
+            body(s, src, (int)((b1 - b0) >> 5), P.slice_if[s], P.slice_if[s + 1]);
         }
+        return;
+    }
+    const int G = gridDim.x;
+    if (warp == W * NG) {   // ---------------- producer warp
+        const uint64_t pol = policy_evict_first();
+        int64_t ch = blockIdx.x;
+        // metadata pipeline: chunk ch + d*G was requested d iterations ago (d = 1, 2)
+        ChunkMeta cur = load_meta<KIND, W>(P, ch, lane, G);
+        ChunkMeta m1 = load_meta<KIND, W>(P, ch + G, lane, G);
+        ChunkMeta m2 = load_meta<KIND, W>(P, ch + 2 * G, lane, G);
+        while (true) {
+            const uint32_t st = R.n % NS, ph = (R.n / NS) & 1u;
+            if (ch >= P.nchunks) {   // end markers for every consumer group
+                const uint32_t m0 = R.n;
+                for (int q = 0; q < NG; ++q) {
+                    const uint32_t sq = R.n % NS, pq = (R.n / NS) & 1u;
+                    if (lane == 0) {
+                        mbar_wait(&R.empty[sq], pq ^ 1u);
+                        int *hdr = reinterpret_cast<int *>(R.stage + (size_t)sq * R.stage_bytes);
+                        hdr[31] = -1;
+                        hdr[30] = (int)m0;
+                        mbar_arrive(&R.full[sq]);
+                    }
+                    __syncwarp();
+                    ++R.n;
+                }
+                break;
+            }
+            const ChunkMeta m3 = load_meta<KIND, W>(P, ch + 3 * G, lane, G);   // in flight meanwhile
+            const int nruns = KIND == 2 ? (lane < cur.nruns ? 1 : 0) : 0;
+            int woff = 0, wtot = 0;
+            if (KIND == 2) {   // exclusive scan of the run lengths -> window offsets
+                const int len = nruns ? cur.run.y : 0;
+                int x = len;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, x, o);
+                    if (lane >= o) x += y;
+                }
+                woff = x - len;
+                wtot = __shfl_sync(0xffffffffu, x, 31);
+            }
+            const int64_t e0 = __shfl_sync(0xffffffffu, cur.ptr, 0);
+            const int64_t e1 = __shfl_sync(0xffffffffu, cur.ptr, W);
+            if (lane == 0) mbar_wait(&R.empty[st], ph ^ 1u);
+            __syncwarp();
+            unsigned char *sb = R.stage + (size_t)st * R.stage_bytes;
+            int *hdr = reinterpret_cast<int *>(sb);
+            if (lane <= W) {
+                hdr[lane] = (int)(cur.ptr - e0);
+                hdr[16 + lane] = cur.sif;
+            }
+            if (lane == 0) {
+                hdr[31] = (int)ch;
+                hdr[29] = cur.lown;
+            }
+            const uint32_t cnt = (uint32_t)(e1 - e0);
+            __syncwarp();
+            if (lane == 0) {
+                const uint32_t cbytes = KIND == 2 ? cnt * 2u : cnt * 4u;
+                const uint32_t wbytes = KIND == 2 ? (uint32_t)P.nwv * (uint32_t)wtot * 8u : 0u;
+                mbar_arrive_expect_tx(&R.full[st], cnt * 8u + cbytes + wbytes);
+                bulk_g2s(sb + CG_HDR, P.val + e0, cnt * 8u, &R.full[st], pol);
+                if (KIND == 2) bulk_g2s(sb + R.col_off, P.lcol + e0, cbytes, &R.full[st], pol);
+                else bulk_g2s(sb + R.col_off, P.col + e0, cbytes, &R.full[st], pol);
+            }
+            __syncwarp();
+            if (KIND == 2 && nruns) {
+#pragma unroll
+                for (int v = 0; v < 2; ++v)
+                    if (v < P.nwv)
+                        bulk_g2s_nohint(sb + R.win_off + ((size_t)v * P.win_cap + woff) * 8, P.wv[v] + cur.run.x,
+                                        (uint32_t)cur.run.y * 8u, &R.full[st]);
+            }
+            if (lane == 0) {
+                prefetch_edge<W>(P, cur.hi_own);
+                prefetch_edge<W>(P, cur.hi_pf);
+            }
+            __syncwarp();
+            ++R.n;
+            ch += G;
+            cur = m1;
+            m1 = m2;
+            m2 = m3;
+        }
+        return;
+    }
+    // ---------------- consumer warps: group g takes every NG-th stage
+    const int g = warp / W, wg = warp % W;
+    while (true) {
+        const uint32_t st = R.n % NS, ph = (R.n / NS) & 1u;
+        if ((int)(R.n % NG) == g) {
+            mbar_wait(&R.full[st], ph);
+            const unsigned char *sb = R.stage + (size_t)st * R.stage_bytes;
+            const int *hdr = reinterpret_cast<const int *>(sb);
+            const int ch = hdr[31];
+            if (ch < 0) {
+                const uint32_t m0 = (uint32_t)hdr[30];
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&R.empty[st]);
+                R.n = m0 + NG;
+                break;
+            }
+            const int64_t s = (int64_t)ch * W + wg;
+            if (s < P.nslices) {
+                const double *vals = reinterpret_cast<const double *>(sb + CG_HDR);
+                const int o0 = hdr[wg], o1 = hdr[wg + 1];
+                if (KIND == 2) {
+                    const uint16_t *lc = reinterpret_cast<const uint16_t *>(sb + R.col_off);
+                    const double *w1 = reinterpret_cast<const double *>(sb + R.win_off);
+                    SrcWin src{lc + o0 + lane, vals + o0 + lane, w1, w1 + P.win_cap, hdr[29] + 32 * wg + lane};
+                    body(s, src, (o1 - o0) >> 5, hdr[16 + wg], hdr[17 + wg]);
+                } else {
+                    const int32_t *cols = reinterpret_cast<const int32_t *>(sb + R.col_off);
+                    SrcRing src{cols + o0 + lane, vals + o0 + lane};
+                    body(s, src, (o1 - o0) >> 5, hdr[16 + wg], hdr[17 + wg]);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&R.empty[st]);
+        }
+        ++R.n;
     }
 }
 
-template <bool kTMA, int V>
-__global__ void __launch_bounds__(kTMA ? cg_threads(V) : THERMO_BLOCK, kTMA ? 1 : 2) k_cg_step(CGParams P) {
-    constexpr int CG_W = cg_w(V), CG_NS = cg_ns(V);
+__host__ __device__ constexpr int cg_threads(int kind, int W, int NG) { return kind == 0 ? THERMO_BLOCK : (W * NG + 1) * 32; }
+
+template <int KIND, int W, int NG>
+__global__ void __launch_bounds__(cg_threads(KIND, W, NG), KIND == 0 ? 2 : 1) k_cg_step(CGParams P) {
+    const int NS = P.nstages;
     __shared__ double red_smem[THERMO_RED_SMEM];
     extern __shared__ __align__(128) unsigned char ring_raw[];
     if (P.status[0] || P.status[1]) {   // an earlier step failed or the interface overflowed
@@ -302,43 +438,50 @@ __global__ void __launch_bounds__(kTMA ? cg_threads(V) : THERMO_BLOCK, kTMA ? 1 
     const int lane = threadIdx.x & 31;
     const int G = gridDim.x;
     const int64_t N = P.N;
-    constexpr bool kSmem = kTMA;
 
     Ring R;
     R.n = 0;
-    if (kTMA) {
+    if (KIND != 0) {
         R.full = reinterpret_cast<uint64_t *>(ring_raw);
-        R.empty = R.full + CG_NS;
+        R.empty = R.full + NS;
         R.stage = ring_raw + 128;
-        R.stage_bytes = CG_HDR + (size_t)P.stage_entries * 12;
+        R.col_off = CG_HDR + (size_t)P.stage_entries * 8;
+        R.win_off = align16(R.col_off + (size_t)P.stage_entries * (KIND == 2 ? 2 : 4));
+        R.stage_bytes = align16(R.win_off + (KIND == 2 ? (size_t)2 * P.win_cap * 8 : 0));
         if (threadIdx.x == 0) {
-            for (int s = 0; s < CG_NS; ++s) {
+            for (int s = 0; s < NS; ++s) {
                 mbar_init(&R.full[s], 1);
-                mbar_init(&R.empty[s], CG_W);
+                mbar_init(&R.empty[s], W);
             }
             fence_mbar_init();
         }
         __syncthreads();
     }
-    const uint64_t pol = kTMA ? 0ull : policy_evict_first();
 
     // ---- r0 = b - K~ x0 with x0 = T^n, b = M_L T^n + dt (b_env + b_G); z0 = D^{-1} r0
+    const bool tr_on = P.trace && blockIdx.x == 0 && threadIdx.x == 0;
+    int ntr = 0;
+    if (tr_on) P.trace[ntr++] = gtimer();
     double red0[4] = {0.0, 0.0, 0.0, 0.0};   // b.b, r.r, r.z, |Gamma_R|
     P.pf[0] = P.T_in; P.pf[1] = P.ML; P.pf[2] = P.benv; P.pf[3] = P.Dinv;
     P.npf = 4;
-    int sw = 0;   // sweep counter: sweep sw claims chunks from P.chunk_ctr[sw & 1]
-    sweep<kTMA, V>(P, R, P.chunk_ctr + (sw & 1), [&](int64_t s, const int32_t *cp, const double *vp, int w, int ib, int ie) {
+    P.wv[0] = P.T_in;
+    P.nwv = 1;
+    sweep<KIND, W, NG>(P, R, [&](int64_t s, const auto &src, int w, int ib, int ie) {
         const int64_t i = 32 * s + lane;
+        const int64_t ii = i < N ? i : N - 1;
+        // own-row loads first: their latency overlaps the row sum
+        const double be = P.benv[ii], ml = P.ML[ii], di = P.Dinv[ii];
+        const double Ti = src.own1(P.T_in, ii);
         const int ik = iface_index_r(P, ib, ie, i, lane);
-        double ax = row_dot<kSmem, false>(cp, vp, w, P.T_in, nullptr, 0.0, pol);
+        double ax = src.template dot<false>(w, P.T_in, nullptr, 0.0);
         if (ik >= 0) ax += ell_row<false>(P, ik, P.T_in, nullptr, 0.0);
         if (i < N) {
-            const double Ti = P.T_in[i];
-            double bi = P.benv[i];
+            double bi = be;
             if (ik >= 0) bi += P.if_b[ik];
-            bi = fma(P.ML[i], Ti, P.dt * bi);
+            bi = fma(ml, Ti, P.dt * bi);
             const double r = bi - ax;
-            const double zi = P.Dinv[i] * r;
+            const double zi = di * r;
             P.z[i] = zi;
             red0[0] = fma(bi, bi, red0[0]);
             red0[1] = fma(r, r, red0[1]);
@@ -348,8 +491,7 @@ __global__ void __launch_bounds__(kTMA ? cg_threads(V) : THERMO_BLOCK, kTMA ? 1 
     });
     cta_reduce_store<4>(red0, red_smem, P.partials, 0);
     grid.sync();
-    if (blockIdx.x == 0 && threadIdx.x == 0) P.chunk_ctr[sw & 1] = 0;   // next used after >= 1 more barrier
-    ++sw;
+    if (tr_on) P.trace[ntr++] = gtimer();
     double tot0[4];
     grid_total<4>(P.partials, G, 0, red_smem, tot0);
     const double tol2 = P.rtol2 * tot0[0];
@@ -367,19 +509,24 @@ __global__ void __launch_bounds__(kTMA ? cg_threads(V) : THERMO_BLOCK, kTMA ? 1 
         const bool first = it == 0;
         P.pf[0] = P.z; P.pf[1] = pold;
         P.npf = first ? 1 : 2;
-        sweep<kTMA, V>(P, R, P.chunk_ctr + (sw & 1), [&](int64_t s, const int32_t *cp, const double *vp, int w, int ib, int ie) {
+        P.wv[0] = P.z; P.wv[1] = pold;
+        P.nwv = first ? 1 : 2;
+        sweep<KIND, W, NG>(P, R, [&](int64_t s, const auto &src, int w, int ib, int ie) {
             const int64_t i = 32 * s + lane;
+            const int64_t ii = i < N ? i : N - 1;
+            const double zo = src.own1(P.z, ii);   // issued before the row sum
+            const double po = first ? 0.0 : src.own2(pold, ii);
             const int ik = iface_index_r(P, ib, ie, i, lane);
             double acc;
             if (first) {
-                acc = row_dot<kSmem, false>(cp, vp, w, P.z, nullptr, 0.0, pol);
+                acc = src.template dot<false>(w, P.z, nullptr, 0.0);
                 if (ik >= 0) acc += ell_row<false>(P, ik, P.z, nullptr, 0.0);
             } else {
-                acc = row_dot<kSmem, true>(cp, vp, w, P.z, pold, beta, pol);
+                acc = src.template dot<true>(w, P.z, pold, beta);
                 if (ik >= 0) acc += ell_row<true>(P, ik, P.z, pold, beta);
             }
             if (i < N) {
-                const double pi = first ? P.z[i] : fma(beta, pold[i], P.z[i]);
+                const double pi = first ? zo : fma(beta, po, zo);
                 pnew[i] = pi;
                 P.q[i] = acc;
                 pq[0] = fma(pi, acc, pq[0]);
@@ -387,8 +534,7 @@ __global__ void __launch_bounds__(kTMA ? cg_threads(V) : THERMO_BLOCK, kTMA ? 1 
         });
         cta_reduce_store<1>(pq, red_smem, P.partials, 4);
         grid.sync();
-        if (blockIdx.x == 0 && threadIdx.x == 0) P.chunk_ctr[sw & 1] = 0;
-        ++sw;
+        if (tr_on && ntr < 1000) P.trace[ntr++] = gtimer();
         double tpq[1];
         grid_total<1>(P.partials, G, 4, red_smem, tpq);
         const double alpha = rho / tpq[0];
@@ -417,15 +563,21 @@ __global__ void __launch_bounds__(kTMA ? cg_threads(V) : THERMO_BLOCK, kTMA ? 1 
                 red[0] = fma(r1, zo.y, red[0]);
                 red[1] = fma(r1, r1, red[1]);
             };
+            // UU element pairs per thread and trip, all loads issued before any use
+            constexpr int UU = KIND == 0 ? 2 : 4;
             int64_t j = tid;
-            for (; j + nthr < npair; j += 2 * nthr) {
-                const int64_t j2 = j + nthr;
-                const double2 pa = p2[j], pb = p2[j2], qa = q2[j], qb = q2[j2], da = d2[j], db = d2[j2];
-                const double2 xa = x2[j], xb = x2[j2], za = z2[j], zb = z2[j2];
-                upd(pa, qa, da, xa, za, j);
-                upd(pb, qb, db, xb, zb, j2);
+            for (; j + (UU - 1) * nthr < npair; j += UU * nthr) {
+                double2 pv[UU], qv[UU], dv[UU], xv[UU], zv[UU];
+#pragma unroll
+                for (int u = 0; u < UU; ++u) {
+                    const int64_t jj = j + u * nthr;
+                    pv[u] = ld_cg2(p2 + jj); qv[u] = ld_cg2(q2 + jj); dv[u] = ld_cg2(d2 + jj);
+                    xv[u] = ld_cg2(x2 + jj); zv[u] = ld_cg2(z2 + jj);
+                }
+#pragma unroll
+                for (int u = 0; u < UU; ++u) upd(pv[u], qv[u], dv[u], xv[u], zv[u], j + u * nthr);
             }
-            if (j < npair) upd(p2[j], q2[j], d2[j], x2[j], z2[j], j);
+            for (; j < npair; j += nthr) upd(p2[j], q2[j], d2[j], x2[j], z2[j], j);
             if ((N & 1) && tid == nthr - 1) {
                 const int64_t i = N - 1;
                 const double di = P.Dinv[i];
@@ -439,6 +591,7 @@ __global__ void __launch_bounds__(kTMA ? cg_threads(V) : THERMO_BLOCK, kTMA ? 1 
         }
         cta_reduce_store<2>(red, red_smem, P.partials, 5);
         grid.sync();
+        if (tr_on && ntr < 1000) P.trace[ntr++] = gtimer();
         double tr[2];
         grid_total<2>(P.partials, G, 5, red_smem, tr);
         beta = tr[0] / rho;
@@ -466,75 +619,208 @@ __global__ void __launch_bounds__(kTMA ? cg_threads(V) : THERMO_BLOCK, kTMA ? 1 
     }
 }
 
-// largest column index of every chunk of CG_W slices (warp per chunk)
+// ---------------------------------------------------------------------------------
+// setup
+// ---------------------------------------------------------------------------------
+
+// largest column index of every chunk of W slices (warp per chunk)
 __global__ void k_chunk_hi(const int64_t *slice_ptr, const int32_t *col, int64_t nslices, int64_t nchunks,
-                           int CG_W, int32_t *hi) {
+                           int W, int32_t *hi) {
     const int64_t ch = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (ch >= nchunks) return;
-    const int64_t s0 = ch * CG_W, s1 = min(s0 + (int64_t)CG_W, nslices);
+    const int64_t s0 = ch * W, s1 = min(s0 + (int64_t)W, nslices);
     int m = 0;
     for (int64_t e = slice_ptr[s0] + lane; e < slice_ptr[s1]; e += 32) m = max(m, col[e]);
     for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
     if (lane == 0) hi[ch] = m;
 }
 
-template <int V>
-static int setup_variant(Ctx &c, int *per_sm) {
-    CK(cudaFuncSetAttribute(k_cg_step<true, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.cg_smem));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_cg_step<true, V>, cg_threads(V), c.cg_smem));
-    return 0;
+// Column window of every chunk (block per chunk, KIND 2): the chunk's distinct columns,
+// sorted, cut into runs wherever a gap exceeds CG_GAP, runs widened to even bounds (16-byte
+// bulk copies); then every entry's chunk-local 16-bit column index.  stats[0] = max window,
+// stats[1] = max runs, stats[2] = overflow (window > 65535 or chunk > CW_MAXE entries).
+#define CW_MAXE 4096
+__global__ void __launch_bounds__(256) k_chunk_windows(const int64_t *slice_ptr, const int32_t *col,
+                                                       int64_t nslices, int W, int2 *runs_out,
+                                                       int32_t *nruns_out, int32_t *lown_out, uint16_t *lcol,
+                                                       int *stats) {
+    __shared__ int key[CW_MAXE];
+    __shared__ int rstart[CW_MAXE / 2 + 1], rlast[CW_MAXE / 2 + 1], roff[CW_MAXE / 2 + 2];
+    __shared__ int nr_s;
+    const int64_t ch = blockIdx.x;
+    const int64_t s0 = ch * W, s1 = min(s0 + (int64_t)W, nslices);
+    const int64_t e0 = slice_ptr[s0];
+    const int E = (int)(slice_ptr[s1] - e0);
+    if (E > CW_MAXE) {
+        if (threadIdx.x == 0) atomicOr(&stats[2], 1);
+        return;
+    }
+    int n2 = 1;
+    while (n2 < E) n2 <<= 1;
+    for (int e = threadIdx.x; e < n2; e += blockDim.x) key[e] = e < E ? col[e0 + e] : 0x7fffffff;
+    __syncthreads();
+    for (int size = 2; size <= n2; size <<= 1)
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int i = threadIdx.x; i < n2 / 2; i += blockDim.x) {
+                const int lo = 2 * stride * (i / stride) + (i % stride), hi = lo + stride;
+                const bool up = (lo & size) == 0;
+                const int a = key[lo], b = key[hi];
+                if ((a > b) == up) { key[lo] = b; key[hi] = a; }
+            }
+            __syncthreads();
+        }
+    if (threadIdx.x == 0) {   // runs (serial over <= 4096 sorted keys)
+        int nr = 0;
+        for (int j = 0; j < E; ++j) {
+            if (j == 0 || key[j] - key[j - 1] > CG_GAP + 1) {
+                rstart[nr] = key[j] & ~1;
+                if (nr > 0) rlast[nr - 1] = key[j - 1];
+                ++nr;
+            }
+        }
+        rlast[nr - 1] = key[E - 1];
+        roff[0] = 0;
+        for (int r = 0; r < nr; ++r) roff[r + 1] = roff[r] + (((rlast[r] + 2) & ~1) - rstart[r]);
+        nr_s = nr;
+        atomicMax(&stats[0], roff[nr]);
+        atomicMax(&stats[1], nr);
+        if (roff[nr] > 65535) atomicOr(&stats[2], 2);
+        nruns_out[ch] = nr;
+        // local index of the chunk's first row (its own rows are one contiguous block)
+        const int r0 = (int)(s0 * 32);
+        int lo = 0;
+        for (int r = 0; r < nr; ++r) if (rstart[r] <= r0) lo = r;
+        lown_out[ch] = roff[lo] + (r0 - rstart[lo]);
+        for (int r = 0; r < nr && r < CG_MAXR; ++r) runs_out[ch * CG_MAXR + r] = make_int2(rstart[r], roff[r + 1] - roff[r]);
+    }
+    __syncthreads();
+    const int nr = nr_s;
+    for (int e = threadIdx.x; e < E; e += blockDim.x) {
+        const int c = col[e0 + e];
+        int lo = 0, hi = nr - 1;
+        while (lo < hi) {   // last run with start <= c
+            const int mid = (lo + hi + 1) >> 1;
+            if (rstart[mid] <= c) lo = mid; else hi = mid - 1;
+        }
+        int lc = roff[lo] + (c - rstart[lo]);
+        if (c < rstart[lo] || c > rlast[lo] + 1) lc = 0;   // cannot happen: every column is in a run
+        lcol[e0 + e] = (uint16_t)lc;
+    }
+}
+
+struct Variant {
+    int kind, W, NG;
+};
+static const Variant kVariants[] = {{0, 8, 1}, {1, 8, 2}, {2, 8, 1}, {2, 8, 2}, {2, 6, 1}, {2, 6, 2}, {2, 4, 2}, {2, 4, 1}};
+#define CG_NVAR 8
+
+template <int KIND, int W, int NG>
+static const void *kernel_ptr() { return (const void *)k_cg_step<KIND, W, NG>; }
+
+static const void *variant_kernel(int v) {
+    switch (v) {
+        case 0: return kernel_ptr<0, 8, 1>();
+        case 1: return kernel_ptr<1, 8, 2>();
+        case 2: return kernel_ptr<2, 8, 1>();
+        case 3: return kernel_ptr<2, 8, 2>();
+        case 4: return kernel_ptr<2, 6, 1>();
+        case 5: return kernel_ptr<2, 6, 2>();
+        case 6: return kernel_ptr<2, 4, 2>();
+        default: return kernel_ptr<2, 4, 1>();
+    }
+}
+
+static size_t stage_bytes(const Variant &v, int E, int wc) {
+    size_t col_off = CG_HDR + (size_t)E * 8;
+    size_t win_off = align16(col_off + (size_t)E * (v.kind == 2 ? 2 : 4));
+    return align16(win_off + (v.kind == 2 ? (size_t)2 * wc * 8 : 0));
 }
 
 int cg_setup(Ctx &c) {
-    const char *env = getenv("THERMO_CG_PATH");   // testing hook: 0 = register path, 1 = TMA
-    const int force = env ? atoi(env) : -1;
-    const char *envv = getenv("THERMO_CG_VARIANT");
-    c.cg_variant = envv ? std::max(0, std::min(CG_NVARIANT - 1, atoi(envv))) : 0;
-    const int W = cg_w(c.cg_variant);
-    c.cg_chunk = W;
-    // largest chunk of W consecutive slices -> stage size of the TMA ring
+    const char *env = getenv("THERMO_CG_VARIANT");   // testing / tuning hook
+    int want = env ? atoi(env) : -1;
+    if (want >= CG_NVAR) want = -1;
     std::vector<int64_t> sp(c.nslices + 1);
     CK(cudaMemcpy(sp.data(), c.d_slice_ptr, sizeof(int64_t) * (c.nslices + 1), cudaMemcpyDeviceToHost));
-    int64_t emax = 0;
-    for (int64_t s0 = 0; s0 < c.nslices; s0 += W) {
-        const int64_t s1 = std::min<int64_t>(s0 + W, c.nslices);
-        emax = std::max(emax, sp[s1] - sp[s0]);
+    auto emax_for = [&](int W) {
+        int64_t m = 0;
+        for (int64_t s0 = 0; s0 < c.nslices; s0 += W) m = std::max(m, sp[std::min<int64_t>(s0 + W, c.nslices)] - sp[s0]);
+        return (int)((m + 31) / 32 * 32);
+    };
+    // candidate order: the requested variant, then the default preference
+    std::vector<int> order;
+    if (want >= 0) order.push_back(want);
+    for (int v : {2, 3, 4, 5, 6, 7, 1, 0}) if (v != want) order.push_back(v);
+    int chosen = -1, per_sm = 0;
+    for (int vi : order) {
+        const Variant &v = kVariants[vi];
+        const int E = emax_for(v.W);
+        const int64_t nchunks = (c.nslices + v.W - 1) / v.W;
+        int wc = 0;
+        if (v.kind == 2) {
+            if (E > CW_MAXE) continue;
+            // windows of every chunk (and the 16-bit local columns) for this chunk size
+            if (!c.d_lcol) CK(cudaMalloc(&c.d_lcol, sizeof(uint16_t) * (c.nnz_pad + 8)));
+            if (c.d_chunk_runs) { cudaFree(c.d_chunk_runs); cudaFree(c.d_chunk_nruns); }
+            CK(cudaMalloc(&c.d_chunk_runs, sizeof(int2) * nchunks * CG_MAXR));
+            CK(cudaMalloc(&c.d_chunk_nruns, sizeof(int32_t) * (nchunks + 1)));
+            if (c.d_chunk_lown) cudaFree(c.d_chunk_lown);
+            CK(cudaMalloc(&c.d_chunk_lown, sizeof(int32_t) * (nchunks + 1)));
+            int *d_stats = nullptr;
+            CK(cudaMalloc(&d_stats, sizeof(int) * 4));
+            CK(cudaMemsetAsync(d_stats, 0, sizeof(int) * 4, c.stream));
+            k_chunk_windows<<<(unsigned)nchunks, 256, 0, c.stream>>>(c.d_slice_ptr, c.d_col, c.nslices, v.W,
+                                                                    c.d_chunk_runs, c.d_chunk_nruns, c.d_chunk_lown,
+                                                                    c.d_lcol, d_stats);
+            CK(cudaGetLastError());
+            int stats[4];
+            CK(cudaMemcpyAsync(stats, d_stats, sizeof stats, cudaMemcpyDeviceToHost, c.stream));
+            CK(cudaStreamSynchronize(c.stream));
+            cudaFree(d_stats);
+            if (stats[2] || stats[1] > CG_MAXR) continue;
+            wc = (stats[0] + 1) & ~1;
+        }
+        const size_t sb = stage_bytes(v, E, wc);
+        const int ns = v.kind == 0 ? 1 : (int)std::min<size_t>(8, (210 * 1024 - 128) / sb);
+        if (v.kind != 0 && ns < v.NG + 1) continue;   // at least one stage in flight
+        const size_t smem = v.kind == 0 ? 0 : 128 + (size_t)ns * sb;
+        const void *fn = variant_kernel(vi);
+        if (smem > 48 * 1024) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, cg_threads(v.kind, v.W, v.NG), smem));
+        if (per_sm < 1) continue;
+        chosen = vi;
+        c.cg_smem = smem;
+        c.cg_stage_entries = E;
+        c.cg_win_cap = wc;
+        c.cg_chunk = v.W;
+        c.cg_block = cg_threads(v.kind, v.W, v.NG);
+        c.cg_nstages = ns;
+        break;
     }
-    c.cg_stage_entries = (int)((emax + 31) / 32 * 32);
-    c.cg_smem = 128 + (size_t)cg_ns(c.cg_variant) * (CG_HDR + (size_t)c.cg_stage_entries * 12);
-    c.cg_tma = c.cg_smem <= 220 * 1024 && force != 0;
-    int per_sm = 0;
-    if (c.cg_tma) {
-        int rc = c.cg_variant == 0 ? setup_variant<0>(c, &per_sm)
-                 : c.cg_variant == 1 ? setup_variant<1>(c, &per_sm) : setup_variant<2>(c, &per_sm);
-        if (rc) return rc;
-        c.cg_block = cg_threads(c.cg_variant);
-    } else {
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cg_step<false, 0>, THERMO_BLOCK, 0));
-        c.cg_block = THERMO_BLOCK;
-        c.cg_smem = 0;
-    }
-    if (per_sm < 1) { c.err = "CG kernel cannot be resident"; return -3; }
+    if (chosen < 0) { c.err = "no CG kernel variant can be resident"; return -3; }
+    c.cg_variant = chosen;
+    c.cg_tma = kVariants[chosen].kind != 0;
+    const int W = c.cg_chunk;
     const int64_t nchunks = (c.nslices + W - 1) / W;
     CK(cudaMalloc(&c.d_chunk_hi, sizeof(int32_t) * (nchunks + 1)));
-    CK(cudaMalloc(&c.d_chunk_ctr, sizeof(int) * 2));
-    CK(cudaMemsetAsync(c.d_chunk_ctr, 0, sizeof(int) * 2, c.stream));
     k_chunk_hi<<<(unsigned)((nchunks * 32 + 255) / 256), 256, 0, c.stream>>>(c.d_slice_ptr, c.d_col, c.nslices,
                                                                            nchunks, W, c.d_chunk_hi);
     CK(cudaGetLastError());
-    c.cg_grid = per_sm * c.num_sms;
+    c.cg_grid = (kVariants[chosen].kind == 0 ? per_sm : 1) * c.num_sms;
     CK(cudaMalloc(&c.d_partials, sizeof(double) * THERMO_NRED * c.cg_grid));
     return 0;
 }
 
 int cg_launch_step(Ctx &c, int step, double dt) {
     CGParams P;
+    memset(&P, 0, sizeof P);
     P.N = c.N;
     P.nslices = c.nslices;
     P.nchunks = (c.nslices + c.cg_chunk - 1) / c.cg_chunk;
     P.slice_ptr = c.d_slice_ptr;
     P.col = c.d_col;
+    P.lcol = c.d_lcol;
     P.val = c.d_val;
     P.ML = c.d_ML;
     P.benv = c.d_benv;
@@ -565,15 +851,16 @@ int cg_launch_step(Ctx &c, int step, double dt) {
     P.maxit = c.maxit > 0 ? c.maxit : (int)std::min<int64_t>(10 * c.N, 10000);
     P.step = step;
     P.stage_entries = c.cg_stage_entries;
+    P.nstages = c.cg_nstages;
+    P.win_cap = c.cg_win_cap;
     P.chunk_hi = c.d_chunk_hi;
-    P.chunk_ctr = c.d_chunk_ctr;
-    P.npf = 0;
+    P.chunk_runs = c.d_chunk_runs;
+    P.chunk_nruns = c.d_chunk_nruns;
+    P.chunk_lown = c.d_chunk_lown;
+    P.trace = c.d_trace;
     void *args[] = {&P};
-    const void *fn = !c.cg_tma ? (const void *)k_cg_step<false, 0>
-                     : c.cg_variant == 0 ? (const void *)k_cg_step<true, 0>
-                     : c.cg_variant == 1 ? (const void *)k_cg_step<true, 1>
-                                         : (const void *)k_cg_step<true, 2>;
-    CK(cudaLaunchCooperativeKernel(fn, dim3(c.cg_grid), dim3(c.cg_block), args, c.cg_tma ? c.cg_smem : 0, c.stream));
+    CK(cudaLaunchCooperativeKernel(variant_kernel(c.cg_variant), dim3(c.cg_grid), dim3(c.cg_block), args,
+                                   c.cg_smem, c.stream));
     return 0;
 }
 

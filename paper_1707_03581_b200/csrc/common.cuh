@@ -36,6 +36,15 @@ __device__ __forceinline__ int ld_stream(const int *p, uint64_t pol) {
     return v;
 }
 
+// Coherent load that bypasses L1 (cached in L2 only): streams that are read once per phase
+// but written by other CTAs earlier in the same kernel.  Keeps L1 miss slots free when most
+// of the shared memory is taken by a TMA ring.
+__device__ __forceinline__ double2 ld_cg2(const double2 *p) {
+    double2 v;
+    asm volatile("ld.global.cg.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return v;
+}
+
 // ---------------------------------------------------------------------------------
 // mbarrier + bulk-copy (TMA engine) helpers
 // ---------------------------------------------------------------------------------
@@ -75,6 +84,13 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
             smem_u32(dst)),
         "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
         : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s_nohint(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
 }
 
 // L2 prefetch of a contiguous range on the TMA engine (16-byte aligned, size % 16 == 0)

@@ -93,6 +93,12 @@ struct Ctx {
     bool cg_tma = false;
     int cg_variant = 0, cg_chunk = 8;
     int32_t *d_chunk_hi = nullptr;
+    uint16_t *d_lcol = nullptr;      // chunk-local 16-bit columns (window kernels)
+    int2 *d_chunk_runs = nullptr;    // window runs per chunk
+    int32_t *d_chunk_nruns = nullptr;
+    int32_t *d_chunk_lown = nullptr;
+    unsigned long long *d_trace = nullptr;   // THERMO_CG_TRACE=1: barrier timestamps of the last solve
+    int cg_win_cap = 0, cg_nstages = 1;
     int *d_chunk_ctr = nullptr;
 
     double rtol = 1e-12;

@@ -41,7 +41,8 @@ static void free_ctx(Ctx *c) {
                     c->d_binB_ptr, c->d_binB_ids, c->d_slice_if, c->d_ell_cnt, c->d_ell_col, c->d_ell_val,
                     c->d_if_b, c->d_if_phi, c->d_if_dinv, c->d_T[0], c->d_T[1], c->d_z, c->d_p[0], c->d_p[1],
                     c->d_q, c->d_partials, c->d_status, c->d_fail_relres, c->d_step_sc, c->d_iters,
-                    c->d_relres, c->d_area, c->d_pairs, c->d_pcnt, c->d_chunk_hi, c->d_chunk_ctr};
+                    c->d_relres, c->d_area, c->d_pairs, c->d_pcnt, c->d_chunk_hi, c->d_chunk_ctr, c->d_lcol, c->d_chunk_runs,
+                    c->d_chunk_nruns, c->d_chunk_lown, c->d_trace};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     for (cudaEvent_t e : c->events) cudaEventDestroy(e);
@@ -153,8 +154,11 @@ extern "C" int thermo_create_mesh(void **out, const thermo_mesh *fixed, const th
         // state and workspace
         const int64_t NS = N * c->S;
         bool ok = true;
-        for (double **p : {&c->d_T[0], &c->d_T[1], &c->d_z, &c->d_p[0], &c->d_p[1], &c->d_q})
-            ok &= cudaMalloc(p, sizeof(double) * NS) == cudaSuccess;
+        // vectors padded by 16 entries: window bulk copies may read up to one element past N
+        for (double **p : {&c->d_T[0], &c->d_T[1], &c->d_z, &c->d_p[0], &c->d_p[1], &c->d_q}) {
+            ok &= cudaMalloc(p, sizeof(double) * (NS + 16)) == cudaSuccess;
+            if (ok) cudaMemsetAsync(*p, 0, sizeof(double) * (NS + 16), c->stream);
+        }
         ok &= cudaMalloc(&c->d_status, sizeof(int) * 8) == cudaSuccess;
         ok &= cudaMalloc(&c->d_fail_relres, sizeof(double)) == cudaSuccess;
         if (!ok) { g_create_err = "device allocation failed"; free_ctx(c); return THERMO_ENOMEM; }
@@ -164,6 +168,10 @@ extern "C" int thermo_create_mesh(void **out, const thermo_mesh *fixed, const th
         cudaMemsetAsync(c->d_status, 0, sizeof(int) * 8, c->stream);
         rc = thermo::assemble_robin(*c);
         if (!rc) rc = thermo::cg_setup(*c);
+        if (!rc && getenv("THERMO_CG_TRACE")) {
+            if (cudaMalloc(&c->d_trace, sizeof(unsigned long long) * 1024) != cudaSuccess) rc = -3;
+            else cudaMemsetAsync(c->d_trace, 0, sizeof(unsigned long long) * 1024, c->stream);
+        }
         if (!rc && cudaStreamSynchronize(c->stream) != cudaSuccess) { c->err = "CUDA error during create"; rc = -3; }
         if (rc) { g_create_err = c->err; free_ctx(c); return THERMO_ECUDA; }
         *out = c;
@@ -311,6 +319,18 @@ extern "C" int thermo_step(void *ctx, double t, double dt, int32_t nsteps) {
             char buf[160];
             snprintf(buf, sizeof buf, "CG did not converge at step %d (scenario %d), relres %.3e", f, status[3], frel);
             return fail(c, THERMO_ENOCONV, buf);
+        }
+        if (c->d_trace) {   // phase split of the last solve (debug aid)
+            unsigned long long tr[1024];
+            API_CK(cudaMemcpy(tr, c->d_trace, sizeof tr, cudaMemcpyDeviceToHost));
+            const int it = c->h_iters[(size_t)(nsteps - 1) * S];
+            double s_ns = 0, u_ns = 0;
+            for (int k = 0; k < it && 2 + 2 * k + 1 < 1024; ++k) {
+                s_ns += (double)(tr[2 + 2 * k] - tr[1 + 2 * k]);
+                u_ns += (double)(tr[3 + 2 * k] - tr[2 + 2 * k]);
+            }
+            fprintf(stderr, "[thermo trace] phase0 %.1f us, S %.1f us/iter, U %.1f us/iter (%d iters)\n",
+                    (tr[1] - tr[0]) * 1e-3, s_ns * 1e-3 / it, u_ns * 1e-3 / it, it);
         }
         c->failed_step = -1;
         c->failed_scen = -1;
