@@ -1,0 +1,426 @@
+// cg_batched.cu -- S independent scenarios advanced together (BASELINE.json config 4,
+// SURVEY 8(a) a5): the implicit-Euler solve of every scenario by Jacobi-PCG with per-column
+// alpha, beta and convergence mask, the shared volume operator applied as an SpMM.
+//
+// Layout: every state / workspace vector is an N x SP row-major block (SP even, >= S); lane l
+// of a warp owns the columns 2l, 2l+1 of every row it touches, so one row of a block vector is
+// one coalesced 512-byte access for S = 64.  Per-scenario pieces: the interface rows (ELL,
+// [k][c][s]), the friction source, and the Jacobi diagonal DinvS[N][SP] (volume diagonal,
+// interface rows rewritten per step by the interface kernels).
+//
+// Per CG iteration (same z-primary schedule as cg.cu, column-wise):
+//   S: p = z + beta p_old on the fly, q = K~ p (warp per slice, rows in turn: the row's entries
+//      are broadcast by shuffles, every lane gathers its two columns), partial p.q per column
+//   U: x += alpha p, z -= alpha D^{-1} q, partial r.z, r.r per column
+// Converged columns are frozen (alpha = 0).  Reductions are deterministic: lanes own columns,
+// warps combine in fixed order, CTAs in fixed order; every CTA computes identical scalars.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "ctx.h"
+
+namespace cg = cooperative_groups;
+
+namespace thermo {
+
+#define CK(x)                                                                    \
+    do {                                                                         \
+        cudaError_t e_ = (x);                                                    \
+        if (e_ != cudaSuccess) {                                                 \
+            c.err = std::string("CUDA: ") + cudaGetErrorString(e_) + " at " #x; \
+            return -3;                                                           \
+        }                                                                        \
+    } while (0)
+
+#define CGB_BLOCK 256
+#define CGB_WARPS (CGB_BLOCK / 32)
+#define CGB_MAXS 64
+#define CGB_NV 4   // reduction values per column and phase (max)
+
+struct CGBParams {
+    int64_t N, nslices;
+    int S, SP;
+    const int64_t *slice_ptr;
+    const int32_t *col;
+    const double *val;
+    const double *ML, *benv, *DinvS;
+    int n_if, nA, cap;
+    const int32_t *if_rows, *slice_if, *ell_cnt, *ell_col;
+    const double *ell_val, *if_b, *if_phi;
+    const double *T_in;
+    double *T_out, *z, *pa, *pb, *q;
+    double *partials;   // [G][CGB_NV][64]
+    int *status;
+    double *fail_relres;
+    int32_t *iters_out;
+    double *relres_out, *area_out;
+    double dt, rtol2;
+    int maxit, step;
+};
+
+__device__ __forceinline__ int64_t ellb(const CGBParams &P, int s, int c, int k) {
+    return ((int64_t)k * P.cap + c) * P.S + s;
+}
+
+// CTA + grid reduction of NV values per column (lanes own columns 2l, 2l+1).
+template <int NV>
+__device__ __forceinline__ void cgb_reduce(double (&v)[NV][2], double *sm, double *partials, cg::grid_group &grid,
+                                           double (&out)[NV][2]) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+        sm[(warp * NV + j) * 64 + 2 * lane] = v[j][0];
+        sm[(warp * NV + j) * 64 + 2 * lane + 1] = v[j][1];
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < NV * 64; t += blockDim.x) {
+        double a = 0.0;
+        for (int w = 0; w < CGB_WARPS; ++w) a += sm[w * NV * 64 + t];
+        partials[(int64_t)blockIdx.x * CGB_NV * 64 + t] = a;
+    }
+    grid.sync();
+    for (int t = threadIdx.x; t < NV * 64; t += blockDim.x) {
+        double a = 0.0;
+        for (int g = 0; g < (int)gridDim.x; ++g) a += partials[(int64_t)g * CGB_NV * 64 + t];
+        sm[t] = a;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+        out[j][0] = sm[j * 64 + 2 * lane];
+        out[j][1] = sm[j * 64 + 2 * lane + 1];
+    }
+    __syncthreads();
+}
+
+// Row sum of the shared volume operator applied to the lane's two columns of
+// y = x1 + beta x2 (beta per column; kTwo = false: y = x1).  Entries of row r of slice s sit
+// at base + 32 k + r; lane k loads entry k, the warp broadcasts it.
+template <bool kTwo>
+__device__ __forceinline__ double2 row_spmm(const CGBParams &P, int64_t base, int w, int r, const double *x1,
+                                            const double *x2, double2 beta, int lane) {
+    double2 acc = make_double2(0.0, 0.0);
+    for (int k0 = 0; k0 < w; k0 += 32) {
+        const int kk = k0 + lane;
+        int cl = 0;
+        double vl = 0.0;
+        if (kk < w) {
+            cl = P.col[base + 32 * (int64_t)kk + r];
+            vl = P.val[base + 32 * (int64_t)kk + r];
+        }
+        const int m = min(32, w - k0);
+        int k = 0;
+        for (; k + 8 <= m; k += 8) {
+            double2 y[8];
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int c = __shfl_sync(0xffffffffu, cl, k + u);
+                v[u] = __shfl_sync(0xffffffffu, vl, k + u);
+                const double2 a = reinterpret_cast<const double2 *>(x1 + (int64_t)c * P.SP)[lane];
+                if (kTwo) {
+                    const double2 b = reinterpret_cast<const double2 *>(x2 + (int64_t)c * P.SP)[lane];
+                    y[u] = make_double2(fma(beta.x, b.x, a.x), fma(beta.y, b.y, a.y));
+                } else {
+                    y[u] = a;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                acc.x = fma(v[u], y[u].x, acc.x);
+                acc.y = fma(v[u], y[u].y, acc.y);
+            }
+        }
+        for (; k < m; ++k) {
+            const int c = __shfl_sync(0xffffffffu, cl, k);
+            const double v = __shfl_sync(0xffffffffu, vl, k);
+            const double2 a = reinterpret_cast<const double2 *>(x1 + (int64_t)c * P.SP)[lane];
+            double2 y = a;
+            if (kTwo) {
+                const double2 b = reinterpret_cast<const double2 *>(x2 + (int64_t)c * P.SP)[lane];
+                y = make_double2(fma(beta.x, b.x, a.x), fma(beta.y, b.y, a.y));
+            }
+            acc.x = fma(v, y.x, acc.x);
+            acc.y = fma(v, y.y, acc.y);
+        }
+    }
+    return acc;
+}
+
+// Interface rows (per scenario): lane's two columns of row ik.
+template <bool kTwo>
+__device__ __forceinline__ double2 row_iface(const CGBParams &P, int ik, const double *x1, const double *x2,
+                                             double2 beta, int lane) {
+    double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int s = 2 * lane + h;
+        if (s >= P.S) break;
+        const int cnt = P.ell_cnt[(int64_t)ik * P.S + s];
+        const double b = h ? beta.y : beta.x;
+        double a = 0.0;
+        for (int c = 0; c < cnt; ++c) {
+            const int64_t e = ellb(P, s, c, ik);
+            const int j = P.ell_col[e];
+            double y = x1[(int64_t)j * P.SP + s];
+            if (kTwo) y = fma(b, x2[(int64_t)j * P.SP + s], y);
+            a = fma(P.ell_val[e], y, a);
+        }
+        if (h) acc.y = a; else acc.x = a;
+    }
+    return acc;
+}
+
+__global__ void __launch_bounds__(CGB_BLOCK) k_cgb_step(CGBParams P) {
+    __shared__ double sm[CGB_WARPS * CGB_NV * 64];
+    if (P.status[0] || P.status[1]) {
+        if (!P.status[0] && blockIdx.x == 0 && threadIdx.x == 0) {
+            P.status[0] = 2;
+            P.status[2] = P.step;
+        }
+        return;
+    }
+    cg::grid_group grid = cg::this_grid();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t N = P.N;
+    const int gw = blockIdx.x * CGB_WARPS + warp, TW = gridDim.x * CGB_WARPS;
+    const bool col_ok[2] = {2 * lane < P.S, 2 * lane + 1 < P.S};
+
+    // ---- phase 0: r0 = b - K~ x0, z0 = D^{-1} r0 per column
+    double v0[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};   // b.b, r.r, r.z, |Gamma_R| (scenario 0)
+    for (int64_t s = gw; s < P.nslices; s += TW) {
+        const int64_t base = P.slice_ptr[s];
+        const int w = (int)((P.slice_ptr[s + 1] - base) >> 5);
+        int ip = P.slice_if[s];
+        const int ie = P.slice_if[s + 1];
+        for (int r = 0; r < 32; ++r) {
+            const int64_t i = 32 * s + r;
+            if (i >= N) break;
+            int ik = -1;
+            if (ip < ie && P.if_rows[ip] == (int)i) ik = ip++;
+            double2 ax = row_spmm<false>(P, base, w, r, P.T_in, nullptr, make_double2(0, 0), lane);
+            double2 bg = make_double2(0.0, 0.0);
+            if (ik >= 0) {
+                const double2 ai = row_iface<false>(P, ik, P.T_in, nullptr, make_double2(0, 0), lane);
+                ax.x += ai.x;
+                ax.y += ai.y;
+                if (col_ok[0]) bg.x = P.if_b[(int64_t)ik * P.S + 2 * lane];
+                if (col_ok[1]) bg.y = P.if_b[(int64_t)ik * P.S + 2 * lane + 1];
+                if (lane == 0 && ik < P.nA) v0[3][0] += P.if_phi[(int64_t)ik * P.S];
+            }
+            const double2 Ti = reinterpret_cast<const double2 *>(P.T_in + i * P.SP)[lane];
+            const double2 di = reinterpret_cast<const double2 *>(P.DinvS + i * P.SP)[lane];
+            const double ml = P.ML[i], be = P.benv[i];
+            double2 b, rr, zz;
+            b.x = fma(ml, Ti.x, P.dt * (be + bg.x));
+            b.y = fma(ml, Ti.y, P.dt * (be + bg.y));
+            rr.x = b.x - ax.x;
+            rr.y = b.y - ax.y;
+            zz.x = col_ok[0] ? di.x * rr.x : 0.0;
+            zz.y = col_ok[1] ? di.y * rr.y : 0.0;
+            reinterpret_cast<double2 *>(P.z + i * P.SP)[lane] = zz;
+            if (col_ok[0]) {
+                v0[0][0] = fma(b.x, b.x, v0[0][0]);
+                v0[1][0] = fma(rr.x, rr.x, v0[1][0]);
+                v0[2][0] = fma(rr.x, zz.x, v0[2][0]);
+            }
+            if (col_ok[1]) {
+                v0[0][1] = fma(b.y, b.y, v0[0][1]);
+                v0[1][1] = fma(rr.y, rr.y, v0[1][1]);
+                v0[2][1] = fma(rr.y, zz.y, v0[2][1]);
+            }
+        }
+    }
+    double t0[4][2];
+    cgb_reduce<4>(v0, sm, P.partials, grid, t0);
+    double rho[2] = {t0[2][0], t0[2][1]}, rr2[2] = {t0[1][0], t0[1][1]}, tol2[2], beta[2] = {0.0, 0.0};
+    bool conv[2];
+    int itc[2] = {0, 0};
+    for (int h = 0; h < 2; ++h) {
+        tol2[h] = P.rtol2 * t0[0][h];
+        conv[h] = !col_ok[h] || rr2[h] <= tol2[h];
+    }
+    const double area = __shfl_sync(0xffffffffu, t0[3][0], 0);
+    const double *xsrc = P.T_in;
+    double *pold = P.pa, *pnew = P.pb;
+    int it = 0;
+    while (it < P.maxit) {
+        const bool any = __syncthreads_or(!(conv[0] && conv[1])) != 0;   // same in every CTA
+        if (!any) break;
+        // ---- S
+        const bool first = it == 0;
+        const double2 b2 = make_double2(beta[0], beta[1]);
+        double vs[1][2] = {{0.0, 0.0}};
+        for (int64_t s = gw; s < P.nslices; s += TW) {
+            const int64_t base = P.slice_ptr[s];
+            const int w = (int)((P.slice_ptr[s + 1] - base) >> 5);
+            int ip = P.slice_if[s];
+            const int ie = P.slice_if[s + 1];
+            for (int r = 0; r < 32; ++r) {
+                const int64_t i = 32 * s + r;
+                if (i >= N) break;
+                int ik = -1;
+                if (ip < ie && P.if_rows[ip] == (int)i) ik = ip++;
+                double2 acc = first ? row_spmm<false>(P, base, w, r, P.z, nullptr, b2, lane)
+                                    : row_spmm<true>(P, base, w, r, P.z, pold, b2, lane);
+                if (ik >= 0) {
+                    const double2 ai = first ? row_iface<false>(P, ik, P.z, nullptr, b2, lane)
+                                             : row_iface<true>(P, ik, P.z, pold, b2, lane);
+                    acc.x += ai.x;
+                    acc.y += ai.y;
+                }
+                const double2 zi = reinterpret_cast<const double2 *>(P.z + i * P.SP)[lane];
+                double2 pi = zi;
+                if (!first) {
+                    const double2 po = reinterpret_cast<const double2 *>(pold + i * P.SP)[lane];
+                    pi = make_double2(fma(b2.x, po.x, zi.x), fma(b2.y, po.y, zi.y));
+                }
+                reinterpret_cast<double2 *>(pnew + i * P.SP)[lane] = pi;
+                reinterpret_cast<double2 *>(P.q + i * P.SP)[lane] = acc;
+                vs[0][0] = fma(pi.x, acc.x, vs[0][0]);
+                vs[0][1] = fma(pi.y, acc.y, vs[0][1]);
+            }
+        }
+        double tpq[1][2];
+        cgb_reduce<1>(vs, sm, P.partials, grid, tpq);
+        double alpha[2];
+        for (int h = 0; h < 2; ++h) alpha[h] = conv[h] ? 0.0 : rho[h] / tpq[0][h];   // frozen columns
+        // ---- U (warp per row, lanes over columns)
+        double vu[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+        for (int64_t i = gw; i < N; i += TW) {
+            const double2 pv = ld_cg2(reinterpret_cast<const double2 *>(pnew + i * P.SP) + lane);
+            const double2 qv = ld_cg2(reinterpret_cast<const double2 *>(P.q + i * P.SP) + lane);
+            const double2 dv = ld_cg2(reinterpret_cast<const double2 *>(P.DinvS + i * P.SP) + lane);
+            const double2 xv = ld_cg2(reinterpret_cast<const double2 *>(xsrc + i * P.SP) + lane);
+            const double2 zv = ld_cg2(reinterpret_cast<const double2 *>(P.z + i * P.SP) + lane);
+            double2 xo, zo;
+            xo.x = fma(alpha[0], pv.x, xv.x);
+            xo.y = fma(alpha[1], pv.y, xv.y);
+            zo.x = fma(-alpha[0] * dv.x, qv.x, zv.x);
+            zo.y = fma(-alpha[1] * dv.y, qv.y, zv.y);
+            reinterpret_cast<double2 *>(P.T_out + i * P.SP)[lane] = xo;
+            reinterpret_cast<double2 *>(P.z + i * P.SP)[lane] = zo;
+            if (col_ok[0]) {
+                const double r0 = zo.x / dv.x;
+                vu[0][0] = fma(r0, zo.x, vu[0][0]);
+                vu[1][0] = fma(r0, r0, vu[1][0]);
+            }
+            if (col_ok[1]) {
+                const double r1 = zo.y / dv.y;
+                vu[0][1] = fma(r1, zo.y, vu[0][1]);
+                vu[1][1] = fma(r1, r1, vu[1][1]);
+            }
+        }
+        double tu[2][2];
+        cgb_reduce<2>(vu, sm, P.partials, grid, tu);
+        ++it;
+        for (int h = 0; h < 2; ++h) {
+            if (conv[h]) continue;
+            beta[h] = tu[0][h] / rho[h];
+            rho[h] = tu[0][h];
+            rr2[h] = tu[1][h];
+            itc[h] = it;
+            conv[h] = rr2[h] <= tol2[h];
+        }
+        xsrc = P.T_out;
+        double *t = pold; pold = pnew; pnew = t;
+    }
+    if (it == 0) {
+        for (int64_t i = gw; i < N; i += TW)
+            reinterpret_cast<double2 *>(P.T_out + i * P.SP)[lane] = reinterpret_cast<const double2 *>(P.T_in + i * P.SP)[lane];
+    }
+    if (blockIdx.x == 0 && warp == 0) {
+        for (int h = 0; h < 2; ++h) {
+            const int s = 2 * lane + h;
+            if (s >= P.S) continue;
+            const double rel = t0[0][h] > 0.0 ? sqrt(rr2[h] / t0[0][h]) : sqrt(rr2[h]);
+            P.iters_out[(int64_t)P.step * P.S + s] = itc[h];
+            P.relres_out[(int64_t)P.step * P.S + s] = rel;
+            if (!conv[h]) {
+                if (atomicCAS(&P.status[0], 0, 1) == 0) {
+                    P.status[2] = P.step;
+                    P.status[3] = s;
+                    *P.fail_relres = rel;
+                }
+            }
+        }
+        if (lane == 0) P.area_out[P.step] = area;
+    }
+}
+
+__global__ void k_dinv_broadcast(const double *Dinv, int64_t N, int S, int SP, double *DinvS) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= N * SP) return;
+    const int64_t i = t / SP;
+    const int s = (int)(t % SP);
+    DinvS[t] = s < S ? Dinv[i] : 1.0;
+}
+
+int cgb_setup(Ctx &c) {
+    if (c.S > CGB_MAXS) { c.err = "at most 64 scenarios per context"; return -1; }
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cgb_step, CGB_BLOCK, 0));
+    if (per_sm < 1) { c.err = "batched CG kernel cannot be resident"; return -3; }
+    c.cg_grid = per_sm * c.num_sms;
+    c.cg_block = CGB_BLOCK;
+    CK(cudaMalloc(&c.d_partials, sizeof(double) * (size_t)CGB_NV * 64 * c.cg_grid));
+    CK(cudaMalloc(&c.d_DinvS, sizeof(double) * (size_t)c.N * c.SP + 16));
+    return 0;
+}
+
+int cgb_prepare(Ctx &c) {
+    const int64_t n = c.N * c.SP;
+    k_dinv_broadcast<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(c.d_Dinv, c.N, c.S, c.SP, c.d_DinvS);
+    CK(cudaGetLastError());
+    return 0;
+}
+
+int cgb_launch_step(Ctx &c, int step, double dt) {
+    CGBParams P;
+    memset(&P, 0, sizeof P);
+    P.N = c.N;
+    P.nslices = c.nslices;
+    P.S = c.S;
+    P.SP = c.SP;
+    P.slice_ptr = c.d_slice_ptr;
+    P.col = c.d_col;
+    P.val = c.d_val;
+    P.ML = c.d_ML;
+    P.benv = c.d_benv;
+    P.DinvS = c.d_DinvS;
+    P.n_if = c.n_if;
+    P.nA = c.nA;
+    P.cap = c.cap;
+    P.if_rows = c.d_if_rows;
+    P.slice_if = c.d_slice_if;
+    P.ell_cnt = c.d_ell_cnt;
+    P.ell_col = c.d_ell_col;
+    P.ell_val = c.d_ell_val;
+    P.if_b = c.d_if_b;
+    P.if_phi = c.d_if_phi;
+    P.T_in = c.d_T[(c.cur + step) & 1];
+    P.T_out = c.d_T[(c.cur + step + 1) & 1];
+    P.z = c.d_z;
+    P.pa = c.d_p[0];
+    P.pb = c.d_p[1];
+    P.q = c.d_q;
+    P.partials = c.d_partials;
+    P.status = c.d_status;
+    P.fail_relres = c.d_fail_relres;
+    P.iters_out = c.d_iters;
+    P.relres_out = c.d_relres;
+    P.area_out = c.d_area;
+    P.dt = dt;
+    P.rtol2 = c.rtol * c.rtol;
+    P.maxit = c.maxit > 0 ? c.maxit : (int)std::min<int64_t>(10 * c.N, 10000);
+    P.step = step;
+    void *args[] = {&P};
+    CK(cudaLaunchCooperativeKernel((const void *)k_cgb_step, dim3(c.cg_grid), dim3(c.cg_block), args, 0, c.stream));
+    return 0;
+}
+
+}  // namespace thermo

@@ -204,8 +204,17 @@ struct IfaceParams {
     double *if_b;             // [S][n_if] dt-free friction source eta/2 int phi
     double *if_phi;           // [S][n_if] int_{Gamma_R} phi
     double *Dinv;             // S == 1: [N] Jacobi inverse diagonal, interface rows rewritten
-    double *if_dinv;          // S > 1: [S][n_if]
+    double *if_dinv;          // (unused)
+    double *DinvS;            // S > 1: [N][SP] per-scenario Jacobi inverse diagonal
+    int SP;                   // S > 1: row stride of the block vectors (even, >= S)
     int *status;              // status[1] |= overflow
 };
+
+// ELL slot c of interface row k, scenario s.  S == 1: slot-major [c][k] (coalesced across the
+// rows of a slice); S > 1: [k][c][s] (coalesced across the scenarios of one row).
+// ell_cnt, if_b, if_phi are indexed [k * S + s].
+__host__ __device__ __forceinline__ int64_t ell_index(const IfaceParams &P, int s, int c, int k) {
+    return P.S == 1 ? (int64_t)c * P.n_if + k : ((int64_t)k * P.cap + c) * P.S + s;
+}
 
 }  // namespace thermo

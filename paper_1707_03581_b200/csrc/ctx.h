@@ -30,6 +30,8 @@ struct Ctx {
 
     int64_t nf = 0, nm = 0, N = 0;
     int S = 1;
+    int SP = 1;                      // row stride of the state / workspace block vectors (N x SP)
+    double *d_DinvS = nullptr;       // S > 1: per-scenario Jacobi inverse diagonal [N][SP]
     double nu = 0, rho_cp = 0, alpha = 0;
     int iface_tag_f = 0, iface_tag_m = 0;
     std::vector<Scen> scen;
@@ -131,5 +133,10 @@ int iface_launch(Ctx &c, const IfaceParams &p);
 // cg.cu
 int cg_setup(Ctx &c);
 int cg_launch_step(Ctx &c, int step, double dt);
+
+// cg_batched.cu (S > 1 scenarios advanced together)
+int cgb_setup(Ctx &c);
+int cgb_prepare(Ctx &c);   // broadcast the volume D^{-1} into DinvS (after build_operator)
+int cgb_launch_step(Ctx &c, int step, double dt);
 
 }  // namespace thermo

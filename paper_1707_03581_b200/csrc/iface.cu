@@ -367,7 +367,7 @@ __global__ void __launch_bounds__(32 * ROW_WPB) k_rows(IfaceParams P) {
     double dself = 0.0;
     if (ok) {
         for (int u = lane; u < count; u += 32) {
-            const int64_t idx = ((int64_t)s * P.cap + u) * P.n_if + k;
+            const int64_t idx = ell_index(P, s, u, k);
             P.ell_col[idx] = W.ucol[u];
             P.ell_val[idx] = W.val[u];
             if (W.ucol[u] == row) dself = W.val[u];
@@ -376,12 +376,12 @@ __global__ void __launch_bounds__(32 * ROW_WPB) k_rows(IfaceParams P) {
     dself = warp_sum(dself);   // exactly one lane holds the diagonal (others add 0)
     if (lane == 0) {
         if (!ok) atomicOr(&P.status[1], 1);
-        P.ell_cnt[(int64_t)s * P.n_if + k] = ok ? count : 0;
-        P.if_phi[(int64_t)s * P.n_if + k] = phi;
-        P.if_b[(int64_t)s * P.n_if + k] = 0.5 * P.step_sc[4 * s + 2] * phi;
+        P.ell_cnt[(int64_t)k * P.S + s] = ok ? count : 0;
+        P.if_phi[(int64_t)k * P.S + s] = phi;
+        P.if_b[(int64_t)k * P.S + s] = 0.5 * P.step_sc[4 * s + 2] * phi;
         const double dinv = 1.0 / (P.Dvol[row] + dself);
         if (P.S == 1) P.Dinv[row] = dinv;
-        else P.if_dinv[(int64_t)s * P.n_if + k] = dinv;
+        else P.DinvS[(int64_t)row * P.SP + s] = dinv;
     }
 }
 
@@ -734,6 +734,8 @@ void iface_params(Ctx &c, IfaceParams &P, const double *step_sc, double dt) {
     P.if_phi = c.d_if_phi;
     P.Dinv = c.d_Dinv;
     P.if_dinv = c.d_if_dinv;
+    P.DinvS = c.d_DinvS;
+    P.SP = c.SP;
     P.status = c.d_status;
 }
 

@@ -42,7 +42,7 @@ static void free_ctx(Ctx *c) {
                     c->d_if_b, c->d_if_phi, c->d_if_dinv, c->d_T[0], c->d_T[1], c->d_z, c->d_p[0], c->d_p[1],
                     c->d_q, c->d_partials, c->d_status, c->d_fail_relres, c->d_step_sc, c->d_iters,
                     c->d_relres, c->d_area, c->d_pairs, c->d_pcnt, c->d_chunk_hi, c->d_chunk_ctr, c->d_lcol, c->d_chunk_runs,
-                    c->d_chunk_nruns, c->d_chunk_lown, c->d_trace};
+                    c->d_chunk_nruns, c->d_chunk_lown, c->d_trace, c->d_DinvS};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     for (cudaEvent_t e : c->events) cudaEventDestroy(e);
@@ -89,6 +89,7 @@ extern "C" int thermo_create_mesh(void **out, const thermo_mesh *fixed, const th
         c->N = c->nf + c->nm;
         if (c->N >= (1LL << 31)) { g_create_err = "too many nodes"; free_ctx(c); return THERMO_EINVAL; }
         c->S = n_scen;
+        c->SP = n_scen == 1 ? 1 : (n_scen + 1) & ~1;
         c->nu = nu;
         c->rho_cp = rho_cp;
         c->alpha = alpha_iface;
@@ -151,8 +152,8 @@ extern "C" int thermo_create_mesh(void **out, const thermo_mesh *fixed, const th
             free_ctx(c);
             return rc == -1 ? THERMO_EINVAL : (rc == -5 ? THERMO_EGEOM : THERMO_ECUDA);
         }
-        // state and workspace
-        const int64_t NS = N * c->S;
+        // state and workspace (N x SP row-major blocks)
+        const int64_t NS = N * c->SP;
         bool ok = true;
         // vectors padded by 16 entries: window bulk copies may read up to one element past N
         for (double **p : {&c->d_T[0], &c->d_T[1], &c->d_z, &c->d_p[0], &c->d_p[1], &c->d_q}) {
@@ -167,7 +168,7 @@ extern "C" int thermo_create_mesh(void **out, const thermo_mesh *fixed, const th
         cudaMemsetAsync(c->d_p[1], 0, sizeof(double) * NS, c->stream);
         cudaMemsetAsync(c->d_status, 0, sizeof(int) * 8, c->stream);
         rc = thermo::assemble_robin(*c);
-        if (!rc) rc = thermo::cg_setup(*c);
+        if (!rc) rc = c->S == 1 ? thermo::cg_setup(*c) : thermo::cgb_setup(*c);
         if (!rc && getenv("THERMO_CG_TRACE")) {
             if (cudaMalloc(&c->d_trace, sizeof(unsigned long long) * 1024) != cudaSuccess) rc = -3;
             else cudaMemsetAsync(c->d_trace, 0, sizeof(unsigned long long) * 1024, c->stream);
@@ -239,6 +240,7 @@ extern "C" int thermo_step(void *ctx, double t, double dt, int32_t nsteps) {
         const int S = c->S;
         if (c->built_dt != dt) {
             if (thermo::build_operator(*c, dt)) return THERMO_ECUDA;
+            if (S > 1 && thermo::cgb_prepare(*c)) return THERMO_ECUDA;
         }
         if ((int64_t)nsteps > c->step_cap) {
             for (void *p : {(void *)c->d_step_sc, (void *)c->d_iters, (void *)c->d_relres, (void *)c->d_area})
@@ -266,7 +268,6 @@ extern "C" int thermo_step(void *ctx, double t, double dt, int32_t nsteps) {
         }
         API_CK(cudaMemcpyAsync(c->d_step_sc, sc.data(), sizeof(double) * sc.size(), cudaMemcpyHostToDevice, c->stream));
         API_CK(cudaMemsetAsync(c->d_status, 0, sizeof(int) * 8, c->stream));
-        if (S != 1) return fail(c, THERMO_EINVAL, "batched scenarios not enabled in this build");
         if (c->timing) {
             while (c->events.size() < 2 * (size_t)nsteps + 1) {
                 cudaEvent_t e;
@@ -281,7 +282,7 @@ extern "C" int thermo_step(void *ctx, double t, double dt, int32_t nsteps) {
             if (c->timing) API_CK(cudaEventRecord(c->events[2 * n], c->stream));
             if (thermo::iface_launch(*c, P)) return THERMO_ECUDA;
             if (c->timing) API_CK(cudaEventRecord(c->events[2 * n + 1], c->stream));
-            if (thermo::cg_launch_step(*c, n, dt)) return THERMO_ECUDA;
+            if ((S == 1 ? thermo::cg_launch_step(*c, n, dt) : thermo::cgb_launch_step(*c, n, dt))) return THERMO_ECUDA;
         }
         if (c->timing) API_CK(cudaEventRecord(c->events[2 * nsteps], c->stream));
         int status[8];
@@ -358,10 +359,10 @@ extern "C" int thermo_get_T(void *ctx, int32_t scen, int32_t part, double *out, 
     if (!c || !out) return c ? fail(c, THERMO_EINVAL, "out is NULL") : THERMO_EINVAL;
     int64_t off, cnt;
     if (int rc = selection(c, scen, part, n, &off, &cnt)) return rc;
-    const double *src = c->d_T[c->cur] + off * c->S + scen;
+    const double *src = c->d_T[c->cur] + off * c->SP + scen;
     cudaMemcpyKind kind = out_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
-    if (c->S == 1) API_CK(cudaMemcpyAsync(out, src, sizeof(double) * cnt, kind, c->stream));
-    else API_CK(cudaMemcpy2DAsync(out, sizeof(double), src, sizeof(double) * c->S, sizeof(double), cnt, kind, c->stream));
+    if (c->SP == 1) API_CK(cudaMemcpyAsync(out, src, sizeof(double) * cnt, kind, c->stream));
+    else API_CK(cudaMemcpy2DAsync(out, sizeof(double), src, sizeof(double) * c->SP, sizeof(double), cnt, kind, c->stream));
     if (!out_on_device) API_CK(cudaStreamSynchronize(c->stream));
     return THERMO_OK;
 }
@@ -372,10 +373,10 @@ extern "C" int thermo_set_T(void *ctx, int32_t scen, int32_t part, const double 
     if (!c || !in) return c ? fail(c, THERMO_EINVAL, "in is NULL") : THERMO_EINVAL;
     int64_t off, cnt;
     if (int rc = selection(c, scen, part, n, &off, &cnt)) return rc;
-    double *dst = c->d_T[c->cur] + off * c->S + scen;
+    double *dst = c->d_T[c->cur] + off * c->SP + scen;
     cudaMemcpyKind kind = in_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-    if (c->S == 1) API_CK(cudaMemcpyAsync(dst, in, sizeof(double) * cnt, kind, c->stream));
-    else API_CK(cudaMemcpy2DAsync(dst, sizeof(double) * c->S, in, sizeof(double), sizeof(double), cnt, kind, c->stream));
+    if (c->SP == 1) API_CK(cudaMemcpyAsync(dst, in, sizeof(double) * cnt, kind, c->stream));
+    else API_CK(cudaMemcpy2DAsync(dst, sizeof(double) * c->SP, in, sizeof(double), sizeof(double), cnt, kind, c->stream));
     if (!in_on_device) API_CK(cudaStreamSynchronize(c->stream));
     return THERMO_OK;
 }

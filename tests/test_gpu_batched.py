@@ -1,0 +1,71 @@
+"""Batched scenarios (BASELINE.json config 4): S scenarios with different
+motion periods and friction laws advanced together through one context; every column is
+checked against an independent oracle run of that scenario (max-norm relative <= 1e-9)."""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_1707_03581_b200 import inputs as I
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-9
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    import __graft_entry__ as g
+    g.build()
+
+
+def rel(a, b):
+    return float(np.abs(a - b).max() / np.abs(b).max())
+
+
+def _scen(k):
+    return I.Scenario(0.375, 0.375, 20.0 + k, 100.0 + 15.0 * k, 0.3 * (k % 2), 7.0 + k)
+
+
+@pytest.mark.parametrize("S", [2, 3, 5])
+def test_batched_columns_match_oracle(S):
+    from paper_1707_03581_b200.thermo import Thermo
+    cfg = I.make_config("small", jitter=0.1)
+    scen = [_scen(k) for k in range(S)]
+    th = Thermo.from_config(cfg, scenarios=scen)
+    T0 = I.initial_field(cfg)[0]
+    for k in range(S):
+        th.set_T(T0 + 0.1 * k, scen=k)
+    th.step(0.0, cfg.dt, 20)
+    o = O.Oracle.from_config(cfg)
+    for k in range(S):
+        Tr, st = o.step(T0 + 0.1 * k, 0.0, cfg.dt, 20, scen[k])
+        assert rel(th.get_T(scen=k), Tr) <= TOL, k
+    it = th.step_iters()
+    assert it.shape == (20, S) and it.min() > 0
+
+
+def test_batched_equals_single_runs():
+    """Column k of a batched run equals a single-scenario run of scenario k (same row sums;
+    only the dot-product reduction trees differ)."""
+    from paper_1707_03581_b200.thermo import Thermo
+    cfg = I.make_config("medium", jitter=0.1)
+    scen = [_scen(k) for k in range(4)]
+    tb = Thermo.from_config(cfg, scenarios=scen)
+    tb.step(0.0, 1.0, 6)
+    for k in (0, 3):
+        ts = Thermo.from_config(cfg, scenarios=[scen[k]])
+        ts.step(0.0, 1.0, 6)
+        assert rel(tb.get_T(scen=k), ts.get_T()) < 1e-12
+
+
+def test_cfg4_sampled_scenarios():
+    """Config 4 (cfg 1 meshes, 64 scenarios, dt = 1 s): a short horizon, sampled columns
+    against the oracle."""
+    from paper_1707_03581_b200.thermo import Thermo
+    cfg = I.make_config("cfg4")
+    th = Thermo.from_config(cfg)
+    n = 5
+    th.step(0.0, cfg.dt, n)
+    o = O.Oracle.from_config(cfg)
+    for k in (0, 37, 63):
+        Tr, st = o.step(np.full(o.n, cfg.T0), 0.0, cfg.dt, n, cfg.scenarios[k])
+        assert rel(th.get_T(scen=k), Tr) <= TOL, k
