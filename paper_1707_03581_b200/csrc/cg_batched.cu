@@ -36,7 +36,7 @@ namespace thermo {
         }                                                                        \
     } while (0)
 
-#define CGB_BLOCK 256
+#define CGB_BLOCK 512
 #define CGB_WARPS (CGB_BLOCK / 32)
 #define CGB_MAXS 64
 #define CGB_NV 4   // reduction values per column and phase (max)
@@ -85,7 +85,16 @@ __device__ __forceinline__ void cgb_reduce(double (&v)[NV][2], double *sm, doubl
     grid.sync();
     for (int t = threadIdx.x; t < NV * 64; t += blockDim.x) {
         double a = 0.0;
-        for (int g = 0; g < (int)gridDim.x; ++g) a += partials[(int64_t)g * CGB_NV * 64 + t];
+        const int G = gridDim.x;
+        int g = 0;
+        for (; g + 8 <= G; g += 8) {   // loads issued together, adds in the serial order
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = partials[(int64_t)(g + u) * CGB_NV * 64 + t];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) a += v[u];
+        }
+        for (; g < G; ++g) a += partials[(int64_t)g * CGB_NV * 64 + t];
         sm[t] = a;
     }
     __syncthreads();
@@ -104,6 +113,7 @@ template <bool kTwo>
 __device__ __forceinline__ double2 row_spmm(const CGBParams &P, int64_t base, int w, int r, const double *x1,
                                             const double *x2, double2 beta, int lane) {
     double2 acc = make_double2(0.0, 0.0);
+    const int ln = 2 * lane < P.SP ? lane : 0;   // lanes past the row stride re-read column 0..1
     for (int k0 = 0; k0 < w; k0 += 32) {
         const int kk = k0 + lane;
         int cl = 0;
@@ -121,9 +131,9 @@ __device__ __forceinline__ double2 row_spmm(const CGBParams &P, int64_t base, in
             for (int u = 0; u < 8; ++u) {
                 const int c = __shfl_sync(0xffffffffu, cl, k + u);
                 v[u] = __shfl_sync(0xffffffffu, vl, k + u);
-                const double2 a = reinterpret_cast<const double2 *>(x1 + (int64_t)c * P.SP)[lane];
+                const double2 a = reinterpret_cast<const double2 *>(x1 + (int64_t)c * P.SP)[ln];
                 if (kTwo) {
-                    const double2 b = reinterpret_cast<const double2 *>(x2 + (int64_t)c * P.SP)[lane];
+                    const double2 b = reinterpret_cast<const double2 *>(x2 + (int64_t)c * P.SP)[ln];
                     y[u] = make_double2(fma(beta.x, b.x, a.x), fma(beta.y, b.y, a.y));
                 } else {
                     y[u] = a;
@@ -138,10 +148,10 @@ __device__ __forceinline__ double2 row_spmm(const CGBParams &P, int64_t base, in
         for (; k < m; ++k) {
             const int c = __shfl_sync(0xffffffffu, cl, k);
             const double v = __shfl_sync(0xffffffffu, vl, k);
-            const double2 a = reinterpret_cast<const double2 *>(x1 + (int64_t)c * P.SP)[lane];
+            const double2 a = reinterpret_cast<const double2 *>(x1 + (int64_t)c * P.SP)[ln];
             double2 y = a;
             if (kTwo) {
-                const double2 b = reinterpret_cast<const double2 *>(x2 + (int64_t)c * P.SP)[lane];
+                const double2 b = reinterpret_cast<const double2 *>(x2 + (int64_t)c * P.SP)[ln];
                 y = make_double2(fma(beta.x, b.x, a.x), fma(beta.y, b.y, a.y));
             }
             acc.x = fma(v, y.x, acc.x);
@@ -149,6 +159,70 @@ __device__ __forceinline__ double2 row_spmm(const CGBParams &P, int64_t base, in
         }
     }
     return acc;
+}
+
+// Two rows (rA, rB) of one slice at once: lanes 0-15 load the entries of row A, lanes 16-31
+// those of row B (16 per round), the warp broadcasts them; every lane gathers its two columns
+// for both rows, so twice the loads are in flight.  Same fma order per row as row_spmm.
+template <bool kTwo>
+__device__ __forceinline__ void row_spmm2(const CGBParams &P, int64_t base, int w, int rA, bool validB,
+                                          const double *x1, const double *x2, double2 beta, int lane,
+                                          double2 &accA, double2 &accB) {
+    accA = make_double2(0.0, 0.0);
+    accB = make_double2(0.0, 0.0);
+    const int ln = 2 * lane < P.SP ? lane : 0;
+    const int half = lane >> 4, hk = lane & 15;
+    for (int k0 = 0; k0 < w; k0 += 16) {
+        const int kk = k0 + hk;
+        int cl = 0;
+        double vl = 0.0;
+        if (kk < w && (half == 0 || validB)) {
+            cl = P.col[base + 32 * (int64_t)kk + rA + half];
+            vl = P.val[base + 32 * (int64_t)kk + rA + half];
+        }
+        const int m = min(16, w - k0);
+        for (int k = 0; k < m; k += 4) {
+            double2 yA[4], yB[4];
+            double vA[4], vB[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int ku = min(k + u, m - 1);
+                const int cA = __shfl_sync(0xffffffffu, cl, ku);
+                const int cB = __shfl_sync(0xffffffffu, cl, 16 + ku);
+                vA[u] = k + u < m ? __shfl_sync(0xffffffffu, vl, ku) : 0.0;
+                vB[u] = k + u < m ? __shfl_sync(0xffffffffu, vl, 16 + ku) : 0.0;
+                const double2 a = reinterpret_cast<const double2 *>(x1 + (int64_t)cA * P.SP)[ln];
+                const double2 b = reinterpret_cast<const double2 *>(x1 + (int64_t)cB * P.SP)[ln];
+                if (kTwo) {
+                    const double2 a2 = reinterpret_cast<const double2 *>(x2 + (int64_t)cA * P.SP)[ln];
+                    const double2 b2 = reinterpret_cast<const double2 *>(x2 + (int64_t)cB * P.SP)[ln];
+                    yA[u] = make_double2(fma(beta.x, a2.x, a.x), fma(beta.y, a2.y, a.y));
+                    yB[u] = make_double2(fma(beta.x, b2.x, b.x), fma(beta.y, b2.y, b.y));
+                } else {
+                    yA[u] = a;
+                    yB[u] = b;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (k + u < m) {
+                    accA.x = fma(vA[u], yA[u].x, accA.x);
+                    accA.y = fma(vA[u], yA[u].y, accA.y);
+                    accB.x = fma(vB[u], yB[u].x, accB.x);
+                    accB.y = fma(vB[u], yB[u].y, accB.y);
+                }
+            }
+        }
+    }
+}
+
+// Interface index of row i of slice s (-1 if none); warp-uniform.
+__device__ __forceinline__ int iface_of(const CGBParams &P, int64_t s, int64_t i, int lane) {
+    const int b = P.slice_if[s], e = P.slice_if[s + 1];
+    if (b == e) return -1;
+    const int j = b + lane;
+    const unsigned m = __ballot_sync(0xffffffffu, j < e && P.if_rows[j] == (int)i);
+    return m ? b + __ffs(m) - 1 : -1;
 }
 
 // Interface rows (per scenario): lane's two columns of row ik.
@@ -175,7 +249,7 @@ __device__ __forceinline__ double2 row_iface(const CGBParams &P, int ik, const d
     return acc;
 }
 
-__global__ void __launch_bounds__(CGB_BLOCK) k_cgb_step(CGBParams P) {
+__global__ void __launch_bounds__(CGB_BLOCK, 1) k_cgb_step(CGBParams P) {
     __shared__ double sm[CGB_WARPS * CGB_NV * 64];
     if (P.status[0] || P.status[1]) {
         if (!P.status[0] && blockIdx.x == 0 && threadIdx.x == 0) {
@@ -189,20 +263,26 @@ __global__ void __launch_bounds__(CGB_BLOCK) k_cgb_step(CGBParams P) {
     const int64_t N = P.N;
     const int gw = blockIdx.x * CGB_WARPS + warp, TW = gridDim.x * CGB_WARPS;
     const bool col_ok[2] = {2 * lane < P.S, 2 * lane + 1 < P.S};
+    const bool lane_ok = 2 * lane < P.SP;   // lanes past the row stride touch no memory
 
     // ---- phase 0: r0 = b - K~ x0, z0 = D^{-1} r0 per column
     double v0[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};   // b.b, r.r, r.z, |Gamma_R| (scenario 0)
-    for (int64_t s = gw; s < P.nslices; s += TW) {
+    const int64_t npairs = P.nslices * 16;   // units: (slice, row pair)
+    for (int64_t u = gw; u < npairs; u += TW) {
+        const int64_t s = u >> 4;
+        const int rA = 2 * (int)(u & 15);
+        const int64_t iA = 32 * s + rA;
+        if (iA >= N) continue;
+        const bool validB = iA + 1 < N;
         const int64_t base = P.slice_ptr[s];
         const int w = (int)((P.slice_ptr[s + 1] - base) >> 5);
-        int ip = P.slice_if[s];
-        const int ie = P.slice_if[s + 1];
-        for (int r = 0; r < 32; ++r) {
-            const int64_t i = 32 * s + r;
-            if (i >= N) break;
-            int ik = -1;
-            if (ip < ie && P.if_rows[ip] == (int)i) ik = ip++;
-            double2 ax = row_spmm<false>(P, base, w, r, P.T_in, nullptr, make_double2(0, 0), lane);
+        double2 axr[2];
+        row_spmm2<false>(P, base, w, rA, validB, P.T_in, nullptr, make_double2(0, 0), lane, axr[0], axr[1]);
+        for (int h = 0; h < 2; ++h) {
+            const int64_t i = iA + h;
+            if (h == 1 && !validB) break;
+            const int ik = iface_of(P, s, i, lane);
+            double2 ax = axr[h];
             double2 bg = make_double2(0.0, 0.0);
             if (ik >= 0) {
                 const double2 ai = row_iface<false>(P, ik, P.T_in, nullptr, make_double2(0, 0), lane);
@@ -212,6 +292,7 @@ __global__ void __launch_bounds__(CGB_BLOCK) k_cgb_step(CGBParams P) {
                 if (col_ok[1]) bg.y = P.if_b[(int64_t)ik * P.S + 2 * lane + 1];
                 if (lane == 0 && ik < P.nA) v0[3][0] += P.if_phi[(int64_t)ik * P.S];
             }
+            if (!lane_ok) continue;
             const double2 Ti = reinterpret_cast<const double2 *>(P.T_in + i * P.SP)[lane];
             const double2 di = reinterpret_cast<const double2 *>(P.DinvS + i * P.SP)[lane];
             const double ml = P.ML[i], be = P.benv[i];
@@ -255,24 +336,29 @@ __global__ void __launch_bounds__(CGB_BLOCK) k_cgb_step(CGBParams P) {
         const bool first = it == 0;
         const double2 b2 = make_double2(beta[0], beta[1]);
         double vs[1][2] = {{0.0, 0.0}};
-        for (int64_t s = gw; s < P.nslices; s += TW) {
+        for (int64_t u = gw; u < npairs; u += TW) {
+            const int64_t s = u >> 4;
+            const int rA = 2 * (int)(u & 15);
+            const int64_t iA = 32 * s + rA;
+            if (iA >= N) continue;
+            const bool validB = iA + 1 < N;
             const int64_t base = P.slice_ptr[s];
             const int w = (int)((P.slice_ptr[s + 1] - base) >> 5);
-            int ip = P.slice_if[s];
-            const int ie = P.slice_if[s + 1];
-            for (int r = 0; r < 32; ++r) {
-                const int64_t i = 32 * s + r;
-                if (i >= N) break;
-                int ik = -1;
-                if (ip < ie && P.if_rows[ip] == (int)i) ik = ip++;
-                double2 acc = first ? row_spmm<false>(P, base, w, r, P.z, nullptr, b2, lane)
-                                    : row_spmm<true>(P, base, w, r, P.z, pold, b2, lane);
+            double2 accr[2];
+            if (first) row_spmm2<false>(P, base, w, rA, validB, P.z, nullptr, b2, lane, accr[0], accr[1]);
+            else row_spmm2<true>(P, base, w, rA, validB, P.z, pold, b2, lane, accr[0], accr[1]);
+            for (int h = 0; h < 2; ++h) {
+                const int64_t i = iA + h;
+                if (h == 1 && !validB) break;
+                const int ik = iface_of(P, s, i, lane);
+                double2 acc = accr[h];
                 if (ik >= 0) {
                     const double2 ai = first ? row_iface<false>(P, ik, P.z, nullptr, b2, lane)
                                              : row_iface<true>(P, ik, P.z, pold, b2, lane);
                     acc.x += ai.x;
                     acc.y += ai.y;
                 }
+                if (!lane_ok) continue;
                 const double2 zi = reinterpret_cast<const double2 *>(P.z + i * P.SP)[lane];
                 double2 pi = zi;
                 if (!first) {
@@ -291,12 +377,7 @@ __global__ void __launch_bounds__(CGB_BLOCK) k_cgb_step(CGBParams P) {
         for (int h = 0; h < 2; ++h) alpha[h] = conv[h] ? 0.0 : rho[h] / tpq[0][h];   // frozen columns
         // ---- U (warp per row, lanes over columns)
         double vu[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-        for (int64_t i = gw; i < N; i += TW) {
-            const double2 pv = ld_cg2(reinterpret_cast<const double2 *>(pnew + i * P.SP) + lane);
-            const double2 qv = ld_cg2(reinterpret_cast<const double2 *>(P.q + i * P.SP) + lane);
-            const double2 dv = ld_cg2(reinterpret_cast<const double2 *>(P.DinvS + i * P.SP) + lane);
-            const double2 xv = ld_cg2(reinterpret_cast<const double2 *>(xsrc + i * P.SP) + lane);
-            const double2 zv = ld_cg2(reinterpret_cast<const double2 *>(P.z + i * P.SP) + lane);
+        auto upd = [&](double2 pv, double2 qv, double2 dv, double2 xv, double2 zv, int64_t i) {
             double2 xo, zo;
             xo.x = fma(alpha[0], pv.x, xv.x);
             xo.y = fma(alpha[1], pv.y, xv.y);
@@ -314,6 +395,29 @@ __global__ void __launch_bounds__(CGB_BLOCK) k_cgb_step(CGBParams P) {
                 vu[0][1] = fma(r1, zo.y, vu[0][1]);
                 vu[1][1] = fma(r1, r1, vu[1][1]);
             }
+        };
+        if (lane_ok) {
+            int64_t i = gw;
+            for (; i + 3 * (int64_t)TW < N; i += 4 * (int64_t)TW) {   // 4 rows in flight
+                double2 pv[4], qv[4], dv[4], xv[4], zv[4];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const int64_t ir = i + r * (int64_t)TW;
+                    pv[r] = ld_cg2(reinterpret_cast<const double2 *>(pnew + ir * P.SP) + lane);
+                    qv[r] = ld_cg2(reinterpret_cast<const double2 *>(P.q + ir * P.SP) + lane);
+                    dv[r] = ld_cg2(reinterpret_cast<const double2 *>(P.DinvS + ir * P.SP) + lane);
+                    xv[r] = ld_cg2(reinterpret_cast<const double2 *>(xsrc + ir * P.SP) + lane);
+                    zv[r] = ld_cg2(reinterpret_cast<const double2 *>(P.z + ir * P.SP) + lane);
+                }
+#pragma unroll
+                for (int r = 0; r < 4; ++r) upd(pv[r], qv[r], dv[r], xv[r], zv[r], i + r * (int64_t)TW);
+            }
+            for (; i < N; i += TW)
+                upd(ld_cg2(reinterpret_cast<const double2 *>(pnew + i * P.SP) + lane),
+                    ld_cg2(reinterpret_cast<const double2 *>(P.q + i * P.SP) + lane),
+                    ld_cg2(reinterpret_cast<const double2 *>(P.DinvS + i * P.SP) + lane),
+                    ld_cg2(reinterpret_cast<const double2 *>(xsrc + i * P.SP) + lane),
+                    ld_cg2(reinterpret_cast<const double2 *>(P.z + i * P.SP) + lane), i);
         }
         double tu[2][2];
         cgb_reduce<2>(vu, sm, P.partials, grid, tu);
@@ -329,7 +433,7 @@ __global__ void __launch_bounds__(CGB_BLOCK) k_cgb_step(CGBParams P) {
         xsrc = P.T_out;
         double *t = pold; pold = pnew; pnew = t;
     }
-    if (it == 0) {
+    if (it == 0 && lane_ok) {
         for (int64_t i = gw; i < N; i += TW)
             reinterpret_cast<double2 *>(P.T_out + i * P.SP)[lane] = reinterpret_cast<const double2 *>(P.T_in + i * P.SP)[lane];
     }

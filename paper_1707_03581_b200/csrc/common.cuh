@@ -145,7 +145,15 @@ __device__ __forceinline__ void grid_total(const double *partials, int G, int sl
 #pragma unroll
         for (int j = 0; j < NV; ++j) {
             double x = 0.0;
-            for (int g = lane; g < G; g += 32) x += partials[g * THERMO_NRED + slot + j];
+            int g = lane;
+            for (; g + 96 < G; g += 128) {   // loads issued together, adds in the serial order
+                const double a0 = partials[g * THERMO_NRED + slot + j];
+                const double a1 = partials[(g + 32) * THERMO_NRED + slot + j];
+                const double a2 = partials[(g + 64) * THERMO_NRED + slot + j];
+                const double a3 = partials[(g + 96) * THERMO_NRED + slot + j];
+                x += a0; x += a1; x += a2; x += a3;
+            }
+            for (; g < G; g += 32) x += partials[g * THERMO_NRED + slot + j];
             x = warp_sum(x);
             if (lane == 0) smem[136 + j] = x;
         }

@@ -161,3 +161,46 @@ def test_cg_kernel_variants_agree(monkeypatch, variant):
     assert rel(a.get_T(), b.get_T()) < 1e-12
     Tr, _ = O.run_config(cfg)
     assert rel(a.get_T(), Tr) <= TOL
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name,nsteps", [("cfg2", 4), ("cfg3", 2)])
+def test_stand_scale_short_horizon(name, nsteps):
+    """BASELINE configs 2 and 3 at full size (1.28 M / 10.0 M DoF, jittered L-shape, the
+    launch configuration bench.py times): a short horizon from a seeded non-uniform field,
+    every DoF against the oracle (its full 3600 / 200-step runs are out of a test's reach)."""
+    cfg = I.make_config(name)
+    T0 = I.initial_field(cfg)[0]
+    th = _thermo(cfg)
+    th.set_T(T0)
+    t0 = 7.0
+    th.step(t0, cfg.dt, nsteps)
+    Tg = th.get_T()
+    o = O.Oracle.from_config(cfg)
+    Tr, st = o.step(T0, t0, cfg.dt, nsteps, cfg.scenarios[0])
+    assert rel(Tg, Tr) <= TOL
+    assert abs(th.stats()["iface_area"] - 0.08) < 1e-12
+
+
+@pytest.mark.slow
+def test_cfg2_full_run_invariants():
+    """BASELINE config 2 for its full 3600 steps on the GPU: every step converged, the
+    interface area stays 0.08 m^2, and sampled rows of the last step satisfy the oracle's
+    own implicit-Euler equations (row residuals assembled by the oracle, one by one)."""
+    cfg = I.make_config("cfg2")
+    th = _thermo(cfg)
+    th.step(0.0, cfg.dt, cfg.nsteps - 1)
+    Tprev = th.get_T()
+    th.step((cfg.nsteps - 1) * cfg.dt, cfg.dt, 1)
+    Tlast = th.get_T()
+    s = th.stats()
+    assert s["steps_done"] == cfg.nsteps and s["last_relres"] <= 1e-12
+    assert abs(s["iface_area"] - 0.08) < 1e-12
+    assert np.isfinite(Tlast).all() and 17.0 < Tlast.min() and Tlast.max() < 40.0
+    o = O.Oracle.from_config(cfg)
+    tp = cfg.nsteps * cfg.dt
+    sv, eta = I.scenario_scalars(cfg.scenarios[0], tp)
+    rng = np.random.default_rng(3)
+    rows = np.concatenate([rng.integers(0, o.n, 2000), np.arange(o.n - 50, o.n)])
+    res, bnorm = o.residual_rows(cfg.dt, (sv, 0.0, 0.0), eta, Tprev, Tlast, rows)
+    assert np.abs(res).max() <= 1e-10 * bnorm
