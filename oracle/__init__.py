@@ -56,6 +56,9 @@ def lib():
         L.or_step.argtypes = [_p, _d, _d, _i32, _d, _d, _d, _d, _d, _d, _d, _d, _d, _p, _i32, _d, _i32, _p]
         L.or_ie_residual_rows.argtypes = [_p, _d, _d, _d, _d, _d, _p, _p, _i64, _p, _p, _p]
         L.or_apply_system.argtypes = [_p, _d, _p, _p]
+        L.or_mrsdc_weights.argtypes = [ctypes.c_int, ctypes.c_int, _d, _d, _p, _p, _p, _p, _p, _p]
+        L.or_step_mrsdc.argtypes = [_p, _d, _d, _i32, _i32, _i32, _i32, _d, _d, _d, _d, _d, _d, _d, _d, _d, _p,
+                                    _d, _p]
         _lib = L
     return _lib
 
@@ -165,6 +168,32 @@ class Oracle:
         y = np.zeros_like(x)
         lib().or_apply_system(self.h, dt, _ptr(x), _ptr(y))
         return y
+
+
+def mrsdc_weights(M: int, P: int, t0: float = 0.0, dt: float = 1.0):
+    """(tau[M], taue[M,P], s[M,M], shat[M,P], stilde[M,P,M], semb[M,P,P]) of Table 1."""
+    tau, taue = np.zeros(M), np.zeros((M, P))
+    s, shat = np.zeros((M, M)), np.zeros((M, P))
+    st, se = np.zeros((M, P, M)), np.zeros((M, P, P))
+    rc = lib().or_mrsdc_weights(M, P, t0, dt, _ptr(tau), _ptr(taue), _ptr(s), _ptr(shat), _ptr(st), _ptr(se))
+    if rc:
+        raise ValueError("oracle: " + lib().or_last_error().decode())
+    return tau, taue, s, shat, st, se
+
+
+def _step_mrsdc(self, T, t, dt, nsteps, scen, M=3, P=2, K=1, rtol=1e-12):
+    """MRSDC(M, P) with K sweeps (Algorithms 1-2).  Returns (T_new, stats[nsteps, 3])."""
+    T = np.array(T, dtype=np.float64, copy=True)
+    stats = np.zeros((nsteps, 3))
+    rc = lib().or_step_mrsdc(self.h, t, dt, nsteps, M, P, K, scen.s0, scen.amp, scen.period, scen.dir[0],
+                             scen.dir[1], scen.dir[2], scen.eta0, scen.eta_amp, scen.eta_period, _ptr(T), rtol,
+                             _ptr(stats))
+    if rc:
+        raise RuntimeError(f"oracle mrsdc failed rc={rc}: " + lib().or_last_error().decode())
+    return T, stats
+
+
+Oracle.step_mrsdc = _step_mrsdc
 
 
 def run_config(cfg, scen_index: int = 0, T_init: Optional[np.ndarray] = None, nsteps: Optional[int] = None,

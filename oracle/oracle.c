@@ -751,3 +751,251 @@ int or_ie_residual_rows(or_sys *s, double dt, double ox, double oy, double oz, d
     free(b);
     return 0;
 }
+
+/* ==================================================================================== */
+/* Multi-rate SDC: the paper's method, in the order of Algorithms 1 and 2.   */
+/* f^I(T) = (A + B_env) T, g = b_env, f^E(T, t) = K_G(t) T + b_G(t).        */
+/* ==================================================================================== */
+
+/* integral over [a, b] of the Lagrange polynomial l_j on the nodes x[0..n-1] (exact:
+ * expand the product in the monomial basis of (s - x0), integrate term by term) */
+static double lagrange_integral(const double *x, int n, int j, double a, double b) {
+    double c[32] = {0}, t[32];
+    c[0] = 1.0;
+    int deg = 0;
+    double den = 1.0;
+    for (int k = 0; k < n; k++) {
+        if (k == j) continue;
+        /* multiply by (s - x[k]) = (u + x0 - x[k]) with u = s - x0 */
+        double r = x[0] - x[k];
+        for (int d = 0; d <= deg + 1; d++) t[d] = 0.0;
+        for (int d = 0; d <= deg; d++) {
+            t[d + 1] += c[d];
+            t[d] += c[d] * r;
+        }
+        deg++;
+        for (int d = 0; d <= deg; d++) c[d] = t[d];
+        den *= x[j] - x[k];
+    }
+    double ua = a - x[0], ub = b - x[0], acc = 0.0;
+    for (int d = 0; d <= deg; d++) acc += c[d] * (pow(ub, d + 1) - pow(ua, d + 1)) / (d + 1);
+    return acc / den;
+}
+
+/* Equidistant no-left nodes of [t0, t0 + dt] and the four weight families of
+ * Table 1:  s[m][j], shat[m][p], stilde[m][p][j], semb[m][p][q]. */
+int or_mrsdc_weights(int M, int P, double t0, double dt, double *tau, double *taue,
+                     double *s, double *shat, double *stilde, double *semb) {
+    if (M < 1 || P < 1 || M > 16 || P > 16) { set_err("MRSDC: 1 <= M, P <= 16"); return -1; }
+    double tm[17];
+    tm[0] = t0;
+    for (int m = 1; m <= M; m++) tm[m] = t0 + dt * (double)m / (double)M;
+    for (int m = 0; m < M; m++) tau[m] = tm[m + 1];
+    for (int m = 1; m <= M; m++) {
+        double emb[16];
+        for (int p = 1; p <= P; p++) {
+            emb[p - 1] = tm[m - 1] + (tm[m] - tm[m - 1]) * (double)p / (double)P;
+            taue[(m - 1) * P + (p - 1)] = emb[p - 1];
+        }
+        for (int j = 0; j < M; j++)
+            s[(m - 1) * M + j] = lagrange_integral(tau, M, j, tm[m - 1], tm[m]);
+        for (int p = 0; p < P; p++)
+            shat[(m - 1) * P + p] = lagrange_integral(emb, P, p, tm[m - 1], tm[m]);
+        for (int p = 1; p <= P; p++) {
+            double lo = p == 1 ? tm[m - 1] : emb[p - 2], hi = emb[p - 1];
+            for (int j = 0; j < M; j++)
+                stilde[((m - 1) * P + (p - 1)) * M + j] = lagrange_integral(tau, M, j, lo, hi);
+            for (int q = 0; q < P; q++)
+                semb[((m - 1) * P + (p - 1)) * P + q] = lagrange_integral(emb, P, q, lo, hi);
+        }
+    }
+    return 0;
+}
+
+/* y = (A + B_env) x  (f^I without g) */
+static void apply_vol(const or_sys *s, const double *x, double *y) {
+    for (int64_t i = 0; i < s->n; i++) {
+        double acc = 0.0;
+        for (int64_t k = s->rowptr[i]; k < s->rowptr[i + 1]; k++) acc += (s->A[k] + s->B[k]) * x[s->col[k]];
+        y[i] = acc;
+    }
+}
+
+/* y = K_G x + b_G with the interface assembled at (offset, eta) of time t (f^E) */
+static int apply_fe(or_sys *s, double t, double s0, double amp, double period, const double *dir,
+                    double eta0, double eta_amp, double eta_period, const double *x, double *y) {
+    double sp = s0 + amp * sin(2.0 * M_PI * t / period);
+    double etap = eta0 * (1.0 + eta_amp * sin(2.0 * M_PI * t / eta_period));
+    if (or_assemble_interface(s, sp * dir[0], sp * dir[1], sp * dir[2], etap)) return -5;
+    for (int64_t i = 0; i < s->n; i++) {
+        double acc = s->bG[i];
+        for (int64_t k = s->irowptr[i]; k < s->irowptr[i + 1]; k++) acc += s->ival[k] * x[s->icol[k]];
+        y[i] = acc;
+    }
+    return 0;
+}
+
+/* (M_L - a (A + B_env)) x = b by Jacobi-PCG from the given x, ||r||_2 <= rtol ||b||_2 */
+static int64_t pcg_shifted(const or_sys *s, double a, const double *b, double *x, double rtol, int64_t maxit) {
+    int64_t n = s->n;
+    double *r = malloc(sizeof *r * (size_t)n), *z = malloc(sizeof *z * (size_t)n);
+    double *p = malloc(sizeof *p * (size_t)n), *q = malloc(sizeof *q * (size_t)n);
+    double *d = malloc(sizeof *d * (size_t)n);
+    if (!r || !z || !p || !q || !d) return -2;
+    for (int64_t i = 0; i < n; i++) {
+        int64_t k = find_entry(s->rowptr, s->col, i, (int32_t)i);
+        d[i] = s->ML[i] - a * (s->A[k] + s->B[k]);
+    }
+    apply_vol(s, x, q);
+    for (int64_t i = 0; i < n; i++) { r[i] = b[i] - (s->ML[i] * x[i] - a * q[i]); z[i] = r[i] / d[i]; p[i] = z[i]; }
+    double bnorm = sqrt(dot(n, b, b)), rz = dot(n, r, z), rnorm = sqrt(dot(n, r, r));
+    int64_t it = 0;
+    while (rnorm > rtol * bnorm && it < maxit) {
+        apply_vol(s, p, q);
+        for (int64_t i = 0; i < n; i++) q[i] = s->ML[i] * p[i] - a * q[i];
+        double alpha = rz / dot(n, p, q);
+        for (int64_t i = 0; i < n; i++) { x[i] += alpha * p[i]; r[i] -= alpha * q[i]; }
+        for (int64_t i = 0; i < n; i++) z[i] = r[i] / d[i];
+        double rz_new = dot(n, r, z), beta = rz_new / rz;
+        rz = rz_new;
+        for (int64_t i = 0; i < n; i++) p[i] = z[i] + beta * p[i];
+        rnorm = sqrt(dot(n, r, r));
+        it++;
+    }
+    free(r); free(z); free(p); free(q); free(d);
+    return rnorm > rtol * bnorm ? -1 : it;
+}
+
+/* MRSDC(M, P) with K correction sweeps, nsteps steps of size dt from t.
+ * T[N] in/out.  stats (may be NULL): per step {solves, CG iterations, final SDC residual
+ * r^K (max-norm over the standard nodes, in units of M T)}. */
+int or_step_mrsdc(or_sys *s, double t, double dt, int32_t nsteps, int32_t M, int32_t P, int32_t K,
+                  double s0, double amp, double period, double dx, double dy, double dz,
+                  double eta0, double eta_amp, double eta_period, double *T, double rtol, double *stats) {
+    const int64_t n = s->n;
+    const double dir[3] = {dx, dy, dz};
+    double tau[16], taue[256], sw[256], shat[256], stil[4096], semb[4096];
+    const int NE = M * P;
+    /* node states: Ts[m] (m = 0..M, Ts[0] = T(t_n)), Te[m][p] (p = 1..P, Te[m][P] = Ts[m]) */
+    double *buf = malloc(sizeof(double) * (size_t)n * (size_t)(2 * (M + 1) + 2 * (NE + M) + 2 * NE + M + 8));
+    if (!buf) return -2;
+    double *Ts = buf, *Tsn = Ts + n * (M + 1);              /* old / new standard-node states */
+    double *Te = Tsn + n * (M + 1), *Ten = Te + n * (NE + M); /* old / new embedded (p = 0..P) */
+    double *FE = Ten + n * (NE + M), *FI = FE + n * NE;     /* f^E(T_mp), f^I(T_j) + g */
+    double *Imm = FI + n * M, *rhs = Imm + n, *fs = rhs + n, *fe_new = fs + n, *fe_old = fe_new + n;
+    double *KvTk = fe_old + n, *tmp = KvTk + n, *Iemb = tmp + n;
+#define TE(arr, m, p) ((arr) + n * (size_t)((m - 1) * (P + 1) + (p)))   /* m = 1..M, p = 0..P */
+    int rc = 0;
+    for (int32_t step = 0; step < nsteps && !rc; step++) {
+        const double tn = t + (double)step * dt, dtm = dt / M, dtp = dt / (M * P);
+        or_mrsdc_weights(M, P, tn, dt, tau, taue, sw, shat, stil, semb);
+        double solves = 0, cgits = 0;
+        /* ---- Algorithm 1: predictor */
+        memcpy(Ts, T, sizeof(double) * (size_t)n);
+        for (int m = 1; m <= M; m++) {
+            double *Tprev = Ts + n * (m - 1);
+            for (int64_t i = 0; i < n; i++) rhs[i] = s->ML[i] * Tprev[i] + dtm * s->benv[i];
+            double *Tstar = Ts + n * m;
+            memcpy(Tstar, Tprev, sizeof(double) * (size_t)n);
+            int64_t it = pcg_shifted(s, dtm, rhs, Tstar, rtol, 10 * n);
+            if (it < 0) { rc = -4; break; }
+            solves += 1; cgits += (double)it;
+            apply_vol(s, Tstar, fs);
+            for (int64_t i = 0; i < n; i++) fs[i] += s->benv[i];          /* f*_m = f^I(T*) + g */
+            memcpy(TE(Te, m, 0), Tprev, sizeof(double) * (size_t)n);
+            for (int p = 1; p <= P; p++) {
+                double tprev = p == 1 ? (m == 1 ? tn : tau[m - 2]) : taue[(m - 1) * P + p - 2];
+                if (apply_fe(s, tprev, s0, amp, period, dir, eta0, eta_amp, eta_period, TE(Te, m, p - 1), fe_new)) { rc = -5; break; }
+                for (int64_t i = 0; i < n; i++)
+                    TE(Te, m, p)[i] = TE(Te, m, p - 1)[i] + dtp * (fs[i] + fe_new[i]) / s->ML[i];
+            }
+            if (rc) break;
+            memcpy(Ts + n * m, TE(Te, m, P), sizeof(double) * (size_t)n);
+        }
+        /* ---- Algorithm 2: K correction sweeps */
+        double res = 0.0;
+        for (int k = 0; k < K && !rc; k++) {
+            for (int j = 1; j <= M; j++) {                                 /* f^I(T^k_j) + g */
+                apply_vol(s, Ts + n * j, FI + n * (j - 1));
+                for (int64_t i = 0; i < n; i++) FI[n * (j - 1) + i] += s->benv[i];
+            }
+            for (int m = 1; m <= M && !rc; m++)
+                for (int p = 1; p <= P; p++)
+                    if (apply_fe(s, taue[(m - 1) * P + p - 1], s0, amp, period, dir, eta0, eta_amp, eta_period,
+                                 TE(Te, m, p), FE + n * ((m - 1) * P + p - 1))) { rc = -5; break; }
+            if (rc) break;
+            memcpy(Tsn, T, sizeof(double) * (size_t)n);                     /* T^{k+1}_0 = T(t_n) */
+            for (int m = 1; m <= M && !rc; m++) {
+                /* I_{m-1}^m */
+                for (int64_t i = 0; i < n; i++) {
+                    double acc = 0.0;
+                    for (int j = 0; j < M; j++) acc += sw[(m - 1) * M + j] * FI[n * j + i];
+                    for (int p = 0; p < P; p++) acc += shat[(m - 1) * P + p] * FE[n * ((m - 1) * P + p) + i];
+                    Imm[i] = acc;
+                }
+                apply_vol(s, Ts + n * m, KvTk);                             /* f^I(T^k_m) */
+                double *Tprev = Tsn + n * (m - 1);
+                for (int64_t i = 0; i < n; i++) rhs[i] = s->ML[i] * Tprev[i] - dtm * KvTk[i] + Imm[i];
+                memcpy(tmp, Ts + n * m, sizeof(double) * (size_t)n);       /* initial guess T^k_m */
+                int64_t it = pcg_shifted(s, dtm, rhs, tmp, rtol, 10 * n);
+                if (it < 0) { rc = -4; break; }
+                solves += 1; cgits += (double)it;
+                apply_vol(s, tmp, fs);
+                for (int64_t i = 0; i < n; i++) fs[i] -= KvTk[i];            /* f*_m = f^I(T*) - f^I(T^k_m) */
+                memcpy(TE(Ten, m, 0), Tprev, sizeof(double) * (size_t)n);
+                for (int p = 1; p <= P; p++) {
+                    double tprev = p == 1 ? (m == 1 ? tn : tau[m - 2]) : taue[(m - 1) * P + p - 2];
+                    /* I_{m,p-1}^p */
+                    for (int64_t i = 0; i < n; i++) {
+                        double acc = 0.0;
+                        for (int j = 0; j < M; j++) acc += stil[((m - 1) * P + p - 1) * M + j] * FI[n * j + i];
+                        for (int q = 0; q < P; q++) acc += semb[((m - 1) * P + p - 1) * P + q] * FE[n * ((m - 1) * P + q) + i];
+                        Iemb[i] = acc;
+                    }
+                    if (apply_fe(s, tprev, s0, amp, period, dir, eta0, eta_amp, eta_period, TE(Ten, m, p - 1), fe_new) ||
+                        apply_fe(s, tprev, s0, amp, period, dir, eta0, eta_amp, eta_period, TE(Te, m, p - 1), fe_old)) { rc = -5; break; }
+                    for (int64_t i = 0; i < n; i++)
+                        TE(Ten, m, p)[i] = TE(Ten, m, p - 1)[i] +
+                                           (dtp * fs[i] + dtp * (fe_new[i] - fe_old[i]) + Iemb[i]) / s->ML[i];
+                }
+                if (rc) break;
+                memcpy(Tsn + n * m, TE(Ten, m, P), sizeof(double) * (size_t)n);
+            }
+            if (rc) break;
+            /* T^{k+1} becomes T^k */
+            memcpy(Ts, Tsn, sizeof(double) * (size_t)n * (size_t)(M + 1));
+            memcpy(Te, Ten, sizeof(double) * (size_t)n * (size_t)(NE + M));
+            /* SDC residual of the new iterate at the standard nodes */
+            if (k == K - 1) {
+                for (int j = 1; j <= M; j++) {
+                    apply_vol(s, Ts + n * j, FI + n * (j - 1));
+                    for (int64_t i = 0; i < n; i++) FI[n * (j - 1) + i] += s->benv[i];
+                }
+                for (int m = 1; m <= M && !rc; m++)
+                    for (int p = 1; p <= P; p++)
+                        if (apply_fe(s, taue[(m - 1) * P + p - 1], s0, amp, period, dir, eta0, eta_amp, eta_period,
+                                     TE(Te, m, p), FE + n * ((m - 1) * P + p - 1))) { rc = -5; break; }
+                res = 0.0;
+                for (int64_t i = 0; i < n && !rc; i++) {
+                    double cum = 0.0;
+                    for (int m = 1; m <= M; m++) {
+                        for (int j = 0; j < M; j++) cum += sw[(m - 1) * M + j] * FI[n * j + i];
+                        for (int p = 0; p < P; p++) cum += shat[(m - 1) * P + p] * FE[n * ((m - 1) * P + p) + i];
+                        double v = fabs(s->ML[i] * (Ts[n * m + i] - T[i]) - cum);
+                        if (v > res) res = v;
+                    }
+                }
+            }
+        }
+        if (rc) break;
+        memcpy(T, Ts + n * M, sizeof(double) * (size_t)n);
+        if (stats) {
+            stats[3 * step + 0] = solves;
+            stats[3 * step + 1] = cgits;
+            stats[3 * step + 2] = res;
+        }
+    }
+#undef TE
+    free(buf);
+    return rc;
+}

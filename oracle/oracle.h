@@ -86,6 +86,20 @@ int or_ie_residual_rows(or_sys *s, double dt, double ox, double oy, double oz, d
 /* Apply y = K~ x with K~ = M_L - dt (A + B_env + K_G) (current interface). */
 void or_apply_system(const or_sys *s, double dt, const double *x, double *y);
 
+/* MRSDC: equidistant no-left standard nodes tau[M] of [t0, t0+dt], embedded
+ * nodes taue[M*P] and the weights of Table 1: s[M*M], shat[M*P], stilde[M*P*M], semb[M*P*P]
+ * (row-major in the index order of P:474-479), by exact integration of Lagrange polynomials. */
+int or_mrsdc_weights(int M, int P, double t0, double dt, double *tau, double *taue,
+                     double *s, double *shat, double *stilde, double *semb);
+
+/* MRSDC(M, P) with K sweeps: Algorithm 1 (predictor) then K x Algorithm 2, with
+ * f^I = (A + B_env) T, g = b_env, f^E = K_G(t) T + b_G(t).  Implicit solves
+ * (M_L - dt/M (A + B_env)) x = rhs by Jacobi-PCG to rtol.  stats: per step {solves,
+ * CG iterations, SDC residual r^K}.  T[N] in/out. */
+int or_step_mrsdc(or_sys *s, double t, double dt, int32_t nsteps, int32_t M, int32_t P, int32_t K,
+                  double s0, double amp, double period, double dx, double dy, double dz,
+                  double eta0, double eta_amp, double eta_period, double *T, double rtol, double *stats);
+
 #ifdef __cplusplus
 }
 #endif
