@@ -120,6 +120,16 @@ int thermo_get_T(void *ctx, int32_t scen, int32_t part, double *out, int64_t n,
 int thermo_set_T(void *ctx, int32_t scen, int32_t part, const double *in, int64_t n,
                  int32_t in_on_device);
 
+/* Time-stepping method for thermo_step:
+ *   method 0 (default): implicit Euler on the fully coupled system (above);
+ *   method 1: multi-rate SDC, MRSDC(M, P) with K correction sweeps:
+ *     f^I(T) = (A + B_env) T implicit with one solve of (M_L - dt/M (A + B_env)) per standard
+ *     interval, f^E(T, t) = K_G(t) T + b_G(t) explicit on P embedded sub-steps (Algorithms 1-2),
+ *     equidistant no-left nodes, Table-1 quadrature.  The paper's 3-D runs use M = 3, P = 2,
+ *     K = 0..2.  Requires a single scenario.
+ * EINVAL for other methods, M or P outside [1, 8], K < 0, or method 1 with n_scen > 1. */
+int thermo_set_method(void *ctx, int32_t method, int32_t M, int32_t P, int32_t K);
+
 /* CG stopping rule ||r||_2 <= rtol ||b||_2 (default 1e-12) and iteration cap
  * (default 0 = min(10 N, 10000)).  EINVAL if rtol <= 0 or maxit < 0. */
 int thermo_set_solver(void *ctx, double rtol, int32_t maxit);

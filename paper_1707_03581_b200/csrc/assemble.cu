@@ -290,7 +290,7 @@ __global__ void k_build_vals(const double *A, const double *R, int64_t n, double
 }
 
 __global__ void k_build_diag(const int64_t *diagpos, const double *ML, int64_t N, double *val,
-                             double *Dvol, double *Dinv) {
+                             double *Dvol, double *Dinv, double *Dinv_vol) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= N) return;
     int64_t e = diagpos[i];
@@ -298,6 +298,13 @@ __global__ void k_build_diag(const int64_t *diagpos, const double *ML, int64_t N
     val[e] = d;
     Dvol[i] = d;
     Dinv[i] = 1.0 / d;
+    Dinv_vol[i] = 1.0 / d;
+}
+
+// f^I operator values A + B_env (MRSDC)
+__global__ void k_build_kv(const double *A, const double *R, int64_t n, double *KV) {
+    int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e < n) KV[e] = A[e] + R[e];
 }
 
 // ------------------------------------------------------------------------------ host side
@@ -412,7 +419,11 @@ int build_operator(Ctx &c, double dt) {
     cudaStream_t st = c.stream;
     k_build_vals<<<nb(c.nnz_pad), 256, 0, st>>>(c.d_A, c.d_R, c.nnz_pad, dt, c.d_val);
     CK(cudaGetLastError());
-    k_build_diag<<<nb(c.N), 256, 0, st>>>(c.d_diagpos, c.d_ML, c.N, c.d_val, c.d_Dvol, c.d_Dinv);
+    if (!c.d_Dinv_vol) CK(cudaMalloc(&c.d_Dinv_vol, sizeof(double) * c.N));
+    k_build_diag<<<nb(c.N), 256, 0, st>>>(c.d_diagpos, c.d_ML, c.N, c.d_val, c.d_Dvol, c.d_Dinv, c.d_Dinv_vol);
+    CK(cudaGetLastError());
+    if (!c.d_KV) CK(cudaMalloc(&c.d_KV, sizeof(double) * (c.nnz_pad + 1)));
+    k_build_kv<<<nb(c.nnz_pad), 256, 0, st>>>(c.d_A, c.d_R, c.nnz_pad, c.d_KV);
     CK(cudaGetLastError());
     c.built_dt = dt;
     return 0;

@@ -62,6 +62,7 @@ struct CGParams {
     const int32_t *if_rows, *slice_if, *ell_cnt, *ell_col;
     const double *ell_val, *if_b, *if_phi;
     const double *T_in;
+    const double *rhs;         // optional explicit right-hand side (MRSDC implicit solves)
     double *T_out, *z, *pa, *pb, *q;
     double *partials;
     int *status;
@@ -479,7 +480,7 @@ __global__ void __launch_bounds__(cg_threads(KIND, W, NG), KIND == 0 ? 2 : 1) k_
         if (i < N) {
             double bi = be;
             if (ik >= 0) bi += P.if_b[ik];
-            bi = fma(ml, Ti, P.dt * bi);
+            bi = P.rhs ? P.rhs[i] : fma(ml, Ti, P.dt * bi);
             const double r = bi - ax;
             const double zi = di * r;
             P.z[i] = zi;
@@ -809,6 +810,60 @@ int cg_setup(Ctx &c) {
     CK(cudaGetLastError());
     c.cg_grid = (kVariants[chosen].kind == 0 ? per_sm : 1) * c.num_sms;
     CK(cudaMalloc(&c.d_partials, sizeof(double) * THERMO_NRED * c.cg_grid));
+    return 0;
+}
+
+int cg_launch_solve(Ctx &c, const double *x0, double *x, const double *rhs, const double *Dinv, bool iface,
+                    int32_t *iters_out, double *relres_out, int slot) {
+    CGParams P;
+    memset(&P, 0, sizeof P);
+    P.N = c.N;
+    P.nslices = c.nslices;
+    P.nchunks = (c.nslices + c.cg_chunk - 1) / c.cg_chunk;
+    P.slice_ptr = c.d_slice_ptr;
+    P.col = c.d_col;
+    P.lcol = c.d_lcol;
+    P.val = c.d_val;
+    P.ML = c.d_ML;
+    P.benv = c.d_benv;
+    P.Dinv = Dinv;
+    P.n_if = iface ? c.n_if : 0;
+    P.nA = c.nA;
+    P.if_rows = c.d_if_rows;
+    P.slice_if = iface ? c.d_slice_if : c.d_slice_if_zero;
+    P.ell_cnt = c.d_ell_cnt;
+    P.ell_col = c.d_ell_col;
+    P.ell_val = c.d_ell_val;
+    P.if_b = c.d_if_b;
+    P.if_phi = c.d_if_phi;
+    P.T_in = x0;
+    P.rhs = rhs;
+    P.T_out = x;
+    P.z = c.d_z;
+    P.pa = c.d_p[0];
+    P.pb = c.d_p[1];
+    P.q = c.d_q;
+    P.partials = c.d_partials;
+    P.status = c.d_status;
+    P.fail_relres = c.d_fail_relres;
+    P.iters_out = iters_out;
+    P.relres_out = relres_out;
+    P.area_out = c.d_area;
+    P.dt = 0.0;
+    P.rtol2 = c.rtol * c.rtol;
+    P.maxit = c.maxit > 0 ? c.maxit : (int)std::min<int64_t>(10 * c.N, 10000);
+    P.step = slot;
+    P.stage_entries = c.cg_stage_entries;
+    P.nstages = c.cg_nstages;
+    P.win_cap = c.cg_win_cap;
+    P.chunk_hi = c.d_chunk_hi;
+    P.chunk_runs = c.d_chunk_runs;
+    P.chunk_nruns = c.d_chunk_nruns;
+    P.chunk_lown = c.d_chunk_lown;
+    P.trace = nullptr;
+    void *args[] = {&P};
+    CK(cudaLaunchCooperativeKernel(variant_kernel(c.cg_variant), dim3(c.cg_grid), dim3(c.cg_block), args,
+                                   c.cg_smem, c.stream));
     return 0;
 }
 

@@ -215,6 +215,7 @@ struct IfaceParams {
     double *if_dinv;          // (unused)
     double *DinvS;            // S > 1: [N][SP] per-scenario Jacobi inverse diagonal
     int SP;                   // S > 1: row stride of the block vectors (even, >= S)
+    int no_dinv;              // 1: leave the Jacobi diagonal alone (MRSDC: f^E is explicit)
     int *status;              // status[1] |= overflow
 };
 

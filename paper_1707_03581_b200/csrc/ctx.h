@@ -105,6 +105,20 @@ struct Ctx {
 
     double rtol = 1e-12;
     int maxit = 0;
+    // time-stepping method: 0 implicit Euler, 1 MRSDC(M, P) with K sweeps
+    int method = 0, mr_M = 3, mr_P = 2, mr_K = 1;
+    int32_t *d_slice_if_zero = nullptr;   // all-empty interface ranges (volume-only solves)
+    double *d_KV = nullptr;               // A + B_env values (sliced ELL), f^I operator
+    double *d_Dinv_vol = nullptr;         // 1 / diag(M_L - a (A + B_env)), untouched by the interface
+    int32_t *d_if_of_row = nullptr;       // [N] interface index of a row or -1
+    double *d_mr = nullptr;               // MRSDC node states and caches (see mrsdc.cu)
+    size_t mr_vectors = 0;
+    int32_t *d_mr_iters = nullptr;        // per implicit solve of the last step
+    double *d_mr_relres = nullptr;
+    int32_t *d_ell_cnt_s = nullptr, *d_ell_col_s = nullptr;   // MRSDC: interface operators at the
+    double *d_ell_val_s = nullptr, *d_if_b_s = nullptr;       // M P + 1 node times of a step
+    double *d_if_phi_s = nullptr;
+    int mr_nslots = 0, mr_solves = 0;
     bool timing = false;
     std::vector<cudaEvent_t> events;   // 2 * nsteps + 1 when timing
     double ms_iface = 0.0, ms_solve = 0.0;
@@ -133,6 +147,14 @@ int iface_launch(Ctx &c, const IfaceParams &p);
 // cg.cu
 int cg_setup(Ctx &c);
 int cg_launch_step(Ctx &c, int step, double dt);
+// Solve (M_L - a K_vol [- a K_G]) x = rhs from x0 with the operator currently in d_val (a =
+// built_dt); iface = false: no interface rows.  Iterations / residual to iters_out[slot].
+int cg_launch_solve(Ctx &c, const double *x0, double *x, const double *rhs, const double *Dinv, bool iface,
+                    int32_t *iters_out, double *relres_out, int slot);
+
+// mrsdc.cu (multi-rate SDC)
+int mrsdc_setup(Ctx &c);
+int mrsdc_step(Ctx &c, double tn, double dt, int step_index);
 
 // cg_batched.cu (S > 1 scenarios advanced together)
 int cgb_setup(Ctx &c);

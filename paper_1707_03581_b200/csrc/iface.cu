@@ -380,8 +380,12 @@ __global__ void __launch_bounds__(32 * ROW_WPB) k_rows(IfaceParams P) {
         P.if_phi[(int64_t)k * P.S + s] = phi;
         P.if_b[(int64_t)k * P.S + s] = 0.5 * P.step_sc[4 * s + 2] * phi;
         const double dinv = 1.0 / (P.Dvol[row] + dself);
-        if (P.S == 1) P.Dinv[row] = dinv;
-        else P.DinvS[(int64_t)row * P.SP + s] = dinv;
+        if (P.no_dinv) {
+        } else if (P.S == 1) {
+            P.Dinv[row] = dinv;
+        } else {
+            P.DinvS[(int64_t)row * P.SP + s] = dinv;
+        }
     }
 }
 
@@ -529,6 +533,10 @@ int iface_setup(Ctx &c, const double *X, const std::vector<int32_t> &fA, const s
     for (int64_t s = 0; s <= c.nslices; ++s)
         slice_if[s] = (int32_t)(std::lower_bound(rows.begin(), rows.end(), (int32_t)std::min<int64_t>(32 * s, INT32_MAX)) - rows.begin());
     if (int rc = upload(c, &c.d_slice_if, slice_if)) return rc;
+    {
+        std::vector<int32_t> zeros(c.nslices + 1, 0);
+        if (int rc = upload(c, &c.d_slice_if_zero, zeros)) return rc;
+    }
     if (c.n_if == 0) return 0;
     if (nTA == 0 || nTB == 0) { c.err = "interface tag present on only one part"; return -1; }
 

@@ -1,0 +1,406 @@
+// mrsdc.cu -- multi-rate spectral deferred corrections, the paper's method, on the
+// B200 kernels of the implicit-Euler path.
+//
+// Splitting: f^I(T) = (A + B_env) T (slow, implicit), g = b_env, f^E(T, t) =
+// K_G(t) T + b_G(t) (interface coupling and friction, fast, explicit).  One step of size dt:
+// M equidistant no-left standard nodes, P embedded nodes per standard interval.
+//   Algorithm 1 (predictor): per standard interval one implicit solve
+//       (M_L - dt/M (A + B_env)) T* = M_L T_{m-1} + dt/M g,   f* = f^I(T*) + g
+//     then P explicit Euler sub-steps in f^E:  M_L T_{m,p} = M_L T_{m,p-1} + dt/(MP) (f* + f^E(T_{m,p-1}))
+//   Algorithm 2 (sweep k -> k+1): the same structure with the quadrature terms I_{m-1}^m,
+//     I_{m,p-1}^p of Table 1 built from the previous iterate.
+// The implicit operator M_L - dt/M (A + B_env) never changes within a run, so the persistent CG
+// kernel of cg.cu is reused with an explicit right-hand side and no interface rows; the
+// interface operators K_G(t) at the M P + 1 node times of a step are integrated once per
+// step by the interface kernels (unscaled, dt = -1) and applied explicitly.
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "ctx.h"
+
+namespace thermo {
+
+#define CK(x)                                                                    \
+    do {                                                                         \
+        cudaError_t e_ = (x);                                                    \
+        if (e_ != cudaSuccess) {                                                 \
+            c.err = std::string("CUDA: ") + cudaGetErrorString(e_) + " at " #x; \
+            return -3;                                                           \
+        }                                                                        \
+    } while (0)
+
+#define MR_MAX 8
+
+struct MrW {            // one row of a weight family (by value)
+    double a[MR_MAX];
+    double b[MR_MAX];
+};
+
+static inline unsigned nbk(int64_t n, int t = 256) { return (unsigned)((n + t - 1) / t); }
+
+// y_i = sum_j (A + B_env)_ij x_j + sgn * addv_i   (sliced ELL, thread per row)
+__global__ void k_vol_apply(const int64_t *slice_ptr, const int32_t *col, const double *KV, int64_t N,
+                            const double *x, const double *addv, double sgn, double *y) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    const int64_t s = i >> 5;
+    const int lane = (int)(i & 31);
+    const int64_t b0 = slice_ptr[s], w = (slice_ptr[s + 1] - b0) >> 5;
+    double acc = 0.0;
+    for (int64_t k = 0; k < w; ++k) acc = fma(KV[b0 + 32 * k + lane], x[col[b0 + 32 * k + lane]], acc);
+    if (addv) acc = fma(sgn, addv[i], acc);
+    y[i] = acc;
+}
+
+// compact f^E on the interface rows: y[k] = b_G[k] + sum_c K_G[k][c] x[col]
+__global__ void k_fe_apply(int n_if, const int32_t *cnt, const int32_t *ecol, const double *evals, const double *bG,
+                           const double *x, double *y) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n_if) return;
+    double acc = bG[k];
+    const int m = cnt[k];
+    for (int c = 0; c < m; ++c) acc = fma(evals[(int64_t)c * n_if + k], x[ecol[(int64_t)c * n_if + k]], acc);
+    y[k] = acc;
+}
+
+// right-hand side of an implicit solve.
+//  predictor:  rhs = M_L Tprev + a g
+//  sweep:      rhs = M_L Tprev - a f^I(T^k_m) + I_{m-1}^m,
+//              I_{m-1}^m = sum_j s_mj (f^I(T_j) + g) + sum_p shat_mp f^E(T_mp)
+__global__ void k_mr_rhs(int64_t N, int64_t ldf, const double *ML, const double *Tprev, const double *benv,
+                         const double *KvTk, double a, const double *FI, const double *FE, const int32_t *if_of_row,
+                         int n_if, int M, int P, MrW w, double *rhs) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    double r = ML[i] * Tprev[i];
+    if (!KvTk) {
+        r = fma(a, benv[i], r);
+    } else {
+        double I = 0.0;
+        for (int j = 0; j < M; ++j) I = fma(w.a[j], FI[(int64_t)j * ldf + i], I);
+        const int k = if_of_row[i];
+        if (k >= 0)
+            for (int p = 0; p < P; ++p) I = fma(w.b[p], FE[(int64_t)p * n_if + k], I);
+        r = fma(-a, KvTk[i], r) + I;
+    }
+    rhs[i] = r;
+}
+
+// one embedded explicit-Euler sub-step (Algorithm 1 / 2 inner loop)
+//  predictor: T = Tprev + dtp (fs + fe_new) / M_L
+//  sweep:     T = Tprev + (dtp fs + dtp (fe_new - fe_old) + I_{m,p-1}^p) / M_L,
+//             I_{m,p-1}^p = sum_j st_j (f^I(T_j) + g) + sum_q se_q f^E(T_mq)
+__global__ void k_mr_emb(int64_t N, int64_t ldf, const double *ML, const double *Tprev, const double *fs,
+                         const double *fe_new, const double *fe_old, double dtp, const double *FI, const double *FE,
+                         const int32_t *if_of_row, int n_if, int M, int P, MrW w, double *Tout) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    const int k = if_of_row[i];
+    double num;
+    if (!fe_old) {
+        num = dtp * (fs[i] + (k >= 0 ? fe_new[k] : 0.0));
+    } else {
+        double I = 0.0;
+        for (int j = 0; j < M; ++j) I = fma(w.a[j], FI[(int64_t)j * ldf + i], I);
+        double fe = 0.0;
+        if (k >= 0) {
+            for (int q = 0; q < P; ++q) I = fma(w.b[q], FE[(int64_t)q * n_if + k], I);
+            fe = fe_new[k] - fe_old[k];
+        }
+        num = dtp * fs[i] + dtp * fe + I;
+    }
+    Tout[i] = Tprev[i] + num / ML[i];
+}
+
+__global__ void k_if_of_row(const int32_t *if_rows, int n_if, int32_t *map) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n_if) map[if_rows[k]] = k;
+}
+
+// ---------------------------------------------------------------------------------
+// Table 1 weights on the host: exact integrals of Lagrange polynomials.
+// ---------------------------------------------------------------------------------
+static double lag_int(const double *x, int n, int j, double a, double b) {
+    // l_j(s) = prod_{k != j} (s - x_k) / (x_j - x_k), integrated by Gauss-Legendre with n
+    // points (exact for degree n - 1 <= 2n - 1)
+    static const double gx[8][8] = {
+        {0},
+        {-0.5773502691896257, 0.5773502691896257},
+        {-0.7745966692414834, 0.0, 0.7745966692414834},
+        {-0.8611363115940526, -0.3399810435848563, 0.3399810435848563, 0.8611363115940526},
+        {-0.9061798459386640, -0.5384693101056831, 0.0, 0.5384693101056831, 0.9061798459386640},
+        {-0.9324695142031521, -0.6612093864662645, -0.2386191860831969, 0.2386191860831969, 0.6612093864662645,
+         0.9324695142031521},
+        {-0.9491079123427585, -0.7415311855993945, -0.4058451513773972, 0.0, 0.4058451513773972,
+         0.7415311855993945, 0.9491079123427585},
+        {-0.9602898564975363, -0.7966664774136267, -0.5255324099163290, -0.1834346424956498,
+         0.1834346424956498, 0.5255324099163290, 0.7966664774136267, 0.9602898564975363}};
+    static const double gw[8][8] = {
+        {2.0},
+        {1.0, 1.0},
+        {0.5555555555555556, 0.8888888888888888, 0.5555555555555556},
+        {0.3478548451374538, 0.6521451548625461, 0.6521451548625461, 0.3478548451374538},
+        {0.2369268850561891, 0.4786286704993665, 0.5688888888888889, 0.4786286704993665, 0.2369268850561891},
+        {0.1713244923791704, 0.3607615730481386, 0.4679139345726910, 0.4679139345726910, 0.3607615730481386,
+         0.1713244923791704},
+        {0.1294849661688697, 0.2797053914892766, 0.3818300505051189, 0.4179591836734694, 0.3818300505051189,
+         0.2797053914892766, 0.1294849661688697},
+        {0.1012285362903763, 0.2223810344533745, 0.3137066458778873, 0.3626837833783620, 0.3626837833783620,
+         0.3137066458778873, 0.2223810344533745, 0.1012285362903763}};
+    const int ng = n;   // n points integrate the degree n-1 polynomial exactly
+    double acc = 0.0;
+    const double hm = 0.5 * (b - a), cm = 0.5 * (a + b);
+    for (int g = 0; g < ng; ++g) {
+        const double sx = cm + hm * gx[ng - 1][g];
+        double l = 1.0;
+        for (int k = 0; k < n; ++k)
+            if (k != j) l *= (sx - x[k]) / (x[j] - x[k]);
+        acc += gw[ng - 1][g] * l;
+    }
+    return acc * hm;
+}
+
+struct MrTables {
+    double tau[MR_MAX + 1];                 // tau[0] = t_n, tau[m] = standard node m
+    double s[MR_MAX][MR_MAX];               // s[m-1][j]
+    double shat[MR_MAX][MR_MAX];            // shat[m-1][p]
+    double st[MR_MAX][MR_MAX][MR_MAX];      // stilde[m-1][p-1][j]
+    double se[MR_MAX][MR_MAX][MR_MAX];      // s_{m,p,q}[m-1][p-1][q]
+};
+
+static void mr_tables(int M, int P, double tn, double dt, MrTables &T) {
+    // work on the unit step (weights scale with dt)
+    double x[MR_MAX];
+    T.tau[0] = 0.0;
+    for (int m = 1; m <= M; ++m) T.tau[m] = (double)m / M;
+    for (int m = 0; m < M; ++m) x[m] = T.tau[m + 1];
+    for (int m = 1; m <= M; ++m) {
+        double e[MR_MAX];
+        for (int p = 1; p <= P; ++p) e[p - 1] = T.tau[m - 1] + (T.tau[m] - T.tau[m - 1]) * p / P;
+        for (int j = 0; j < M; ++j) T.s[m - 1][j] = dt * lag_int(x, M, j, T.tau[m - 1], T.tau[m]);
+        for (int p = 0; p < P; ++p) T.shat[m - 1][p] = dt * lag_int(e, P, p, T.tau[m - 1], T.tau[m]);
+        for (int p = 1; p <= P; ++p) {
+            const double lo = p == 1 ? T.tau[m - 1] : e[p - 2], hi = e[p - 1];
+            for (int j = 0; j < M; ++j) T.st[m - 1][p - 1][j] = dt * lag_int(x, M, j, lo, hi);
+            for (int q = 0; q < P; ++q) T.se[m - 1][p - 1][q] = dt * lag_int(e, P, q, lo, hi);
+        }
+    }
+    for (int m = 0; m <= M; ++m) T.tau[m] = tn + dt * T.tau[m];
+}
+
+// ---------------------------------------------------------------------------------
+// setup and one step
+// ---------------------------------------------------------------------------------
+struct MrPtr {
+    double *TSo[MR_MAX + 1], *TSn[MR_MAX + 1];
+    double *TEo[MR_MAX][MR_MAX + 1], *TEn[MR_MAX][MR_MAX + 1];   // [m-1][p], p = 0..P
+    double *FI, *FE, *fe_new, *fe_old, *fs, *rhs, *Tstar, *KvTk;
+};
+
+int mrsdc_setup(Ctx &c) {
+    const int M = c.mr_M, P = c.mr_P;
+    const int64_t N = c.N, nif = std::max(c.n_if, 1);
+    const int64_t Np = (N + 31) & ~(int64_t)31;   // 256-byte aligned vectors (TMA windows, 16-B loads)
+    const size_t nfull = 2 * (size_t)M + 2 * (size_t)M * (P - 1) + M + 4;   // TS (1..M) x2, interior TE x2, FI, 4 temps
+    const size_t ncomp = (size_t)M * P + 2;
+    if (c.d_mr) cudaFree(c.d_mr);
+    CK(cudaMalloc(&c.d_mr, sizeof(double) * (nfull * Np + ncomp * nif + 64)));
+    CK(cudaMemsetAsync(c.d_mr, 0, sizeof(double) * (nfull * Np + ncomp * nif + 64), c.stream));
+    c.mr_vectors = nfull;
+    if (!c.d_if_of_row) {
+        CK(cudaMalloc(&c.d_if_of_row, sizeof(int32_t) * N));
+        CK(cudaMemsetAsync(c.d_if_of_row, 0xff, sizeof(int32_t) * N, c.stream));
+        if (c.n_if) k_if_of_row<<<nbk(c.n_if), 256, 0, c.stream>>>(c.d_if_rows, c.n_if, c.d_if_of_row);
+        CK(cudaGetLastError());
+    }
+    // interface operators at the M P + 1 node times of a step
+    const int nslot = M * P + 1;
+    if (c.mr_nslots < nslot && c.n_if) {
+        for (void *p : {(void *)c.d_ell_cnt_s, (void *)c.d_ell_col_s, (void *)c.d_ell_val_s, (void *)c.d_if_b_s,
+                        (void *)c.d_if_phi_s})
+            if (p) cudaFree(p);
+        CK(cudaMalloc(&c.d_ell_cnt_s, sizeof(int32_t) * nslot * nif));
+        CK(cudaMalloc(&c.d_ell_col_s, sizeof(int32_t) * (size_t)nslot * c.cap * nif));
+        CK(cudaMalloc(&c.d_ell_val_s, sizeof(double) * (size_t)nslot * c.cap * nif));
+        CK(cudaMalloc(&c.d_if_b_s, sizeof(double) * nslot * nif));
+        CK(cudaMalloc(&c.d_if_phi_s, sizeof(double) * nslot * nif));
+        c.mr_nslots = nslot;
+    }
+    if (!c.d_mr_iters) {
+        CK(cudaMalloc(&c.d_mr_iters, sizeof(int32_t) * MR_MAX * (MR_MAX + 64)));
+        CK(cudaMalloc(&c.d_mr_relres, sizeof(double) * MR_MAX * (MR_MAX + 64)));
+    }
+    return 0;
+}
+
+static MrPtr mr_pointers(Ctx &c, double *T0) {
+    const int M = c.mr_M, P = c.mr_P;
+    const int64_t N = (c.N + 31) & ~(int64_t)31, nif = std::max(c.n_if, 1);   // padded vector stride
+    MrPtr q;
+    double *p = c.d_mr;
+    q.TSo[0] = q.TSn[0] = T0;
+    for (int m = 1; m <= M; ++m) { q.TSo[m] = p; p += N; }
+    for (int m = 1; m <= M; ++m) { q.TSn[m] = p; p += N; }
+    for (int m = 1; m <= M; ++m) {
+        q.TEo[m - 1][0] = q.TSo[m - 1];
+        q.TEn[m - 1][0] = q.TSn[m - 1];
+        for (int e = 1; e < P; ++e) { q.TEo[m - 1][e] = p; p += N; }
+        for (int e = 1; e < P; ++e) { q.TEn[m - 1][e] = p; p += N; }
+        q.TEo[m - 1][P] = q.TSo[m];
+        q.TEn[m - 1][P] = q.TSn[m];
+    }
+    q.FI = p; p += (size_t)M * N;
+    q.fs = p; p += N;
+    q.rhs = p; p += N;
+    q.Tstar = p; p += N;
+    q.KvTk = p; p += N;
+    q.FE = p; p += (size_t)M * P * nif;
+    q.fe_new = p; p += nif;
+    q.fe_old = p; p += nif;
+    return q;
+}
+
+int mrsdc_step(Ctx &c, double tn, double dt, int step_index) {
+    const int M = c.mr_M, P = c.mr_P, K = c.mr_K;
+    const int64_t N = c.N;
+    const int nif = c.n_if;
+    const double a = dt / M, dtp = dt / (M * P);
+    const int64_t ldf = (N + 31) & ~(int64_t)31;
+    cudaStream_t st = c.stream;
+    if (c.built_dt != a) {
+        if (build_operator(c, a)) return -3;
+    }
+    MrTables W;
+    mr_tables(M, P, tn, dt, W);
+    // ---- interface operators K_G, b_G at the node times t_n + q dt/(MP), q = 0..MP
+    const int nslot = M * P + 1;
+    std::vector<double> sc(4 * (size_t)nslot);
+    const Scen &sn = c.scen[0];
+    for (int q = 0; q < nslot; ++q) {
+        const double tq = tn + dt * (double)q / (double)(M * P);
+        const double sv = sn.s0 + sn.amp * std::sin(2.0 * M_PI * tq / sn.period);
+        sc[4 * q + 0] = sv * sn.d2[0];
+        sc[4 * q + 1] = sv * sn.d2[1];
+        sc[4 * q + 2] = sn.eta0 * (1.0 + sn.eta_amp * std::sin(2.0 * M_PI * tq / sn.eta_period));
+        sc[4 * q + 3] = sv;
+    }
+    if ((int64_t)nslot > c.step_cap) {
+        for (void *p : {(void *)c.d_step_sc, (void *)c.d_iters, (void *)c.d_relres, (void *)c.d_area})
+            if (p) cudaFree(p);
+        c.step_cap = nslot;
+        CK(cudaMalloc(&c.d_step_sc, sizeof(double) * 4 * (size_t)nslot));
+        CK(cudaMalloc(&c.d_iters, sizeof(int32_t) * (size_t)nslot));
+        CK(cudaMalloc(&c.d_relres, sizeof(double) * (size_t)nslot));
+        CK(cudaMalloc(&c.d_area, sizeof(double) * (size_t)nslot));
+    }
+    CK(cudaMemcpyAsync(c.d_step_sc, sc.data(), sizeof(double) * sc.size(), cudaMemcpyHostToDevice, st));
+    const size_t ell_stride = (size_t)c.cap * std::max(nif, 1);
+    auto slot_ptrs = [&](int q, const int32_t *&cnt, const int32_t *&col, const double *&val, const double *&b) {
+        cnt = c.d_ell_cnt_s + (size_t)q * nif;
+        col = c.d_ell_col_s + (size_t)q * ell_stride;
+        val = c.d_ell_val_s + (size_t)q * ell_stride;
+        b = c.d_if_b_s + (size_t)q * nif;
+    };
+    if (nif) {
+        for (int q = 0; q < nslot; ++q) {
+            IfaceParams Pf;
+            memset(&Pf, 0, sizeof Pf);
+            iface_params(c, Pf, c.d_step_sc + 4 * q, -1.0);   // dt = -1: K_G = M_B + C_B unscaled
+            Pf.ell_cnt = c.d_ell_cnt_s + (size_t)q * nif;
+            Pf.ell_col = c.d_ell_col_s + (size_t)q * ell_stride;
+            Pf.ell_val = c.d_ell_val_s + (size_t)q * ell_stride;
+            Pf.if_b = c.d_if_b_s + (size_t)q * nif;
+            Pf.if_phi = c.d_if_phi_s + (size_t)q * nif;
+            Pf.no_dinv = 1;
+            if (iface_launch(c, Pf)) return -3;
+        }
+    }
+    double *T0 = c.d_T[c.cur];
+    MrPtr q = mr_pointers(c, T0);
+    auto fe_apply = [&](int slot, const double *x, double *y) -> int {
+        if (!nif) return 0;
+        const int32_t *cnt, *col;
+        const double *val, *b;
+        slot_ptrs(slot, cnt, col, val, b);
+        k_fe_apply<<<nbk(nif), 256, 0, st>>>(nif, cnt, col, val, b, x, y);
+        CK(cudaGetLastError());
+        return 0;
+    };
+    auto vol_apply = [&](const double *x, const double *addv, double sgn, double *y) -> int {
+        k_vol_apply<<<nbk(N), 256, 0, st>>>(c.d_slice_ptr, c.d_col, c.d_KV, N, x, addv, sgn, y);
+        CK(cudaGetLastError());
+        return 0;
+    };
+    int solve_no = 0;
+    auto solve = [&](const double *x0, double *x, const double *rhs) -> int {
+        const int slot = solve_no++;
+        return cg_launch_solve(c, x0, x, rhs, c.d_Dinv_vol, false, c.d_mr_iters, c.d_mr_relres, slot);
+    };
+    MrW w0;
+    memset(&w0, 0, sizeof w0);
+    // ---- Algorithm 1: predictor
+    for (int m = 1; m <= M; ++m) {
+        k_mr_rhs<<<nbk(N), 256, 0, st>>>(N, ldf, c.d_ML, q.TSo[m - 1], c.d_benv, nullptr, a, nullptr, nullptr,
+                                         c.d_if_of_row, nif, M, P, w0, q.rhs);
+        CK(cudaGetLastError());
+        if (solve(q.TSo[m - 1], q.Tstar, q.rhs)) return -3;
+        if (vol_apply(q.Tstar, c.d_benv, 1.0, q.fs)) return -3;   // f* = f^I(T*) + g
+        for (int p = 1; p <= P; ++p) {
+            if (fe_apply((m - 1) * P + p - 1, q.TEo[m - 1][p - 1], q.fe_new)) return -3;
+            k_mr_emb<<<nbk(N), 256, 0, st>>>(N, ldf, c.d_ML, q.TEo[m - 1][p - 1], q.fs, q.fe_new, nullptr, dtp, nullptr,
+                                             nullptr, c.d_if_of_row, nif, M, P, w0, q.TEo[m - 1][p]);
+            CK(cudaGetLastError());
+        }
+    }
+    // ---- Algorithm 2: K correction sweeps
+    for (int k = 0; k < K; ++k) {
+        for (int j = 1; j <= M; ++j)
+            if (vol_apply(q.TSo[j], c.d_benv, 1.0, q.FI + (size_t)(j - 1) * ldf)) return -3;   // f^I(T^k_j) + g
+        for (int m = 1; m <= M; ++m)
+            for (int p = 1; p <= P; ++p)
+                if (fe_apply((m - 1) * P + p, q.TEo[m - 1][p], q.FE + (size_t)((m - 1) * P + p - 1) * std::max(nif, 1)))
+                    return -3;
+        for (int m = 1; m <= M; ++m) {
+            MrW wr;
+            memset(&wr, 0, sizeof wr);
+            for (int j = 0; j < M; ++j) wr.a[j] = W.s[m - 1][j];
+            for (int p = 0; p < P; ++p) wr.b[p] = W.shat[m - 1][p];
+            if (vol_apply(q.TSo[m], nullptr, 0.0, q.KvTk)) return -3;                 // f^I(T^k_m)
+            const double *FEm = q.FE + (size_t)(m - 1) * P * std::max(nif, 1);
+            k_mr_rhs<<<nbk(N), 256, 0, st>>>(N, ldf, c.d_ML, q.TSn[m - 1], c.d_benv, q.KvTk, a, q.FI, FEm, c.d_if_of_row,
+                                             nif, M, P, wr, q.rhs);
+            CK(cudaGetLastError());
+            if (solve(q.TSo[m], q.Tstar, q.rhs)) return -3;
+            if (vol_apply(q.Tstar, q.KvTk, -1.0, q.fs)) return -3;                    // f^I(T*) - f^I(T^k_m)
+            for (int p = 1; p <= P; ++p) {
+                MrW we;
+                memset(&we, 0, sizeof we);
+                for (int j = 0; j < M; ++j) we.a[j] = W.st[m - 1][p - 1][j];
+                for (int qq = 0; qq < P; ++qq) we.b[qq] = W.se[m - 1][p - 1][qq];
+                const int slot = (m - 1) * P + p - 1;
+                if (fe_apply(slot, q.TEn[m - 1][p - 1], q.fe_new)) return -3;
+                if (fe_apply(slot, q.TEo[m - 1][p - 1], q.fe_old)) return -3;
+                k_mr_emb<<<nbk(N), 256, 0, st>>>(N, ldf, c.d_ML, q.TEn[m - 1][p - 1], q.fs, q.fe_new, q.fe_old, dtp, q.FI,
+                                                 FEm, c.d_if_of_row, nif, M, P, we, q.TEn[m - 1][p]);
+                CK(cudaGetLastError());
+            }
+        }
+        // T^{k+1} becomes T^k
+        for (int m = 1; m <= M; ++m) std::swap(q.TSo[m], q.TSn[m]);
+        for (int m = 1; m <= M; ++m) {
+            for (int e = 1; e < P; ++e) std::swap(q.TEo[m - 1][e], q.TEn[m - 1][e]);
+            q.TEo[m - 1][0] = q.TSo[m - 1];
+            q.TEn[m - 1][0] = q.TSn[m - 1];
+            q.TEo[m - 1][P] = q.TSo[m];
+            q.TEn[m - 1][P] = q.TSn[m];
+        }
+    }
+    // ---- commit T(t_{n+1}) = T_M
+    CK(cudaMemcpyAsync(c.d_T[c.cur ^ 1], q.TSo[M], sizeof(double) * N, cudaMemcpyDeviceToDevice, st));
+    c.mr_solves = solve_no;
+    (void)step_index;
+    return 0;
+}
+
+}  // namespace thermo

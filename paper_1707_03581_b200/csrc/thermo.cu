@@ -4,6 +4,7 @@
 // t' = t + (n+1) dt, s(t'), eta(t') (reading R3) and kernel launches.
 // Every arithmetic step of the hot path runs in the kernels of assemble.cu, iface.cu and
 // cg.cu.  No CPU fallback exists.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -42,7 +43,9 @@ static void free_ctx(Ctx *c) {
                     c->d_if_b, c->d_if_phi, c->d_if_dinv, c->d_T[0], c->d_T[1], c->d_z, c->d_p[0], c->d_p[1],
                     c->d_q, c->d_partials, c->d_status, c->d_fail_relres, c->d_step_sc, c->d_iters,
                     c->d_relres, c->d_area, c->d_pairs, c->d_pcnt, c->d_chunk_hi, c->d_chunk_ctr, c->d_lcol, c->d_chunk_runs,
-                    c->d_chunk_nruns, c->d_chunk_lown, c->d_trace, c->d_DinvS};
+                    c->d_chunk_nruns, c->d_chunk_lown, c->d_trace, c->d_DinvS, c->d_slice_if_zero,
+                    c->d_KV, c->d_Dinv_vol, c->d_if_of_row, c->d_mr, c->d_mr_iters, c->d_mr_relres,
+                    c->d_ell_cnt_s, c->d_ell_col_s, c->d_ell_val_s, c->d_if_b_s, c->d_if_phi_s};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     for (cudaEvent_t e : c->events) cudaEventDestroy(e);
@@ -222,6 +225,24 @@ extern "C" int thermo_set_bc(void *ctx, int32_t part, int32_t tag, double alpha,
     }
 }
 
+extern "C" int thermo_set_method(void *ctx, int32_t method, int32_t M, int32_t P, int32_t K) {
+    Ctx *c = (Ctx *)ctx;
+    if (!c) return THERMO_EINVAL;
+    if (method == 0) {
+        c->method = 0;
+        return THERMO_OK;
+    }
+    if (method != 1) return fail(c, THERMO_EINVAL, "method must be 0 (implicit Euler) or 1 (MRSDC)");
+    if (M < 1 || M > 8 || P < 1 || P > 8 || K < 0) return fail(c, THERMO_EINVAL, "MRSDC needs 1 <= M, P <= 8, K >= 0");
+    if (c->S != 1) return fail(c, THERMO_EINVAL, "MRSDC runs a single scenario");
+    c->method = 1;
+    c->mr_M = M;
+    c->mr_P = P;
+    c->mr_K = K;
+    int rc = thermo::mrsdc_setup(*c);
+    return rc ? THERMO_ECUDA : THERMO_OK;
+}
+
 extern "C" int thermo_set_solver(void *ctx, double rtol, int32_t maxit) {
     Ctx *c = (Ctx *)ctx;
     if (!c) return THERMO_EINVAL;
@@ -268,6 +289,41 @@ extern "C" int thermo_step(void *ctx, double t, double dt, int32_t nsteps) {
         }
         API_CK(cudaMemcpyAsync(c->d_step_sc, sc.data(), sizeof(double) * sc.size(), cudaMemcpyHostToDevice, c->stream));
         API_CK(cudaMemsetAsync(c->d_status, 0, sizeof(int) * 8, c->stream));
+        if (c->method == 1) {   // MRSDC: one step at a time, status checked per step
+            c->h_iters.assign((size_t)nsteps, 0);
+            c->h_relres.assign((size_t)nsteps, 0.0);
+            c->h_area.assign(nsteps, 0.0);
+            c->ms_iface = c->ms_solve = 0.0;
+            for (int n = 0; n < nsteps; ++n) {
+                API_CK(cudaMemsetAsync(c->d_status, 0, sizeof(int) * 8, c->stream));
+                if (thermo::mrsdc_step(*c, t + (double)n * dt, dt, n)) return THERMO_ECUDA;
+                int status[8];
+                std::vector<int32_t> it(c->mr_solves);
+                std::vector<double> rr(c->mr_solves);
+                API_CK(cudaMemcpyAsync(status, c->d_status, sizeof status, cudaMemcpyDeviceToHost, c->stream));
+                API_CK(cudaMemcpyAsync(it.data(), c->d_mr_iters, sizeof(int32_t) * it.size(), cudaMemcpyDeviceToHost, c->stream));
+                API_CK(cudaMemcpyAsync(rr.data(), c->d_mr_relres, sizeof(double) * rr.size(), cudaMemcpyDeviceToHost, c->stream));
+                API_CK(cudaStreamSynchronize(c->stream));
+                c->last_nsteps = n + 1;
+                for (int j = 0; j < c->mr_solves; ++j) {
+                    c->h_iters[n] += it[j];
+                    c->h_relres[n] = std::max(c->h_relres[n], rr[j]);
+                }
+                if (status[0] || status[1]) {
+                    c->failed_step = n;
+                    c->failed_scen = 0;
+                    c->failed_relres = c->h_relres[n];
+                    c->last_nsteps = n;
+                    return fail(c, status[1] ? THERMO_EGEOM : THERMO_ENOCONV,
+                                "MRSDC step " + std::to_string(n) + " failed (implicit solve or interface)");
+                }
+                c->cur ^= 1;
+                c->steps_done += 1;
+            }
+            c->failed_step = -1;
+            c->failed_scen = -1;
+            return THERMO_OK;
+        }
         if (c->timing) {
             while (c->events.size() < 2 * (size_t)nsteps + 1) {
                 cudaEvent_t e;

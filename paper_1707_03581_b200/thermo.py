@@ -20,7 +20,7 @@ _CODES = {-1: "EINVAL", -2: "ENOMEM", -3: "ECUDA", -4: "ENOCONV", -5: "EGEOM"}
 # symbols declared in include/thermo.h
 EXPORTS = ["thermo_create_mesh", "thermo_set_bc", "thermo_step", "thermo_get_T", "thermo_set_T",
            "thermo_set_solver", "thermo_get_stats", "thermo_get_step_iters", "thermo_last_error",
-           "thermo_destroy", "thermo_set_timing"]
+           "thermo_destroy", "thermo_set_timing", "thermo_set_method"]
 
 
 class ThermoError(RuntimeError):
@@ -81,6 +81,7 @@ def load(path: str = LIB_PATH):
     L.thermo_last_error.restype = ctypes.c_char_p
     L.thermo_destroy.argtypes = [vp]
     L.thermo_set_timing.argtypes = [vp, i32]
+    L.thermo_set_method.argtypes = [vp, i32, i32, i32, i32]
     _lib = L
     return L
 
@@ -151,6 +152,11 @@ class Thermo:
 
     def set_timing(self, enable=True):
         self._check(load().thermo_set_timing(self.h, 1 if enable else 0))
+
+    def set_method(self, method: str = "ie", M: int = 3, P: int = 2, K: int = 1):
+        """'ie' (implicit Euler, default) or 'mrsdc' (MRSDC(M, P) with K sweeps)."""
+        code = {"ie": 0, "mrsdc": 1}[method]
+        self._check(load().thermo_set_method(self.h, code, M, P, K))
 
     def set_solver(self, rtol=1e-12, maxit=0):
         self._check(load().thermo_set_solver(self.h, rtol, maxit))
