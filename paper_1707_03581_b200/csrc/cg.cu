@@ -73,6 +73,7 @@ struct CGParams {
     int maxit, step;
     int stage_entries;         // TMA: matrix entries per stage
     int nstages;               // TMA: ring stages (<= 8)
+    int64_t u_rows;            // TMA: rows per update-phase chunk (5 streams per stage)
     int win_cap;               // KIND 2: window entries per vector per stage
     const int32_t *chunk_hi;   // TMA: largest column index referenced by each chunk
     const int2 *chunk_runs;    // KIND 2: [nchunks][CG_MAXR] (start, length) of the window runs
@@ -83,6 +84,9 @@ struct CGParams {
     const double *wv[2];       // KIND 2: vectors staged through the window
     int nwv;
     unsigned long long *trace; // optional: %globaltimer after every grid barrier (CTA 0)
+    int prefetch;              // L2 leading-edge prefetch (THERMO_CG_PREFETCH=1; measured slower on cfg3)
+    int debug;                 // THERMO_CG_DEBUG bits (measurement only, results invalid):
+                               // 1 consumers skip the row work, 2 no window copies, 4 no prefetch
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -356,21 +360,21 @@ __device__ __forceinline__ void sweep(const CGParams &P, Ring &R, Body &&body) {
             __syncwarp();
             if (lane == 0) {
                 const uint32_t cbytes = KIND == 2 ? cnt * 2u : cnt * 4u;
-                const uint32_t wbytes = KIND == 2 ? (uint32_t)P.nwv * (uint32_t)wtot * 8u : 0u;
+                const uint32_t wbytes = KIND == 2 && !(P.debug & 2) ? (uint32_t)P.nwv * (uint32_t)wtot * 8u : 0u;
                 mbar_arrive_expect_tx(&R.full[st], cnt * 8u + cbytes + wbytes);
                 bulk_g2s(sb + CG_HDR, P.val + e0, cnt * 8u, &R.full[st], pol);
                 if (KIND == 2) bulk_g2s(sb + R.col_off, P.lcol + e0, cbytes, &R.full[st], pol);
                 else bulk_g2s(sb + R.col_off, P.col + e0, cbytes, &R.full[st], pol);
             }
             __syncwarp();
-            if (KIND == 2 && nruns) {
+            if (KIND == 2 && nruns && !(P.debug & 2)) {
 #pragma unroll
                 for (int v = 0; v < 2; ++v)
                     if (v < P.nwv)
                         bulk_g2s_nohint(sb + R.win_off + ((size_t)v * P.win_cap + woff) * 8, P.wv[v] + cur.run.x,
                                         (uint32_t)cur.run.y * 8u, &R.full[st]);
             }
-            if (lane == 0) {
+            if (lane == 0 && !(P.debug & 4)) {
                 prefetch_edge<W>(P, cur.hi_own);
                 prefetch_edge<W>(P, cur.hi_pf);
             }
@@ -400,7 +404,7 @@ __device__ __forceinline__ void sweep(const CGParams &P, Ring &R, Body &&body) {
                 break;
             }
             const int64_t s = (int64_t)ch * W + wg;
-            if (s < P.nslices) {
+            if (s < P.nslices && !(P.debug & 1)) {
                 const double *vals = reinterpret_cast<const double *>(sb + CG_HDR);
                 const int o0 = hdr[wg], o1 = hdr[wg + 1];
                 if (KIND == 2) {
@@ -414,6 +418,83 @@ __device__ __forceinline__ void sweep(const CGParams &P, Ring &R, Body &&body) {
                     body(s, src, (o1 - o0) >> 5, hdr[16 + wg], hdr[17 + wg]);
                 }
             }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&R.empty[st]);
+        }
+        ++R.n;
+    }
+}
+
+// Update phase through the TMA ring (TMA kinds): the producer bulk-copies chunks of UR rows
+// of the five input streams (p, q, D^{-1}, x, z) into a ring stage; consumer threads update
+// their rows from shared memory and store x, z.  No L1 involvement: with most of the shared
+// memory taken by the ring, L1-allocating loads would be limited by the small L1.
+// body(row, p, q, dinv, x, z) for every row of this CTA's chunks; static chunk order.
+template <int W, int NG, class Body>
+__device__ __forceinline__ void sweep_u(const CGParams &P, Ring &R, const double *const (&src)[5], Body &&body) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t NS = (uint32_t)P.nstages;
+    const int G = gridDim.x;
+    const int64_t UR = P.u_rows;
+    const int64_t nch = (P.N + UR - 1) / UR;
+    if (warp == W * NG) {   // producer
+        int64_t ch = blockIdx.x;
+        while (true) {
+            const uint32_t st = R.n % NS, ph = (R.n / NS) & 1u;
+            if (ch >= nch) {
+                const uint32_t m0 = R.n;
+                for (int q = 0; q < NG; ++q) {
+                    const uint32_t sq = R.n % NS, pq = (R.n / NS) & 1u;
+                    if (lane == 0) {
+                        mbar_wait(&R.empty[sq], pq ^ 1u);
+                        int *hdr = reinterpret_cast<int *>(R.stage + (size_t)sq * R.stage_bytes);
+                        hdr[31] = -1;
+                        hdr[30] = (int)m0;
+                        mbar_arrive(&R.full[sq]);
+                    }
+                    __syncwarp();
+                    ++R.n;
+                }
+                break;
+            }
+            if (lane == 0) {
+                mbar_wait(&R.empty[st], ph ^ 1u);
+                unsigned char *sb = R.stage + (size_t)st * R.stage_bytes;
+                int *hdr = reinterpret_cast<int *>(sb);
+                hdr[31] = (int)ch;
+                const int64_t r0 = ch * UR;
+                const int64_t rows = min(UR, P.N - r0);
+                const uint32_t bytes = (uint32_t)(((rows + 1) & ~(int64_t)1) * 8);   // 16-B multiple
+                mbar_arrive_expect_tx(&R.full[st], 5u * bytes);
+#pragma unroll
+                for (int v = 0; v < 5; ++v)
+                    bulk_g2s_nohint(sb + CG_HDR + (size_t)v * UR * 8, src[v] + r0, bytes, &R.full[st]);
+            }
+            __syncwarp();
+            ++R.n;
+            ch += G;
+        }
+        return;
+    }
+    const int g = warp / W, tid = threadIdx.x - g * W * 32;
+    while (true) {
+        const uint32_t st = R.n % NS, ph = (R.n / NS) & 1u;
+        if ((int)(R.n % NG) == g) {
+            mbar_wait(&R.full[st], ph);
+            const unsigned char *sb = R.stage + (size_t)st * R.stage_bytes;
+            const int ch = reinterpret_cast<const int *>(sb)[31];
+            if (ch < 0) {
+                const uint32_t m0 = (uint32_t)reinterpret_cast<const int *>(sb)[30];
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&R.empty[st]);
+                R.n = m0 + NG;
+                break;
+            }
+            const double *base = reinterpret_cast<const double *>(sb + CG_HDR);
+            const int64_t r0 = (int64_t)ch * UR;
+            const int rows = (int)min(UR, P.N - r0);
+            for (int r = tid; r < rows; r += W * 32)
+                body(r0 + r, base[r], base[UR + r], base[2 * UR + r], base[3 * UR + r], base[4 * UR + r]);
             __syncwarp();
             if (lane == 0) mbar_arrive(&R.empty[st]);
         }
@@ -465,7 +546,7 @@ __global__ void __launch_bounds__(cg_threads(KIND, W, NG), KIND == 0 ? 2 : 1) k_
     if (tr_on) P.trace[ntr++] = gtimer();
     double red0[4] = {0.0, 0.0, 0.0, 0.0};   // b.b, r.r, r.z, |Gamma_R|
     P.pf[0] = P.T_in; P.pf[1] = P.ML; P.pf[2] = P.benv; P.pf[3] = P.Dinv;
-    P.npf = 4;
+    P.npf = P.prefetch ? 4 : 0;
     P.wv[0] = P.T_in;
     P.nwv = 1;
     sweep<KIND, W, NG>(P, R, [&](int64_t s, const auto &src, int w, int ib, int ie) {
@@ -509,7 +590,7 @@ __global__ void __launch_bounds__(cg_threads(KIND, W, NG), KIND == 0 ? 2 : 1) k_
         double pq[1] = {0.0};
         const bool first = it == 0;
         P.pf[0] = P.z; P.pf[1] = pold;
-        P.npf = first ? 1 : 2;
+        P.npf = P.prefetch ? (first ? 1 : 2) : 0;
         P.wv[0] = P.z; P.wv[1] = pold;
         P.nwv = first ? 1 : 2;
         sweep<KIND, W, NG>(P, R, [&](int64_t s, const auto &src, int w, int ib, int ie) {
@@ -539,10 +620,19 @@ __global__ void __launch_bounds__(cg_threads(KIND, W, NG), KIND == 0 ? 2 : 1) k_
         double tpq[1];
         grid_total<1>(P.partials, G, 4, red_smem, tpq);
         const double alpha = rho / tpq[0];
-        // ---- U: x += alpha p, z -= alpha D^{-1} q, partials r.z and r.r (r = z / D^{-1});
-        // element pairs with 16-byte loads, two pairs in flight per thread and trip
+        // ---- U: x += alpha p, z -= alpha D^{-1} q, partials r.z and r.r (r = z / D^{-1})
         double red[2] = {0.0, 0.0};
-        {
+        if constexpr (KIND != 0) {
+            const double *const usrc[5] = {pnew, P.q, P.Dinv, xsrc, P.z};
+            sweep_u<W, NG>(P, R, usrc, [&](int64_t i, double pv, double qv, double dv, double xv, double zv) {
+                P.T_out[i] = fma(alpha, pv, xv);
+                const double zo = fma(-alpha * dv, qv, zv);
+                P.z[i] = zo;
+                const double r = zo / dv;
+                red[0] = fma(r, zo, red[0]);
+                red[1] = fma(r, r, red[1]);
+            });
+        } else {   // element pairs with 16-byte loads, two pairs in flight per thread and trip
             const int64_t npair = N >> 1;
             const double2 *p2 = reinterpret_cast<const double2 *>(pnew);
             const double2 *q2 = reinterpret_cast<const double2 *>(P.q);
@@ -564,8 +654,7 @@ __global__ void __launch_bounds__(cg_threads(KIND, W, NG), KIND == 0 ? 2 : 1) k_
                 red[0] = fma(r1, zo.y, red[0]);
                 red[1] = fma(r1, r1, red[1]);
             };
-            // UU element pairs per thread and trip, all loads issued before any use
-            constexpr int UU = KIND == 0 ? 2 : 4;
+            constexpr int UU = 2;
             int64_t j = tid;
             for (; j + (UU - 1) * nthr < npair; j += UU * nthr) {
                 double2 pv[UU], qv[UU], dv[UU], xv[UU], zv[UU];
@@ -598,7 +687,7 @@ __global__ void __launch_bounds__(cg_threads(KIND, W, NG), KIND == 0 ? 2 : 1) k_
         beta = tr[0] / rho;
         rho = tr[0];
         rr = tr[1];
-        conv = rr <= tol2;
+        conv = rr <= tol2 && !P.debug;   // debug runs: fixed iteration count (maxit)
         xsrc = P.T_out;
         double *t = pold; pold = pnew; pnew = t;
         ++it;
@@ -611,7 +700,7 @@ __global__ void __launch_bounds__(cg_threads(KIND, W, NG), KIND == 0 ? 2 : 1) k_
         P.iters_out[P.step] = it;
         P.relres_out[P.step] = rel;
         P.area_out[P.step] = tot0[3];
-        if (!conv) {
+        if (!conv && !P.debug) {
             P.status[0] = 1;
             P.status[2] = P.step;
             P.status[3] = 0;
@@ -643,7 +732,7 @@ __global__ void k_chunk_hi(const int64_t *slice_ptr, const int32_t *col, int64_t
 // stats[1] = max runs, stats[2] = overflow (window > 65535 or chunk > CW_MAXE entries).
 #define CW_MAXE 4096
 __global__ void __launch_bounds__(256) k_chunk_windows(const int64_t *slice_ptr, const int32_t *col,
-                                                       int64_t nslices, int W, int2 *runs_out,
+                                                       int64_t nslices, int W, int gap, int2 *runs_out,
                                                        int32_t *nruns_out, int32_t *lown_out, uint16_t *lcol,
                                                        int *stats) {
     __shared__ int key[CW_MAXE];
@@ -674,7 +763,7 @@ __global__ void __launch_bounds__(256) k_chunk_windows(const int64_t *slice_ptr,
     if (threadIdx.x == 0) {   // runs (serial over <= 4096 sorted keys)
         int nr = 0;
         for (int j = 0; j < E; ++j) {
-            if (j == 0 || key[j] - key[j - 1] > CG_GAP + 1) {
+            if (j == 0 || key[j] - key[j - 1] > gap + 1) {
                 rstart[nr] = key[j] & ~1;
                 if (nr > 0) rlast[nr - 1] = key[j - 1];
                 ++nr;
@@ -771,7 +860,9 @@ int cg_setup(Ctx &c) {
             int *d_stats = nullptr;
             CK(cudaMalloc(&d_stats, sizeof(int) * 4));
             CK(cudaMemsetAsync(d_stats, 0, sizeof(int) * 4, c.stream));
-            k_chunk_windows<<<(unsigned)nchunks, 256, 0, c.stream>>>(c.d_slice_ptr, c.d_col, c.nslices, v.W,
+            const char *eg = getenv("THERMO_CG_GAP");   // tuning hook: bridged column gap
+            const int gap = eg ? std::max(2, atoi(eg)) : CG_GAP;
+            k_chunk_windows<<<(unsigned)nchunks, 256, 0, c.stream>>>(c.d_slice_ptr, c.d_col, c.nslices, v.W, gap,
                                                                     c.d_chunk_runs, c.d_chunk_nruns, c.d_chunk_lown,
                                                                     c.d_lcol, d_stats);
             CK(cudaGetLastError());
@@ -783,7 +874,8 @@ int cg_setup(Ctx &c) {
             wc = (stats[0] + 1) & ~1;
         }
         const size_t sb = stage_bytes(v, E, wc);
-        const int ns = v.kind == 0 ? 1 : (int)std::min<size_t>(8, (210 * 1024 - 128) / sb);
+        int ns = v.kind == 0 ? 1 : (int)std::min<size_t>(8, (210 * 1024 - 128) / sb);
+        if (const char *e = getenv("THERMO_CG_STAGES")) ns = std::min(ns, std::max(2, atoi(e)));   // tuning hook
         if (v.kind != 0 && ns < v.NG + 1) continue;   // at least one stage in flight
         const size_t smem = v.kind == 0 ? 0 : 128 + (size_t)ns * sb;
         const void *fn = variant_kernel(vi);
@@ -797,10 +889,15 @@ int cg_setup(Ctx &c) {
         c.cg_chunk = v.W;
         c.cg_block = cg_threads(v.kind, v.W, v.NG);
         c.cg_nstages = ns;
+        c.cg_u_rows = v.kind == 0 ? 0 : (int64_t)((sb - CG_HDR) / 40) & ~(int64_t)31;
         break;
     }
     if (chosen < 0) { c.err = "no CG kernel variant can be resident"; return -3; }
     c.cg_variant = chosen;
+    const char *dbg = getenv("THERMO_CG_DEBUG");
+    c.cg_debug = dbg ? atoi(dbg) : 0;
+    const char *pfe = getenv("THERMO_CG_PREFETCH");
+    c.cg_prefetch = pfe ? atoi(pfe) : 0;
     c.cg_tma = kVariants[chosen].kind != 0;
     const int W = c.cg_chunk;
     const int64_t nchunks = (c.nslices + W - 1) / W;
@@ -855,6 +952,7 @@ int cg_launch_solve(Ctx &c, const double *x0, double *x, const double *rhs, cons
     P.step = slot;
     P.stage_entries = c.cg_stage_entries;
     P.nstages = c.cg_nstages;
+    P.u_rows = c.cg_u_rows;
     P.win_cap = c.cg_win_cap;
     P.chunk_hi = c.d_chunk_hi;
     P.chunk_runs = c.d_chunk_runs;
@@ -903,16 +1001,19 @@ int cg_launch_step(Ctx &c, int step, double dt) {
     P.area_out = c.d_area;
     P.dt = dt;
     P.rtol2 = c.rtol * c.rtol;
-    P.maxit = c.maxit > 0 ? c.maxit : (int)std::min<int64_t>(10 * c.N, 10000);
+    P.maxit = c.cg_debug ? 50 : (c.maxit > 0 ? c.maxit : (int)std::min<int64_t>(10 * c.N, 10000));
     P.step = step;
     P.stage_entries = c.cg_stage_entries;
     P.nstages = c.cg_nstages;
+    P.u_rows = c.cg_u_rows;
     P.win_cap = c.cg_win_cap;
     P.chunk_hi = c.d_chunk_hi;
     P.chunk_runs = c.d_chunk_runs;
     P.chunk_nruns = c.d_chunk_nruns;
     P.chunk_lown = c.d_chunk_lown;
     P.trace = c.d_trace;
+    P.debug = c.cg_debug;
+    P.prefetch = c.cg_prefetch;
     void *args[] = {&P};
     CK(cudaLaunchCooperativeKernel(variant_kernel(c.cg_variant), dim3(c.cg_grid), dim3(c.cg_block), args,
                                    c.cg_smem, c.stream));

@@ -93,7 +93,7 @@ struct Ctx {
     int cg_grid = 0, cg_block = 0, cg_stage_entries = 0;
     size_t cg_smem = 0;
     bool cg_tma = false;
-    int cg_variant = 0, cg_chunk = 8;
+    int cg_variant = 0, cg_chunk = 8, cg_debug = 0, cg_prefetch = 0;
     int32_t *d_chunk_hi = nullptr;
     uint16_t *d_lcol = nullptr;      // chunk-local 16-bit columns (window kernels)
     int2 *d_chunk_runs = nullptr;    // window runs per chunk
@@ -101,6 +101,7 @@ struct Ctx {
     int32_t *d_chunk_lown = nullptr;
     unsigned long long *d_trace = nullptr;   // THERMO_CG_TRACE=1: barrier timestamps of the last solve
     int cg_win_cap = 0, cg_nstages = 1;
+    int64_t cg_u_rows = 0;
     int *d_chunk_ctr = nullptr;
 
     double rtol = 1e-12;
