@@ -11,7 +11,9 @@ re-integration + right-hand side (a3) + Jacobi-PCG solve (a4) +
 
 Rank 0 prints one JSON line.  Multi-GPU: the single-run IE step does not shard (DESIGN.md:
 "replicas only"); under torchrun each rank advances its own replica, `value` is the
-whole-job DoF-steps/s over the max-over-ranks device time, scaling "weak".
+whole-job DoF-steps/s over the max-over-ranks device time, scaling "weak".  The batched
+configuration (--config cfg4, 64 scenarios) shards its scenarios over the ranks with no
+data-path collective (paper_1707_03581_b200/dist.py); scaling "strong" (total work fixed).
 --impl reference times the CPU oracle (oracle/, the reference arm for this tier) on a
 bounded sample of the same workload on the host cores.
 """
@@ -121,10 +123,8 @@ class ClockSampler:
 
 
 def dist_setup():
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return world, rank, local
+    from paper_1707_03581_b200.dist import env_world
+    return env_world()
 
 
 def cpu_baseline(cfg, steps=1):
@@ -144,6 +144,11 @@ def cpu_baseline(cfg, steps=1):
             "seconds": dt}
 
 
+def workload_name(name):
+    return {"cfg0": "configs[0]", "cfg1": "configs[1]", "cfg2": "configs[2]", "cfg3": "configs[3]",
+            "cfg4": "configs[4]"}.get(name, name)
+
+
 def run_reference(args):
     world, rank, local = dist_setup()
     if rank != 0:
@@ -155,7 +160,8 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus,
             "steps": steps, "warmup": 0, "ms_per_step": cb["seconds"] / steps * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"BASELINE configs[3] ({cfg.name}): {cfg.description}", "n_dof": cfg.n_dof,
+            "config": {"workload": f"BASELINE {workload_name(cfg.name)} ({cfg.name}): {cfg.description}",
+                       "n_dof": cfg.n_dof,
                        "dt": cfg.dt, "sample": f"{steps} of the requested {args.steps} steps (bounded)"},
             "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -169,12 +175,15 @@ def run_thermo(args):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1707_03581_b200 import dist as D
     from paper_1707_03581_b200 import inputs as I
     from paper_1707_03581_b200.thermo import Thermo
 
     W = max(3, args.warmup)
     K = args.steps
-    cfg = I.make_config(args.config)
+    cfg_all = I.make_config(args.config)
+    sharded = cfg_all.n_scen > 1 and world > 1     # batched mode: scenarios split over ranks
+    cfg = D.shard_config(cfg_all, rank, world) if sharded else cfg_all
     stream = torch.cuda.current_stream()
     th = Thermo.from_config(cfg, stream=stream.cuda_stream)
     th.set_timing(True)
@@ -200,42 +209,42 @@ def run_thermo(args):
     t += K * cfg.dt
     ms = e0.elapsed_time(e1)
     st = th.stats()
-    iters = th.step_iters()[:, 0]
-    ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        torch.distributed.all_reduce(ms_t, op=torch.distributed.ReduceOp.MAX)
-    ms_max = float(ms_t.item())
+    iters = th.step_iters().max(axis=1)      # loop iterations of the (batched) solve per step
+    ms_max = D.max_over_ranks(ms, device="cuda")
 
     # ---- e2e through the C ABI with host buffers: per step, H2D of the step's time scalars
     # (inside thermo_step) + D2H of the whole temperature field into pinned host memory
     KE = max(1, args.e2e_steps)
     host = torch.empty(cfg.n_dof, dtype=torch.float64, pin_memory=True)
+    hosts = [host] + [torch.empty(cfg.n_dof, dtype=torch.float64, pin_memory=True) for _ in range(th.S - 1)]
     barrier()
     e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e2.record(stream)
     for k in range(KE):
         th.step(t, cfg.dt, 1)
-        th.get_T_host_ptr(host.data_ptr())
+        for sc, h in enumerate(hosts):
+            th.get_T_host_ptr(h.data_ptr(), scen=sc)
         t += cfg.dt
     e3.record(stream)
     torch.cuda.synchronize()
-    ms_e2e = e2.elapsed_time(e3)
-    ms_e2e_t = torch.tensor([ms_e2e], dtype=torch.float64, device="cuda")
-    if world > 1:
-        torch.distributed.all_reduce(ms_e2e_t, op=torch.distributed.ReduceOp.MAX)
-    ms_e2e = float(ms_e2e_t.item())
+    ms_e2e = D.max_over_ranks(e2.elapsed_time(e3), device="cuda")
 
     if rank != 0:
         if world > 1:
             torch.distributed.barrier()
             torch.distributed.destroy_process_group()
         return
-    N, Z = cfg.n_dof, st["nnz_volume"]
-    value = world * N * K / (ms_max * 1e-3)
+    N, Z, S = cfg.n_dof, st["nnz_volume"], th.S
+    units = N * cfg_all.n_scen if sharded else world * N * S     # DoF-steps per step, whole job
+    value = units * K / (ms_max * 1e-3)
     # roofline of the dominant kernel (the persistent CG solve, one launch per step):
-    # SURVEY 8(d) per-iteration bytes 12 Z + 108 N, plus 12 Z + 40 N for r0 = b - K~ x0
-    per_iter = 12 * Z + 108 * N
-    alg_bytes = float(iters.sum()) * per_iter + K * (12 * Z + 40 * N)
+    # SURVEY 8(d) per-iteration bytes 12 Z + 108 N, plus 12 Z + 40 N for r0 = b - K~ x0;
+    # batched: 12 Z + 4 N + S 104 N per iteration (SURVEY 8(d) cfg 4 row), 12 Z + S 40 N phase 0
+    if S == 1:
+        per_iter, phase0 = 12 * Z + 108 * N, 12 * Z + 40 * N
+    else:
+        per_iter, phase0 = 12 * Z + 4 * N + S * 104 * N, 12 * Z + S * 40 * N
+    alg_bytes = float(iters.sum()) * per_iter + K * phase0
     achieved = alg_bytes / (st["ms_solve"] * 1e-3) / 1e9
     peak, peak_kind = peaks()
     prof = ncu_traffic(args.config)
@@ -244,19 +253,22 @@ def run_thermo(args):
         traffic = prof.get("dram_bytes_per_launch")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
-        "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"BASELINE configs[3] ({cfg.name}): {cfg.description}", "n_dof": N,
-                   "nnz_volume": Z, "dt": cfg.dt, "rtol": 1e-12, "l2": "inputs > L2 (2.8 GB streamed per CG iteration)",
-                   "parallelism": "replicas only" if world > 1 else "single GPU",
+        "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "strong" if sharded else "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"BASELINE {workload_name(cfg_all.name)} ({cfg_all.name}): {cfg_all.description}",
+                   "n_dof": N, "n_scenarios": cfg_all.n_scen, "nnz_volume": Z, "dt": cfg.dt, "rtol": 1e-12,
+                   "l2": f"inputs > L2 ({per_iter / 1e9:.2f} GB algorithmic per CG iteration)" if per_iter > 126e6
+                         else "working set fits L2 (no flush; small config)",
+                   "parallelism": (f"scenarios sharded over {world} ranks" if sharded else
+                                   "replicas only" if world > 1 else "single GPU"),
                    "cg_iters_per_step": float(iters.mean())},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": "k_cg_step (persistent Jacobi-PCG, one launch per step)",
                      "peak_kind": peak_kind, "achieved_vs_8TBs": achieved / 8000.0,
                      "solve_share_of_step": st["ms_solve"] / ms,
                      "iface_share_of_step": st["ms_iface"] / ms},
-        "e2e": {"value": world * N * KE / (ms_e2e * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 32 * th.S,
-                "d2h_bytes_per_step": 8 * N},
+        "e2e": {"value": units * KE / (ms_e2e * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 32 * S,
+                "d2h_bytes_per_step": 8 * N * S},
         "gpu_launches": K * (4 if st["n_iface_rows"] else 1),
         "clocks": clk.summary(),
     }

@@ -89,12 +89,6 @@ struct CGParams {
                                // 1 consumers skip the row work, 2 no window copies, 4 no prefetch
 };
 
-__device__ __forceinline__ unsigned long long gtimer() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
-
 // Prefetch into L2 the leading edge of the column window of a chunk whose largest column
 // index is hi_col: rows [hi_col - len + 1, hi_col] of each vector in pf (len = rows of the
 // chunk, 16-B aligned).  hi_col < 0: nothing.

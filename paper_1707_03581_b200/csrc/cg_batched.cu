@@ -60,6 +60,7 @@ struct CGBParams {
     double *relres_out, *area_out;
     double dt, rtol2;
     int maxit, step;
+    unsigned long long *trace;   // optional: %globaltimer after every grid barrier (CTA 0)
 };
 
 __device__ __forceinline__ int64_t ellb(const CGBParams &P, int s, int c, int k) {
@@ -260,6 +261,9 @@ __global__ void __launch_bounds__(CGB_BLOCK, 1) k_cgb_step(CGBParams P) {
     }
     cg::grid_group grid = cg::this_grid();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const bool tr_on = P.trace && blockIdx.x == 0 && threadIdx.x == 0;
+    int ntr = 0;
+    if (tr_on) P.trace[ntr++] = gtimer();
     const int64_t N = P.N;
     const int gw = blockIdx.x * CGB_WARPS + warp, TW = gridDim.x * CGB_WARPS;
     const bool col_ok[2] = {2 * lane < P.S, 2 * lane + 1 < P.S};
@@ -318,6 +322,7 @@ __global__ void __launch_bounds__(CGB_BLOCK, 1) k_cgb_step(CGBParams P) {
     }
     double t0[4][2];
     cgb_reduce<4>(v0, sm, P.partials, grid, t0);
+    if (tr_on) P.trace[ntr++] = gtimer();
     double rho[2] = {t0[2][0], t0[2][1]}, rr2[2] = {t0[1][0], t0[1][1]}, tol2[2], beta[2] = {0.0, 0.0};
     bool conv[2];
     int itc[2] = {0, 0};
@@ -373,6 +378,7 @@ __global__ void __launch_bounds__(CGB_BLOCK, 1) k_cgb_step(CGBParams P) {
         }
         double tpq[1][2];
         cgb_reduce<1>(vs, sm, P.partials, grid, tpq);
+        if (tr_on && ntr < 1000) P.trace[ntr++] = gtimer();
         double alpha[2];
         for (int h = 0; h < 2; ++h) alpha[h] = conv[h] ? 0.0 : rho[h] / tpq[0][h];   // frozen columns
         // ---- U (warp per row, lanes over columns)
@@ -421,6 +427,7 @@ __global__ void __launch_bounds__(CGB_BLOCK, 1) k_cgb_step(CGBParams P) {
         }
         double tu[2][2];
         cgb_reduce<2>(vu, sm, P.partials, grid, tu);
+        if (tr_on && ntr < 1000) P.trace[ntr++] = gtimer();
         ++it;
         for (int h = 0; h < 2; ++h) {
             if (conv[h]) continue;
@@ -522,6 +529,7 @@ int cgb_launch_step(Ctx &c, int step, double dt) {
     P.rtol2 = c.rtol * c.rtol;
     P.maxit = c.maxit > 0 ? c.maxit : (int)std::min<int64_t>(10 * c.N, 10000);
     P.step = step;
+    P.trace = c.d_trace;
     void *args[] = {&P};
     CK(cudaLaunchCooperativeKernel((const void *)k_cgb_step, dim3(c.cg_grid), dim3(c.cg_block), args, 0, c.stream));
     return 0;

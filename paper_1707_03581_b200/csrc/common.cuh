@@ -39,6 +39,12 @@ __device__ __forceinline__ int ld_stream(const int *p, uint64_t pol) {
 // Coherent load that bypasses L1 (cached in L2 only): streams that are read once per phase
 // but written by other CTAs earlier in the same kernel.  Keeps L1 miss slots free when most
 // of the shared memory is taken by a TMA ring.
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 __device__ __forceinline__ double2 ld_cg2(const double2 *p) {
     double2 v;
     asm volatile("ld.global.cg.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
@@ -170,6 +176,7 @@ __device__ __forceinline__ void grid_total(const double *partials, int G, int sl
 
 struct BinGrid {      // uniform bin grid over one surface triangulation (2-D, own frame)
     double x0, y0, inv_h;
+    double lx, ly, hx, hy;   // union box of the surface's triangles
     int nx, ny;
     const int32_t *ptr;   // [nx*ny + 1]
     const int32_t *ids;   // triangle ids, ascending within a bin

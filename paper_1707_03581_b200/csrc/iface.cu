@@ -31,7 +31,7 @@ namespace thermo {
         }                                                                        \
     } while (0)
 
-#define IF_MAXV 12   // polygon vertices (triangle clipped by 3 half-planes: <= 6, + slack)
+#define IF_MAXV 8    // polygon vertices (a triangle clipped by 3 half-planes has <= 6)
 
 __device__ __forceinline__ double cross2(double ax, double ay, double bx, double by) {
     return ax * by - ay * bx;
@@ -98,38 +98,68 @@ __device__ bool pair_integrals(const double2 F[3], const double2 G[3], bool ownI
     double2 poly[IF_MAXV];
     const int nv = clip_tri(F, G, poly);
     if (nv < 3) return false;
-    double lf[IF_MAXV][3], lg[IF_MAXV][3];
-    for (int v = 0; v < nv; ++v) {
-        bary(F, poly[v], lf[v]);
-        bary(G, poly[v], lg[v]);
-    }
-    double(*own)[3] = ownIsF ? lf : lg;
-    double(*oth)[3] = ownIsF ? lg : lf;
-    for (int q = 0; q < 6; ++q) r.own[q] = 0.0;
-    for (int q = 0; q < 9; ++q) r.cross[q] = 0.0;
-    for (int q = 0; q < 3; ++q) r.b[q] = 0.0;
+    // barycentric maps of both triangles (the same arithmetic as bary(), inverse hoisted)
+    const double invF = 1.0 / cross2(F[1].x - F[0].x, F[1].y - F[0].y, F[2].x - F[0].x, F[2].y - F[0].y);
+    const double invG = 1.0 / cross2(G[1].x - G[0].x, G[1].y - G[0].y, G[2].x - G[0].x, G[2].y - G[0].y);
+    auto bc = [](const double2 T[3], double inv, double2 y, double l[3]) {
+        l[1] = cross2(y.x - T[0].x, y.y - T[0].y, T[2].x - T[0].x, T[2].y - T[0].y) * inv;
+        l[2] = cross2(T[1].x - T[0].x, T[1].y - T[0].y, y.x - T[0].x, y.y - T[0].y) * inv;
+        l[0] = 1.0 - l[1] - l[2];
+    };
+    auto vtx = [&](double2 y, double own[3], double oth[3]) {
+        double lf[3], lg[3];
+        bc(F, invF, y, lf);
+        bc(G, invG, y, lg);
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            own[a] = ownIsF ? lf[a] : lg[a];
+            oth[a] = ownIsF ? lg[a] : lf[a];
+        }
+    };
+    double R[18];   // own[6] cross[9] b[3]
+#pragma unroll
+    for (int q = 0; q < 18; ++q) R[q] = 0.0;
+    double o0[3], t0[3], o1[3], t1[3], o2[3], t2[3];
+    vtx(poly[0], o0, t0);
+    vtx(poly[1], o1, t1);
     double area = 0.0;
     for (int f = 1; f + 1 < nv; ++f) {
-        const int i0 = 0, i1 = f, i2 = f + 1;
-        const double ar = 0.5 * cross2(poly[i1].x - poly[i0].x, poly[i1].y - poly[i0].y,
-                                       poly[i2].x - poly[i0].x, poly[i2].y - poly[i0].y);
-        if (!(ar > 0.0)) continue;
-        area += ar;
-        const double w12 = ar * (1.0 / 12.0), w3 = ar * (1.0 / 3.0);
-        double so[3], st[3];
-        for (int a = 0; a < 3; ++a) {
-            so[a] = own[i0][a] + own[i1][a] + own[i2][a];
-            st[a] = oth[i0][a] + oth[i1][a] + oth[i2][a];
+        const double2 p0 = poly[0], p1 = poly[f], p2 = poly[f + 1];
+        vtx(p2, o2, t2);
+        const double ar = 0.5 * cross2(p1.x - p0.x, p1.y - p0.y, p2.x - p0.x, p2.y - p0.y);
+        if (ar > 0.0) {
+            area += ar;
+            const double w12 = ar * (1.0 / 12.0), w3 = ar * (1.0 / 3.0);
+            double so[3], st[3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                so[a] = o0[a] + o1[a] + o2[a];
+                st[a] = t0[a] + t1[a] + t2[a];
+            }
+            int q = 0;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                R[15 + a] += w3 * so[a];
+#pragma unroll
+                for (int b = a; b < 3; ++b, ++q)
+                    R[q] += w12 * (o0[a] * o0[b] + o1[a] * o1[b] + o2[a] * o2[b] + so[a] * so[b]);
+#pragma unroll
+                for (int b = 0; b < 3; ++b)
+                    R[6 + a * 3 + b] += w12 * (o0[a] * t0[b] + o1[a] * t1[b] + o2[a] * t2[b] + so[a] * st[b]);
+            }
         }
-        int q = 0;
+#pragma unroll
         for (int a = 0; a < 3; ++a) {
-            r.b[a] += w3 * so[a];
-            for (int b = a; b < 3; ++b, ++q)
-                r.own[q] += w12 * (own[i0][a] * own[i0][b] + own[i1][a] * own[i1][b] + own[i2][a] * own[i2][b] + so[a] * so[b]);
-            for (int b = 0; b < 3; ++b)
-                r.cross[a * 3 + b] += w12 * (own[i0][a] * oth[i0][b] + own[i1][a] * oth[i1][b] + own[i2][a] * oth[i2][b] + so[a] * st[b]);
+            o1[a] = o2[a];
+            t1[a] = t2[a];
         }
     }
+#pragma unroll
+    for (int q = 0; q < 6; ++q) r.own[q] = R[q];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) r.cross[q] = R[6 + q];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) r.b[q] = R[15 + q];
     return area > 0.0;
 }
 
@@ -143,96 +173,144 @@ __device__ __forceinline__ int warp_excl_scan(int v, int lane) {
     return x - v;
 }
 
-// Warp per (own triangle t of side `side`, scenario s): the candidates of all bins under the
-// triangle's box are flattened (bins row-major, ascending ids) and spread over the lanes;
-// hits are written in that order (ballot prefix), so the record list is deterministic.
-__global__ void __launch_bounds__(128) k_pairs(IfaceParams P, int side) {
-    const int lane = threadIdx.x & 31;
+// Warp per (PAIR_TPW consecutive own triangles of side `side`, scenario s).
+//  1. candidates: per triangle, the candidates of all bins under its box (in the other
+//     surface's frame) are flattened (bins row-major, ascending ids) and spread over the
+//     lanes; box-overlapping ones, each counted in one bin only, are appended to a per-warp
+//     shared-memory queue in that order (ballot prefix).  A triangle whose box misses the
+//     other surface's union box has none (most rail triangles: the stock covers a part of it).
+//  2. integrals: the queue is clipped 32 pairs at a time, one pair per lane, so the lanes stay
+//     busy across triangles; a hit's record slot is its rank among its own triangle's hits.
+// Records per triangle therefore come out in candidate order, the same for every run.
+#define PAIR_TPW 4
+#define PAIR_WPB 4
+
+__global__ void __launch_bounds__(32 * PAIR_WPB, 4) k_pairs(IfaceParams P, int side) {
+    extern __shared__ int pair_q_all[];   // [PAIR_WPB][PAIR_TPW * pcap]
+    __shared__ int pair_cnt_all[PAIR_WPB][PAIR_TPW];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const unsigned lt = (1u << lane) - 1u;
     const int nT = side == 0 ? P.nTA : P.nTB;
-    const int t = blockIdx.x * 4 + (threadIdx.x >> 5);
+    const int t0 = (blockIdx.x * PAIR_WPB + wib) * PAIR_TPW;
     const int s = blockIdx.y;
-    if (t >= nT) return;
+    if (t0 >= nT) return;
+    int *q = pair_q_all + wib * PAIR_TPW * P.pcap;
+    int *qcnt = pair_cnt_all[wib];
+    const int qcap = PAIR_TPW * P.pcap;
     const double ox = P.step_sc[4 * s + 0], oy = P.step_sc[4 * s + 1];
-    const int4 T = (side == 0 ? P.triA : P.triB)[t];
+    const int4 *own_tri = side == 0 ? P.triA : P.triB;
     const int4 *oth_tri = side == 0 ? P.triB : P.triA;
     const double4 *oth_box = side == 0 ? P.boxB : P.boxA;
     const BinGrid &G = side == 0 ? P.binB : P.binA;
     const double sx_own = side == 0 ? 0.0 : ox, sy_own = side == 0 ? 0.0 : oy;
     const double sx_oth = side == 0 ? ox : 0.0, sy_oth = side == 0 ? oy : 0.0;
-    const int tv[3] = {T.x, T.y, T.z};
-    double2 Tp[3];
-    double lox = 1e300, loy = 1e300, hix = -1e300, hiy = -1e300;
-    for (int v = 0; v < 3; ++v) {
-        const double2 u = P.uv[tv[v]];
-        Tp[v] = make_double2(u.x + sx_own, u.y + sy_own);
-        lox = fmin(lox, Tp[v].x); hix = fmax(hix, Tp[v].x);
-        loy = fmin(loy, Tp[v].y); hiy = fmax(hiy, Tp[v].y);
+    const int64_t rid0 = (side == 0 ? 0 : (int64_t)P.nTA * P.S) + (int64_t)s * nT;
+
+    // lane j < PAIR_TPW: query box of triangle t0 + j in the other surface's frame
+    double qlx_l = 1.0, qhx_l = 0.0, qly_l = 1.0, qhy_l = 0.0;
+    if (lane < PAIR_TPW && t0 + lane < nT) {
+        const int4 T = own_tri[t0 + lane];
+        const int tv[3] = {T.x, T.y, T.z};
+        double lox = 1e300, loy = 1e300, hix = -1e300, hiy = -1e300;
+        for (int v = 0; v < 3; ++v) {
+            const double2 u = P.uv[tv[v]];
+            const double px = u.x + sx_own, py = u.y + sy_own;
+            lox = fmin(lox, px); hix = fmax(hix, px);
+            loy = fmin(loy, py); hiy = fmax(hiy, py);
+        }
+        qlx_l = lox - sx_oth; qhx_l = hix - sx_oth; qly_l = loy - sy_oth; qhy_l = hiy - sy_oth;
+        if (qlx_l > G.hx || qhx_l < G.lx || qly_l > G.hy || qhy_l < G.ly) {   // misses the surface
+            qlx_l = 1.0; qhx_l = 0.0;
+        }
     }
-    const double qlx = lox - sx_oth, qhx = hix - sx_oth, qly = loy - sy_oth, qhy = hiy - sy_oth;
-    const int bx0 = bin_coord(qlx, G.x0, G.inv_h, G.nx), bx1 = bin_coord(qhx, G.x0, G.inv_h, G.nx);
-    const int by0 = bin_coord(qly, G.y0, G.inv_h, G.ny), by1 = bin_coord(qhy, G.y0, G.inv_h, G.ny);
-    const int nbx = bx1 - bx0 + 1, nbins = nbx * (by1 - by0 + 1);
-    const int64_t rid = (side == 0 ? 0 : (int64_t)P.nTA * P.S) + (int64_t)s * nT + t;
-    PairRec *out = P.pairs + rid * P.pcap;
-    int j = 0;
+    // ---- 1. candidates -> queue
+    int qn = 0;
     bool ok = true;
-    for (int b0 = 0; b0 < nbins; b0 += 32) {   // up to 32 bins per round
-        const int bl = b0 + lane;
-        int bin = -1, cnt = 0;
-        if (bl < nbins) {
-            bin = (by0 + bl / nbx) * G.nx + bx0 + bl % nbx;
-            cnt = G.ptr[bin + 1] - G.ptr[bin];
-        }
-        const int off = warp_excl_scan(cnt, lane);
-        const int total = __shfl_sync(0xffffffffu, off + cnt, 31);
-        for (int base = 0; base < total; base += 32) {
-            const int idx = base + lane;
-            bool hit = false;
-            PairRec r;
-            int u = -1;
-            // bin slot q holding candidate idx (every lane takes part in the shuffles)
-            int q = 0;
-            for (int l = 1; l < 32; ++l) {
-                const int ol = __shfl_sync(0xffffffffu, off, l);
-                if (l < nbins - b0 && ol <= idx) q = l;
+    for (int j = 0; j < PAIR_TPW; ++j) {
+        const double qlx = __shfl_sync(0xffffffffu, qlx_l, j), qhx = __shfl_sync(0xffffffffu, qhx_l, j);
+        const double qly = __shfl_sync(0xffffffffu, qly_l, j), qhy = __shfl_sync(0xffffffffu, qhy_l, j);
+        if (lane == 0) qcnt[j] = 0;
+        if (!(qlx <= qhx)) continue;   // no triangle / no candidate
+        const int bx0 = bin_coord(qlx, G.x0, G.inv_h, G.nx), bx1 = bin_coord(qhx, G.x0, G.inv_h, G.nx);
+        const int by0 = bin_coord(qly, G.y0, G.inv_h, G.ny), by1 = bin_coord(qhy, G.y0, G.inv_h, G.ny);
+        const int nbx = bx1 - bx0 + 1, nbins = nbx * (by1 - by0 + 1);
+        for (int b0 = 0; b0 < nbins; b0 += 32) {   // up to 32 bins per round
+            const int bl = b0 + lane;
+            int bin = -1, cnt = 0;
+            if (bl < nbins) {
+                bin = (by0 + bl / nbx) * G.nx + bx0 + bl % nbx;
+                cnt = G.ptr[bin + 1] - G.ptr[bin];
             }
-            const int binq = __shfl_sync(0xffffffffu, bin, q);
-            const int offq = __shfl_sync(0xffffffffu, off, q);
-            if (idx < total) {
-                const int m = G.ptr[binq] + (idx - offq);
-                u = G.ids[m];
-                const double4 ub = oth_box[u];
-                const int bx = bx0 + (b0 + q) % nbx, by = by0 + (b0 + q) / nbx;
-                if (!(ub.x > qhx || ub.z < qlx || ub.y > qhy || ub.w < qly) &&
-                    bin_coord(fmax(qlx, ub.x), G.x0, G.inv_h, G.nx) == bx &&
-                    bin_coord(fmax(qly, ub.y), G.y0, G.inv_h, G.ny) == by) {
-                    const int4 W = oth_tri[u];
-                    const int wv[3] = {W.x, W.y, W.z};
-                    double2 Up[3];
-                    for (int v = 0; v < 3; ++v) {
-                        const double2 c2 = P.uv[wv[v]];
-                        Up[v] = make_double2(c2.x + sx_oth, c2.y + sy_oth);
-                    }
-                    hit = side == 0 ? pair_integrals(Tp, Up, true, r) : pair_integrals(Up, Tp, false, r);
+            const int off = warp_excl_scan(cnt, lane);
+            const int total = __shfl_sync(0xffffffffu, off + cnt, 31);
+            for (int base = 0; base < total; base += 32) {
+                const int idx = base + lane;
+                int qq = 0;   // bin slot holding candidate idx (every lane takes part in the shuffles)
+                for (int l = 1; l < 32; ++l) {
+                    const int ol = __shfl_sync(0xffffffffu, off, l);
+                    if (l < nbins - b0 && ol <= idx) qq = l;
                 }
-            }
-            const unsigned mask = __ballot_sync(0xffffffffu, hit);
-            if (hit) {
-                const int pos = j + __popc(mask & ((1u << lane) - 1u));
-                if (pos < P.pcap) {
-                    r.other = u;
-                    out[pos] = r;
-                } else {
-                    ok = false;
+                const int binq = __shfl_sync(0xffffffffu, bin, qq);
+                const int offq = __shfl_sync(0xffffffffu, off, qq);
+                bool cand = false;
+                int u = -1;
+                if (idx < total) {
+                    u = G.ids[G.ptr[binq] + (idx - offq)];
+                    const double4 ub = oth_box[u];
+                    const int bx = bx0 + (b0 + qq) % nbx, by = by0 + (b0 + qq) / nbx;
+                    cand = !(ub.x > qhx || ub.z < qlx || ub.y > qhy || ub.w < qly) &&
+                           bin_coord(fmax(qlx, ub.x), G.x0, G.inv_h, G.nx) == bx &&
+                           bin_coord(fmax(qly, ub.y), G.y0, G.inv_h, G.ny) == by;
                 }
+                const unsigned m = __ballot_sync(0xffffffffu, cand);
+                if (cand) {
+                    const int pos = qn + __popc(m & lt);
+                    if (pos < qcap) q[pos] = (u << 3) | j; else ok = false;
+                }
+                qn += __popc(m);
             }
-            j += __popc(mask);
         }
     }
-    if (!__all_sync(0xffffffffu, ok) || j > P.pcap) {
-        if (lane == 0) atomicOr(&P.status[1], 1);
+    __syncwarp();
+    // ---- 2. integrals, 32 queued pairs per round
+    const int nq = min(qn, qcap);
+    for (int r0 = 0; r0 < nq; r0 += 32) {
+        const int r = r0 + lane;
+        const bool valid = r < nq;
+        int j = 0, u = 0;
+        bool hit = false;
+        PairRec rec;
+        if (valid) {
+            const int e = q[r];
+            j = e & 7;
+            u = e >> 3;
+            const int4 T = own_tri[t0 + j], W = oth_tri[u];
+            const int tv[3] = {T.x, T.y, T.z}, wv[3] = {W.x, W.y, W.z};
+            double2 Tp[3], Up[3];
+            for (int v = 0; v < 3; ++v) {
+                const double2 a = P.uv[tv[v]], b = P.uv[wv[v]];
+                Tp[v] = make_double2(a.x + sx_own, a.y + sy_own);
+                Up[v] = make_double2(b.x + sx_oth, b.y + sy_oth);
+            }
+            hit = side == 0 ? pair_integrals(Tp, Up, true, rec) : pair_integrals(Up, Tp, false, rec);
+        }
+        const unsigned hm = __ballot_sync(0xffffffffu, hit);
+        const unsigned grp = __match_any_sync(0xffffffffu, valid ? j : 8 + lane);
+        if (hit) {
+            const int pos = qcnt[j] + __popc(hm & grp & lt);
+            if (pos < P.pcap) {
+                rec.other = u;
+                P.pairs[(rid0 + t0 + j) * P.pcap + pos] = rec;
+            } else {
+                ok = false;
+            }
+        }
+        __syncwarp();
+        if (valid && (grp & lt) == 0) qcnt[j] += __popc(hm & grp);   // group leader
+        __syncwarp();
     }
-    if (lane == 0) P.pcnt[rid] = min(j, P.pcap);
+    if (!__all_sync(0xffffffffu, ok) && lane == 0) atomicOr(&P.status[1], 1);
+    if (lane < PAIR_TPW && t0 + lane < nT) P.pcnt[rid0 + t0 + lane] = min(qcnt[lane], P.pcap);
 }
 
 // ------------------------------------------------------------------------------ K2b: rows
@@ -483,6 +561,7 @@ static void make_bins(const std::vector<double4> &box, std::vector<int32_t> &ptr
     if (!(h > 0)) h = 1.0;
     g.x0 = nt ? lx : 0.0;
     g.y0 = nt ? ly : 0.0;
+    g.lx = lx; g.ly = ly; g.hx = hx; g.hy = hy;
     g.inv_h = 1.0 / h;
     g.nx = nx;
     g.ny = ny;
@@ -688,6 +767,10 @@ int iface_setup(Ctx &c, const double *X, const std::vector<int32_t> &fA, const s
     if (mx > 2048) { c.err = "interface rows too dense (capacity > 2048)"; return -5; }
     c.cap = ((mx + 4) + 3) / 4 * 4;
     c.pcap = pmx + 2;
+    if ((size_t)PAIR_WPB * PAIR_TPW * c.pcap * sizeof(int) > 48 * 1024) {
+        c.err = "interface triangles overlap too many triangles of the other surface";
+        return -5;
+    }
     // contributions per row: 6 per record, records <= star size x pcap
     int max_star = 0;
     for (int k = 0; k < c.n_if; ++k) max_star = std::max(max_star, sptr[k + 1] - sptr[k]);
@@ -749,9 +832,11 @@ void iface_params(Ctx &c, IfaceParams &P, const double *step_sc, double dt) {
 
 int iface_launch(Ctx &c, const IfaceParams &P) {
     if (c.n_if == 0) return 0;
-    k_pairs<<<dim3((unsigned)((c.nTA + 3) / 4), (unsigned)c.S), 128, 0, c.stream>>>(P, 0);
+    const int tpb = PAIR_WPB * PAIR_TPW;
+    const size_t qsm = sizeof(int) * (size_t)PAIR_WPB * PAIR_TPW * c.pcap;
+    k_pairs<<<dim3((unsigned)((c.nTA + tpb - 1) / tpb), (unsigned)c.S), 32 * PAIR_WPB, qsm, c.stream>>>(P, 0);
     CK(cudaGetLastError());
-    k_pairs<<<dim3((unsigned)((c.nTB + 3) / 4), (unsigned)c.S), 128, 0, c.stream>>>(P, 1);
+    k_pairs<<<dim3((unsigned)((c.nTB + tpb - 1) / tpb), (unsigned)c.S), 32 * PAIR_WPB, qsm, c.stream>>>(P, 1);
     CK(cudaGetLastError());
     k_rows<<<dim3((unsigned)((c.n_if + ROW_WPB - 1) / ROW_WPB), (unsigned)c.S), 32 * ROW_WPB, 0, c.stream>>>(P);
     CK(cudaGetLastError());

@@ -380,7 +380,8 @@ extern "C" int thermo_step(void *ctx, double t, double dt, int32_t nsteps) {
         if (c->d_trace) {   // phase split of the last solve (debug aid)
             unsigned long long tr[1024];
             API_CK(cudaMemcpy(tr, c->d_trace, sizeof tr, cudaMemcpyDeviceToHost));
-            const int it = c->h_iters[(size_t)(nsteps - 1) * S];
+            int it = 0;   // loop iterations of the last solve (max over the scenarios)
+            for (int j = 0; j < S; ++j) it = std::max(it, (int)c->h_iters[(size_t)(nsteps - 1) * S + j]);
             double s_ns = 0, u_ns = 0;
             for (int k = 0; k < it && 2 + 2 * k + 1 < 1024; ++k) {
                 s_ns += (double)(tr[2 + 2 * k] - tr[1 + 2 * k]);
