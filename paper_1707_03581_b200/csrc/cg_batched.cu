@@ -50,6 +50,7 @@ struct CGBParams {
     const double *ML, *benv, *DinvS;
     int n_if, nA, cap;
     const int32_t *if_rows, *slice_if, *ell_cnt, *ell_col;
+    const int32_t *if_of_row;   // [N] interface index of a row, -1 if none
     const double *ell_val, *if_b, *if_phi;
     const double *T_in;
     double *T_out, *z, *pa, *pb, *q;
@@ -162,68 +163,128 @@ __device__ __forceinline__ double2 row_spmm(const CGBParams &P, int64_t base, in
     return acc;
 }
 
-// Two rows (rA, rB) of one slice at once: lanes 0-15 load the entries of row A, lanes 16-31
-// those of row B (16 per round), the warp broadcasts them; every lane gathers its two columns
-// for both rows, so twice the loads are in flight.  Same fma order per row as row_spmm.
+// Two rows (rA, rA + 1) of one slice at once: lanes 0-15 hold the entries of row A, lanes
+// 16-31 those of row B (16 per round); the warp broadcasts them and every lane gathers its two
+// columns for both rows, so 16 loads per lane are in flight.  The entries of a round are
+// loaded by load_cv (for the first round one unit ahead, see unit_loop).
+__device__ __forceinline__ void load_cv(const CGBParams &P, int64_t base, int w, int rA, bool validB, int k0,
+                                        int lane, int &cl, double &vl) {
+    const int half = lane >> 4, kk = k0 + (lane & 15);
+    cl = 0;
+    vl = 0.0;
+    if (kk < w && (half == 0 || validB)) {
+        cl = P.col[base + 32 * (int64_t)kk + rA + half];
+        vl = P.val[base + 32 * (int64_t)kk + rA + half];
+    }
+}
+
 template <bool kTwo>
-__device__ __forceinline__ void row_spmm2(const CGBParams &P, int64_t base, int w, int rA, bool validB,
-                                          const double *x1, const double *x2, double2 beta, int lane,
-                                          double2 &accA, double2 &accB) {
-    accA = make_double2(0.0, 0.0);
-    accB = make_double2(0.0, 0.0);
-    const int ln = 2 * lane < P.SP ? lane : 0;
-    const int half = lane >> 4, hk = lane & 15;
-    for (int k0 = 0; k0 < w; k0 += 16) {
-        const int kk = k0 + hk;
-        int cl = 0;
-        double vl = 0.0;
-        if (kk < w && (half == 0 || validB)) {
-            cl = P.col[base + 32 * (int64_t)kk + rA + half];
-            vl = P.val[base + 32 * (int64_t)kk + rA + half];
-        }
-        const int m = min(16, w - k0);
-        for (int k = 0; k < m; k += 4) {
-            double2 yA[4], yB[4];
-            double vA[4], vB[4];
+__device__ __forceinline__ void gather_round(const CGBParams &P, int cl, double vl, int m, const double *x1,
+                                             const double *x2, double2 beta, int ln, double2 &accA, double2 &accB) {
+    for (int k = 0; k < m; k += 4) {
+        double2 yA[4], yB[4];
+        double vA[4], vB[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int ku = min(k + u, m - 1);
-                const int cA = __shfl_sync(0xffffffffu, cl, ku);
-                const int cB = __shfl_sync(0xffffffffu, cl, 16 + ku);
-                vA[u] = k + u < m ? __shfl_sync(0xffffffffu, vl, ku) : 0.0;
-                vB[u] = k + u < m ? __shfl_sync(0xffffffffu, vl, 16 + ku) : 0.0;
-                const double2 a = reinterpret_cast<const double2 *>(x1 + (int64_t)cA * P.SP)[ln];
-                const double2 b = reinterpret_cast<const double2 *>(x1 + (int64_t)cB * P.SP)[ln];
-                if (kTwo) {
-                    const double2 a2 = reinterpret_cast<const double2 *>(x2 + (int64_t)cA * P.SP)[ln];
-                    const double2 b2 = reinterpret_cast<const double2 *>(x2 + (int64_t)cB * P.SP)[ln];
-                    yA[u] = make_double2(fma(beta.x, a2.x, a.x), fma(beta.y, a2.y, a.y));
-                    yB[u] = make_double2(fma(beta.x, b2.x, b.x), fma(beta.y, b2.y, b.y));
-                } else {
-                    yA[u] = a;
-                    yB[u] = b;
-                }
+        for (int u = 0; u < 4; ++u) {
+            const int ku = min(k + u, m - 1);
+            const int cA = __shfl_sync(0xffffffffu, cl, ku);
+            const int cB = __shfl_sync(0xffffffffu, cl, 16 + ku);
+            vA[u] = k + u < m ? __shfl_sync(0xffffffffu, vl, ku) : 0.0;
+            vB[u] = k + u < m ? __shfl_sync(0xffffffffu, vl, 16 + ku) : 0.0;
+            const double2 a = reinterpret_cast<const double2 *>(x1 + (int64_t)cA * P.SP)[ln];
+            const double2 b = reinterpret_cast<const double2 *>(x1 + (int64_t)cB * P.SP)[ln];
+            if (kTwo) {
+                const double2 a2 = reinterpret_cast<const double2 *>(x2 + (int64_t)cA * P.SP)[ln];
+                const double2 b2 = reinterpret_cast<const double2 *>(x2 + (int64_t)cB * P.SP)[ln];
+                yA[u] = make_double2(fma(beta.x, a2.x, a.x), fma(beta.y, a2.y, a.y));
+                yB[u] = make_double2(fma(beta.x, b2.x, b.x), fma(beta.y, b2.y, b.y));
+            } else {
+                yA[u] = a;
+                yB[u] = b;
             }
+        }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                if (k + u < m) {
-                    accA.x = fma(vA[u], yA[u].x, accA.x);
-                    accA.y = fma(vA[u], yA[u].y, accA.y);
-                    accB.x = fma(vB[u], yB[u].x, accB.x);
-                    accB.y = fma(vB[u], yB[u].y, accB.y);
-                }
+        for (int u = 0; u < 4; ++u) {
+            if (k + u < m) {
+                accA.x = fma(vA[u], yA[u].x, accA.x);
+                accA.y = fma(vA[u], yA[u].y, accA.y);
+                accB.x = fma(vB[u], yB[u].x, accB.x);
+                accB.y = fma(vB[u], yB[u].y, accB.y);
             }
         }
     }
 }
 
-// Interface index of row i of slice s (-1 if none); warp-uniform.
-__device__ __forceinline__ int iface_of(const CGBParams &P, int64_t s, int64_t i, int lane) {
-    const int b = P.slice_if[s], e = P.slice_if[s + 1];
-    if (b == e) return -1;
-    const int j = b + lane;
-    const unsigned m = __ballot_sync(0xffffffffu, j < e && P.if_rows[j] == (int)i);
-    return m ? b + __ffs(m) - 1 : -1;
+// Row sums of the shared volume operator for rows rA, rA + 1 of a slice applied to the lane's
+// two columns of y = x1 + beta x2 (kTwo = false: y = x1).  (cl, vl): entries 0..15, preloaded.
+template <bool kTwo>
+__device__ __forceinline__ void row_spmm2(const CGBParams &P, int64_t base, int w, int rA, bool validB, int cl,
+                                          double vl, const double *x1, const double *x2, double2 beta, int lane,
+                                          double2 &accA, double2 &accB) {
+    accA = make_double2(0.0, 0.0);
+    accB = make_double2(0.0, 0.0);
+    const int ln = 2 * lane < P.SP ? lane : 0;   // lanes past the row stride re-read columns 0..1
+    gather_round<kTwo>(P, cl, vl, min(16, w), x1, x2, beta, ln, accA, accB);
+    for (int k0 = 16; k0 < w; k0 += 16) {
+        load_cv(P, base, w, rA, validB, k0, lane, cl, vl);
+        gather_round<kTwo>(P, cl, vl, min(16, w - k0), x1, x2, beta, ln, accA, accB);
+    }
+}
+
+// Walk this warp's units (slice s, row pair rA, rA + 1; unit u = gw + k TW).  Per 32 units,
+// lane k loads unit k's slice offset, width and interface indices in one round trip; the
+// first round of matrix entries of the next unit is loaded while the current one gathers.
+// body(u, base, w, rA, validB, ikA, ikB, cl, vl) runs once per unit, warp-uniformly.
+template <class Body>
+__device__ __forceinline__ void unit_loop(const CGBParams &P, int64_t npairs, int gw, int TW, int lane, Body body) {
+    const int64_t N = P.N;
+    for (int64_t c0 = gw; c0 < npairs; c0 += 32 * (int64_t)TW) {
+        const int64_t uk = c0 + (int64_t)lane * TW;
+        long long m_base = 0;
+        int m_w = -1, m_ikA = -1, m_ikB = -1;
+        if (uk < npairs) {
+            const int64_t s = uk >> 4, iA = 32 * s + 2 * (uk & 15);
+            if (iA < N) {
+                m_base = P.slice_ptr[s];
+                m_w = (int)((P.slice_ptr[s + 1] - m_base) >> 5);
+                m_ikA = P.if_of_row[iA];
+                m_ikB = iA + 1 < N ? P.if_of_row[iA + 1] : -1;
+            }
+        }
+        const int64_t rem = (npairs - c0 + TW - 1) / TW;
+        const int nun = rem < 32 ? (int)rem : 32;
+        int cl = 0, cln = 0;
+        double vl = 0.0, vln = 0.0;
+        {
+            const int w0 = __shfl_sync(0xffffffffu, m_w, 0);
+            if (w0 >= 0) {
+                const int64_t iA = 32 * (c0 >> 4) + 2 * (c0 & 15);
+                load_cv(P, __shfl_sync(0xffffffffu, m_base, 0), w0, 2 * (int)(c0 & 15), iA + 1 < N, 0, lane, cl, vl);
+            }
+        }
+        for (int k = 0; k < nun; ++k) {
+            const int64_t u = c0 + (int64_t)k * TW;
+            const int64_t base = __shfl_sync(0xffffffffu, m_base, k);
+            const int w = __shfl_sync(0xffffffffu, m_w, k);
+            const int ikA = __shfl_sync(0xffffffffu, m_ikA, k), ikB = __shfl_sync(0xffffffffu, m_ikB, k);
+            if (k + 1 < nun) {   // next unit's first round of entries
+                const int64_t un = u + TW;
+                const int wn = __shfl_sync(0xffffffffu, m_w, k + 1);
+                const long long bn = __shfl_sync(0xffffffffu, m_base, k + 1);
+                if (wn >= 0) {
+                    const int64_t iAn = 32 * (un >> 4) + 2 * (un & 15);
+                    load_cv(P, bn, wn, 2 * (int)(un & 15), iAn + 1 < N, 0, lane, cln, vln);
+                }
+            }
+            if (w >= 0) {
+                const int rA = 2 * (int)(u & 15);
+                const bool validB = 32 * (u >> 4) + rA + 1 < N;
+                body(u, base, w, rA, validB, ikA, ikB, cl, vl);
+            }
+            cl = cln;
+            vl = vln;
+        }
+    }
 }
 
 // Interface rows (per scenario): lane's two columns of row ik.
@@ -272,20 +333,24 @@ __global__ void __launch_bounds__(CGB_BLOCK, 1) k_cgb_step(CGBParams P) {
     // ---- phase 0: r0 = b - K~ x0, z0 = D^{-1} r0 per column
     double v0[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};   // b.b, r.r, r.z, |Gamma_R| (scenario 0)
     const int64_t npairs = P.nslices * 16;   // units: (slice, row pair)
-    for (int64_t u = gw; u < npairs; u += TW) {
-        const int64_t s = u >> 4;
-        const int rA = 2 * (int)(u & 15);
-        const int64_t iA = 32 * s + rA;
-        if (iA >= N) continue;
-        const bool validB = iA + 1 < N;
-        const int64_t base = P.slice_ptr[s];
-        const int w = (int)((P.slice_ptr[s + 1] - base) >> 5);
+    unit_loop(P, npairs, gw, TW, lane, [&](int64_t u, int64_t base, int w, int rA, bool validB, int ikA, int ikB,
+                                           int cl, double vl) {
+        const int64_t iA = 32 * (u >> 4) + rA;
+        double2 Tr[2], dr[2];   // own rows, loaded ahead of the gathers
+        if (lane_ok) {
+            Tr[0] = reinterpret_cast<const double2 *>(P.T_in + iA * P.SP)[lane];
+            dr[0] = reinterpret_cast<const double2 *>(P.DinvS + iA * P.SP)[lane];
+            if (validB) {
+                Tr[1] = reinterpret_cast<const double2 *>(P.T_in + (iA + 1) * P.SP)[lane];
+                dr[1] = reinterpret_cast<const double2 *>(P.DinvS + (iA + 1) * P.SP)[lane];
+            }
+        }
         double2 axr[2];
-        row_spmm2<false>(P, base, w, rA, validB, P.T_in, nullptr, make_double2(0, 0), lane, axr[0], axr[1]);
+        row_spmm2<false>(P, base, w, rA, validB, cl, vl, P.T_in, nullptr, make_double2(0, 0), lane, axr[0], axr[1]);
         for (int h = 0; h < 2; ++h) {
             const int64_t i = iA + h;
             if (h == 1 && !validB) break;
-            const int ik = iface_of(P, s, i, lane);
+            const int ik = h ? ikB : ikA;
             double2 ax = axr[h];
             double2 bg = make_double2(0.0, 0.0);
             if (ik >= 0) {
@@ -297,8 +362,7 @@ __global__ void __launch_bounds__(CGB_BLOCK, 1) k_cgb_step(CGBParams P) {
                 if (lane == 0 && ik < P.nA) v0[3][0] += P.if_phi[(int64_t)ik * P.S];
             }
             if (!lane_ok) continue;
-            const double2 Ti = reinterpret_cast<const double2 *>(P.T_in + i * P.SP)[lane];
-            const double2 di = reinterpret_cast<const double2 *>(P.DinvS + i * P.SP)[lane];
+            const double2 Ti = Tr[h], di = dr[h];
             const double ml = P.ML[i], be = P.benv[i];
             double2 b, rr, zz;
             b.x = fma(ml, Ti.x, P.dt * (be + bg.x));
@@ -319,7 +383,7 @@ __global__ void __launch_bounds__(CGB_BLOCK, 1) k_cgb_step(CGBParams P) {
                 v0[2][1] = fma(rr.y, zz.y, v0[2][1]);
             }
         }
-    }
+    });
     double t0[4][2];
     cgb_reduce<4>(v0, sm, P.partials, grid, t0);
     if (tr_on) P.trace[ntr++] = gtimer();
@@ -341,21 +405,25 @@ __global__ void __launch_bounds__(CGB_BLOCK, 1) k_cgb_step(CGBParams P) {
         const bool first = it == 0;
         const double2 b2 = make_double2(beta[0], beta[1]);
         double vs[1][2] = {{0.0, 0.0}};
-        for (int64_t u = gw; u < npairs; u += TW) {
-            const int64_t s = u >> 4;
-            const int rA = 2 * (int)(u & 15);
-            const int64_t iA = 32 * s + rA;
-            if (iA >= N) continue;
-            const bool validB = iA + 1 < N;
-            const int64_t base = P.slice_ptr[s];
-            const int w = (int)((P.slice_ptr[s + 1] - base) >> 5);
+        unit_loop(P, npairs, gw, TW, lane, [&](int64_t u, int64_t base, int w, int rA, bool validB, int ikA,
+                                               int ikB, int cl, double vl) {
+            const int64_t iA = 32 * (u >> 4) + rA;
+            double2 zr[2], pr[2];   // own rows, loaded ahead of the gathers
+            if (lane_ok) {
+                zr[0] = reinterpret_cast<const double2 *>(P.z + iA * P.SP)[lane];
+                if (!first) pr[0] = reinterpret_cast<const double2 *>(pold + iA * P.SP)[lane];
+                if (validB) {
+                    zr[1] = reinterpret_cast<const double2 *>(P.z + (iA + 1) * P.SP)[lane];
+                    if (!first) pr[1] = reinterpret_cast<const double2 *>(pold + (iA + 1) * P.SP)[lane];
+                }
+            }
             double2 accr[2];
-            if (first) row_spmm2<false>(P, base, w, rA, validB, P.z, nullptr, b2, lane, accr[0], accr[1]);
-            else row_spmm2<true>(P, base, w, rA, validB, P.z, pold, b2, lane, accr[0], accr[1]);
+            if (first) row_spmm2<false>(P, base, w, rA, validB, cl, vl, P.z, nullptr, b2, lane, accr[0], accr[1]);
+            else row_spmm2<true>(P, base, w, rA, validB, cl, vl, P.z, pold, b2, lane, accr[0], accr[1]);
             for (int h = 0; h < 2; ++h) {
                 const int64_t i = iA + h;
                 if (h == 1 && !validB) break;
-                const int ik = iface_of(P, s, i, lane);
+                const int ik = h ? ikB : ikA;
                 double2 acc = accr[h];
                 if (ik >= 0) {
                     const double2 ai = first ? row_iface<false>(P, ik, P.z, nullptr, b2, lane)
@@ -364,18 +432,14 @@ __global__ void __launch_bounds__(CGB_BLOCK, 1) k_cgb_step(CGBParams P) {
                     acc.y += ai.y;
                 }
                 if (!lane_ok) continue;
-                const double2 zi = reinterpret_cast<const double2 *>(P.z + i * P.SP)[lane];
-                double2 pi = zi;
-                if (!first) {
-                    const double2 po = reinterpret_cast<const double2 *>(pold + i * P.SP)[lane];
-                    pi = make_double2(fma(b2.x, po.x, zi.x), fma(b2.y, po.y, zi.y));
-                }
+                double2 pi = zr[h];
+                if (!first) pi = make_double2(fma(b2.x, pr[h].x, pi.x), fma(b2.y, pr[h].y, pi.y));
                 reinterpret_cast<double2 *>(pnew + i * P.SP)[lane] = pi;
                 reinterpret_cast<double2 *>(P.q + i * P.SP)[lane] = acc;
                 vs[0][0] = fma(pi.x, acc.x, vs[0][0]);
                 vs[0][1] = fma(pi.y, acc.y, vs[0][1]);
             }
-        }
+        });
         double tpq[1][2];
         cgb_reduce<1>(vs, sm, P.partials, grid, tpq);
         if (tr_on && ntr < 1000) P.trace[ntr++] = gtimer();
@@ -480,7 +544,7 @@ int cgb_setup(Ctx &c) {
     c.cg_block = CGB_BLOCK;
     CK(cudaMalloc(&c.d_partials, sizeof(double) * (size_t)CGB_NV * 64 * c.cg_grid));
     CK(cudaMalloc(&c.d_DinvS, sizeof(double) * (size_t)c.N * c.SP + 16));
-    return 0;
+    return build_if_of_row(c);
 }
 
 int cgb_prepare(Ctx &c) {
@@ -508,6 +572,7 @@ int cgb_launch_step(Ctx &c, int step, double dt) {
     P.cap = c.cap;
     P.if_rows = c.d_if_rows;
     P.slice_if = c.d_slice_if;
+    P.if_of_row = c.d_if_of_row;
     P.ell_cnt = c.d_ell_cnt;
     P.ell_col = c.d_ell_col;
     P.ell_val = c.d_ell_val;

@@ -155,6 +155,7 @@ int cg_launch_solve(Ctx &c, const double *x0, double *x, const double *rhs, cons
 
 // mrsdc.cu (multi-rate SDC)
 int mrsdc_setup(Ctx &c);
+int build_if_of_row(Ctx &c);
 int mrsdc_step(Ctx &c, double tn, double dt, int step_index);
 
 // cg_batched.cu (S > 1 scenarios advanced together)

@@ -118,6 +118,16 @@ __global__ void k_if_of_row(const int32_t *if_rows, int n_if, int32_t *map) {
     if (k < n_if) map[if_rows[k]] = k;
 }
 
+// row -> interface index map (-1 for volume-only rows), built once per context
+int build_if_of_row(Ctx &c) {
+    if (c.d_if_of_row) return 0;
+    CK(cudaMalloc(&c.d_if_of_row, sizeof(int32_t) * (size_t)c.N));
+    CK(cudaMemsetAsync(c.d_if_of_row, 0xff, sizeof(int32_t) * (size_t)c.N, c.stream));
+    if (c.n_if) k_if_of_row<<<nbk(c.n_if), 256, 0, c.stream>>>(c.d_if_rows, c.n_if, c.d_if_of_row);
+    CK(cudaGetLastError());
+    return 0;
+}
+
 // ---------------------------------------------------------------------------------
 // Table 1 weights on the host: exact integrals of Lagrange polynomials.
 // ---------------------------------------------------------------------------------
@@ -208,12 +218,7 @@ int mrsdc_setup(Ctx &c) {
     CK(cudaMalloc(&c.d_mr, sizeof(double) * (nfull * Np + ncomp * nif + 64)));
     CK(cudaMemsetAsync(c.d_mr, 0, sizeof(double) * (nfull * Np + ncomp * nif + 64), c.stream));
     c.mr_vectors = nfull;
-    if (!c.d_if_of_row) {
-        CK(cudaMalloc(&c.d_if_of_row, sizeof(int32_t) * N));
-        CK(cudaMemsetAsync(c.d_if_of_row, 0xff, sizeof(int32_t) * N, c.stream));
-        if (c.n_if) k_if_of_row<<<nbk(c.n_if), 256, 0, c.stream>>>(c.d_if_rows, c.n_if, c.d_if_of_row);
-        CK(cudaGetLastError());
-    }
+    if (int rc = build_if_of_row(c)) return rc;
     // interface operators at the M P + 1 node times of a step
     const int nslot = M * P + 1;
     if (c.mr_nslots < nslot && c.n_if) {
