@@ -56,6 +56,7 @@ def lib():
         L.or_step.argtypes = [_p, _d, _d, _i32, _d, _d, _d, _d, _d, _d, _d, _d, _d, _p, _i32, _d, _i32, _p]
         L.or_ie_residual_rows.argtypes = [_p, _d, _d, _d, _d, _d, _p, _p, _i64, _p, _p, _p]
         L.or_apply_system.argtypes = [_p, _d, _p, _p]
+        L.or_stationary.argtypes = [_p, _d, _i32, _d, _d, _d, _d, _d, _d, _d, _d, _d, _p, _i32, _d, _i32, _p]
         L.or_mrsdc_weights.argtypes = [ctypes.c_int, ctypes.c_int, _d, _d, _p, _p, _p, _p, _p, _p]
         L.or_step_mrsdc.argtypes = [_p, _d, _d, _i32, _i32, _i32, _i32, _d, _d, _d, _d, _d, _d, _d, _d, _d, _p,
                                     _d, _p]
@@ -194,6 +195,22 @@ def _step_mrsdc(self, T, t, dt, nsteps, scen, M=3, P=2, K=1, rtol=1e-12):
 
 
 Oracle.step_mrsdc = _step_mrsdc
+
+
+def _stationary(self, T, t, scen, with_interface=False, solver="cg", rtol=1e-12, maxit=0):
+    """Stationary state (reading R19/R28) from the initial guess T.
+    Returns (T, stats[3] = iterations, rel. residual, true rel. residual)."""
+    T = np.array(T, dtype=np.float64, copy=True)
+    stats = np.zeros(3)
+    rc = lib().or_stationary(self.h, t, 1 if with_interface else 0, scen.s0, scen.amp, scen.period,
+                             scen.dir[0], scen.dir[1], scen.dir[2], scen.eta0, scen.eta_amp, scen.eta_period,
+                             _ptr(T), 1 if solver == "cholesky" else 0, rtol, maxit, _ptr(stats))
+    if rc:
+        raise RuntimeError(f"oracle stationary failed rc={rc}: " + lib().or_last_error().decode())
+    return T, stats
+
+
+Oracle.stationary = _stationary
 
 
 def run_config(cfg, scen_index: int = 0, T_init: Optional[np.ndarray] = None, nsteps: Optional[int] = None,

@@ -72,6 +72,7 @@ struct or_sys {
     int64_t *irowptr;
     int32_t *icol;
     double *ival, *bG, iarea;
+    double mass;          /* coefficient of M_L in the system: 1 (implicit Euler), 0 (stationary) */
 };
 
 /* ------------------------------------------------------------------------------------ */
@@ -332,6 +333,7 @@ or_sys *or_create(int64_t nf, const double *xyz_f, int64_t ntf, const int32_t *t
     s->nf = nf; s->nm = nm; s->n = nf + nm;
     s->nt = ntf + ntm; s->nb = nbf + nbm;
     s->iface_tag = iface_tag; s->nu = nu; s->rho_cp = rho_cp; s->alpha = alpha_iface;
+    s->mass = 1.0;
     s->xyz = malloc(sizeof *s->xyz * (size_t)(3 * s->n));
     s->tets = malloc(sizeof *s->tets * (size_t)(4 * s->nt));
     s->faces = malloc(sizeof *s->faces * (size_t)(3 * s->nb + 1));
@@ -589,7 +591,7 @@ void or_apply_system(const or_sys *s, double dt, const double *x, double *y) {
             acc += (s->A[k] + s->B[k]) * x[s->col[k]];
         for (int64_t k = s->irowptr[i]; k < s->irowptr[i + 1]; k++)
             acc += s->ival[k] * x[s->icol[k]];
-        y[i] = s->ML[i] * x[i] - dt * acc;
+        y[i] = s->mass * s->ML[i] * x[i] - dt * acc;
     }
 }
 
@@ -600,12 +602,12 @@ static void system_diagonal(const or_sys *s, double dt, double *d) {
         kii += s->A[k] + s->B[k];
         for (int64_t m = s->irowptr[i]; m < s->irowptr[i + 1]; m++)
             if (s->icol[m] == i) kii += s->ival[m];
-        d[i] = s->ML[i] - dt * kii;
+        d[i] = s->mass * s->ML[i] - dt * kii;
     }
 }
 
 static void system_rhs(const or_sys *s, double dt, const double *T, double *b) {
-    for (int64_t i = 0; i < s->n; i++) b[i] = s->ML[i] * T[i] + dt * (s->benv[i] + s->bG[i]);
+    for (int64_t i = 0; i < s->n; i++) b[i] = s->mass * s->ML[i] * T[i] + dt * (s->benv[i] + s->bG[i]);
 }
 
 static double dot(int64_t n, const double *a, const double *b) {
@@ -660,7 +662,7 @@ static int dense_cholesky_solve(const or_sys *s, double dt, const double *b, dou
             K[i * n + s->col[k]] -= dt * (s->A[k] + s->B[k]);
         for (int64_t k = s->irowptr[i]; k < s->irowptr[i + 1]; k++)
             K[i * n + s->icol[k]] -= dt * s->ival[k];
-        K[i * n + i] += s->ML[i];
+        K[i * n + i] += s->mass * s->ML[i];
     }
     for (int64_t j = 0; j < n; j++) {
         double dsum = K[j * n + j];
@@ -726,6 +728,56 @@ int or_step(or_sys *s, double t, double dt, int32_t nsteps,
         if (it < 0) { rc = -4; break; }
         memcpy(T, x, sizeof *T * (size_t)n);
     }
+    free(b); free(x);
+    return rc;
+}
+
+/* Stationary state of the machine at rest (reading R19 of DESIGN.md): the
+ * printed "M T(0) = f^I(T(0)) + g(0)" is read as 0 = f^I(T) + g = (A + B_env) T + b_env,
+ * i.e. -(A + B_env) T = b_env for both parts (uncoupled: f^E is not part of f^I).  With
+ * with_interface != 0 the coupling and friction at time t are added (reading R28):
+ * -(A + B_env + K_G(t)) T = b_env + b_G(t).  This is the implicit-Euler system with the mass
+ * term dropped and dt = 1, solved by the same dense Cholesky (solver = 1) or Jacobi-PCG from
+ * x0 = T.  stats (may be NULL): {iterations, rel. residual, true rel. residual}. */
+int or_stationary(or_sys *s, double t, int32_t with_interface, double s0, double amp, double period,
+                  double dx, double dy, double dz, double eta0, double eta_amp, double eta_period,
+                  double *T, int32_t solver, double rtol, int32_t maxit, double *stats) {
+    int64_t n = s->n;
+    if (with_interface) {
+        double sp = s0 + amp * sin(2.0 * M_PI * t / period);
+        double etap = eta0 * (1.0 + eta_amp * sin(2.0 * M_PI * t / eta_period));
+        if (or_assemble_interface(s, sp * dx, sp * dy, sp * dz, etap)) return -5;
+    } else {   /* no coupling: empty interface rows, no friction */
+        memset(s->bG, 0, sizeof *s->bG * (size_t)n);
+        for (int64_t i = 0; i <= n; i++) s->irowptr[i] = 0;
+        s->inz = 0;
+        s->iarea = 0.0;
+    }
+    double *b = malloc(sizeof *b * (size_t)n), *x = malloc(sizeof *x * (size_t)n);
+    if (!b || !x) return -2;
+    s->mass = 0.0;
+    system_rhs(s, 1.0, T, b);   /* = b_env (+ b_G) */
+    memcpy(x, T, sizeof *x * (size_t)n);
+    double relres = 0.0, truerel = 0.0;
+    int64_t it = 0;
+    int rc = 0;
+    if (solver == 1) {
+        if (dense_cholesky_solve(s, 1.0, b, x)) rc = -3;
+        else {
+            double *q = malloc(sizeof *q * (size_t)n);
+            or_apply_system(s, 1.0, x, q);
+            double rr = 0.0, bb = dot(n, b, b);
+            for (int64_t i = 0; i < n; i++) rr += (b[i] - q[i]) * (b[i] - q[i]);
+            free(q);
+            relres = truerel = sqrt(rr / bb);
+        }
+    } else {
+        it = pcg(s, 1.0, b, x, rtol, maxit > 0 ? maxit : 10 * n, &relres, &truerel);
+        if (it < 0) rc = -4;
+    }
+    s->mass = 1.0;
+    if (stats) { stats[0] = (double)it; stats[1] = relres; stats[2] = truerel; }
+    if (!rc) memcpy(T, x, sizeof *T * (size_t)n);
     free(b); free(x);
     return rc;
 }

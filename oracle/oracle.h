@@ -79,6 +79,14 @@ int or_step(or_sys *s, double t, double dt, int32_t nsteps,
 
 /* Residual rows of the IE system for given T^n, T^{n+1}: res[k] = (K~ T1 - b)[rows[k]],
  * with the system assembled at offset o, eta (both given).  Also returns ||b||_2 in bnorm. */
+/* Stationary state at rest (reading R19): -(A + B_env [+ K_G(t)]) T = b_env
+ * [+ b_G(t)]; with_interface selects the coupled variant (reading R28).  T: in = x0, out =
+ * solution.  solver 1 = dense Cholesky, else Jacobi-PCG to rtol.  stats[3] = {iterations,
+ * rel. residual, true rel. residual}.  Returns 0, -4 (no convergence), -5 (interface). */
+int or_stationary(or_sys *s, double t, int32_t with_interface, double s0, double amp, double period,
+                  double dx, double dy, double dz, double eta0, double eta_amp, double eta_period,
+                  double *T, int32_t solver, double rtol, int32_t maxit, double *stats);
+
 int or_ie_residual_rows(or_sys *s, double dt, double ox, double oy, double oz, double eta,
                         const double *T0, const double *T1, int64_t nrows,
                         const int64_t *rows, double *res, double *bnorm);

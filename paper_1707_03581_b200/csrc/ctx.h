@@ -94,6 +94,11 @@ struct Ctx {
     size_t cg_smem = 0;
     bool cg_tma = false;
     int cg_variant = 0, cg_chunk = 8, cg_debug = 0, cg_prefetch = 0;
+    // batched windowed sweeps (cg_batched.cu); reuse d_chunk_runs / nruns / lown and d_lcol
+    int cgw_on = 0, cgw_CR = 0, cgw_NS = 0, cgw_wcap = 0;
+    int64_t cgw_nchunks = 0;
+    uint32_t cgw_stage = 0, cgw_off[4] = {0, 0, 0, 0};
+    size_t cgw_smem = 0;
     int32_t *d_chunk_hi = nullptr;
     uint16_t *d_lcol = nullptr;      // chunk-local 16-bit columns (window kernels)
     int2 *d_chunk_runs = nullptr;    // window runs per chunk

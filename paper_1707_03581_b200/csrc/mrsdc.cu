@@ -119,10 +119,10 @@ __global__ void k_if_of_row(const int32_t *if_rows, int n_if, int32_t *map) {
 }
 
 // row -> interface index map (-1 for volume-only rows), built once per context
-int build_if_of_row(Ctx &c) {
+int build_if_of_row(Ctx &c) {   // padded to whole slices (nslices * 32 entries)
     if (c.d_if_of_row) return 0;
-    CK(cudaMalloc(&c.d_if_of_row, sizeof(int32_t) * (size_t)c.N));
-    CK(cudaMemsetAsync(c.d_if_of_row, 0xff, sizeof(int32_t) * (size_t)c.N, c.stream));
+    CK(cudaMalloc(&c.d_if_of_row, sizeof(int32_t) * (size_t)c.nslices * 32));
+    CK(cudaMemsetAsync(c.d_if_of_row, 0xff, sizeof(int32_t) * (size_t)c.nslices * 32, c.stream));
     if (c.n_if) k_if_of_row<<<nbk(c.n_if), 256, 0, c.stream>>>(c.d_if_rows, c.n_if, c.d_if_of_row);
     CK(cudaGetLastError());
     return 0;
