@@ -130,6 +130,20 @@ int thermo_set_T(void *ctx, int32_t scen, int32_t part, const double *in, int64_
  * EINVAL for other methods, M or P outside [1, 8], K < 0, or method 1 with n_scen > 1. */
 int thermo_set_method(void *ctx, int32_t method, int32_t M, int32_t P, int32_t K);
 
+/* Replace the temperature by the stationary state of the machine at rest (the
+ * initial data of the paper's 3-D runs; readings R19, R28):
+ *   with_interface == 0:  0 = f^I(T) + g,  i.e. -(A + B_env) T = b_env for both parts
+ *                         (uncoupled, as printed: f^E is not part of f^I);
+ *   with_interface != 0:  -(A + B_env + K_G(t)) T = b_env + b_G(t), the coupling and friction
+ *                         of the scenario's stock position s(t) and eta(t) included.
+ * Solved by the same Jacobi-PCG kernel (x0 = current temperature, rtol / maxit of
+ * thermo_set_solver; the unshifted operator needs O(1/h) iterations).  Requires a single
+ * scenario (EINVAL otherwise: solve on a one-scenario context, copy with thermo_set_T).
+ * ENOCONV if the solve did not converge (the temperature is then unchanged), EGEOM on
+ * interface overflow.  Iterations / residual / |Gamma_R| are reported by thermo_get_stats
+ * as a one-step run. */
+int thermo_stationary(void *ctx, double t, int32_t with_interface);
+
 /* CG stopping rule ||r||_2 <= rtol ||b||_2 (default 1e-12) and iteration cap
  * (default 0 = min(10 N, 10000)).  EINVAL if rtol <= 0 or maxit < 0. */
 int thermo_set_solver(void *ctx, double rtol, int32_t maxit);

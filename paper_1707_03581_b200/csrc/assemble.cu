@@ -289,12 +289,12 @@ __global__ void k_build_vals(const double *A, const double *R, int64_t n, double
     if (e < n) val[e] = -dt * (A[e] + R[e]);
 }
 
-__global__ void k_build_diag(const int64_t *diagpos, const double *ML, int64_t N, double *val,
+__global__ void k_build_diag(const int64_t *diagpos, const double *ML, double mu, int64_t N, double *val,
                              double *Dvol, double *Dinv, double *Dinv_vol) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= N) return;
     int64_t e = diagpos[i];
-    double d = val[e] + ML[i];
+    double d = val[e] + mu * ML[i];
     val[e] = d;
     Dvol[i] = d;
     Dinv[i] = 1.0 / d;
@@ -415,17 +415,17 @@ int assemble_robin(Ctx &c) {
     return 0;
 }
 
-int build_operator(Ctx &c, double dt) {
+int build_operator(Ctx &c, double dt, double mu) {
     cudaStream_t st = c.stream;
     k_build_vals<<<nb(c.nnz_pad), 256, 0, st>>>(c.d_A, c.d_R, c.nnz_pad, dt, c.d_val);
     CK(cudaGetLastError());
     if (!c.d_Dinv_vol) CK(cudaMalloc(&c.d_Dinv_vol, sizeof(double) * c.N));
-    k_build_diag<<<nb(c.N), 256, 0, st>>>(c.d_diagpos, c.d_ML, c.N, c.d_val, c.d_Dvol, c.d_Dinv, c.d_Dinv_vol);
+    k_build_diag<<<nb(c.N), 256, 0, st>>>(c.d_diagpos, c.d_ML, mu, c.N, c.d_val, c.d_Dvol, c.d_Dinv, c.d_Dinv_vol);
     CK(cudaGetLastError());
     if (!c.d_KV) CK(cudaMalloc(&c.d_KV, sizeof(double) * (c.nnz_pad + 1)));
     k_build_kv<<<nb(c.nnz_pad), 256, 0, st>>>(c.d_A, c.d_R, c.nnz_pad, c.d_KV);
     CK(cudaGetLastError());
-    c.built_dt = dt;
+    c.built_dt = mu == 1.0 ? dt : -1.0;   // anything but the implicit-Euler operator: rebuild next step
     return 0;
 }
 

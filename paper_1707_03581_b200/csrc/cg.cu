@@ -404,7 +404,11 @@ __device__ __forceinline__ void sweep(const CGParams &P, Ring &R, Body &&body) {
                 if (KIND == 2) {
                     const uint16_t *lc = reinterpret_cast<const uint16_t *>(sb + R.col_off);
                     const double *w1 = reinterpret_cast<const double *>(sb + R.win_off);
-                    SrcWin src{lc + o0 + lane, vals + o0 + lane, w1, w1 + P.win_cap, hdr[29] + 32 * wg + lane};
+                    // own row in the window; rows past N (padding lanes of the last slice) read
+                    // row N - 1 instead, whose value they discard
+                    const int64_t irow = 32 * s + lane;
+                    const int pad = irow > P.N - 1 ? (int)(irow - (P.N - 1)) : 0;
+                    SrcWin src{lc + o0 + lane, vals + o0 + lane, w1, w1 + P.win_cap, hdr[29] + 32 * wg + lane - pad};
                     body(s, src, (o1 - o0) >> 5, hdr[16 + wg], hdr[17 + wg]);
                 } else {
                     const int32_t *cols = reinterpret_cast<const int32_t *>(sb + R.col_off);

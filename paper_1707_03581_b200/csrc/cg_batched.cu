@@ -859,6 +859,10 @@ static int cgw_build(Ctx &c) {
     const size_t red = (size_t)CGW_WARPS * CGB_NV * 64 * 8;
     int NS = (int)std::min<size_t>(8, budget / stage);
     if (const char *e = getenv("THERMO_CGB_NS")) NS = std::min(NS, std::max(2, atoi(e)));
+    // a consumer group waits on parity (n / NS) & 1 of its stage: with more groups than
+    // stages - 1 a group could see the phase of the chunk NS earlier, so NS >= groups + 1
+    const int ngroups = 2 * CGW_NCW / (CR < CGW_NCW ? CR : CGW_NCW);
+    if (NS < ngroups + 1) return 0;
     if (NS < 2 || std::max((size_t)NS * stage, red) > budget) return 0;
     c.cgw_CR = CR;
     c.cgw_NS = NS;
@@ -885,9 +889,11 @@ static int cgw_build(Ctx &c) {
 int cgb_setup(Ctx &c) {
     if (c.S > CGB_MAXS) { c.err = "at most 64 scenarios per context"; return -1; }
     if (int rc = build_if_of_row(c)) return rc;
-    const char *kind = getenv("THERMO_CGB_KIND");   // 0: register gathers, 1 (default): windows
+    // THERMO_CGB_KIND=1 selects the windowed sweeps; measured slower than the register gathers
+    // on cfg 4, so the register kernel is the default
+    const char *kind = getenv("THERMO_CGB_KIND");
     c.cgw_on = 0;
-    if (!kind || atoi(kind) != 0) {
+    if (kind && atoi(kind) == 1) {
         const int r = cgw_build(c);
         if (r < 0) return r;
         c.cgw_on = r;

@@ -90,6 +90,7 @@ struct Ctx {
     double *d_relres = nullptr;      // [steps][S]
     double *d_area = nullptr;        // [steps]
     int64_t step_cap = 0;
+    double *d_rhs = nullptr;           // [N] right-hand side of the stationary solve
     int cg_grid = 0, cg_block = 0, cg_stage_entries = 0;
     size_t cg_smem = 0;
     bool cg_tma = false;
@@ -142,7 +143,7 @@ struct Ctx {
 int assemble_create(Ctx &c, const double *xyz, const int32_t *tets, const int32_t *faces,
                     const int32_t *fkey);
 int assemble_robin(Ctx &c);
-int build_operator(Ctx &c, double dt);
+int build_operator(Ctx &c, double dt, double mu = 1.0);   // K~ = mu M_L - dt (A + B_env)
 
 // iface.cu
 int iface_setup(Ctx &c, const double *h_xyz, const std::vector<int32_t> &facesA,

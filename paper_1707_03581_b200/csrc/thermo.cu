@@ -45,7 +45,7 @@ static void free_ctx(Ctx *c) {
                     c->d_relres, c->d_area, c->d_pairs, c->d_pcnt, c->d_chunk_hi, c->d_chunk_ctr, c->d_lcol, c->d_chunk_runs,
                     c->d_chunk_nruns, c->d_chunk_lown, c->d_trace, c->d_DinvS, c->d_slice_if_zero,
                     c->d_KV, c->d_Dinv_vol, c->d_if_of_row, c->d_mr, c->d_mr_iters, c->d_mr_relres,
-                    c->d_ell_cnt_s, c->d_ell_col_s, c->d_ell_val_s, c->d_if_b_s, c->d_if_phi_s};
+                    c->d_ell_cnt_s, c->d_ell_col_s, c->d_ell_val_s, c->d_if_b_s, c->d_if_phi_s, c->d_rhs};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     for (cudaEvent_t e : c->events) cudaEventDestroy(e);
@@ -220,6 +220,87 @@ extern "C" int thermo_set_bc(void *ctx, int32_t part, int32_t tag, double alpha,
         }
         int rc = thermo::assemble_robin(*c);
         return rc ? THERMO_ECUDA : THERMO_OK;
+    } catch (...) {
+        return fail(c, THERMO_ENOMEM, "host allocation failed");
+    }
+}
+
+// right-hand side of the stationary solve: b_env (+ b_G on the interface rows)
+__global__ void k_stat_rhs(const double *benv, int64_t N, const int32_t *if_of_row, const double *if_b, double *rhs) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    const int k = if_b ? if_of_row[i] : -1;
+    rhs[i] = k >= 0 ? benv[i] + if_b[k] : benv[i];
+}
+
+extern "C" int thermo_stationary(void *ctx, double t, int32_t with_interface) {
+    Ctx *c = (Ctx *)ctx;
+    if (!c) return THERMO_EINVAL;
+    if (!std::isfinite(t)) return fail(c, THERMO_EINVAL, "t must be finite");
+    if (c->S != 1)
+        return fail(c, THERMO_EINVAL, "the stationary solve runs on a single-scenario context (copy its result "
+                                      "into a batched one with thermo_set_T)");
+    try {
+        const int64_t N = c->N;
+        // -(A + B_env [+ K_G(t)]): the implicit-Euler operator with the mass term dropped, dt = 1
+        if (thermo::build_operator(*c, 1.0, 0.0)) return THERMO_ECUDA;
+        if (c->step_cap < 1) {
+            for (void *p : {(void *)c->d_step_sc, (void *)c->d_iters, (void *)c->d_relres, (void *)c->d_area})
+                if (p) cudaFree(p);
+            c->step_cap = 1;
+            API_CK(cudaMalloc(&c->d_step_sc, sizeof(double) * 4));
+            API_CK(cudaMalloc(&c->d_iters, sizeof(int32_t)));
+            API_CK(cudaMalloc(&c->d_relres, sizeof(double)));
+            API_CK(cudaMalloc(&c->d_area, sizeof(double)));
+        }
+        if (!c->d_rhs) API_CK(cudaMalloc(&c->d_rhs, sizeof(double) * (N + 16)));
+        API_CK(cudaMemsetAsync(c->d_status, 0, sizeof(int) * 8, c->stream));
+        const bool iface = with_interface && c->n_if > 0;
+        if (iface) {   // K_G, b_G, Jacobi rows at the stock position and friction of time t
+            const thermo::Scen &q = c->scen[0];
+            const double sv = q.s0 + q.amp * std::sin(2.0 * M_PI * t / q.period);
+            const double eta = q.eta0 * (1.0 + q.eta_amp * std::sin(2.0 * M_PI * t / q.eta_period));
+            const double sc[4] = {sv * q.d2[0], sv * q.d2[1], eta, sv};
+            API_CK(cudaMemcpyAsync(c->d_step_sc, sc, sizeof sc, cudaMemcpyHostToDevice, c->stream));
+            thermo::IfaceParams P;
+            memset(&P, 0, sizeof P);
+            thermo::iface_params(*c, P, c->d_step_sc, 1.0);
+            if (thermo::iface_launch(*c, P)) return THERMO_ECUDA;
+        }
+        if (thermo::build_if_of_row(*c)) return THERMO_ECUDA;
+        k_stat_rhs<<<(unsigned)((N + 255) / 256), 256, 0, c->stream>>>(c->d_benv, N, c->d_if_of_row,
+                                                                         iface ? c->d_if_b : nullptr, c->d_rhs);
+        API_CK(cudaGetLastError());
+        double *x0 = c->d_T[c->cur], *x = c->d_T[c->cur ^ 1];
+        if (thermo::cg_launch_solve(*c, x0, x, c->d_rhs, iface ? c->d_Dinv : c->d_Dinv_vol, iface, c->d_iters,
+                                    c->d_relres, 0))
+            return THERMO_ECUDA;
+        int status[8];
+        int32_t it = 0;
+        double rr = 0.0, area = 0.0;
+        API_CK(cudaMemcpyAsync(status, c->d_status, sizeof status, cudaMemcpyDeviceToHost, c->stream));
+        API_CK(cudaMemcpyAsync(&it, c->d_iters, sizeof it, cudaMemcpyDeviceToHost, c->stream));
+        API_CK(cudaMemcpyAsync(&rr, c->d_relres, sizeof rr, cudaMemcpyDeviceToHost, c->stream));
+        API_CK(cudaMemcpyAsync(&area, c->d_area, sizeof area, cudaMemcpyDeviceToHost, c->stream));
+        API_CK(cudaStreamSynchronize(c->stream));
+        c->h_iters.assign(1, it);
+        c->h_relres.assign(1, rr);
+        c->h_area.assign(1, iface ? area : 0.0);
+        c->last_nsteps = 1;
+        c->ms_iface = c->ms_solve = 0.0;
+        if (status[1]) return fail(c, THERMO_EGEOM, "interface row capacity exceeded in the stationary solve");
+        if (status[0]) {
+            c->failed_step = 0;
+            c->failed_scen = 0;
+            c->failed_relres = rr;
+            char buf[128];
+            snprintf(buf, sizeof buf, "stationary solve did not converge, relres %.3e", rr);
+            return fail(c, THERMO_ENOCONV, buf);
+        }
+        c->failed_step = -1;
+        c->failed_scen = -1;
+        c->cur ^= 1;
+        return THERMO_OK;
     } catch (...) {
         return fail(c, THERMO_ENOMEM, "host allocation failed");
     }

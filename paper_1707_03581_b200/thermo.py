@@ -20,7 +20,7 @@ _CODES = {-1: "EINVAL", -2: "ENOMEM", -3: "ECUDA", -4: "ENOCONV", -5: "EGEOM"}
 # symbols declared in include/thermo.h
 EXPORTS = ["thermo_create_mesh", "thermo_set_bc", "thermo_step", "thermo_get_T", "thermo_set_T",
            "thermo_set_solver", "thermo_get_stats", "thermo_get_step_iters", "thermo_last_error",
-           "thermo_destroy", "thermo_set_timing", "thermo_set_method"]
+           "thermo_destroy", "thermo_set_timing", "thermo_set_method", "thermo_stationary"]
 
 
 class ThermoError(RuntimeError):
@@ -82,6 +82,7 @@ def load(path: str = LIB_PATH):
     L.thermo_destroy.argtypes = [vp]
     L.thermo_set_timing.argtypes = [vp, i32]
     L.thermo_set_method.argtypes = [vp, i32, i32, i32, i32]
+    L.thermo_stationary.argtypes = [vp, ctypes.c_double, i32]
     _lib = L
     return L
 
@@ -157,6 +158,10 @@ class Thermo:
         """'ie' (implicit Euler, default) or 'mrsdc' (MRSDC(M, P) with K sweeps)."""
         code = {"ie": 0, "mrsdc": 1}[method]
         self._check(load().thermo_set_method(self.h, code, M, P, K))
+
+    def stationary(self, t: float = 0.0, with_interface: bool = False):
+        """Replace T by the stationary state at rest; see thermo_stationary."""
+        self._check(load().thermo_stationary(self.h, float(t), 1 if with_interface else 0))
 
     def set_solver(self, rtol=1e-12, maxit=0):
         self._check(load().thermo_set_solver(self.h, rtol, maxit))

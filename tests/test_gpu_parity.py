@@ -204,3 +204,18 @@ def test_cfg2_full_run_invariants():
     rows = np.concatenate([rng.integers(0, o.n, 2000), np.arange(o.n - 50, o.n)])
     res, bnorm = o.residual_rows(cfg.dt, (sv, 0.0, 0.0), eta, Tprev, Tlast, rows)
     assert np.abs(res).max() <= 1e-10 * bnorm
+
+
+@pytest.mark.parametrize("stock_cells", [(5, 3, 4), (5, 3, 3)])
+def test_one_row_tail_slice(stock_cells):
+    """N = 225 leaves a last slice with a single row (31 padding lanes) -- the regression case
+    of the window kernel's own-row index; N = 201 leaves 9 rows.  Parity vs dense Cholesky."""
+    from paper_1707_03581_b200.thermo import Thermo
+    f, m = I.two_slab_pair(stock_cells=stock_cells, jitter=0.1)
+    robin = [I.Robin(0, I.TAG_FLOOR, 50.0, 24.0), I.Robin(1, I.TAG_COOL, 200.0, 18.0)]
+    sc = I.Scenario(0.0, 0.0, 1.0, 500.0)
+    th = Thermo(f, m, 50.0, 3.6e6, 1000.0, [sc], 24.0, (4, 4), robin)
+    th.step(0.0, 5.0, 8)
+    o = O.Oracle(f, m, 50.0, 3.6e6, 1000.0, robin=robin)
+    Tr, _ = o.step(np.full(o.n, 24.0), 0.0, 5.0, 8, sc, solver="cholesky")
+    assert rel(th.get_T(), Tr) <= TOL

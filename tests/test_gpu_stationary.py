@@ -1,0 +1,103 @@
+"""GPU parity of the stationary solve (thermo_stationary; readings R19, R28)
+against the oracle, through the C ABI, plus closed-form and error-path checks."""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_1707_03581_b200 import inputs as I
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-9
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    import __graft_entry__ as g
+    g.build()
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+
+
+def _thermo(cfg, **kw):
+    from paper_1707_03581_b200.thermo import Thermo
+    return Thermo.from_config(cfg, **kw)
+
+
+def rel(a, b):
+    return float(np.abs(a - b).max() / np.abs(b).max())
+
+
+@pytest.mark.parametrize("coupled", [False, True])
+def test_cfg0_vs_dense_cholesky(coupled):
+    cfg = I.make_config("cfg0")
+    th = _thermo(cfg)
+    th.stationary(5.0, coupled)
+    o = O.Oracle.from_config(cfg)
+    Tr, _ = o.stationary(np.full(o.n, cfg.T0), 5.0, cfg.scenarios[0], coupled, solver="cholesky")
+    assert rel(th.get_T(), Tr) <= TOL
+    s = th.stats()
+    assert s["last_relres"] <= 1e-12 and s["max_iters"] > 10
+    if coupled:
+        assert abs(s["iface_area"] - 0.05) < 1e-14
+
+
+@pytest.mark.parametrize("name,jitter,coupled", [("small", 0.1, False), ("small", 0.1, True),
+                                                  ("medium", 0.1, True)])
+def test_vs_oracle_cg(name, jitter, coupled):
+    """Several slices, ragged tail, jittered meshes, non-uniform start (x0)."""
+    cfg = I.make_config(name, jitter=jitter)
+    T0 = I.initial_field(cfg)[0]
+    th = _thermo(cfg)
+    th.set_T(T0)
+    th.stationary(11.0, coupled)
+    o = O.Oracle.from_config(cfg)
+    Tr, st = o.stationary(T0, 11.0, cfg.scenarios[0], coupled)
+    assert rel(th.get_T(), Tr) <= TOL
+
+
+def test_two_slab_closed_form_on_gpu():
+    """Coupled two-slab steady state = the analytic piecewise-linear profile (pin shared with
+    the oracle tests), computed by the CUDA path directly."""
+    from test_oracle_stepping import two_slab_closed_form
+    from paper_1707_03581_b200.thermo import Thermo
+    f, m = I.two_slab_pair(jitter=0.1)
+    robin = [I.Robin(0, I.TAG_FLOOR, 50.0, 24.0), I.Robin(1, I.TAG_COOL, 200.0, 18.0)]
+    th = Thermo(f, m, 50.0, 3.6e6, 1000.0, [I.Scenario(0.0, 0.0, 1.0, 500.0)], 24.0, (4, 4), robin)
+    th.stationary(0.0, True)
+    Tbot, T1, T2, Ttop = two_slab_closed_form(0.1, 0.1, 50.0, 1000.0, 500.0, 50.0, 24.0, 200.0, 18.0)
+    z = np.concatenate([f.xyz[:, 2], m.xyz[:, 2]])
+    n = th.n
+    expect = np.where(np.arange(n) < th.nf, Tbot + (T1 - Tbot) * z / 0.1, T2 + (Ttop - T2) * (z - 0.1) / 0.1)
+    assert np.abs(th.get_T() - expect).max() < 1e-9
+    th.stationary(0.0, False)   # uncoupled: each slab at its Robin temperature
+    assert np.abs(th.get_T() - np.where(np.arange(n) < th.nf, 24.0, 18.0)).max() < 1e-9
+
+
+def test_then_time_steps_match_oracle():
+    """Stationary start, then implicit-Euler steps (the operator is rebuilt for dt)."""
+    cfg = I.make_config("small", jitter=0.1)
+    th = _thermo(cfg)
+    th.stationary(0.0, False)
+    th.step(0.0, cfg.dt, 10)
+    o = O.Oracle.from_config(cfg)
+    Ts, _ = o.stationary(np.full(o.n, cfg.T0), 0.0, cfg.scenarios[0], False)
+    Tr, _ = o.step(Ts, 0.0, cfg.dt, 10, cfg.scenarios[0])
+    assert rel(th.get_T(), Tr) <= TOL
+
+
+def test_errors():
+    from paper_1707_03581_b200.thermo import ThermoError
+    cfg = I.make_config("small")
+    th = _thermo(cfg)
+    T0 = th.get_T()
+    th.set_solver(1e-12, 5)                      # far too few iterations: ENOCONV, state kept
+    with pytest.raises(ThermoError, match="ENOCONV"):
+        th.stationary(0.0, True)
+    assert np.array_equal(th.get_T(), T0)
+    th.set_solver(1e-12, 0)
+    th.stationary(0.0, True)
+    cfgb = I.make_config("cfg4", n_scen=2)
+    tb = _thermo(cfgb)
+    with pytest.raises(ThermoError, match="EINVAL"):
+        tb.stationary(0.0)
