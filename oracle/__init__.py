@@ -57,6 +57,7 @@ def lib():
         L.or_ie_residual_rows.argtypes = [_p, _d, _d, _d, _d, _d, _p, _p, _i64, _p, _p, _p]
         L.or_apply_system.argtypes = [_p, _d, _p, _p]
         L.or_stationary.argtypes = [_p, _d, _i32, _d, _d, _d, _d, _d, _d, _d, _d, _d, _p, _i32, _d, _i32, _p]
+        L.or_step_sdc.argtypes = [_p, _d, _d, _i32, _i32, _i32, _d, _d, _d, _d, _d, _d, _d, _d, _d, _p, _d, _p]
         L.or_mrsdc_weights.argtypes = [ctypes.c_int, ctypes.c_int, _d, _d, _p, _p, _p, _p, _p, _p]
         L.or_step_mrsdc.argtypes = [_p, _d, _d, _i32, _i32, _i32, _i32, _d, _d, _d, _d, _d, _d, _d, _d, _d, _p,
                                     _d, _p]
@@ -211,6 +212,21 @@ def _stationary(self, T, t, scen, with_interface=False, solver="cg", rtol=1e-12,
 
 
 Oracle.stationary = _stationary
+
+
+def _step_sdc(self, T, t, dt, nsteps, scen, M=3, K=1, rtol=1e-12):
+    """Single-rate SDC(M) with K sweeps, interface implicit (reading R29).
+    Returns (T_new, stats[nsteps, 3] = solves, CG iterations, SDC residual)."""
+    T = np.array(T, dtype=np.float64, copy=True)
+    stats = np.zeros((nsteps, 3))
+    rc = lib().or_step_sdc(self.h, t, dt, nsteps, M, K, scen.s0, scen.amp, scen.period, scen.dir[0], scen.dir[1],
+                           scen.dir[2], scen.eta0, scen.eta_amp, scen.eta_period, _ptr(T), rtol, _ptr(stats))
+    if rc:
+        raise RuntimeError(f"oracle sdc failed rc={rc}: " + lib().or_last_error().decode())
+    return T, stats
+
+
+Oracle.step_sdc = _step_sdc
 
 
 def run_config(cfg, scen_index: int = 0, T_init: Optional[np.ndarray] = None, nsteps: Optional[int] = None,

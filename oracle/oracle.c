@@ -1051,3 +1051,115 @@ int or_step_mrsdc(or_sys *s, double t, double dt, int32_t nsteps, int32_t M, int
     free(buf);
     return rc;
 }
+
+/* ==================================================================================== */
+/* Single-rate SDC as used in the work-precision comparison: the */
+/* interface operator is part of the implicit term, so its Jacobian is reassembled at    */
+/* every node of every sweep (reading R29: the whole K_G(t), not only M_B,fix; b(t) =     */
+/* b_env + b_G(t) is the source g).  F(T, t) = K(t) T + b(t), K = A + B_env + K_G(t).     */
+/* Predictor: implicit Euler through the nodes,                                          */
+/*   M T^0_m = M T^0_{m-1} + dtau (K(tau_m) T^0_m + b(tau_m))                             */
+/* Sweep (P:389-395 with every term implicit, f^E = 0):                                  */
+/*   M T^{k+1}_m = M T^{k+1}_{m-1} + dtau K(tau_m) (T^{k+1}_m - T^k_m) + I_{m-1}^m,       */
+/*   I_{m-1}^m = sum_j s_{m,j} F(T^k_j, tau_j)                                            */
+/* with equidistant no-left nodes (dtau = dt / M) and the weights s of Table 1.          */
+/* stats (may be NULL): per step {solves, CG iterations, SDC residual r^K}.  */
+/* ==================================================================================== */
+
+/* y = K(t) x + b(t) with the interface assembled at time t */
+static int apply_full(or_sys *s, double t, double s0, double amp, double period, const double *dir, double eta0,
+                      double eta_amp, double eta_period, const double *x, double *y) {
+    double sp = s0 + amp * sin(2.0 * M_PI * t / period);
+    double etap = eta0 * (1.0 + eta_amp * sin(2.0 * M_PI * t / eta_period));
+    if (or_assemble_interface(s, sp * dir[0], sp * dir[1], sp * dir[2], etap)) return -5;
+    for (int64_t i = 0; i < s->n; i++) {
+        double acc = 0.0;
+        for (int64_t k = s->rowptr[i]; k < s->rowptr[i + 1]; k++) acc += (s->A[k] + s->B[k]) * x[s->col[k]];
+        for (int64_t k = s->irowptr[i]; k < s->irowptr[i + 1]; k++) acc += s->ival[k] * x[s->icol[k]];
+        y[i] = acc + s->benv[i] + s->bG[i];
+    }
+    return 0;
+}
+
+int or_step_sdc(or_sys *s, double t, double dt, int32_t nsteps, int32_t M, int32_t K,
+                double s0, double amp, double period, double dx, double dy, double dz,
+                double eta0, double eta_amp, double eta_period, double *T, double rtol, double *stats) {
+    const int64_t n = s->n;
+    const double dir[3] = {dx, dy, dz};
+    if (M < 1 || M > 16 || K < 0) { set_err("SDC: 1 <= M <= 16, K >= 0"); return -1; }
+    double tau[16], taue[16], sw[256], shat[16], stil[256], semb[16];
+    double *buf = malloc(sizeof(double) * (size_t)n * (size_t)(2 * (M + 1) + M + 3));
+    if (!buf) return -2;
+    double *Ts = buf, *Tsn = Ts + n * (M + 1), *F = Tsn + n * (M + 1), *rhs = F + n * M, *x = rhs + n;
+    double *q = x + n;
+    int rc = 0;
+    for (int32_t step = 0; step < nsteps && !rc; step++) {
+        const double tn = t + (double)step * dt, dtau = dt / M;
+        or_mrsdc_weights(M, 1, tn, dt, tau, taue, sw, shat, stil, semb);
+        double solves = 0, cgits = 0, relres, truerel;
+        /* predictor: implicit Euler from node to node (interface at tau_m) */
+        memcpy(Ts, T, sizeof(double) * (size_t)n);
+        for (int m = 1; m <= M && !rc; m++) {
+            double sp = s0 + amp * sin(2.0 * M_PI * tau[m - 1] / period);
+            double etap = eta0 * (1.0 + eta_amp * sin(2.0 * M_PI * tau[m - 1] / eta_period));
+            if (or_assemble_interface(s, sp * dx, sp * dy, sp * dz, etap)) { rc = -5; break; }
+            system_rhs(s, dtau, Ts + n * (m - 1), rhs);
+            memcpy(x, Ts + n * (m - 1), sizeof(double) * (size_t)n);
+            int64_t it = pcg(s, dtau, rhs, x, rtol, 10 * n, &relres, &truerel);
+            if (it < 0) { rc = -4; break; }
+            solves += 1; cgits += (double)it;
+            memcpy(Ts + n * m, x, sizeof(double) * (size_t)n);
+        }
+        /* K sweeps */
+        double res = 0.0;
+        for (int k = 0; k < K && !rc; k++) {
+            for (int j = 1; j <= M && !rc; j++)                                  /* F(T^k_j, tau_j) */
+                if (apply_full(s, tau[j - 1], s0, amp, period, dir, eta0, eta_amp, eta_period, Ts + n * j,
+                               F + n * (j - 1))) rc = -5;
+            if (rc) break;
+            memcpy(Tsn, T, sizeof(double) * (size_t)n);
+            for (int m = 1; m <= M && !rc; m++) {
+                /* K(tau_m) T^k_m (interface at tau_m, kept assembled for the solve) */
+                if (apply_full(s, tau[m - 1], s0, amp, period, dir, eta0, eta_amp, eta_period, Ts + n * m, q)) {
+                    rc = -5; break;
+                }
+                for (int64_t i = 0; i < n; i++) {
+                    double I = 0.0;
+                    for (int j = 0; j < M; j++) I += sw[(m - 1) * M + j] * F[n * j + i];
+                    double KT = q[i] - s->benv[i] - s->bG[i];
+                    rhs[i] = s->ML[i] * Tsn[n * (m - 1) + i] - dtau * KT + I;
+                }
+                memcpy(x, Ts + n * m, sizeof(double) * (size_t)n);          /* x0 = T^k_m */
+                int64_t it = pcg(s, dtau, rhs, x, rtol, 10 * n, &relres, &truerel);
+                if (it < 0) { rc = -4; break; }
+                solves += 1; cgits += (double)it;
+                memcpy(Tsn + n * m, x, sizeof(double) * (size_t)n);
+            }
+            if (rc) break;
+            memcpy(Ts, Tsn, sizeof(double) * (size_t)n * (size_t)(M + 1));
+            if (k == K - 1) {   /* SDC residual of the new iterate */
+                for (int j = 1; j <= M && !rc; j++)
+                    if (apply_full(s, tau[j - 1], s0, amp, period, dir, eta0, eta_amp, eta_period, Ts + n * j,
+                                   F + n * (j - 1))) rc = -5;
+                res = 0.0;
+                for (int64_t i = 0; i < n && !rc; i++) {
+                    double cum = 0.0;
+                    for (int m = 1; m <= M; m++) {
+                        for (int j = 0; j < M; j++) cum += sw[(m - 1) * M + j] * F[n * j + i];
+                        double v = fabs(s->ML[i] * (Ts[n * m + i] - T[i]) - cum);
+                        if (v > res) res = v;
+                    }
+                }
+            }
+        }
+        if (rc) break;
+        memcpy(T, Ts + n * M, sizeof(double) * (size_t)n);
+        if (stats) {
+            stats[3 * step + 0] = solves;
+            stats[3 * step + 1] = cgits;
+            stats[3 * step + 2] = res;
+        }
+    }
+    free(buf);
+    return rc;
+}

@@ -108,6 +108,14 @@ int or_step_mrsdc(or_sys *s, double t, double dt, int32_t nsteps, int32_t M, int
                   double s0, double amp, double period, double dx, double dy, double dz,
                   double eta0, double eta_amp, double eta_period, double *T, double rtol, double *stats);
 
+/* Single-rate SDC with M equidistant no-left nodes and K sweeps, every term
+ * implicit -- the interface operator reassembled at each node of each sweep (the "single-rate
+ * SDC" of the work-precision study P:730-736, reading R29).  M = 1, K = 0 is implicit Euler.
+ * stats (may be NULL): per step {solves, CG iterations, SDC residual}. */
+int or_step_sdc(or_sys *s, double t, double dt, int32_t nsteps, int32_t M, int32_t K,
+                double s0, double amp, double period, double dx, double dy, double dz,
+                double eta0, double eta_amp, double eta_period, double *T, double rtol, double *stats);
+
 #ifdef __cplusplus
 }
 #endif
