@@ -163,6 +163,7 @@ int cg_launch_solve(Ctx &c, const double *x0, double *x, const double *rhs, cons
 int mrsdc_setup(Ctx &c);
 int build_if_of_row(Ctx &c);
 int mrsdc_step(Ctx &c, double tn, double dt, int step_index);
+int sdc_step(Ctx &c, double tn, double dt, int step_index);   // single-rate SDC (method 2)
 
 // cg_batched.cu (S > 1 scenarios advanced together)
 int cgb_setup(Ctx &c);

@@ -113,6 +113,34 @@ __global__ void k_mr_emb(int64_t N, int64_t ldf, const double *ML, const double 
     Tout[i] = Tprev[i] + num / ML[i];
 }
 
+// right-hand side of a single-rate SDC solve (every term implicit, reading R29):
+//  predictor (KvTk == nullptr): rhs = M_L Tprev + a (b_env + b_G(tau_m))
+//  sweep:  rhs = M_L Tprev - a K(tau_m) T^k_m + sum_j s_mj F(T^k_j, tau_j)
+//          K(tau_m) T^k_m = KvTk + (FE_m - b_G(tau_m)) on the interface rows,
+//          F(T^k_j, tau_j) = FI_j + FE_j (FI_j = (A + B_env) T^k_j + b_env, FE_j = K_G T^k_j + b_G)
+__global__ void k_sdc_rhs(int64_t N, int64_t ldf, const double *ML, const double *Tprev, const double *benv,
+                          const double *KvTk, double a, const double *FI, const double *FE, int nif,
+                          const double *bGm, const int32_t *if_of_row, int M, int mcur, MrW w, double *rhs) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    const int k = nif ? if_of_row[i] : -1;
+    double r = ML[i] * Tprev[i];
+    if (!KvTk) {
+        r = fma(a, k >= 0 ? benv[i] + bGm[k] : benv[i], r);
+    } else {
+        double KT = KvTk[i];
+        if (k >= 0) KT += FE[(int64_t)(mcur - 1) * nif + k] - bGm[k];
+        double I = 0.0;
+        for (int j = 0; j < M; ++j) {
+            double Fj = FI[(int64_t)j * ldf + i];
+            if (k >= 0) Fj += FE[(int64_t)j * nif + k];
+            I = fma(w.a[j], Fj, I);
+        }
+        r = fma(-a, KT, r) + I;
+    }
+    rhs[i] = r;
+}
+
 __global__ void k_if_of_row(const int32_t *if_rows, int n_if, int32_t *map) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k < n_if) map[if_rows[k]] = k;
@@ -402,6 +430,124 @@ int mrsdc_step(Ctx &c, double tn, double dt, int step_index) {
         }
     }
     // ---- commit T(t_{n+1}) = T_M
+    CK(cudaMemcpyAsync(c.d_T[c.cur ^ 1], q.TSo[M], sizeof(double) * N, cudaMemcpyDeviceToDevice, st));
+    c.mr_solves = solve_no;
+    (void)step_index;
+    return 0;
+}
+
+// One single-rate SDC step (method 2; P:354-413 with every term implicit, reading R29):
+// predictor = implicit Euler through the M nodes, then K sweeps; before every solve the
+// interface Jacobian is reassembled at that node (the overhead the paper attributes to
+// single-rate SDC).  Uses the MRSDC storage with P = 1 (slots = node times).
+int sdc_step(Ctx &c, double tn, double dt, int step_index) {
+    const int M = c.mr_M, K = c.mr_K;
+    const int64_t N = c.N;
+    const int nif = c.n_if, nifs = std::max(nif, 1);
+    const double a = dt / M;
+    const int64_t ldf = (N + 31) & ~(int64_t)31;
+    cudaStream_t st = c.stream;
+    if (c.built_dt != a) {
+        if (build_operator(c, a)) return -3;
+    }
+    MrTables W;
+    mr_tables(M, 1, tn, dt, W);
+    const int nslot = M + 1;   // slot m = node tau_m (slot 0 = t_n, unused)
+    std::vector<double> sc(4 * (size_t)2 * nslot);
+    const Scen &sn = c.scen[0];
+    for (int q = 0; q < nslot; ++q) {
+        const double tq = tn + dt * (double)q / (double)M;
+        const double sv = sn.s0 + sn.amp * std::sin(2.0 * M_PI * tq / sn.period);
+        sc[4 * q + 0] = sv * sn.d2[0];
+        sc[4 * q + 1] = sv * sn.d2[1];
+        sc[4 * q + 2] = sn.eta0 * (1.0 + sn.eta_amp * std::sin(2.0 * M_PI * tq / sn.eta_period));
+        sc[4 * q + 3] = sv;
+    }
+    if ((int64_t)nslot > c.step_cap) {
+        for (void *p : {(void *)c.d_step_sc, (void *)c.d_iters, (void *)c.d_relres, (void *)c.d_area})
+            if (p) cudaFree(p);
+        c.step_cap = nslot;
+        CK(cudaMalloc(&c.d_step_sc, sizeof(double) * 4 * (size_t)nslot));
+        CK(cudaMalloc(&c.d_iters, sizeof(int32_t) * (size_t)nslot));
+        CK(cudaMalloc(&c.d_relres, sizeof(double) * (size_t)nslot));
+        CK(cudaMalloc(&c.d_area, sizeof(double) * (size_t)nslot));
+    }
+    CK(cudaMemcpyAsync(c.d_step_sc, sc.data(), sizeof(double) * 4 * nslot, cudaMemcpyHostToDevice, st));
+    const size_t ell_stride = (size_t)c.cap * nifs;
+    // unscaled K_G, b_G at the node times (for F(T^k_j, tau_j) in the quadrature)
+    if (nif) {
+        for (int q = 1; q < nslot; ++q) {
+            IfaceParams Pf;
+            memset(&Pf, 0, sizeof Pf);
+            iface_params(c, Pf, c.d_step_sc + 4 * q, -1.0);
+            Pf.ell_cnt = c.d_ell_cnt_s + (size_t)q * nif;
+            Pf.ell_col = c.d_ell_col_s + (size_t)q * ell_stride;
+            Pf.ell_val = c.d_ell_val_s + (size_t)q * ell_stride;
+            Pf.if_b = c.d_if_b_s + (size_t)q * nif;
+            Pf.if_phi = c.d_if_phi_s + (size_t)q * nif;
+            Pf.no_dinv = 1;
+            if (iface_launch(c, Pf)) return -3;
+        }
+    }
+    // implicit Jacobian M_L - a K(tau_m): interface rows reassembled into the solve arrays
+    auto reassemble = [&](int m) -> int {
+        if (!nif) return 0;
+        IfaceParams Pf;
+        memset(&Pf, 0, sizeof Pf);
+        iface_params(c, Pf, c.d_step_sc + 4 * m, a);
+        return iface_launch(c, Pf);
+    };
+    double *T0 = c.d_T[c.cur];
+    MrPtr q = mr_pointers(c, T0);
+    const double *bG_of = c.d_if_b_s;   // slot m: c.d_if_b_s + m * nif
+    auto fe_apply = [&](int slot, const double *x, double *y) -> int {
+        if (!nif) return 0;
+        k_fe_apply<<<nbk(nif), 256, 0, st>>>(nif, c.d_ell_cnt_s + (size_t)slot * nif,
+                                             c.d_ell_col_s + (size_t)slot * ell_stride,
+                                             c.d_ell_val_s + (size_t)slot * ell_stride, c.d_if_b_s + (size_t)slot * nif,
+                                             x, y);
+        CK(cudaGetLastError());
+        return 0;
+    };
+    auto vol_apply = [&](const double *x, const double *addv, double sgn, double *y) -> int {
+        k_vol_apply<<<nbk(N), 256, 0, st>>>(c.d_slice_ptr, c.d_col, c.d_KV, N, x, addv, sgn, y);
+        CK(cudaGetLastError());
+        return 0;
+    };
+    int solve_no = 0;
+    auto solve = [&](const double *x0, double *x, const double *rhs) -> int {
+        const int slot = solve_no++;
+        return cg_launch_solve(c, x0, x, rhs, c.d_Dinv, nif > 0, c.d_mr_iters, c.d_mr_relres, slot);
+    };
+    MrW w0;
+    memset(&w0, 0, sizeof w0);
+    // ---- predictor: implicit Euler from node to node
+    for (int m = 1; m <= M; ++m) {
+        if (reassemble(m)) return -3;
+        k_sdc_rhs<<<nbk(N), 256, 0, st>>>(N, ldf, c.d_ML, q.TSo[m - 1], c.d_benv, nullptr, a, nullptr, nullptr, nif,
+                                          bG_of + (size_t)m * nifs, c.d_if_of_row, M, m, w0, q.rhs);
+        CK(cudaGetLastError());
+        if (solve(q.TSo[m - 1], q.TSo[m], q.rhs)) return -3;
+    }
+    // ---- K sweeps
+    for (int k = 0; k < K; ++k) {
+        for (int j = 1; j <= M; ++j) {
+            if (vol_apply(q.TSo[j], c.d_benv, 1.0, q.FI + (size_t)(j - 1) * ldf)) return -3;   // (A + B) T + b_env
+            if (fe_apply(j, q.TSo[j], q.FE + (size_t)(j - 1) * nifs)) return -3;              // K_G T + b_G
+        }
+        for (int m = 1; m <= M; ++m) {
+            MrW wr;
+            memset(&wr, 0, sizeof wr);
+            for (int j = 0; j < M; ++j) wr.a[j] = W.s[m - 1][j];
+            if (vol_apply(q.TSo[m], nullptr, 0.0, q.KvTk)) return -3;   // (A + B_env) T^k_m
+            if (reassemble(m)) return -3;
+            k_sdc_rhs<<<nbk(N), 256, 0, st>>>(N, ldf, c.d_ML, q.TSn[m - 1], c.d_benv, q.KvTk, a, q.FI, q.FE, nif,
+                                              bG_of + (size_t)m * nifs, c.d_if_of_row, M, m, wr, q.rhs);
+            CK(cudaGetLastError());
+            if (solve(q.TSo[m], q.TSn[m], q.rhs)) return -3;
+        }
+        for (int m = 1; m <= M; ++m) std::swap(q.TSo[m], q.TSn[m]);
+    }
     CK(cudaMemcpyAsync(c.d_T[c.cur ^ 1], q.TSo[M], sizeof(double) * N, cudaMemcpyDeviceToDevice, st));
     c.mr_solves = solve_no;
     (void)step_index;

@@ -313,10 +313,12 @@ extern "C" int thermo_set_method(void *ctx, int32_t method, int32_t M, int32_t P
         c->method = 0;
         return THERMO_OK;
     }
-    if (method != 1) return fail(c, THERMO_EINVAL, "method must be 0 (implicit Euler) or 1 (MRSDC)");
-    if (M < 1 || M > 8 || P < 1 || P > 8 || K < 0) return fail(c, THERMO_EINVAL, "MRSDC needs 1 <= M, P <= 8, K >= 0");
-    if (c->S != 1) return fail(c, THERMO_EINVAL, "MRSDC runs a single scenario");
-    c->method = 1;
+    if (method != 1 && method != 2)
+        return fail(c, THERMO_EINVAL, "method must be 0 (implicit Euler), 1 (MRSDC) or 2 (single-rate SDC)");
+    if (method == 2) P = 1;
+    if (M < 1 || M > 8 || P < 1 || P > 8 || K < 0) return fail(c, THERMO_EINVAL, "SDC needs 1 <= M, P <= 8, K >= 0");
+    if (c->S != 1) return fail(c, THERMO_EINVAL, "SDC methods run a single scenario");
+    c->method = method;
     c->mr_M = M;
     c->mr_P = P;
     c->mr_K = K;
@@ -370,14 +372,16 @@ extern "C" int thermo_step(void *ctx, double t, double dt, int32_t nsteps) {
         }
         API_CK(cudaMemcpyAsync(c->d_step_sc, sc.data(), sizeof(double) * sc.size(), cudaMemcpyHostToDevice, c->stream));
         API_CK(cudaMemsetAsync(c->d_status, 0, sizeof(int) * 8, c->stream));
-        if (c->method == 1) {   // MRSDC: one step at a time, status checked per step
+        if (c->method >= 1) {   // MRSDC / single-rate SDC: one step at a time, status checked per step
             c->h_iters.assign((size_t)nsteps, 0);
             c->h_relres.assign((size_t)nsteps, 0.0);
             c->h_area.assign(nsteps, 0.0);
             c->ms_iface = c->ms_solve = 0.0;
             for (int n = 0; n < nsteps; ++n) {
                 API_CK(cudaMemsetAsync(c->d_status, 0, sizeof(int) * 8, c->stream));
-                if (thermo::mrsdc_step(*c, t + (double)n * dt, dt, n)) return THERMO_ECUDA;
+                if ((c->method == 1 ? thermo::mrsdc_step(*c, t + (double)n * dt, dt, n)
+                                    : thermo::sdc_step(*c, t + (double)n * dt, dt, n)))
+                    return THERMO_ECUDA;
                 int status[8];
                 std::vector<int32_t> it(c->mr_solves);
                 std::vector<double> rr(c->mr_solves);
@@ -396,7 +400,8 @@ extern "C" int thermo_step(void *ctx, double t, double dt, int32_t nsteps) {
                     c->failed_relres = c->h_relres[n];
                     c->last_nsteps = n;
                     return fail(c, status[1] ? THERMO_EGEOM : THERMO_ENOCONV,
-                                "MRSDC step " + std::to_string(n) + " failed (implicit solve or interface)");
+                                (c->method == 1 ? "MRSDC step " : "SDC step ") + std::to_string(n) +
+                                    " failed (implicit solve or interface)");
                 }
                 c->cur ^= 1;
                 c->steps_done += 1;

@@ -155,8 +155,9 @@ class Thermo:
         self._check(load().thermo_set_timing(self.h, 1 if enable else 0))
 
     def set_method(self, method: str = "ie", M: int = 3, P: int = 2, K: int = 1):
-        """'ie' (implicit Euler, default) or 'mrsdc' (MRSDC(M, P) with K sweeps)."""
-        code = {"ie": 0, "mrsdc": 1}[method]
+        """'ie' (implicit Euler, default), 'mrsdc' (MRSDC(M, P) with K sweeps) or
+        'sdc' (single-rate SDC(M) with K sweeps, interface implicit)."""
+        code = {"ie": 0, "mrsdc": 1, "sdc": 2}[method]
         self._check(load().thermo_set_method(self.h, code, M, P, K))
 
     def stationary(self, t: float = 0.0, with_interface: bool = False):

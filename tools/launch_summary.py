@@ -21,6 +21,14 @@ def main(path, out=None):
     lines = [f"{'kernel':60s} {'launches':>8s} {'total_us':>12s} {'avg_us':>10s} {'share':>7s}"]
     for k in sorted(tot, key=lambda k: -tot[k]):
         lines.append(f"{k[:60]:60s} {cnt[k]:8d} {tot[k]:12.1f} {tot[k] / cnt[k]:10.1f} {tot[k] / T * 100:6.1f}%")
+    # the time-step kernels only (setup / assembly launches excluded): the step's split
+    step = {k: v for k, v in tot.items() if any(x in k for x in ("k_cg_step", "k_cgb_step", "k_pairs", "k_rows"))}
+    S = sum(step.values())
+    if S > 0:
+        lines.append("")
+        lines.append("time-step kernels only (interface pairs / rows + CG solve):")
+        for k in sorted(step, key=lambda k: -step[k]):
+            lines.append(f"{k[:60]:60s} {cnt[k]:8d} {step[k]:12.1f} {step[k] / cnt[k]:10.1f} {step[k] / S * 100:6.1f}%")
     txt = "\n".join(lines)
     print(txt)
     if out:

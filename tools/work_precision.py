@@ -1,6 +1,6 @@
-"""Work-precision of implicit Euler vs MRSDC(3,2) on the B200 (synthetic analogue of the
-paper's Fig. 7): time-discretisation error at t_end against the look-ahead factor
-eta = simulated time / device time.
+"""Work-precision of implicit Euler, single-rate SDC(3) and MRSDC(3,2) on the B200 (synthetic
+analogue of the paper's Fig. 7): time-discretisation error at t_end against the
+look-ahead factor eta = simulated time / device time.
 
     python tools/work_precision.py [config] [t_end]
 
@@ -31,7 +31,7 @@ def run(method, dt, M=3, P=2, K=1):
     if method == "ie":
         th.set_method("ie")
     else:
-        th.set_method("mrsdc", M, P, K)
+        th.set_method(method, M, P, K)
     n = int(round(t_end / dt))
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
@@ -53,6 +53,11 @@ for K in (0, 1, 2):
     for dt in dts:
         T, sec = run("mrsdc", dt, 3, 2, K)
         rows.append({"method": f"MRSDC(3,2) k={K}", "dt": dt, "err": float(np.abs(T - Tref).max() / scale),
+                     "seconds": sec, "lookahead": t_end / sec})
+for K in (0, 1, 2):
+    for dt in dts:
+        T, sec = run("sdc", dt, 3, 1, K)
+        rows.append({"method": f"SDC(3) k={K}", "dt": dt, "err": float(np.abs(T - Tref).max() / scale),
                      "seconds": sec, "lookahead": t_end / sec})
 print(f"# work-precision on {name} ({cfg.n_dof} DoF), t_end = {t_end} s, reference MRSDC(3,2) k=3 "
       f"dt = {dts[-1] / 16} s ({tref:.2f} s), error relative to max|T_ref - T0| = {scale:.4f} K")
