@@ -128,61 +128,6 @@ __device__ __forceinline__ void cgb_reduce(double (&v)[NV][2], double *sm, doubl
     __syncthreads();
 }
 
-// Row sum of the shared volume operator applied to the lane's two columns of
-// y = x1 + beta x2 (beta per column; kTwo = false: y = x1).  Entries of row r of slice s sit
-// at base + 32 k + r; lane k loads entry k, the warp broadcasts it.
-template <bool kTwo>
-__device__ __forceinline__ double2 row_spmm(const CGBParams &P, int64_t base, int w, int r, const double *x1,
-                                            const double *x2, double2 beta, int lane) {
-    double2 acc = make_double2(0.0, 0.0);
-    const int ln = 2 * lane < P.SP ? lane : 0;   // lanes past the row stride re-read column 0..1
-    for (int k0 = 0; k0 < w; k0 += 32) {
-        const int kk = k0 + lane;
-        int cl = 0;
-        double vl = 0.0;
-        if (kk < w) {
-            cl = P.col[base + 32 * (int64_t)kk + r];
-            vl = P.val[base + 32 * (int64_t)kk + r];
-        }
-        const int m = min(32, w - k0);
-        int k = 0;
-        for (; k + 8 <= m; k += 8) {
-            double2 y[8];
-            double v[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int c = __shfl_sync(0xffffffffu, cl, k + u);
-                v[u] = __shfl_sync(0xffffffffu, vl, k + u);
-                const double2 a = reinterpret_cast<const double2 *>(x1 + (int64_t)c * P.SP)[ln];
-                if (kTwo) {
-                    const double2 b = reinterpret_cast<const double2 *>(x2 + (int64_t)c * P.SP)[ln];
-                    y[u] = make_double2(fma(beta.x, b.x, a.x), fma(beta.y, b.y, a.y));
-                } else {
-                    y[u] = a;
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                acc.x = fma(v[u], y[u].x, acc.x);
-                acc.y = fma(v[u], y[u].y, acc.y);
-            }
-        }
-        for (; k < m; ++k) {
-            const int c = __shfl_sync(0xffffffffu, cl, k);
-            const double v = __shfl_sync(0xffffffffu, vl, k);
-            const double2 a = reinterpret_cast<const double2 *>(x1 + (int64_t)c * P.SP)[ln];
-            double2 y = a;
-            if (kTwo) {
-                const double2 b = reinterpret_cast<const double2 *>(x2 + (int64_t)c * P.SP)[ln];
-                y = make_double2(fma(beta.x, b.x, a.x), fma(beta.y, b.y, a.y));
-            }
-            acc.x = fma(v, y.x, acc.x);
-            acc.y = fma(v, y.y, acc.y);
-        }
-    }
-    return acc;
-}
-
 // Two rows (rA, rA + 1) of one slice at once: lanes 0-15 hold the entries of row A, lanes
 // 16-31 those of row B (16 per round); the warp broadcasts them and every lane gathers its two
 // columns for both rows, so 16 loads per lane are in flight.  The entries of a round are
@@ -198,19 +143,17 @@ __device__ __forceinline__ void load_cv(const CGBParams &P, int64_t base, int w,
     }
 }
 
-template <bool kTwo>
+// U entries per row and round: 4 with two gathered vectors, 8 with one (same register budget).
+template <bool kTwo, int U>
 __device__ __forceinline__ void gather_round(const CGBParams &P, int cl, double vl, int m, const double *x1,
                                              const double *x2, double2 beta, int ln, double2 &accA, double2 &accB) {
-    for (int k = 0; k < m; k += 4) {
-        double2 yA[4], yB[4];
-        double vA[4], vB[4];
+    for (int k = 0; k < m; k += U) {
+        double2 yA[U], yB[U];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < U; ++u) {   // all gathers of the round first
             const int ku = min(k + u, m - 1);
             const int cA = __shfl_sync(0xffffffffu, cl, ku);
             const int cB = __shfl_sync(0xffffffffu, cl, 16 + ku);
-            vA[u] = k + u < m ? __shfl_sync(0xffffffffu, vl, ku) : 0.0;
-            vB[u] = k + u < m ? __shfl_sync(0xffffffffu, vl, 16 + ku) : 0.0;
             const double2 a = reinterpret_cast<const double2 *>(x1 + (int64_t)cA * P.SP)[ln];
             const double2 b = reinterpret_cast<const double2 *>(x1 + (int64_t)cB * P.SP)[ln];
             if (kTwo) {
@@ -224,12 +167,14 @@ __device__ __forceinline__ void gather_round(const CGBParams &P, int cl, double 
             }
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < U; ++u) {   // then the values (broadcast) and the row sums
+            const int ku = min(k + u, m - 1);
+            const double vA = __shfl_sync(0xffffffffu, vl, ku), vB = __shfl_sync(0xffffffffu, vl, 16 + ku);
             if (k + u < m) {
-                accA.x = fma(vA[u], yA[u].x, accA.x);
-                accA.y = fma(vA[u], yA[u].y, accA.y);
-                accB.x = fma(vB[u], yB[u].x, accB.x);
-                accB.y = fma(vB[u], yB[u].y, accB.y);
+                accA.x = fma(vA, yA[u].x, accA.x);
+                accA.y = fma(vA, yA[u].y, accA.y);
+                accB.x = fma(vB, yB[u].x, accB.x);
+                accB.y = fma(vB, yB[u].y, accB.y);
             }
         }
     }
@@ -244,10 +189,11 @@ __device__ __forceinline__ void row_spmm2(const CGBParams &P, int64_t base, int 
     accA = make_double2(0.0, 0.0);
     accB = make_double2(0.0, 0.0);
     const int ln = 2 * lane < P.SP ? lane : 0;   // lanes past the row stride re-read columns 0..1
-    gather_round<kTwo>(P, cl, vl, min(16, w), x1, x2, beta, ln, accA, accB);
+    constexpr int U = kTwo ? 4 : 8;
+    gather_round<kTwo, U>(P, cl, vl, min(16, w), x1, x2, beta, ln, accA, accB);
     for (int k0 = 16; k0 < w; k0 += 16) {
         load_cv(P, base, w, rA, validB, k0, lane, cl, vl);
-        gather_round<kTwo>(P, cl, vl, min(16, w - k0), x1, x2, beta, ln, accA, accB);
+        gather_round<kTwo, U>(P, cl, vl, min(16, w - k0), x1, x2, beta, ln, accA, accB);
     }
 }
 
