@@ -1,7 +1,5 @@
 #!/bin/bash
 mkdir -p gpurun_out
-rm -f gpurun_out/probe_cfg4_v.log
-for pm in 1; do
-echo "== pmode $pm" >> gpurun_out/probe_cfg4_v.log
-THERMO_CGB_PMODE=$pm THERMO_CG_TRACE=1 timeout 300 python tools/probe.py cfg4 3 2>&1 | grep -E "trace|solve" >> gpurun_out/probe_cfg4_v.log
-done
+timeout 900 python -m pytest tests -m gpu -x -q -k "not slow" > gpurun_out/pytest_gpu.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 300 python tools/probe.py cfg4 3 > gpurun_out/probe_cfg4.log 2>&1 && \
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_cfg4.csv python tools/probe.py cfg4 3 > gpurun_out/ncu_launch4.log 2>&1
