@@ -261,7 +261,8 @@ def run_thermo(args):
                          else "working set fits L2 (no flush; small config)",
                    "parallelism": (f"scenarios sharded over {world} ranks" if sharded else
                                    "replicas only" if world > 1 else "single GPU"),
-                   "cg_iters_per_step": float(iters.mean())},
+                   "cg_iters_per_step": float(iters.mean()),
+                   "iface_overlapped_with_solve": bool(st["overlap"])},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": "k_cg_step (persistent Jacobi-PCG, one launch per step)",
                      "peak_kind": peak_kind, "achieved_vs_8TBs": achieved / 8000.0,
@@ -269,7 +270,7 @@ def run_thermo(args):
                      "iface_share_of_step": st["ms_iface"] / ms},
         "e2e": {"value": units * KE / (ms_e2e * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 32 * S,
                 "d2h_bytes_per_step": 8 * N * S},
-        "gpu_launches": K * (4 if st["n_iface_rows"] else 1),
+        "gpu_launches": K * st["launches_per_step"],
         "clocks": clk.summary(),
     }
     th.close()

@@ -127,7 +127,14 @@ struct Ctx {
     double *d_if_phi_s = nullptr;
     int mr_nslots = 0, mr_solves = 0;
     bool timing = false;
-    std::vector<cudaEvent_t> events;   // 2 * nsteps + 1 when timing
+    std::vector<cudaEvent_t> events;   // 2 * nsteps + 1 when timing (4 * nsteps overlapped)
+    // overlap of the interface assembly of step n + 1 (side stream, twin output buffer) with
+    // the solve of step n (S == 1, implicit Euler; THERMO_OVERLAP=0 disables)
+    int overlap = 0;
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_if[2] = {nullptr, nullptr}, ev_cg[2] = {nullptr, nullptr}, ev_join = nullptr;
+    int32_t *d_ell_cnt1 = nullptr, *d_ell_col1 = nullptr;
+    double *d_ell_val1 = nullptr, *d_if_b1 = nullptr, *d_if_phi1 = nullptr, *d_if_dinv1 = nullptr;
     double ms_iface = 0.0, ms_solve = 0.0;
 
     // stats of the last thermo_step
@@ -149,11 +156,13 @@ int build_operator(Ctx &c, double dt, double mu = 1.0);   // K~ = mu M_L - dt (A
 int iface_setup(Ctx &c, const double *h_xyz, const std::vector<int32_t> &facesA,
                 const std::vector<int32_t> &facesB);
 void iface_params(Ctx &c, IfaceParams &p, const double *step_sc, double dt);
-int iface_launch(Ctx &c, const IfaceParams &p);
+int iface_launch(Ctx &c, const IfaceParams &p, cudaStream_t stream = nullptr);
+void iface_params_buf(Ctx &c, IfaceParams &p, int buf);   // overlapped step: output buffer 0 / 1
+int scatter_dinv(Ctx &c, int buf);                          // if_dinv of buffer -> Dinv rows (main stream)
 
 // cg.cu
 int cg_setup(Ctx &c);
-int cg_launch_step(Ctx &c, int step, double dt);
+int cg_launch_step(Ctx &c, int step, double dt, int buf = 0);
 // Solve (M_L - a K_vol [- a K_G]) x = rhs from x0 with the operator currently in d_val (a =
 // built_dt); iface = false: no interface rows.  Iterations / residual to iters_out[slot].
 int cg_launch_solve(Ctx &c, const double *x0, double *x, const double *rhs, const double *Dinv, bool iface,
