@@ -135,6 +135,8 @@ struct Ctx {
     cudaEvent_t ev_if[2] = {nullptr, nullptr}, ev_cg[2] = {nullptr, nullptr}, ev_join = nullptr;
     int32_t *d_ell_cnt1 = nullptr, *d_ell_col1 = nullptr;
     double *d_ell_val1 = nullptr, *d_if_b1 = nullptr, *d_if_phi1 = nullptr, *d_if_dinv1 = nullptr;
+    PairRec *d_pairs_s = nullptr;        // pair records of the SDC node-time slots
+    int32_t *d_pcnt_s = nullptr;
     double ms_iface = 0.0, ms_solve = 0.0;
 
     // stats of the last thermo_step

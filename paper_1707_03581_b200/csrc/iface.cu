@@ -871,11 +871,12 @@ int iface_launch(Ctx &c, const IfaceParams &P, cudaStream_t stream) {
     const int tpb = PAIR_WPB * PAIR_TPW;
     const size_t qsm = sizeof(int) * (size_t)PAIR_WPB * PAIR_TPW * c.pcap;
     cudaStream_t st = stream ? stream : c.stream;
-    k_pairs<<<dim3((unsigned)((c.nTA + tpb - 1) / tpb), (unsigned)c.S), 32 * PAIR_WPB, qsm, st>>>(P, 0);
+    // blockIdx.y = scenario (batched mode) or node time (the slots of the SDC methods): P.S of them
+    k_pairs<<<dim3((unsigned)((c.nTA + tpb - 1) / tpb), (unsigned)P.S), 32 * PAIR_WPB, qsm, st>>>(P, 0);
     CK(cudaGetLastError());
-    k_pairs<<<dim3((unsigned)((c.nTB + tpb - 1) / tpb), (unsigned)c.S), 32 * PAIR_WPB, qsm, st>>>(P, 1);
+    k_pairs<<<dim3((unsigned)((c.nTB + tpb - 1) / tpb), (unsigned)P.S), 32 * PAIR_WPB, qsm, st>>>(P, 1);
     CK(cudaGetLastError());
-    k_rows<<<dim3((unsigned)((c.n_if + ROW_WPB - 1) / ROW_WPB), (unsigned)c.S), 32 * ROW_WPB, 0, st>>>(P);
+    k_rows<<<dim3((unsigned)((c.n_if + ROW_WPB - 1) / ROW_WPB), (unsigned)P.S), 32 * ROW_WPB, 0, st>>>(P);
     CK(cudaGetLastError());
     return 0;
 }

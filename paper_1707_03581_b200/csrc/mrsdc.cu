@@ -53,14 +53,18 @@ __global__ void k_vol_apply(const int64_t *slice_ptr, const int32_t *col, const 
     y[i] = acc;
 }
 
-// compact f^E on the interface rows: y[k] = b_G[k] + sum_c K_G[k][c] x[col]
-__global__ void k_fe_apply(int n_if, const int32_t *cnt, const int32_t *ecol, const double *evals, const double *bG,
-                           const double *x, double *y) {
+// compact f^E on the interface rows of node-time slot s (slot arrays laid out like the batched
+// scenarios, [k][c][slot] with ns slots): y[k] = b_G[k] + sum_c K_G[k][c] x[col]
+__global__ void k_fe_apply(int n_if, int ns, int s, int cap, const int32_t *cnt, const int32_t *ecol,
+                           const double *evals, const double *bG, const double *x, double *y) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n_if) return;
-    double acc = bG[k];
-    const int m = cnt[k];
-    for (int c = 0; c < m; ++c) acc = fma(evals[(int64_t)c * n_if + k], x[ecol[(int64_t)c * n_if + k]], acc);
+    double acc = bG[(int64_t)k * ns + s];
+    const int m = cnt[(int64_t)k * ns + s];
+    for (int c = 0; c < m; ++c) {
+        const int64_t e = ((int64_t)k * cap + c) * ns + s;
+        acc = fma(evals[e], x[ecol[e]], acc);
+    }
     y[k] = acc;
 }
 
@@ -120,16 +124,17 @@ __global__ void k_mr_emb(int64_t N, int64_t ldf, const double *ML, const double 
 //          F(T^k_j, tau_j) = FI_j + FE_j (FI_j = (A + B_env) T^k_j + b_env, FE_j = K_G T^k_j + b_G)
 __global__ void k_sdc_rhs(int64_t N, int64_t ldf, const double *ML, const double *Tprev, const double *benv,
                           const double *KvTk, double a, const double *FI, const double *FE, int nif,
-                          const double *bGm, const int32_t *if_of_row, int M, int mcur, MrW w, double *rhs) {
+                          const double *bG, int ns, const int32_t *if_of_row, int M, int mcur, MrW w, double *rhs) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= N) return;
     const int k = nif ? if_of_row[i] : -1;
+    const double bGm = k >= 0 ? bG[(int64_t)k * ns + mcur] : 0.0;   // b_G(tau_m), slot m
     double r = ML[i] * Tprev[i];
     if (!KvTk) {
-        r = fma(a, k >= 0 ? benv[i] + bGm[k] : benv[i], r);
+        r = fma(a, k >= 0 ? benv[i] + bGm : benv[i], r);
     } else {
         double KT = KvTk[i];
-        if (k >= 0) KT += FE[(int64_t)(mcur - 1) * nif + k] - bGm[k];
+        if (k >= 0) KT += FE[(int64_t)(mcur - 1) * nif + k] - bGm;
         double I = 0.0;
         for (int j = 0; j < M; ++j) {
             double Fj = FI[(int64_t)j * ldf + i];
@@ -251,8 +256,11 @@ int mrsdc_setup(Ctx &c) {
     const int nslot = M * P + 1;
     if (c.mr_nslots < nslot && c.n_if) {
         for (void *p : {(void *)c.d_ell_cnt_s, (void *)c.d_ell_col_s, (void *)c.d_ell_val_s, (void *)c.d_if_b_s,
-                        (void *)c.d_if_phi_s})
+                        (void *)c.d_if_phi_s, (void *)c.d_pairs_s, (void *)c.d_pcnt_s})
             if (p) cudaFree(p);
+        // pair records of all node times at once (one launch set per step, slot = blockIdx.y)
+        CK(cudaMalloc(&c.d_pairs_s, sizeof(PairRec) * (size_t)nslot * (c.nTA + c.nTB) * c.pcap));
+        CK(cudaMalloc(&c.d_pcnt_s, sizeof(int32_t) * (size_t)nslot * (c.nTA + c.nTB)));
         CK(cudaMalloc(&c.d_ell_cnt_s, sizeof(int32_t) * nslot * nif));
         CK(cudaMalloc(&c.d_ell_col_s, sizeof(int32_t) * (size_t)nslot * c.cap * nif));
         CK(cudaMalloc(&c.d_ell_val_s, sizeof(double) * (size_t)nslot * c.cap * nif));
@@ -294,6 +302,25 @@ static MrPtr mr_pointers(Ctx &c, double *T0) {
     return q;
 }
 
+// K_G, b_G unscaled (dt = -1, Jacobi rows untouched) at the node times of d_step_sc[0..ns), all
+// in one launch set with the slot as the batch index (layout [k][c][slot]).
+static int assemble_slots(Ctx &c, int ns) {
+    if (!c.n_if) return 0;
+    IfaceParams Pf;
+    memset(&Pf, 0, sizeof Pf);
+    iface_params(c, Pf, c.d_step_sc, -1.0);
+    Pf.S = ns;
+    Pf.pairs = c.d_pairs_s;
+    Pf.pcnt = c.d_pcnt_s;
+    Pf.ell_cnt = c.d_ell_cnt_s;
+    Pf.ell_col = c.d_ell_col_s;
+    Pf.ell_val = c.d_ell_val_s;
+    Pf.if_b = c.d_if_b_s;
+    Pf.if_phi = c.d_if_phi_s;
+    Pf.no_dinv = 1;
+    return iface_launch(c, Pf);
+}
+
 int mrsdc_step(Ctx &c, double tn, double dt, int step_index) {
     const int M = c.mr_M, P = c.mr_P, K = c.mr_K;
     const int64_t N = c.N;
@@ -328,35 +355,13 @@ int mrsdc_step(Ctx &c, double tn, double dt, int step_index) {
         CK(cudaMalloc(&c.d_area, sizeof(double) * (size_t)nslot));
     }
     CK(cudaMemcpyAsync(c.d_step_sc, sc.data(), sizeof(double) * sc.size(), cudaMemcpyHostToDevice, st));
-    const size_t ell_stride = (size_t)c.cap * std::max(nif, 1);
-    auto slot_ptrs = [&](int q, const int32_t *&cnt, const int32_t *&col, const double *&val, const double *&b) {
-        cnt = c.d_ell_cnt_s + (size_t)q * nif;
-        col = c.d_ell_col_s + (size_t)q * ell_stride;
-        val = c.d_ell_val_s + (size_t)q * ell_stride;
-        b = c.d_if_b_s + (size_t)q * nif;
-    };
-    if (nif) {
-        for (int q = 0; q < nslot; ++q) {
-            IfaceParams Pf;
-            memset(&Pf, 0, sizeof Pf);
-            iface_params(c, Pf, c.d_step_sc + 4 * q, -1.0);   // dt = -1: K_G = M_B + C_B unscaled
-            Pf.ell_cnt = c.d_ell_cnt_s + (size_t)q * nif;
-            Pf.ell_col = c.d_ell_col_s + (size_t)q * ell_stride;
-            Pf.ell_val = c.d_ell_val_s + (size_t)q * ell_stride;
-            Pf.if_b = c.d_if_b_s + (size_t)q * nif;
-            Pf.if_phi = c.d_if_phi_s + (size_t)q * nif;
-            Pf.no_dinv = 1;
-            if (iface_launch(c, Pf)) return -3;
-        }
-    }
+    if (assemble_slots(c, nslot)) return -3;
     double *T0 = c.d_T[c.cur];
     MrPtr q = mr_pointers(c, T0);
     auto fe_apply = [&](int slot, const double *x, double *y) -> int {
         if (!nif) return 0;
-        const int32_t *cnt, *col;
-        const double *val, *b;
-        slot_ptrs(slot, cnt, col, val, b);
-        k_fe_apply<<<nbk(nif), 256, 0, st>>>(nif, cnt, col, val, b, x, y);
+        k_fe_apply<<<nbk(nif), 256, 0, st>>>(nif, nslot, slot, c.cap, c.d_ell_cnt_s, c.d_ell_col_s, c.d_ell_val_s,
+                                             c.d_if_b_s, x, y);
         CK(cudaGetLastError());
         return 0;
     };
@@ -473,22 +478,8 @@ int sdc_step(Ctx &c, double tn, double dt, int step_index) {
         CK(cudaMalloc(&c.d_area, sizeof(double) * (size_t)nslot));
     }
     CK(cudaMemcpyAsync(c.d_step_sc, sc.data(), sizeof(double) * 4 * nslot, cudaMemcpyHostToDevice, st));
-    const size_t ell_stride = (size_t)c.cap * nifs;
-    // unscaled K_G, b_G at the node times (for F(T^k_j, tau_j) in the quadrature)
-    if (nif) {
-        for (int q = 1; q < nslot; ++q) {
-            IfaceParams Pf;
-            memset(&Pf, 0, sizeof Pf);
-            iface_params(c, Pf, c.d_step_sc + 4 * q, -1.0);
-            Pf.ell_cnt = c.d_ell_cnt_s + (size_t)q * nif;
-            Pf.ell_col = c.d_ell_col_s + (size_t)q * ell_stride;
-            Pf.ell_val = c.d_ell_val_s + (size_t)q * ell_stride;
-            Pf.if_b = c.d_if_b_s + (size_t)q * nif;
-            Pf.if_phi = c.d_if_phi_s + (size_t)q * nif;
-            Pf.no_dinv = 1;
-            if (iface_launch(c, Pf)) return -3;
-        }
-    }
+    // unscaled K_G, b_G at the node times (for F(T^k_j, tau_j) in the quadrature), one launch set
+    if (assemble_slots(c, nslot)) return -3;
     // implicit Jacobian M_L - a K(tau_m): interface rows reassembled into the solve arrays
     auto reassemble = [&](int m) -> int {
         if (!nif) return 0;
@@ -499,13 +490,10 @@ int sdc_step(Ctx &c, double tn, double dt, int step_index) {
     };
     double *T0 = c.d_T[c.cur];
     MrPtr q = mr_pointers(c, T0);
-    const double *bG_of = c.d_if_b_s;   // slot m: c.d_if_b_s + m * nif
     auto fe_apply = [&](int slot, const double *x, double *y) -> int {
         if (!nif) return 0;
-        k_fe_apply<<<nbk(nif), 256, 0, st>>>(nif, c.d_ell_cnt_s + (size_t)slot * nif,
-                                             c.d_ell_col_s + (size_t)slot * ell_stride,
-                                             c.d_ell_val_s + (size_t)slot * ell_stride, c.d_if_b_s + (size_t)slot * nif,
-                                             x, y);
+        k_fe_apply<<<nbk(nif), 256, 0, st>>>(nif, nslot, slot, c.cap, c.d_ell_cnt_s, c.d_ell_col_s, c.d_ell_val_s,
+                                             c.d_if_b_s, x, y);
         CK(cudaGetLastError());
         return 0;
     };
@@ -525,7 +513,7 @@ int sdc_step(Ctx &c, double tn, double dt, int step_index) {
     for (int m = 1; m <= M; ++m) {
         if (reassemble(m)) return -3;
         k_sdc_rhs<<<nbk(N), 256, 0, st>>>(N, ldf, c.d_ML, q.TSo[m - 1], c.d_benv, nullptr, a, nullptr, nullptr, nif,
-                                          bG_of + (size_t)m * nifs, c.d_if_of_row, M, m, w0, q.rhs);
+                                          c.d_if_b_s, nslot, c.d_if_of_row, M, m, w0, q.rhs);
         CK(cudaGetLastError());
         if (solve(q.TSo[m - 1], q.TSo[m], q.rhs)) return -3;
     }
@@ -542,7 +530,7 @@ int sdc_step(Ctx &c, double tn, double dt, int step_index) {
             if (vol_apply(q.TSo[m], nullptr, 0.0, q.KvTk)) return -3;   // (A + B_env) T^k_m
             if (reassemble(m)) return -3;
             k_sdc_rhs<<<nbk(N), 256, 0, st>>>(N, ldf, c.d_ML, q.TSn[m - 1], c.d_benv, q.KvTk, a, q.FI, q.FE, nif,
-                                              bG_of + (size_t)m * nifs, c.d_if_of_row, M, m, wr, q.rhs);
+                                              c.d_if_b_s, nslot, c.d_if_of_row, M, m, wr, q.rhs);
             CK(cudaGetLastError());
             if (solve(q.TSo[m], q.TSn[m], q.rhs)) return -3;
         }
