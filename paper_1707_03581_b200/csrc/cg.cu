@@ -904,6 +904,10 @@ int cg_setup(Ctx &c) {
                                                                            nchunks, W, c.d_chunk_hi);
     CK(cudaGetLastError());
     c.cg_grid = (kVariants[chosen].kind == 0 ? per_sm : 1) * c.num_sms;
+    if (const char *e = getenv("THERMO_CG_CTAS")) {   // tuning hook: fewer CTAs than SMs
+        const int g = atoi(e);
+        if (g >= 1 && g < c.cg_grid) c.cg_grid = g;
+    }
     CK(cudaMalloc(&c.d_partials, sizeof(double) * THERMO_NRED * c.cg_grid));
     return 0;
 }

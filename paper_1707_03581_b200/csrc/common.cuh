@@ -223,6 +223,8 @@ struct IfaceParams {
     double *DinvS;            // S > 1: [N][SP] per-scenario Jacobi inverse diagonal
     int SP;                   // S > 1: row stride of the block vectors (even, >= S)
     int no_dinv;              // 1: leave the Jacobi diagonal alone (MRSDC: f^E is explicit)
+    int slot_major;           // 1: batch index = node-time slot, arrays laid out slot by slot
+                              // ([s][c][k], [s][k]) so per-slot row loops stay coalesced
     int dinv_compact;         // 1 (S == 1): write the rows' Jacobi inverses to if_dinv[k] instead of
                               // Dinv[row] (the overlapped step scatters them before the solve)
     int *status;              // status[1] |= overflow
@@ -232,7 +234,12 @@ struct IfaceParams {
 // rows of a slice); S > 1: [k][c][s] (coalesced across the scenarios of one row).
 // ell_cnt, if_b, if_phi are indexed [k * S + s].
 __host__ __device__ __forceinline__ int64_t ell_index(const IfaceParams &P, int s, int c, int k) {
+    if (P.slot_major) return ((int64_t)s * P.cap + c) * P.n_if + k;
     return P.S == 1 ? (int64_t)c * P.n_if + k : ((int64_t)k * P.cap + c) * P.S + s;
+}
+// per-row entries (ell_cnt, if_b, if_phi) of row k, batch index s
+__host__ __device__ __forceinline__ int64_t row_index(const IfaceParams &P, int s, int k) {
+    return P.slot_major ? (int64_t)s * P.n_if + k : (int64_t)k * P.S + s;
 }
 
 }  // namespace thermo

@@ -454,9 +454,9 @@ __global__ void __launch_bounds__(32 * ROW_WPB) k_rows(IfaceParams P) {
     dself = warp_sum(dself);   // exactly one lane holds the diagonal (others add 0)
     if (lane == 0) {
         if (!ok) atomicOr(&P.status[1], 1);
-        P.ell_cnt[(int64_t)k * P.S + s] = ok ? count : 0;
-        P.if_phi[(int64_t)k * P.S + s] = phi;
-        P.if_b[(int64_t)k * P.S + s] = 0.5 * P.step_sc[4 * s + 2] * phi;
+        P.ell_cnt[row_index(P, s, k)] = ok ? count : 0;
+        P.if_phi[row_index(P, s, k)] = phi;
+        P.if_b[row_index(P, s, k)] = 0.5 * P.step_sc[4 * s + 2] * phi;
         const double dinv = 1.0 / (P.Dvol[row] + dself);
         if (P.no_dinv) {
         } else if (P.dinv_compact) {

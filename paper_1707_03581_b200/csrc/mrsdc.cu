@@ -53,16 +53,16 @@ __global__ void k_vol_apply(const int64_t *slice_ptr, const int32_t *col, const 
     y[i] = acc;
 }
 
-// compact f^E on the interface rows of node-time slot s (slot arrays laid out like the batched
-// scenarios, [k][c][slot] with ns slots): y[k] = b_G[k] + sum_c K_G[k][c] x[col]
-__global__ void k_fe_apply(int n_if, int ns, int s, int cap, const int32_t *cnt, const int32_t *ecol,
-                           const double *evals, const double *bG, const double *x, double *y) {
+// compact f^E on the interface rows of node-time slot s (slot-major arrays [s][c][k], [s][k]):
+// y[k] = b_G[k] + sum_c K_G[k][c] x[col]
+__global__ void k_fe_apply(int n_if, int s, int cap, const int32_t *cnt, const int32_t *ecol, const double *evals,
+                           const double *bG, const double *x, double *y) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n_if) return;
-    double acc = bG[(int64_t)k * ns + s];
-    const int m = cnt[(int64_t)k * ns + s];
+    double acc = bG[(int64_t)s * n_if + k];
+    const int m = cnt[(int64_t)s * n_if + k];
     for (int c = 0; c < m; ++c) {
-        const int64_t e = ((int64_t)k * cap + c) * ns + s;
+        const int64_t e = ((int64_t)s * cap + c) * n_if + k;
         acc = fma(evals[e], x[ecol[e]], acc);
     }
     y[k] = acc;
@@ -128,7 +128,7 @@ __global__ void k_sdc_rhs(int64_t N, int64_t ldf, const double *ML, const double
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= N) return;
     const int k = nif ? if_of_row[i] : -1;
-    const double bGm = k >= 0 ? bG[(int64_t)k * ns + mcur] : 0.0;   // b_G(tau_m), slot m
+    const double bGm = k >= 0 ? bG[(int64_t)mcur * nif + k] : 0.0;   // b_G(tau_m), slot m
     double r = ML[i] * Tprev[i];
     if (!KvTk) {
         r = fma(a, k >= 0 ? benv[i] + bGm : benv[i], r);
@@ -318,6 +318,7 @@ static int assemble_slots(Ctx &c, int ns) {
     Pf.if_b = c.d_if_b_s;
     Pf.if_phi = c.d_if_phi_s;
     Pf.no_dinv = 1;
+    Pf.slot_major = 1;
     return iface_launch(c, Pf);
 }
 
@@ -360,7 +361,7 @@ int mrsdc_step(Ctx &c, double tn, double dt, int step_index) {
     MrPtr q = mr_pointers(c, T0);
     auto fe_apply = [&](int slot, const double *x, double *y) -> int {
         if (!nif) return 0;
-        k_fe_apply<<<nbk(nif), 256, 0, st>>>(nif, nslot, slot, c.cap, c.d_ell_cnt_s, c.d_ell_col_s, c.d_ell_val_s,
+        k_fe_apply<<<nbk(nif), 256, 0, st>>>(nif, slot, c.cap, c.d_ell_cnt_s, c.d_ell_col_s, c.d_ell_val_s,
                                              c.d_if_b_s, x, y);
         CK(cudaGetLastError());
         return 0;
@@ -492,7 +493,7 @@ int sdc_step(Ctx &c, double tn, double dt, int step_index) {
     MrPtr q = mr_pointers(c, T0);
     auto fe_apply = [&](int slot, const double *x, double *y) -> int {
         if (!nif) return 0;
-        k_fe_apply<<<nbk(nif), 256, 0, st>>>(nif, nslot, slot, c.cap, c.d_ell_cnt_s, c.d_ell_col_s, c.d_ell_val_s,
+        k_fe_apply<<<nbk(nif), 256, 0, st>>>(nif, slot, c.cap, c.d_ell_cnt_s, c.d_ell_col_s, c.d_ell_val_s,
                                              c.d_if_b_s, x, y);
         CK(cudaGetLastError());
         return 0;

@@ -5,8 +5,9 @@ implicit-Euler steps from the uniform start T0, sampled at a fixed seeded set of
 interface row plus a uniform sample) -- the GPU full run is compared against them in
 tests/test_gpu_fullrun.py.
 
-    python tools/make_golden_fullrun.py cfg2 [nsteps]      (~30 min single thread)
-    python tools/make_golden_fullrun.py cfg3 [nsteps]      (~1 h)
+    python tools/make_golden_fullrun.py cfg2 [nsteps]      (~1.7 h single thread)
+    python tools/make_golden_fullrun.py cfg3 [nsteps]      (~1.5 h)
+    python tools/make_golden_fullrun.py cfg4 [nsteps]      (scenarios 0, 37, 63 of the batch, whole fields)
 """
 import json
 import os
@@ -34,10 +35,31 @@ def sample_rows(cfg, n_uniform=20000, seed=1707):
     return np.array(sorted(rows), dtype=np.int64)
 
 
+def batched(cfg, nsteps, scen=(0, 37, 63)):
+    """Config 4: independent oracle runs of sampled scenarios of the batch, whole fields."""
+    o = O.Oracle.from_config(cfg)
+    t1 = time.time()
+    vals, iters = [], 0
+    for k in scen:
+        T, st = o.step(np.full(o.n, cfg.T0), 0.0, cfg.dt, nsteps, cfg.scenarios[k])
+        vals.append(T)
+        iters += int(st[:, 0].sum())
+        print(f"{cfg.name}: scenario {k} done, {time.time() - t1:.0f} s", flush=True)
+    out = os.path.join(ROOT, "tests", "golden", f"fullrun_{cfg.name}.npz")
+    meta = {"config": cfg.name, "nsteps": nsteps, "dt": cfg.dt, "t0": 0.0, "T0": cfg.T0, "n_dof": cfg.n_dof,
+            "n_scen": cfg.n_scen, "scenarios": list(scen), "solver": "oracle Jacobi-PCG, rtol 1e-12, x0 = T^n",
+            "script": "tools/make_golden_fullrun.py", "oracle_seconds": time.time() - t1,
+            "cg_iterations_total": iters}
+    np.savez_compressed(out, scen=np.array(scen), values=np.stack(vals), meta=json.dumps(meta))
+    print(json.dumps(meta))
+
+
 def main():
     name = sys.argv[1]
     cfg = I.make_config(name)
     nsteps = int(sys.argv[2]) if len(sys.argv) > 2 else cfg.nsteps
+    if cfg.n_scen > 1:
+        return batched(cfg, nsteps)
     t0 = time.time()
     o = O.Oracle.from_config(cfg)
     t1 = time.time()
