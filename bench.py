@@ -44,7 +44,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="thermo", choices=["thermo", "reference"])
     ap.add_argument("--config", default="cfg3")
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
@@ -213,18 +213,20 @@ def run_thermo(args):
     ms_max = D.max_over_ranks(ms, device="cuda")
 
     # ---- e2e through the C ABI with host buffers: per step, H2D of the step's time scalars
-    # (inside thermo_step) + D2H of the whole temperature field into pinned host memory
+    # (inside thermo_step) + D2H of the whole temperature field of every scenario into pinned
+    # host memory (thermo_get_T_async: the copy of step k overlaps step k + 1; two host
+    # buffer sets alternate); thermo_sync waits for the last copies inside the timed region
     KE = max(1, args.e2e_steps)
-    host = torch.empty(cfg.n_dof, dtype=torch.float64, pin_memory=True)
-    hosts = [host] + [torch.empty(cfg.n_dof, dtype=torch.float64, pin_memory=True) for _ in range(th.S - 1)]
+    hosts = [[torch.empty(cfg.n_dof, dtype=torch.float64, pin_memory=True) for _ in range(th.S)] for _ in range(2)]
     barrier()
     e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e2.record(stream)
     for k in range(KE):
         th.step(t, cfg.dt, 1)
-        for sc, h in enumerate(hosts):
-            th.get_T_host_ptr(h.data_ptr(), scen=sc)
+        for sc, h in enumerate(hosts[k & 1]):
+            th.get_T_async(h.data_ptr(), scen=sc)
         t += cfg.dt
+    th.sync()
     e3.record(stream)
     torch.cuda.synchronize()
     ms_e2e = D.max_over_ranks(e2.elapsed_time(e3), device="cuda")

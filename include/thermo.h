@@ -116,6 +116,17 @@ int thermo_step(void *ctx, double t, double dt, int32_t nsteps);
 int thermo_get_T(void *ctx, int32_t scen, int32_t part, double *out, int64_t n,
                  int32_t out_on_device);
 
+/* Asynchronous variant of thermo_get_T for host memory: enqueues the copy of the current state
+ * (as of the work queued so far) on the context's copy stream and returns at once, so the
+ * transfer overlaps the next thermo_step (the state is double-buffered; a later call that would
+ * overwrite the buffer being copied waits for the copy on the device).  host_out should be
+ * pinned (e.g. cudaHostAlloc / a pinned torch tensor) for a real overlap; its contents are valid
+ * after thermo_sync().  Same selection rules and errors as thermo_get_T. */
+int thermo_get_T_async(void *ctx, int32_t scen, int32_t part, double *host_out, int64_t n);
+
+/* Wait for all work of the context: its stream and every pending asynchronous copy. */
+int thermo_sync(void *ctx);
+
 /* Overwrite the temperature of one scenario and part (same selection rules as get_T). */
 int thermo_set_T(void *ctx, int32_t scen, int32_t part, const double *in, int64_t n,
                  int32_t in_on_device);

@@ -132,6 +132,11 @@ struct Ctx {
     // the solve of step n (S == 1, implicit Euler; THERMO_OVERLAP=0 disables)
     int overlap = 0;
     cudaStream_t side = nullptr;
+    // asynchronous host copies of the state (thermo_get_T_async): a copy stream, and per state
+    // buffer the event after which a pending copy has read it
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t ev_ready = nullptr, ev_copy[2] = {nullptr, nullptr};
+    int copy_pending[2] = {0, 0};
     cudaEvent_t ev_if[2] = {nullptr, nullptr}, ev_cg[2] = {nullptr, nullptr}, ev_join = nullptr;
     int32_t *d_ell_cnt1 = nullptr, *d_ell_col1 = nullptr;
     double *d_ell_val1 = nullptr, *d_if_b1 = nullptr, *d_if_phi1 = nullptr, *d_if_dinv1 = nullptr;

@@ -33,6 +33,14 @@ static int fail(Ctx *c, int code, const std::string &msg) {
     return code;
 }
 
+// Before work on the context stream overwrites state buffer b: wait for an asynchronous host
+// copy still reading it (thermo_get_T_async).
+static cudaError_t guard_write(Ctx *c, int b) {
+    if (!c->copy_pending[b]) return cudaSuccess;
+    c->copy_pending[b] = 0;
+    return cudaStreamWaitEvent(c->stream, c->ev_copy[b], 0);
+}
+
 static void free_ctx(Ctx *c) {
     if (!c) return;
     void *ptrs[] = {c->d_xyz, c->d_tets, c->d_faces, c->d_fkey, c->d_tinc_ptr, c->d_tinc, c->d_finc_ptr,
@@ -51,9 +59,12 @@ static void free_ctx(Ctx *c) {
     for (void *p : ptrs)
         if (p) cudaFree(p);
     for (cudaEvent_t e : c->events) cudaEventDestroy(e);
-    for (cudaEvent_t e : {c->ev_if[0], c->ev_if[1], c->ev_cg[0], c->ev_cg[1], c->ev_join})
+    if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
+    for (cudaEvent_t e : {c->ev_if[0], c->ev_if[1], c->ev_cg[0], c->ev_cg[1], c->ev_join, c->ev_ready, c->ev_copy[0],
+                          c->ev_copy[1]})
         if (e) cudaEventDestroy(e);
     if (c->side) cudaStreamDestroy(c->side);
+    if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     delete c;
 }
 
@@ -290,6 +301,7 @@ extern "C" int thermo_stationary(void *ctx, double t, int32_t with_interface) {
                                                                          iface ? c->d_if_b : nullptr, c->d_rhs);
         API_CK(cudaGetLastError());
         double *x0 = c->d_T[c->cur], *x = c->d_T[c->cur ^ 1];
+        API_CK(guard_write(c, c->cur ^ 1));
         if (thermo::cg_launch_solve(*c, x0, x, c->d_rhs, iface ? c->d_Dinv : c->d_Dinv_vol, iface, c->d_iters,
                                     c->d_relres, 0))
             return THERMO_ECUDA;
@@ -397,6 +409,7 @@ extern "C" int thermo_step(void *ctx, double t, double dt, int32_t nsteps) {
             c->ms_iface = c->ms_solve = 0.0;
             for (int n = 0; n < nsteps; ++n) {
                 API_CK(cudaMemsetAsync(c->d_status, 0, sizeof(int) * 8, c->stream));
+                API_CK(guard_write(c, c->cur ^ 1));
                 if ((c->method == 1 ? thermo::mrsdc_step(*c, t + (double)n * dt, dt, n)
                                     : thermo::sdc_step(*c, t + (double)n * dt, dt, n)))
                     return THERMO_ECUDA;
@@ -460,6 +473,7 @@ extern "C" int thermo_step(void *ctx, double t, double dt, int32_t nsteps) {
                 if (n + 1 < nsteps)
                     if (int rc = assemble(n + 1)) return rc;
                 API_CK(cudaStreamWaitEvent(c->stream, c->ev_if[n & 1], 0));
+                API_CK(guard_write(c, (c->cur + n + 1) & 1));
                 if (c->timing) API_CK(cudaEventRecord(c->events[4 * n + 2], c->stream));
                 if (thermo::scatter_dinv(*c, n & 1) || thermo::cg_launch_step(*c, n, dt, n & 1)) return THERMO_ECUDA;
                 if (c->timing) API_CK(cudaEventRecord(c->events[4 * n + 3], c->stream));
@@ -475,6 +489,7 @@ extern "C" int thermo_step(void *ctx, double t, double dt, int32_t nsteps) {
                 if (c->timing) API_CK(cudaEventRecord(c->events[2 * n], c->stream));
                 if (thermo::iface_launch(*c, P)) return THERMO_ECUDA;
                 if (c->timing) API_CK(cudaEventRecord(c->events[2 * n + 1], c->stream));
+                API_CK(guard_write(c, (c->cur + n + 1) & 1));
                 if ((S == 1 ? thermo::cg_launch_step(*c, n, dt) : thermo::cgb_launch_step(*c, n, dt))) return THERMO_ECUDA;
             }
             if (c->timing) API_CK(cudaEventRecord(c->events[2 * nsteps], c->stream));
@@ -567,6 +582,41 @@ extern "C" int thermo_get_T(void *ctx, int32_t scen, int32_t part, double *out, 
     return THERMO_OK;
 }
 
+extern "C" int thermo_get_T_async(void *ctx, int32_t scen, int32_t part, double *host_out, int64_t n) {
+    Ctx *c = (Ctx *)ctx;
+    if (!c || !host_out) return c ? fail(c, THERMO_EINVAL, "host_out is NULL") : THERMO_EINVAL;
+    int64_t off, cnt;
+    if (int rc = selection(c, scen, part, n, &off, &cnt)) return rc;
+    if (!c->copy_stream) {
+        API_CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+        for (cudaEvent_t *e : {&c->ev_ready, &c->ev_copy[0], &c->ev_copy[1]})
+            API_CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    }
+    const int b = c->cur;
+    const double *src = c->d_T[b] + off * c->SP + scen;
+    API_CK(cudaEventRecord(c->ev_ready, c->stream));   // the state as of the work queued so far
+    API_CK(cudaStreamWaitEvent(c->copy_stream, c->ev_ready, 0));
+    if (c->SP == 1)
+        API_CK(cudaMemcpyAsync(host_out, src, sizeof(double) * cnt, cudaMemcpyDeviceToHost, c->copy_stream));
+    else
+        API_CK(cudaMemcpy2DAsync(host_out, sizeof(double), src, sizeof(double) * c->SP, sizeof(double), cnt,
+                                 cudaMemcpyDeviceToHost, c->copy_stream));
+    API_CK(cudaEventRecord(c->ev_copy[b], c->copy_stream));
+    c->copy_pending[b] = 1;
+    return THERMO_OK;
+}
+
+extern "C" int thermo_sync(void *ctx) {
+    Ctx *c = (Ctx *)ctx;
+    if (!c) return THERMO_EINVAL;
+    if (c->copy_stream) {
+        API_CK(cudaStreamSynchronize(c->copy_stream));
+        c->copy_pending[0] = c->copy_pending[1] = 0;
+    }
+    API_CK(cudaStreamSynchronize(c->stream));
+    return THERMO_OK;
+}
+
 extern "C" int thermo_set_T(void *ctx, int32_t scen, int32_t part, const double *in, int64_t n,
                             int32_t in_on_device) {
     Ctx *c = (Ctx *)ctx;
@@ -574,6 +624,7 @@ extern "C" int thermo_set_T(void *ctx, int32_t scen, int32_t part, const double 
     int64_t off, cnt;
     if (int rc = selection(c, scen, part, n, &off, &cnt)) return rc;
     double *dst = c->d_T[c->cur] + off * c->SP + scen;
+    API_CK(guard_write(c, c->cur));
     cudaMemcpyKind kind = in_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     if (c->SP == 1) API_CK(cudaMemcpyAsync(dst, in, sizeof(double) * cnt, kind, c->stream));
     else API_CK(cudaMemcpy2DAsync(dst, sizeof(double) * c->SP, in, sizeof(double), sizeof(double), cnt, kind, c->stream));

@@ -20,7 +20,8 @@ _CODES = {-1: "EINVAL", -2: "ENOMEM", -3: "ECUDA", -4: "ENOCONV", -5: "EGEOM"}
 # symbols declared in include/thermo.h
 EXPORTS = ["thermo_create_mesh", "thermo_set_bc", "thermo_step", "thermo_get_T", "thermo_set_T",
            "thermo_set_solver", "thermo_get_stats", "thermo_get_step_iters", "thermo_last_error",
-           "thermo_destroy", "thermo_set_timing", "thermo_set_method", "thermo_stationary"]
+           "thermo_destroy", "thermo_set_timing", "thermo_set_method", "thermo_stationary",
+           "thermo_get_T_async", "thermo_sync"]
 
 
 class ThermoError(RuntimeError):
@@ -83,6 +84,8 @@ def load(path: str = LIB_PATH):
     L.thermo_set_timing.argtypes = [vp, i32]
     L.thermo_set_method.argtypes = [vp, i32, i32, i32, i32]
     L.thermo_stationary.argtypes = [vp, ctypes.c_double, i32]
+    L.thermo_get_T_async.argtypes = [vp, i32, i32, vp, ctypes.c_int64]
+    L.thermo_sync.argtypes = [vp]
     _lib = L
     return L
 
@@ -190,6 +193,15 @@ class Thermo:
         synchronises the context stream."""
         n = self._count(part)
         self._check(load().thermo_get_T(self.h, scen, part, ctypes.c_void_p(ptr), n, 0))
+
+    def get_T_async(self, ptr: int, scen: int = 0, part: int = -1):
+        """Enqueue a copy of the current state into caller-owned (pinned) host memory at `ptr`
+        and return at once; valid after sync()."""
+        n = self._count(part)
+        self._check(load().thermo_get_T_async(self.h, scen, part, ctypes.c_void_p(ptr), n))
+
+    def sync(self):
+        self._check(load().thermo_sync(self.h))
 
     def set_T(self, T, scen: int = 0, part: int = -1):
         n = self._count(part)

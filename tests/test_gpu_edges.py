@@ -101,3 +101,25 @@ def test_overlapped_interface_path_is_bitwise_identical(monkeypatch):
         th.step(7 * cfg.dt, cfg.dt, 1)
     assert np.array_equal(seq.get_T(), ovl.get_T())
     assert seq.stats()["iface_area"] == ovl.stats()["iface_area"]
+
+
+def test_async_host_copies_overlap_safely():
+    """thermo_get_T_async: each copy holds the state of the moment it was enqueued, even when the
+    following steps overwrite the double-buffered state while the copies are in flight."""
+    import torch
+    from paper_1707_03581_b200.thermo import Thermo
+    cfg = I.make_config("small", jitter=0.1)
+    ref = Thermo.from_config(cfg)
+    expect = []
+    for k in range(4):
+        ref.step(k * cfg.dt, cfg.dt, 1)
+        expect.append(ref.get_T())
+    th = Thermo.from_config(cfg)
+    hosts = [torch.empty(cfg.n_dof, dtype=torch.float64, pin_memory=True) for _ in range(4)]
+    for k in range(4):
+        th.step(k * cfg.dt, cfg.dt, 1)
+        th.get_T_async(hosts[k].data_ptr())
+    th.set_T(np.zeros(cfg.n_dof))          # overwrites the current buffer: must wait for its copy
+    th.sync()
+    for k in range(4):
+        assert np.array_equal(hosts[k].numpy(), expect[k]), k
