@@ -5,6 +5,8 @@ Reading R24: P:510 prints s^_{m,p} = sum_q s_{m,p,q}; the consistenc
 I_{m-1}^m = sum_p I_{m,p-1}^p requires the sum over the sub-intervals p, i.e.
 s^_{m,q} = sum_p s_{m,p,q} (summing over q instead gives the sub-interval length).
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -17,10 +19,16 @@ def test_weights_closed_forms():
     tau, taue, s, sh, st, se = O.mrsdc_weights(1, 1, 0.0, 2.0)
     np.testing.assert_allclose(tau, [2.0])
     np.testing.assert_allclose(s, [[2.0]])
-    # M = 2 on [0, 1] (nodes .5, 1): q = [[.75, -.25], [1, 0]], s = q_m - q_{m-1}
+    # M = 2 on [0, 1] (nodes .5, 1): the golden fixture
     tau, taue, s, sh, st, se = O.mrsdc_weights(2, 1, 0.0, 1.0)
     np.testing.assert_allclose(tau, [0.5, 1.0])
-    np.testing.assert_allclose(s, [[0.75, -0.25], [0.25, 0.25]], atol=1e-15)
+    gold = {"q": [], "s": []}
+    for line in open(os.path.join(os.path.dirname(__file__), "golden", "sdc_weights_M2.txt")):
+        if line.strip() and not line.startswith("#"):
+            k, *v = line.split()
+            gold[k].append([float(x) for x in v])
+    np.testing.assert_allclose(s, gold["s"], atol=1e-15)
+    np.testing.assert_allclose(np.cumsum(s, axis=0), gold["q"], atol=1e-15)   # q_m = sum_{m' <= m} s_m
 
 
 @pytest.mark.parametrize("M,P", [(3, 2), (5, 8), (4, 3), (2, 5)])

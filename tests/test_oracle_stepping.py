@@ -123,9 +123,12 @@ def two_slab_closed_form(H1, H2, nu, alpha, eta, ab, Tb, at, Tt):
 
 
 def test_two_slab_closed_form_values():
-    """The closed form reproduces the profile quoted in SURVEY App. A.3 for the same data."""
+    """The closed form reproduces the profile of the golden fixture."""
+    import os
     sol = two_slab_closed_form(0.1, 0.1, 50.0, 1000.0, 500.0, 50.0, 24.0, 200.0, 18.0)
-    np.testing.assert_allclose(sol, [22.5, 22.35, 22.025, 20.875], rtol=0, atol=1e-12)
+    path = os.path.join(os.path.dirname(__file__), "golden", "two_slab_profile.txt")
+    gold = [float(x) for line in open(path) if not line.startswith("#") for x in line.split()]
+    np.testing.assert_allclose(sol, gold, rtol=0, atol=1e-12)
 
 
 @pytest.mark.parametrize("jitter", [0.0, 0.1])
