@@ -250,9 +250,15 @@ def run_thermo(args):
     achieved = alg_bytes / (st["ms_solve"] * 1e-3) / 1e9
     peak, peak_kind = peaks()
     prof = ncu_traffic(args.config)
-    traffic = None
+    traffic, dram = None, {}
     if prof:
         traffic = prof.get("dram_bytes_per_launch")
+        if prof.get("cg_iterations") and S == 1:
+            # actual DRAM bytes per CG iteration (ncu, one launch) x this run's iterations / time
+            per_it = traffic / (prof["cg_iterations"] + 0.76)   # phase 0 ~ 0.76 iteration (trace)
+            gbs = per_it * (float(iters.sum()) + 0.76 * K) / (st["ms_solve"] * 1e-3) / 1e9
+            dram = {"actual_dram_gbs_est": gbs, "actual_dram_frac_est": gbs / peak,
+                    "actual_bytes_per_iter_ncu": per_it, "algorithmic_bytes_per_iter": per_iter}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "strong" if sharded else "weak",
@@ -269,7 +275,7 @@ def run_thermo(args):
                      "traffic": traffic, "kernel": "k_cg_step (persistent Jacobi-PCG, one launch per step)",
                      "peak_kind": peak_kind, "achieved_vs_8TBs": achieved / 8000.0,
                      "solve_share_of_step": st["ms_solve"] / ms,
-                     "iface_share_of_step": st["ms_iface"] / ms},
+                     "iface_share_of_step": st["ms_iface"] / ms, **dram},
         "e2e": {"value": units * KE / (ms_e2e * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 32 * S,
                 "d2h_bytes_per_step": 8 * N * S},
         "gpu_launches": K * st["launches_per_step"],

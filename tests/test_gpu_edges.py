@@ -123,3 +123,19 @@ def test_async_host_copies_overlap_safely():
     th.sync()
     for k in range(4):
         assert np.array_equal(hosts[k].numpy(), expect[k]), k
+
+
+@pytest.mark.parametrize("s0", [0.375, 0.5, 0.0])
+def test_coincident_edges_and_vertices(s0):
+    """Static stock whose x-edges fall exactly on rail lattice lines (cfg 0: rail h_x = 1/16,
+    offsets multiples of it): degenerate overlaps (shared edges / vertices, zero-area slivers,
+    reading R7) -- parity vs Cholesky and the exact contact area 0.25 x 0.2."""
+    from paper_1707_03581_b200.thermo import Thermo
+    cfg = I.make_config("cfg0")
+    sc = I.Scenario(s0, 0.0, 60.0, 500.0)
+    cfg.scenarios = [sc]
+    th = Thermo.from_config(cfg)
+    th.step(0.0, cfg.dt, 6)
+    Tr, _ = O.Oracle.from_config(cfg).step(np.full(cfg.n_dof, cfg.T0), 0.0, cfg.dt, 6, sc, solver="cholesky")
+    assert rel(th.get_T(), Tr) <= TOL
+    assert abs(th.stats()["iface_area"] - 0.05) < 1e-14

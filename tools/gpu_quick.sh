@@ -1,5 +1,3 @@
 #!/bin/bash
 mkdir -p gpurun_out
-rm -f gpurun_out/probe_all.log
-for c in cfg0 cfg1 cfg2 cfg4; do timeout 300 python tools/probe.py $c 20 >> gpurun_out/probe_all.log 2>&1; done
-timeout 300 python tools/probe.py cfg3 10 >> gpurun_out/probe_all.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_edges.py -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_gpu.log

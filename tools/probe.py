@@ -35,5 +35,6 @@ gbs = (it.mean() * bytes_it + 12 * Z + 40 * N) / (ms * 1e-3) / 1e9
 print(f"{name}: {ms:.3f} ms/step, iters/step {it.mean():.1f} (min {it.min()} max {it.max()}), "
       f"DoF-steps/s {N / (ms * 1e-3):.3e}, alg GB/s {gbs:.0f}, per-iter {ms / it.mean() * 1e3:.1f} us", flush=True)
 st = th.stats()
+print(f"{name}: CG iterations of the timed steps (launches 4..{3 + K}): {[int(x) for x in it]}", flush=True)
 print(f"{name}: iface {st['ms_iface'] / K * 1e3:.1f} us/step, solve {st['ms_solve'] / K:.3f} ms/step "
       f"({st['ms_solve'] / K / it.mean() * 1e3:.1f} us/iter), grid {st['solve_grid']}x{st['solve_block']}", flush=True)
