@@ -72,6 +72,8 @@ struct CGBParams {
     double dt, rtol2;
     int maxit, step;
     unsigned long long *trace;   // optional: %globaltimer after every grid barrier (CTA 0)
+    int contiguous;              // 1: CTA b sweeps one contiguous block of row pairs (L1 reuse of
+                                 // the gathered neighbour rows), 0: row pairs dealt round-robin
     // windowed sweeps: chunk = CR consecutive rows of one slice; the producer bulk-copies the
     // chunk's slice (values, window-local columns, interface map) and its column window (<=
     // CGW_MAXR runs of whole block-vector rows) into one stage of an NS-stage ring
@@ -202,7 +204,8 @@ __device__ __forceinline__ void row_spmm2(const CGBParams &P, int64_t base, int 
 // first round of matrix entries of the next unit is loaded while the current one gathers.
 // body(u, base, w, rA, validB, ikA, ikB, cl, vl) runs once per unit, warp-uniformly.
 template <class Body>
-__device__ __forceinline__ void unit_loop(const CGBParams &P, int64_t npairs, int gw, int TW, int lane, Body body) {
+__device__ __forceinline__ void unit_loop(const CGBParams &P, int64_t npairs, int64_t gw, int64_t TW, int lane,
+                                          Body body) {
     const int64_t N = P.N;
     for (int64_t c0 = gw; c0 < npairs; c0 += 32 * (int64_t)TW) {
         const int64_t uk = c0 + (int64_t)lane * TW;
@@ -523,6 +526,14 @@ __global__ void __launch_bounds__(WIN ? CGW_BLOCK : CGB_BLOCK, 1) k_cgb_step(CGB
     // ---- phase 0: r0 = b - K~ x0, z0 = D^{-1} r0 per column
     double v0[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};   // b.b, r.r, r.z, |Gamma_R| (scenario 0)
     const int64_t npairs = P.nslices * 16;   // units: (slice, row pair)
+    // this warp's units: u0, u0 + ust, ... < uend
+    int64_t u0 = gw, ust = TW, uend = npairs;
+    if (P.contiguous) {
+        const int64_t upc = (npairs + gridDim.x - 1) / gridDim.x;
+        u0 = (int64_t)blockIdx.x * upc + warp;
+        ust = NW;
+        uend = min(npairs, (int64_t)(blockIdx.x + 1) * upc);
+    }
     // epilogue of one row: ax = (K~ x0)_i without the interface part, Ti = x0_i
     auto fin0 = [&](int64_t i, int ik, double2 ax, double2 Ti, double2 di) {
         double2 bg = make_double2(0.0, 0.0);
@@ -571,7 +582,7 @@ __global__ void __launch_bounds__(WIN ? CGW_BLOCK : CGB_BLOCK, 1) k_cgb_step(CGB
         R.n += (uint32_t)nloc;
         __syncthreads();   // ring drained before its memory serves as reduction scratch
     } else {
-        unit_loop(P, npairs, gw, TW, lane, [&](int64_t u, int64_t base, int w, int rA, bool validB, int ikA,
+        unit_loop(P, uend, u0, ust, lane, [&](int64_t u, int64_t base, int w, int rA, bool validB, int ikA,
                                                int ikB, int cl, double vl) {
             const int64_t iA = 32 * (u >> 4) + rA;
             double2 Tr[2], dr[2];   // own rows, loaded ahead of the gathers
@@ -647,7 +658,7 @@ __global__ void __launch_bounds__(WIN ? CGW_BLOCK : CGB_BLOCK, 1) k_cgb_step(CGB
             R.n += (uint32_t)nloc;
             __syncthreads();
         } else {
-            unit_loop(P, npairs, gw, TW, lane, [&](int64_t u, int64_t base, int w, int rA, bool validB, int ikA,
+            unit_loop(P, uend, u0, ust, lane, [&](int64_t u, int64_t base, int w, int rA, bool validB, int ikA,
                                                    int ikB, int cl, double vl) {
                 const int64_t iA = 32 * (u >> 4) + rA;
                 double2 zr[2], pr[2];   // own rows, loaded ahead of the gathers
@@ -856,6 +867,8 @@ int cgb_setup(Ctx &c) {
     }
     if (per_sm < 1) { c.err = "batched CG kernel cannot be resident"; return -3; }
     c.cg_grid = (c.cgw_on ? 1 : per_sm) * c.num_sms;
+    const char *ord = getenv("THERMO_CGB_ORDER");
+    c.cgb_contiguous = ord ? atoi(ord) : 0;   // contiguous blocks measured 3.5x slower (L2 thrash)
     if (getenv("THERMO_CG_TRACE"))
         fprintf(stderr, "[thermo] batched CG: %s, rows/chunk %d, stages %d, window rows %d, stage %u B\n",
                 c.cgw_on ? "windows" : "register gathers", c.cgw_CR, c.cgw_NS, c.cgw_wcap, c.cgw_stage);
@@ -912,6 +925,7 @@ int cgb_launch_step(Ctx &c, int step, double dt) {
     P.maxit = c.maxit > 0 ? c.maxit : (int)std::min<int64_t>(10 * c.N, 10000);
     P.step = step;
     P.trace = c.d_trace;
+    P.contiguous = c.cgb_contiguous;
     void *args[] = {&P};
     if (c.cgw_on) {
         P.CR = c.cgw_CR;

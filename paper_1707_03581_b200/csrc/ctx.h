@@ -97,6 +97,7 @@ struct Ctx {
     int cg_variant = 0, cg_chunk = 8, cg_debug = 0, cg_prefetch = 0;
     // batched windowed sweeps (cg_batched.cu); reuse d_chunk_runs / nruns / lown and d_lcol
     int cgw_on = 0, cgw_CR = 0, cgw_NS = 0, cgw_wcap = 0;
+    int cgb_contiguous = 0;            // batched: contiguous row blocks per CTA (THERMO_CGB_ORDER=1)
     int64_t cgw_nchunks = 0;
     uint32_t cgw_stage = 0, cgw_off[4] = {0, 0, 0, 0};
     size_t cgw_smem = 0;
