@@ -217,18 +217,23 @@ __global__ void k_row_fill(const int64_t *tptr, const int32_t *tinc, const int32
             acc[pos] += -nu * V * gab;
         }
     }
+    // entry 0 of every row is its diagonal (the solve reads D from there), then the other
+    // columns ascending; short rows are padded with (i, 0)
+    int d = 0;
+    while (d < n && nb[d] != i) ++d;
     for (int k = 0; k < w; ++k) {
         int64_t e = base + 32 * (int64_t)k;
-        if (k < n) {
-            col[e] = nb[k];
-            A[e] = acc[k];
-            if (nb[k] == i) diagpos[i] = e;
+        const int src = k == 0 ? d : (k <= d ? k - 1 : k);   // sorted position of entry k
+        if (k < n && d < n) {
+            col[e] = nb[src];
+            A[e] = acc[src];
         } else {
             col[e] = (int32_t)i;
             A[e] = 0.0;
         }
         R[e] = 0.0;
     }
+    diagpos[i] = base;
     ML[i] = ml;
 }
 

@@ -73,7 +73,7 @@ struct CGParams {
     int maxit, step;
     int stage_entries;         // TMA: matrix entries per stage
     int nstages;               // TMA: ring stages (<= 8)
-    int64_t u_rows;            // TMA: rows per update-phase chunk (5 streams per stage)
+    int64_t u_rows;            // TMA: rows per update-phase chunk (4 streams per stage)
     int win_cap;               // KIND 2: window entries per vector per stage
     const int32_t *chunk_hi;   // TMA: largest column index referenced by each chunk
     const int2 *chunk_runs;    // KIND 2: [nchunks][CG_MAXR] (start, length) of the window runs
@@ -159,7 +159,7 @@ __device__ __forceinline__ int iface_index_r(const CGParams &P, int b, int e, in
 
 template <bool kTwo>
 __device__ __forceinline__ double ell_row(const CGParams &P, int ik, const double *x1, const double *x2,
-                                          double beta) {
+                                          double beta, int64_t row = -1, double *self = nullptr) {
     const int cnt = P.ell_cnt[ik];
     double acc = 0.0;
     for (int c = 0; c < cnt; ++c) {
@@ -167,7 +167,9 @@ __device__ __forceinline__ double ell_row(const CGParams &P, int ik, const doubl
         const int j = P.ell_col[e];
         double y = x1[j];
         if (kTwo) y = fma(beta, x2[j], y);
-        acc = fma(P.ell_val[e], y, acc);
+        const double v = P.ell_val[e];
+        acc = fma(v, y, acc);
+        if (self && j == row) *self += v;   // the interface part of the diagonal
     }
     return acc;
 }
@@ -184,6 +186,8 @@ struct SrcGlobal {   // KIND 0: matrix streamed from HBM, gathers from L1/L2
     // own-row value of the first / second gathered vector
     __device__ __forceinline__ double own1(const double *g, int64_t i) const { return g[i]; }
     __device__ __forceinline__ double own2(const double *g, int64_t i) const { return g[i]; }
+    // value of the row's entry 0 = its diagonal (assembly order)
+    __device__ __forceinline__ double first() const { return ld_stream(vp, pol); }
     template <bool kTwo>
     __device__ __forceinline__ double dot(int w, const double *x1, const double *x2, double beta) const {
         double acc = 0.0;
@@ -214,6 +218,7 @@ struct SrcRing {     // KIND 1: matrix in the shared-memory ring, gathers from L
     const double *vp;
     __device__ __forceinline__ double own1(const double *g, int64_t i) const { return g[i]; }
     __device__ __forceinline__ double own2(const double *g, int64_t i) const { return g[i]; }
+    __device__ __forceinline__ double first() const { return vp[0]; }
     template <bool kTwo>
     __device__ __forceinline__ double dot(int w, const double *x1, const double *x2, double beta) const {
         constexpr int B = 16;
@@ -241,6 +246,7 @@ struct SrcWin {      // KIND 2: matrix and gathered vectors in shared memory
                          // one contiguous block of its column set)
     __device__ __forceinline__ double own1(const double *, int64_t) const { return w1[lown]; }
     __device__ __forceinline__ double own2(const double *, int64_t) const { return w2[lown]; }
+    __device__ __forceinline__ double first() const { return vp[0]; }
     template <bool kTwo>
     __device__ __forceinline__ double dot(int w, const double *, const double *, double beta) const {
         double acc = 0.0;
@@ -424,12 +430,12 @@ __device__ __forceinline__ void sweep(const CGParams &P, Ring &R, Body &&body) {
 }
 
 // Update phase through the TMA ring (TMA kinds): the producer bulk-copies chunks of UR rows
-// of the five input streams (p, q, D^{-1}, x, z) into a ring stage; consumer threads update
+// of the four input streams (p, D^{-1} q, x, z) into a ring stage; consumer threads update
 // their rows from shared memory and store x, z.  No L1 involvement: with most of the shared
 // memory taken by the ring, L1-allocating loads would be limited by the small L1.
-// body(row, p, q, dinv, x, z) for every row of this CTA's chunks; static chunk order.
+// body(row, p, q', x, z) for every row of this CTA's chunks; static chunk order.
 template <int W, int NG, class Body>
-__device__ __forceinline__ void sweep_u(const CGParams &P, Ring &R, const double *const (&src)[5], Body &&body) {
+__device__ __forceinline__ void sweep_u(const CGParams &P, Ring &R, const double *const (&src)[4], Body &&body) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t NS = (uint32_t)P.nstages;
     const int G = gridDim.x;
@@ -463,9 +469,9 @@ __device__ __forceinline__ void sweep_u(const CGParams &P, Ring &R, const double
                 const int64_t r0 = ch * UR;
                 const int64_t rows = min(UR, P.N - r0);
                 const uint32_t bytes = (uint32_t)(((rows + 1) & ~(int64_t)1) * 8);   // 16-B multiple
-                mbar_arrive_expect_tx(&R.full[st], 5u * bytes);
+                mbar_arrive_expect_tx(&R.full[st], 4u * bytes);
 #pragma unroll
-                for (int v = 0; v < 5; ++v)
+                for (int v = 0; v < 4; ++v)
                     bulk_g2s_nohint(sb + CG_HDR + (size_t)v * UR * 8, src[v] + r0, bytes, &R.full[st]);
             }
             __syncwarp();
@@ -492,7 +498,7 @@ __device__ __forceinline__ void sweep_u(const CGParams &P, Ring &R, const double
             const int64_t r0 = (int64_t)ch * UR;
             const int rows = (int)min(UR, P.N - r0);
             for (int r = tid; r < rows; r += W * 32)
-                body(r0 + r, base[r], base[UR + r], base[2 * UR + r], base[3 * UR + r], base[4 * UR + r]);
+                body(r0 + r, base[r], base[UR + r], base[2 * UR + r], base[3 * UR + r]);
             __syncwarp();
             if (lane == 0) mbar_arrive(&R.empty[st]);
         }
@@ -584,8 +590,11 @@ __global__ void __launch_bounds__(cg_threads(KIND, W, NG), KIND == 0 ? 2 : 1) k_
     const int64_t nthr = (int64_t)G * blockDim.x;
     int it = 0;
     while (!conv && it < P.maxit) {
-        // ---- S: p = z + beta p_old, q = K~ p, partial p.q
-        double pq[1] = {0.0};
+        // ---- S: p = z + beta p_old, q = K~ p; q' = D^{-1} q with the diagonal d taken from the
+        // row's own entries; partials of p.q and of the expansions of the next r.z and r.r
+        //   z_new = z - alpha q', r_new = z_new d:  r.z = z^2 d - 2 alpha z q + alpha^2 q^2 / d,
+        //   r.r = (z d)^2 - 2 alpha z d q + alpha^2 q^2,  so the U phase needs no reduction
+        double red[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
         const bool first = it == 0;
         P.pf[0] = P.z; P.pf[1] = pold;
         P.npf = P.prefetch ? (first ? 1 : 2) : 0;
@@ -597,94 +606,79 @@ __global__ void __launch_bounds__(cg_threads(KIND, W, NG), KIND == 0 ? 2 : 1) k_
             const double zo = src.own1(P.z, ii);   // issued before the row sum
             const double po = first ? 0.0 : src.own2(pold, ii);
             const int ik = iface_index_r(P, ib, ie, i, lane);
-            double acc;
+            double acc, dg = src.first();   // the diagonal (entry 0) + the interface self term
             if (first) {
                 acc = src.template dot<false>(w, P.z, nullptr, 0.0);
-                if (ik >= 0) acc += ell_row<false>(P, ik, P.z, nullptr, 0.0);
+                if (ik >= 0) acc += ell_row<false>(P, ik, P.z, nullptr, 0.0, ii, &dg);
             } else {
                 acc = src.template dot<true>(w, P.z, pold, beta);
-                if (ik >= 0) acc += ell_row<true>(P, ik, P.z, pold, beta);
+                if (ik >= 0) acc += ell_row<true>(P, ik, P.z, pold, beta, ii, &dg);
             }
             if (i < N) {
                 const double pi = first ? zo : fma(beta, po, zo);
+                const double qs = acc / dg;
+                const double zd = zo * dg;
                 pnew[i] = pi;
-                P.q[i] = acc;
-                pq[0] = fma(pi, acc, pq[0]);
+                P.q[i] = qs;
+                red[0] = fma(pi, acc, red[0]);
+                red[1] = fma(zo, zd, red[1]);
+                red[2] = fma(zo, acc, red[2]);
+                red[3] = fma(acc, qs, red[3]);
+                red[4] = fma(zd, zd, red[4]);
+                red[5] = fma(zd, acc, red[5]);
+                red[6] = fma(acc, acc, red[6]);
             }
         });
-        cta_reduce_store<1>(pq, red_smem, P.partials, 4);
+        cta_reduce_store<7>(red, red_smem, P.partials, 4);
         grid.sync();
         if (tr_on && ntr < 1000) P.trace[ntr++] = gtimer();
-        double tpq[1];
-        grid_total<1>(P.partials, G, 4, red_smem, tpq);
-        const double alpha = rho / tpq[0];
-        // ---- U: x += alpha p, z -= alpha D^{-1} q, partials r.z and r.r (r = z / D^{-1})
-        double red[2] = {0.0, 0.0};
+        double t7[7];
+        grid_total<7>(P.partials, G, 4, red_smem, t7);
+        const double alpha = rho / t7[0];
+        const double rz_new = fma(alpha, fma(alpha, t7[3], -2.0 * t7[2]), t7[1]);
+        const double rr_new = fma(alpha, fma(alpha, t7[6], -2.0 * t7[5]), t7[4]);
+        // ---- U: x += alpha p, z -= alpha q' (streams only, no reduction)
         if constexpr (KIND != 0) {
-            const double *const usrc[5] = {pnew, P.q, P.Dinv, xsrc, P.z};
-            sweep_u<W, NG>(P, R, usrc, [&](int64_t i, double pv, double qv, double dv, double xv, double zv) {
+            const double *const usrc[4] = {pnew, P.q, xsrc, P.z};
+            sweep_u<W, NG>(P, R, usrc, [&](int64_t i, double pv, double qv, double xv, double zv) {
                 P.T_out[i] = fma(alpha, pv, xv);
-                const double zo = fma(-alpha * dv, qv, zv);
-                P.z[i] = zo;
-                const double r = zo / dv;
-                red[0] = fma(r, zo, red[0]);
-                red[1] = fma(r, r, red[1]);
+                P.z[i] = fma(-alpha, qv, zv);
             });
         } else {   // element pairs with 16-byte loads, two pairs in flight per thread and trip
             const int64_t npair = N >> 1;
             const double2 *p2 = reinterpret_cast<const double2 *>(pnew);
             const double2 *q2 = reinterpret_cast<const double2 *>(P.q);
-            const double2 *d2 = reinterpret_cast<const double2 *>(P.Dinv);
             const double2 *x2 = reinterpret_cast<const double2 *>(xsrc);
             double2 *z2 = reinterpret_cast<double2 *>(P.z);
             double2 *o2 = reinterpret_cast<double2 *>(P.T_out);
-            auto upd = [&](double2 pv, double2 qv, double2 dv, double2 xv, double2 zv, int64_t j) {
-                double2 xo, zo;
-                xo.x = fma(alpha, pv.x, xv.x);
-                xo.y = fma(alpha, pv.y, xv.y);
-                zo.x = fma(-alpha * dv.x, qv.x, zv.x);
-                zo.y = fma(-alpha * dv.y, qv.y, zv.y);
-                o2[j] = xo;
-                z2[j] = zo;
-                const double r0 = zo.x / dv.x, r1 = zo.y / dv.y;
-                red[0] = fma(r0, zo.x, red[0]);
-                red[1] = fma(r0, r0, red[1]);
-                red[0] = fma(r1, zo.y, red[0]);
-                red[1] = fma(r1, r1, red[1]);
+            auto upd = [&](double2 pv, double2 qv, double2 xv, double2 zv, int64_t j) {
+                o2[j] = make_double2(fma(alpha, pv.x, xv.x), fma(alpha, pv.y, xv.y));
+                z2[j] = make_double2(fma(-alpha, qv.x, zv.x), fma(-alpha, qv.y, zv.y));
             };
             constexpr int UU = 2;
             int64_t j = tid;
             for (; j + (UU - 1) * nthr < npair; j += UU * nthr) {
-                double2 pv[UU], qv[UU], dv[UU], xv[UU], zv[UU];
+                double2 pv[UU], qv[UU], xv[UU], zv[UU];
 #pragma unroll
                 for (int u = 0; u < UU; ++u) {
                     const int64_t jj = j + u * nthr;
-                    pv[u] = ld_cg2(p2 + jj); qv[u] = ld_cg2(q2 + jj); dv[u] = ld_cg2(d2 + jj);
-                    xv[u] = ld_cg2(x2 + jj); zv[u] = ld_cg2(z2 + jj);
+                    pv[u] = ld_cg2(p2 + jj); qv[u] = ld_cg2(q2 + jj); xv[u] = ld_cg2(x2 + jj); zv[u] = ld_cg2(z2 + jj);
                 }
 #pragma unroll
-                for (int u = 0; u < UU; ++u) upd(pv[u], qv[u], dv[u], xv[u], zv[u], j + u * nthr);
+                for (int u = 0; u < UU; ++u) upd(pv[u], qv[u], xv[u], zv[u], j + u * nthr);
             }
-            for (; j < npair; j += nthr) upd(p2[j], q2[j], d2[j], x2[j], z2[j], j);
+            for (; j < npair; j += nthr) upd(p2[j], q2[j], x2[j], z2[j], j);
             if ((N & 1) && tid == nthr - 1) {
                 const int64_t i = N - 1;
-                const double di = P.Dinv[i];
                 P.T_out[i] = fma(alpha, pnew[i], xsrc[i]);
-                const double zi = fma(-alpha * di, P.q[i], P.z[i]);
-                P.z[i] = zi;
-                const double r = zi / di;
-                red[0] = fma(r, zi, red[0]);
-                red[1] = fma(r, r, red[1]);
+                P.z[i] = fma(-alpha, P.q[i], P.z[i]);
             }
         }
-        cta_reduce_store<2>(red, red_smem, P.partials, 5);
         grid.sync();
         if (tr_on && ntr < 1000) P.trace[ntr++] = gtimer();
-        double tr[2];
-        grid_total<2>(P.partials, G, 5, red_smem, tr);
-        beta = tr[0] / rho;
-        rho = tr[0];
-        rr = tr[1];
+        beta = rz_new / rho;
+        rho = rz_new;
+        rr = rr_new;
         conv = rr <= tol2 && !P.debug;   // debug runs: fixed iteration count (maxit)
         xsrc = P.T_out;
         double *t = pold; pold = pnew; pnew = t;
@@ -887,7 +881,7 @@ int cg_setup(Ctx &c) {
         c.cg_chunk = v.W;
         c.cg_block = cg_threads(v.kind, v.W, v.NG);
         c.cg_nstages = ns;
-        c.cg_u_rows = v.kind == 0 ? 0 : (int64_t)((sb - CG_HDR) / 40) & ~(int64_t)31;
+        c.cg_u_rows = v.kind == 0 ? 0 : (int64_t)((sb - CG_HDR) / 32) & ~(int64_t)31;   // 4 streams
         break;
     }
     if (chosen < 0) { c.err = "no CG kernel variant can be resident"; return -3; }

@@ -9,7 +9,7 @@
 #define THERMO_BLOCK 256
 #endif
 #define THERMO_WARPS (THERMO_BLOCK / 32)
-#define THERMO_NRED 8  // reduction slots per CTA
+#define THERMO_NRED 16  // reduction slots per CTA
 
 namespace thermo {
 
@@ -148,20 +148,29 @@ __device__ __forceinline__ void grid_total(const double *partials, int G, int sl
                                            double (&out)[NV]) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (warp == 0) {
+        double x[NV];
+#pragma unroll
+        for (int j = 0; j < NV; ++j) x[j] = 0.0;
+        constexpr int UN = NV > 4 ? 2 : 4;   // CTAs per batch of loads (register budget)
+        int g = lane;
+        for (; g + 32 * (UN - 1) < G; g += 32 * UN) {   // all loads of UN CTAs x NV values together
+            double a[UN][NV];
+#pragma unroll
+            for (int u = 0; u < UN; ++u)
+#pragma unroll
+                for (int j = 0; j < NV; ++j) a[u][j] = partials[(g + 32 * u) * THERMO_NRED + slot + j];
+#pragma unroll
+            for (int u = 0; u < UN; ++u)
+#pragma unroll
+                for (int j = 0; j < NV; ++j) x[j] += a[u][j];   // adds in the serial order
+        }
+        for (; g < G; g += 32)
+#pragma unroll
+            for (int j = 0; j < NV; ++j) x[j] += partials[g * THERMO_NRED + slot + j];
 #pragma unroll
         for (int j = 0; j < NV; ++j) {
-            double x = 0.0;
-            int g = lane;
-            for (; g + 96 < G; g += 128) {   // loads issued together, adds in the serial order
-                const double a0 = partials[g * THERMO_NRED + slot + j];
-                const double a1 = partials[(g + 32) * THERMO_NRED + slot + j];
-                const double a2 = partials[(g + 64) * THERMO_NRED + slot + j];
-                const double a3 = partials[(g + 96) * THERMO_NRED + slot + j];
-                x += a0; x += a1; x += a2; x += a3;
-            }
-            for (; g < G; g += 32) x += partials[g * THERMO_NRED + slot + j];
-            x = warp_sum(x);
-            if (lane == 0) smem[136 + j] = x;
+            const double t = warp_sum(x[j]);
+            if (lane == 0) smem[136 + j] = t;
         }
     }
     __syncthreads();
