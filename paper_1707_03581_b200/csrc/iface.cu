@@ -351,9 +351,6 @@ __global__ void __launch_bounds__(32 * ROW_WPB) k_rows(IfaceParams P) {
     const double scale = P.dt * P.alpha;
     const int st0 = P.star_ptr[k], nstar = P.star_ptr[k + 1] - st0;   // <= 32 (checked at setup)
     const unsigned lt = (1u << lane) - 1u;
-    for (int h = lane; h < ROW_HS; h += 32) W.hkey[h] = -1;
-    __syncwarp();
-
     int t_l = 0, np_l = 0, a_l = 0;
     if (lane < nstar) {
         t_l = P.star_tri[st0 + lane];
@@ -363,6 +360,10 @@ __global__ void __launch_bounds__(32 * ROW_WPB) k_rows(IfaceParams P) {
     }
     const int roff = warp_excl_scan(np_l, lane);
     const int R = __shfl_sync(0xffffffffu, roff + np_l, 31);
+    if (R > 0) {   // rows without overlap (most of the rail top) skip the hash table
+        for (int h = lane; h < ROW_HS; h += 32) W.hkey[h] = -1;
+        __syncwarp();
+    }
     int count = 0;
     bool ok = true;
     double phi = 0.0;
