@@ -1,5 +1,7 @@
 #!/bin/bash
-# bench + launch list + one ncu --set full capture of the CG kernel (cfg3), tests
+# tests, bench, launch list of the bench command, one ncu --set full capture of the CG kernel
+# (cfg3, first timed launch of the probe: its CG iteration count is printed by the probe), the
+# interface kernels of one step
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests -m "gpu and not slow" -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 timeout 900 python bench.py > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
