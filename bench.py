@@ -269,8 +269,7 @@ def run_thermo(args):
                          else "working set fits L2 (no flush; small config)",
                    "parallelism": (f"scenarios sharded over {world} ranks" if sharded else
                                    "replicas only" if world > 1 else "single GPU"),
-                   "cg_iters_per_step": float(iters.mean()),
-                   "iface_overlapped_with_solve": bool(st["overlap"])},
+                   "cg_iters_per_step": float(iters.mean())},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": "k_cg_step (persistent Jacobi-PCG, one launch per step)",
                      "peak_kind": peak_kind, "achieved_vs_8TBs": achieved / 8000.0,

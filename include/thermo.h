@@ -184,7 +184,6 @@ typedef struct {
     int32_t solve_grid;              /* CTAs of the persistent CG kernel */
     int32_t solve_block;             /* threads per CTA */
     int32_t launches_per_step;       /* kernels one implicit-Euler step launches (interface + solve) */
-    int32_t overlap;                 /* 1: interface assembly of step n+1 overlaps the solve of step n */
 } thermo_stats;
 
 int thermo_get_stats(const void *ctx, thermo_stats *out);

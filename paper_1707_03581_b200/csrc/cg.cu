@@ -961,7 +961,7 @@ int cg_launch_solve(Ctx &c, const double *x0, double *x, const double *rhs, cons
     return 0;
 }
 
-int cg_launch_step(Ctx &c, int step, double dt, int buf) {
+int cg_launch_step(Ctx &c, int step, double dt) {
     CGParams P;
     memset(&P, 0, sizeof P);
     P.N = c.N;
@@ -978,11 +978,11 @@ int cg_launch_step(Ctx &c, int step, double dt, int buf) {
     P.nA = c.nA;
     P.if_rows = c.d_if_rows;
     P.slice_if = c.d_slice_if;
-    P.ell_cnt = buf ? c.d_ell_cnt1 : c.d_ell_cnt;
-    P.ell_col = buf ? c.d_ell_col1 : c.d_ell_col;
-    P.ell_val = buf ? c.d_ell_val1 : c.d_ell_val;
-    P.if_b = buf ? c.d_if_b1 : c.d_if_b;
-    P.if_phi = buf ? c.d_if_phi1 : c.d_if_phi;
+    P.ell_cnt = c.d_ell_cnt;
+    P.ell_col = c.d_ell_col;
+    P.ell_val = c.d_ell_val;
+    P.if_b = c.d_if_b;
+    P.if_phi = c.d_if_phi;
     P.T_in = c.d_T[(c.cur + step) & 1];
     P.T_out = c.d_T[(c.cur + step + 1) & 1];
     P.z = c.d_z;

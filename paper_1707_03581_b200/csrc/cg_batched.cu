@@ -44,12 +44,6 @@ namespace thermo {
 #define CGB_MAXS 64
 #define CGB_NV 4   // reduction values per column and phase (max)
 
-// windowed variant (k_cgb_step<true>): 2 groups of 8 consumer warps + 1 producer warp
-#define CGW_NCW 8
-#define CGW_WARPS 17
-#define CGW_BLOCK (32 * CGW_WARPS)
-#define CGW_MAXR 16     // window runs per chunk (one per producer lane)
-#define CGW_HDR 128     // stage header bytes: [0] window index of the chunk's first row, [1] slice width
 
 struct CGBParams {
     int64_t N, nslices;
@@ -72,18 +66,6 @@ struct CGBParams {
     double dt, rtol2;
     int maxit, step;
     unsigned long long *trace;   // optional: %globaltimer after every grid barrier (CTA 0)
-    int contiguous;              // 1: CTA b sweeps one contiguous block of row pairs (L1 reuse of
-                                 // the gathered neighbour rows), 0: row pairs dealt round-robin
-    // windowed sweeps: chunk = CR consecutive rows of one slice; the producer bulk-copies the
-    // chunk's slice (values, window-local columns, interface map) and its column window (<=
-    // CGW_MAXR runs of whole block-vector rows) into one stage of an NS-stage ring
-    int CR, NS, wcap;
-    int64_t nchunks;
-    uint32_t stage_bytes, off_col, off_if, off_w1, off_w2;
-    const int2 *wruns;           // [nchunks][CGW_MAXR] (first row, rows)
-    const int32_t *wnruns;       // [nchunks]
-    const int32_t *wlown;        // [nchunks] window index of the chunk's first row
-    const uint16_t *wcol;        // [nnz_pad] window-local column of every stored entry
 };
 
 __device__ __forceinline__ int64_t ellb(const CGBParams &P, int s, int c, int k) {
@@ -330,172 +312,9 @@ __device__ __forceinline__ void cgb_update(const CGBParams &P, const double (&al
     }
 }
 
-// ---------------------------------------------------------------------------------
-// windowed sweeps (TMA ring)
-// ---------------------------------------------------------------------------------
-struct WinRing {
-    uint64_t *full, *empty;
-    unsigned char *stage;
-    uint32_t n;   // stages passed through the ring so far (same count in every warp)
-};
-
-struct WinMeta {
-    int64_t base;
-    int w, s, lown, nruns;
-    int2 run;
-};
-
-__device__ __forceinline__ WinMeta win_meta(const CGBParams &P, int64_t ch, int lane) {
-    WinMeta m;
-    m.base = 0; m.w = 0; m.s = 0; m.lown = 0; m.nruns = 0;
-    m.run = make_int2(0, 0);
-    if (ch >= P.nchunks) return m;
-    m.s = (int)((ch * P.CR) >> 5);
-    m.base = P.slice_ptr[m.s];
-    m.w = (int)((P.slice_ptr[m.s + 1] - m.base) >> 5);
-    m.lown = P.wlown[ch];
-    m.nruns = P.wnruns[ch];
-    if (lane < CGW_MAXR) m.run = P.wruns[ch * CGW_MAXR + lane];
-    return m;
-}
-
-// Producer warp: CTA b streams its chunks b, b + G, ... (static order) into the ring.
-template <int NVEC>
-__device__ __forceinline__ void win_produce(const CGBParams &P, WinRing &R, const double *v1, const double *v2,
-                                            int lane) {
-    const int G = gridDim.x;
-    const uint32_t RB = (uint32_t)P.SP * 8u;
-    // the vectors were written by generic stores of other CTAs before the last grid barrier,
-    // and the ring's first stage served as reduction scratch: order both before the copies
-    asm volatile("fence.proxy.async.global;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    int64_t ch = blockIdx.x;
-    WinMeta cur = win_meta(P, ch, lane), nxt = win_meta(P, ch + G, lane);
-    uint32_t n = R.n;
-    for (; ch < P.nchunks; ch += G, ++n) {
-        const WinMeta m2 = win_meta(P, ch + 2 * (int64_t)G, lane);   // in flight meanwhile
-        const uint32_t st = n % (uint32_t)P.NS, ph = (n / (uint32_t)P.NS) & 1u;
-        const int len = lane < cur.nruns ? cur.run.y : 0;
-        int off = len;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, off, o);
-            if (lane >= o) off += y;
-        }
-        const int tot = __shfl_sync(0xffffffffu, off, 31);
-        off -= len;
-        unsigned char *stg = R.stage + (size_t)st * P.stage_bytes;
-        if (lane == 0) {
-            mbar_wait(&R.empty[st], ph ^ 1u);
-            int *hdr = reinterpret_cast<int *>(stg);
-            hdr[0] = cur.lown;
-            hdr[1] = cur.w;
-            const uint32_t bytes = (uint32_t)cur.w * 32u * 10u + 128u + (uint32_t)NVEC * (uint32_t)tot * RB;
-            mbar_arrive_expect_tx(&R.full[st], bytes);
-        }
-        __syncwarp();
-        if (lane == 0) bulk_g2s_nohint(stg + CGW_HDR, P.val + cur.base, (uint32_t)cur.w * 256u, &R.full[st]);
-        if (lane == 1) bulk_g2s_nohint(stg + P.off_col, P.wcol + cur.base, (uint32_t)cur.w * 64u, &R.full[st]);
-        if (lane == 2) bulk_g2s_nohint(stg + P.off_if, P.if_of_row + 32 * (int64_t)cur.s, 128u, &R.full[st]);
-        if (len > 0) {
-            bulk_g2s_nohint(stg + P.off_w1 + (size_t)off * RB, v1 + (int64_t)cur.run.x * P.SP, (uint32_t)len * RB,
-                            &R.full[st]);
-            if (NVEC == 2)
-                bulk_g2s_nohint(stg + P.off_w2 + (size_t)off * RB, v2 + (int64_t)cur.run.x * P.SP,
-                                (uint32_t)len * RB, &R.full[st]);
-        }
-        cur = nxt;
-        nxt = m2;
-    }
-}
-
-// Consumer warp: 16 consumer warps form NG = 16 / NCW groups of NCW = min(CR, 8) warps; group
-// g takes the chunks j = g, g + NG, ... of the CTA, warp r of a group the rows r, r + NCW, ...
-// of a chunk: body(i, rr, w, vals, cols, ifmap, win1, win2, own, SPh) per row.
-template <class Body>
-__device__ __forceinline__ void win_consume(const CGBParams &P, WinRing &R, int warp, int lane, Body body) {
-    const int NCW = P.CR < CGW_NCW ? P.CR : CGW_NCW, NG = 2 * CGW_NCW / NCW;
-    const int G = gridDim.x, g = warp / NCW, r = warp % NCW;
-    const int64_t b = blockIdx.x;
-    const int64_t nloc = b < P.nchunks ? (P.nchunks - 1 - b) / G + 1 : 0;
-    const int SPh = P.SP >> 1;
-    for (int64_t j = g; j < nloc; j += NG) {
-        const uint32_t n = R.n + (uint32_t)j;
-        const uint32_t st = n % (uint32_t)P.NS, ph = (n / (uint32_t)P.NS) & 1u;
-        mbar_wait(&R.full[st], ph);
-        const unsigned char *stg = R.stage + (size_t)st * P.stage_bytes;
-        const int *hdr = reinterpret_cast<const int *>(stg);
-        const int lown = hdr[0], w = hdr[1];
-        const double *vals = reinterpret_cast<const double *>(stg + CGW_HDR);
-        const uint16_t *cols = reinterpret_cast<const uint16_t *>(stg + P.off_col);
-        const int32_t *ifmap = reinterpret_cast<const int32_t *>(stg + P.off_if);
-        const double2 *w1 = reinterpret_cast<const double2 *>(stg + P.off_w1);
-        const double2 *w2 = reinterpret_cast<const double2 *>(stg + P.off_w2);
-        const int64_t row0 = (b + j * G) * P.CR;
-        for (int m = r; m < P.CR; m += NCW) {
-            const int64_t i = row0 + m;
-            if (i >= P.N) break;
-            body(i, (int)(i & 31), w, vals, cols, ifmap, w1, w2, (lown + m) * SPh, SPh);
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&R.empty[st]);
-    }
-}
-
-// sum_k val_k (w1[col_k] + beta w2[col_k]) of one row from the stage (same fma order as row_spmm2)
-template <bool kTwo>
-__device__ __forceinline__ double2 win_row(const double *vals, const uint16_t *cols, int rr, int w, const double2 *w1,
-                                           const double2 *w2, int SPh, int ln, double2 beta) {
-    double2 acc = make_double2(0.0, 0.0);
-    int k = 0;
-    for (; k + 4 <= w; k += 4) {
-        double2 y[4];
-        double v[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int c = cols[(k + u) * 32 + rr];
-            v[u] = vals[(k + u) * 32 + rr];
-            const double2 a = w1[c * SPh + ln];
-            if (kTwo) {
-                const double2 bb = w2[c * SPh + ln];
-                y[u] = make_double2(fma(beta.x, bb.x, a.x), fma(beta.y, bb.y, a.y));
-            } else {
-                y[u] = a;
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            acc.x = fma(v[u], y[u].x, acc.x);
-            acc.y = fma(v[u], y[u].y, acc.y);
-        }
-    }
-    for (; k < w; ++k) {
-        const int c = cols[k * 32 + rr];
-        const double v = vals[k * 32 + rr];
-        double2 y = w1[c * SPh + ln];
-        if (kTwo) {
-            const double2 bb = w2[c * SPh + ln];
-            y = make_double2(fma(beta.x, bb.x, y.x), fma(beta.y, bb.y, y.y));
-        }
-        acc.x = fma(v, y.x, acc.x);
-        acc.y = fma(v, y.y, acc.y);
-    }
-    return acc;
-}
-
-template <bool WIN>
-__global__ void __launch_bounds__(WIN ? CGW_BLOCK : CGB_BLOCK, 1) k_cgb_step(CGBParams P) {
-    constexpr int NW = WIN ? CGW_WARPS : CGB_WARPS;
-    __shared__ double sm_static[WIN ? 1 : CGB_WARPS * CGB_NV * 64];
-    extern __shared__ __align__(128) unsigned char dsm[];
-    // WIN: [full[NS] | empty[NS] | pad to 128 | NS stages]; the reduction scratch aliases the
-    // stages (the ring is drained at every reduction)
-    WinRing R;
-    R.full = reinterpret_cast<uint64_t *>(dsm);
-    R.empty = R.full + 8;
-    R.stage = dsm + 128;
-    R.n = 0;
-    double *sm = WIN ? reinterpret_cast<double *>(dsm + 128) : sm_static;
+__global__ void __launch_bounds__(CGB_BLOCK, 1) k_cgb_step(CGBParams P) {
+    constexpr int NW = CGB_WARPS;
+    __shared__ double sm[CGB_WARPS * CGB_NV * 64];
     if (P.status[0] || P.status[1]) {
         if (!P.status[0] && blockIdx.x == 0 && threadIdx.x == 0) {
             P.status[0] = 2;
@@ -512,28 +331,9 @@ __global__ void __launch_bounds__(WIN ? CGW_BLOCK : CGB_BLOCK, 1) k_cgb_step(CGB
     const int gw = blockIdx.x * NW + warp, TW = gridDim.x * NW;
     const bool col_ok[2] = {2 * lane < P.S, 2 * lane + 1 < P.S};
     const bool lane_ok = 2 * lane < P.SP;   // lanes past the row stride touch no memory
-    const int ln = lane_ok ? lane : 0;
-    if (WIN) {
-        if (threadIdx.x < P.NS) {
-            mbar_init(&R.full[threadIdx.x], 1);
-            mbar_init(&R.empty[threadIdx.x], P.CR < CGW_NCW ? P.CR : CGW_NCW);
-        }
-        fence_mbar_init();
-        __syncthreads();
-    }
-    const int64_t nloc = WIN ? (blockIdx.x < P.nchunks ? (P.nchunks - 1 - blockIdx.x) / gridDim.x + 1 : 0) : 0;
-
     // ---- phase 0: r0 = b - K~ x0, z0 = D^{-1} r0 per column
     double v0[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};   // b.b, r.r, r.z, |Gamma_R| (scenario 0)
     const int64_t npairs = P.nslices * 16;   // units: (slice, row pair)
-    // this warp's units: u0, u0 + ust, ... < uend
-    int64_t u0 = gw, ust = TW, uend = npairs;
-    if (P.contiguous) {
-        const int64_t upc = (npairs + gridDim.x - 1) / gridDim.x;
-        u0 = (int64_t)blockIdx.x * upc + warp;
-        ust = NW;
-        uend = min(npairs, (int64_t)(blockIdx.x + 1) * upc);
-    }
     // epilogue of one row: ax = (K~ x0)_i without the interface part, Ti = x0_i
     auto fin0 = [&](int64_t i, int ik, double2 ax, double2 Ti, double2 di) {
         double2 bg = make_double2(0.0, 0.0);
@@ -566,41 +366,24 @@ __global__ void __launch_bounds__(WIN ? CGW_BLOCK : CGB_BLOCK, 1) k_cgb_step(CGB
             v0[2][1] = fma(rr.y, zz.y, v0[2][1]);
         }
     };
-    if constexpr (WIN) {
-        if (warp == CGW_WARPS - 1) {
-            win_produce<1>(P, R, P.T_in, nullptr, lane);
-        } else {
-            win_consume(P, R, warp, lane, [&](int64_t i, int rr, int w, const double *vals, const uint16_t *cols,
-                                              const int32_t *ifmap, const double2 *w1, const double2 *, int own,
-                                              int SPh) {
-                const double2 di = lane_ok ? reinterpret_cast<const double2 *>(P.DinvS + i * P.SP)[lane]
-                                           : make_double2(0.0, 0.0);
-                const double2 ax = win_row<false>(vals, cols, rr, w, w1, nullptr, SPh, ln, make_double2(0, 0));
-                fin0(i, ifmap[rr], ax, w1[own + ln], di);
-            });
-        }
-        R.n += (uint32_t)nloc;
-        __syncthreads();   // ring drained before its memory serves as reduction scratch
-    } else {
-        unit_loop(P, uend, u0, ust, lane, [&](int64_t u, int64_t base, int w, int rA, bool validB, int ikA,
-                                               int ikB, int cl, double vl) {
-            const int64_t iA = 32 * (u >> 4) + rA;
-            double2 Tr[2], dr[2];   // own rows, loaded ahead of the gathers
-            if (lane_ok) {
-                Tr[0] = reinterpret_cast<const double2 *>(P.T_in + iA * P.SP)[lane];
-                dr[0] = reinterpret_cast<const double2 *>(P.DinvS + iA * P.SP)[lane];
-                if (validB) {
-                    Tr[1] = reinterpret_cast<const double2 *>(P.T_in + (iA + 1) * P.SP)[lane];
-                    dr[1] = reinterpret_cast<const double2 *>(P.DinvS + (iA + 1) * P.SP)[lane];
-                }
+    unit_loop(P, npairs, gw, TW, lane, [&](int64_t u, int64_t base, int w, int rA, bool validB, int ikA,
+                                           int ikB, int cl, double vl) {
+        const int64_t iA = 32 * (u >> 4) + rA;
+        double2 Tr[2], dr[2];   // own rows, loaded ahead of the gathers
+        if (lane_ok) {
+            Tr[0] = reinterpret_cast<const double2 *>(P.T_in + iA * P.SP)[lane];
+            dr[0] = reinterpret_cast<const double2 *>(P.DinvS + iA * P.SP)[lane];
+            if (validB) {
+                Tr[1] = reinterpret_cast<const double2 *>(P.T_in + (iA + 1) * P.SP)[lane];
+                dr[1] = reinterpret_cast<const double2 *>(P.DinvS + (iA + 1) * P.SP)[lane];
             }
-            double2 axr[2];
-            row_spmm2<false>(P, base, w, rA, validB, cl, vl, P.T_in, nullptr, make_double2(0, 0), lane, axr[0],
-                             axr[1]);
-            fin0(iA, ikA, axr[0], Tr[0], dr[0]);
-            if (validB) fin0(iA + 1, ikB, axr[1], Tr[1], dr[1]);
-        });
-    }
+        }
+        double2 axr[2];
+        row_spmm2<false>(P, base, w, rA, validB, cl, vl, P.T_in, nullptr, make_double2(0, 0), lane, axr[0],
+                         axr[1]);
+        fin0(iA, ikA, axr[0], Tr[0], dr[0]);
+        if (validB) fin0(iA + 1, ikB, axr[1], Tr[1], dr[1]);
+    });
     double t0[4][2];
     cgb_reduce<4, NW>(v0, sm, P.partials, grid, t0);
     if (tr_on) P.trace[ntr++] = gtimer();
@@ -636,51 +419,28 @@ __global__ void __launch_bounds__(WIN ? CGW_BLOCK : CGB_BLOCK, 1) k_cgb_step(CGB
             vs[0][0] = fma(pi.x, acc.x, vs[0][0]);
             vs[0][1] = fma(pi.y, acc.y, vs[0][1]);
         };
-        if constexpr (WIN) {
-            if (warp == CGW_WARPS - 1) {
-                if (first) win_produce<1>(P, R, P.z, nullptr, lane);
-                else win_produce<2>(P, R, P.z, pold, lane);
-            } else {
-                win_consume(P, R, warp, lane, [&](int64_t i, int rr, int w, const double *vals, const uint16_t *cols,
-                                                  const int32_t *ifmap, const double2 *w1, const double2 *w2, int own,
-                                                  int SPh) {
-                    double2 acc, pi = w1[own + ln];
-                    if (first) {
-                        acc = win_row<false>(vals, cols, rr, w, w1, nullptr, SPh, ln, b2);
-                    } else {
-                        acc = win_row<true>(vals, cols, rr, w, w1, w2, SPh, ln, b2);
-                        const double2 po = w2[own + ln];
-                        pi = make_double2(fma(b2.x, po.x, pi.x), fma(b2.y, po.y, pi.y));
-                    }
-                    finS(i, ifmap[rr], acc, pi);
-                });
+        unit_loop(P, npairs, gw, TW, lane, [&](int64_t u, int64_t base, int w, int rA, bool validB, int ikA,
+                                               int ikB, int cl, double vl) {
+            const int64_t iA = 32 * (u >> 4) + rA;
+            double2 zr[2], pr[2];   // own rows, loaded ahead of the gathers
+            if (lane_ok) {
+                zr[0] = reinterpret_cast<const double2 *>(P.z + iA * P.SP)[lane];
+                if (!first) pr[0] = reinterpret_cast<const double2 *>(pold + iA * P.SP)[lane];
+                if (validB) {
+                    zr[1] = reinterpret_cast<const double2 *>(P.z + (iA + 1) * P.SP)[lane];
+                    if (!first) pr[1] = reinterpret_cast<const double2 *>(pold + (iA + 1) * P.SP)[lane];
+                }
             }
-            R.n += (uint32_t)nloc;
-            __syncthreads();
-        } else {
-            unit_loop(P, uend, u0, ust, lane, [&](int64_t u, int64_t base, int w, int rA, bool validB, int ikA,
-                                                   int ikB, int cl, double vl) {
-                const int64_t iA = 32 * (u >> 4) + rA;
-                double2 zr[2], pr[2];   // own rows, loaded ahead of the gathers
-                if (lane_ok) {
-                    zr[0] = reinterpret_cast<const double2 *>(P.z + iA * P.SP)[lane];
-                    if (!first) pr[0] = reinterpret_cast<const double2 *>(pold + iA * P.SP)[lane];
-                    if (validB) {
-                        zr[1] = reinterpret_cast<const double2 *>(P.z + (iA + 1) * P.SP)[lane];
-                        if (!first) pr[1] = reinterpret_cast<const double2 *>(pold + (iA + 1) * P.SP)[lane];
-                    }
-                }
-                double2 accr[2];
-                if (first) row_spmm2<false>(P, base, w, rA, validB, cl, vl, P.z, nullptr, b2, lane, accr[0], accr[1]);
-                else row_spmm2<true>(P, base, w, rA, validB, cl, vl, P.z, pold, b2, lane, accr[0], accr[1]);
-                for (int h = 0; h < 2; ++h) {
-                    if (h == 1 && !validB) break;
-                    double2 pi = zr[h];
-                    if (!first && lane_ok) pi = make_double2(fma(b2.x, pr[h].x, pi.x), fma(b2.y, pr[h].y, pi.y));
-                    finS(iA + h, h ? ikB : ikA, accr[h], pi);
-                }
-            });
-        }
+            double2 accr[2];
+            if (first) row_spmm2<false>(P, base, w, rA, validB, cl, vl, P.z, nullptr, b2, lane, accr[0], accr[1]);
+            else row_spmm2<true>(P, base, w, rA, validB, cl, vl, P.z, pold, b2, lane, accr[0], accr[1]);
+            for (int h = 0; h < 2; ++h) {
+                if (h == 1 && !validB) break;
+                double2 pi = zr[h];
+                if (!first && lane_ok) pi = make_double2(fma(b2.x, pr[h].x, pi.x), fma(b2.y, pr[h].y, pi.y));
+                finS(iA + h, h ? ikB : ikA, accr[h], pi);
+            }
+        });
         double tpq[1][2];
         cgb_reduce<1, NW>(vs, sm, P.partials, grid, tpq);
         if (tr_on && ntr < 1000) P.trace[ntr++] = gtimer();
@@ -735,143 +495,14 @@ __global__ void k_dinv_broadcast(const double *Dinv, int64_t N, int S, int SP, d
     DinvS[t] = s < S ? Dinv[i] : 1.0;
 }
 
-// Column windows of the windowed sweeps (host, once per context): chunk = CR consecutive rows
-// of one slice (CR = 8 for 64 columns: a window then holds ~64 block-vector rows = 64 KB per
-// vector); the sorted column set of the chunk is cut into runs of consecutive rows, the
-// closest runs merged until at most CGW_MAXR remain.  Returns 1 if the windows fit the
-// shared-memory budget (else the register-gather kernel is used), < 0 on error.
-static int cgw_build(Ctx &c) {
-    const int SP = c.SP;
-    int CR = SP >= 48 ? 8 : (SP >= 24 ? 16 : 32);
-    if (const char *e = getenv("THERMO_CGB_CR")) {   // tuning override: 4, 8, 16 or 32
-        const int v = atoi(e);
-        if (v == 4 || v == 8 || v == 16 || v == 32) CR = v;
-    }
-    const int64_t N = c.N, nsl = c.nslices;
-    std::vector<int64_t> sp(nsl + 1);
-    std::vector<int32_t> col((size_t)c.nnz_pad);
-    CK(cudaMemcpyAsync(sp.data(), c.d_slice_ptr, sizeof(int64_t) * (nsl + 1), cudaMemcpyDeviceToHost, c.stream));
-    CK(cudaMemcpyAsync(col.data(), c.d_col, sizeof(int32_t) * col.size(), cudaMemcpyDeviceToHost, c.stream));
-    CK(cudaStreamSynchronize(c.stream));
-    int wmax = 0;
-    for (int64_t s = 0; s < nsl; ++s) wmax = std::max(wmax, (int)((sp[s + 1] - sp[s]) >> 5));
-    const int64_t nch = (N + CR - 1) / CR;
-    std::vector<int2> runs((size_t)nch * CGW_MAXR, make_int2(0, 0));
-    std::vector<int32_t> nruns(nch), lown(nch);
-    std::vector<uint16_t> wcol(col.size(), 0);
-    std::vector<int32_t> cs;
-    std::vector<int2> rv;
-    int wcap = 0;
-    for (int64_t ch = 0; ch < nch; ++ch) {
-        const int64_t r0 = ch * CR, r1 = std::min(r0 + CR, N), s = r0 >> 5, base = sp[s];
-        const int w = (int)((sp[s + 1] - base) >> 5);
-        cs.clear();
-        for (int64_t i = r0; i < r1; ++i)
-            for (int k = 0; k < w; ++k) cs.push_back(col[base + 32 * k + (i & 31)]);
-        std::sort(cs.begin(), cs.end());
-        cs.erase(std::unique(cs.begin(), cs.end()), cs.end());
-        rv.clear();
-        for (int32_t x : cs) {
-            if (!rv.empty() && rv.back().x + rv.back().y == x) rv.back().y++;
-            else rv.push_back(make_int2(x, 1));
-        }
-        while ((int)rv.size() > CGW_MAXR) {   // bridge the smallest gap
-            size_t best = 0;
-            int64_t bg = INT64_MAX;
-            for (size_t q = 0; q + 1 < rv.size(); ++q) {
-                const int64_t g = (int64_t)rv[q + 1].x - (rv[q].x + rv[q].y);
-                if (g < bg) { bg = g; best = q; }
-            }
-            rv[best].y = rv[best + 1].x + rv[best + 1].y - rv[best].x;
-            rv.erase(rv.begin() + best + 1);
-        }
-        int tot = 0;
-        std::vector<int> off(rv.size());
-        for (size_t q = 0; q < rv.size(); ++q) { off[q] = tot; tot += rv[q].y; }
-        if (tot > 65535) return 0;
-        wcap = std::max(wcap, tot);
-        auto local = [&](int32_t x) {
-            size_t q = std::upper_bound(rv.begin(), rv.end(), x, [](int32_t v, const int2 &r) { return v < r.x; }) -
-                       rv.begin() - 1;
-            return off[q] + (x - rv[q].x);
-        };
-        nruns[ch] = (int)rv.size();
-        for (size_t q = 0; q < rv.size(); ++q) runs[ch * CGW_MAXR + q] = rv[q];
-        lown[ch] = local((int32_t)r0);
-        for (int64_t i = r0; i < r1; ++i)
-            for (int k = 0; k < w; ++k) {
-                const int64_t e = base + 32 * k + (i & 31);
-                wcol[e] = (uint16_t)local(col[e]);
-            }
-    }
-    // stage layout: header | values [wmax][32] | columns [wmax][32] | interface map [32] | windows
-    const size_t RB = (size_t)SP * 8;
-    wcap = (wcap + 7) & ~7;
-    const size_t off_col = CGW_HDR + (size_t)wmax * 32 * 8;
-    const size_t off_if = off_col + (((size_t)wmax * 32 * 2 + 127) & ~(size_t)127);
-    const size_t off_w1 = off_if + 128;
-    const size_t off_w2 = off_w1 + (size_t)wcap * RB;
-    const size_t stage = (off_w2 + (size_t)wcap * RB + 127) & ~(size_t)127;
-    const size_t budget = 227 * 1024 - 128;
-    const size_t red = (size_t)CGW_WARPS * CGB_NV * 64 * 8;
-    int NS = (int)std::min<size_t>(8, budget / stage);
-    if (const char *e = getenv("THERMO_CGB_NS")) NS = std::min(NS, std::max(2, atoi(e)));
-    // a consumer group waits on parity (n / NS) & 1 of its stage: with more groups than
-    // stages - 1 a group could see the phase of the chunk NS earlier, so NS >= groups + 1
-    const int ngroups = 2 * CGW_NCW / (CR < CGW_NCW ? CR : CGW_NCW);
-    if (NS < ngroups + 1) return 0;
-    if (NS < 2 || std::max((size_t)NS * stage, red) > budget) return 0;
-    c.cgw_CR = CR;
-    c.cgw_NS = NS;
-    c.cgw_wcap = wcap;
-    c.cgw_nchunks = nch;
-    c.cgw_stage = (uint32_t)stage;
-    c.cgw_off[0] = (uint32_t)off_col;
-    c.cgw_off[1] = (uint32_t)off_if;
-    c.cgw_off[2] = (uint32_t)off_w1;
-    c.cgw_off[3] = (uint32_t)off_w2;
-    c.cgw_smem = 128 + std::max((size_t)NS * stage, red);
-    CK(cudaMalloc(&c.d_chunk_runs, sizeof(int2) * runs.size()));
-    CK(cudaMalloc(&c.d_chunk_nruns, sizeof(int32_t) * nch));
-    CK(cudaMalloc(&c.d_chunk_lown, sizeof(int32_t) * nch));
-    CK(cudaMalloc(&c.d_lcol, sizeof(uint16_t) * wcol.size() + 64));
-    CK(cudaMemcpyAsync(c.d_chunk_runs, runs.data(), sizeof(int2) * runs.size(), cudaMemcpyHostToDevice, c.stream));
-    CK(cudaMemcpyAsync(c.d_chunk_nruns, nruns.data(), sizeof(int32_t) * nch, cudaMemcpyHostToDevice, c.stream));
-    CK(cudaMemcpyAsync(c.d_chunk_lown, lown.data(), sizeof(int32_t) * nch, cudaMemcpyHostToDevice, c.stream));
-    CK(cudaMemcpyAsync(c.d_lcol, wcol.data(), sizeof(uint16_t) * wcol.size(), cudaMemcpyHostToDevice, c.stream));
-    CK(cudaStreamSynchronize(c.stream));   // host vectors die here
-    return 1;
-}
-
 int cgb_setup(Ctx &c) {
     if (c.S > CGB_MAXS) { c.err = "at most 64 scenarios per context"; return -1; }
     if (int rc = build_if_of_row(c)) return rc;
-    // THERMO_CGB_KIND=1 selects the windowed sweeps; measured slower than the register gathers
-    // on cfg 4, so the register kernel is the default
-    const char *kind = getenv("THERMO_CGB_KIND");
-    c.cgw_on = 0;
-    if (kind && atoi(kind) == 1) {
-        const int r = cgw_build(c);
-        if (r < 0) return r;
-        c.cgw_on = r;
-    }
     int per_sm = 0;
-    if (c.cgw_on) {
-        CK(cudaFuncSetAttribute((const void *)k_cgb_step<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)c.cgw_smem));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cgb_step<true>, CGW_BLOCK, c.cgw_smem));
-        c.cg_block = CGW_BLOCK;
-    } else {
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cgb_step<false>, CGB_BLOCK, 0));
-        c.cg_block = CGB_BLOCK;
-    }
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cgb_step, CGB_BLOCK, 0));
     if (per_sm < 1) { c.err = "batched CG kernel cannot be resident"; return -3; }
-    c.cg_grid = (c.cgw_on ? 1 : per_sm) * c.num_sms;
-    const char *ord = getenv("THERMO_CGB_ORDER");
-    c.cgb_contiguous = ord ? atoi(ord) : 0;   // contiguous blocks measured 3.5x slower (L2 thrash)
-    if (getenv("THERMO_CG_TRACE"))
-        fprintf(stderr, "[thermo] batched CG: %s, rows/chunk %d, stages %d, window rows %d, stage %u B\n",
-                c.cgw_on ? "windows" : "register gathers", c.cgw_CR, c.cgw_NS, c.cgw_wcap, c.cgw_stage);
+    c.cg_block = CGB_BLOCK;
+    c.cg_grid = per_sm * c.num_sms;
     CK(cudaMalloc(&c.d_partials, sizeof(double) * (size_t)CGB_NV * 64 * c.cg_grid));
     CK(cudaMalloc(&c.d_DinvS, sizeof(double) * (size_t)c.N * c.SP + 16));
     return 0;
@@ -925,28 +556,8 @@ int cgb_launch_step(Ctx &c, int step, double dt) {
     P.maxit = c.maxit > 0 ? c.maxit : (int)std::min<int64_t>(10 * c.N, 10000);
     P.step = step;
     P.trace = c.d_trace;
-    P.contiguous = c.cgb_contiguous;
     void *args[] = {&P};
-    if (c.cgw_on) {
-        P.CR = c.cgw_CR;
-        P.NS = c.cgw_NS;
-        P.wcap = c.cgw_wcap;
-        P.nchunks = c.cgw_nchunks;
-        P.stage_bytes = c.cgw_stage;
-        P.off_col = c.cgw_off[0];
-        P.off_if = c.cgw_off[1];
-        P.off_w1 = c.cgw_off[2];
-        P.off_w2 = c.cgw_off[3];
-        P.wruns = c.d_chunk_runs;
-        P.wnruns = c.d_chunk_nruns;
-        P.wlown = c.d_chunk_lown;
-        P.wcol = c.d_lcol;
-        CK(cudaLaunchCooperativeKernel((const void *)k_cgb_step<true>, dim3(c.cg_grid), dim3(c.cg_block), args,
-                                       c.cgw_smem, c.stream));
-    } else {
-        CK(cudaLaunchCooperativeKernel((const void *)k_cgb_step<false>, dim3(c.cg_grid), dim3(c.cg_block), args, 0,
-                                       c.stream));
-    }
+    CK(cudaLaunchCooperativeKernel((const void *)k_cgb_step, dim3(c.cg_grid), dim3(c.cg_block), args, 0, c.stream));
     return 0;
 }
 

@@ -228,14 +228,12 @@ struct IfaceParams {
     double *if_b;             // [S][n_if] dt-free friction source eta/2 int phi
     double *if_phi;           // [S][n_if] int_{Gamma_R} phi
     double *Dinv;             // S == 1: [N] Jacobi inverse diagonal, interface rows rewritten
-    double *if_dinv;          // [n_if] Jacobi inverse of the interface rows (dinv_compact)
+    double *if_dinv;          // (unused)
     double *DinvS;            // S > 1: [N][SP] per-scenario Jacobi inverse diagonal
     int SP;                   // S > 1: row stride of the block vectors (even, >= S)
     int no_dinv;              // 1: leave the Jacobi diagonal alone (MRSDC: f^E is explicit)
     int slot_major;           // 1: batch index = node-time slot, arrays laid out slot by slot
                               // ([s][c][k], [s][k]) so per-slot row loops stay coalesced
-    int dinv_compact;         // 1 (S == 1): write the rows' Jacobi inverses to if_dinv[k] instead of
-                              // Dinv[row] (the overlapped step scatters them before the solve)
     int *status;              // status[1] |= overflow
 };
 

@@ -95,12 +95,6 @@ struct Ctx {
     size_t cg_smem = 0;
     bool cg_tma = false;
     int cg_variant = 0, cg_chunk = 8, cg_debug = 0, cg_prefetch = 0;
-    // batched windowed sweeps (cg_batched.cu); reuse d_chunk_runs / nruns / lown and d_lcol
-    int cgw_on = 0, cgw_CR = 0, cgw_NS = 0, cgw_wcap = 0;
-    int cgb_contiguous = 0;            // batched: contiguous row blocks per CTA (THERMO_CGB_ORDER=1)
-    int64_t cgw_nchunks = 0;
-    uint32_t cgw_stage = 0, cgw_off[4] = {0, 0, 0, 0};
-    size_t cgw_smem = 0;
     int32_t *d_chunk_hi = nullptr;
     uint16_t *d_lcol = nullptr;      // chunk-local 16-bit columns (window kernels)
     int2 *d_chunk_runs = nullptr;    // window runs per chunk
@@ -128,19 +122,12 @@ struct Ctx {
     double *d_if_phi_s = nullptr;
     int mr_nslots = 0, mr_solves = 0;
     bool timing = false;
-    std::vector<cudaEvent_t> events;   // 2 * nsteps + 1 when timing (4 * nsteps overlapped)
-    // overlap of the interface assembly of step n + 1 (side stream, twin output buffer) with
-    // the solve of step n (S == 1, implicit Euler; THERMO_OVERLAP=0 disables)
-    int overlap = 0;
-    cudaStream_t side = nullptr;
+    std::vector<cudaEvent_t> events;   // 2 * nsteps + 1 when timing
     // asynchronous host copies of the state (thermo_get_T_async): a copy stream, and per state
     // buffer the event after which a pending copy has read it
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t ev_ready = nullptr, ev_copy[2] = {nullptr, nullptr};
     int copy_pending[2] = {0, 0};
-    cudaEvent_t ev_if[2] = {nullptr, nullptr}, ev_cg[2] = {nullptr, nullptr}, ev_join = nullptr;
-    int32_t *d_ell_cnt1 = nullptr, *d_ell_col1 = nullptr;
-    double *d_ell_val1 = nullptr, *d_if_b1 = nullptr, *d_if_phi1 = nullptr, *d_if_dinv1 = nullptr;
     PairRec *d_pairs_s = nullptr;        // pair records of the SDC node-time slots
     int32_t *d_pcnt_s = nullptr;
     double ms_iface = 0.0, ms_solve = 0.0;
@@ -165,12 +152,10 @@ int iface_setup(Ctx &c, const double *h_xyz, const std::vector<int32_t> &facesA,
                 const std::vector<int32_t> &facesB);
 void iface_params(Ctx &c, IfaceParams &p, const double *step_sc, double dt);
 int iface_launch(Ctx &c, const IfaceParams &p, cudaStream_t stream = nullptr);
-void iface_params_buf(Ctx &c, IfaceParams &p, int buf);   // overlapped step: output buffer 0 / 1
-int scatter_dinv(Ctx &c, int buf);                          // if_dinv of buffer -> Dinv rows (main stream)
 
 // cg.cu
 int cg_setup(Ctx &c);
-int cg_launch_step(Ctx &c, int step, double dt, int buf = 0);
+int cg_launch_step(Ctx &c, int step, double dt);
 // Solve (M_L - a K_vol [- a K_G]) x = rhs from x0 with the operator currently in d_val (a =
 // built_dt); iface = false: no interface rows.  Iterations / residual to iters_out[slot].
 int cg_launch_solve(Ctx &c, const double *x0, double *x, const double *rhs, const double *Dinv, bool iface,

@@ -460,8 +460,6 @@ __global__ void __launch_bounds__(32 * ROW_WPB) k_rows(IfaceParams P) {
         P.if_b[row_index(P, s, k)] = 0.5 * P.step_sc[4 * s + 2] * phi;
         const double dinv = 1.0 / (P.Dvol[row] + dself);
         if (P.no_dinv) {
-        } else if (P.dinv_compact) {
-            P.if_dinv[k] = dinv;
         } else if (P.S == 1) {
             P.Dinv[row] = dinv;
         } else {
@@ -793,15 +791,6 @@ int iface_setup(Ctx &c, const double *X, const std::vector<int32_t> &fA, const s
     CK(cudaMemsetAsync(c.d_ell_cnt, 0, sizeof(int32_t) * S * nif, c.stream));
     CK(cudaMemsetAsync(c.d_if_b, 0, sizeof(double) * S * nif, c.stream));
     CK(cudaMemsetAsync(c.d_if_phi, 0, sizeof(double) * S * nif, c.stream));
-    if (S == 1) {   // twin buffer of the overlapped implicit-Euler step
-        CK(cudaMalloc(&c.d_ell_cnt1, sizeof(int32_t) * nif));
-        CK(cudaMalloc(&c.d_ell_col1, sizeof(int32_t) * c.cap * nif));
-        CK(cudaMalloc(&c.d_ell_val1, sizeof(double) * c.cap * nif));
-        CK(cudaMalloc(&c.d_if_b1, sizeof(double) * nif));
-        CK(cudaMalloc(&c.d_if_phi1, sizeof(double) * nif));
-        CK(cudaMalloc(&c.d_if_dinv1, sizeof(double) * nif));
-        CK(cudaMemsetAsync(c.d_ell_cnt1, 0, sizeof(int32_t) * nif, c.stream));
-    }
     return 0;
 }
 
@@ -840,31 +829,6 @@ void iface_params(Ctx &c, IfaceParams &P, const double *step_sc, double dt) {
     P.DinvS = c.d_DinvS;
     P.SP = c.SP;
     P.status = c.d_status;
-}
-
-// Interface output buffer `buf` of the overlapped implicit-Euler step (S == 1): buffer 0 is the
-// one every other path uses, buffer 1 its twin; the Jacobi rows go to the buffer's if_dinv.
-void iface_params_buf(Ctx &c, IfaceParams &P, int buf) {
-    P.ell_cnt = buf ? c.d_ell_cnt1 : c.d_ell_cnt;
-    P.ell_col = buf ? c.d_ell_col1 : c.d_ell_col;
-    P.ell_val = buf ? c.d_ell_val1 : c.d_ell_val;
-    P.if_b = buf ? c.d_if_b1 : c.d_if_b;
-    P.if_phi = buf ? c.d_if_phi1 : c.d_if_phi;
-    P.if_dinv = buf ? c.d_if_dinv1 : c.d_if_dinv;
-    P.dinv_compact = 1;
-}
-
-__global__ void k_scatter_dinv(int n_if, const int32_t *if_rows, const double *if_dinv, double *Dinv) {
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k < n_if) Dinv[if_rows[k]] = if_dinv[k];
-}
-
-int scatter_dinv(Ctx &c, int buf) {
-    if (c.n_if == 0) return 0;
-    k_scatter_dinv<<<(unsigned)((c.n_if + 255) / 256), 256, 0, c.stream>>>(c.n_if, c.d_if_rows,
-                                                                           buf ? c.d_if_dinv1 : c.d_if_dinv, c.d_Dinv);
-    CK(cudaGetLastError());
-    return 0;
 }
 
 int iface_launch(Ctx &c, const IfaceParams &P, cudaStream_t stream) {

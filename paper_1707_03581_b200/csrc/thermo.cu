@@ -54,16 +54,13 @@ static void free_ctx(Ctx *c) {
                     c->d_chunk_nruns, c->d_chunk_lown, c->d_trace, c->d_DinvS, c->d_slice_if_zero,
                     c->d_KV, c->d_Dinv_vol, c->d_if_of_row, c->d_mr, c->d_mr_iters, c->d_mr_relres,
                     c->d_ell_cnt_s, c->d_ell_col_s, c->d_ell_val_s, c->d_if_b_s, c->d_if_phi_s, c->d_rhs,
-                    c->d_ell_cnt1, c->d_ell_col1, c->d_ell_val1, c->d_if_b1, c->d_if_phi1, c->d_if_dinv1,
                     c->d_pairs_s, c->d_pcnt_s};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     for (cudaEvent_t e : c->events) cudaEventDestroy(e);
     if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
-    for (cudaEvent_t e : {c->ev_if[0], c->ev_if[1], c->ev_cg[0], c->ev_cg[1], c->ev_join, c->ev_ready, c->ev_copy[0],
-                          c->ev_copy[1]})
+    for (cudaEvent_t e : {c->ev_ready, c->ev_copy[0], c->ev_copy[1]})
         if (e) cudaEventDestroy(e);
-    if (c->side) cudaStreamDestroy(c->side);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     delete c;
 }
@@ -191,19 +188,6 @@ extern "C" int thermo_create_mesh(void **out, const thermo_mesh *fixed, const th
         if (!rc && getenv("THERMO_CG_TRACE")) {
             if (cudaMalloc(&c->d_trace, sizeof(unsigned long long) * 1024) != cudaSuccess) rc = -3;
             else cudaMemsetAsync(c->d_trace, 0, sizeof(unsigned long long) * 1024, c->stream);
-        }
-        if (!rc && c->S == 1 && c->n_if > 0) {
-            // interface assembly of step n + 1 overlapped with the solve of step n: opt-in
-            // (THERMO_OVERLAP=1) -- measured no faster: the side kernels cannot become resident
-            // next to the persistent solve
-            const char *ov = getenv("THERMO_OVERLAP");
-            if (ov && atoi(ov) == 1) {
-                bool ok2 = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) == cudaSuccess;
-                for (cudaEvent_t *e : {&c->ev_if[0], &c->ev_if[1], &c->ev_cg[0], &c->ev_cg[1], &c->ev_join})
-                    ok2 = ok2 && cudaEventCreateWithFlags(e, cudaEventDisableTiming) == cudaSuccess;
-                if (!ok2) rc = -3;
-                else c->overlap = 1;
-            }
         }
         if (!rc && cudaStreamSynchronize(c->stream) != cudaSuccess) { c->err = "CUDA error during create"; rc = -3; }
         if (rc) { g_create_err = c->err; free_ctx(c); return THERMO_ECUDA; }
@@ -441,59 +425,24 @@ extern "C" int thermo_step(void *ctx, double t, double dt, int32_t nsteps) {
             c->failed_scen = -1;
             return THERMO_OK;
         }
-        const bool ovl = c->overlap && S == 1;
         if (c->timing) {
-            while (c->events.size() < (ovl ? 4 * (size_t)nsteps : 2 * (size_t)nsteps + 1)) {
+            while (c->events.size() < 2 * (size_t)nsteps + 1) {
                 cudaEvent_t e;
                 API_CK(cudaEventCreate(&e));
                 c->events.push_back(e);
             }
         }
-        if (ovl) {
-            // The interface terms of step n depend on time only, so step n + 1's are assembled on
-            // the side stream into the twin buffer while step n solves; before each solve the
-            // main stream waits for its buffer and scatters the rows' Jacobi inverses into D^-1.
-            API_CK(cudaEventRecord(c->ev_join, c->stream));   // side starts after earlier work
-            API_CK(cudaStreamWaitEvent(c->side, c->ev_join, 0));
-            auto assemble = [&](int n) -> int {
-                const int b = n & 1;
-                if (n >= 2) API_CK(cudaStreamWaitEvent(c->side, c->ev_cg[b], 0));   // solve n - 2 done with b
-                thermo::IfaceParams P;
-                memset(&P, 0, sizeof P);
-                thermo::iface_params(*c, P, c->d_step_sc + 4 * (size_t)n, dt);
-                thermo::iface_params_buf(*c, P, b);
-                if (c->timing) API_CK(cudaEventRecord(c->events[4 * n], c->side));
-                if (thermo::iface_launch(*c, P, c->side)) return THERMO_ECUDA;
-                if (c->timing) API_CK(cudaEventRecord(c->events[4 * n + 1], c->side));
-                API_CK(cudaEventRecord(c->ev_if[b], c->side));
-                return THERMO_OK;
-            };
-            if (int rc = assemble(0)) return rc;
-            for (int n = 0; n < nsteps; ++n) {
-                if (n + 1 < nsteps)
-                    if (int rc = assemble(n + 1)) return rc;
-                API_CK(cudaStreamWaitEvent(c->stream, c->ev_if[n & 1], 0));
-                API_CK(guard_write(c, (c->cur + n + 1) & 1));
-                if (c->timing) API_CK(cudaEventRecord(c->events[4 * n + 2], c->stream));
-                if (thermo::scatter_dinv(*c, n & 1) || thermo::cg_launch_step(*c, n, dt, n & 1)) return THERMO_ECUDA;
-                if (c->timing) API_CK(cudaEventRecord(c->events[4 * n + 3], c->stream));
-                API_CK(cudaEventRecord(c->ev_cg[n & 1], c->stream));
-            }
-            API_CK(cudaEventRecord(c->ev_join, c->side));   // the caller's stream sees all side work
-            API_CK(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
-        } else {
-            for (int n = 0; n < nsteps; ++n) {
-                thermo::IfaceParams P;
-                memset(&P, 0, sizeof P);
-                thermo::iface_params(*c, P, c->d_step_sc + 4 * (size_t)n * S, dt);
-                if (c->timing) API_CK(cudaEventRecord(c->events[2 * n], c->stream));
-                if (thermo::iface_launch(*c, P)) return THERMO_ECUDA;
-                if (c->timing) API_CK(cudaEventRecord(c->events[2 * n + 1], c->stream));
-                API_CK(guard_write(c, (c->cur + n + 1) & 1));
-                if ((S == 1 ? thermo::cg_launch_step(*c, n, dt) : thermo::cgb_launch_step(*c, n, dt))) return THERMO_ECUDA;
-            }
-            if (c->timing) API_CK(cudaEventRecord(c->events[2 * nsteps], c->stream));
+        for (int n = 0; n < nsteps; ++n) {
+            thermo::IfaceParams P;
+            memset(&P, 0, sizeof P);
+            thermo::iface_params(*c, P, c->d_step_sc + 4 * (size_t)n * S, dt);
+            if (c->timing) API_CK(cudaEventRecord(c->events[2 * n], c->stream));
+            if (thermo::iface_launch(*c, P)) return THERMO_ECUDA;
+            if (c->timing) API_CK(cudaEventRecord(c->events[2 * n + 1], c->stream));
+            API_CK(guard_write(c, (c->cur + n + 1) & 1));
+            if ((S == 1 ? thermo::cg_launch_step(*c, n, dt) : thermo::cgb_launch_step(*c, n, dt))) return THERMO_ECUDA;
         }
+        if (c->timing) API_CK(cudaEventRecord(c->events[2 * nsteps], c->stream));
         int status[8];
         c->h_iters.assign((size_t)nsteps * S, 0);
         c->h_relres.assign((size_t)nsteps * S, 0.0);
@@ -510,13 +459,8 @@ extern "C" int thermo_step(void *ctx, double t, double dt, int32_t nsteps) {
         if (c->timing) {
             for (int n = 0; n < nsteps; ++n) {
                 float a = 0.f, b = 0.f;
-                if (ovl) {
-                    API_CK(cudaEventElapsedTime(&a, c->events[4 * n], c->events[4 * n + 1]));
-                    API_CK(cudaEventElapsedTime(&b, c->events[4 * n + 2], c->events[4 * n + 3]));
-                } else {
-                    API_CK(cudaEventElapsedTime(&a, c->events[2 * n], c->events[2 * n + 1]));
-                    API_CK(cudaEventElapsedTime(&b, c->events[2 * n + 1], c->events[2 * n + 2]));
-                }
+                API_CK(cudaEventElapsedTime(&a, c->events[2 * n], c->events[2 * n + 1]));
+                API_CK(cudaEventElapsedTime(&b, c->events[2 * n + 1], c->events[2 * n + 2]));
                 c->ms_iface += a;
                 c->ms_solve += b;
             }
@@ -665,8 +609,7 @@ extern "C" int thermo_get_stats(const void *ctx, thermo_stats *out) {
     out->ms_solve = c->ms_solve;
     out->solve_grid = c->cg_grid;
     out->solve_block = c->cg_block;
-    out->launches_per_step = 1 + (c->n_if ? 3 : 0) + (c->overlap && c->n_if ? 1 : 0);
-    out->overlap = c->overlap;
+    out->launches_per_step = 1 + (c->n_if ? 3 : 0);
     return THERMO_OK;
 }
 

@@ -85,24 +85,6 @@ def test_huge_step_reaches_two_slab_profile():
     assert np.abs(th.get_T() - expect).max() < 1e-9
 
 
-def test_overlapped_interface_path_is_bitwise_identical(monkeypatch):
-    """The opt-in overlapped step (interface of step n+1 on a side stream into a twin buffer,
-    Jacobi rows scattered before each solve) computes exactly what the sequential step does."""
-    from paper_1707_03581_b200.thermo import Thermo
-    cfg = I.make_config("small", jitter=0.1)
-    T0 = I.initial_field(cfg)[0]
-    seq = Thermo.from_config(cfg)
-    monkeypatch.setenv("THERMO_OVERLAP", "1")
-    ovl = Thermo.from_config(cfg)
-    assert ovl.stats()["overlap"] == 1 and seq.stats()["overlap"] == 0
-    for th in (seq, ovl):
-        th.set_T(T0)
-        th.step(0.0, cfg.dt, 7)
-        th.step(7 * cfg.dt, cfg.dt, 1)
-    assert np.array_equal(seq.get_T(), ovl.get_T())
-    assert seq.stats()["iface_area"] == ovl.stats()["iface_area"]
-
-
 def test_async_host_copies_overlap_safely():
     """thermo_get_T_async: each copy holds the state of the moment it was enqueued, even when the
     following steps overwrite the double-buffered state while the copies are in flight."""

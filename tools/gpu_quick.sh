@@ -2,4 +2,4 @@
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests -m gpu -x -q -k "not slow" > gpurun_out/pytest_gpu.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_gpu.log
 rm -f gpurun_out/probe_exp.log
-for c in cfg4 cfg3; do timeout 300 python tools/probe.py $c 5 2>&1 | grep -E "ms/step|solve" | tail -n 2 >> gpurun_out/probe_exp.log; done
+for c in cfg1 cfg4; do timeout 300 python tools/probe.py $c 5 2>&1 | grep -E "ms/step|solve" | tail -n 2 >> gpurun_out/probe_exp.log; done
