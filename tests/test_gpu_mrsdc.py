@@ -58,3 +58,17 @@ def test_method_switch_and_validation():
     tb = Thermo.from_config(cfgb)
     with pytest.raises(ThermoError):
         tb.set_method("mrsdc", 3, 2, 1)
+
+
+@pytest.mark.slow
+def test_mrsdc_stand_scale_one_step():
+    """BASELINE configs[2] geometry (1.28 M DoF, jittered L-shape stand): one MRSDC(3,2) k = 1
+    step through the C ABI against the oracle's Algorithms 1-2."""
+    from paper_1707_03581_b200.thermo import Thermo
+    cfg = I.make_config("cfg2")
+    th = Thermo.from_config(cfg)
+    th.set_method("mrsdc", 3, 2, 1)
+    th.step(3.0, cfg.dt, 1)
+    o = O.Oracle.from_config(cfg)
+    Tr, _ = o.step_mrsdc(np.full(o.n, cfg.T0), 3.0, cfg.dt, 1, cfg.scenarios[0], 3, 2, 1)
+    assert rel(th.get_T(), Tr) <= TOL

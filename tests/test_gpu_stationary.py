@@ -101,3 +101,16 @@ def test_errors():
     tb = _thermo(cfgb)
     with pytest.raises(ThermoError, match="EINVAL"):
         tb.stationary(0.0)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("coupled", [False, True])
+def test_cfg1_stationary_vs_oracle(coupled):
+    """BASELINE configs[1] meshes (85,694 DoF): the unshifted operator needs O(1/h) iterations."""
+    cfg = I.make_config("cfg1")
+    th = _thermo(cfg)
+    th.stationary(0.0, coupled)
+    o = O.Oracle.from_config(cfg)
+    Tr, st = o.stationary(np.full(o.n, cfg.T0), 0.0, cfg.scenarios[0], coupled)
+    assert rel(th.get_T(), Tr) <= TOL
+    assert th.stats()["max_iters"] > 100
