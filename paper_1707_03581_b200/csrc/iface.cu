@@ -1,12 +1,12 @@
 // iface.cu -- per-step re-integration of the interface terms on Gamma_R(t).
 //
-// K2a (k_pairs, twice: once per surface): one thread per surface triangle finds every
-// triangle of the other surface whose box overlaps (uniform bin grid, each pair visited
+// K2a (k_pairs, one launch for both surfaces): a warp takes 4 triangles of one surface, finds
+// every triangle of the other surface whose box overlaps (uniform bin grid, each pair visited
 // once), cuts the overlap polygon F cap (G + o) by Sutherland-Hodgman (F = rail-top
 // triangle, G = stock-bottom triangle, o = in-plane offset of the stock), fans it from
 // vertex 0 and integrates the products of the two P1 fields exactly with the P1 mass formula
 //   int_tau g h = |tau|/12 (sum_i g_i h_i + sum_i g_i sum_i h_i)
-// on every fan triangle tau; the result is one record per overlapping pair.
+// on every fan triangle tau; the result is one record per overlapping pair and side.
 // K2b (k_rows): one warp per interface node sums the records of its star into its row of
 // K~_G = -dt [[M_B,fix, C_B], [C_B^T, M_B,mov]] and its friction source
 // eta/2 int phi, and refreshes its Jacobi diagonal.
@@ -185,13 +185,17 @@ __device__ __forceinline__ int warp_excl_scan(int v, int lane) {
 #define PAIR_TPW 4
 #define PAIR_WPB 4
 
-__global__ void __launch_bounds__(32 * PAIR_WPB, 4) k_pairs(IfaceParams P, int side) {
+// Both surfaces in one launch: blocks [0, nbA) take the rail-top triangles (side 0), the rest
+// the stock-bottom triangles (side 1), so the two passes run concurrently.
+__global__ void __launch_bounds__(32 * PAIR_WPB, 4) k_pairs(IfaceParams P, int nbA) {
     extern __shared__ int pair_q_all[];   // [PAIR_WPB][PAIR_TPW * pcap]
     __shared__ int pair_cnt_all[PAIR_WPB][PAIR_TPW];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const unsigned lt = (1u << lane) - 1u;
+    const int side = (int)blockIdx.x < nbA ? 0 : 1;
+    const int bx = side == 0 ? (int)blockIdx.x : (int)blockIdx.x - nbA;
     const int nT = side == 0 ? P.nTA : P.nTB;
-    const int t0 = (blockIdx.x * PAIR_WPB + wib) * PAIR_TPW;
+    const int t0 = (bx * PAIR_WPB + wib) * PAIR_TPW;
     const int s = blockIdx.y;
     if (t0 >= nT) return;
     int *q = pair_q_all + wib * PAIR_TPW * P.pcap;
@@ -837,9 +841,8 @@ int iface_launch(Ctx &c, const IfaceParams &P, cudaStream_t stream) {
     const size_t qsm = sizeof(int) * (size_t)PAIR_WPB * PAIR_TPW * c.pcap;
     cudaStream_t st = stream ? stream : c.stream;
     // blockIdx.y = scenario (batched mode) or node time (the slots of the SDC methods): P.S of them
-    k_pairs<<<dim3((unsigned)((c.nTA + tpb - 1) / tpb), (unsigned)P.S), 32 * PAIR_WPB, qsm, st>>>(P, 0);
-    CK(cudaGetLastError());
-    k_pairs<<<dim3((unsigned)((c.nTB + tpb - 1) / tpb), (unsigned)P.S), 32 * PAIR_WPB, qsm, st>>>(P, 1);
+    const int nbA = (c.nTA + tpb - 1) / tpb, nbB = (c.nTB + tpb - 1) / tpb;
+    k_pairs<<<dim3((unsigned)(nbA + nbB), (unsigned)P.S), 32 * PAIR_WPB, qsm, st>>>(P, nbA);
     CK(cudaGetLastError());
     k_rows<<<dim3((unsigned)((c.n_if + ROW_WPB - 1) / ROW_WPB), (unsigned)P.S), 32 * ROW_WPB, 0, st>>>(P);
     CK(cudaGetLastError());

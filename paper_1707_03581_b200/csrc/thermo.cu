@@ -609,7 +609,7 @@ extern "C" int thermo_get_stats(const void *ctx, thermo_stats *out) {
     out->ms_solve = c->ms_solve;
     out->solve_grid = c->cg_grid;
     out->solve_block = c->cg_block;
-    out->launches_per_step = 1 + (c->n_if ? 3 : 0);
+    out->launches_per_step = 1 + (c->n_if ? 2 : 0);
     return THERMO_OK;
 }
 
