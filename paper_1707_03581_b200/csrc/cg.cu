@@ -634,9 +634,18 @@ __global__ void __launch_bounds__(cg_threads(KIND, W, NG), KIND == 0 ? 2 : 1) k_
         if (tr_on && ntr < 1000) P.trace[ntr++] = gtimer();
         double t7[7];
         grid_total<7>(P.partials, G, 4, red_smem, t7);
+        // t7[4] = sum (z d)^2 is the current r.r computed directly: if an expansion below was
+        // too close to its rounding noise to be trusted, the convergence test lands here, one
+        // S phase later, before the update
+        if (!first && !P.debug) {
+            rr = t7[4];
+            if (rr <= tol2) { conv = true; break; }
+        }
         const double alpha = rho / t7[0];
         const double rz_new = fma(alpha, fma(alpha, t7[3], -2.0 * t7[2]), t7[1]);
         const double rr_new = fma(alpha, fma(alpha, t7[6], -2.0 * t7[5]), t7[4]);
+        // rounding noise of the expansion (terms of size r.r of this iteration)
+        const double rr_noise = 1e-13 * (t7[4] + fabs(2.0 * alpha * t7[5]) + alpha * alpha * t7[6]);
         // ---- U: x += alpha p, z -= alpha q' (streams only, no reduction)
         if constexpr (KIND != 0) {
             const double *const usrc[4] = {pnew, P.q, xsrc, P.z};
@@ -679,7 +688,8 @@ __global__ void __launch_bounds__(cg_threads(KIND, W, NG), KIND == 0 ? 2 : 1) k_
         beta = rz_new / rho;
         rho = rz_new;
         rr = rr_new;
-        conv = rr <= tol2 && !P.debug;   // debug runs: fixed iteration count (maxit)
+        // debug runs: fixed iteration count (maxit); an expansion within its noise is not trusted
+        conv = rr <= tol2 && rr > rr_noise && !P.debug;
         xsrc = P.T_out;
         double *t = pold; pold = pnew; pnew = t;
         ++it;
