@@ -1,5 +1,3 @@
 #!/bin/bash
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q -k "not slow" > gpurun_out/pytest_gpu.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_gpu.log
-rm -f gpurun_out/probe_exp.log
-for c in cfg0 cfg1 cfg3; do timeout 300 python tools/probe.py $c 10 2>&1 | grep -E "ms/step|solve" | tail -n 2 >> gpurun_out/probe_exp.log; done
+timeout 900 python tools/fullrun_errors.py > gpurun_out/fullrun_errors.txt 2>&1
