@@ -8,10 +8,15 @@
 // [k][c][s]), the friction source, and the Jacobi diagonal DinvS[N][SP] (volume diagonal,
 // interface rows rewritten per step by the interface kernels).
 //
-// Per CG iteration (same z-primary schedule as cg.cu, column-wise):
-//   S: p = z + beta p_old on the fly, q = K~ p (warp per slice, rows in turn: the row's entries
-//      are broadcast by shuffles, every lane gathers its two columns), partial p.q per column
+// Per CG iteration (z-primary, column-wise):
+//   P: p = z + beta p_old (streaming pass; first iteration p = z), grid barrier
+//   S: q = K~ p (warp per row pair: the rows' entries are broadcast by shuffles, every lane
+//      gathers its two columns of p with L2-only loads), partial p.q per column
 //   U: x += alpha p, z -= alpha D^{-1} q, partial r.z, r.r per column
+// Forming p in its own pass (instead of z + beta p_old on the fly for every gathered column, as
+// the single-vector kernel does from shared memory) halves the gathered bytes: the gathers are
+// latency-bound with the rows held in registers, so one vector per entry allows twice the
+// entries per round.
 // Converged columns are frozen (alpha = 0).  Reductions are deterministic: lanes own columns,
 // warps combine in fixed order, CTAs in fixed order; every CTA computes identical scalars.
 #include <cooperative_groups.h>
@@ -128,7 +133,7 @@ __device__ __forceinline__ void load_cv(const CGBParams &P, int64_t base, int w,
 }
 
 // U entries per row and round: 4 with two gathered vectors, 8 with one (same register budget).
-template <bool kTwo, int U>
+template <bool kTwo, int U, bool CGL = false>
 __device__ __forceinline__ void gather_round(const CGBParams &P, int cl, double vl, int m, const double *x1,
                                              const double *x2, double2 beta, int ln, double2 &accA, double2 &accB) {
     for (int k = 0; k < m; k += U) {
@@ -138,11 +143,15 @@ __device__ __forceinline__ void gather_round(const CGBParams &P, int cl, double 
             const int ku = min(k + u, m - 1);
             const int cA = __shfl_sync(0xffffffffu, cl, ku);
             const int cB = __shfl_sync(0xffffffffu, cl, 16 + ku);
-            const double2 a = reinterpret_cast<const double2 *>(x1 + (int64_t)cA * P.SP)[ln];
-            const double2 b = reinterpret_cast<const double2 *>(x1 + (int64_t)cB * P.SP)[ln];
+            const double2 *pa = reinterpret_cast<const double2 *>(x1 + (int64_t)cA * P.SP) + ln;
+            const double2 *pb = reinterpret_cast<const double2 *>(x1 + (int64_t)cB * P.SP) + ln;
+            const double2 a = CGL ? ld_cg2(pa) : *pa;
+            const double2 b = CGL ? ld_cg2(pb) : *pb;
             if (kTwo) {
-                const double2 a2 = reinterpret_cast<const double2 *>(x2 + (int64_t)cA * P.SP)[ln];
-                const double2 b2 = reinterpret_cast<const double2 *>(x2 + (int64_t)cB * P.SP)[ln];
+                const double2 *qa = reinterpret_cast<const double2 *>(x2 + (int64_t)cA * P.SP) + ln;
+                const double2 *qb = reinterpret_cast<const double2 *>(x2 + (int64_t)cB * P.SP) + ln;
+                const double2 a2 = CGL ? ld_cg2(qa) : *qa;
+                const double2 b2 = CGL ? ld_cg2(qb) : *qb;
                 yA[u] = make_double2(fma(beta.x, a2.x, a.x), fma(beta.y, a2.y, a.y));
                 yB[u] = make_double2(fma(beta.x, b2.x, b.x), fma(beta.y, b2.y, b.y));
             } else {
@@ -166,7 +175,7 @@ __device__ __forceinline__ void gather_round(const CGBParams &P, int cl, double 
 
 // Row sums of the shared volume operator for rows rA, rA + 1 of a slice applied to the lane's
 // two columns of y = x1 + beta x2 (kTwo = false: y = x1).  (cl, vl): entries 0..15, preloaded.
-template <bool kTwo>
+template <bool kTwo, bool CGL = false>
 __device__ __forceinline__ void row_spmm2(const CGBParams &P, int64_t base, int w, int rA, bool validB, int cl,
                                           double vl, const double *x1, const double *x2, double2 beta, int lane,
                                           double2 &accA, double2 &accB) {
@@ -174,10 +183,10 @@ __device__ __forceinline__ void row_spmm2(const CGBParams &P, int64_t base, int 
     accB = make_double2(0.0, 0.0);
     const int ln = 2 * lane < P.SP ? lane : 0;   // lanes past the row stride re-read columns 0..1
     constexpr int U = kTwo ? 4 : 8;
-    gather_round<kTwo, U>(P, cl, vl, min(16, w), x1, x2, beta, ln, accA, accB);
+    gather_round<kTwo, U, CGL>(P, cl, vl, min(16, w), x1, x2, beta, ln, accA, accB);
     for (int k0 = 16; k0 < w; k0 += 16) {
         load_cv(P, base, w, rA, validB, k0, lane, cl, vl);
-        gather_round<kTwo, U>(P, cl, vl, min(16, w - k0), x1, x2, beta, ln, accA, accB);
+        gather_round<kTwo, U, CGL>(P, cl, vl, min(16, w - k0), x1, x2, beta, ln, accA, accB);
     }
 }
 
@@ -401,44 +410,63 @@ __global__ void __launch_bounds__(CGB_BLOCK, 1) k_cgb_step(CGBParams P) {
     while (it < P.maxit) {
         const bool any = __syncthreads_or(!(conv[0] && conv[1])) != 0;   // same in every CTA
         if (!any) break;
-        // ---- S
+        // ---- S: p = z + beta p_old in its own streaming pass (first iteration: p = z), then
+        // q = K~ p gathering p only -- one vector, 8 entries per round -- with L2-only loads
+        // (p was written by other SMs moments ago; L1-allocating gathers of it ran 2.8x slower)
         const bool first = it == 0;
         const double2 b2 = make_double2(beta[0], beta[1]);
+        const double *pv = first ? P.z : pnew;
         double vs[1][2] = {{0.0, 0.0}};
-        // epilogue of one row: acc = (K~ p)_i without the interface part, pi = p_i
-        auto finS = [&](int64_t i, int ik, double2 acc, double2 pi) {
-            if (ik >= 0) {
-                const double2 ai = first ? row_iface<false>(P, ik, P.z, nullptr, b2, lane)
-                                         : row_iface<true>(P, ik, P.z, pold, b2, lane);
-                acc.x += ai.x;
-                acc.y += ai.y;
+        if (!first) {
+            if (lane_ok) {
+                int64_t i = gw;
+                for (; i + 3 * (int64_t)TW < N; i += 4 * (int64_t)TW) {   // 4 rows in flight
+                    double2 zv[4], po[4];
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        zv[r] = ld_cg2(reinterpret_cast<const double2 *>(P.z + (i + r * (int64_t)TW) * P.SP) + lane);
+                        po[r] = ld_cg2(reinterpret_cast<const double2 *>(pold + (i + r * (int64_t)TW) * P.SP) + lane);
+                    }
+#pragma unroll
+                    for (int r = 0; r < 4; ++r)
+                        reinterpret_cast<double2 *>(pnew + (i + r * (int64_t)TW) * P.SP)[lane] =
+                            make_double2(fma(b2.x, po[r].x, zv[r].x), fma(b2.y, po[r].y, zv[r].y));
+                }
+                for (; i < N; i += TW) {
+                    const double2 zv = ld_cg2(reinterpret_cast<const double2 *>(P.z + i * P.SP) + lane);
+                    const double2 po = ld_cg2(reinterpret_cast<const double2 *>(pold + i * P.SP) + lane);
+                    reinterpret_cast<double2 *>(pnew + i * P.SP)[lane] =
+                        make_double2(fma(b2.x, po.x, zv.x), fma(b2.y, po.y, zv.y));
+                }
             }
-            if (!lane_ok) return;
-            reinterpret_cast<double2 *>(pnew + i * P.SP)[lane] = pi;
-            reinterpret_cast<double2 *>(P.q + i * P.SP)[lane] = acc;
-            vs[0][0] = fma(pi.x, acc.x, vs[0][0]);
-            vs[0][1] = fma(pi.y, acc.y, vs[0][1]);
-        };
+            grid.sync();
+        }
         unit_loop(P, npairs, gw, TW, lane, [&](int64_t u, int64_t base, int w, int rA, bool validB, int ikA,
                                                int ikB, int cl, double vl) {
             const int64_t iA = 32 * (u >> 4) + rA;
-            double2 zr[2], pr[2];   // own rows, loaded ahead of the gathers
+            double2 own[2];   // own rows of p, loaded ahead of the gathers
             if (lane_ok) {
-                zr[0] = reinterpret_cast<const double2 *>(P.z + iA * P.SP)[lane];
-                if (!first) pr[0] = reinterpret_cast<const double2 *>(pold + iA * P.SP)[lane];
-                if (validB) {
-                    zr[1] = reinterpret_cast<const double2 *>(P.z + (iA + 1) * P.SP)[lane];
-                    if (!first) pr[1] = reinterpret_cast<const double2 *>(pold + (iA + 1) * P.SP)[lane];
-                }
+                own[0] = ld_cg2(reinterpret_cast<const double2 *>(pv + iA * P.SP) + lane);
+                if (validB) own[1] = ld_cg2(reinterpret_cast<const double2 *>(pv + (iA + 1) * P.SP) + lane);
             }
             double2 accr[2];
-            if (first) row_spmm2<false>(P, base, w, rA, validB, cl, vl, P.z, nullptr, b2, lane, accr[0], accr[1]);
-            else row_spmm2<true>(P, base, w, rA, validB, cl, vl, P.z, pold, b2, lane, accr[0], accr[1]);
+            row_spmm2<false, true>(P, base, w, rA, validB, cl, vl, pv, nullptr, b2, lane, accr[0], accr[1]);
             for (int h = 0; h < 2; ++h) {
                 if (h == 1 && !validB) break;
-                double2 pi = zr[h];
-                if (!first && lane_ok) pi = make_double2(fma(b2.x, pr[h].x, pi.x), fma(b2.y, pr[h].y, pi.y));
-                finS(iA + h, h ? ikB : ikA, accr[h], pi);
+                const int64_t i = iA + h;
+                const int ik = h ? ikB : ikA;
+                double2 acc = accr[h];
+                if (ik >= 0) {
+                    const double2 ai = row_iface<false>(P, ik, pv, nullptr, b2, lane);
+                    acc.x += ai.x;
+                    acc.y += ai.y;
+                }
+                if (!lane_ok) continue;
+                const double2 pi = own[h];
+                if (first) reinterpret_cast<double2 *>(pnew + i * P.SP)[lane] = pi;   // p_0 = z_0
+                reinterpret_cast<double2 *>(P.q + i * P.SP)[lane] = acc;
+                vs[0][0] = fma(pi.x, acc.x, vs[0][0]);
+                vs[0][1] = fma(pi.y, acc.y, vs[0][1]);
             }
         });
         double tpq[1][2];
