@@ -213,6 +213,10 @@ struct IfaceParams {
     const double2 *uv;        // [n_if] in-plane coordinates (fixed frame / stock reference frame)
     const int32_t *star_ptr;  // [n_if + 1]
     const int32_t *star_tri;  // own-surface triangles around each node, ascending
+    const int32_t *star_own;  // per star entry: the slots of the triangle's 3 vertices in the
+                              // node's own-column list (3 x 8 bits)
+    const int32_t *own_ptr;   // [n_if + 1] own-column lists (sorted interface-node indices
+    const int32_t *own_idx;   //   of the node's star vertices)
     const int4 *triA;         // [nTA] (k0, k1, k2, -) interface-row indices, counter-clockwise
     const int4 *triB;
     const double4 *boxA;      // [nTA] (lo.x, lo.y, hi.x, hi.y)

@@ -68,6 +68,7 @@ struct Ctx {
     int32_t *d_if_rows = nullptr;
     double2 *d_uv = nullptr;
     int32_t *d_star_ptr = nullptr, *d_star_tri = nullptr;
+    int32_t *d_star_own = nullptr, *d_own_ptr = nullptr, *d_own_idx = nullptr;   // k_rows own-column slots
     int4 *d_triA = nullptr, *d_triB = nullptr;
     double4 *d_boxA = nullptr, *d_boxB = nullptr;
     BinGrid binA{}, binB{};

@@ -355,20 +355,28 @@ __global__ void __launch_bounds__(32 * ROW_WPB) k_rows(IfaceParams P) {
     const double scale = P.dt * P.alpha;
     const int st0 = P.star_ptr[k], nstar = P.star_ptr[k + 1] - st0;   // <= 32 (checked at setup)
     const unsigned lt = (1u << lane) - 1u;
-    int t_l = 0, np_l = 0, a_l = 0;
+    int t_l = 0, np_l = 0, a_l = 0, so_l = 0;
     if (lane < nstar) {
         t_l = P.star_tri[st0 + lane];
+        so_l = P.star_own[st0 + lane];
         const int4 T = own_tri[t_l];
         a_l = (T.x == k) ? 0 : ((T.y == k) ? 1 : 2);
         np_l = P.pcnt[base_rec + (int64_t)s * nT + t_l];
     }
     const int roff = warp_excl_scan(np_l, lane);
     const int R = __shfl_sync(0xffffffffu, roff + np_l, 31);
-    if (R > 0) {   // rows without overlap (most of the rail top) skip the hash table
+    // slots [0, n_own): the node's own-surface columns (its star vertices, ascending), fixed;
+    // the other surface's columns get the following slots in order of first appearance
+    const int o0 = P.own_ptr[k], n_own = R > 0 ? P.own_ptr[k + 1] - o0 : 0;
+    if (R > 0) {   // rows without overlap (most of the rail top) skip all of this
         for (int h = lane; h < ROW_HS; h += 32) W.hkey[h] = -1;
+        for (int u = lane; u < n_own; u += 32) {
+            W.ucol[u] = P.if_rows[P.own_idx[o0 + u]];
+            W.val[u] = 0.0;
+        }
         __syncwarp();
     }
-    int count = 0;
+    int count = n_own;
     bool ok = true;
     double phi = 0.0;
     for (int r0 = 0; r0 < R; r0 += 32) {
@@ -381,6 +389,7 @@ __global__ void __launch_bounds__(32 * ROW_WPB) k_rows(IfaceParams P) {
         const int tq = __shfl_sync(0xffffffffu, t_l, q);
         const int aq = __shfl_sync(0xffffffffu, a_l, q);
         const int oq = __shfl_sync(0xffffffffu, roff, q);
+        const int soq = __shfl_sync(0xffffffffu, so_l, q);
         const bool valid = r < R;
         int cc[6];
         double cv[6];
@@ -402,9 +411,10 @@ __global__ void __launch_bounds__(32 * ROW_WPB) k_rows(IfaceParams P) {
 #pragma unroll
         for (int qq = 0; qq < 6; ++qq) {
             const int key = valid ? cc[qq] : -1;
-            // existing slot?
             int slot = -1;
-            if (valid) {
+            if (qq < 3) {   // own-surface column: its slot is known
+                slot = valid ? (soq >> (8 * qq)) & 255 : -1;
+            } else if (valid) {   // other surface: existing slot?
                 int h = hslot(key);
                 for (int pr = 0; pr < ROW_HS; ++pr) {
                     const int kk = W.hkey[h];
@@ -414,7 +424,7 @@ __global__ void __launch_bounds__(32 * ROW_WPB) k_rows(IfaceParams P) {
                 }
             }
             // new keys: one leader per distinct key, slots by leader lane order
-            const bool isnew = valid && slot < 0;
+            const bool isnew = qq >= 3 && valid && slot < 0;
             const unsigned grp = __match_any_sync(0xffffffffu, isnew ? key : (valid ? -2 : -3 - lane));
             const bool leader_new = isnew && (grp & lt) == 0;
             const unsigned lm = __ballot_sync(0xffffffffu, leader_new);
@@ -699,11 +709,41 @@ int iface_setup(Ctx &c, const double *X, const std::vector<int32_t> &fA, const s
         for (int t = 0; t < nTA; ++t) { stri[pos[triA[t].x]++] = t; stri[pos[triA[t].y]++] = t; stri[pos[triA[t].z]++] = t; }
         for (int t = 0; t < nTB; ++t) { stri[pos[triB[t].x]++] = t; stri[pos[triB[t].y]++] = t; stri[pos[triB[t].z]++] = t; }
     }
+    // own-column lists of the rows: the sorted star vertices of every node, and per star entry
+    // the slots of its triangle's three vertices in that list (k_rows adds these without hashing)
+    std::vector<int32_t> optr(c.n_if + 1, 0), oidx, sown(stri.size(), 0);
+    {
+        std::vector<int32_t> verts;
+        for (int k = 0; k < c.n_if; ++k) {
+            verts.clear();
+            const bool sa = k < c.nA;
+            for (int e = sptr[k]; e < sptr[k + 1]; ++e) {
+                const int4 t = sa ? triA[stri[e]] : triB[stri[e]];
+                verts.push_back(t.x); verts.push_back(t.y); verts.push_back(t.z);
+            }
+            std::sort(verts.begin(), verts.end());
+            verts.erase(std::unique(verts.begin(), verts.end()), verts.end());
+            if (verts.size() > 255) { c.err = "interface node with more than 255 star vertices"; return -1; }
+            optr[k + 1] = optr[k] + (int32_t)verts.size();
+            oidx.insert(oidx.end(), verts.begin(), verts.end());
+            for (int e = sptr[k]; e < sptr[k + 1]; ++e) {
+                const int4 t = sa ? triA[stri[e]] : triB[stri[e]];
+                const int tv[3] = {t.x, t.y, t.z};
+                int packed = 0;
+                for (int b = 0; b < 3; ++b) {
+                    const int pos = (int)(std::lower_bound(verts.begin(), verts.end(), tv[b]) - verts.begin());
+                    packed |= pos << (8 * b);
+                }
+                sown[e] = packed;
+            }
+        }
+    }
     std::vector<int32_t> bAp, bAi, bBp, bBi;
     make_bins(boxA, bAp, bAi, c.binA);
     make_bins(boxB, bBp, bBi, c.binB);
     if (upload(c, &c.d_if_rows, rows) || upload(c, &c.d_uv, uv) || upload(c, &c.d_star_ptr, sptr) ||
-        upload(c, &c.d_star_tri, stri) || upload(c, &c.d_triA, triA) || upload(c, &c.d_triB, triB) ||
+        upload(c, &c.d_star_tri, stri) || upload(c, &c.d_star_own, sown) || upload(c, &c.d_own_ptr, optr) ||
+        upload(c, &c.d_own_idx, oidx) || upload(c, &c.d_triA, triA) || upload(c, &c.d_triB, triB) ||
         upload(c, &c.d_boxA, boxA) || upload(c, &c.d_boxB, boxB) || upload(c, &c.d_binA_ptr, bAp) ||
         upload(c, &c.d_binA_ids, bAi) || upload(c, &c.d_binB_ptr, bBp) || upload(c, &c.d_binB_ids, bBi))
         return -3;
@@ -813,6 +853,9 @@ void iface_params(Ctx &c, IfaceParams &P, const double *step_sc, double dt) {
     P.uv = c.d_uv;
     P.star_ptr = c.d_star_ptr;
     P.star_tri = c.d_star_tri;
+    P.star_own = c.d_star_own;
+    P.own_ptr = c.d_own_ptr;
+    P.own_idx = c.d_own_idx;
     P.triA = c.d_triA;
     P.triB = c.d_triB;
     P.boxA = c.d_boxA;

@@ -54,7 +54,7 @@ static void free_ctx(Ctx *c) {
                     c->d_chunk_nruns, c->d_chunk_lown, c->d_trace, c->d_DinvS, c->d_slice_if_zero,
                     c->d_KV, c->d_Dinv_vol, c->d_if_of_row, c->d_mr, c->d_mr_iters, c->d_mr_relres,
                     c->d_ell_cnt_s, c->d_ell_col_s, c->d_ell_val_s, c->d_if_b_s, c->d_if_phi_s, c->d_rhs,
-                    c->d_pairs_s, c->d_pcnt_s};
+                    c->d_pairs_s, c->d_pcnt_s, c->d_star_own, c->d_own_ptr, c->d_own_idx};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     for (cudaEvent_t e : c->events) cudaEventDestroy(e);
