@@ -163,6 +163,18 @@ int thermo_stationary(void *ctx, double t, int32_t with_interface);
  * (default 0 = min(10 N, 10000)).  EINVAL if rtol <= 0 or maxit < 0. */
 int thermo_set_solver(void *ctx, double rtol, int32_t maxit);
 
+/* Initial guess x0 of the implicit-Euler CG solves (every scenario of a batched context alike):
+ *   order 0:  x0 = T^n (reading R17; what the oracle does);
+ *   order 1:  x0 = T^n + (T^n - T^{n-1});
+ *   order 2:  x0 = T^{n-2} + 3 (T^n - T^{n-1})   (default),
+ * the polynomial extrapolation of the last committed implicit-Euler states of equal dt (lower
+ * order while fewer states exist: after create, thermo_set_T, thermo_stationary, an MRSDC/SDC
+ * step, a dt change or a failed step the history restarts).  Only where CG starts changes: every
+ * solve still stops at ||b - K~ x||_2 <= rtol ||b||_2, so results agree with x0 = T^n to the
+ * solver tolerance, and the extrapolation saves iterations.
+ * EINVAL for other orders. */
+int thermo_set_guess(void *ctx, int32_t order);
+
 typedef struct {
     int64_t n_fixed, n_moving;       /* node counts */
     int64_t nnz_volume;              /* stored nonzeros of the volume operator (unpadded) */

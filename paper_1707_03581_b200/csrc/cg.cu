@@ -3,11 +3,11 @@
 // time step.
 //
 // Schedule per CG iteration, z-primary Jacobi-PCG:
-//   S: p = z + beta p_old (recomputed on the fly for every gathered column),
-//      q = K~ p (sliced-ELL volume part + per-step interface rows), partial p.q
-//   -- grid barrier; alpha = rho / p.q
-//   U: x += alpha p ; z -= alpha D^{-1} q ; r = z / D^{-1} ; partials r.z, r.r
-//   -- grid barrier; beta = r.z / rho, convergence test ||r||^2 <= rtol^2 ||b||^2
+//   S: q = K~ p (sliced-ELL volume part + per-step interface rows, p the only gathered
+//      vector), q' = D^{-1} q; partials of p.q and of the expansions of the next r.z, r.r
+//   -- grid barrier; alpha = rho / p.q, beta = r.z_new / rho, convergence test on r.r
+//   U: x += alpha p ; z -= alpha q' ; p = z + beta p   (streams, no reduction)
+//   -- grid barrier
 // Every value of every reduction is combined in a fixed order (deterministic, identical in
 // all CTAs), so all CTAs take the same control-flow decisions.
 //
@@ -29,6 +29,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <cstdio>
 #include <vector>
 
 #include "ctx.h"
@@ -62,6 +63,7 @@ struct CGParams {
     const int32_t *if_rows, *slice_if, *ell_cnt, *ell_col;
     const double *ell_val, *if_b, *if_phi;
     const double *T_in;
+    const double *X0;          // optional initial guess (extrapolated state); nullptr: x0 = T_in
     const double *rhs;         // optional explicit right-hand side (MRSDC implicit solves)
     double *T_out, *z, *pa, *pb, *q;
     double *partials;
@@ -81,8 +83,10 @@ struct CGParams {
     const int32_t *chunk_lown;  // KIND 2: window-local index of the chunk's first row
     const double *pf[4];       // vectors whose leading edge is prefetched into L2
     int npf;
-    const double *wv[2];       // KIND 2: vectors staged through the window
+    const double *wv[1];       // KIND 2: the vector staged through the window (nwv = 1)
     int nwv;
+    const double *ownv;        // KIND 2: vector of which only the chunk's own rows are staged
+                               // (after the window, W * 32 rows)
     unsigned long long *trace; // optional: %globaltimer after every grid barrier (CTA 0)
     int prefetch;              // L2 leading-edge prefetch (THERMO_CG_PREFETCH=1; measured slower on cfg3)
     int debug;                 // THERMO_CG_DEBUG bits (measurement only, results invalid):
@@ -244,8 +248,9 @@ struct SrcWin {      // KIND 2: matrix and gathered vectors in shared memory
     const double *w1, *w2;
     int lown;            // window-local index of this lane's own row (the chunk's rows form
                          // one contiguous block of its column set)
+    int lown2;           // index of this lane's own row in the own-row block (ownv)
     __device__ __forceinline__ double own1(const double *, int64_t) const { return w1[lown]; }
-    __device__ __forceinline__ double own2(const double *, int64_t) const { return w2[lown]; }
+    __device__ __forceinline__ double own2(const double *, int64_t) const { return w2[lown2]; }
     __device__ __forceinline__ double first() const { return vp[0]; }
     template <bool kTwo>
     __device__ __forceinline__ double dot(int w, const double *, const double *, double beta) const {
@@ -281,6 +286,14 @@ struct Ring {
 };
 
 __host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
+
+// Bytes of the own-row copy of chunk ch (rows rounded up to even: 16-byte bulk copies; the
+// vectors carry padding past N).
+__device__ __forceinline__ uint32_t own_bytes(const CGParams &P, int64_t ch, int W) {
+    const int64_t r0 = ch * W * 32;
+    const int64_t rows = min((int64_t)W * 32, P.N - r0);
+    return (uint32_t)(((rows + 1) & ~(int64_t)1) * 8);
+}
 
 // Sweep over all slices: calls body(s, src, w, ib, ie) for every slice owned by this warp.
 // TMA kinds: CTA b takes chunks b, b + G, b + 2G, ... (static order: every CTA's dot-product
@@ -360,7 +373,8 @@ __device__ __forceinline__ void sweep(const CGParams &P, Ring &R, Body &&body) {
             __syncwarp();
             if (lane == 0) {
                 const uint32_t cbytes = KIND == 2 ? cnt * 2u : cnt * 4u;
-                const uint32_t wbytes = KIND == 2 && !(P.debug & 2) ? (uint32_t)P.nwv * (uint32_t)wtot * 8u : 0u;
+                uint32_t wbytes = KIND == 2 && !(P.debug & 2) ? (uint32_t)P.nwv * (uint32_t)wtot * 8u : 0u;
+                if (KIND == 2 && P.ownv && !(P.debug & 2)) wbytes += own_bytes(P, ch, W);
                 mbar_arrive_expect_tx(&R.full[st], cnt * 8u + cbytes + wbytes);
                 bulk_g2s(sb + CG_HDR, P.val + e0, cnt * 8u, &R.full[st], pol);
                 if (KIND == 2) bulk_g2s(sb + R.col_off, P.lcol + e0, cbytes, &R.full[st], pol);
@@ -368,12 +382,13 @@ __device__ __forceinline__ void sweep(const CGParams &P, Ring &R, Body &&body) {
             }
             __syncwarp();
             if (KIND == 2 && nruns && !(P.debug & 2)) {
-#pragma unroll
-                for (int v = 0; v < 2; ++v)
-                    if (v < P.nwv)
-                        bulk_g2s_nohint(sb + R.win_off + ((size_t)v * P.win_cap + woff) * 8, P.wv[v] + cur.run.x,
-                                        (uint32_t)cur.run.y * 8u, &R.full[st]);
+                if (P.nwv)
+                    bulk_g2s_nohint(sb + R.win_off + (size_t)woff * 8, P.wv[0] + cur.run.x, (uint32_t)cur.run.y * 8u,
+                                    &R.full[st]);
             }
+            if (KIND == 2 && P.ownv && lane == 1 && !(P.debug & 2))   // own rows only, second slot
+                bulk_g2s_nohint(sb + R.win_off + (size_t)P.win_cap * 8, P.ownv + ch * W * 32,
+                                own_bytes(P, ch, W), &R.full[st]);
             if (lane == 0 && !(P.debug & 4)) {
                 prefetch_edge<W>(P, cur.hi_own);
                 prefetch_edge<W>(P, cur.hi_pf);
@@ -414,7 +429,8 @@ __device__ __forceinline__ void sweep(const CGParams &P, Ring &R, Body &&body) {
                     // row N - 1 instead, whose value they discard
                     const int64_t irow = 32 * s + lane;
                     const int pad = irow > P.N - 1 ? (int)(irow - (P.N - 1)) : 0;
-                    SrcWin src{lc + o0 + lane, vals + o0 + lane, w1, w1 + P.win_cap, hdr[29] + 32 * wg + lane - pad};
+                    SrcWin src{lc + o0 + lane, vals + o0 + lane, w1, w1 + P.win_cap, hdr[29] + 32 * wg + lane - pad,
+                               32 * wg + lane - pad};
                     body(s, src, (o1 - o0) >> 5, hdr[16 + wg], hdr[17 + wg]);
                 } else {
                     const int32_t *cols = reinterpret_cast<const int32_t *>(sb + R.col_off);
@@ -533,7 +549,7 @@ __global__ void __launch_bounds__(cg_threads(KIND, W, NG), KIND == 0 ? 2 : 1) k_
         R.stage = ring_raw + 128;
         R.col_off = CG_HDR + (size_t)P.stage_entries * 8;
         R.win_off = align16(R.col_off + (size_t)P.stage_entries * (KIND == 2 ? 2 : 4));
-        R.stage_bytes = align16(R.win_off + (KIND == 2 ? (size_t)2 * P.win_cap * 8 : 0));
+        R.stage_bytes = align16(R.win_off + (KIND == 2 ? (size_t)(P.win_cap + 32 * W) * 8 : 0));
         if (threadIdx.x == 0) {
             for (int s = 0; s < NS; ++s) {
                 mbar_init(&R.full[s], 1);
@@ -544,24 +560,27 @@ __global__ void __launch_bounds__(cg_threads(KIND, W, NG), KIND == 0 ? 2 : 1) k_
         __syncthreads();
     }
 
-    // ---- r0 = b - K~ x0 with x0 = T^n, b = M_L T^n + dt (b_env + b_G); z0 = D^{-1} r0
+    // ---- r0 = b - K~ x0, b = M_L T^n + dt (b_env + b_G); z0 = D^{-1} r0, p0 = z0.  x0 = T^n, or
+    // the extrapolation X0 from earlier steps (then T^n's own rows come as the own-row block)
     const bool tr_on = P.trace && blockIdx.x == 0 && threadIdx.x == 0;
     int ntr = 0;
     if (tr_on) P.trace[ntr++] = gtimer();
     double red0[4] = {0.0, 0.0, 0.0, 0.0};   // b.b, r.r, r.z, |Gamma_R|
     P.pf[0] = P.T_in; P.pf[1] = P.ML; P.pf[2] = P.benv; P.pf[3] = P.Dinv;
     P.npf = P.prefetch ? 4 : 0;
-    P.wv[0] = P.T_in;
+    const double *const x0 = P.X0 ? P.X0 : P.T_in;
+    P.wv[0] = x0;
     P.nwv = 1;
+    P.ownv = P.X0 ? P.T_in : nullptr;
     sweep<KIND, W, NG>(P, R, [&](int64_t s, const auto &src, int w, int ib, int ie) {
         const int64_t i = 32 * s + lane;
         const int64_t ii = i < N ? i : N - 1;
         // own-row loads first: their latency overlaps the row sum
         const double be = P.benv[ii], ml = P.ML[ii], di = P.Dinv[ii];
-        const double Ti = src.own1(P.T_in, ii);
+        const double Ti = P.X0 ? src.own2(P.T_in, ii) : src.own1(P.T_in, ii);
         const int ik = iface_index_r(P, ib, ie, i, lane);
-        double ax = src.template dot<false>(w, P.T_in, nullptr, 0.0);
-        if (ik >= 0) ax += ell_row<false>(P, ik, P.T_in, nullptr, 0.0);
+        double ax = src.template dot<false>(w, x0, nullptr, 0.0);
+        if (ik >= 0) ax += ell_row<false>(P, ik, x0, nullptr, 0.0);
         if (i < N) {
             double bi = be;
             if (ik >= 0) bi += P.if_b[ik];
@@ -569,12 +588,14 @@ __global__ void __launch_bounds__(cg_threads(KIND, W, NG), KIND == 0 ? 2 : 1) k_
             const double r = bi - ax;
             const double zi = di * r;
             P.z[i] = zi;
+            P.pa[i] = zi;   // p_0 = z_0
             red0[0] = fma(bi, bi, red0[0]);
             red0[1] = fma(r, r, red0[1]);
             red0[2] = fma(r, zi, red0[2]);
             if (ik >= 0 && ik < P.nA) red0[3] += P.if_phi[ik];
         }
     });
+    P.ownv = nullptr;
     cta_reduce_store<4>(red0, red_smem, P.partials, 0);
     grid.sync();
     if (tr_on) P.trace[ntr++] = gtimer();
@@ -583,42 +604,36 @@ __global__ void __launch_bounds__(cg_threads(KIND, W, NG), KIND == 0 ? 2 : 1) k_
     const double tol2 = P.rtol2 * tot0[0];
     double rho = tot0[2], rr = tot0[1];
     bool conv = rr <= tol2;
-    double beta = 0.0;
-    const double *xsrc = P.T_in;
-    double *pold = P.pa, *pnew = P.pb;
+    const double *xsrc = x0;
+    double *const p = P.pa;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nthr = (int64_t)G * blockDim.x;
     int it = 0;
     while (!conv && it < P.maxit) {
-        // ---- S: p = z + beta p_old, q = K~ p; q' = D^{-1} q with the diagonal d taken from the
-        // row's own entries; partials of p.q and of the expansions of the next r.z and r.r
+        // ---- S: q = K~ p (the only gathered vector); q' = D^{-1} q with the diagonal d taken
+        // from the row's own entries; partials of p.q and of the expansions of the next r.z and r.r
         //   z_new = z - alpha q', r_new = z_new d:  r.z = z^2 d - 2 alpha z q + alpha^2 q^2 / d,
-        //   r.r = (z d)^2 - 2 alpha z d q + alpha^2 q^2,  so the U phase needs no reduction
+        //   r.r = (z d)^2 - 2 alpha z d q + alpha^2 q^2,
+        // so beta is known before the U phase, which forms the next direction itself
         double red[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
         const bool first = it == 0;
-        P.pf[0] = P.z; P.pf[1] = pold;
-        P.npf = P.prefetch ? (first ? 1 : 2) : 0;
-        P.wv[0] = P.z; P.wv[1] = pold;
-        P.nwv = first ? 1 : 2;
+        P.pf[0] = p;
+        P.npf = P.prefetch ? 1 : 0;
+        P.wv[0] = p;
+        P.nwv = 1;
+        P.ownv = P.z;
         sweep<KIND, W, NG>(P, R, [&](int64_t s, const auto &src, int w, int ib, int ie) {
             const int64_t i = 32 * s + lane;
             const int64_t ii = i < N ? i : N - 1;
-            const double zo = src.own1(P.z, ii);   // issued before the row sum
-            const double po = first ? 0.0 : src.own2(pold, ii);
+            const double pi = src.own1(p, ii);      // issued before the row sum
+            const double zo = src.own2(P.z, ii);
             const int ik = iface_index_r(P, ib, ie, i, lane);
-            double acc, dg = src.first();   // the diagonal (entry 0) + the interface self term
-            if (first) {
-                acc = src.template dot<false>(w, P.z, nullptr, 0.0);
-                if (ik >= 0) acc += ell_row<false>(P, ik, P.z, nullptr, 0.0, ii, &dg);
-            } else {
-                acc = src.template dot<true>(w, P.z, pold, beta);
-                if (ik >= 0) acc += ell_row<true>(P, ik, P.z, pold, beta, ii, &dg);
-            }
+            double dg = src.first();   // the diagonal (entry 0) + the interface self term
+            double acc = src.template dot<false>(w, p, nullptr, 0.0);
+            if (ik >= 0) acc += ell_row<false>(P, ik, p, nullptr, 0.0, ii, &dg);
             if (i < N) {
-                const double pi = first ? zo : fma(beta, po, zo);
                 const double qs = acc / dg;
                 const double zd = zo * dg;
-                pnew[i] = pi;
                 P.q[i] = qs;
                 red[0] = fma(pi, acc, red[0]);
                 red[1] = fma(zo, zd, red[1]);
@@ -629,6 +644,7 @@ __global__ void __launch_bounds__(cg_threads(KIND, W, NG), KIND == 0 ? 2 : 1) k_
                 red[6] = fma(acc, acc, red[6]);
             }
         });
+        P.ownv = nullptr;
         cta_reduce_store<7>(red, red_smem, P.partials, 4);
         grid.sync();
         if (tr_on && ntr < 1000) P.trace[ntr++] = gtimer();
@@ -646,23 +662,28 @@ __global__ void __launch_bounds__(cg_threads(KIND, W, NG), KIND == 0 ? 2 : 1) k_
         const double rr_new = fma(alpha, fma(alpha, t7[6], -2.0 * t7[5]), t7[4]);
         // rounding noise of the expansion (terms of size r.r of this iteration)
         const double rr_noise = 1e-13 * (t7[4] + fabs(2.0 * alpha * t7[5]) + alpha * alpha * t7[6]);
-        // ---- U: x += alpha p, z -= alpha q' (streams only, no reduction)
+        const double beta = rz_new / rho;
+        // ---- U: x += alpha p, z -= alpha q', p = z + beta p (streams only, no reduction)
         if constexpr (KIND != 0) {
-            const double *const usrc[4] = {pnew, P.q, xsrc, P.z};
+            const double *const usrc[4] = {p, P.q, xsrc, P.z};
             sweep_u<W, NG>(P, R, usrc, [&](int64_t i, double pv, double qv, double xv, double zv) {
                 P.T_out[i] = fma(alpha, pv, xv);
-                P.z[i] = fma(-alpha, qv, zv);
+                const double zn = fma(-alpha, qv, zv);
+                P.z[i] = zn;
+                p[i] = fma(beta, pv, zn);
             });
         } else {   // element pairs with 16-byte loads, two pairs in flight per thread and trip
             const int64_t npair = N >> 1;
-            const double2 *p2 = reinterpret_cast<const double2 *>(pnew);
+            double2 *p2 = reinterpret_cast<double2 *>(p);
             const double2 *q2 = reinterpret_cast<const double2 *>(P.q);
             const double2 *x2 = reinterpret_cast<const double2 *>(xsrc);
             double2 *z2 = reinterpret_cast<double2 *>(P.z);
             double2 *o2 = reinterpret_cast<double2 *>(P.T_out);
             auto upd = [&](double2 pv, double2 qv, double2 xv, double2 zv, int64_t j) {
                 o2[j] = make_double2(fma(alpha, pv.x, xv.x), fma(alpha, pv.y, xv.y));
-                z2[j] = make_double2(fma(-alpha, qv.x, zv.x), fma(-alpha, qv.y, zv.y));
+                const double2 zn = make_double2(fma(-alpha, qv.x, zv.x), fma(-alpha, qv.y, zv.y));
+                z2[j] = zn;
+                p2[j] = make_double2(fma(beta, pv.x, zn.x), fma(beta, pv.y, zn.y));
             };
             constexpr int UU = 2;
             int64_t j = tid;
@@ -679,23 +700,23 @@ __global__ void __launch_bounds__(cg_threads(KIND, W, NG), KIND == 0 ? 2 : 1) k_
             for (; j < npair; j += nthr) upd(p2[j], q2[j], x2[j], z2[j], j);
             if ((N & 1) && tid == nthr - 1) {
                 const int64_t i = N - 1;
-                P.T_out[i] = fma(alpha, pnew[i], xsrc[i]);
-                P.z[i] = fma(-alpha, P.q[i], P.z[i]);
+                P.T_out[i] = fma(alpha, p[i], xsrc[i]);
+                const double zn = fma(-alpha, P.q[i], P.z[i]);
+                P.z[i] = zn;
+                p[i] = fma(beta, p[i], zn);
             }
         }
         grid.sync();
         if (tr_on && ntr < 1000) P.trace[ntr++] = gtimer();
-        beta = rz_new / rho;
         rho = rz_new;
         rr = rr_new;
         // debug runs: fixed iteration count (maxit); an expansion within its noise is not trusted
         conv = rr <= tol2 && rr > rr_noise && !P.debug;
         xsrc = P.T_out;
-        double *t = pold; pold = pnew; pnew = t;
         ++it;
     }
-    if (it == 0) {   // already converged: T^{n+1} = T^n
-        for (int64_t i = tid; i < N; i += nthr) P.T_out[i] = P.T_in[i];
+    if (it == 0) {   // already converged: T^{n+1} = x0
+        for (int64_t i = tid; i < N; i += nthr) P.T_out[i] = x0[i];
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         const double rel = tot0[0] > 0.0 ? sqrt(rr / tot0[0]) : sqrt(rr);
@@ -826,7 +847,7 @@ static const void *variant_kernel(int v) {
 static size_t stage_bytes(const Variant &v, int E, int wc) {
     size_t col_off = CG_HDR + (size_t)E * 8;
     size_t win_off = align16(col_off + (size_t)E * (v.kind == 2 ? 2 : 4));
-    return align16(win_off + (v.kind == 2 ? (size_t)2 * wc * 8 : 0));
+    return align16(win_off + (v.kind == 2 ? (size_t)(wc + 32 * v.W) * 8 : 0));
 }
 
 int cg_setup(Ctx &c) {
@@ -876,7 +897,11 @@ int cg_setup(Ctx &c) {
             wc = (stats[0] + 1) & ~1;
         }
         const size_t sb = stage_bytes(v, E, wc);
-        int ns = v.kind == 0 ? 1 : (int)std::min<size_t>(8, (210 * 1024 - 128) / sb);
+        // ring budget: 210 KB leaves the rest of the 228-KB carve-out to L1 (224 KB, one more
+        // stage on cfg 3, measured no faster: the ring is not depth-bound)
+        const char *ekb = getenv("THERMO_CG_SMEM_KB");   // tuning hook
+        const size_t budget = (size_t)(ekb ? atoi(ekb) : 210) * 1024 - 128;
+        int ns = v.kind == 0 ? 1 : (int)std::min<size_t>(8, budget / sb);
         if (const char *e = getenv("THERMO_CG_STAGES")) ns = std::min(ns, std::max(2, atoi(e)));   // tuning hook
         if (v.kind != 0 && ns < v.NG + 1) continue;   // at least one stage in flight
         const size_t smem = v.kind == 0 ? 0 : 128 + (size_t)ns * sb;
@@ -895,6 +920,11 @@ int cg_setup(Ctx &c) {
         break;
     }
     if (chosen < 0) { c.err = "no CG kernel variant can be resident"; return -3; }
+    if (getenv("THERMO_CG_VERBOSE"))
+        fprintf(stderr, "[thermo cg] variant %d (kind %d, W %d, NG %d): stage entries %d, window cap %d, "
+                        "stage %zu B, %d stages, smem %zu B\n", chosen, kVariants[chosen].kind, c.cg_chunk,
+                kVariants[chosen].NG, c.cg_stage_entries, c.cg_win_cap,
+                stage_bytes(kVariants[chosen], c.cg_stage_entries, c.cg_win_cap), c.cg_nstages, c.cg_smem);
     c.cg_variant = chosen;
     const char *dbg = getenv("THERMO_CG_DEBUG");
     c.cg_debug = dbg ? atoi(dbg) : 0;
@@ -971,7 +1001,7 @@ int cg_launch_solve(Ctx &c, const double *x0, double *x, const double *rhs, cons
     return 0;
 }
 
-int cg_launch_step(Ctx &c, int step, double dt) {
+int cg_launch_step(Ctx &c, int step, double dt, const double *x0) {
     CGParams P;
     memset(&P, 0, sizeof P);
     P.N = c.N;
@@ -994,6 +1024,7 @@ int cg_launch_step(Ctx &c, int step, double dt) {
     P.if_b = c.d_if_b;
     P.if_phi = c.d_if_phi;
     P.T_in = c.d_T[(c.cur + step) & 1];
+    P.X0 = x0;
     P.T_out = c.d_T[(c.cur + step + 1) & 1];
     P.z = c.d_z;
     P.pa = c.d_p[0];

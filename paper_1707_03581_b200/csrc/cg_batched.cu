@@ -62,6 +62,7 @@ struct CGBParams {
     const int32_t *if_of_row;   // [N] interface index of a row, -1 if none
     const double *ell_val, *if_b, *if_phi;
     const double *T_in;
+    const double *X0;          // optional initial guess (extrapolated states); nullptr: x0 = T_in
     double *T_out, *z, *pa, *pb, *q;
     double *partials;   // [G][CGB_NV][64]
     int *status;
@@ -340,14 +341,16 @@ __global__ void __launch_bounds__(CGB_BLOCK, 1) k_cgb_step(CGBParams P) {
     const int gw = blockIdx.x * NW + warp, TW = gridDim.x * NW;
     const bool col_ok[2] = {2 * lane < P.S, 2 * lane + 1 < P.S};
     const bool lane_ok = 2 * lane < P.SP;   // lanes past the row stride touch no memory
-    // ---- phase 0: r0 = b - K~ x0, z0 = D^{-1} r0 per column
+    // ---- phase 0: r0 = b - K~ x0, z0 = D^{-1} r0 per column (b = M_L T^n + dt (b_env + b_G);
+    // x0 = T^n or the extrapolated guess X0)
+    const double *const x0 = P.X0 ? P.X0 : P.T_in;
     double v0[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};   // b.b, r.r, r.z, |Gamma_R| (scenario 0)
     const int64_t npairs = P.nslices * 16;   // units: (slice, row pair)
     // epilogue of one row: ax = (K~ x0)_i without the interface part, Ti = x0_i
     auto fin0 = [&](int64_t i, int ik, double2 ax, double2 Ti, double2 di) {
         double2 bg = make_double2(0.0, 0.0);
         if (ik >= 0) {
-            const double2 ai = row_iface<false>(P, ik, P.T_in, nullptr, make_double2(0, 0), lane);
+            const double2 ai = row_iface<false>(P, ik, x0, nullptr, make_double2(0, 0), lane);
             ax.x += ai.x;
             ax.y += ai.y;
             if (col_ok[0]) bg.x = P.if_b[(int64_t)ik * P.S + 2 * lane];
@@ -388,7 +391,7 @@ __global__ void __launch_bounds__(CGB_BLOCK, 1) k_cgb_step(CGBParams P) {
             }
         }
         double2 axr[2];
-        row_spmm2<false>(P, base, w, rA, validB, cl, vl, P.T_in, nullptr, make_double2(0, 0), lane, axr[0],
+        row_spmm2<false>(P, base, w, rA, validB, cl, vl, x0, nullptr, make_double2(0, 0), lane, axr[0],
                          axr[1]);
         fin0(iA, ikA, axr[0], Tr[0], dr[0]);
         if (validB) fin0(iA + 1, ikB, axr[1], Tr[1], dr[1]);
@@ -404,7 +407,7 @@ __global__ void __launch_bounds__(CGB_BLOCK, 1) k_cgb_step(CGBParams P) {
         conv[h] = !col_ok[h] || rr2[h] <= tol2[h];
     }
     const double area = __shfl_sync(0xffffffffu, t0[3][0], 0);
-    const double *xsrc = P.T_in;
+    const double *xsrc = x0;
     double *pold = P.pa, *pnew = P.pb;
     int it = 0;
     while (it < P.maxit) {
@@ -494,7 +497,7 @@ __global__ void __launch_bounds__(CGB_BLOCK, 1) k_cgb_step(CGBParams P) {
     }
     if (it == 0 && lane_ok) {
         for (int64_t i = gw; i < N; i += TW)
-            reinterpret_cast<double2 *>(P.T_out + i * P.SP)[lane] = reinterpret_cast<const double2 *>(P.T_in + i * P.SP)[lane];
+            reinterpret_cast<double2 *>(P.T_out + i * P.SP)[lane] = reinterpret_cast<const double2 *>(x0 + i * P.SP)[lane];
     }
     if (blockIdx.x == 0 && warp == 0) {
         for (int h = 0; h < 2; ++h) {
@@ -543,7 +546,7 @@ int cgb_prepare(Ctx &c) {
     return 0;
 }
 
-int cgb_launch_step(Ctx &c, int step, double dt) {
+int cgb_launch_step(Ctx &c, int step, double dt, const double *x0) {
     CGBParams P;
     memset(&P, 0, sizeof P);
     P.N = c.N;
@@ -568,6 +571,7 @@ int cgb_launch_step(Ctx &c, int step, double dt) {
     P.if_b = c.d_if_b;
     P.if_phi = c.d_if_phi;
     P.T_in = c.d_T[(c.cur + step) & 1];
+    P.X0 = x0;
     P.T_out = c.d_T[(c.cur + step + 1) & 1];
     P.z = c.d_z;
     P.pa = c.d_p[0];

@@ -108,6 +108,12 @@ struct Ctx {
 
     double rtol = 1e-12;
     int maxit = 0;
+    // initial guess of the implicit-Euler solves: 0 = T^n (reading R17), 1 = linear, 2 = quadratic
+    // extrapolation of the last states (thermo_set_guess); hist = consecutive committed
+    // implicit-Euler states with step hist_dt behind the current one (0..2)
+    int guess = 2, hist = 0;
+    double hist_dt = 0.0;
+    double *d_x0 = nullptr, *d_Thist = nullptr;   // [N x SP] guess and T^{n-2}
     // time-stepping method: 0 implicit Euler, 1 MRSDC(M, P) with K sweeps
     int method = 0, mr_M = 3, mr_P = 2, mr_K = 1;
     int32_t *d_slice_if_zero = nullptr;   // all-empty interface ranges (volume-only solves)
@@ -156,7 +162,8 @@ int iface_launch(Ctx &c, const IfaceParams &p, cudaStream_t stream = nullptr);
 
 // cg.cu
 int cg_setup(Ctx &c);
-int cg_launch_step(Ctx &c, int step, double dt);
+// x0: initial guess (extrapolated state, see thermo.cu), nullptr = the committed state T^n
+int cg_launch_step(Ctx &c, int step, double dt, const double *x0 = nullptr);
 // Solve (M_L - a K_vol [- a K_G]) x = rhs from x0 with the operator currently in d_val (a =
 // built_dt); iface = false: no interface rows.  Iterations / residual to iters_out[slot].
 int cg_launch_solve(Ctx &c, const double *x0, double *x, const double *rhs, const double *Dinv, bool iface,
@@ -171,6 +178,6 @@ int sdc_step(Ctx &c, double tn, double dt, int step_index);   // single-rate SDC
 // cg_batched.cu (S > 1 scenarios advanced together)
 int cgb_setup(Ctx &c);
 int cgb_prepare(Ctx &c);   // broadcast the volume D^{-1} into DinvS (after build_operator)
-int cgb_launch_step(Ctx &c, int step, double dt);
+int cgb_launch_step(Ctx &c, int step, double dt, const double *x0 = nullptr);
 
 }  // namespace thermo

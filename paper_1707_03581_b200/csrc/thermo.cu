@@ -54,7 +54,7 @@ static void free_ctx(Ctx *c) {
                     c->d_chunk_nruns, c->d_chunk_lown, c->d_trace, c->d_DinvS, c->d_slice_if_zero,
                     c->d_KV, c->d_Dinv_vol, c->d_if_of_row, c->d_mr, c->d_mr_iters, c->d_mr_relres,
                     c->d_ell_cnt_s, c->d_ell_col_s, c->d_ell_val_s, c->d_if_b_s, c->d_if_phi_s, c->d_rhs,
-                    c->d_pairs_s, c->d_pcnt_s, c->d_star_own, c->d_own_ptr, c->d_own_idx};
+                    c->d_pairs_s, c->d_pcnt_s, c->d_star_own, c->d_own_ptr, c->d_own_idx, c->d_x0, c->d_Thist};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     for (cudaEvent_t e : c->events) cudaEventDestroy(e);
@@ -238,6 +238,21 @@ extern "C" int thermo_set_bc(void *ctx, int32_t part, int32_t tag, double alpha,
     }
 }
 
+// Initial guess of an implicit-Euler solve by polynomial extrapolation of the last committed
+// states (equal steps): order 1  x0 = T^n + (T^n - T^{n-1}),
+//                      order 2  x0 = T^{n-2} + 3 (T^n - T^{n-1}),
+// and the history shift Th <- T^{n-1} (the buffer holding T^{n-1} receives T^{n+1}).  The guess
+// changes only where CG starts: the stopping rule ||b - K~ x|| <= rtol ||b|| is the same.
+__global__ void k_extrap(const double *__restrict__ Tn, const double *__restrict__ Tn1, double *__restrict__ Th,
+                         double *__restrict__ x0, int64_t N, int order, int save) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    const double a = Tn[i], b = Tn1[i];
+    const double d = a - b;
+    x0[i] = order >= 2 ? fma(3.0, d, Th[i]) : a + d;
+    if (save) Th[i] = b;
+}
+
 // right-hand side of the stationary solve: b_env (+ b_G on the interface rows)
 __global__ void k_stat_rhs(const double *benv, int64_t N, const int32_t *if_of_row, const double *if_b, double *rhs) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -314,10 +329,20 @@ extern "C" int thermo_stationary(void *ctx, double t, int32_t with_interface) {
         c->failed_step = -1;
         c->failed_scen = -1;
         c->cur ^= 1;
+        c->hist = 0;
         return THERMO_OK;
     } catch (...) {
         return fail(c, THERMO_ENOMEM, "host allocation failed");
     }
+}
+
+extern "C" int thermo_set_guess(void *ctx, int32_t order) {
+    Ctx *c = (Ctx *)ctx;
+    if (!c) return THERMO_EINVAL;
+    if (order < 0 || order > 2) return fail(c, THERMO_EINVAL, "guess order must be 0, 1 or 2");
+    c->guess = order;
+    c->hist = 0;
+    return THERMO_OK;
 }
 
 extern "C" int thermo_set_method(void *ctx, int32_t method, int32_t M, int32_t P, int32_t K) {
@@ -356,6 +381,7 @@ extern "C" int thermo_step(void *ctx, double t, double dt, int32_t nsteps) {
     if (nsteps == 0) return THERMO_OK;
     try {
         const int S = c->S;
+        if (c->method >= 1 || c->hist_dt != dt) c->hist = 0;   // extrapolation needs equal IE steps
         if (c->built_dt != dt) {
             if (thermo::build_operator(*c, dt)) return THERMO_ECUDA;
             if (S > 1 && thermo::cgb_prepare(*c)) return THERMO_ECUDA;
@@ -432,6 +458,14 @@ extern "C" int thermo_step(void *ctx, double t, double dt, int32_t nsteps) {
                 c->events.push_back(e);
             }
         }
+        const bool extrap = c->guess > 0;
+        const int64_t NS = c->N * c->SP;
+        if (extrap && !c->d_x0) {
+            API_CK(cudaMalloc(&c->d_x0, sizeof(double) * (NS + 16)));
+            API_CK(cudaMemsetAsync(c->d_x0, 0, sizeof(double) * (NS + 16), c->stream));
+            API_CK(cudaMalloc(&c->d_Thist, sizeof(double) * (NS + 16)));
+            API_CK(cudaMemsetAsync(c->d_Thist, 0, sizeof(double) * (NS + 16), c->stream));
+        }
         for (int n = 0; n < nsteps; ++n) {
             thermo::IfaceParams P;
             memset(&P, 0, sizeof P);
@@ -440,7 +474,15 @@ extern "C" int thermo_step(void *ctx, double t, double dt, int32_t nsteps) {
             if (thermo::iface_launch(*c, P)) return THERMO_ECUDA;
             if (c->timing) API_CK(cudaEventRecord(c->events[2 * n + 1], c->stream));
             API_CK(guard_write(c, (c->cur + n + 1) & 1));
-            if ((S == 1 ? thermo::cg_launch_step(*c, n, dt) : thermo::cgb_launch_step(*c, n, dt))) return THERMO_ECUDA;
+            // states behind T^n available for the extrapolated guess
+            const int avail = extrap ? std::min(c->hist + n, c->guess) : 0;
+            if (avail > 0)
+                k_extrap<<<(unsigned)((NS + 255) / 256), 256, 0, c->stream>>>(
+                    c->d_T[(c->cur + n) & 1], c->d_T[(c->cur + n + 1) & 1], c->d_Thist, c->d_x0, NS, avail,
+                    c->guess >= 2);
+            const double *x0 = avail > 0 ? c->d_x0 : nullptr;
+            if ((S == 1 ? thermo::cg_launch_step(*c, n, dt, x0) : thermo::cgb_launch_step(*c, n, dt, x0)))
+                return THERMO_ECUDA;
         }
         if (c->timing) API_CK(cudaEventRecord(c->events[2 * nsteps], c->stream));
         int status[8];
@@ -472,6 +514,7 @@ extern "C" int thermo_step(void *ctx, double t, double dt, int32_t nsteps) {
             c->failed_relres = status[0] == 1 ? frel : NAN;
             c->cur = (c->cur + f) & 1;
             c->steps_done += f;
+            c->hist = 0;
             c->last_nsteps = f;
             if (status[0] == 2)
                 return fail(c, THERMO_EGEOM, "interface row capacity exceeded at step " + std::to_string(f));
@@ -496,6 +539,8 @@ extern "C" int thermo_step(void *ctx, double t, double dt, int32_t nsteps) {
         c->failed_scen = -1;
         c->cur = (c->cur + nsteps) & 1;
         c->steps_done += nsteps;
+        c->hist = std::min(c->hist + nsteps, 2);
+        c->hist_dt = dt;
         return THERMO_OK;
     } catch (...) {
         return fail(c, THERMO_ENOMEM, "host allocation failed");
@@ -569,6 +614,7 @@ extern "C" int thermo_set_T(void *ctx, int32_t scen, int32_t part, const double 
     if (int rc = selection(c, scen, part, n, &off, &cnt)) return rc;
     double *dst = c->d_T[c->cur] + off * c->SP + scen;
     API_CK(guard_write(c, c->cur));
+    c->hist = 0;   // the extrapolation history no longer leads to this state
     cudaMemcpyKind kind = in_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     if (c->SP == 1) API_CK(cudaMemcpyAsync(dst, in, sizeof(double) * cnt, kind, c->stream));
     else API_CK(cudaMemcpy2DAsync(dst, sizeof(double) * c->SP, in, sizeof(double), sizeof(double), cnt, kind, c->stream));

@@ -21,7 +21,7 @@ _CODES = {-1: "EINVAL", -2: "ENOMEM", -3: "ECUDA", -4: "ENOCONV", -5: "EGEOM"}
 EXPORTS = ["thermo_create_mesh", "thermo_set_bc", "thermo_step", "thermo_get_T", "thermo_set_T",
            "thermo_set_solver", "thermo_get_stats", "thermo_get_step_iters", "thermo_last_error",
            "thermo_destroy", "thermo_set_timing", "thermo_set_method", "thermo_stationary",
-           "thermo_get_T_async", "thermo_sync"]
+           "thermo_get_T_async", "thermo_sync", "thermo_set_guess"]
 
 
 class ThermoError(RuntimeError):
@@ -76,6 +76,7 @@ def load(path: str = LIB_PATH):
     L.thermo_get_T.argtypes = [vp, i32, i32, vp, i64, i32]
     L.thermo_set_T.argtypes = [vp, i32, i32, vp, i64, i32]
     L.thermo_set_solver.argtypes = [vp, d, i32]
+    L.thermo_set_guess.argtypes = [vp, i32]
     L.thermo_get_stats.argtypes = [vp, ctypes.POINTER(Stats)]
     L.thermo_get_step_iters.argtypes = [vp, ctypes.POINTER(ctypes.c_int32), i64]
     L.thermo_last_error.argtypes = [vp]
@@ -169,6 +170,10 @@ class Thermo:
 
     def set_solver(self, rtol=1e-12, maxit=0):
         self._check(load().thermo_set_solver(self.h, rtol, maxit))
+
+    def set_guess(self, order: int):
+        """CG initial guess: 0 = T^n, 1 / 2 = linear / quadratic extrapolation (thermo_set_guess)."""
+        self._check(load().thermo_set_guess(self.h, int(order)))
 
     def step(self, t: float, dt: float, nsteps: int):
         self._check(load().thermo_step(self.h, t, dt, nsteps))

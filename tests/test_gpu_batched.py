@@ -43,16 +43,20 @@ def test_batched_columns_match_oracle(S):
     assert it.shape == (20, S) and it.min() > 0
 
 
-def test_batched_equals_single_runs():
+@pytest.mark.parametrize("guess", [0, 2])
+def test_batched_equals_single_runs(guess):
     """Column k of a batched run equals a single-scenario run of scenario k (same row sums;
-    only the dot-product reduction trees differ)."""
+    only the dot-product reduction trees differ), with CG started from T^n or from the
+    extrapolated states on both sides."""
     from paper_1707_03581_b200.thermo import Thermo
     cfg = I.make_config("medium", jitter=0.1)
     scen = [_scen(k) for k in range(4)]
     tb = Thermo.from_config(cfg, scenarios=scen)
+    tb.set_guess(guess)
     tb.step(0.0, 1.0, 6)
     for k in (0, 3):
         ts = Thermo.from_config(cfg, scenarios=[scen[k]])
+        ts.set_guess(guess)
         ts.step(0.0, 1.0, 6)
         assert rel(tb.get_T(scen=k), ts.get_T()) < 1e-12
 

@@ -54,14 +54,56 @@ def test_parity_vs_oracle_cg(name, jitter):
     cfg = I.make_config(name, jitter=jitter)
     T0 = I.initial_field(cfg)[0]
     th = _thermo(cfg)
+    th.set_guess(0)   # x0 = T^n as in the oracle (reading R17), so iteration counts compare
     th.set_T(T0)
     th.step(0.0, cfg.dt, cfg.nsteps)
     Tg = th.get_T()
     Tr, st = O.run_config(cfg, T_init=T0)
     assert rel(Tg, Tr) <= TOL
     it = th.step_iters()[:, 0]
-    # same stopping rule on both sides: iteration counts agree to +-1
+    # same stopping rule and start on both sides: iteration counts agree to +-1
     assert np.abs(it - st[:, 0]).max() <= 1
+
+
+@pytest.mark.parametrize("order", [1, 2])
+def test_extrapolated_guess_parity_and_fewer_iterations(order):
+    """thermo_set_guess: CG from the extrapolated state reaches the same IE solution (same
+    stopping rule) in fewer iterations; the history restarts after thermo_set_T and after a
+    dt change (no stale state enters the guess)."""
+    cfg = I.make_config("medium", jitter=0.1)
+    n1 = 24
+    runs = {}
+    for g in (0, order):
+        th = _thermo(cfg)
+        th.set_guess(g)
+        th.step(0.0, cfg.dt, n1 // 2)
+        th.step(n1 // 2 * cfg.dt, cfg.dt, n1 - n1 // 2)   # history carried across calls
+        runs[g] = (th.get_T(), th.step_iters()[:, 0].copy(), th)
+    Tr, st = O.run_config(cfg, nsteps=n1)
+    assert rel(runs[0][0], Tr) <= TOL
+    assert rel(runs[order][0], Tr) <= TOL
+    # the second call's steps all have history: fewer iterations in total
+    assert runs[order][1].sum() < runs[0][1].sum(), (runs[order][1], runs[0][1])
+    th = runs[order][2]
+    # restart: new state, then a different dt -- both must match the oracle from that state
+    T1 = I.initial_field(cfg, seed=5)[0]
+    th.set_T(T1)
+    t1 = 3 * 0.5 * cfg.dt
+    th.step(0.0, 0.5 * cfg.dt, 3)
+    th.step(t1, 0.25 * cfg.dt, 3)
+    o = O.Oracle.from_config(cfg)
+    Ta, _ = o.step(T1, 0.0, 0.5 * cfg.dt, 3, cfg.scenarios[0])
+    Tb, _ = o.step(Ta, t1, 0.25 * cfg.dt, 3, cfg.scenarios[0])
+    assert rel(th.get_T(), Tb) <= TOL
+
+
+def test_guess_argument_errors():
+    from paper_1707_03581_b200.thermo import ThermoError
+    cfg = I.make_config("cfg0")
+    th = _thermo(cfg)
+    for bad in (-1, 3):
+        with pytest.raises(ThermoError):
+            th.set_guess(bad)
 
 
 def test_parts_and_device_copy():

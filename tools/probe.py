@@ -1,4 +1,5 @@
 """Quick timing probe: python tools/probe.py cfg1 100  (device-timed, not the bench)."""
+import os
 import sys
 import time
 
@@ -19,6 +20,8 @@ torch.cuda.synchronize()
 t2 = time.time()
 st = th.stats()
 print(f"{name}: N={cfg.n_dof} nnz={st['nnz_volume']} pad={st['nnz_volume_padded']} n_if={st['n_iface_rows']} cap={st['iface_capacity']} gen={t1-t0:.1f}s create={t2-t1:.1f}s", flush=True)
+if os.environ.get("GUESS"):
+    th.set_guess(int(os.environ["GUESS"]))
 th.set_timing(True)
 th.step(0.0, cfg.dt, 3)
 s = torch.cuda.current_stream()
