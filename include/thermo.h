@@ -191,11 +191,13 @@ typedef struct {
     double last_relres;              /* max over scenarios, last step */
     int64_t steps_done;              /* committed steps since create */
     double iface_area;               /* |Gamma_R| of scenario 0 at the last step (m^2) */
-    double ms_iface;                 /* device time of the interface kernels, last call (ms) */
+    double ms_iface;                 /* device time of the interface kernels and the initial-guess
+                                        extrapolation, last call (ms) */
     double ms_solve;                 /* device time of the CG solve kernels, last call (ms) */
     int32_t solve_grid;              /* CTAs of the persistent CG kernel */
     int32_t solve_block;             /* threads per CTA */
-    int32_t launches_per_step;       /* kernels one implicit-Euler step launches (interface + solve) */
+    int32_t launches_per_step;       /* kernels per implicit-Euler step of the last call (interface,
+                                        guess extrapolation, solve) */
 } thermo_stats;
 
 int thermo_get_stats(const void *ctx, thermo_stats *out);

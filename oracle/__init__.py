@@ -53,6 +53,7 @@ def lib():
         L.or_iface_nnz.restype = _i64
         L.or_iface_nnz.argtypes = [_p]
         L.or_get_interface.argtypes = [_p, _p, _p, _p, _p, _p]
+        L.or_set_guess.argtypes = [_p, _i32]
         L.or_step.argtypes = [_p, _d, _d, _i32, _d, _d, _d, _d, _d, _d, _d, _d, _d, _p, _i32, _d, _i32, _p]
         L.or_ie_residual_rows.argtypes = [_p, _d, _d, _d, _d, _d, _p, _p, _i64, _p, _p, _p]
         L.or_apply_system.argtypes = [_p, _d, _p, _p]
@@ -72,7 +73,7 @@ def _ptr(a: np.ndarray):
 class Oracle:
     """One coupled two-mesh system (fixed part rows first, then moving part)."""
 
-    def __init__(self, fixed, moving, nu, rho_cp, alpha_iface, iface_tag=4, robin=()):
+    def __init__(self, fixed, moving, nu, rho_cp, alpha_iface, iface_tag=4, robin=(), guess=0):
         L = lib()
         self._keep = []
 
@@ -95,10 +96,17 @@ class Oracle:
         self.nf = int(L.or_n_fixed(h))
         for r in robin:
             self.set_robin(r.part, r.tag, r.alpha, r.T_ref, r.grad)
+        if guess:
+            self.set_guess(guess)
 
     @classmethod
-    def from_config(cls, cfg):
-        return cls(cfg.fixed, cfg.moving, cfg.nu, cfg.rho_cp, cfg.alpha_iface, cfg.iface_tag, cfg.robin)
+    def from_config(cls, cfg, guess=0):
+        return cls(cfg.fixed, cfg.moving, cfg.nu, cfg.rho_cp, cfg.alpha_iface, cfg.iface_tag, cfg.robin, guess)
+
+    def set_guess(self, order: int):
+        """CG start of step(): 0 = T^n, 1 / 2 = linear / quadratic extrapolation (or_set_guess)."""
+        if lib().or_set_guess(self.h, int(order)):
+            raise ValueError("oracle: " + lib().or_last_error().decode())
 
     def __del__(self):
         if getattr(self, "h", None):
@@ -230,9 +238,9 @@ Oracle.step_sdc = _step_sdc
 
 
 def run_config(cfg, scen_index: int = 0, T_init: Optional[np.ndarray] = None, nsteps: Optional[int] = None,
-               solver: str = "cg", t0: float = 0.0):
+               solver: str = "cg", t0: float = 0.0, guess: int = 0):
     """Oracle run of one scenario of a config from T0 (uniform) or T_init."""
-    o = Oracle.from_config(cfg)
+    o = Oracle.from_config(cfg, guess)
     T = np.full(o.n, cfg.T0) if T_init is None else np.array(T_init, dtype=np.float64)
     return o.step(T, t0, cfg.dt, cfg.nsteps if nsteps is None else nsteps,
                   cfg.scenarios[scen_index], solver=solver)

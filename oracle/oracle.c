@@ -73,6 +73,12 @@ struct or_sys {
     int32_t *icol;
     double *ival, *bG, iarea;
     double mass;          /* coefficient of M_L in the system: 1 (implicit Euler), 0 (stationary) */
+    /* CG start of or_step (or_set_guess): 0 = T^n; 1, 2 = polynomial extrapolation of the last
+     * committed states.  h0 = the last state or_step returned, h1 = the one before, h2 = the one
+     * before that; hist = how many states behind h0 are valid (0..2) for step size hist_dt */
+    int guess, hist;
+    double hist_dt;
+    double *h0, *h1, *h2;
 };
 
 /* ------------------------------------------------------------------------------------ */
@@ -374,6 +380,7 @@ void or_destroy(or_sys *s) {
         for (int64_t i = 0; i < s->n; i++) { free(s->rows[i].col); free(s->rows[i].val); }
     free(s->rows);
     free(s->irowptr); free(s->icol); free(s->ival); free(s->bG);
+    free(s->h0); free(s->h1); free(s->h2);
     free(s);
 }
 
@@ -690,6 +697,18 @@ static int dense_cholesky_solve(const or_sys *s, double dt, const double *b, dou
     return 0;
 }
 
+int or_set_guess(or_sys *s, int32_t order) {
+    if (order < 0 || order > 2) { set_err("guess order must be 0, 1 or 2"); return -1; }
+    if (order > 0 && !s->h0) {
+        size_t bytes = sizeof(double) * (size_t)s->n;
+        s->h0 = malloc(bytes); s->h1 = malloc(bytes); s->h2 = malloc(bytes);
+        if (!s->h0 || !s->h1 || !s->h2) { set_err("out of memory"); return -2; }
+    }
+    s->guess = order;
+    s->hist = 0;
+    return 0;
+}
+
 int or_step(or_sys *s, double t, double dt, int32_t nsteps,
             double s0, double amp, double period, double dx, double dy, double dz,
             double eta0, double eta_amp, double eta_period,
@@ -698,6 +717,10 @@ int or_step(or_sys *s, double t, double dt, int32_t nsteps,
     double *b = malloc(sizeof *b * (size_t)n), *x = malloc(sizeof *x * (size_t)n);
     if (!b || !x) return -2;
     int rc = 0;
+    /* the extrapolation history continues only from the state this function last returned,
+     * with the same step size */
+    if (s->guess > 0 && !(s->hist > 0 && dt == s->hist_dt && memcmp(T, s->h0, sizeof(double) * (size_t)n) == 0))
+        s->hist = 0;
     for (int32_t step = 0; step < nsteps; step++) {
         /* reading R3: fully implicit, K, b_G, eta and s all at t' = t + (n+1) dt */
         double tp = t + (double)(step + 1) * dt;
@@ -707,7 +730,13 @@ int or_step(or_sys *s, double t, double dt, int32_t nsteps,
         system_rhs(s, dt, T, b);
         double relres = 0.0, truerel = 0.0;
         int64_t it = 0;
-        memcpy(x, T, sizeof *x * (size_t)n);   /* x0 = T^n */
+        /* CG start: x0 = T^n, or the extrapolation of the last states (same IE system and
+         * stopping rule; reading R17):
+         *   order 1:  x0 = T^n + (T^n - T^{n-1}),   order 2:  x0 = T^{n-2} + 3 (T^n - T^{n-1}) */
+        int avail = s->guess < s->hist ? s->guess : s->hist;
+        if (avail == 0) memcpy(x, T, sizeof *x * (size_t)n);
+        else if (avail == 1) for (int64_t i = 0; i < n; i++) x[i] = T[i] + (T[i] - s->h1[i]);
+        else for (int64_t i = 0; i < n; i++) x[i] = s->h2[i] + 3.0 * (T[i] - s->h1[i]);
         if (solver == 1) {
             if (dense_cholesky_solve(s, dt, b, x)) { rc = -3; break; }
             double *q = malloc(sizeof *q * (size_t)n);
@@ -726,8 +755,20 @@ int or_step(or_sys *s, double t, double dt, int32_t nsteps,
             stats[4 * step + 3] = s->iarea;
         }
         if (it < 0) { rc = -4; break; }
+        if (s->guess > 0) {   /* shift the history: h2 <- h1 <- T^n */
+            double *tmp = s->h2;
+            s->h2 = s->h1;
+            s->h1 = tmp;
+            memcpy(s->h1, T, sizeof *T * (size_t)n);
+        }
         memcpy(T, x, sizeof *T * (size_t)n);
+        if (s->guess > 0) {
+            memcpy(s->h0, T, sizeof *T * (size_t)n);
+            s->hist = s->hist < 2 ? s->hist + 1 : 2;
+            s->hist_dt = dt;
+        }
     }
+    if (rc) s->hist = 0;
     free(b); free(x);
     return rc;
 }

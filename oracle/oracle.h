@@ -77,6 +77,14 @@ int or_step(or_sys *s, double t, double dt, int32_t nsteps,
             double eta0, double eta_amp, double eta_period,
             double *T, int32_t solver, double rtol, int32_t maxit, double *stats);
 
+/* CG start of or_step (default 0): 0 = x0 = T^n; 1 = T^n + (T^n - T^{n-1}); 2 = T^{n-2} +
+ * 3 (T^n - T^{n-1}), the polynomial extrapolation of the last committed states (DESIGN.md
+ * reading R17: the start is not part of the method; the CUDA path defaults to order 2).  The
+ * history continues across or_step calls only when T is bitwise the state the previous call
+ * returned and dt is unchanged; it restarts otherwise (lower orders until it has filled).
+ * Returns 0, or -1 for another order. */
+int or_set_guess(or_sys *s, int32_t order);
+
 /* Residual rows of the IE system for given T^n, T^{n+1}: res[k] = (K~ T1 - b)[rows[k]],
  * with the system assembled at offset o, eta (both given).  Also returns ||b||_2 in bnorm. */
 /* Stationary state at rest (reading R19): -(A + B_env [+ K_G(t)]) T = b_env

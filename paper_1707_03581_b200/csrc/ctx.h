@@ -141,6 +141,7 @@ struct Ctx {
 
     // stats of the last thermo_step
     int last_nsteps = 0;
+    int64_t last_launches = 0;       // kernels launched by the last implicit-Euler thermo_step
     std::vector<int32_t> h_iters;
     std::vector<double> h_relres, h_area;
     int64_t steps_done = 0;

@@ -382,6 +382,7 @@ extern "C" int thermo_step(void *ctx, double t, double dt, int32_t nsteps) {
     try {
         const int S = c->S;
         if (c->method >= 1 || c->hist_dt != dt) c->hist = 0;   // extrapolation needs equal IE steps
+        c->last_launches = 0;
         if (c->built_dt != dt) {
             if (thermo::build_operator(*c, dt)) return THERMO_ECUDA;
             if (S > 1 && thermo::cgb_prepare(*c)) return THERMO_ECUDA;
@@ -466,24 +467,31 @@ extern "C" int thermo_step(void *ctx, double t, double dt, int32_t nsteps) {
             API_CK(cudaMalloc(&c->d_Thist, sizeof(double) * (NS + 16)));
             API_CK(cudaMemsetAsync(c->d_Thist, 0, sizeof(double) * (NS + 16), c->stream));
         }
+        int64_t launches = 0;
         for (int n = 0; n < nsteps; ++n) {
             thermo::IfaceParams P;
             memset(&P, 0, sizeof P);
             thermo::iface_params(*c, P, c->d_step_sc + 4 * (size_t)n * S, dt);
+            // timing: [events 2n, 2n+1) = guess extrapolation + interface kernels, [2n+1, 2n+2) = the solve
             if (c->timing) API_CK(cudaEventRecord(c->events[2 * n], c->stream));
-            if (thermo::iface_launch(*c, P)) return THERMO_ECUDA;
-            if (c->timing) API_CK(cudaEventRecord(c->events[2 * n + 1], c->stream));
             API_CK(guard_write(c, (c->cur + n + 1) & 1));
             // states behind T^n available for the extrapolated guess
             const int avail = extrap ? std::min(c->hist + n, c->guess) : 0;
-            if (avail > 0)
+            if (avail > 0) {
                 k_extrap<<<(unsigned)((NS + 255) / 256), 256, 0, c->stream>>>(
                     c->d_T[(c->cur + n) & 1], c->d_T[(c->cur + n + 1) & 1], c->d_Thist, c->d_x0, NS, avail,
                     c->guess >= 2);
+                API_CK(cudaGetLastError());
+                ++launches;
+            }
+            if (thermo::iface_launch(*c, P)) return THERMO_ECUDA;
+            if (c->timing) API_CK(cudaEventRecord(c->events[2 * n + 1], c->stream));
             const double *x0 = avail > 0 ? c->d_x0 : nullptr;
             if ((S == 1 ? thermo::cg_launch_step(*c, n, dt, x0) : thermo::cgb_launch_step(*c, n, dt, x0)))
                 return THERMO_ECUDA;
+            launches += 1 + (c->n_if ? 2 : 0);
         }
+        c->last_launches = launches;
         if (c->timing) API_CK(cudaEventRecord(c->events[2 * nsteps], c->stream));
         int status[8];
         c->h_iters.assign((size_t)nsteps * S, 0);
@@ -655,7 +663,8 @@ extern "C" int thermo_get_stats(const void *ctx, thermo_stats *out) {
     out->ms_solve = c->ms_solve;
     out->solve_grid = c->cg_grid;
     out->solve_block = c->cg_block;
-    out->launches_per_step = 1 + (c->n_if ? 2 : 0);
+    out->launches_per_step = c->last_nsteps > 0 && c->last_launches > 0 ? (int32_t)(c->last_launches / c->last_nsteps)
+                                                                          : 1 + (c->n_if ? 2 : 0);
     return THERMO_OK;
 }
 

@@ -84,6 +84,13 @@ def test_extrapolated_guess_parity_and_fewer_iterations(order):
     assert rel(runs[order][0], Tr) <= TOL
     # the second call's steps all have history: fewer iterations in total
     assert runs[order][1].sum() < runs[0][1].sum(), (runs[order][1], runs[0][1])
+    # the oracle with the same start (or_set_guess, history across its calls as well) takes
+    # the same iterations and lands on the same field to rounding
+    o = O.Oracle.from_config(cfg, order)
+    Ta, _ = o.step(np.full(o.n, cfg.T0), 0.0, cfg.dt, n1 // 2, cfg.scenarios[0])
+    Tg, sg = o.step(Ta, n1 // 2 * cfg.dt, cfg.dt, n1 - n1 // 2, cfg.scenarios[0])
+    assert np.abs(runs[order][1] - sg[:, 0]).max() <= 1
+    assert rel(runs[order][0], Tg) <= 1e-12
     th = runs[order][2]
     # restart: new state, then a different dt -- both must match the oracle from that state
     T1 = I.initial_field(cfg, seed=5)[0]

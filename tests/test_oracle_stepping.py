@@ -153,3 +153,43 @@ def test_implicit_euler_stable_far_beyond_explicit_limit():
     dt = 1e4 * c.rho_cp * h * h / c.nu
     T, st = o.step(np.full(o.n, 24.0), 0.0, dt, 3, c.scenarios[0])
     assert np.isfinite(T).all() and T.min() > 17.0 and T.max() < 60.0
+
+
+@pytest.mark.parametrize("order", [1, 2])
+def test_extrapolated_start(order):
+    """or_set_guess (reading R17: the CG start is not part of the method): CG from the
+    extrapolated states reaches the dense-Cholesky solution of every step to the same bound as
+    from T^n, with fewer iterations; the history carries across calls only from the state the
+    previous call returned (15 + 15 steps = 30 steps bitwise), and a different state or dt
+    restarts it (bitwise equal to a fresh oracle)."""
+    c = I.make_config("cfg0")
+    sc = c.scenarios[0]
+    T0 = np.full(c.n_dof, c.T0)
+    n = 30
+    Td, _ = O.Oracle.from_config(c).step(T0, 0.0, c.dt, n, sc, solver="cholesky")
+    T_0, s_0 = O.Oracle.from_config(c).step(T0, 0.0, c.dt, n, sc)
+    og = O.Oracle.from_config(c, order)
+    T_g, s_g = og.step(T0, 0.0, c.dt, n, sc)
+    assert abs(T_0 - Td).max() / abs(Td).max() < 1e-10
+    assert abs(T_g - Td).max() / abs(Td).max() < 1e-10
+    assert s_g[:, 0].sum() <= s_0[:, 0].sum()
+    assert np.all(s_g[:, 2] < 2e-12)                     # true residual at exit
+    cs = I.make_config("small", jitter=0.1)              # large enough to save iterations
+    Ts0 = np.full(cs.n_dof, cs.T0)
+    _, a = O.Oracle.from_config(cs).step(Ts0, 0.0, cs.dt, 30, cs.scenarios[0])
+    _, b = O.Oracle.from_config(cs, order).step(Ts0, 0.0, cs.dt, 30, cs.scenarios[0])
+    assert b[:, 0].sum() < a[:, 0].sum()
+    o2 = O.Oracle.from_config(c, order)
+    Ta, _ = o2.step(T0, 0.0, c.dt, n // 2, sc)
+    Tb, _ = o2.step(Ta, n // 2 * c.dt, c.dt, n - n // 2, sc)
+    assert np.array_equal(Tb, T_g)
+    # restart: another state, then another dt
+    T1 = I.initial_field(c)[0]
+    Tc, _ = o2.step(T1, 0.0, c.dt, 5, sc)
+    Tf, _ = O.Oracle.from_config(c, order).step(T1, 0.0, c.dt, 5, sc)
+    assert np.array_equal(Tc, Tf)
+    Te, _ = o2.step(Tc, 5 * c.dt, 0.5 * c.dt, 4, sc)
+    Tf2, _ = O.Oracle.from_config(c, order).step(Tc, 5 * c.dt, 0.5 * c.dt, 4, sc)
+    assert np.array_equal(Te, Tf2)
+    with pytest.raises(ValueError):
+        og.set_guess(3)
