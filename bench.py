@@ -255,8 +255,8 @@ def run_thermo(args):
         traffic = prof.get("dram_bytes_per_launch")
         if prof.get("cg_iterations") and S == 1:
             # actual DRAM bytes per CG iteration (ncu, one launch) x this run's iterations / time
-            per_it = traffic / (prof["cg_iterations"] + 0.76)   # phase 0 ~ 0.76 iteration (trace)
-            gbs = per_it * (float(iters.sum()) + 0.76 * K) / (st["ms_solve"] * 1e-3) / 1e9
+            per_it = traffic / (prof["cg_iterations"] + 0.82)   # phase 0 ~ 0.82 iteration (trace)
+            gbs = per_it * (float(iters.sum()) + 0.82 * K) / (st["ms_solve"] * 1e-3) / 1e9
             dram = {"actual_dram_gbs_est": gbs, "actual_dram_frac_est": gbs / peak,
                     "actual_bytes_per_iter_ncu": per_it, "algorithmic_bytes_per_iter": per_iter}
     line = {

@@ -22,11 +22,11 @@ def main(path, out=None):
     for k in sorted(tot, key=lambda k: -tot[k]):
         lines.append(f"{k[:60]:60s} {cnt[k]:8d} {tot[k]:12.1f} {tot[k] / cnt[k]:10.1f} {tot[k] / T * 100:6.1f}%")
     # the time-step kernels only (setup / assembly launches excluded): the step's split
-    step = {k: v for k, v in tot.items() if any(x in k for x in ("k_cg_step", "k_cgb_step", "k_pairs", "k_rows"))}
+    step = {k: v for k, v in tot.items() if any(x in k for x in ("k_cg_step", "k_cgb_step", "k_pairs", "k_rows", "k_extrap"))}
     S = sum(step.values())
     if S > 0:
         lines.append("")
-        lines.append("time-step kernels only (interface pairs / rows + CG solve):")
+        lines.append("time-step kernels only (interface pairs / rows, guess extrapolation, CG solve):")
         for k in sorted(step, key=lambda k: -step[k]):
             lines.append(f"{k[:60]:60s} {cnt[k]:8d} {step[k]:12.1f} {step[k] / cnt[k]:10.1f} {step[k] / S * 100:6.1f}%")
     txt = "\n".join(lines)
