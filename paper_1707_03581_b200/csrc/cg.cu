@@ -66,6 +66,7 @@ struct CGParams {
     const double *X0;          // optional initial guess (extrapolated state); nullptr: x0 = T_in
     const double *rhs;         // optional explicit right-hand side (MRSDC implicit solves)
     double *T_out, *z, *pa, *pb, *q;
+    double *z2, *q2;           // FUSED: second buffer set of z and q' (p uses pa / pb)
     double *partials;
     int *status;
     double *fail_relres;
@@ -83,8 +84,9 @@ struct CGParams {
     const int32_t *chunk_lown;  // KIND 2: window-local index of the chunk's first row
     const double *pf[4];       // vectors whose leading edge is prefetched into L2
     int npf;
-    const double *wv[1];       // KIND 2: the vector staged through the window (nwv = 1)
+    const double *wv[3];       // KIND 2: vectors staged through the window (nwv <= nwin)
     int nwv;
+    int nwin;                  // KIND 2: window slots of the stage layout (1, FUSED: 3)
     const double *ownv;        // KIND 2: vector of which only the chunk's own rows are staged
                                // (after the window, W * 32 rows)
     unsigned long long *trace; // optional: %globaltimer after every grid barrier (CTA 0)
@@ -178,6 +180,22 @@ __device__ __forceinline__ double ell_row(const CGParams &P, int ik, const doubl
     return acc;
 }
 
+// FUSED: interface row applied to p_new = beta p + (z - alpha q') (the owner's formula)
+__device__ __forceinline__ double ell_row3(const CGParams &P, int ik, const double *z, const double *q,
+                                           const double *p, double alpha, double beta, int64_t row, double *self) {
+    const int cnt = P.ell_cnt[ik];
+    double acc = 0.0;
+    for (int c = 0; c < cnt; ++c) {
+        const int64_t e = (int64_t)c * P.n_if + ik;
+        const int j = P.ell_col[e];
+        const double y = fma(beta, p[j], fma(-alpha, q[j], z[j]));
+        const double v = P.ell_val[e];
+        acc = fma(v, y, acc);
+        if (j == row) *self += v;
+    }
+    return acc;
+}
+
 // ---------------------------------------------------------------------------------
 // row sources: sum_k val_k * (x1[col_k] + beta * x2[col_k]) over one sliced-ELL row whose
 // entries sit at stride 32.  All sources add in the same order (k ascending, fused
@@ -187,6 +205,9 @@ struct SrcGlobal {   // KIND 0: matrix streamed from HBM, gathers from L1/L2
     const int32_t *cp;
     const double *vp;
     uint64_t pol;
+    // FUSED kernels are KIND 2 only; these keep the generic sweep body compilable
+    __device__ __forceinline__ double ownw(int) const { return 0.0; }
+    __device__ __forceinline__ double dot3(int, double, double) const { return 0.0; }
     // own-row value of the first / second gathered vector
     __device__ __forceinline__ double own1(const double *g, int64_t i) const { return g[i]; }
     __device__ __forceinline__ double own2(const double *g, int64_t i) const { return g[i]; }
@@ -220,6 +241,9 @@ struct SrcGlobal {   // KIND 0: matrix streamed from HBM, gathers from L1/L2
 struct SrcRing {     // KIND 1: matrix in the shared-memory ring, gathers from L1/L2
     const int32_t *cp;
     const double *vp;
+    // FUSED kernels are KIND 2 only; these keep the generic sweep body compilable
+    __device__ __forceinline__ double ownw(int) const { return 0.0; }
+    __device__ __forceinline__ double dot3(int, double, double) const { return 0.0; }
     __device__ __forceinline__ double own1(const double *g, int64_t i) const { return g[i]; }
     __device__ __forceinline__ double own2(const double *g, int64_t i) const { return g[i]; }
     __device__ __forceinline__ double first() const { return vp[0]; }
@@ -245,15 +269,19 @@ struct SrcRing {     // KIND 1: matrix in the shared-memory ring, gathers from L
 struct SrcWin {      // KIND 2: matrix and gathered vectors in shared memory
     const uint16_t *lp;
     const double *vp;
-    const double *w1, *w2;
+    const double *w1;    // window slot 0 (slots 1, 2 at +wstride, +2 wstride: FUSED)
+    const double *wo;    // own-row block (ownv)
     int lown;            // window-local index of this lane's own row (the chunk's rows form
                          // one contiguous block of its column set)
     int lown2;           // index of this lane's own row in the own-row block (ownv)
+    int wstride;         // window slot stride (entries)
     __device__ __forceinline__ double own1(const double *, int64_t) const { return w1[lown]; }
-    __device__ __forceinline__ double own2(const double *, int64_t) const { return w2[lown2]; }
+    __device__ __forceinline__ double own2(const double *, int64_t) const { return wo[lown2]; }
+    __device__ __forceinline__ double ownw(int slot) const { return w1[slot * wstride + lown]; }
     __device__ __forceinline__ double first() const { return vp[0]; }
     template <bool kTwo>
     __device__ __forceinline__ double dot(int w, const double *, const double *, double beta) const {
+        const double *w2 = w1 + wstride;
         double acc = 0.0;
         int k = 0;
         for (; k + 8 <= w; k += 8) {
@@ -269,6 +297,29 @@ struct SrcWin {      // KIND 2: matrix and gathered vectors in shared memory
         for (; k < w; ++k) {
             const int c0 = lp[32 * k];
             const double y = kTwo ? fma(beta, w2[c0], w1[c0]) : w1[c0];
+            acc = fma(vp[32 * k], y, acc);
+        }
+        return acc;
+    }
+    // FUSED: sum_k val_k * p_new[col_k] with p_new = beta p + (z - alpha q') formed from the
+    // windows of z (slot 0), q' (slot 1), p (slot 2) -- the owner's formula, bit for bit
+    __device__ __forceinline__ double dot3(int w, double alpha, double beta) const {
+        const double *w2 = w1 + wstride, *w3 = w1 + 2 * wstride;
+        double acc = 0.0;
+        int k = 0;
+        for (; k + 8 <= w; k += 8) {
+            int c[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) c[u] = lp[32 * (k + u)];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const double y = fma(beta, w3[c[u]], fma(-alpha, w2[c[u]], w1[c[u]]));
+                acc = fma(vp[32 * (k + u)], y, acc);
+            }
+        }
+        for (; k < w; ++k) {
+            const int c0 = lp[32 * k];
+            const double y = fma(beta, w3[c0], fma(-alpha, w2[c0], w1[c0]));
             acc = fma(vp[32 * k], y, acc);
         }
         return acc;
@@ -382,12 +433,14 @@ __device__ __forceinline__ void sweep(const CGParams &P, Ring &R, Body &&body) {
             }
             __syncwarp();
             if (KIND == 2 && nruns && !(P.debug & 2)) {
-                if (P.nwv)
-                    bulk_g2s_nohint(sb + R.win_off + (size_t)woff * 8, P.wv[0] + cur.run.x, (uint32_t)cur.run.y * 8u,
-                                    &R.full[st]);
+#pragma unroll
+                for (int v = 0; v < 3; ++v)
+                    if (v < P.nwv)
+                        bulk_g2s_nohint(sb + R.win_off + ((size_t)v * P.win_cap + woff) * 8, P.wv[v] + cur.run.x,
+                                        (uint32_t)cur.run.y * 8u, &R.full[st]);
             }
             if (KIND == 2 && P.ownv && lane == 1 && !(P.debug & 2))   // own rows only, second slot
-                bulk_g2s_nohint(sb + R.win_off + (size_t)P.win_cap * 8, P.ownv + ch * W * 32,
+                bulk_g2s_nohint(sb + R.win_off + (size_t)P.nwin * P.win_cap * 8, P.ownv + ch * W * 32,
                                 own_bytes(P, ch, W), &R.full[st]);
             if (lane == 0 && !(P.debug & 4)) {
                 prefetch_edge<W>(P, cur.hi_own);
@@ -429,8 +482,8 @@ __device__ __forceinline__ void sweep(const CGParams &P, Ring &R, Body &&body) {
                     // row N - 1 instead, whose value they discard
                     const int64_t irow = 32 * s + lane;
                     const int pad = irow > P.N - 1 ? (int)(irow - (P.N - 1)) : 0;
-                    SrcWin src{lc + o0 + lane, vals + o0 + lane, w1, w1 + P.win_cap, hdr[29] + 32 * wg + lane - pad,
-                               32 * wg + lane - pad};
+                    SrcWin src{lc + o0 + lane, vals + o0 + lane, w1, w1 + (size_t)P.nwin * P.win_cap,
+                               hdr[29] + 32 * wg + lane - pad, 32 * wg + lane - pad, P.win_cap};
                     body(s, src, (o1 - o0) >> 5, hdr[16 + wg], hdr[17 + wg]);
                 } else {
                     const int32_t *cols = reinterpret_cast<const int32_t *>(sb + R.col_off);
@@ -524,7 +577,7 @@ __device__ __forceinline__ void sweep_u(const CGParams &P, Ring &R, const double
 
 __host__ __device__ constexpr int cg_threads(int kind, int W, int NG) { return kind == 0 ? THERMO_BLOCK : (W * NG + 1) * 32; }
 
-template <int KIND, int W, int NG>
+template <int KIND, int W, int NG, bool FUSED = false>
 __global__ void __launch_bounds__(cg_threads(KIND, W, NG), KIND == 0 ? 2 : 1) k_cg_step(CGParams P) {
     const int NS = P.nstages;
     __shared__ double red_smem[THERMO_RED_SMEM];
@@ -549,7 +602,7 @@ __global__ void __launch_bounds__(cg_threads(KIND, W, NG), KIND == 0 ? 2 : 1) k_
         R.stage = ring_raw + 128;
         R.col_off = CG_HDR + (size_t)P.stage_entries * 8;
         R.win_off = align16(R.col_off + (size_t)P.stage_entries * (KIND == 2 ? 2 : 4));
-        R.stage_bytes = align16(R.win_off + (KIND == 2 ? (size_t)(P.win_cap + 32 * W) * 8 : 0));
+        R.stage_bytes = align16(R.win_off + (KIND == 2 ? (size_t)(P.nwin * P.win_cap + 32 * W) * 8 : 0));
         if (threadIdx.x == 0) {
             for (int s = 0; s < NS; ++s) {
                 mbar_init(&R.full[s], 1);
@@ -609,111 +662,206 @@ __global__ void __launch_bounds__(cg_threads(KIND, W, NG), KIND == 0 ? 2 : 1) k_
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nthr = (int64_t)G * blockDim.x;
     int it = 0;
-    while (!conv && it < P.maxit) {
-        // ---- S: q = K~ p (the only gathered vector); q' = D^{-1} q with the diagonal d taken
-        // from the row's own entries; partials of p.q and of the expansions of the next r.z and r.r
-        //   z_new = z - alpha q', r_new = z_new d:  r.z = z^2 d - 2 alpha z q + alpha^2 q^2 / d,
-        //   r.r = (z d)^2 - 2 alpha z d q + alpha^2 q^2,
-        // so beta is known before the U phase, which forms the next direction itself
-        double red[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-        const bool first = it == 0;
-        P.pf[0] = p;
-        P.npf = P.prefetch ? 1 : 0;
-        P.wv[0] = p;
-        P.nwv = 1;
-        P.ownv = P.z;
-        sweep<KIND, W, NG>(P, R, [&](int64_t s, const auto &src, int w, int ib, int ie) {
-            const int64_t i = 32 * s + lane;
-            const int64_t ii = i < N ? i : N - 1;
-            const double pi = src.own1(p, ii);      // issued before the row sum
-            const double zo = src.own2(P.z, ii);
-            const int ik = iface_index_r(P, ib, ie, i, lane);
-            double dg = src.first();   // the diagonal (entry 0) + the interface self term
-            double acc = src.template dot<false>(w, p, nullptr, 0.0);
-            if (ik >= 0) acc += ell_row<false>(P, ik, p, nullptr, 0.0, ii, &dg);
-            if (i < N) {
-                const double qs = acc / dg;
-                const double zd = zo * dg;
-                P.q[i] = qs;
-                red[0] = fma(pi, acc, red[0]);
-                red[1] = fma(zo, zd, red[1]);
-                red[2] = fma(zo, acc, red[2]);
-                red[3] = fma(acc, qs, red[3]);
-                red[4] = fma(zd, zd, red[4]);
-                red[5] = fma(zd, acc, red[5]);
-                red[6] = fma(acc, acc, red[6]);
+    if constexpr (FUSED) {
+        // One grid barrier per iteration: S(k) gathers the iteration-(k-1) state z, q', p of
+        // buffer set (k-1)&1 and forms p_k = beta p + (z - alpha q') for every column itself,
+        // so the update of iteration k-1 (x, z, p of its own rows) happens inside S(k); S(k)
+        // writes z_k, p_k, q'_k to set k&1 (nobody reads that set during S(k)).  The CTA
+        // partials alternate between two slot groups (a fast CTA's S(k+1) must not overwrite
+        // what a slow CTA still reads).  Same formulas, same order: bitwise the unfused result.
+        double alpha = 0.0, beta = 0.0;
+        while (!conv && it < P.maxit) {
+            const bool first = it == 0;
+            const int sn = it & 1;   // state set written (read: the other one)
+            const double *const zr = sn ? P.z : P.z2, *const qr = sn ? P.q : P.q2, *const pr = sn ? P.pa : P.pb;
+            double *const zw = sn ? P.z2 : P.z, *const qw = sn ? P.q2 : P.q, *const pw = sn ? P.pb : P.pa;
+            double red[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+            P.npf = 0;
+            if (first) {
+                P.wv[0] = P.pa;   // p_0 = z_0; z_0's own rows come as the own-row block
+                P.nwv = 1;
+                P.ownv = P.z;
+            } else {
+                P.wv[0] = zr; P.wv[1] = qr; P.wv[2] = pr;
+                P.nwv = 3;
+                P.ownv = xsrc;
             }
-        });
-        P.ownv = nullptr;
-        cta_reduce_store<7>(red, red_smem, P.partials, 4);
-        grid.sync();
-        if (tr_on && ntr < 1000) P.trace[ntr++] = gtimer();
-        double t7[7];
-        grid_total<7>(P.partials, G, 4, red_smem, t7);
-        // t7[4] = sum (z d)^2 is the current r.r computed directly: if an expansion below was
-        // too close to its rounding noise to be trusted, the convergence test lands here, one
-        // S phase later, before the update
-        if (!first && !P.debug) {
-            rr = t7[4];
-            if (rr <= tol2) { conv = true; break; }
-        }
-        const double alpha = rho / t7[0];
-        const double rz_new = fma(alpha, fma(alpha, t7[3], -2.0 * t7[2]), t7[1]);
-        const double rr_new = fma(alpha, fma(alpha, t7[6], -2.0 * t7[5]), t7[4]);
-        // rounding noise of the expansion (terms of size r.r of this iteration)
-        const double rr_noise = 1e-13 * (t7[4] + fabs(2.0 * alpha * t7[5]) + alpha * alpha * t7[6]);
-        const double beta = rz_new / rho;
-        // ---- U: x += alpha p, z -= alpha q', p = z + beta p (streams only, no reduction)
-        if constexpr (KIND != 0) {
-            const double *const usrc[4] = {p, P.q, xsrc, P.z};
-            sweep_u<W, NG>(P, R, usrc, [&](int64_t i, double pv, double qv, double xv, double zv) {
-                P.T_out[i] = fma(alpha, pv, xv);
-                const double zn = fma(-alpha, qv, zv);
-                P.z[i] = zn;
-                p[i] = fma(beta, pv, zn);
-            });
-        } else {   // element pairs with 16-byte loads, two pairs in flight per thread and trip
-            const int64_t npair = N >> 1;
-            double2 *p2 = reinterpret_cast<double2 *>(p);
-            const double2 *q2 = reinterpret_cast<const double2 *>(P.q);
-            const double2 *x2 = reinterpret_cast<const double2 *>(xsrc);
-            double2 *z2 = reinterpret_cast<double2 *>(P.z);
-            double2 *o2 = reinterpret_cast<double2 *>(P.T_out);
-            auto upd = [&](double2 pv, double2 qv, double2 xv, double2 zv, int64_t j) {
-                o2[j] = make_double2(fma(alpha, pv.x, xv.x), fma(alpha, pv.y, xv.y));
-                const double2 zn = make_double2(fma(-alpha, qv.x, zv.x), fma(-alpha, qv.y, zv.y));
-                z2[j] = zn;
-                p2[j] = make_double2(fma(beta, pv.x, zn.x), fma(beta, pv.y, zn.y));
-            };
-            constexpr int UU = 2;
-            int64_t j = tid;
-            for (; j + (UU - 1) * nthr < npair; j += UU * nthr) {
-                double2 pv[UU], qv[UU], xv[UU], zv[UU];
-#pragma unroll
-                for (int u = 0; u < UU; ++u) {
-                    const int64_t jj = j + u * nthr;
-                    pv[u] = ld_cg2(p2 + jj); qv[u] = ld_cg2(q2 + jj); xv[u] = ld_cg2(x2 + jj); zv[u] = ld_cg2(z2 + jj);
+            sweep<KIND, W, NG>(P, R, [&](int64_t s, const auto &src, int w, int ib, int ie) {
+                const int64_t i = 32 * s + lane;
+                const int64_t ii = i < N ? i : N - 1;
+                double zo, pi, xn = 0.0;
+                if (first) {
+                    pi = src.own1(nullptr, ii);
+                    zo = src.own2(nullptr, ii);
+                } else {
+                    const double z0 = src.ownw(0), q0 = src.ownw(1), p0 = src.ownw(2), x0v = src.own2(nullptr, ii);
+                    zo = fma(-alpha, q0, z0);
+                    pi = fma(beta, p0, zo);
+                    xn = fma(alpha, p0, x0v);
                 }
-#pragma unroll
-                for (int u = 0; u < UU; ++u) upd(pv[u], qv[u], xv[u], zv[u], j + u * nthr);
+                const int ik = iface_index_r(P, ib, ie, i, lane);
+                double dg = src.first();
+                double acc;
+                if (first) {
+                    acc = src.template dot<false>(w, nullptr, nullptr, 0.0);
+                    if (ik >= 0) acc += ell_row<false>(P, ik, P.pa, nullptr, 0.0, ii, &dg);
+                } else {
+                    acc = src.dot3(w, alpha, beta);
+                    if (ik >= 0) acc += ell_row3(P, ik, zr, qr, pr, alpha, beta, ii, &dg);
+                }
+                if (i < N) {
+                    const double qv = acc / dg;
+                    const double zd = zo * dg;
+                    qw[i] = qv;
+                    if (!first) {
+                        zw[i] = zo;
+                        pw[i] = pi;
+                        P.T_out[i] = xn;
+                    }
+                    red[0] = fma(pi, acc, red[0]);
+                    red[1] = fma(zo, zd, red[1]);
+                    red[2] = fma(zo, acc, red[2]);
+                    red[3] = fma(acc, qv, red[3]);
+                    red[4] = fma(zd, zd, red[4]);
+                    red[5] = fma(zd, acc, red[5]);
+                    red[6] = fma(acc, acc, red[6]);
+                }
+            });
+            P.ownv = nullptr;
+            const int slot = 4 + 7 * sn;
+            cta_reduce_store<7>(red, red_smem, P.partials, slot);
+            grid.sync();
+            if (tr_on && ntr < 1000) P.trace[ntr++] = gtimer();
+            double t7[7];
+            grid_total<7>(P.partials, G, slot, red_smem, t7);
+            if (!first) xsrc = P.T_out;   // x_it is complete
+            if (!first && !P.debug) {
+                rr = t7[4];
+                if (rr <= tol2) { conv = true; break; }
             }
-            for (; j < npair; j += nthr) upd(p2[j], q2[j], x2[j], z2[j], j);
-            if ((N & 1) && tid == nthr - 1) {
-                const int64_t i = N - 1;
-                P.T_out[i] = fma(alpha, p[i], xsrc[i]);
-                const double zn = fma(-alpha, P.q[i], P.z[i]);
-                P.z[i] = zn;
-                p[i] = fma(beta, p[i], zn);
+            const double an = rho / t7[0];
+            const double rz_new = fma(an, fma(an, t7[3], -2.0 * t7[2]), t7[1]);
+            const double rr_new = fma(an, fma(an, t7[6], -2.0 * t7[5]), t7[4]);
+            const double rr_noise = 1e-13 * (t7[4] + fabs(2.0 * an * t7[5]) + an * an * t7[6]);
+            beta = rz_new / rho;
+            alpha = an;
+            rho = rz_new;
+            rr = rr_new;
+            conv = rr <= tol2 && rr > rr_noise && !P.debug;
+            ++it;
+            if (conv || it >= P.maxit) {   // the last update x_it = x_{it-1} + alpha p_{it-1} alone
+                const double *pl = pw;   // p_{it-1} (p_0 = P.pa)
+                for (int64_t i = tid; i < N; i += nthr) P.T_out[i] = fma(alpha, pl[i], xsrc[i]);
+                break;
             }
         }
-        grid.sync();
-        if (tr_on && ntr < 1000) P.trace[ntr++] = gtimer();
-        rho = rz_new;
-        rr = rr_new;
-        // debug runs: fixed iteration count (maxit); an expansion within its noise is not trusted
-        conv = rr <= tol2 && rr > rr_noise && !P.debug;
-        xsrc = P.T_out;
-        ++it;
+    } else {
+        while (!conv && it < P.maxit) {
+            // ---- S: q = K~ p (the only gathered vector); q' = D^{-1} q with the diagonal d taken
+            // from the row's own entries; partials of p.q and of the expansions of the next r.z and r.r
+            //   z_new = z - alpha q', r_new = z_new d:  r.z = z^2 d - 2 alpha z q + alpha^2 q^2 / d,
+            //   r.r = (z d)^2 - 2 alpha z d q + alpha^2 q^2,
+            // so beta is known before the U phase, which forms the next direction itself
+            double red[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+            const bool first = it == 0;
+            P.pf[0] = p;
+            P.npf = P.prefetch ? 1 : 0;
+            P.wv[0] = p;
+            P.nwv = 1;
+            P.ownv = P.z;
+            sweep<KIND, W, NG>(P, R, [&](int64_t s, const auto &src, int w, int ib, int ie) {
+                const int64_t i = 32 * s + lane;
+                const int64_t ii = i < N ? i : N - 1;
+                const double pi = src.own1(p, ii);      // issued before the row sum
+                const double zo = src.own2(P.z, ii);
+                const int ik = iface_index_r(P, ib, ie, i, lane);
+                double dg = src.first();   // the diagonal (entry 0) + the interface self term
+                double acc = src.template dot<false>(w, p, nullptr, 0.0);
+                if (ik >= 0) acc += ell_row<false>(P, ik, p, nullptr, 0.0, ii, &dg);
+                if (i < N) {
+                    const double qs = acc / dg;
+                    const double zd = zo * dg;
+                    P.q[i] = qs;
+                    red[0] = fma(pi, acc, red[0]);
+                    red[1] = fma(zo, zd, red[1]);
+                    red[2] = fma(zo, acc, red[2]);
+                    red[3] = fma(acc, qs, red[3]);
+                    red[4] = fma(zd, zd, red[4]);
+                    red[5] = fma(zd, acc, red[5]);
+                    red[6] = fma(acc, acc, red[6]);
+                }
+            });
+            P.ownv = nullptr;
+            cta_reduce_store<7>(red, red_smem, P.partials, 4);
+            grid.sync();
+            if (tr_on && ntr < 1000) P.trace[ntr++] = gtimer();
+            double t7[7];
+            grid_total<7>(P.partials, G, 4, red_smem, t7);
+            // t7[4] = sum (z d)^2 is the current r.r computed directly: if an expansion below was
+            // too close to its rounding noise to be trusted, the convergence test lands here, one
+            // S phase later, before the update
+            if (!first && !P.debug) {
+                rr = t7[4];
+                if (rr <= tol2) { conv = true; break; }
+            }
+            const double alpha = rho / t7[0];
+            const double rz_new = fma(alpha, fma(alpha, t7[3], -2.0 * t7[2]), t7[1]);
+            const double rr_new = fma(alpha, fma(alpha, t7[6], -2.0 * t7[5]), t7[4]);
+            // rounding noise of the expansion (terms of size r.r of this iteration)
+            const double rr_noise = 1e-13 * (t7[4] + fabs(2.0 * alpha * t7[5]) + alpha * alpha * t7[6]);
+            const double beta = rz_new / rho;
+            // ---- U: x += alpha p, z -= alpha q', p = z + beta p (streams only, no reduction)
+            if constexpr (KIND != 0) {
+                const double *const usrc[4] = {p, P.q, xsrc, P.z};
+                sweep_u<W, NG>(P, R, usrc, [&](int64_t i, double pv, double qv, double xv, double zv) {
+                    P.T_out[i] = fma(alpha, pv, xv);
+                    const double zn = fma(-alpha, qv, zv);
+                    P.z[i] = zn;
+                    p[i] = fma(beta, pv, zn);
+                });
+            } else {   // element pairs with 16-byte loads, two pairs in flight per thread and trip
+                const int64_t npair = N >> 1;
+                double2 *p2 = reinterpret_cast<double2 *>(p);
+                const double2 *q2 = reinterpret_cast<const double2 *>(P.q);
+                const double2 *x2 = reinterpret_cast<const double2 *>(xsrc);
+                double2 *z2 = reinterpret_cast<double2 *>(P.z);
+                double2 *o2 = reinterpret_cast<double2 *>(P.T_out);
+                auto upd = [&](double2 pv, double2 qv, double2 xv, double2 zv, int64_t j) {
+                    o2[j] = make_double2(fma(alpha, pv.x, xv.x), fma(alpha, pv.y, xv.y));
+                    const double2 zn = make_double2(fma(-alpha, qv.x, zv.x), fma(-alpha, qv.y, zv.y));
+                    z2[j] = zn;
+                    p2[j] = make_double2(fma(beta, pv.x, zn.x), fma(beta, pv.y, zn.y));
+                };
+                constexpr int UU = 2;
+                int64_t j = tid;
+                for (; j + (UU - 1) * nthr < npair; j += UU * nthr) {
+                    double2 pv[UU], qv[UU], xv[UU], zv[UU];
+    #pragma unroll
+                    for (int u = 0; u < UU; ++u) {
+                        const int64_t jj = j + u * nthr;
+                        pv[u] = ld_cg2(p2 + jj); qv[u] = ld_cg2(q2 + jj); xv[u] = ld_cg2(x2 + jj); zv[u] = ld_cg2(z2 + jj);
+                    }
+    #pragma unroll
+                    for (int u = 0; u < UU; ++u) upd(pv[u], qv[u], xv[u], zv[u], j + u * nthr);
+                }
+                for (; j < npair; j += nthr) upd(p2[j], q2[j], x2[j], z2[j], j);
+                if ((N & 1) && tid == nthr - 1) {
+                    const int64_t i = N - 1;
+                    P.T_out[i] = fma(alpha, p[i], xsrc[i]);
+                    const double zn = fma(-alpha, P.q[i], P.z[i]);
+                    P.z[i] = zn;
+                    p[i] = fma(beta, p[i], zn);
+                }
+            }
+            grid.sync();
+            if (tr_on && ntr < 1000) P.trace[ntr++] = gtimer();
+            rho = rz_new;
+            rr = rr_new;
+            // debug runs: fixed iteration count (maxit); an expansion within its noise is not trusted
+            conv = rr <= tol2 && rr > rr_noise && !P.debug;
+            xsrc = P.T_out;
+            ++it;
+        }
     }
     if (it == 0) {   // already converged: T^{n+1} = x0
         for (int64_t i = tid; i < N; i += nthr) P.T_out[i] = x0[i];
@@ -824,12 +972,15 @@ __global__ void __launch_bounds__(256) k_chunk_windows(const int64_t *slice_ptr,
 
 struct Variant {
     int kind, W, NG;
+    bool fused;   // one grid barrier per iteration (KIND 2 only)
 };
-static const Variant kVariants[] = {{0, 8, 1}, {1, 8, 2}, {2, 8, 1}, {2, 8, 2}, {2, 6, 1}, {2, 6, 2}, {2, 4, 2}, {2, 4, 1}};
-#define CG_NVAR 8
+static const Variant kVariants[] = {{0, 8, 1, false}, {1, 8, 2, false}, {2, 8, 1, false}, {2, 8, 2, false},
+                                   {2, 6, 1, false},  {2, 6, 2, false}, {2, 4, 2, false}, {2, 4, 1, false},
+                                   {2, 8, 1, true},   {2, 6, 1, true},  {2, 4, 1, true}};
+#define CG_NVAR 11
 
-template <int KIND, int W, int NG>
-static const void *kernel_ptr() { return (const void *)k_cg_step<KIND, W, NG>; }
+template <int KIND, int W, int NG, bool FUSED = false>
+static const void *kernel_ptr() { return (const void *)k_cg_step<KIND, W, NG, FUSED>; }
 
 static const void *variant_kernel(int v) {
     switch (v) {
@@ -840,14 +991,17 @@ static const void *variant_kernel(int v) {
         case 4: return kernel_ptr<2, 6, 1>();
         case 5: return kernel_ptr<2, 6, 2>();
         case 6: return kernel_ptr<2, 4, 2>();
-        default: return kernel_ptr<2, 4, 1>();
+        case 7: return kernel_ptr<2, 4, 1>();
+        case 8: return kernel_ptr<2, 8, 1, true>();
+        case 9: return kernel_ptr<2, 6, 1, true>();
+        default: return kernel_ptr<2, 4, 1, true>();
     }
 }
 
 static size_t stage_bytes(const Variant &v, int E, int wc) {
     size_t col_off = CG_HDR + (size_t)E * 8;
     size_t win_off = align16(col_off + (size_t)E * (v.kind == 2 ? 2 : 4));
-    return align16(win_off + (v.kind == 2 ? (size_t)(wc + 32 * v.W) * 8 : 0));
+    return align16(win_off + (v.kind == 2 ? (size_t)((v.fused ? 3 : 1) * wc + 32 * v.W) * 8 : 0));
 }
 
 int cg_setup(Ctx &c) {
@@ -864,7 +1018,13 @@ int cg_setup(Ctx &c) {
     // candidate order: the requested variant, then the default preference
     std::vector<int> order;
     if (want >= 0) order.push_back(want);
-    for (int v : {2, 3, 4, 5, 6, 7, 1, 0}) if (v != want) order.push_back(v);
+    // L2-resident problems are latency-bound: the one-barrier kernel (8) saves a grid barrier
+    // and a ring pass per iteration (cfg 1: 14.6 -> 13.3 us); beyond that its three vector
+    // windows cost more TMA ingress than the update phase it removes (cfg 2: 57 -> 74 us,
+    // cfg 3: 405 -> 459 us per iteration), so the two-phase kernel (2) is the default there
+    const bool small = c.N <= (int64_t)1 << 18;
+    for (int v : {8, 2, 3, 4, 5, 6, 7, 1, 0})
+        if (v != want && (small || v != 8)) order.push_back(v);
     int chosen = -1, per_sm = 0;
     for (int vi : order) {
         const Variant &v = kVariants[vi];
@@ -931,6 +1091,13 @@ int cg_setup(Ctx &c) {
     const char *pfe = getenv("THERMO_CG_PREFETCH");
     c.cg_prefetch = pfe ? atoi(pfe) : 0;
     c.cg_tma = kVariants[chosen].kind != 0;
+    c.cg_fused = kVariants[chosen].fused;
+    if (c.cg_fused && !c.d_z2) {   // second buffer set of z, q' (vectors padded like the others)
+        CK(cudaMalloc(&c.d_z2, sizeof(double) * (c.N + 16)));
+        CK(cudaMalloc(&c.d_q2, sizeof(double) * (c.N + 16)));
+        CK(cudaMemsetAsync(c.d_z2, 0, sizeof(double) * (c.N + 16), c.stream));
+        CK(cudaMemsetAsync(c.d_q2, 0, sizeof(double) * (c.N + 16), c.stream));
+    }
     const int W = c.cg_chunk;
     const int64_t nchunks = (c.nslices + W - 1) / W;
     CK(cudaMalloc(&c.d_chunk_hi, sizeof(int32_t) * (nchunks + 1)));
@@ -990,6 +1157,9 @@ int cg_launch_solve(Ctx &c, const double *x0, double *x, const double *rhs, cons
     P.nstages = c.cg_nstages;
     P.u_rows = c.cg_u_rows;
     P.win_cap = c.cg_win_cap;
+    P.nwin = c.cg_fused ? 3 : 1;
+    P.z2 = c.d_z2;
+    P.q2 = c.d_q2;
     P.chunk_hi = c.d_chunk_hi;
     P.chunk_runs = c.d_chunk_runs;
     P.chunk_nruns = c.d_chunk_nruns;
@@ -1044,6 +1214,9 @@ int cg_launch_step(Ctx &c, int step, double dt, const double *x0) {
     P.nstages = c.cg_nstages;
     P.u_rows = c.cg_u_rows;
     P.win_cap = c.cg_win_cap;
+    P.nwin = c.cg_fused ? 3 : 1;
+    P.z2 = c.d_z2;
+    P.q2 = c.d_q2;
     P.chunk_hi = c.d_chunk_hi;
     P.chunk_runs = c.d_chunk_runs;
     P.chunk_nruns = c.d_chunk_nruns;

@@ -9,7 +9,7 @@
 #define THERMO_BLOCK 256
 #endif
 #define THERMO_WARPS (THERMO_BLOCK / 32)
-#define THERMO_NRED 16  // reduction slots per CTA
+#define THERMO_NRED 24  // reduction slots per CTA (phase 0: 0-3, S: 4-10, fused S of odd iterations: 11-17)
 
 namespace thermo {
 

@@ -96,6 +96,8 @@ struct Ctx {
     size_t cg_smem = 0;
     bool cg_tma = false;
     int cg_variant = 0, cg_chunk = 8, cg_debug = 0, cg_prefetch = 0;
+    bool cg_fused = false;           // one-barrier-per-iteration kernel (second z / q' set below)
+    double *d_z2 = nullptr, *d_q2 = nullptr;
     int32_t *d_chunk_hi = nullptr;
     uint16_t *d_lcol = nullptr;      // chunk-local 16-bit columns (window kernels)
     int2 *d_chunk_runs = nullptr;    // window runs per chunk

@@ -54,7 +54,7 @@ static void free_ctx(Ctx *c) {
                     c->d_chunk_nruns, c->d_chunk_lown, c->d_trace, c->d_DinvS, c->d_slice_if_zero,
                     c->d_KV, c->d_Dinv_vol, c->d_if_of_row, c->d_mr, c->d_mr_iters, c->d_mr_relres,
                     c->d_ell_cnt_s, c->d_ell_col_s, c->d_ell_val_s, c->d_if_b_s, c->d_if_phi_s, c->d_rhs,
-                    c->d_pairs_s, c->d_pcnt_s, c->d_star_own, c->d_own_ptr, c->d_own_idx, c->d_x0, c->d_Thist};
+                    c->d_pairs_s, c->d_pcnt_s, c->d_star_own, c->d_own_ptr, c->d_own_idx, c->d_x0, c->d_Thist, c->d_z2, c->d_q2};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     for (cudaEvent_t e : c->events) cudaEventDestroy(e);
@@ -536,12 +536,19 @@ extern "C" int thermo_step(void *ctx, double t, double dt, int32_t nsteps) {
             int it = 0;   // loop iterations of the last solve (max over the scenarios)
             for (int j = 0; j < S; ++j) it = std::max(it, (int)c->h_iters[(size_t)(nsteps - 1) * S + j]);
             double s_ns = 0, u_ns = 0;
+            if (c->cg_fused) {   // one barrier (one timestamp) per iteration
+                const int n = std::min(it, 1000);
+                fprintf(stderr, "[thermo trace] phase0 %.1f us, fused S+U %.1f us/iter (%d iters)\n",
+                        (tr[1] - tr[0]) * 1e-3, n > 0 ? (tr[n] - tr[1]) * 1e-3 / std::max(n - 1, 1) : 0.0, it);
+                it = 0;
+            }
             for (int k = 0; k < it && 2 + 2 * k + 1 < 1024; ++k) {
                 s_ns += (double)(tr[2 + 2 * k] - tr[1 + 2 * k]);
                 u_ns += (double)(tr[3 + 2 * k] - tr[2 + 2 * k]);
             }
-            fprintf(stderr, "[thermo trace] phase0 %.1f us, S %.1f us/iter, U %.1f us/iter (%d iters)\n",
-                    (tr[1] - tr[0]) * 1e-3, s_ns * 1e-3 / it, u_ns * 1e-3 / it, it);
+            if (it > 0)
+                fprintf(stderr, "[thermo trace] phase0 %.1f us, S %.1f us/iter, U %.1f us/iter (%d iters)\n",
+                        (tr[1] - tr[0]) * 1e-3, s_ns * 1e-3 / it, u_ns * 1e-3 / it, it);
         }
         c->failed_step = -1;
         c->failed_scen = -1;

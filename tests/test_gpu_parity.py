@@ -195,7 +195,26 @@ def test_cfg1_full_run():
     assert rel(Tg, Tr) <= TOL
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4])
+@pytest.mark.parametrize("pair", [(2, 8), (4, 9), (7, 10)])
+@pytest.mark.parametrize("name", ["small", "medium"])
+def test_fused_variant_bitwise_equals_unfused(monkeypatch, name, pair):
+    """The one-barrier-per-iteration kernel (update of iteration k folded into the sweep of
+    k + 1, p formed from the z, q', p windows) computes the same numbers in the same order as
+    the two-phase kernel of the same chunk size: bitwise equal fields and iteration counts."""
+    cfg = I.make_config(name, jitter=0.1)
+    T0 = I.initial_field(cfg)[0]
+    out = []
+    for v in pair:
+        monkeypatch.setenv("THERMO_CG_VARIANT", str(v))
+        th = _thermo(cfg)
+        th.set_T(T0)
+        th.step(0.0, cfg.dt, cfg.nsteps)
+        out.append((th.get_T(), th.step_iters()[:, 0].copy()))
+    assert np.array_equal(out[0][1], out[1][1])
+    assert np.array_equal(out[0][0], out[1][0])
+
+
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 8, 9])
 def test_cg_kernel_variants_agree(monkeypatch, variant):
     """Every sweep kind (register streaming, TMA matrix ring, TMA ring + shared-memory vector
     windows with 16-bit local columns) forms identical row sums; only the CTA-level order of
