@@ -1063,7 +1063,12 @@ int cg_setup(Ctx &c) {
         const size_t budget = (size_t)(ekb ? atoi(ekb) : 210) * 1024 - 128;
         int ns = v.kind == 0 ? 1 : (int)std::min<size_t>(8, budget / sb);
         if (const char *e = getenv("THERMO_CG_STAGES")) ns = std::min(ns, std::max(2, atoi(e)));   // tuning hook
-        if (v.kind != 0 && ns < v.NG + 1) continue;   // at least one stage in flight
+        // consumer group g takes ring slots n = g (mod NG), stage n mod ns: with ns a multiple
+        // of NG every stage belongs to one group, so a group can never run two phases ahead
+        // of a stage's mbarrier (an ns = 3, NG = 2 ring passed a parity wait one phase early
+        // and read a stale stage on cfg 3)
+        if (v.kind != 0) ns -= ns % v.NG;
+        if (v.kind != 0 && ns < std::max(2, v.NG)) continue;   // at least one stage in flight
         const size_t smem = v.kind == 0 ? 0 : 128 + (size_t)ns * sb;
         const void *fn = variant_kernel(vi);
         if (smem > 48 * 1024) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

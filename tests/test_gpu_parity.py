@@ -214,6 +214,21 @@ def test_fused_variant_bitwise_equals_unfused(monkeypatch, name, pair):
     assert np.array_equal(out[0][0], out[1][0])
 
 
+@pytest.mark.parametrize("stages", [3, 5])
+@pytest.mark.parametrize("variant", [1, 3, 5])
+def test_two_consumer_groups_any_stage_cap(monkeypatch, variant, stages):
+    """Kernels with two consumer groups take alternate ring slots; a stage count that is not a
+    multiple of the group count once let a group pass a stage's mbarrier one phase early (stale
+    stage, launch failure on cfg 3).  The ring is now rounded to a multiple of the groups."""
+    cfg = I.make_config("medium", jitter=0.1)
+    monkeypatch.setenv("THERMO_CG_VARIANT", str(variant))
+    monkeypatch.setenv("THERMO_CG_STAGES", str(stages))
+    a = _thermo(cfg)
+    a.step(0.0, cfg.dt, 8)
+    Tr, _ = O.run_config(cfg, nsteps=8)
+    assert rel(a.get_T(), Tr) <= TOL
+
+
 @pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 8, 9])
 def test_cg_kernel_variants_agree(monkeypatch, variant):
     """Every sweep kind (register streaming, TMA matrix ring, TMA ring + shared-memory vector
