@@ -148,6 +148,7 @@ int main(void) {
     thermo_stats st;
     if (thermo_get_stats(ctx, &st) || st.steps_done != 5 || st.failed_step != -1) bad = 1;
     if (thermo_get_T(ctx, 0, -1, T0, 3, 0) != THERMO_EINVAL) bad = 1;   /* wrong n */
+    if (thermo_set_guess(ctx, 3) != THERMO_EINVAL || thermo_set_guess(ctx, 0) != THERMO_OK) bad = 1;
     thermo_destroy(ctx);
     free(T0);
     if (bad) { printf("abi_demo FAILED\n"); return 1; }
