@@ -427,6 +427,9 @@ int build_operator(Ctx &c, double dt, double mu) {
     if (!c.d_Dinv_vol) CK(cudaMalloc(&c.d_Dinv_vol, sizeof(double) * c.N));
     k_build_diag<<<nb(c.N), 256, 0, st>>>(c.d_diagpos, c.d_ML, mu, c.N, c.d_val, c.d_Dvol, c.d_Dinv, c.d_Dinv_vol);
     CK(cudaGetLastError());
+    // overlap mode: the second interface buffer set carries its own Jacobi vector (the interface
+    // kernels rewrite its interface rows every other step; all other rows are the volume ones)
+    if (c.d_Dinv_b) CK(cudaMemcpyAsync(c.d_Dinv_b, c.d_Dinv, sizeof(double) * c.N, cudaMemcpyDeviceToDevice, st));
     if (!c.d_KV) CK(cudaMalloc(&c.d_KV, sizeof(double) * (c.nnz_pad + 1)));
     k_build_kv<<<nb(c.nnz_pad), 256, 0, st>>>(c.d_A, c.d_R, c.nnz_pad, c.d_KV);
     CK(cudaGetLastError());

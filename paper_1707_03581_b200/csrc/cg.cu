@@ -582,7 +582,8 @@ __global__ void __launch_bounds__(cg_threads(KIND, W, NG), KIND == 0 ? 2 : 1) k_
     const int NS = P.nstages;
     __shared__ double red_smem[THERMO_RED_SMEM];
     extern __shared__ __align__(128) unsigned char ring_raw[];
-    if (P.status[0] || P.status[1]) {   // an earlier step failed or the interface overflowed
+    // an earlier step failed, or the interface of this or an earlier step overflowed
+    if (P.status[0] || (P.status[1] && P.status[4] <= P.step)) {   // an earlier step failed or the interface overflowed
         if (!P.status[0] && blockIdx.x == 0 && threadIdx.x == 0) {
             P.status[0] = 2;
             P.status[2] = P.step;
@@ -1176,7 +1177,7 @@ int cg_launch_solve(Ctx &c, const double *x0, double *x, const double *rhs, cons
     return 0;
 }
 
-int cg_launch_step(Ctx &c, int step, double dt, const double *x0) {
+int cg_launch_step(Ctx &c, int step, double dt, const double *x0, int buf) {
     CGParams P;
     memset(&P, 0, sizeof P);
     P.N = c.N;
@@ -1188,16 +1189,16 @@ int cg_launch_step(Ctx &c, int step, double dt, const double *x0) {
     P.val = c.d_val;
     P.ML = c.d_ML;
     P.benv = c.d_benv;
-    P.Dinv = c.d_Dinv;
+    P.Dinv = buf ? c.d_Dinv_b : c.d_Dinv;
     P.n_if = c.n_if;
     P.nA = c.nA;
     P.if_rows = c.d_if_rows;
     P.slice_if = c.d_slice_if;
-    P.ell_cnt = c.d_ell_cnt;
-    P.ell_col = c.d_ell_col;
-    P.ell_val = c.d_ell_val;
-    P.if_b = c.d_if_b;
-    P.if_phi = c.d_if_phi;
+    P.ell_cnt = buf ? c.d_ell_cnt_b : c.d_ell_cnt;
+    P.ell_col = buf ? c.d_ell_col_b : c.d_ell_col;
+    P.ell_val = buf ? c.d_ell_val_b : c.d_ell_val;
+    P.if_b = buf ? c.d_if_b_b : c.d_if_b;
+    P.if_phi = buf ? c.d_if_phi_b : c.d_if_phi;
     P.T_in = c.d_T[(c.cur + step) & 1];
     P.X0 = x0;
     P.T_out = c.d_T[(c.cur + step + 1) & 1];
@@ -1232,6 +1233,46 @@ int cg_launch_step(Ctx &c, int step, double dt, const double *x0) {
     void *args[] = {&P};
     CK(cudaLaunchCooperativeKernel(variant_kernel(c.cg_variant), dim3(c.cg_grid), dim3(c.cg_block), args,
                                    c.cg_smem, c.stream));
+    return 0;
+}
+
+// Overlap mode: a second interface buffer set, a side stream with its events,
+// and a CG grid that leaves overlap_sms SMs to the side stream's interface kernels.
+int overlap_setup(Ctx &c) {
+    if (c.S != 1 || c.n_if == 0) return 0;
+    const char *e = getenv("THERMO_OVERLAP");   // 0: off, 1: on, unset: L2-resident sizes only
+    const bool want = e ? atoi(e) != 0 : c.N <= (int64_t)1 << 18;
+    if (!want) return 0;
+    const char *es = getenv("THERMO_OVERLAP_SMS");
+    int free_sms = es ? atoi(es) : 24;
+    free_sms = std::max(1, std::min(free_sms, c.num_sms / 2));
+    const int64_t nif = c.n_if;
+    CK(cudaMalloc(&c.d_ell_cnt_b, sizeof(int32_t) * nif));
+    CK(cudaMalloc(&c.d_ell_col_b, sizeof(int32_t) * c.cap * nif));
+    CK(cudaMalloc(&c.d_ell_val_b, sizeof(double) * c.cap * nif));
+    CK(cudaMalloc(&c.d_if_b_b, sizeof(double) * nif));
+    CK(cudaMalloc(&c.d_if_phi_b, sizeof(double) * nif));
+    CK(cudaMalloc(&c.d_Dinv_b, sizeof(double) * (c.N + 16)));
+    CK(cudaMemsetAsync(c.d_ell_cnt_b, 0, sizeof(int32_t) * nif, c.stream));
+    CK(cudaMemsetAsync(c.d_if_b_b, 0, sizeof(double) * nif, c.stream));
+    CK(cudaMemsetAsync(c.d_if_phi_b, 0, sizeof(double) * nif, c.stream));
+    CK(cudaStreamCreateWithFlags(&c.if_stream, cudaStreamNonBlocking));
+    for (cudaEvent_t *ev : {&c.ev_if[0], &c.ev_if[1], &c.ev_cg[0], &c.ev_cg[1], &c.ev_main})
+        CK(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
+    c.overlap = true;
+    c.overlap_sms = free_sms;
+    if (c.cg_grid > c.num_sms - free_sms) c.cg_grid = c.num_sms - free_sms;
+    // the solve CTAs claim all of their SMs' shared memory, so no interface block is placed next
+    // to them (co-resident interface blocks slowed the latency-bound solve by ~25 % on cfg 1)
+    if (c.cg_tma) {
+        int dev_max = 0;
+        CK(cudaDeviceGetAttribute(&dev_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, c.dev));
+        const size_t claim = (size_t)dev_max - sizeof(double) * THERMO_RED_SMEM;
+        if (claim > c.cg_smem) {
+            CK(cudaFuncSetAttribute(variant_kernel(c.cg_variant), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)claim));
+            c.cg_smem = claim;
+        }
+    }
     return 0;
 }
 

@@ -325,7 +325,8 @@ __device__ __forceinline__ void cgb_update(const CGBParams &P, const double (&al
 __global__ void __launch_bounds__(CGB_BLOCK, 1) k_cgb_step(CGBParams P) {
     constexpr int NW = CGB_WARPS;
     __shared__ double sm[CGB_WARPS * CGB_NV * 64];
-    if (P.status[0] || P.status[1]) {
+    // an earlier step failed, or the interface of this or an earlier step overflowed
+    if (P.status[0] || (P.status[1] && P.status[4] <= P.step)) {
         if (!P.status[0] && blockIdx.x == 0 && threadIdx.x == 0) {
             P.status[0] = 2;
             P.status[2] = P.step;

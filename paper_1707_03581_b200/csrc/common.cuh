@@ -233,6 +233,8 @@ struct IfaceParams {
     double *if_phi;           // [S][n_if] int_{Gamma_R} phi
     double *Dinv;             // S == 1: [N] Jacobi inverse diagonal, interface rows rewritten
     double *if_dinv;          // (unused)
+    int step;                 // time step of this assembly: an overflow records the first one in
+                              // status[4] (the overlap mode assembles one step ahead of the solve)
     double *DinvS;            // S > 1: [N][SP] per-scenario Jacobi inverse diagonal
     int SP;                   // S > 1: row stride of the block vectors (even, >= S)
     int no_dinv;              // 1: leave the Jacobi diagonal alone (MRSDC: f^E is explicit)

@@ -108,6 +108,17 @@ struct Ctx {
     int64_t cg_u_rows = 0;
     int *d_chunk_ctr = nullptr;
 
+    // Overlap (single scenario, implicit Euler, L2-resident sizes): the interface kernels of
+    // step n+1 run on if_stream into the second interface buffer set (suffix _b) while the solve
+    // of step n runs on the remaining SMs (the persistent CG grid leaves overlap_sms free).
+    bool overlap = false;
+    int overlap_sms = 0;
+    int32_t *d_ell_cnt_b = nullptr, *d_ell_col_b = nullptr;
+    double *d_ell_val_b = nullptr, *d_if_b_b = nullptr, *d_if_phi_b = nullptr, *d_Dinv_b = nullptr;
+    cudaStream_t if_stream = nullptr;
+    cudaEvent_t ev_if[2] = {nullptr, nullptr}, ev_cg[2] = {nullptr, nullptr}, ev_main = nullptr;
+    std::vector<cudaEvent_t> events_if;   // timing of the side-stream interface kernels
+
     double rtol = 1e-12;
     int maxit = 0;
     // initial guess of the implicit-Euler solves: 0 = T^n (reading R17), 1 = linear, 2 = quadratic
@@ -160,13 +171,14 @@ int build_operator(Ctx &c, double dt, double mu = 1.0);   // K~ = mu M_L - dt (A
 // iface.cu
 int iface_setup(Ctx &c, const double *h_xyz, const std::vector<int32_t> &facesA,
                 const std::vector<int32_t> &facesB);
-void iface_params(Ctx &c, IfaceParams &p, const double *step_sc, double dt);
+void iface_params(Ctx &c, IfaceParams &p, const double *step_sc, double dt, int buf = 0);
 int iface_launch(Ctx &c, const IfaceParams &p, cudaStream_t stream = nullptr);
 
 // cg.cu
 int cg_setup(Ctx &c);
 // x0: initial guess (extrapolated state, see thermo.cu), nullptr = the committed state T^n
-int cg_launch_step(Ctx &c, int step, double dt, const double *x0 = nullptr);
+int cg_launch_step(Ctx &c, int step, double dt, const double *x0 = nullptr, int buf = 0);
+int overlap_setup(Ctx &c);   // second interface buffer set, side stream, reduced CG grid
 // Solve (M_L - a K_vol [- a K_G]) x = rhs from x0 with the operator currently in d_val (a =
 // built_dt); iface = false: no interface rows.  Iterations / residual to iters_out[slot].
 int cg_launch_solve(Ctx &c, const double *x0, double *x, const double *rhs, const double *Dinv, bool iface,

@@ -313,7 +313,10 @@ __global__ void __launch_bounds__(32 * PAIR_WPB, 4) k_pairs(IfaceParams P, int n
         if (valid && (grp & lt) == 0) qcnt[j] += __popc(hm & grp);   // group leader
         __syncwarp();
     }
-    if (!__all_sync(0xffffffffu, ok) && lane == 0) atomicOr(&P.status[1], 1);
+    if (!__all_sync(0xffffffffu, ok) && lane == 0) {
+        atomicOr(&P.status[1], 1);
+        atomicMin(&P.status[4], P.step);
+    }
     if (lane < PAIR_TPW && t0 + lane < nT) P.pcnt[rid0 + t0 + lane] = min(qcnt[lane], P.pcap);
 }
 
@@ -468,7 +471,10 @@ __global__ void __launch_bounds__(32 * ROW_WPB) k_rows(IfaceParams P) {
     }
     dself = warp_sum(dself);   // exactly one lane holds the diagonal (others add 0)
     if (lane == 0) {
-        if (!ok) atomicOr(&P.status[1], 1);
+        if (!ok) {
+            atomicOr(&P.status[1], 1);
+            atomicMin(&P.status[4], P.step);
+        }
         P.ell_cnt[row_index(P, s, k)] = ok ? count : 0;
         P.if_phi[row_index(P, s, k)] = phi;
         P.if_b[row_index(P, s, k)] = 0.5 * P.step_sc[4 * s + 2] * phi;
@@ -838,7 +844,7 @@ int iface_setup(Ctx &c, const double *X, const std::vector<int32_t> &fA, const s
     return 0;
 }
 
-void iface_params(Ctx &c, IfaceParams &P, const double *step_sc, double dt) {
+void iface_params(Ctx &c, IfaceParams &P, const double *step_sc, double dt, int buf) {
     P.nTA = c.nTA;
     P.nTB = c.nTB;
     P.pcap = c.pcap;
@@ -866,12 +872,12 @@ void iface_params(Ctx &c, IfaceParams &P, const double *step_sc, double dt) {
     P.dt = dt;
     P.step_sc = step_sc;
     P.Dvol = c.d_Dvol;
-    P.ell_cnt = c.d_ell_cnt;
-    P.ell_col = c.d_ell_col;
-    P.ell_val = c.d_ell_val;
-    P.if_b = c.d_if_b;
-    P.if_phi = c.d_if_phi;
-    P.Dinv = c.d_Dinv;
+    P.ell_cnt = buf ? c.d_ell_cnt_b : c.d_ell_cnt;
+    P.ell_col = buf ? c.d_ell_col_b : c.d_ell_col;
+    P.ell_val = buf ? c.d_ell_val_b : c.d_ell_val;
+    P.if_b = buf ? c.d_if_b_b : c.d_if_b;
+    P.if_phi = buf ? c.d_if_phi_b : c.d_if_phi;
+    P.Dinv = buf ? c.d_Dinv_b : c.d_Dinv;
     P.if_dinv = c.d_if_dinv;
     P.DinvS = c.d_DinvS;
     P.SP = c.SP;

@@ -54,10 +54,18 @@ static void free_ctx(Ctx *c) {
                     c->d_chunk_nruns, c->d_chunk_lown, c->d_trace, c->d_DinvS, c->d_slice_if_zero,
                     c->d_KV, c->d_Dinv_vol, c->d_if_of_row, c->d_mr, c->d_mr_iters, c->d_mr_relres,
                     c->d_ell_cnt_s, c->d_ell_col_s, c->d_ell_val_s, c->d_if_b_s, c->d_if_phi_s, c->d_rhs,
-                    c->d_pairs_s, c->d_pcnt_s, c->d_star_own, c->d_own_ptr, c->d_own_idx, c->d_x0, c->d_Thist, c->d_z2, c->d_q2};
+                    c->d_pairs_s, c->d_pcnt_s, c->d_star_own, c->d_own_ptr, c->d_own_idx, c->d_x0, c->d_Thist, c->d_z2, c->d_q2,
+                    c->d_ell_cnt_b, c->d_ell_col_b, c->d_ell_val_b, c->d_if_b_b, c->d_if_phi_b, c->d_Dinv_b};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     for (cudaEvent_t e : c->events) cudaEventDestroy(e);
+    for (cudaEvent_t e : c->events_if) cudaEventDestroy(e);
+    if (c->if_stream) {
+        cudaStreamSynchronize(c->if_stream);
+        cudaStreamDestroy(c->if_stream);
+    }
+    for (cudaEvent_t e : {c->ev_if[0], c->ev_if[1], c->ev_cg[0], c->ev_cg[1], c->ev_main})
+        if (e) cudaEventDestroy(e);
     if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
     for (cudaEvent_t e : {c->ev_ready, c->ev_copy[0], c->ev_copy[1]})
         if (e) cudaEventDestroy(e);
@@ -185,6 +193,7 @@ extern "C" int thermo_create_mesh(void **out, const thermo_mesh *fixed, const th
         cudaMemsetAsync(c->d_status, 0, sizeof(int) * 8, c->stream);
         rc = thermo::assemble_robin(*c);
         if (!rc) rc = c->S == 1 ? thermo::cg_setup(*c) : thermo::cgb_setup(*c);
+        if (!rc) rc = thermo::overlap_setup(*c);
         if (!rc && getenv("THERMO_CG_TRACE")) {
             if (cudaMalloc(&c->d_trace, sizeof(unsigned long long) * 1024) != cudaSuccess) rc = -3;
             else cudaMemsetAsync(c->d_trace, 0, sizeof(unsigned long long) * 1024, c->stream);
@@ -413,6 +422,7 @@ extern "C" int thermo_step(void *ctx, double t, double dt, int32_t nsteps) {
         }
         API_CK(cudaMemcpyAsync(c->d_step_sc, sc.data(), sizeof(double) * sc.size(), cudaMemcpyHostToDevice, c->stream));
         API_CK(cudaMemsetAsync(c->d_status, 0, sizeof(int) * 8, c->stream));
+        API_CK(cudaMemsetAsync(c->d_status + 4, 0x7f, sizeof(int), c->stream));   // no overflow step yet
         if (c->method >= 1) {   // MRSDC / single-rate SDC: one step at a time, status checked per step
             c->h_iters.assign((size_t)nsteps, 0);
             c->h_relres.assign((size_t)nsteps, 0.0);
@@ -468,11 +478,43 @@ extern "C" int thermo_step(void *ctx, double t, double dt, int32_t nsteps) {
             API_CK(cudaMemsetAsync(c->d_Thist, 0, sizeof(double) * (NS + 16), c->stream));
         }
         int64_t launches = 0;
-        for (int n = 0; n < nsteps; ++n) {
+        const bool ovl = c->overlap && S == 1;
+        if (ovl) {
+            // the side stream runs one step ahead: interface(n + 1) into buffer set (n + 1) & 1
+            // while the solve of step n reads set n & 1; interface(n + 1) waits for the solve of
+            // step n - 1 (the previous reader of its set), solve(n) for interface(n)
+            if (c->timing)
+                while (c->events_if.size() < 2 * (size_t)nsteps) {
+                    cudaEvent_t e;
+                    API_CK(cudaEventCreate(&e));
+                    c->events_if.push_back(e);
+                }
+            API_CK(cudaEventRecord(c->ev_main, c->stream));   // time scalars copied, earlier work queued
+            API_CK(cudaStreamWaitEvent(c->if_stream, c->ev_main, 0));
+        }
+        auto launch_iface = [&](int n, cudaStream_t st) -> int {
             thermo::IfaceParams P;
             memset(&P, 0, sizeof P);
-            thermo::iface_params(*c, P, c->d_step_sc + 4 * (size_t)n * S, dt);
-            // timing: [events 2n, 2n+1) = guess extrapolation + interface kernels, [2n+1, 2n+2) = the solve
+            thermo::iface_params(*c, P, c->d_step_sc + 4 * (size_t)n * S, dt, ovl ? (n & 1) : 0);
+            P.step = n;
+            if (thermo::iface_launch(*c, P, st)) return -1;
+            launches += c->n_if ? 2 : 0;
+            return 0;
+        };
+        auto side_iface = [&](int n) -> int {   // overlap mode: interface(n) on the side stream
+            if (n >= 2) API_CK(cudaStreamWaitEvent(c->if_stream, c->ev_cg[n & 1], 0));
+            if (c->timing) API_CK(cudaEventRecord(c->events_if[2 * n], c->if_stream));
+            if (launch_iface(n, c->if_stream)) return THERMO_ECUDA;
+            if (c->timing) API_CK(cudaEventRecord(c->events_if[2 * n + 1], c->if_stream));
+            API_CK(cudaEventRecord(c->ev_if[n & 1], c->if_stream));
+            return THERMO_OK;
+        };
+        if (ovl && side_iface(0)) return THERMO_ECUDA;
+        for (int n = 0; n < nsteps; ++n) {
+            if (ovl && n + 1 < nsteps && side_iface(n + 1)) return THERMO_ECUDA;
+            // timing: [events 2n, 2n+1) = guess extrapolation + interface kernels (overlap mode:
+            // extrapolation only, the interface kernels are timed on the side stream),
+            // [2n+1, 2n+2) = the solve
             if (c->timing) API_CK(cudaEventRecord(c->events[2 * n], c->stream));
             API_CK(guard_write(c, (c->cur + n + 1) & 1));
             // states behind T^n available for the extrapolated guess
@@ -484,12 +526,15 @@ extern "C" int thermo_step(void *ctx, double t, double dt, int32_t nsteps) {
                 API_CK(cudaGetLastError());
                 ++launches;
             }
-            if (thermo::iface_launch(*c, P)) return THERMO_ECUDA;
+            if (ovl) API_CK(cudaStreamWaitEvent(c->stream, c->ev_if[n & 1], 0));
+            else if (launch_iface(n, c->stream)) return THERMO_ECUDA;
             if (c->timing) API_CK(cudaEventRecord(c->events[2 * n + 1], c->stream));
             const double *x0 = avail > 0 ? c->d_x0 : nullptr;
-            if ((S == 1 ? thermo::cg_launch_step(*c, n, dt, x0) : thermo::cgb_launch_step(*c, n, dt, x0)))
+            if ((S == 1 ? thermo::cg_launch_step(*c, n, dt, x0, ovl ? (n & 1) : 0)
+                        : thermo::cgb_launch_step(*c, n, dt, x0)))
                 return THERMO_ECUDA;
-            launches += 1 + (c->n_if ? 2 : 0);
+            if (ovl) API_CK(cudaEventRecord(c->ev_cg[n & 1], c->stream));
+            launches += 1;
         }
         c->last_launches = launches;
         if (c->timing) API_CK(cudaEventRecord(c->events[2 * nsteps], c->stream));
@@ -511,6 +556,11 @@ extern "C" int thermo_step(void *ctx, double t, double dt, int32_t nsteps) {
                 float a = 0.f, b = 0.f;
                 API_CK(cudaEventElapsedTime(&a, c->events[2 * n], c->events[2 * n + 1]));
                 API_CK(cudaEventElapsedTime(&b, c->events[2 * n + 1], c->events[2 * n + 2]));
+                if (ovl) {   // interface kernels ran on the side stream, overlapped with the solves
+                    float f = 0.f;
+                    API_CK(cudaEventElapsedTime(&f, c->events_if[2 * n], c->events_if[2 * n + 1]));
+                    a += f;
+                }
                 c->ms_iface += a;
                 c->ms_solve += b;
             }

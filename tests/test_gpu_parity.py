@@ -214,6 +214,29 @@ def test_fused_variant_bitwise_equals_unfused(monkeypatch, name, pair):
     assert np.array_equal(out[0][0], out[1][0])
 
 
+@pytest.mark.parametrize("name", ["cfg0", "medium"])
+def test_interface_overlap_mode(monkeypatch, name):
+    """Overlap mode (interface kernels of step n+1 on a side stream into the second buffer set
+    while step n solves on the remaining SMs): same result as the serial schedule to rounding
+    (only the CTA count of the reductions differs), bitwise reproducible, split calls equal one
+    call, and both match the oracle."""
+    cfg = I.make_config(name, jitter=0.1 if name != "cfg0" else None)
+    runs = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("THERMO_OVERLAP", mode)
+        a = _thermo(cfg)
+        a.step(0.0, cfg.dt, 12)
+        b = _thermo(cfg)
+        b.step(0.0, cfg.dt, 5)
+        b.step(5 * cfg.dt, cfg.dt, 7)
+        assert np.array_equal(a.get_T(), b.get_T())
+        runs[mode] = a.get_T()
+        assert a.stats()["failed_step"] == -1
+    assert rel(runs["1"], runs["0"]) < 1e-12
+    Tr, _ = O.run_config(cfg, nsteps=12)
+    assert rel(runs["1"], Tr) <= TOL
+
+
 @pytest.mark.parametrize("stages", [3, 5])
 @pytest.mark.parametrize("variant", [1, 3, 5])
 def test_two_consumer_groups_any_stage_cap(monkeypatch, variant, stages):
