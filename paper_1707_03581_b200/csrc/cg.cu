@@ -1177,7 +1177,7 @@ int cg_launch_solve(Ctx &c, const double *x0, double *x, const double *rhs, cons
     return 0;
 }
 
-int cg_launch_step(Ctx &c, int step, double dt, const double *x0, int buf) {
+int cg_launch_step(Ctx &c, int step, double dt, const double *x0, int buf, bool ovl) {
     CGParams P;
     memset(&P, 0, sizeof P);
     P.N = c.N;
@@ -1231,7 +1231,8 @@ int cg_launch_step(Ctx &c, int step, double dt, const double *x0, int buf) {
     P.debug = c.cg_debug;
     P.prefetch = c.cg_prefetch;
     void *args[] = {&P};
-    CK(cudaLaunchCooperativeKernel(variant_kernel(c.cg_variant), dim3(c.cg_grid), dim3(c.cg_block), args,
+    CK(cudaLaunchCooperativeKernel(variant_kernel(c.cg_variant), dim3(ovl ? c.cg_grid_ovl : c.cg_grid),
+                                   dim3(c.cg_block), args,
                                    c.cg_smem, c.stream));
     return 0;
 }
@@ -1261,7 +1262,7 @@ int overlap_setup(Ctx &c) {
         CK(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
     c.overlap = true;
     c.overlap_sms = free_sms;
-    if (c.cg_grid > c.num_sms - free_sms) c.cg_grid = c.num_sms - free_sms;
+    c.cg_grid_ovl = std::min(c.cg_grid, c.num_sms - free_sms);   // the other solves keep the full grid
     // the solve CTAs claim all of their SMs' shared memory, so no interface block is placed next
     // to them (co-resident interface blocks slowed the latency-bound solve by ~25 % on cfg 1)
     if (c.cg_tma) {

@@ -112,7 +112,7 @@ struct Ctx {
     // step n+1 run on if_stream into the second interface buffer set (suffix _b) while the solve
     // of step n runs on the remaining SMs (the persistent CG grid leaves overlap_sms free).
     bool overlap = false;
-    int overlap_sms = 0;
+    int overlap_sms = 0, cg_grid_ovl = 0;
     int32_t *d_ell_cnt_b = nullptr, *d_ell_col_b = nullptr;
     double *d_ell_val_b = nullptr, *d_if_b_b = nullptr, *d_if_phi_b = nullptr, *d_Dinv_b = nullptr;
     cudaStream_t if_stream = nullptr;
@@ -177,7 +177,7 @@ int iface_launch(Ctx &c, const IfaceParams &p, cudaStream_t stream = nullptr);
 // cg.cu
 int cg_setup(Ctx &c);
 // x0: initial guess (extrapolated state, see thermo.cu), nullptr = the committed state T^n
-int cg_launch_step(Ctx &c, int step, double dt, const double *x0 = nullptr, int buf = 0);
+int cg_launch_step(Ctx &c, int step, double dt, const double *x0 = nullptr, int buf = 0, bool ovl = false);
 int overlap_setup(Ctx &c);   // second interface buffer set, side stream, reduced CG grid
 // Solve (M_L - a K_vol [- a K_G]) x = rhs from x0 with the operator currently in d_val (a =
 // built_dt); iface = false: no interface rows.  Iterations / residual to iters_out[slot].

@@ -530,7 +530,7 @@ extern "C" int thermo_step(void *ctx, double t, double dt, int32_t nsteps) {
             else if (launch_iface(n, c->stream)) return THERMO_ECUDA;
             if (c->timing) API_CK(cudaEventRecord(c->events[2 * n + 1], c->stream));
             const double *x0 = avail > 0 ? c->d_x0 : nullptr;
-            if ((S == 1 ? thermo::cg_launch_step(*c, n, dt, x0, ovl ? (n & 1) : 0)
+            if ((S == 1 ? thermo::cg_launch_step(*c, n, dt, x0, ovl ? (n & 1) : 0, ovl)
                         : thermo::cgb_launch_step(*c, n, dt, x0)))
                 return THERMO_ECUDA;
             if (ovl) API_CK(cudaEventRecord(c->ev_cg[n & 1], c->stream));
@@ -718,7 +718,7 @@ extern "C" int thermo_get_stats(const void *ctx, thermo_stats *out) {
     out->iface_area = c->last_nsteps > 0 ? c->h_area[c->last_nsteps - 1] : 0.0;
     out->ms_iface = c->ms_iface;
     out->ms_solve = c->ms_solve;
-    out->solve_grid = c->cg_grid;
+    out->solve_grid = c->overlap && c->method == 0 ? c->cg_grid_ovl : c->cg_grid;
     out->solve_block = c->cg_block;
     out->launches_per_step = c->last_nsteps > 0 && c->last_launches > 0 ? (int32_t)(c->last_launches / c->last_nsteps)
                                                                           : 1 + (c->n_if ? 2 : 0);
