@@ -1231,6 +1231,24 @@ int cg_launch_step(Ctx &c, int step, double dt, const double *x0, int buf, bool 
     P.debug = c.cg_debug;
     P.prefetch = c.cg_prefetch;
     void *args[] = {&P};
+    if (ovl) {   // cooperative launch that records ev_cg[step & 1] once all of its CTAs have begun
+        cudaLaunchAttribute at[2];
+        at[0].id = cudaLaunchAttributeCooperative;
+        at[0].val.cooperative = 1;
+        at[1].id = cudaLaunchAttributeLaunchCompletionEvent;
+        at[1].val.launchCompletionEvent.event = c.ev_cg[step & 1];
+        at[1].val.launchCompletionEvent.flags = 0;
+        cudaLaunchConfig_t cfg;
+        memset(&cfg, 0, sizeof cfg);
+        cfg.gridDim = dim3(c.cg_grid_ovl);
+        cfg.blockDim = dim3(c.cg_block);
+        cfg.dynamicSmemBytes = c.cg_smem;
+        cfg.stream = c.stream;
+        cfg.attrs = at;
+        cfg.numAttrs = 2;
+        CK(cudaLaunchKernelExC(&cfg, variant_kernel(c.cg_variant), args));
+        return 0;
+    }
     CK(cudaLaunchCooperativeKernel(variant_kernel(c.cg_variant), dim3(ovl ? c.cg_grid_ovl : c.cg_grid),
                                    dim3(c.cg_block), args,
                                    c.cg_smem, c.stream));
@@ -1258,7 +1276,7 @@ int overlap_setup(Ctx &c) {
     CK(cudaMemsetAsync(c.d_if_b_b, 0, sizeof(double) * nif, c.stream));
     CK(cudaMemsetAsync(c.d_if_phi_b, 0, sizeof(double) * nif, c.stream));
     CK(cudaStreamCreateWithFlags(&c.if_stream, cudaStreamNonBlocking));
-    for (cudaEvent_t *ev : {&c.ev_if[0], &c.ev_if[1], &c.ev_cg[0], &c.ev_cg[1], &c.ev_main})
+    for (cudaEvent_t *ev : {&c.ev_if[0], &c.ev_if[1], &c.ev_cg[0], &c.ev_cg[1], &c.ev_done[0], &c.ev_done[1], &c.ev_main})
         CK(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
     c.overlap = true;
     c.overlap_sms = free_sms;

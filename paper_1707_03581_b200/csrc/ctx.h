@@ -116,7 +116,9 @@ struct Ctx {
     int32_t *d_ell_cnt_b = nullptr, *d_ell_col_b = nullptr;
     double *d_ell_val_b = nullptr, *d_if_b_b = nullptr, *d_if_phi_b = nullptr, *d_Dinv_b = nullptr;
     cudaStream_t if_stream = nullptr;
+    // ev_if: interface(n) done; ev_cg: launch completion of solve(n) (all CTAs begun)
     cudaEvent_t ev_if[2] = {nullptr, nullptr}, ev_cg[2] = {nullptr, nullptr}, ev_main = nullptr;
+    cudaEvent_t ev_done[2] = {nullptr, nullptr};   // solve(n) complete
     std::vector<cudaEvent_t> events_if;   // timing of the side-stream interface kernels
 
     double rtol = 1e-12;

@@ -64,7 +64,7 @@ static void free_ctx(Ctx *c) {
         cudaStreamSynchronize(c->if_stream);
         cudaStreamDestroy(c->if_stream);
     }
-    for (cudaEvent_t e : {c->ev_if[0], c->ev_if[1], c->ev_cg[0], c->ev_cg[1], c->ev_main})
+    for (cudaEvent_t e : {c->ev_if[0], c->ev_if[1], c->ev_cg[0], c->ev_cg[1], c->ev_done[0], c->ev_done[1], c->ev_main})
         if (e) cudaEventDestroy(e);
     if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
     for (cudaEvent_t e : {c->ev_ready, c->ev_copy[0], c->ev_copy[1]})
@@ -501,8 +501,14 @@ extern "C" int thermo_step(void *ctx, double t, double dt, int32_t nsteps) {
             launches += c->n_if ? 2 : 0;
             return 0;
         };
-        auto side_iface = [&](int n) -> int {   // overlap mode: interface(n) on the side stream
-            if (n >= 2) API_CK(cudaStreamWaitEvent(c->if_stream, c->ev_cg[n & 1], 0));
+        // overlap mode: interface(n) on the side stream.  For n >= 1 it waits for the launch of
+        // solve(n - 1) (all of its CTAs placed: the side kernels then only find the free SMs;
+        // solve(n - 1) launched also means solve(n - 2), the previous reader of set n & 1, is done)
+        auto side_iface = [&](int n) -> int {
+            // (the explicit completion of solve(n - 2) as well: the launch-completion trigger is
+            // documented as best effort)
+            if (n >= 2) API_CK(cudaStreamWaitEvent(c->if_stream, c->ev_done[n & 1], 0));
+            if (n >= 1) API_CK(cudaStreamWaitEvent(c->if_stream, c->ev_cg[(n - 1) & 1], 0));
             if (c->timing) API_CK(cudaEventRecord(c->events_if[2 * n], c->if_stream));
             if (launch_iface(n, c->if_stream)) return THERMO_ECUDA;
             if (c->timing) API_CK(cudaEventRecord(c->events_if[2 * n + 1], c->if_stream));
@@ -511,7 +517,6 @@ extern "C" int thermo_step(void *ctx, double t, double dt, int32_t nsteps) {
         };
         if (ovl && side_iface(0)) return THERMO_ECUDA;
         for (int n = 0; n < nsteps; ++n) {
-            if (ovl && n + 1 < nsteps && side_iface(n + 1)) return THERMO_ECUDA;
             // timing: [events 2n, 2n+1) = guess extrapolation + interface kernels (overlap mode:
             // extrapolation only, the interface kernels are timed on the side stream),
             // [2n+1, 2n+2) = the solve
@@ -533,8 +538,9 @@ extern "C" int thermo_step(void *ctx, double t, double dt, int32_t nsteps) {
             if ((S == 1 ? thermo::cg_launch_step(*c, n, dt, x0, ovl ? (n & 1) : 0, ovl)
                         : thermo::cgb_launch_step(*c, n, dt, x0)))
                 return THERMO_ECUDA;
-            if (ovl) API_CK(cudaEventRecord(c->ev_cg[n & 1], c->stream));
             launches += 1;
+            if (ovl) API_CK(cudaEventRecord(c->ev_done[n & 1], c->stream));
+            if (ovl && n + 1 < nsteps && side_iface(n + 1)) return THERMO_ECUDA;
         }
         c->last_launches = launches;
         if (c->timing) API_CK(cudaEventRecord(c->events[2 * nsteps], c->stream));
