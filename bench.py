@@ -271,7 +271,9 @@ def run_thermo(args):
                                    "replicas only" if world > 1 else "single GPU"),
                    "cg_iters_per_step": float(iters.mean())},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": "k_cg_step (persistent Jacobi-PCG, one launch per step)",
+                     "traffic": traffic,
+                     "kernel": ("k_cg_step (persistent Jacobi-PCG, one launch per step)" if S == 1 else
+                                "k_cgb_step (persistent batched Jacobi-PCG over all scenarios, one launch per step)"),
                      "peak_kind": peak_kind, "achieved_vs_8TBs": achieved / 8000.0,
                      "solve_share_of_step": st["ms_solve"] / ms,
                      "iface_share_of_step": st["ms_iface"] / ms, **dram},
