@@ -192,7 +192,9 @@ typedef struct {
     int64_t steps_done;              /* committed steps since create */
     double iface_area;               /* |Gamma_R| of scenario 0 at the last step (m^2) */
     double ms_iface;                 /* device time of the interface kernels and the initial-guess
-                                        extrapolation, last call (ms) */
+                                        extrapolation, last call (ms); for small single-scenario
+                                        runs the interface kernels of step n+1 run on a side stream
+                                        during the solve of step n, and their time is included */
     double ms_solve;                 /* device time of the CG solve kernels, last call (ms) */
     int32_t solve_grid;              /* CTAs of the persistent CG kernel */
     int32_t solve_block;             /* threads per CTA */
