@@ -90,6 +90,7 @@ struct CGParams {
     const double *ownv;        // KIND 2: vector of which only the chunk's own rows are staged
                                // (after the window, W * 32 rows)
     unsigned long long *trace; // optional: %globaltimer after every grid barrier (CTA 0)
+    int trace_fine;            // fused kernel: also at the iteration start, sweep end, CTA reduction
     int prefetch;              // L2 leading-edge prefetch (THERMO_CG_PREFETCH=1; measured slower on cfg3)
     int debug;                 // THERMO_CG_DEBUG bits (measurement only, results invalid):
                                // 1 consumers skip the row work, 2 no window copies, 4 no prefetch
@@ -671,7 +672,9 @@ __global__ void __launch_bounds__(cg_threads(KIND, W, NG), KIND == 0 ? 2 : 1) k_
         // partials alternate between two slot groups (a fast CTA's S(k+1) must not overwrite
         // what a slow CTA still reads).  Same formulas, same order: bitwise the unfused result.
         double alpha = 0.0, beta = 0.0;
+        const bool fine = tr_on && P.trace_fine;   // THERMO_CG_TRACE=2: 4 stamps per iteration
         while (!conv && it < P.maxit) {
+            if (fine && ntr < 1000) P.trace[ntr++] = gtimer();
             const bool first = it == 0;
             const int sn = it & 1;   // state set written (read: the other one)
             const double *const zr = sn ? P.z : P.z2, *const qr = sn ? P.q : P.q2, *const pr = sn ? P.pa : P.pb;
@@ -729,8 +732,10 @@ __global__ void __launch_bounds__(cg_threads(KIND, W, NG), KIND == 0 ? 2 : 1) k_
                 }
             });
             P.ownv = nullptr;
+            if (fine && ntr < 1000) P.trace[ntr++] = gtimer();
             const int slot = 4 + 7 * sn;
             cta_reduce_store<7>(red, red_smem, P.partials, slot);
+            if (fine && ntr < 1000) P.trace[ntr++] = gtimer();
             grid.sync();
             if (tr_on && ntr < 1000) P.trace[ntr++] = gtimer();
             double t7[7];
@@ -1228,6 +1233,7 @@ int cg_launch_step(Ctx &c, int step, double dt, const double *x0, int buf, bool 
     P.chunk_nruns = c.d_chunk_nruns;
     P.chunk_lown = c.d_chunk_lown;
     P.trace = c.d_trace;
+    P.trace_fine = c.d_trace && getenv("THERMO_CG_TRACE") && atoi(getenv("THERMO_CG_TRACE")) == 2;
     P.debug = c.cg_debug;
     P.prefetch = c.cg_prefetch;
     void *args[] = {&P};

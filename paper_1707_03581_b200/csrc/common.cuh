@@ -146,32 +146,30 @@ __device__ __forceinline__ void cta_reduce_store(double (&v)[NV], double *smem, 
 template <int NV>
 __device__ __forceinline__ void grid_total(const double *partials, int G, int slot, double *smem,
                                            double (&out)[NV]) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (warp == 0) {
-        double x[NV];
+    // warp w sums value j = w (w + nwarps, ...): lane l takes CTAs l, l + 32, ... with all of its
+    // loads in flight together (one L2 round trip for G <= 256), adds them in ascending CTA
+    // order, then the xor butterfly -- a fixed order, so every CTA gets the identical bits
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int j = warp; j < NV; j += nw) {
+        double x = 0.0;
+        int g0 = 0;
+        for (; g0 + 32 * 8 <= G; g0 += 32 * 8) {
+            double a[8];
 #pragma unroll
-        for (int j = 0; j < NV; ++j) x[j] = 0.0;
-        constexpr int UN = NV > 4 ? 2 : 4;   // CTAs per batch of loads (register budget)
-        int g = lane;
-        for (; g + 32 * (UN - 1) < G; g += 32 * UN) {   // all loads of UN CTAs x NV values together
-            double a[UN][NV];
+            for (int u = 0; u < 8; ++u) a[u] = partials[(g0 + 32 * u + lane) * THERMO_NRED + slot + j];
 #pragma unroll
-            for (int u = 0; u < UN; ++u)
-#pragma unroll
-                for (int j = 0; j < NV; ++j) a[u][j] = partials[(g + 32 * u) * THERMO_NRED + slot + j];
-#pragma unroll
-            for (int u = 0; u < UN; ++u)
-#pragma unroll
-                for (int j = 0; j < NV; ++j) x[j] += a[u][j];   // adds in the serial order
+            for (int u = 0; u < 8; ++u) x += a[u];
         }
-        for (; g < G; g += 32)
+        double a[8];
 #pragma unroll
-            for (int j = 0; j < NV; ++j) x[j] += partials[g * THERMO_NRED + slot + j];
-#pragma unroll
-        for (int j = 0; j < NV; ++j) {
-            const double t = warp_sum(x[j]);
-            if (lane == 0) smem[136 + j] = t;
+        for (int u = 0; u < 8; ++u) {
+            const int g = g0 + 32 * u + lane;
+            a[u] = g < G ? partials[g * THERMO_NRED + slot + j] : 0.0;
         }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) x += a[u];
+        x = warp_sum(x);
+        if (lane == 0) smem[136 + j] = x;
     }
     __syncthreads();
 #pragma unroll

@@ -592,7 +592,18 @@ extern "C" int thermo_step(void *ctx, double t, double dt, int32_t nsteps) {
             int it = 0;   // loop iterations of the last solve (max over the scenarios)
             for (int j = 0; j < S; ++j) it = std::max(it, (int)c->h_iters[(size_t)(nsteps - 1) * S + j]);
             double s_ns = 0, u_ns = 0;
-            if (c->cg_fused) {   // one barrier (one timestamp) per iteration
+            const char *tv = getenv("THERMO_CG_TRACE");
+            if (c->cg_fused && tv && atoi(tv) == 2) {   // 4 stamps per iteration after phase 0
+                double d[4] = {0, 0, 0, 0};
+                int m = 0;
+                for (int k = 0; k + 1 < it && 2 + 4 * k + 4 < 1000; ++k, ++m)
+                    for (int j = 0; j < 4; ++j) d[j] += (double)(tr[2 + 4 * k + j + 1] - tr[2 + 4 * k + j]);
+                if (m > 0)
+                    fprintf(stderr, "[thermo trace] fused per iteration: sweep %.2f us, CTA reduce %.2f us, grid sync %.2f us, "
+                            "grid total + loop %.2f us (%d iters)\n", d[0] * 1e-3 / m, d[1] * 1e-3 / m, d[2] * 1e-3 / m,
+                            d[3] * 1e-3 / m, m);
+                it = 0;
+            } else if (c->cg_fused) {   // one barrier (one timestamp) per iteration
                 const int n = std::min(it, 1000);
                 fprintf(stderr, "[thermo trace] phase0 %.1f us, fused S+U %.1f us/iter (%d iters)\n",
                         (tr[1] - tr[0]) * 1e-3, n > 0 ? (tr[n] - tr[1]) * 1e-3 / std::max(n - 1, 1) : 0.0, it);
