@@ -335,6 +335,11 @@ struct Ring {
     unsigned char *stage;   // NS stages of [header | values | columns | windows]
     size_t stage_bytes, col_off, win_off;
     uint32_t n;             // stages passed through the ring so far (same count in every warp)
+    // producer: metadata of the CTA's first three chunks, loaded by the first sweep and reused by
+    // every later one (the chunk set of a CTA never changes), so a sweep starts without a
+    // global-memory round trip
+    bool meta_ok;
+    ChunkMeta m0, m1, m2;
 };
 
 __host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
@@ -372,9 +377,15 @@ __device__ __forceinline__ void sweep(const CGParams &P, Ring &R, Body &&body) {
         const uint64_t pol = policy_evict_first();
         int64_t ch = blockIdx.x;
         // metadata pipeline: chunk ch + d*G was requested d iterations ago (d = 1, 2)
-        ChunkMeta cur = load_meta<KIND, W>(P, ch, lane, G);
-        ChunkMeta m1 = load_meta<KIND, W>(P, ch + G, lane, G);
-        ChunkMeta m2 = load_meta<KIND, W>(P, ch + 2 * G, lane, G);
+        if (!R.meta_ok) {
+            R.m0 = load_meta<KIND, W>(P, ch, lane, G);
+            R.m1 = load_meta<KIND, W>(P, ch + G, lane, G);
+            R.m2 = load_meta<KIND, W>(P, ch + 2 * G, lane, G);
+            R.meta_ok = true;
+        }
+        ChunkMeta cur = R.m0;
+        ChunkMeta m1 = R.m1;
+        ChunkMeta m2 = R.m2;
         while (true) {
             const uint32_t st = R.n % NS, ph = (R.n / NS) & 1u;
             if (ch >= P.nchunks) {   // end markers for every consumer group
@@ -598,6 +609,7 @@ __global__ void __launch_bounds__(cg_threads(KIND, W, NG), KIND == 0 ? 2 : 1) k_
 
     Ring R;
     R.n = 0;
+    R.meta_ok = false;
     if (KIND != 0) {
         R.full = reinterpret_cast<uint64_t *>(ring_raw);
         R.empty = R.full + NS;
