@@ -164,19 +164,35 @@ __device__ __forceinline__ int iface_index_r(const CGParams &P, int b, int e, in
     return ik;
 }
 
+// Interface rows: entries in rounds of IB -- every column / value load of a round issued, then
+// every gather, then the sums in ascending entry order (the same order as one at a time), so a
+// row costs two dependent round trips per round instead of two per entry.
+#define IB 8
 template <bool kTwo>
 __device__ __forceinline__ double ell_row(const CGParams &P, int ik, const double *x1, const double *x2,
                                           double beta, int64_t row = -1, double *self = nullptr) {
     const int cnt = P.ell_cnt[ik];
     double acc = 0.0;
-    for (int c = 0; c < cnt; ++c) {
-        const int64_t e = (int64_t)c * P.n_if + ik;
-        const int j = P.ell_col[e];
-        double y = x1[j];
-        if (kTwo) y = fma(beta, x2[j], y);
-        const double v = P.ell_val[e];
-        acc = fma(v, y, acc);
-        if (self && j == row) *self += v;   // the interface part of the diagonal
+    for (int c0 = 0; c0 < cnt; c0 += IB) {
+        int j[IB];
+        double v[IB], y[IB];
+#pragma unroll
+        for (int u = 0; u < IB; ++u) {
+            const int64_t e = (int64_t)min(c0 + u, cnt - 1) * P.n_if + ik;
+            j[u] = P.ell_col[e];
+            v[u] = P.ell_val[e];
+        }
+#pragma unroll
+        for (int u = 0; u < IB; ++u) {
+            y[u] = x1[j[u]];
+            if (kTwo) y[u] = fma(beta, x2[j[u]], y[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < IB; ++u)
+            if (c0 + u < cnt) {
+                acc = fma(v[u], y[u], acc);
+                if (self && j[u] == row) *self += v[u];   // the interface part of the diagonal
+            }
     }
     return acc;
 }
@@ -186,16 +202,27 @@ __device__ __forceinline__ double ell_row3(const CGParams &P, int ik, const doub
                                            const double *p, double alpha, double beta, int64_t row, double *self) {
     const int cnt = P.ell_cnt[ik];
     double acc = 0.0;
-    for (int c = 0; c < cnt; ++c) {
-        const int64_t e = (int64_t)c * P.n_if + ik;
-        const int j = P.ell_col[e];
-        const double y = fma(beta, p[j], fma(-alpha, q[j], z[j]));
-        const double v = P.ell_val[e];
-        acc = fma(v, y, acc);
-        if (j == row) *self += v;
+    for (int c0 = 0; c0 < cnt; c0 += IB) {
+        int j[IB];
+        double v[IB], y[IB];
+#pragma unroll
+        for (int u = 0; u < IB; ++u) {
+            const int64_t e = (int64_t)min(c0 + u, cnt - 1) * P.n_if + ik;
+            j[u] = P.ell_col[e];
+            v[u] = P.ell_val[e];
+        }
+#pragma unroll
+        for (int u = 0; u < IB; ++u) y[u] = fma(beta, p[j[u]], fma(-alpha, q[j[u]], z[j[u]]));
+#pragma unroll
+        for (int u = 0; u < IB; ++u)
+            if (c0 + u < cnt) {
+                acc = fma(v[u], y[u], acc);
+                if (j[u] == row) *self += v[u];
+            }
     }
     return acc;
 }
+#undef IB
 
 // ---------------------------------------------------------------------------------
 // row sources: sum_k val_k * (x1[col_k] + beta * x2[col_k]) over one sliced-ELL row whose

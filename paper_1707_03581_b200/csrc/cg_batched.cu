@@ -260,12 +260,25 @@ __device__ __forceinline__ double2 row_iface(const CGBParams &P, int ik, const d
         const int cnt = P.ell_cnt[(int64_t)ik * P.S + s];
         const double b = h ? beta.y : beta.x;
         double a = 0.0;
-        for (int c = 0; c < cnt; ++c) {
-            const int64_t e = ellb(P, s, c, ik);
-            const int j = P.ell_col[e];
-            double y = x1[(int64_t)j * P.SP + s];
-            if (kTwo) y = fma(b, x2[(int64_t)j * P.SP + s], y);
-            a = fma(P.ell_val[e], y, a);
+        // rounds of 8 entries: all column / value loads, then all gathers, then the sums in
+        // ascending entry order (same order as one at a time)
+        for (int c0 = 0; c0 < cnt; c0 += 8) {
+            int j[8];
+            double v[8], y[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int64_t e = ellb(P, s, min(c0 + u, cnt - 1), ik);
+                j[u] = P.ell_col[e];
+                v[u] = P.ell_val[e];
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                y[u] = x1[(int64_t)j[u] * P.SP + s];
+                if (kTwo) y[u] = fma(b, x2[(int64_t)j[u] * P.SP + s], y[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (c0 + u < cnt) a = fma(v[u], y[u], a);
         }
         if (h) acc.y = a; else acc.x = a;
     }
