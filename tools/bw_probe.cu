@@ -71,7 +71,8 @@ __device__ __forceinline__ void bulk(void *dst, const void *src, uint32_t bytes,
 }
 
 // chunk c of `chunk` bytes goes to CTA c % G (static round robin, as the CG kernel)
-__global__ void __launch_bounds__(288, 1) read_tma(const char *a, int64_t nchunks, int chunk, int NS, double *out) {
+__global__ void __launch_bounds__(288, 1) read_tma(const char *a, int64_t nchunks, int chunk, int NS, double *out,
+                                                   int ncopies) {
     extern __shared__ __align__(128) unsigned char sm[];
     uint64_t *full = (uint64_t *)sm, *empty = full + NS;
     unsigned char *stage = sm + 128;
@@ -88,10 +89,16 @@ __global__ void __launch_bounds__(288, 1) read_tma(const char *a, int64_t nchunk
                 const uint32_t s = n % NS, ph = (n / NS) & 1u;
                 mbar_wait(&empty[s], ph ^ 1u);
                 mbar_expect(&full[s], (uint32_t)chunk);
-                // two copies per stage, like the values + columns of a CG chunk
-                const uint32_t a0 = (uint32_t)(chunk * 4 / 5) & ~15u;
-                bulk(stage + (size_t)s * chunk, a + c * chunk, a0, &full[s]);
-                bulk(stage + (size_t)s * chunk + a0, a + c * chunk + a0, chunk - a0, &full[s]);
+                if (ncopies == 1) {
+                    bulk(stage + (size_t)s * chunk, a + c * chunk, chunk, &full[s]);
+                } else {
+                    // values + columns (+ a 2-KB own-row block) of a CG chunk
+                    const uint32_t tail = ncopies >= 3 ? 2048u : 0u;
+                    const uint32_t a0 = (uint32_t)((chunk - tail) * 4 / 5) & ~15u;
+                    bulk(stage + (size_t)s * chunk, a + c * chunk, a0, &full[s]);
+                    bulk(stage + (size_t)s * chunk + a0, a + c * chunk + a0, chunk - tail - a0, &full[s]);
+                    if (tail) bulk(stage + (size_t)s * chunk + chunk - tail, a + c * chunk + chunk - tail, tail, &full[s]);
+                }
             }
         }
         return;
@@ -144,13 +151,13 @@ int main(int argc, char **argv) {
     const int64_t nv = vb / 16;
     timeit([&] { u_pattern<<<sms * 8, 256>>>((const double2 *)a, (const double2 *)b, (double2 *)c, (double2 *)d, (double2 *)e, nv); },
            7.0 * vb, "u_pattern (4 read, 3 written)");
-    for (int chunk : {40960, 49152}) for (int NS : {2, 3, 4, 5}) {
+    for (int nc : {1, 2, 3}) for (int chunk : {40960}) for (int NS : {3, 4}) {
         const size_t smem = 128 + (size_t)NS * chunk;
         if (smem > 227 * 1024) continue;
         CK(cudaFuncSetAttribute(read_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         const int64_t nch = bytes / chunk;
-        char nm[64]; snprintf(nm, sizeof nm, "read_tma chunk %d B x %d stages", chunk, NS);
-        timeit([&] { read_tma<<<sms, 288, smem>>>(a, nch, chunk, NS, out); }, (double)nch * chunk, nm);
+        char nm[64]; snprintf(nm, sizeof nm, "read_tma %d copies, %d B x %d stages", nc, chunk, NS);
+        timeit([&] { read_tma<<<sms, 288, smem>>>(a, nch, chunk, NS, out, nc); }, (double)nch * chunk, nm);
     }
     return 0;
 }
