@@ -422,6 +422,7 @@ int assemble_robin(Ctx &c) {
 
 int build_operator(Ctx &c, double dt, double mu) {
     cudaStream_t st = c.stream;
+    c.spec_valid = false;   // the Jacobi vectors are rewritten below
     k_build_vals<<<nb(c.nnz_pad), 256, 0, st>>>(c.d_A, c.d_R, c.nnz_pad, dt, c.d_val);
     CK(cudaGetLastError());
     if (!c.d_Dinv_vol) CK(cudaMalloc(&c.d_Dinv_vol, sizeof(double) * c.N));

@@ -1281,7 +1281,7 @@ int cg_launch_step(Ctx &c, int step, double dt, const double *x0, int buf, bool 
         at[0].id = cudaLaunchAttributeCooperative;
         at[0].val.cooperative = 1;
         at[1].id = cudaLaunchAttributeLaunchCompletionEvent;
-        at[1].val.launchCompletionEvent.event = c.ev_cg[step & 1];
+        at[1].val.launchCompletionEvent.event = c.ev_cg[buf];   // events follow the buffer sets
         at[1].val.launchCompletionEvent.flags = 0;
         cudaLaunchConfig_t cfg;
         memset(&cfg, 0, sizeof cfg);
@@ -1317,11 +1317,14 @@ int overlap_setup(Ctx &c) {
     CK(cudaMalloc(&c.d_if_b_b, sizeof(double) * nif));
     CK(cudaMalloc(&c.d_if_phi_b, sizeof(double) * nif));
     CK(cudaMalloc(&c.d_Dinv_b, sizeof(double) * (c.N + 16)));
+    CK(cudaMalloc(&c.d_step_sc_spec, sizeof(double) * 4));
+    CK(cudaMalloc(&c.d_spec_status, sizeof(int) * 8));
     CK(cudaMemsetAsync(c.d_ell_cnt_b, 0, sizeof(int32_t) * nif, c.stream));
     CK(cudaMemsetAsync(c.d_if_b_b, 0, sizeof(double) * nif, c.stream));
     CK(cudaMemsetAsync(c.d_if_phi_b, 0, sizeof(double) * nif, c.stream));
     CK(cudaStreamCreateWithFlags(&c.if_stream, cudaStreamNonBlocking));
-    for (cudaEvent_t *ev : {&c.ev_if[0], &c.ev_if[1], &c.ev_cg[0], &c.ev_cg[1], &c.ev_done[0], &c.ev_done[1], &c.ev_main})
+    for (cudaEvent_t *ev : {&c.ev_if[0], &c.ev_if[1], &c.ev_cg[0], &c.ev_cg[1], &c.ev_done[0], &c.ev_done[1], &c.ev_main,
+                            &c.ev_side_end})
         CK(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
     c.overlap = true;
     c.overlap_sms = free_sms;

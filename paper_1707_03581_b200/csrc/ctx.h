@@ -119,6 +119,18 @@ struct Ctx {
     // ev_if: interface(n) done; ev_cg: launch completion of solve(n) (all CTAs begun)
     cudaEvent_t ev_if[2] = {nullptr, nullptr}, ev_cg[2] = {nullptr, nullptr}, ev_main = nullptr;
     cudaEvent_t ev_done[2] = {nullptr, nullptr};   // solve(n) complete
+    // buffer set of a call's step n: (if_phase + n) & 1 (if_phase advances by nsteps per call).
+    // Speculation: after the last solve of a call, the interface of the presumed next step
+    // (t + nsteps dt, same dt) is assembled on the side stream into the next buffer set, so a
+    // caller stepping one step per call (a digital twin reading every field) still overlaps;
+    // a mismatching next call (or any rebuild / SDC step / stationary solve) discards it.
+    int if_phase = 0;
+    bool spec_valid = false;
+    double spec_t = 0.0, spec_dt = 0.0;
+    double *d_step_sc_spec = nullptr;   // [4] scalars of the speculated step
+    int *d_spec_status = nullptr;       // [8] overflow flag / step of the speculated assembly
+    bool side_pending = false;          // side-stream work not yet ordered before the main stream
+    cudaEvent_t ev_side_end = nullptr;  // recorded after the speculated assembly
     std::vector<cudaEvent_t> events_if;   // timing of the side-stream interface kernels
 
     double rtol = 1e-12;

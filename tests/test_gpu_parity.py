@@ -235,6 +235,26 @@ def test_interface_overlap_mode(monkeypatch, name):
     assert rel(runs["1"], runs["0"]) < 1e-12
     Tr, _ = O.run_config(cfg, nsteps=12)
     assert rel(runs["1"], Tr) <= TOL
+    # one step per call (the speculated assembly of the next step is used) = one call; a call
+    # that does not continue the time line (or changes dt) discards the speculation
+    monkeypatch.setenv("THERMO_OVERLAP", "1")
+    c1 = _thermo(cfg)
+    for n in range(12):
+        c1.step(n * cfg.dt, cfg.dt, 1)
+    assert np.array_equal(c1.get_T(), runs["1"])
+    d = _thermo(cfg)
+    d.step(0.0, cfg.dt, 3)
+    d.step(7.0 * cfg.dt, cfg.dt, 2)          # jump in time: speculation for t = 3 dt unused
+    d.step(9.0 * cfg.dt, 0.5 * cfg.dt, 2)    # other dt
+    d.stationary(0.0, with_interface=True)   # joins the side stream, reuses the first buffer set
+    d.step(0.0, cfg.dt, 2)
+    o = O.Oracle.from_config(cfg)
+    Ta, _ = o.step(np.full(o.n, cfg.T0), 0.0, cfg.dt, 3, cfg.scenarios[0])
+    Tb, _ = o.step(Ta, 7.0 * cfg.dt, cfg.dt, 2, cfg.scenarios[0])
+    Tc, _ = o.step(Tb, 9.0 * cfg.dt, 0.5 * cfg.dt, 2, cfg.scenarios[0])
+    Ts, _ = o.stationary(Tc, 0.0, cfg.scenarios[0], with_interface=True)
+    Td, _ = o.step(Ts, 0.0, cfg.dt, 2, cfg.scenarios[0])
+    assert rel(d.get_T(), Td) <= TOL
 
 
 @pytest.mark.parametrize("stages", [3, 5])
