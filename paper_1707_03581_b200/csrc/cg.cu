@@ -93,7 +93,8 @@ struct CGParams {
     int trace_fine;            // fused kernel: also at the iteration start, sweep end, CTA reduction
     int prefetch;              // L2 leading-edge prefetch (THERMO_CG_PREFETCH=1; measured slower on cfg3)
     int debug;                 // THERMO_CG_DEBUG bits (measurement only, results invalid):
-                               // 1 consumers skip the row work, 2 no window copies, 4 no prefetch
+                               // 1 consumers skip the row work, 2 no window copies, 4 no prefetch,
+                               // 8 no q' store
 };
 
 // Prefetch into L2 the leading edge of the column window of a chunk whose largest column
@@ -826,7 +827,7 @@ __global__ void __launch_bounds__(cg_threads(KIND, W, NG), KIND == 0 ? 2 : 1) k_
                 if (i < N) {
                     const double qs = acc / dg;
                     const double zd = zo * dg;
-                    P.q[i] = qs;
+                    if (!(P.debug & 8)) P.q[i] = qs;   // debug bit 8: timing without the store
                     red[0] = fma(pi, acc, red[0]);
                     red[1] = fma(zo, zd, red[1]);
                     red[2] = fma(zo, acc, red[2]);
