@@ -175,6 +175,23 @@ int thermo_set_solver(void *ctx, double rtol, int32_t maxit);
  * EINVAL for other orders. */
 int thermo_set_guess(void *ctx, int32_t order);
 
+/* Inspection / test aid (not needed for stepping): runs the interface kernels of every
+ * scenario at time t (stock offset s(t), friction eta(t)) for step size dt, exactly
+ * as thermo_step assembles a step, and copies scenario `scen`'s rows out.  n_if = the
+ * interface row count and cap = the row capacity (thermo_get_stats: n_iface_rows,
+ * iface_capacity); caller-owned host arrays:
+ *   rows[n_if]      coupled row index of interface row k (rail-top nodes, then stock-bottom nodes)
+ *   cnt[n_if]       entries of row k;  col[n_if][cap], val[n_if][cap]: column (coupled index) and
+ *                   value of entry q < cnt[k] (col = -1, val = 0 beyond): val = -dt K_G(t) with
+ *                   K_G = [[M_B,fix, C_B], [C_B^T, M_B,mov]], the term the operator
+ *                   M_L - dt K(t) adds on those rows;
+ *   b[n_if]         the friction source eta(t)/2 int phi_k of row k.
+ * Order of the entries within a row is unspecified.  EINVAL for a bad scenario, dt <= 0,
+ * non-finite t or NULL outputs; EGEOM on interface capacity overflow.  The solve data of the
+ * next thermo_step are unaffected (it reassembles its own interface). */
+int thermo_get_interface(void *ctx, int32_t scen, double t, double dt, int32_t *rows, int32_t *cnt,
+                         int32_t *col, double *val, double *b);
+
 typedef struct {
     int64_t n_fixed, n_moving;       /* node counts */
     int64_t nnz_volume;              /* stored nonzeros of the volume operator (unpadded) */

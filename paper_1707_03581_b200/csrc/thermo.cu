@@ -356,6 +356,64 @@ extern "C" int thermo_stationary(void *ctx, double t, int32_t with_interface) {
     }
 }
 
+extern "C" int thermo_get_interface(void *ctx, int32_t scen, double t, double dt, int32_t *rows, int32_t *cnt,
+                                    int32_t *col, double *val, double *b) {
+    Ctx *c = (Ctx *)ctx;
+    if (!c) return THERMO_EINVAL;
+    if (scen < 0 || scen >= c->S) return fail(c, THERMO_EINVAL, "scenario index out of range");
+    if (!(dt > 0) || !std::isfinite(t)) return fail(c, THERMO_EINVAL, "dt must be > 0 and t finite");
+    if (!rows || !cnt || !col || !val || !b) return fail(c, THERMO_EINVAL, "output pointer is NULL");
+    try {
+        const int S = c->S, nif = c->n_if, cap = c->cap;
+        if (nif == 0) return THERMO_OK;
+        API_CK(side_join(c));
+        c->spec_valid = false;   // the first interface buffer set is rewritten below
+        std::vector<double> sc(4 * (size_t)S);
+        for (int q = 0; q < S; ++q) {   // the time scalars of thermo_step (reading R3) at time t
+            const thermo::Scen &w = c->scen[q];
+            const double sv = w.s0 + w.amp * std::sin(2.0 * M_PI * t / w.period);
+            const double eta = w.eta0 * (1.0 + w.eta_amp * std::sin(2.0 * M_PI * t / w.eta_period));
+            sc[4 * q + 0] = sv * w.d2[0];
+            sc[4 * q + 1] = sv * w.d2[1];
+            sc[4 * q + 2] = eta;
+            sc[4 * q + 3] = sv;
+        }
+        double *d_sc = nullptr;
+        API_CK(cudaMalloc(&d_sc, sizeof(double) * sc.size()));
+        API_CK(cudaMemcpyAsync(d_sc, sc.data(), sizeof(double) * sc.size(), cudaMemcpyHostToDevice, c->stream));
+        API_CK(cudaMemsetAsync(c->d_status, 0, sizeof(int) * 8, c->stream));
+        thermo::IfaceParams P;
+        memset(&P, 0, sizeof P);
+        thermo::iface_params(*c, P, d_sc, dt);
+        if (thermo::iface_launch(*c, P)) { cudaFree(d_sc); return THERMO_ECUDA; }
+        std::vector<int32_t> h_cnt((size_t)nif * S), h_col((size_t)nif * S * cap), h_rows(nif);
+        std::vector<double> h_val((size_t)nif * S * cap), h_b((size_t)nif * S);
+        int status[8];
+        API_CK(cudaMemcpyAsync(h_cnt.data(), c->d_ell_cnt, sizeof(int32_t) * h_cnt.size(), cudaMemcpyDeviceToHost, c->stream));
+        API_CK(cudaMemcpyAsync(h_col.data(), c->d_ell_col, sizeof(int32_t) * h_col.size(), cudaMemcpyDeviceToHost, c->stream));
+        API_CK(cudaMemcpyAsync(h_val.data(), c->d_ell_val, sizeof(double) * h_val.size(), cudaMemcpyDeviceToHost, c->stream));
+        API_CK(cudaMemcpyAsync(h_b.data(), c->d_if_b, sizeof(double) * h_b.size(), cudaMemcpyDeviceToHost, c->stream));
+        API_CK(cudaMemcpyAsync(h_rows.data(), c->d_if_rows, sizeof(int32_t) * nif, cudaMemcpyDeviceToHost, c->stream));
+        API_CK(cudaMemcpyAsync(status, c->d_status, sizeof status, cudaMemcpyDeviceToHost, c->stream));
+        API_CK(cudaStreamSynchronize(c->stream));
+        cudaFree(d_sc);
+        if (status[1]) return fail(c, THERMO_EGEOM, "interface row capacity exceeded");
+        for (int k = 0; k < nif; ++k) {
+            rows[k] = h_rows[k];
+            cnt[k] = h_cnt[thermo::row_index(P, scen, k)];
+            b[k] = h_b[thermo::row_index(P, scen, k)];
+            for (int q = 0; q < cap; ++q) {
+                const int64_t e = thermo::ell_index(P, scen, q, k);
+                col[(int64_t)k * cap + q] = q < cnt[k] ? h_col[e] : -1;
+                val[(int64_t)k * cap + q] = q < cnt[k] ? h_val[e] : 0.0;
+            }
+        }
+        return THERMO_OK;
+    } catch (...) {
+        return fail(c, THERMO_ENOMEM, "host allocation failed");
+    }
+}
+
 extern "C" int thermo_set_guess(void *ctx, int32_t order) {
     Ctx *c = (Ctx *)ctx;
     if (!c) return THERMO_EINVAL;

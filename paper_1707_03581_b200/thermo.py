@@ -21,7 +21,7 @@ _CODES = {-1: "EINVAL", -2: "ENOMEM", -3: "ECUDA", -4: "ENOCONV", -5: "EGEOM"}
 EXPORTS = ["thermo_create_mesh", "thermo_set_bc", "thermo_step", "thermo_get_T", "thermo_set_T",
            "thermo_set_solver", "thermo_get_stats", "thermo_get_step_iters", "thermo_last_error",
            "thermo_destroy", "thermo_set_timing", "thermo_set_method", "thermo_stationary",
-           "thermo_get_T_async", "thermo_sync", "thermo_set_guess"]
+           "thermo_get_T_async", "thermo_sync", "thermo_set_guess", "thermo_get_interface"]
 
 
 class ThermoError(RuntimeError):
@@ -77,6 +77,7 @@ def load(path: str = LIB_PATH):
     L.thermo_set_T.argtypes = [vp, i32, i32, vp, i64, i32]
     L.thermo_set_solver.argtypes = [vp, d, i32]
     L.thermo_set_guess.argtypes = [vp, i32]
+    L.thermo_get_interface.argtypes = [vp, i32, d, d, vp, vp, vp, vp, vp]
     L.thermo_get_stats.argtypes = [vp, ctypes.POINTER(Stats)]
     L.thermo_get_step_iters.argtypes = [vp, ctypes.POINTER(ctypes.c_int32), i64]
     L.thermo_last_error.argtypes = [vp]
@@ -170,6 +171,18 @@ class Thermo:
 
     def set_solver(self, rtol=1e-12, maxit=0):
         self._check(load().thermo_set_solver(self.h, rtol, maxit))
+
+    def get_interface(self, t: float, dt: float, scen: int = 0):
+        """Interface rows of scenario `scen` at time t for step dt (thermo_get_interface):
+        (rows[n_if], cnt[n_if], col[n_if, cap], val[n_if, cap] = -dt K_G entries, b[n_if])."""
+        import numpy as np
+        st = self.stats()
+        n, cap = st["n_iface_rows"], st["iface_capacity"]
+        rows, cnt = np.zeros(n, np.int32), np.zeros(n, np.int32)
+        col, val, b = np.zeros((n, cap), np.int32), np.zeros((n, cap)), np.zeros(n)
+        self._check(load().thermo_get_interface(self.h, int(scen), float(t), float(dt), rows.ctypes.data,
+                                                cnt.ctypes.data, col.ctypes.data, val.ctypes.data, b.ctypes.data))
+        return rows, cnt, col, val, b
 
     def set_guess(self, order: int):
         """CG initial guess: 0 = T^n, 1 / 2 = linear / quadratic extrapolation (thermo_set_guess)."""

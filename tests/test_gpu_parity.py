@@ -345,3 +345,33 @@ def test_one_row_tail_slice(stock_cells):
     o = O.Oracle(f, m, 50.0, 3.6e6, 1000.0, robin=robin)
     Tr, _ = o.step(np.full(o.n, 24.0), 0.0, 5.0, 8, sc, solver="cholesky")
     assert rel(th.get_T(), Tr) <= TOL
+
+
+@pytest.mark.parametrize("name,jitter", [("cfg0", None), ("small", 0.1)])
+def test_interface_rows_vs_oracle_matrices(name, jitter):
+    """Per-kernel check of the interface assembly: the GPU's interface rows
+    (-dt K_G(t) entries) and friction sources (eta/2 int phi) at several stock
+    positions against the oracle's independently clipped and integrated matrices, entry by entry."""
+    cfg = I.make_config(name, jitter=jitter)
+    th = _thermo(cfg)
+    o = O.Oracle.from_config(cfg)
+    sc = cfg.scenarios[0]
+    dt = 0.7
+    for t in (0.0, 3.3, 11.0, 17.25, 41.0):
+        rows, cnt, col, val, b = th.get_interface(t, dt)
+        s, eta = I.scenario_scalars(sc, t)
+        rp, icol, ival, bG, area = o.interface(np.array(sc.dir) * s, eta)
+        scale = max(np.abs(ival).max() * dt, 1e-300)
+        worst = 0.0
+        for k, r in enumerate(rows):
+            g = {}
+            for q in range(cnt[k]):
+                g[int(col[k, q])] = g.get(int(col[k, q]), 0.0) + val[k, q]
+            ref = {int(c): -dt * v for c, v in zip(icol[rp[r]:rp[r + 1]], ival[rp[r]:rp[r + 1]])}
+            for c in set(g) | set(ref):
+                worst = max(worst, abs(g.get(c, 0.0) - ref.get(c, 0.0)))
+            assert abs(b[k] - bG[r]) <= 1e-13 * max(abs(bG).max(), 1e-300), (t, k)
+        assert worst <= 1e-13 * scale, (t, worst / scale)
+        # rows outside the interface carry no interface terms in the oracle either
+        others = np.setdiff1d(np.arange(o.n), rows)
+        assert np.all(rp[others + 1] - rp[others] == 0) or np.abs(ival).max() == 0
