@@ -121,3 +121,37 @@ def test_coincident_edges_and_vertices(s0):
     Tr, _ = O.Oracle.from_config(cfg).step(np.full(cfg.n_dof, cfg.T0), 0.0, cfg.dt, 6, sc, solver="cholesky")
     assert rel(th.get_T(), Tr) <= TOL
     assert abs(th.stats()["iface_area"] - 0.05) < 1e-14
+
+
+def _single_tet(pts, tags):
+    """One positively oriented tetrahedron with its four outward faces and their tags."""
+    x = np.array(pts, dtype=np.float64)
+    t = [0, 1, 2, 3]
+    if np.linalg.det(np.stack([x[1] - x[0], x[2] - x[0], x[3] - x[0]])) < 0:
+        t = [0, 2, 1, 3]
+    faces = np.array([[t[1], t[2], t[3]], [t[0], t[3], t[2]], [t[0], t[1], t[3]], [t[0], t[2], t[1]]], np.int32)
+    return I.Mesh(xyz=x, tets=np.array([t], np.int32), bfaces=faces,
+                  bface_tag=np.array([tags[tuple(sorted(f))] for f in faces.tolist()], np.int32))
+
+
+def test_smallest_pair_one_tet_each():
+    """SURVEY 4.1's smallest real case: one tetrahedron per part (8 DoF), a triangular contact
+    patch partially covered and moving, Robin floor and cooled top; GPU vs the oracle's dense
+    Cholesky over a few steps (the degenerate end of every kernel: one slice, one chunk, one
+    triangle per surface)."""
+    # fixed tet: top face (nodes 0, 1, 2) in z = 0.1 is the contact surface, the rest is floor
+    fixed = _single_tet([(0, 0, 0.1), (1, 0, 0.1), (0, 1, 0.1), (0, 0, 0)],
+                        {(0, 1, 2): 4, (0, 1, 3): 3, (0, 2, 3): 3, (1, 2, 3): 3})
+    # moving tet: bottom face (nodes 0, 1, 2) in z = 0.1, the others cooled
+    moving = _single_tet([(0.1, 0.1, 0.1), (0.6, 0.1, 0.1), (0.1, 0.6, 0.1), (0.1, 0.1, 0.4)],
+                         {(0, 1, 2): 4, (0, 1, 3): 2, (0, 2, 3): 2, (1, 2, 3): 2})
+    cfg = I.make_config("cfg0")
+    cfg.fixed, cfg.moving = fixed, moving
+    cfg.robin = [I.Robin(0, 3, 50.0, 24.0), I.Robin(1, 2, 200.0, 18.0)]
+    cfg.scenarios = [I.Scenario(0.2, 0.2, 8.0, 500.0, 0.5, 3.0)]   # partly off the fixed triangle
+    from paper_1707_03581_b200.thermo import Thermo
+    th = Thermo.from_config(cfg)
+    th.step(0.0, 1.0, 6)
+    Tr, st = O.run_config(cfg, nsteps=6, solver="cholesky")
+    assert rel(th.get_T(), Tr) <= TOL
+    assert th.stats()["failed_step"] == -1
