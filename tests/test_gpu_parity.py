@@ -375,3 +375,27 @@ def test_interface_rows_vs_oracle_matrices(name, jitter):
         # rows outside the interface carry no interface terms in the oracle either
         others = np.setdiff1d(np.arange(o.n), rows)
         assert np.all(rp[others + 1] - rp[others] == 0) or np.abs(ival).max() == 0
+
+
+def test_interface_rows_batched_scenarios():
+    """The same per-kernel check for a batched context: the rows of scenarios 1 and 2 (their own
+    stock positions and friction laws, blockIdx.y = scenario) against the oracle."""
+    from paper_1707_03581_b200.thermo import Thermo
+    cfg = I.make_config("small", jitter=0.1)
+    scen = [I.Scenario(0.375, 0.375, 20.0 + 7 * k, 100.0 + 150.0 * k, 0.3 * k, 9.0) for k in range(3)]
+    th = Thermo.from_config(cfg, scenarios=scen)
+    o = O.Oracle.from_config(cfg)
+    dt, t = 0.5, 6.5
+    for k in (1, 2):
+        rows, cnt, col, val, b = th.get_interface(t, dt, scen=k)
+        s, eta = I.scenario_scalars(scen[k], t)
+        rp, icol, ival, bG, area = o.interface(np.array(scen[k].dir) * s, eta)
+        scale = np.abs(ival).max() * dt
+        for j, r in enumerate(rows):
+            g = {}
+            for q in range(cnt[j]):
+                g[int(col[j, q])] = g.get(int(col[j, q]), 0.0) + val[j, q]
+            ref = {int(c): -dt * v for c, v in zip(icol[rp[r]:rp[r + 1]], ival[rp[r]:rp[r + 1]])}
+            for c in set(g) | set(ref):
+                assert abs(g.get(c, 0.0) - ref.get(c, 0.0)) <= 1e-13 * scale, (k, j, c)
+            assert abs(b[j] - bG[r]) <= 1e-13 * np.abs(bG).max(), (k, j)
