@@ -653,6 +653,7 @@ extern "C" int thermo_step(void *ctx, double t, double dt, int32_t nsteps) {
             P.status = c->d_spec_status;
             P.step = 0;
             if (thermo::iface_launch(*c, P, c->if_stream)) return THERMO_ECUDA;
+            launches += c->n_if ? 2 : 0;   // launched by this call (for the next call's first step)
             API_CK(cudaEventRecord(c->ev_if[nb], c->if_stream));
             API_CK(cudaEventRecord(c->ev_side_end, c->if_stream));
             c->side_pending = true;
