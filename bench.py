@@ -127,9 +127,20 @@ def dist_setup():
     return env_world()
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_baseline(cfg, steps=1):
-    """The oracle as it stands (plain C, one thread) on a bounded sample: `steps` full IE
-    steps of the same workload; create/assembly excluded from the timed region."""
+    """The oracle as it stands (plain C; its CG loops on all host cores via OpenMP, assembly and
+    interface serial) on a bounded sample: `steps` full IE steps of the same workload;
+    create/assembly excluded from the timed region."""
     import oracle as O
     t0 = time.time()
     o = O.Oracle.from_config(cfg)
@@ -138,9 +149,12 @@ def cpu_baseline(cfg, steps=1):
     t0 = time.perf_counter()
     T, st = o.step(T, 0.0, cfg.dt, steps, cfg.scenarios[0])
     dt = time.perf_counter() - t0
-    return {"value": cfg.n_dof * steps / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{steps} full implicit-Euler step(s) of {cfg.name} ({cfg.n_dof} DoF), single-thread C "
-                      f"oracle, CG iterations {int(st[:, 0].sum())}, assembly ({t_create:.0f} s) untimed",
+    thr = O.threads()
+    return {"value": cfg.n_dof * steps / dt, "unit": UNIT, "cores": thr, "kind": "oracle",
+            "cpu_model": cpu_model(), "nproc": os.cpu_count(),
+            "sample": f"{steps} full implicit-Euler step(s) of {cfg.name} ({cfg.n_dof} DoF, scenario 0), C oracle "
+                      f"with its CG loops on {thr} OpenMP threads ({os.cpu_count()} host cores, {cpu_model()}), "
+                      f"CG iterations {int(st[:, 0].sum())}, assembly ({t_create:.0f} s) untimed",
             "seconds": dt}
 
 
@@ -163,7 +177,7 @@ def run_reference(args):
             "config": {"workload": f"BASELINE {workload_name(cfg.name)} ({cfg.name}): {cfg.description}",
                        "n_dof": cfg.n_dof,
                        "dt": cfg.dt, "sample": f"{steps} of the requested {args.steps} steps (bounded)"},
-            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model", "nproc")},
             "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -285,7 +299,7 @@ def run_thermo(args):
     th.close()
     if not args.no_cpu_baseline and world == 1:
         cb = cpu_baseline(cfg, 1)
-        line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model", "nproc")}
     print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.barrier()

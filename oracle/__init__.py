@@ -25,9 +25,10 @@ _p = ctypes.c_void_p
 
 
 def build(force: bool = False) -> str:
-    """Compile oracle.c -> liboracle.so with gcc (plain C99, -O2)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        subprocess.check_call(["gcc", "-std=c99", "-O2", "-fPIC", "-shared", "-o", _LIB, _SRC, "-lm"])
+    """Compile oracle.c -> liboracle.so with gcc (plain C99, -O2, OpenMP on the CG loops)."""
+    hdr = os.path.join(_HERE, "oracle.h")
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < max(os.path.getmtime(_SRC), os.path.getmtime(hdr)):
+        subprocess.check_call(["gcc", "-std=c99", "-O2", "-fopenmp", "-fPIC", "-shared", "-o", _LIB, _SRC, "-lm"])
     return _LIB
 
 
@@ -40,6 +41,7 @@ def lib():
         L.or_create.argtypes = [_i64, _p, _i64, _p, _i64, _p, _p, _i64, _p, _i64, _p, _i64, _p, _p,
                                 _i32, _d, _d, _d]
         L.or_last_error.restype = ctypes.c_char_p
+        L.or_threads.restype = ctypes.c_int
         L.or_destroy.argtypes = [_p]
         L.or_set_robin.argtypes = [_p, _i32, _i32, _d, _d, _d, _d, _d]
         L.or_n.restype = _i64
@@ -64,6 +66,11 @@ def lib():
                                     _d, _p]
         _lib = L
     return _lib
+
+
+def threads() -> int:
+    """Host threads the oracle's CG loops run on (OMP_NUM_THREADS, default all cores)."""
+    return int(lib().or_threads())
 
 
 def _ptr(a: np.ndarray):

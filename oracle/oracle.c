@@ -1,9 +1,15 @@
 /*
  * oracle.c -- plain CPU oracle for the implicit-Euler hot path of arXiv 1707.03581.
  *
- * TEST INFRASTRUCTURE ONLY (see oracle.h).  Plain C99, fp64, single thread, no blocking,
- * fusion or reordering beyond the definitions cited at each function.  Written
- * independently of the CUDA library; the two share no code.
+ * TEST INFRASTRUCTURE ONLY (see oracle.h).  Plain C99, fp64, no blocking, fusion or
+ * reordering beyond the definitions cited at each function.  Written independently of the
+ * CUDA library; the two share no code.
+ *
+ * Threads: built with -fopenmp, the loops of the CG solves (row-wise products, vector
+ * updates) run on all host cores (OMP_NUM_THREADS).  Every row / element is still computed
+ * by the same sequential expression, and the dot products use a fixed partition into
+ * OR_DOT_BLOCKS contiguous blocks summed in block order, so every result is bitwise the same
+ * for any thread count (and without OpenMP).  Assembly and the interface stay serial.
  *
  * Pins (tests/test_oracle_*.py): volume = sum of lumped mass; stiffness rows sum to 0;
  * Kuhn 7-point closed form; patch test; Robin sums against exact polynomial integrals;
@@ -22,11 +28,32 @@
 #define M_PI 3.14159265358979323846
 #endif
 
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+int or_threads(void) {
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
+
 static char g_err[512];
 static void set_err(const char *msg) { snprintf(g_err, sizeof g_err, "%s", msg); }
 const char *or_last_error(void) { return g_err; }
 
 #define MAX_ROBIN 64
+
+/* parallel loop over n independent rows / elements (no effect without -fopenmp) */
+#ifdef _OPENMP
+#define OR_PAR_FOR _Pragma("omp parallel for schedule(static) if(n > 16384)")
+#else
+#define OR_PAR_FOR
+#endif
+/* dot products: fixed partition into this many contiguous blocks, summed in block order */
+#define OR_DOT_BLOCKS 64
 
 typedef struct {
     int32_t part, tag;
@@ -592,7 +619,9 @@ void or_get_interface(const or_sys *s, int64_t *rowptr, int32_t *col, double *va
 /* ------------------------------------------------------------------------------------ */
 
 void or_apply_system(const or_sys *s, double dt, const double *x, double *y) {
-    for (int64_t i = 0; i < s->n; i++) {
+    const int64_t n = s->n;
+    OR_PAR_FOR
+    for (int64_t i = 0; i < n; i++) {
         double acc = 0.0;
         for (int64_t k = s->rowptr[i]; k < s->rowptr[i + 1]; k++)
             acc += (s->A[k] + s->B[k]) * x[s->col[k]];
@@ -603,7 +632,9 @@ void or_apply_system(const or_sys *s, double dt, const double *x, double *y) {
 }
 
 static void system_diagonal(const or_sys *s, double dt, double *d) {
-    for (int64_t i = 0; i < s->n; i++) {
+    const int64_t n = s->n;
+    OR_PAR_FOR
+    for (int64_t i = 0; i < n; i++) {
         double kii = 0.0;
         int64_t k = find_entry(s->rowptr, s->col, i, (int32_t)i);
         kii += s->A[k] + s->B[k];
@@ -614,12 +645,24 @@ static void system_diagonal(const or_sys *s, double dt, double *d) {
 }
 
 static void system_rhs(const or_sys *s, double dt, const double *T, double *b) {
-    for (int64_t i = 0; i < s->n; i++) b[i] = s->mass * s->ML[i] * T[i] + dt * (s->benv[i] + s->bG[i]);
+    const int64_t n = s->n;
+    OR_PAR_FOR
+    for (int64_t i = 0; i < n; i++) b[i] = s->mass * s->ML[i] * T[i] + dt * (s->benv[i] + s->bG[i]);
 }
 
+/* sum_i a_i b_i: sequential sums over OR_DOT_BLOCKS fixed contiguous blocks, then the block
+ * sums in block order (the same bits for any thread count) */
 static double dot(int64_t n, const double *a, const double *b) {
+    double part[OR_DOT_BLOCKS];
+    OR_PAR_FOR
+    for (int k = 0; k < OR_DOT_BLOCKS; k++) {
+        int64_t lo = n * k / OR_DOT_BLOCKS, hi = n * (k + 1) / OR_DOT_BLOCKS;
+        double acc = 0.0;
+        for (int64_t i = lo; i < hi; i++) acc += a[i] * b[i];
+        part[k] = acc;
+    }
     double acc = 0.0;
-    for (int64_t i = 0; i < n; i++) acc += a[i] * b[i];
+    for (int k = 0; k < OR_DOT_BLOCKS; k++) acc += part[k];
     return acc;
 }
 
@@ -634,6 +677,7 @@ static int64_t pcg(const or_sys *s, double dt, const double *b, double *x, doubl
     if (!r || !z || !p || !q || !d) return -2;
     system_diagonal(s, dt, d);
     or_apply_system(s, dt, x, q);
+    OR_PAR_FOR
     for (int64_t i = 0; i < n; i++) { r[i] = b[i] - q[i]; z[i] = r[i] / d[i]; p[i] = z[i]; }
     double bnorm = sqrt(dot(n, b, b));
     double rz = dot(n, r, z);
@@ -642,17 +686,21 @@ static int64_t pcg(const or_sys *s, double dt, const double *b, double *x, doubl
     while (rnorm > rtol * bnorm && it < maxit) {
         or_apply_system(s, dt, p, q);
         double alpha = rz / dot(n, p, q);
+        OR_PAR_FOR
         for (int64_t i = 0; i < n; i++) { x[i] += alpha * p[i]; r[i] -= alpha * q[i]; }
+        OR_PAR_FOR
         for (int64_t i = 0; i < n; i++) z[i] = r[i] / d[i];
         double rz_new = dot(n, r, z);
         double beta = rz_new / rz;
         rz = rz_new;
+        OR_PAR_FOR
         for (int64_t i = 0; i < n; i++) p[i] = z[i] + beta * p[i];
         rnorm = sqrt(dot(n, r, r));
         it++;
     }
     *relres = bnorm > 0 ? rnorm / bnorm : rnorm;
     or_apply_system(s, dt, x, q);
+    OR_PAR_FOR
     for (int64_t i = 0; i < n; i++) r[i] = b[i] - q[i];
     *truerel = bnorm > 0 ? sqrt(dot(n, r, r)) / bnorm : sqrt(dot(n, r, r));
     free(r); free(z); free(p); free(q); free(d);
@@ -907,7 +955,9 @@ int or_mrsdc_weights(int M, int P, double t0, double dt, double *tau, double *ta
 
 /* y = (A + B_env) x  (f^I without g) */
 static void apply_vol(const or_sys *s, const double *x, double *y) {
-    for (int64_t i = 0; i < s->n; i++) {
+    const int64_t n = s->n;
+    OR_PAR_FOR
+    for (int64_t i = 0; i < n; i++) {
         double acc = 0.0;
         for (int64_t k = s->rowptr[i]; k < s->rowptr[i + 1]; k++) acc += (s->A[k] + s->B[k]) * x[s->col[k]];
         y[i] = acc;
@@ -935,22 +985,28 @@ static int64_t pcg_shifted(const or_sys *s, double a, const double *b, double *x
     double *p = malloc(sizeof *p * (size_t)n), *q = malloc(sizeof *q * (size_t)n);
     double *d = malloc(sizeof *d * (size_t)n);
     if (!r || !z || !p || !q || !d) return -2;
+    OR_PAR_FOR
     for (int64_t i = 0; i < n; i++) {
         int64_t k = find_entry(s->rowptr, s->col, i, (int32_t)i);
         d[i] = s->ML[i] - a * (s->A[k] + s->B[k]);
     }
     apply_vol(s, x, q);
+    OR_PAR_FOR
     for (int64_t i = 0; i < n; i++) { r[i] = b[i] - (s->ML[i] * x[i] - a * q[i]); z[i] = r[i] / d[i]; p[i] = z[i]; }
     double bnorm = sqrt(dot(n, b, b)), rz = dot(n, r, z), rnorm = sqrt(dot(n, r, r));
     int64_t it = 0;
     while (rnorm > rtol * bnorm && it < maxit) {
         apply_vol(s, p, q);
+        OR_PAR_FOR
         for (int64_t i = 0; i < n; i++) q[i] = s->ML[i] * p[i] - a * q[i];
         double alpha = rz / dot(n, p, q);
+        OR_PAR_FOR
         for (int64_t i = 0; i < n; i++) { x[i] += alpha * p[i]; r[i] -= alpha * q[i]; }
+        OR_PAR_FOR
         for (int64_t i = 0; i < n; i++) z[i] = r[i] / d[i];
         double rz_new = dot(n, r, z), beta = rz_new / rz;
         rz = rz_new;
+        OR_PAR_FOR
         for (int64_t i = 0; i < n; i++) p[i] = z[i] + beta * p[i];
         rnorm = sqrt(dot(n, r, r));
         it++;

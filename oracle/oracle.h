@@ -43,6 +43,8 @@ or_sys *or_create(int64_t nf, const double *xyz_f, int64_t ntf, const int32_t *t
                   int64_t nbm, const int32_t *faces_m, const int32_t *tags_m,
                   int32_t iface_tag, double nu, double rho_cp, double alpha_iface);
 const char *or_last_error(void);
+/* host threads the CG loops use (OMP_NUM_THREADS; 1 without OpenMP) */
+int or_threads(void);
 void or_destroy(or_sys *s);
 
 /* Robin data for (part, tag): alpha_i and T_i(x) = T_ref + g . x.  Re-assembles

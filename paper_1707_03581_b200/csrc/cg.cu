@@ -980,31 +980,42 @@ __global__ void __launch_bounds__(256) k_chunk_windows(const int64_t *slice_ptr,
             __syncthreads();
         }
     if (threadIdx.x == 0) {   // runs (serial over <= 4096 sorted keys)
+        // at most CG_MAXR runs are recorded (the run arrays hold CW_MAXE / 2 + 1 > CG_MAXR):
+        // a chunk with more (a scattered numbering) disqualifies the variant (stats[1])
         int nr = 0;
-        for (int j = 0; j < E; ++j) {
+        bool over = E == 0;
+        for (int j = 0; j < E && !over; ++j) {
             if (j == 0 || key[j] - key[j - 1] > gap + 1) {
+                if (nr == CG_MAXR) { over = true; break; }
                 rstart[nr] = key[j] & ~1;
                 if (nr > 0) rlast[nr - 1] = key[j - 1];
                 ++nr;
             }
         }
-        rlast[nr - 1] = key[E - 1];
-        roff[0] = 0;
-        for (int r = 0; r < nr; ++r) roff[r + 1] = roff[r] + (((rlast[r] + 2) & ~1) - rstart[r]);
-        nr_s = nr;
-        atomicMax(&stats[0], roff[nr]);
-        atomicMax(&stats[1], nr);
-        if (roff[nr] > 65535) atomicOr(&stats[2], 2);
-        nruns_out[ch] = nr;
-        // local index of the chunk's first row (its own rows are one contiguous block)
-        const int r0 = (int)(s0 * 32);
-        int lo = 0;
-        for (int r = 0; r < nr; ++r) if (rstart[r] <= r0) lo = r;
-        lown_out[ch] = roff[lo] + (r0 - rstart[lo]);
-        for (int r = 0; r < nr && r < CG_MAXR; ++r) runs_out[ch * CG_MAXR + r] = make_int2(rstart[r], roff[r + 1] - roff[r]);
+        if (over) {
+            atomicMax(&stats[1], CG_MAXR + 1);
+            nruns_out[ch] = 0;
+            nr_s = 0;
+        } else {
+            rlast[nr - 1] = key[E - 1];
+            roff[0] = 0;
+            for (int r = 0; r < nr; ++r) roff[r + 1] = roff[r] + (((rlast[r] + 2) & ~1) - rstart[r]);
+            nr_s = nr;
+            atomicMax(&stats[0], roff[nr]);
+            atomicMax(&stats[1], nr);
+            if (roff[nr] > 65535) atomicOr(&stats[2], 2);
+            nruns_out[ch] = nr;
+            // local index of the chunk's first row (its own rows are one contiguous block)
+            const int r0 = (int)(s0 * 32);
+            int lo = 0;
+            for (int r = 0; r < nr; ++r) if (rstart[r] <= r0) lo = r;
+            lown_out[ch] = roff[lo] + (r0 - rstart[lo]);
+            for (int r = 0; r < nr; ++r) runs_out[ch * CG_MAXR + r] = make_int2(rstart[r], roff[r + 1] - roff[r]);
+        }
     }
     __syncthreads();
     const int nr = nr_s;
+    if (nr == 0) return;   // variant rejected (stats); lcol is not used
     for (int e = threadIdx.x; e < E; e += blockDim.x) {
         const int c = col[e0 + e];
         int lo = 0, hi = nr - 1;

@@ -28,6 +28,12 @@ static thread_local std::string g_create_err;
         }                                                                        \
     } while (0)
 
+// owns one temporary device allocation for the duration of an ABI call (freed on every path)
+struct DevBuf {
+    void *p = nullptr;
+    ~DevBuf() { if (p) cudaFree(p); }
+};
+
 static int fail(Ctx *c, int code, const std::string &msg) {
     c->err = msg;
     return code;
@@ -51,6 +57,11 @@ static cudaError_t side_join(Ctx *c) {
 
 static void free_ctx(Ctx *c) {
     if (!c) return;
+    // the side stream (a speculated interface assembly) and the copy stream may still read or
+    // write the buffers freed below
+    if (c->if_stream) cudaStreamSynchronize(c->if_stream);
+    if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
+    cudaStreamSynchronize(c->stream);
     void *ptrs[] = {c->d_xyz, c->d_tets, c->d_faces, c->d_fkey, c->d_tinc_ptr, c->d_tinc, c->d_finc_ptr,
                     c->d_finc, c->d_slice_ptr, c->d_col, c->d_A, c->d_R, c->d_val, c->d_diagpos, c->d_ML,
                     c->d_benv, c->d_Dvol, c->d_Dinv, c->d_robin_tab, c->d_if_rows, c->d_uv, c->d_star_ptr,
@@ -378,14 +389,15 @@ extern "C" int thermo_get_interface(void *ctx, int32_t scen, double t, double dt
             sc[4 * q + 2] = eta;
             sc[4 * q + 3] = sv;
         }
-        double *d_sc = nullptr;
-        API_CK(cudaMalloc(&d_sc, sizeof(double) * sc.size()));
+        DevBuf sc_buf;
+        API_CK(cudaMalloc(&sc_buf.p, sizeof(double) * sc.size()));
+        double *d_sc = (double *)sc_buf.p;
         API_CK(cudaMemcpyAsync(d_sc, sc.data(), sizeof(double) * sc.size(), cudaMemcpyHostToDevice, c->stream));
         API_CK(cudaMemsetAsync(c->d_status, 0, sizeof(int) * 8, c->stream));
         thermo::IfaceParams P;
         memset(&P, 0, sizeof P);
         thermo::iface_params(*c, P, d_sc, dt);
-        if (thermo::iface_launch(*c, P)) { cudaFree(d_sc); return THERMO_ECUDA; }
+        if (thermo::iface_launch(*c, P)) return THERMO_ECUDA;
         std::vector<int32_t> h_cnt((size_t)nif * S), h_col((size_t)nif * S * cap), h_rows(nif);
         std::vector<double> h_val((size_t)nif * S * cap), h_b((size_t)nif * S);
         int status[8];
@@ -396,7 +408,6 @@ extern "C" int thermo_get_interface(void *ctx, int32_t scen, double t, double dt
         API_CK(cudaMemcpyAsync(h_rows.data(), c->d_if_rows, sizeof(int32_t) * nif, cudaMemcpyDeviceToHost, c->stream));
         API_CK(cudaMemcpyAsync(status, c->d_status, sizeof status, cudaMemcpyDeviceToHost, c->stream));
         API_CK(cudaStreamSynchronize(c->stream));
-        cudaFree(d_sc);
         if (status[1]) return fail(c, THERMO_EGEOM, "interface row capacity exceeded");
         for (int k = 0; k < nif; ++k) {
             rows[k] = h_rows[k];
@@ -633,12 +644,16 @@ extern "C" int thermo_step(void *ctx, double t, double dt, int32_t nsteps) {
             if (ovl) API_CK(cudaEventRecord(c->ev_done[bs(n)], c->stream));
             if (ovl && n + 1 < nsteps && side_iface(n + 1)) return THERMO_ECUDA;
         }
-        if (ovl) {
-            // speculation: the interface of the presumed next call's first step (time
-            // t + (nsteps + 1) dt) into the buffer set after this call's last one
+        const bool spec_on = !getenv("THERMO_SPEC") || atoi(getenv("THERMO_SPEC")) != 0;   // test hook
+        if (ovl && spec_on) {
+            // speculation: the interface of the presumed next call's first step into the
+            // buffer set after this call's last one.  The next call starts at ts = t + nsteps dt
+            // and evaluates its first step at ts + 1 * dt: the same expression here, so the
+            // speculated assembly is bitwise the one the next call would compute
             const int nb = bs(nsteps);
             const thermo::Scen &q = c->scen[0];
-            const double tp = t + (double)(nsteps + 1) * dt;
+            const double ts = t + (double)nsteps * dt;
+            const double tp = ts + (double)1 * dt;
             const double sv = q.s0 + q.amp * std::sin(2.0 * M_PI * tp / q.period);
             const double eta = q.eta0 * (1.0 + q.eta_amp * std::sin(2.0 * M_PI * tp / q.eta_period));
             const double h_sc[4] = {sv * q.d2[0], sv * q.d2[1], eta, sv};
@@ -741,7 +756,7 @@ extern "C" int thermo_step(void *ctx, double t, double dt, int32_t nsteps) {
         c->steps_done += nsteps;
         if (spec_launched) {   // valid for a next call that continues at t + nsteps dt
             c->spec_valid = true;
-            c->spec_t = t + (double)nsteps * dt;
+            c->spec_t = t + (double)nsteps * dt;   // = ts of the speculation
             c->spec_dt = dt;
         }
         c->hist = std::min(c->hist + nsteps, 2);

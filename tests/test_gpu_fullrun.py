@@ -1,19 +1,32 @@
-"""Full-run parity at the stand scale (BASELINE.json configs[2]: 1.28 M DoF, 3600 steps;
-configs[3]: 10 M DoF, 200 steps) and for the batch (configs[4]: 64 scenarios, 500 steps): the
-GPU temperatures after the configured run against the oracle's, stored by
-tools/make_golden_fullrun.py (which calls only oracle/) at a seeded sample of DoF (every
-interface node + 20k uniform) for configs 2-3 and as whole fields of sampled scenarios for
-config 4.  North-star bar: max-norm relative error <= 1e-9 after the full run."""
+"""Full-run parity of the PRODUCT path against a start-agnostic oracle, on every stored DoF.
+
+References (tests/golden/fullrun_<cfg>.npz, written by tools/make_golden_fullrun.py, which
+calls only oracle/): the implicit-Euler solution after the configured
+run of BASELINE.json configs[1..4], with the oracle's textbook Jacobi-PCG started at x0 = T^n
+and driven to a relative residual of 1e-14 (true residual checked at every step's exit), so
+the reference does not depend on any CG start and its own solver error is negligible.
+
+The GPU side runs the library's defaults (quadratic-extrapolation CG start, rtol 1e-12 --
+the configuration bench.py times), plus the x0 = T^n start as a second mode.  North-star
+bar: max-norm relative error <= 1e-9 after the full run (reading R18), over
+  cfg1, cfg2   every DoF
+  cfg3         1.3 M stored DoF (every boundary node, every interface-adjacent node, a seeded
+               uniform sample) and the whole-field max / min / sum
+  cfg4         every DoF of all 64 scenarios.
+The stored values are rounded to 2^-36 (<= 7.3e-12 absolute, tests/golden_codec.py)."""
 import json
 import os
 
 import numpy as np
 import pytest
 
+import golden_codec as G
 from paper_1707_03581_b200 import inputs as I
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+TOL = 1e-9
+MODES = {"default": None, "x0_Tn": 0}
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -22,49 +35,59 @@ def _built():
     g.build()
 
 
-def _golden(name, guess):
-    path = os.path.join(GOLDEN, f"fullrun_{name}{'_g%d' % guess if guess else ''}.npz")
+def _golden(name):
+    path = os.path.join(GOLDEN, f"fullrun_{name}.npz")
     if not os.path.exists(path):
-        pytest.skip(f"{path} not generated (GUESS={guess} tools/make_golden_fullrun.py {name})")
-    return np.load(path)
+        pytest.skip(f"{path} not generated (tools/make_golden_fullrun.py {name})")
+    g = np.load(path)
+    return g, json.loads(str(g["meta"]))
 
 
-# guess: the CG start on both sides (0: x0 = T^n; 2: quadratic extrapolation, the CUDA path's
-# default).  Both sides stop at the same relative residual 1e-12; over thousands of steps the
-# solver-tolerance errors accumulate to ~1e-9 of the field unless both sides take the same
-# iterations from the same start, so each GPU mode is compared with the oracle run of that mode.
-@pytest.mark.parametrize("guess", [0, 2])
-@pytest.mark.parametrize("name", ["cfg2", "cfg3"])
-def test_full_run_vs_oracle_samples(name, guess):
+def _run(cfg, mode, nsteps):
     from paper_1707_03581_b200.thermo import Thermo
-    g = _golden(name, guess)
-    meta = json.loads(str(g["meta"]))
+    th = Thermo.from_config(cfg)
+    if MODES[mode] is not None:
+        th.set_guess(MODES[mode])
+    th.step(0.0, cfg.dt, nsteps)
+    return th
+
+
+@pytest.mark.parametrize("mode", list(MODES))
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3"])
+def test_full_run_vs_start_agnostic_oracle(name, mode):
+    g, meta = _golden(name)
     cfg = I.make_config(name)
-    assert meta["n_dof"] == cfg.n_dof and meta["dt"] == cfg.dt
-    th = Thermo.from_config(cfg)
-    th.set_guess(guess)
-    th.step(meta["t0"], cfg.dt, meta["nsteps"])
+    assert meta["n_dof"] == cfg.n_dof and meta["dt"] == cfg.dt and meta["t0"] == 0.0
+    assert "x0 = T^n" in meta["solver"] and meta["max_true_rel_residual"] <= 1e-13
+    th = _run(cfg, mode, meta["nsteps"])
     T = th.get_T()
-    ref = g["values"]
-    err = np.abs(T[g["rows"]] - ref).max() / np.abs(ref).max()
-    assert err <= 1e-9, err
-    # whole-field properties the oracle recorded (range and sum)
-    assert abs(T.max() - meta["T_max"]) <= 1e-9 * abs(meta["T_max"])
-    assert abs(T.min() - meta["T_min"]) <= 1e-9 * abs(meta["T_max"])
-    assert abs(T.sum() - meta["T_sum"]) <= 1e-9 * abs(meta["T_sum"])
-
-
-@pytest.mark.parametrize("guess", [0, 2])
-def test_cfg4_full_run_vs_oracle_scenarios(guess):
-    from paper_1707_03581_b200.thermo import Thermo
-    g = _golden("cfg4", guess)
-    meta = json.loads(str(g["meta"]))
-    cfg = I.make_config("cfg4")
-    assert meta["n_dof"] == cfg.n_dof and meta["n_scen"] == cfg.n_scen
-    th = Thermo.from_config(cfg)
-    th.set_guess(guess)
-    th.step(meta["t0"], cfg.dt, meta["nsteps"])
-    for k, ref in zip(g["scen"], g["values"]):
-        T = th.get_T(scen=int(k))
+    if "field" in g.files:
+        ref = G.unpack_field(g["field"], cfg.n_dof)
         err = np.abs(T - ref).max() / np.abs(ref).max()
-        assert err <= 1e-9, (int(k), err)
+    else:
+        rows = G.unpack_rows(g["rows"], meta["n_rows"])
+        ref = G.unpack_field(g["values"], meta["n_rows"])
+        err = np.abs(T[rows] - ref).max() / np.abs(ref).max()
+        # whole-field properties the oracle recorded (range and sum)
+        assert abs(T.max() - meta["T_max"]) <= TOL * abs(meta["T_max"])
+        assert abs(T.min() - meta["T_min"]) <= TOL * abs(meta["T_max"])
+        assert abs(T.sum() - meta["T_sum"]) <= TOL * abs(meta["T_sum"])
+    print(f"{name} {mode}: max-norm rel err {err:.3e} over the stored DoF")
+    assert err <= TOL, err
+
+
+@pytest.mark.parametrize("mode", list(MODES))
+def test_cfg4_full_run_every_scenario(mode):
+    g, meta = _golden("cfg4")
+    cfg = I.make_config("cfg4")
+    S = cfg.n_scen
+    assert meta["n_dof"] == cfg.n_dof and meta["n_scen"] == S
+    ref = G.unpack_field(g["field"], S * cfg.n_dof).reshape(S, cfg.n_dof)
+    th = _run(cfg, mode, meta["nsteps"])
+    worst = 0.0
+    for k in range(S):
+        T = th.get_T(scen=k)
+        err = np.abs(T - ref[k]).max() / np.abs(ref[k]).max()
+        worst = max(worst, err)
+        assert err <= TOL, (k, err)
+    print(f"cfg4 {mode}: worst scenario max-norm rel err {worst:.3e}")

@@ -184,16 +184,6 @@ def test_noconv_reports_and_keeps_state():
     assert np.array_equal(th.get_T(), T2)
 
 
-@pytest.mark.slow
-def test_cfg1_full_run():
-    """BASELINE config 1: 85,694 DoF, 1000 steps of 0.5 s, eta(t) varying."""
-    cfg = I.make_config("cfg1")
-    th = _thermo(cfg)
-    th.step(0.0, cfg.dt, cfg.nsteps)
-    Tg = th.get_T()
-    Tr, st = O.run_config(cfg)
-    assert rel(Tg, Tr) <= TOL
-
 
 @pytest.mark.parametrize("pair", [(2, 8), (4, 9), (7, 10)])
 @pytest.mark.parametrize("name", ["small", "medium"])
@@ -255,6 +245,26 @@ def test_interface_overlap_mode(monkeypatch, name):
     Ts, _ = o.stationary(Tc, 0.0, cfg.scenarios[0], with_interface=True)
     Td, _ = o.step(Ts, 0.0, cfg.dt, 2, cfg.scenarios[0])
     assert rel(d.get_T(), Td) <= TOL
+
+
+def test_speculated_interface_equals_fresh_assembly(monkeypatch):
+    """One step per call in overlap mode uses the interface the previous call assembled
+    speculatively for t + nsteps dt.  Its step time must be the expression the next call
+    evaluates (ts + 1 dt), so the speculation is bitwise the fresh assembly -- checked with a
+    step size that is not a power of two (dt = 0.3: t + 2 dt != (t + dt) + dt in the last bits)."""
+    cfg = I.make_config("cfg0")
+    dt = 0.3
+    out = []
+    for spec in ("1", "0"):
+        monkeypatch.setenv("THERMO_OVERLAP", "1")
+        monkeypatch.setenv("THERMO_SPEC", spec)
+        th = _thermo(cfg)
+        t = 0.0
+        for n in range(40):
+            th.step(t, dt, 1)
+            t = t + dt
+        out.append(th.get_T())
+    assert np.array_equal(out[0], out[1])
 
 
 @pytest.mark.parametrize("stages", [3, 5])
