@@ -217,6 +217,17 @@ typedef struct {
     int32_t solve_block;             /* threads per CTA */
     int32_t launches_per_step;       /* kernels per implicit-Euler step of the last call (interface,
                                         guess extrapolation, solve) */
+    int32_t reordered;               /* 1: nodes renumbered internally at create (reverse
+                                        Cuthill-McKee per part, because the caller's numbering
+                                        failed the solve kernel's window test); the ABI keeps
+                                        the caller's numbering either way */
+    int32_t order_max_runs;          /* window test of the caller's numbering at create: max
+                                        contiguous column runs of a 256-row chunk (0: not probed) */
+    int32_t order_max_window;        /*   ... and max window entries of a chunk */
+    int32_t solve_variant;           /* CG kernel variant chosen at create (S = 1): kind 2 =
+                                        windowed TMA sweep */
+    int32_t solve_kind;
+    int32_t reserved_;
 } thermo_stats;
 
 int thermo_get_stats(const void *ctx, thermo_stats *out);

@@ -1029,6 +1029,13 @@ __global__ void __launch_bounds__(256) k_chunk_windows(const int64_t *slice_ptr,
     }
 }
 
+void chunk_windows_launch(Ctx &c, int W, int gap, int2 *runs, int32_t *nruns, int32_t *lown, uint16_t *lcol,
+                          int *d_stats) {
+    const int64_t nchunks = (c.nslices + W - 1) / W;
+    k_chunk_windows<<<(unsigned)nchunks, 256, 0, c.stream>>>(c.d_slice_ptr, c.d_col, c.nslices, W, gap, runs, nruns,
+                                                            lown, lcol, d_stats);
+}
+
 struct Variant {
     int kind, W, NG;
     bool fused;   // one grid barrier per iteration (KIND 2 only)
@@ -1150,6 +1157,7 @@ int cg_setup(Ctx &c) {
                 kVariants[chosen].NG, c.cg_stage_entries, c.cg_win_cap,
                 stage_bytes(kVariants[chosen], c.cg_stage_entries, c.cg_win_cap), c.cg_nstages, c.cg_smem);
     c.cg_variant = chosen;
+    c.cg_kind = kVariants[chosen].kind;
     const char *dbg = getenv("THERMO_CG_DEBUG");
     c.cg_debug = dbg ? atoi(dbg) : 0;
     const char *pfe = getenv("THERMO_CG_PREFETCH");

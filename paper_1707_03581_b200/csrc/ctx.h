@@ -95,7 +95,7 @@ struct Ctx {
     int cg_grid = 0, cg_block = 0, cg_stage_entries = 0;
     size_t cg_smem = 0;
     bool cg_tma = false;
-    int cg_variant = 0, cg_chunk = 8, cg_debug = 0, cg_prefetch = 0;
+    int cg_variant = 0, cg_kind = -1, cg_chunk = 8, cg_debug = 0, cg_prefetch = 0;
     bool cg_fused = false;           // one-barrier-per-iteration kernel (second z / q' set below)
     double *d_z2 = nullptr, *d_q2 = nullptr;
     int32_t *d_chunk_hi = nullptr;
@@ -166,6 +166,16 @@ struct Ctx {
     int32_t *d_pcnt_s = nullptr;
     double ms_iface = 0.0, ms_solve = 0.0;
 
+    // internal numbering (reorder.cu): nullptr / empty = the caller's numbering
+    int32_t *d_int_of_ext = nullptr;      // [N] internal index of the caller's node e
+    std::vector<int32_t> h_ext_of_int;    // [N] the caller's index of internal node i
+    int reorder = 0;                      // 0 caller's numbering kept, 1 RCM
+    int probe_runs = 0, probe_window = 0; // window test of the caller's numbering (create)
+    // staging of the host transfers: one contiguous field per scenario for state buffer b,
+    // valid while stage_ver[b] == ver[b] (ver[b] counts the writes of d_T[b], see guard_write)
+    double *d_stage[2] = {nullptr, nullptr};
+    int64_t ver[2] = {0, 0}, stage_ver[2] = {-1, -1};
+
     // stats of the last thermo_step
     int last_nsteps = 0;
     int64_t last_launches = 0;       // kernels launched by the last implicit-Euler thermo_step
@@ -190,6 +200,10 @@ int iface_launch(Ctx &c, const IfaceParams &p, cudaStream_t stream = nullptr);
 
 // cg.cu
 int cg_setup(Ctx &c);
+// chunk windows of the current pattern (W slices per chunk, runs merged below `gap`);
+// stats: [0] max window entries, [1] max runs, [2] flags (too many entries / window too wide)
+void chunk_windows_launch(Ctx &c, int W, int gap, int2 *runs, int32_t *nruns, int32_t *lown, uint16_t *lcol,
+                          int *d_stats);
 // x0: initial guess (extrapolated state, see thermo.cu), nullptr = the committed state T^n
 int cg_launch_step(Ctx &c, int step, double dt, const double *x0 = nullptr, int buf = 0, bool ovl = false);
 int overlap_setup(Ctx &c);   // second interface buffer set, side stream, reduced CG grid
@@ -208,5 +222,12 @@ int sdc_step(Ctx &c, double tn, double dt, int step_index);   // single-rate SDC
 int cgb_setup(Ctx &c);
 int cgb_prepare(Ctx &c);   // broadcast the volume D^{-1} into DinvS (after build_operator)
 int cgb_launch_step(Ctx &c, int step, double dt, const double *x0 = nullptr);
+
+// reorder.cu (internal numbering, state transfers in the caller's numbering)
+int order_probe(Ctx &c, bool *good, int *max_runs, int *max_window);
+int rcm_order(Ctx &c, std::vector<int32_t> &new_to_old);
+int gather_T(Ctx &c, int scen, int64_t off, int64_t cnt, const double *T, double *out, cudaStream_t st);
+int scatter_T(Ctx &c, int scen, int64_t off, int64_t cnt, double *T, const double *in, cudaStream_t st);
+int gather_all(Ctx &c, const double *T, double *out, cudaStream_t st);
 
 }  // namespace thermo

@@ -42,6 +42,7 @@ static int fail(Ctx *c, int code, const std::string &msg) {
 // Before work on the context stream overwrites state buffer b: wait for an asynchronous host
 // copy still reading it (thermo_get_T_async).
 static cudaError_t guard_write(Ctx *c, int b) {
+    ++c->ver[b];   // staged host-transfer copies of buffer b are stale from here on
     if (!c->copy_pending[b]) return cudaSuccess;
     c->copy_pending[b] = 0;
     return cudaStreamWaitEvent(c->stream, c->ev_copy[b], 0);
@@ -75,7 +76,7 @@ static void free_ctx(Ctx *c) {
                     c->d_ell_cnt_s, c->d_ell_col_s, c->d_ell_val_s, c->d_if_b_s, c->d_if_phi_s, c->d_rhs,
                     c->d_pairs_s, c->d_pcnt_s, c->d_star_own, c->d_own_ptr, c->d_own_idx, c->d_x0, c->d_Thist, c->d_z2, c->d_q2,
                     c->d_ell_cnt_b, c->d_ell_col_b, c->d_ell_val_b, c->d_if_b_b, c->d_if_phi_b, c->d_Dinv_b,
-                    c->d_step_sc_spec, c->d_spec_status};
+                    c->d_step_sc_spec, c->d_spec_status, c->d_int_of_ext, c->d_stage[0], c->d_stage[1]};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     for (cudaEvent_t e : c->events) cudaEventDestroy(e);
@@ -105,6 +106,70 @@ __global__ void k_fill_value(double *p, int64_t n, double v) {
     if (i < n) p[i] = v;
 }
 
+// Coupled host arrays of the two meshes in the caller's numbering (fixed part first).
+struct HostMesh {
+    int64_t nf = 0, nm = 0, ntets = 0, nfaces = 0;
+    std::vector<double> xyz;
+    std::vector<int32_t> tets, faces, fkey, fA, fB;
+};
+
+static int host_mesh(HostMesh &h, const thermo_mesh *fixed, const thermo_mesh *moving, int32_t iface_tag_fixed,
+                     int32_t iface_tag_moving) {
+    h.nf = fixed->n_nodes;
+    h.nm = moving->n_nodes;
+    const int64_t N = h.nf + h.nm;
+    if (N >= (1LL << 31)) { g_create_err = "too many nodes"; return THERMO_EINVAL; }
+    h.ntets = fixed->n_tets + moving->n_tets;
+    h.nfaces = fixed->n_bfaces + moving->n_bfaces;
+    h.xyz.resize(3 * N);
+    memcpy(h.xyz.data(), fixed->xyz, sizeof(double) * 3 * h.nf);
+    memcpy(h.xyz.data() + 3 * h.nf, moving->xyz, sizeof(double) * 3 * h.nm);
+    h.tets.resize(4 * h.ntets);
+    for (int64_t e = 0; e < 4 * fixed->n_tets; ++e) {
+        if (fixed->tets[e] < 0 || fixed->tets[e] >= h.nf) { g_create_err = "fixed tet index out of range"; return THERMO_EINVAL; }
+        h.tets[e] = fixed->tets[e];
+    }
+    for (int64_t e = 0; e < 4 * moving->n_tets; ++e) {
+        if (moving->tets[e] < 0 || moving->tets[e] >= h.nm) { g_create_err = "moving tet index out of range"; return THERMO_EINVAL; }
+        h.tets[4 * fixed->n_tets + e] = (int32_t)(moving->tets[e] + h.nf);
+    }
+    h.faces.resize(3 * h.nfaces);
+    h.fkey.resize(h.nfaces);
+    for (int64_t f = 0; f < fixed->n_bfaces; ++f) {
+        for (int a = 0; a < 3; ++a) {
+            int32_t v = fixed->bfaces[3 * f + a];
+            if (v < 0 || v >= h.nf) { g_create_err = "fixed face index out of range"; return THERMO_EINVAL; }
+            h.faces[3 * f + a] = v;
+        }
+        h.fkey[f] = fixed->bface_tag[f];
+        if (fixed->bface_tag[f] == iface_tag_fixed) h.fA.insert(h.fA.end(), &h.faces[3 * f], &h.faces[3 * f] + 3);
+    }
+    for (int64_t f = 0; f < moving->n_bfaces; ++f) {
+        int64_t g = fixed->n_bfaces + f;
+        for (int a = 0; a < 3; ++a) {
+            int32_t v = moving->bfaces[3 * f + a];
+            if (v < 0 || v >= h.nm) { g_create_err = "moving face index out of range"; return THERMO_EINVAL; }
+            h.faces[3 * g + a] = (int32_t)(v + h.nf);
+        }
+        h.fkey[g] = 65536 + moving->bface_tag[f];
+        if (moving->bface_tag[f] == iface_tag_moving) h.fB.insert(h.fB.end(), &h.faces[3 * g], &h.faces[3 * g] + 3);
+    }
+    return THERMO_OK;
+}
+
+// Renumber the host arrays: internal node i is the caller's node new_to_old[i].
+static void permute_host_mesh(HostMesh &h, const std::vector<int32_t> &new_to_old, std::vector<int32_t> &old_to_new) {
+    const int64_t N = h.nf + h.nm;
+    old_to_new.assign(N, 0);
+    for (int64_t i = 0; i < N; ++i) old_to_new[new_to_old[i]] = (int32_t)i;
+    std::vector<double> x(3 * N);
+    for (int64_t i = 0; i < N; ++i)
+        for (int d = 0; d < 3; ++d) x[3 * i + d] = h.xyz[3 * (int64_t)new_to_old[i] + d];
+    h.xyz.swap(x);
+    for (auto *v : {&h.tets, &h.faces, &h.fA, &h.fB})
+        for (int32_t &e : *v) e = old_to_new[e];
+}
+
 extern "C" int thermo_create_mesh(void **out, const thermo_mesh *fixed, const thermo_mesh *moving,
                                   int32_t iface_tag_fixed, int32_t iface_tag_moving, double nu,
                                   double rho_cp, double alpha_iface, int32_t n_scen,
@@ -116,118 +181,125 @@ extern "C" int thermo_create_mesh(void **out, const thermo_mesh *fixed, const th
         g_create_err = "invalid material parameters or scenarios";
         return THERMO_EINVAL;
     }
-    Ctx *c = new (std::nothrow) Ctx();
-    if (!c) { g_create_err = "host allocation failed"; return THERMO_ENOMEM; }
+    for (int s = 0; s < n_scen; ++s)
+        if (!(scen[s].period != 0.0) || !(scen[s].eta_period != 0.0) || !std::isfinite(scen[s].s0) ||
+            !std::isfinite(scen[s].amp)) {
+            g_create_err = "invalid scenario (zero period or non-finite values)";
+            return THERMO_EINVAL;
+        }
+    // THERMO_REORDER (tuning / test hook): unset = renumber only if the caller's numbering fails
+    // the window test, 0 = never, 1 = always (reverse Cuthill-McKee)
+    const char *ro = getenv("THERMO_REORDER");
+    const int reorder_mode = ro ? atoi(ro) : -1;
+    HostMesh hm;
+    std::vector<int32_t> new_to_old, old_to_new;
+    int probe_runs = 0, probe_window = 0;
     try {
-        c->stream = (cudaStream_t)cuda_stream;
-        if (cudaGetDevice(&c->dev) != cudaSuccess ||
-            cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->dev) != cudaSuccess) {
-            g_create_err = "no CUDA device";
-            free_ctx(c);
-            return THERMO_ECUDA;
-        }
-        int coop = 0;
-        cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, c->dev);
-        if (!coop) { g_create_err = "device lacks cooperative launch"; free_ctx(c); return THERMO_ECUDA; }
-        c->nf = fixed->n_nodes;
-        c->nm = moving->n_nodes;
-        c->N = c->nf + c->nm;
-        if (c->N >= (1LL << 31)) { g_create_err = "too many nodes"; free_ctx(c); return THERMO_EINVAL; }
-        c->S = n_scen;
-        c->SP = n_scen == 1 ? 1 : (n_scen + 1) & ~1;
-        c->nu = nu;
-        c->rho_cp = rho_cp;
-        c->alpha = alpha_iface;
-        c->iface_tag_f = iface_tag_fixed;
-        c->iface_tag_m = iface_tag_moving;
-        for (int s = 0; s < n_scen; ++s) {
-            thermo::Scen q;
-            q.s0 = scen[s].s0; q.amp = scen[s].amp; q.period = scen[s].period;
-            for (int d = 0; d < 3; ++d) q.dir[d] = scen[s].dir[d];
-            q.eta0 = scen[s].eta0; q.eta_amp = scen[s].eta_amp; q.eta_period = scen[s].eta_period;
-            q.d2[0] = q.d2[1] = 0.0;
-            if (!(q.period != 0.0) || !(q.eta_period != 0.0) || !std::isfinite(q.s0) || !std::isfinite(q.amp)) {
-                g_create_err = "invalid scenario (zero period or non-finite values)";
-                free_ctx(c);
-                return THERMO_EINVAL;
-            }
-            c->scen.push_back(q);
-        }
-        // coupled host arrays: fixed part first
-        const int64_t N = c->N;
-        c->ntets = fixed->n_tets + moving->n_tets;
-        c->nfaces = fixed->n_bfaces + moving->n_bfaces;
-        std::vector<double> xyz(3 * N);
-        memcpy(xyz.data(), fixed->xyz, sizeof(double) * 3 * c->nf);
-        memcpy(xyz.data() + 3 * c->nf, moving->xyz, sizeof(double) * 3 * c->nm);
-        std::vector<int32_t> tets(4 * c->ntets);
-        for (int64_t e = 0; e < 4 * fixed->n_tets; ++e) {
-            if (fixed->tets[e] < 0 || fixed->tets[e] >= c->nf) { g_create_err = "fixed tet index out of range"; free_ctx(c); return THERMO_EINVAL; }
-            tets[e] = fixed->tets[e];
-        }
-        for (int64_t e = 0; e < 4 * moving->n_tets; ++e) {
-            if (moving->tets[e] < 0 || moving->tets[e] >= c->nm) { g_create_err = "moving tet index out of range"; free_ctx(c); return THERMO_EINVAL; }
-            tets[4 * fixed->n_tets + e] = (int32_t)(moving->tets[e] + c->nf);
-        }
-        std::vector<int32_t> faces(3 * c->nfaces), fkey(c->nfaces);
-        std::vector<int32_t> fA, fB;
-        for (int64_t f = 0; f < fixed->n_bfaces; ++f) {
-            for (int a = 0; a < 3; ++a) {
-                int32_t v = fixed->bfaces[3 * f + a];
-                if (v < 0 || v >= c->nf) { g_create_err = "fixed face index out of range"; free_ctx(c); return THERMO_EINVAL; }
-                faces[3 * f + a] = v;
-            }
-            fkey[f] = fixed->bface_tag[f];
-            if (fixed->bface_tag[f] == iface_tag_fixed) fA.insert(fA.end(), &faces[3 * f], &faces[3 * f] + 3);
-        }
-        for (int64_t f = 0; f < moving->n_bfaces; ++f) {
-            int64_t g = fixed->n_bfaces + f;
-            for (int a = 0; a < 3; ++a) {
-                int32_t v = moving->bfaces[3 * f + a];
-                if (v < 0 || v >= c->nm) { g_create_err = "moving face index out of range"; free_ctx(c); return THERMO_EINVAL; }
-                faces[3 * g + a] = (int32_t)(v + c->nf);
-            }
-            fkey[g] = 65536 + moving->bface_tag[f];
-            if (moving->bface_tag[f] == iface_tag_moving) fB.insert(fB.end(), &faces[3 * g], &faces[3 * g] + 3);
-        }
-        int rc = thermo::assemble_create(*c, xyz.data(), tets.data(), faces.data(), fkey.data());
-        if (!rc) rc = thermo::iface_setup(*c, xyz.data(), fA, fB);
-        if (rc) {
-            g_create_err = c->err;
-            free_ctx(c);
-            return rc == -1 ? THERMO_EINVAL : (rc == -5 ? THERMO_EGEOM : THERMO_ECUDA);
-        }
-        // state and workspace (N x SP row-major blocks)
-        const int64_t NS = N * c->SP;
-        bool ok = true;
-        // vectors padded by 16 entries: window bulk copies may read up to one element past N
-        for (double **p : {&c->d_T[0], &c->d_T[1], &c->d_z, &c->d_p[0], &c->d_p[1], &c->d_q}) {
-            ok &= cudaMalloc(p, sizeof(double) * (NS + 16)) == cudaSuccess;
-            if (ok) cudaMemsetAsync(*p, 0, sizeof(double) * (NS + 16), c->stream);
-        }
-        ok &= cudaMalloc(&c->d_status, sizeof(int) * 8) == cudaSuccess;
-        ok &= cudaMalloc(&c->d_fail_relres, sizeof(double)) == cudaSuccess;
-        if (!ok) { g_create_err = "device allocation failed"; free_ctx(c); return THERMO_ENOMEM; }
-        k_fill_value<<<(unsigned)((NS + 255) / 256), 256, 0, c->stream>>>(c->d_T[0], NS, T_init);
-        cudaMemsetAsync(c->d_p[0], 0, sizeof(double) * NS, c->stream);
-        cudaMemsetAsync(c->d_p[1], 0, sizeof(double) * NS, c->stream);
-        cudaMemsetAsync(c->d_status, 0, sizeof(int) * 8, c->stream);
-        rc = thermo::assemble_robin(*c);
-        if (!rc) rc = c->S == 1 ? thermo::cg_setup(*c) : thermo::cgb_setup(*c);
-        if (!rc) rc = thermo::overlap_setup(*c);
-        if (!rc && getenv("THERMO_CG_TRACE")) {
-            if (cudaMalloc(&c->d_trace, sizeof(unsigned long long) * 1024) != cudaSuccess) rc = -3;
-            else cudaMemsetAsync(c->d_trace, 0, sizeof(unsigned long long) * 1024, c->stream);
-        }
-        if (!rc && cudaStreamSynchronize(c->stream) != cudaSuccess) { c->err = "CUDA error during create"; rc = -3; }
-        if (rc) { g_create_err = c->err; free_ctx(c); return THERMO_ECUDA; }
-        *out = c;
-        return THERMO_OK;
+        if (int rc = host_mesh(hm, fixed, moving, iface_tag_fixed, iface_tag_moving)) return rc;
     } catch (const std::exception &e) {
         g_create_err = std::string("exception: ") + e.what();
-        free_ctx(c);
         return THERMO_ENOMEM;
     }
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        Ctx *c = new (std::nothrow) Ctx();
+        if (!c) { g_create_err = "host allocation failed"; return THERMO_ENOMEM; }
+        try {
+            c->stream = (cudaStream_t)cuda_stream;
+            if (cudaGetDevice(&c->dev) != cudaSuccess ||
+                cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->dev) != cudaSuccess) {
+                g_create_err = "no CUDA device";
+                free_ctx(c);
+                return THERMO_ECUDA;
+            }
+            int coop = 0;
+            cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, c->dev);
+            if (!coop) { g_create_err = "device lacks cooperative launch"; free_ctx(c); return THERMO_ECUDA; }
+            c->nf = hm.nf;
+            c->nm = hm.nm;
+            c->N = c->nf + c->nm;
+            c->S = n_scen;
+            c->SP = n_scen == 1 ? 1 : (n_scen + 1) & ~1;
+            c->nu = nu;
+            c->rho_cp = rho_cp;
+            c->alpha = alpha_iface;
+            c->iface_tag_f = iface_tag_fixed;
+            c->iface_tag_m = iface_tag_moving;
+            for (int s = 0; s < n_scen; ++s) {
+                thermo::Scen q;
+                q.s0 = scen[s].s0; q.amp = scen[s].amp; q.period = scen[s].period;
+                for (int d = 0; d < 3; ++d) q.dir[d] = scen[s].dir[d];
+                q.eta0 = scen[s].eta0; q.eta_amp = scen[s].eta_amp; q.eta_period = scen[s].eta_period;
+                q.d2[0] = q.d2[1] = 0.0;
+                c->scen.push_back(q);
+            }
+            const int64_t N = c->N;
+            c->ntets = hm.ntets;
+            c->nfaces = hm.nfaces;
+            c->probe_runs = probe_runs;
+            c->probe_window = probe_window;
+            int rc = thermo::assemble_create(*c, hm.xyz.data(), hm.tets.data(), hm.faces.data(), hm.fkey.data());
+            if (!rc && attempt == 0 && reorder_mode != 0) {
+                // window test of the caller's numbering; renumber (RCM) and start over if it fails
+                bool good = true;
+                rc = thermo::order_probe(*c, &good, &probe_runs, &probe_window);
+                c->probe_runs = probe_runs;
+                c->probe_window = probe_window;
+                if (!rc && (!good || reorder_mode == 1)) {
+                    rc = thermo::rcm_order(*c, new_to_old);
+                    if (!rc) {
+                        free_ctx(c);
+                        permute_host_mesh(hm, new_to_old, old_to_new);
+                        continue;
+                    }
+                }
+            }
+            if (!rc) rc = thermo::iface_setup(*c, hm.xyz.data(), hm.fA, hm.fB);
+            if (rc) {
+                g_create_err = c->err;
+                free_ctx(c);
+                return rc == -1 ? THERMO_EINVAL : (rc == -5 ? THERMO_EGEOM : THERMO_ECUDA);
+            }
+            // state and workspace (N x SP row-major blocks)
+            const int64_t NS = N * c->SP;
+            bool ok = true;
+            if (!new_to_old.empty()) {   // the caller's numbering is kept at the ABI
+                c->reorder = 1;
+                c->h_ext_of_int = new_to_old;
+                ok &= cudaMalloc(&c->d_int_of_ext, sizeof(int32_t) * N) == cudaSuccess;
+                if (ok) ok &= cudaMemcpy(c->d_int_of_ext, old_to_new.data(), sizeof(int32_t) * N,
+                                         cudaMemcpyHostToDevice) == cudaSuccess;
+            }
+            // vectors padded by 16 entries: window bulk copies may read up to one element past N
+            for (double **p : {&c->d_T[0], &c->d_T[1], &c->d_z, &c->d_p[0], &c->d_p[1], &c->d_q}) {
+                ok &= cudaMalloc(p, sizeof(double) * (NS + 16)) == cudaSuccess;
+                if (ok) cudaMemsetAsync(*p, 0, sizeof(double) * (NS + 16), c->stream);
+            }
+            ok &= cudaMalloc(&c->d_status, sizeof(int) * 8) == cudaSuccess;
+            ok &= cudaMalloc(&c->d_fail_relres, sizeof(double)) == cudaSuccess;
+            if (!ok) { g_create_err = "device allocation failed"; free_ctx(c); return THERMO_ENOMEM; }
+            k_fill_value<<<(unsigned)((NS + 255) / 256), 256, 0, c->stream>>>(c->d_T[0], NS, T_init);
+            cudaMemsetAsync(c->d_p[0], 0, sizeof(double) * NS, c->stream);
+            cudaMemsetAsync(c->d_p[1], 0, sizeof(double) * NS, c->stream);
+            cudaMemsetAsync(c->d_status, 0, sizeof(int) * 8, c->stream);
+            rc = thermo::assemble_robin(*c);
+            if (!rc) rc = c->S == 1 ? thermo::cg_setup(*c) : thermo::cgb_setup(*c);
+            if (!rc) rc = thermo::overlap_setup(*c);
+            if (!rc && getenv("THERMO_CG_TRACE")) {
+                if (cudaMalloc(&c->d_trace, sizeof(unsigned long long) * 1024) != cudaSuccess) rc = -3;
+                else cudaMemsetAsync(c->d_trace, 0, sizeof(unsigned long long) * 1024, c->stream);
+            }
+            if (!rc && cudaStreamSynchronize(c->stream) != cudaSuccess) { c->err = "CUDA error during create"; rc = -3; }
+            if (rc) { g_create_err = c->err; free_ctx(c); return THERMO_ECUDA; }
+            *out = c;
+            return THERMO_OK;
+        } catch (const std::exception &e) {
+            g_create_err = std::string("exception: ") + e.what();
+            free_ctx(c);
+            return THERMO_ENOMEM;
+        }
+    }
+    g_create_err = "internal: reordering loop";
+    return THERMO_ECUDA;
 }
 
 extern "C" int thermo_set_bc(void *ctx, int32_t part, int32_t tag, double alpha, double T_ref,
@@ -409,13 +481,14 @@ extern "C" int thermo_get_interface(void *ctx, int32_t scen, double t, double dt
         API_CK(cudaMemcpyAsync(status, c->d_status, sizeof status, cudaMemcpyDeviceToHost, c->stream));
         API_CK(cudaStreamSynchronize(c->stream));
         if (status[1]) return fail(c, THERMO_EGEOM, "interface row capacity exceeded");
+        const bool map = !c->h_ext_of_int.empty();   // back to the caller's numbering
         for (int k = 0; k < nif; ++k) {
-            rows[k] = h_rows[k];
+            rows[k] = map ? c->h_ext_of_int[h_rows[k]] : h_rows[k];
             cnt[k] = h_cnt[thermo::row_index(P, scen, k)];
             b[k] = h_b[thermo::row_index(P, scen, k)];
             for (int q = 0; q < cap; ++q) {
                 const int64_t e = thermo::ell_index(P, scen, q, k);
-                col[(int64_t)k * cap + q] = q < cnt[k] ? h_col[e] : -1;
+                col[(int64_t)k * cap + q] = q < cnt[k] ? (map ? c->h_ext_of_int[h_col[e]] : h_col[e]) : -1;
                 val[(int64_t)k * cap + q] = q < cnt[k] ? h_val[e] : 0.0;
             }
         }
@@ -777,17 +850,60 @@ static int selection(Ctx *c, int32_t scen, int32_t part, int64_t n, int64_t *off
     return THERMO_OK;
 }
 
+// The host transfers of state buffer b go through a staging copy in the caller's numbering
+// (one contiguous field per scenario), gathered on the copy stream once per version of the
+// buffer.  Not used when the state is already one contiguous field in the caller's numbering.
+static bool direct_layout(const Ctx *c) { return c->SP == 1 && !c->d_int_of_ext; }
+
+static int ensure_copy_stream(Ctx *c) {
+    if (c->copy_stream) return THERMO_OK;
+    API_CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    for (cudaEvent_t *e : {&c->ev_ready, &c->ev_copy[0], &c->ev_copy[1]})
+        API_CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    return THERMO_OK;
+}
+
+// Queue on the copy stream (after the work queued so far on the context stream): the staged
+// fields of buffer b if stale, then the copy of [off, off + cnt) of scenario scen to host_out.
+static int queue_host_copy(Ctx *c, int scen, int64_t off, int64_t cnt, double *host_out) {
+    if (int rc = ensure_copy_stream(c)) return rc;
+    const int b = c->cur;
+    API_CK(cudaEventRecord(c->ev_ready, c->stream));   // the state as of the work queued so far
+    API_CK(cudaStreamWaitEvent(c->copy_stream, c->ev_ready, 0));
+    if (direct_layout(c)) {
+        API_CK(cudaMemcpyAsync(host_out, c->d_T[b] + off, sizeof(double) * cnt, cudaMemcpyDeviceToHost,
+                               c->copy_stream));
+    } else {
+        if (!c->d_stage[b]) API_CK(cudaMalloc(&c->d_stage[b], sizeof(double) * (size_t)c->N * c->S));
+        if (c->stage_ver[b] != c->ver[b]) {
+            const int rc = c->S == 1 ? thermo::gather_T(*c, 0, 0, c->N, c->d_T[b], c->d_stage[b], c->copy_stream)
+                                     : thermo::gather_all(*c, c->d_T[b], c->d_stage[b], c->copy_stream);
+            if (rc) return THERMO_ECUDA;
+            c->stage_ver[b] = c->ver[b];
+        }
+        API_CK(cudaMemcpyAsync(host_out, c->d_stage[b] + (int64_t)scen * c->N + off, sizeof(double) * cnt,
+                               cudaMemcpyDeviceToHost, c->copy_stream));
+    }
+    API_CK(cudaEventRecord(c->ev_copy[b], c->copy_stream));
+    c->copy_pending[b] = 1;
+    return THERMO_OK;
+}
+
 extern "C" int thermo_get_T(void *ctx, int32_t scen, int32_t part, double *out, int64_t n,
                             int32_t out_on_device) {
     Ctx *c = (Ctx *)ctx;
     if (!c || !out) return c ? fail(c, THERMO_EINVAL, "out is NULL") : THERMO_EINVAL;
     int64_t off, cnt;
     if (int rc = selection(c, scen, part, n, &off, &cnt)) return rc;
-    const double *src = c->d_T[c->cur] + off * c->SP + scen;
-    cudaMemcpyKind kind = out_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
-    if (c->SP == 1) API_CK(cudaMemcpyAsync(out, src, sizeof(double) * cnt, kind, c->stream));
-    else API_CK(cudaMemcpy2DAsync(out, sizeof(double), src, sizeof(double) * c->SP, sizeof(double), cnt, kind, c->stream));
-    if (!out_on_device) API_CK(cudaStreamSynchronize(c->stream));
+    if (out_on_device) {   // async on the context stream
+        if (direct_layout(c))
+            API_CK(cudaMemcpyAsync(out, c->d_T[c->cur] + off, sizeof(double) * cnt, cudaMemcpyDeviceToDevice, c->stream));
+        else if (thermo::gather_T(*c, scen, off, cnt, c->d_T[c->cur], out, c->stream))
+            return fail(c, THERMO_ECUDA, c->err);
+        return THERMO_OK;
+    }
+    if (int rc = queue_host_copy(c, scen, off, cnt, out)) return rc;
+    API_CK(cudaStreamSynchronize(c->copy_stream));
     return THERMO_OK;
 }
 
@@ -796,23 +912,7 @@ extern "C" int thermo_get_T_async(void *ctx, int32_t scen, int32_t part, double 
     if (!c || !host_out) return c ? fail(c, THERMO_EINVAL, "host_out is NULL") : THERMO_EINVAL;
     int64_t off, cnt;
     if (int rc = selection(c, scen, part, n, &off, &cnt)) return rc;
-    if (!c->copy_stream) {
-        API_CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
-        for (cudaEvent_t *e : {&c->ev_ready, &c->ev_copy[0], &c->ev_copy[1]})
-            API_CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
-    }
-    const int b = c->cur;
-    const double *src = c->d_T[b] + off * c->SP + scen;
-    API_CK(cudaEventRecord(c->ev_ready, c->stream));   // the state as of the work queued so far
-    API_CK(cudaStreamWaitEvent(c->copy_stream, c->ev_ready, 0));
-    if (c->SP == 1)
-        API_CK(cudaMemcpyAsync(host_out, src, sizeof(double) * cnt, cudaMemcpyDeviceToHost, c->copy_stream));
-    else
-        API_CK(cudaMemcpy2DAsync(host_out, sizeof(double), src, sizeof(double) * c->SP, sizeof(double), cnt,
-                                 cudaMemcpyDeviceToHost, c->copy_stream));
-    API_CK(cudaEventRecord(c->ev_copy[b], c->copy_stream));
-    c->copy_pending[b] = 1;
-    return THERMO_OK;
+    return queue_host_copy(c, scen, off, cnt, host_out);
 }
 
 extern "C" int thermo_sync(void *ctx) {
@@ -832,12 +932,21 @@ extern "C" int thermo_set_T(void *ctx, int32_t scen, int32_t part, const double 
     if (!c || !in) return c ? fail(c, THERMO_EINVAL, "in is NULL") : THERMO_EINVAL;
     int64_t off, cnt;
     if (int rc = selection(c, scen, part, n, &off, &cnt)) return rc;
-    double *dst = c->d_T[c->cur] + off * c->SP + scen;
+    double *T = c->d_T[c->cur];
     API_CK(guard_write(c, c->cur));
     c->hist = 0;   // the extrapolation history no longer leads to this state
     cudaMemcpyKind kind = in_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-    if (c->SP == 1) API_CK(cudaMemcpyAsync(dst, in, sizeof(double) * cnt, kind, c->stream));
-    else API_CK(cudaMemcpy2DAsync(dst, sizeof(double) * c->SP, in, sizeof(double), sizeof(double), cnt, kind, c->stream));
+    if (direct_layout(c)) {
+        API_CK(cudaMemcpyAsync(T + off, in, sizeof(double) * cnt, kind, c->stream));
+    } else if (in_on_device) {
+        if (thermo::scatter_T(*c, scen, off, cnt, T, in, c->stream)) return fail(c, THERMO_ECUDA, c->err);
+    } else {
+        DevBuf tmp;
+        API_CK(cudaMalloc(&tmp.p, sizeof(double) * (cnt + 1)));
+        API_CK(cudaMemcpyAsync(tmp.p, in, sizeof(double) * cnt, cudaMemcpyHostToDevice, c->stream));
+        if (thermo::scatter_T(*c, scen, off, cnt, T, (const double *)tmp.p, c->stream)) return fail(c, THERMO_ECUDA, c->err);
+        API_CK(cudaStreamSynchronize(c->stream));
+    }
     if (!in_on_device) API_CK(cudaStreamSynchronize(c->stream));
     return THERMO_OK;
 }
@@ -877,6 +986,11 @@ extern "C" int thermo_get_stats(const void *ctx, thermo_stats *out) {
     out->solve_block = c->cg_block;
     out->launches_per_step = c->last_nsteps > 0 && c->last_launches > 0 ? (int32_t)(c->last_launches / c->last_nsteps)
                                                                           : 1 + (c->n_if ? 2 : 0);
+    out->reordered = c->reorder;
+    out->order_max_runs = c->probe_runs;
+    out->order_max_window = c->probe_window;
+    out->solve_variant = c->S == 1 ? c->cg_variant : -1;
+    out->solve_kind = c->S == 1 ? c->cg_kind : -1;
     return THERMO_OK;
 }
 

@@ -407,3 +407,27 @@ def initial_field(cfg: Config, seed: int = 11, amp: float = 0.5) -> np.ndarray:
         r = uniform01(seed + 101 * s, idx, 5)
         out[s] = cfg.T0 + amp * np.sin(3.0 * xyz[:, 0] + 5.0 * xyz[:, 2] + s) + 0.1 * amp * (2 * r - 1)
     return out
+
+
+def permute_mesh(mesh: Mesh, seed: int) -> Tuple[Mesh, np.ndarray]:
+    """The same mesh with its nodes renumbered by a seeded random permutation (an arbitrary
+    caller numbering, as a CAD mesher would produce).  Returns (mesh, old_of_new):
+    node k of the result is node old_of_new[k] of the input.  Tets and faces keep their order
+    and orientation."""
+    n = mesh.n_nodes
+    old_of_new = np.argsort(uniform01(seed, np.arange(n, dtype=np.int64), 3), kind="stable")
+    new_of_old = np.empty(n, dtype=np.int64)
+    new_of_old[old_of_new] = np.arange(n)
+    return Mesh(xyz=np.ascontiguousarray(mesh.xyz[old_of_new]),
+                tets=np.ascontiguousarray(new_of_old[mesh.tets].astype(np.int32)),
+                bfaces=np.ascontiguousarray(new_of_old[mesh.bfaces].astype(np.int32)),
+                bface_tag=mesh.bface_tag.copy()), old_of_new
+
+
+def permute_config(cfg: Config, seed: int = 99) -> Tuple[Config, np.ndarray]:
+    """cfg with both parts' nodes randomly renumbered (seeded).  Returns (cfg', old_of_new) with
+    old_of_new over the coupled numbering (fixed part first): T'[k] = T[old_of_new[k]]."""
+    f, pf = permute_mesh(cfg.fixed, seed)
+    m, pm = permute_mesh(cfg.moving, seed + 1)
+    out = dataclasses.replace(cfg, name=cfg.name + "_perm", fixed=f, moving=m)
+    return out, np.concatenate([pf, pm + cfg.fixed.n_nodes])

@@ -51,7 +51,10 @@ class Stats(ctypes.Structure):
                 ("failed_relres", ctypes.c_double), ("last_relres", ctypes.c_double),
                 ("steps_done", ctypes.c_int64), ("iface_area", ctypes.c_double),
                 ("ms_iface", ctypes.c_double), ("ms_solve", ctypes.c_double), ("solve_grid", ctypes.c_int32),
-                ("solve_block", ctypes.c_int32), ("launches_per_step", ctypes.c_int32)]
+                ("solve_block", ctypes.c_int32), ("launches_per_step", ctypes.c_int32),
+                ("reordered", ctypes.c_int32), ("order_max_runs", ctypes.c_int32),
+                ("order_max_window", ctypes.c_int32), ("solve_variant", ctypes.c_int32),
+                ("solve_kind", ctypes.c_int32), ("reserved_", ctypes.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
