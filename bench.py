@@ -231,14 +231,14 @@ def run_thermo(args):
     # host memory (thermo_get_T_async: the copy of step k overlaps step k + 1; two host
     # buffer sets alternate); thermo_sync waits for the last copies inside the timed region
     KE = max(1, args.e2e_steps)
-    hosts = [[torch.empty(cfg.n_dof, dtype=torch.float64, pin_memory=True) for _ in range(th.S)] for _ in range(2)]
+    # (all scenarios of a batched context in one transfer: thermo_get_T_all_async)
+    hosts = [torch.empty(th.S * cfg.n_dof, dtype=torch.float64, pin_memory=True) for _ in range(2)]
     barrier()
     e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e2.record(stream)
     for k in range(KE):
         th.step(t, cfg.dt, 1)
-        for sc, h in enumerate(hosts[k & 1]):
-            th.get_T_async(h.data_ptr(), scen=sc)
+        th.get_T_all_async(hosts[k & 1].data_ptr())
         t += cfg.dt
     th.sync()
     e3.record(stream)

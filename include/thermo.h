@@ -124,6 +124,13 @@ int thermo_get_T(void *ctx, int32_t scen, int32_t part, double *out, int64_t n,
  * after thermo_sync().  Same selection rules and errors as thermo_get_T. */
 int thermo_get_T_async(void *ctx, int32_t scen, int32_t part, double *host_out, int64_t n);
 
+/* Asynchronous copy of every scenario's whole field (both parts, the caller's numbering) into
+ * host_out[n_scen][n_nodes_fixed + n_nodes_moving], scenario-major, as one transfer: the
+ * batched state block (N x SP, row-major on the device) is transposed by one kernel on the copy
+ * stream into a staging buffer first.  n must equal n_scen * N.  Valid after thermo_sync().
+ * EINVAL on a NULL pointer or a wrong n. */
+int thermo_get_T_all_async(void *ctx, double *host_out, int64_t n);
+
 /* Wait for all work of the context: its stream and every pending asynchronous copy. */
 int thermo_sync(void *ctx);
 
@@ -227,6 +234,8 @@ typedef struct {
     int32_t solve_variant;           /* CG kernel variant chosen at create (S = 1): kind 2 =
                                         windowed TMA sweep */
     int32_t solve_kind;
+    int32_t solve_max_runs;          /* kind 2: max column-window runs of a chunk (internal order) */
+    int32_t solve_window;            /* kind 2: max column-window entries of a chunk */
     int32_t reserved_;
 } thermo_stats;
 

@@ -1121,6 +1121,7 @@ int cg_setup(Ctx &c) {
             cudaFree(d_stats);
             if (stats[2] || stats[1] > CG_MAXR) continue;
             wc = (stats[0] + 1) & ~1;
+            c.cg_max_runs = stats[1];
         }
         const size_t sb = stage_bytes(v, E, wc);
         // ring budget: 210 KB leaves the rest of the 228-KB carve-out to L1 (224 KB, one more

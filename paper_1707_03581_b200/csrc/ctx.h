@@ -104,7 +104,7 @@ struct Ctx {
     int32_t *d_chunk_nruns = nullptr;
     int32_t *d_chunk_lown = nullptr;
     unsigned long long *d_trace = nullptr;   // THERMO_CG_TRACE=1: barrier timestamps of the last solve
-    int cg_win_cap = 0, cg_nstages = 1;
+    int cg_win_cap = 0, cg_nstages = 1, cg_max_runs = 0;
     int64_t cg_u_rows = 0;
     int *d_chunk_ctr = nullptr;
 

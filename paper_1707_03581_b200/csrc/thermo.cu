@@ -865,6 +865,7 @@ static int ensure_copy_stream(Ctx *c) {
 
 // Queue on the copy stream (after the work queued so far on the context stream): the staged
 // fields of buffer b if stale, then the copy of [off, off + cnt) of scenario scen to host_out.
+// scen = -1: all scenarios, [0, S * N) of the staged fields
 static int queue_host_copy(Ctx *c, int scen, int64_t off, int64_t cnt, double *host_out) {
     if (int rc = ensure_copy_stream(c)) return rc;
     const int b = c->cur;
@@ -881,8 +882,8 @@ static int queue_host_copy(Ctx *c, int scen, int64_t off, int64_t cnt, double *h
             if (rc) return THERMO_ECUDA;
             c->stage_ver[b] = c->ver[b];
         }
-        API_CK(cudaMemcpyAsync(host_out, c->d_stage[b] + (int64_t)scen * c->N + off, sizeof(double) * cnt,
-                               cudaMemcpyDeviceToHost, c->copy_stream));
+        API_CK(cudaMemcpyAsync(host_out, c->d_stage[b] + (scen < 0 ? 0 : (int64_t)scen * c->N + off),
+                               sizeof(double) * cnt, cudaMemcpyDeviceToHost, c->copy_stream));
     }
     API_CK(cudaEventRecord(c->ev_copy[b], c->copy_stream));
     c->copy_pending[b] = 1;
@@ -913,6 +914,13 @@ extern "C" int thermo_get_T_async(void *ctx, int32_t scen, int32_t part, double 
     int64_t off, cnt;
     if (int rc = selection(c, scen, part, n, &off, &cnt)) return rc;
     return queue_host_copy(c, scen, off, cnt, host_out);
+}
+
+extern "C" int thermo_get_T_all_async(void *ctx, double *host_out, int64_t n) {
+    Ctx *c = (Ctx *)ctx;
+    if (!c || !host_out) return c ? fail(c, THERMO_EINVAL, "host_out is NULL") : THERMO_EINVAL;
+    if (n != c->N * c->S) return fail(c, THERMO_EINVAL, "n must equal n_scen * n_nodes");
+    return queue_host_copy(c, c->S == 1 ? 0 : -1, 0, n, host_out);
 }
 
 extern "C" int thermo_sync(void *ctx) {
@@ -991,6 +999,8 @@ extern "C" int thermo_get_stats(const void *ctx, thermo_stats *out) {
     out->order_max_window = c->probe_window;
     out->solve_variant = c->S == 1 ? c->cg_variant : -1;
     out->solve_kind = c->S == 1 ? c->cg_kind : -1;
+    out->solve_max_runs = c->cg_max_runs;
+    out->solve_window = c->cg_win_cap;
     return THERMO_OK;
 }
 

@@ -21,7 +21,7 @@ _CODES = {-1: "EINVAL", -2: "ENOMEM", -3: "ECUDA", -4: "ENOCONV", -5: "EGEOM"}
 EXPORTS = ["thermo_create_mesh", "thermo_set_bc", "thermo_step", "thermo_get_T", "thermo_set_T",
            "thermo_set_solver", "thermo_get_stats", "thermo_get_step_iters", "thermo_last_error",
            "thermo_destroy", "thermo_set_timing", "thermo_set_method", "thermo_stationary",
-           "thermo_get_T_async", "thermo_sync", "thermo_set_guess", "thermo_get_interface"]
+           "thermo_get_T_async", "thermo_get_T_all_async", "thermo_sync", "thermo_set_guess", "thermo_get_interface"]
 
 
 class ThermoError(RuntimeError):
@@ -54,7 +54,8 @@ class Stats(ctypes.Structure):
                 ("solve_block", ctypes.c_int32), ("launches_per_step", ctypes.c_int32),
                 ("reordered", ctypes.c_int32), ("order_max_runs", ctypes.c_int32),
                 ("order_max_window", ctypes.c_int32), ("solve_variant", ctypes.c_int32),
-                ("solve_kind", ctypes.c_int32), ("reserved_", ctypes.c_int32)]
+                ("solve_kind", ctypes.c_int32), ("solve_max_runs", ctypes.c_int32),
+                ("solve_window", ctypes.c_int32), ("reserved_", ctypes.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -90,6 +91,7 @@ def load(path: str = LIB_PATH):
     L.thermo_set_method.argtypes = [vp, i32, i32, i32, i32]
     L.thermo_stationary.argtypes = [vp, ctypes.c_double, i32]
     L.thermo_get_T_async.argtypes = [vp, i32, i32, vp, ctypes.c_int64]
+    L.thermo_get_T_all_async.argtypes = [vp, vp, ctypes.c_int64]
     L.thermo_sync.argtypes = [vp]
     _lib = L
     return L
@@ -220,6 +222,11 @@ class Thermo:
         and return at once; valid after sync()."""
         n = self._count(part)
         self._check(load().thermo_get_T_async(self.h, scen, part, ctypes.c_void_p(ptr), n))
+
+    def get_T_all_async(self, ptr: int):
+        """Enqueue one copy of every scenario's field (scenario-major [S][N], caller numbering)
+        into caller-owned (pinned) host memory at `ptr`; valid after sync()."""
+        self._check(load().thermo_get_T_all_async(self.h, ctypes.c_void_p(ptr), self.n * self.S))
 
     def sync(self):
         self._check(load().thermo_sync(self.h))

@@ -7,7 +7,10 @@ and driven to a relative residual of 1e-14 (true residual checked at every step'
 the reference does not depend on any CG start and its own solver error is negligible.
 
 The GPU side runs the library's defaults (quadratic-extrapolation CG start, rtol 1e-12 --
-the configuration bench.py times), plus the x0 = T^n start as a second mode.  North-star
+the configuration bench.py times), plus the x0 = T^n start as a second mode.  From x0 = T^n
+CG stops with a larger error per step (the start is further from the solution, so the last
+iteration's error is larger for the same residual bound) and over the 3600 steps of configs[2]
+the drift reaches 1.62e-9 at rtol 1e-12 (measured); that mode is therefore run at rtol 2e-13.  North-star
 bar: max-norm relative error <= 1e-9 after the full run (reading R18), over
   cfg1, cfg2   every DoF
   cfg3         1.3 M stored DoF (every boundary node, every interface-adjacent node, a seeded
@@ -26,7 +29,7 @@ from paper_1707_03581_b200 import inputs as I
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 TOL = 1e-9
-MODES = {"default": None, "x0_Tn": 0}
+MODES = {"default": (None, None), "x0_Tn": (0, 2e-13)}   # (CG start, rtol)
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -46,8 +49,11 @@ def _golden(name):
 def _run(cfg, mode, nsteps):
     from paper_1707_03581_b200.thermo import Thermo
     th = Thermo.from_config(cfg)
-    if MODES[mode] is not None:
-        th.set_guess(MODES[mode])
+    guess, rtol = MODES[mode]
+    if guess is not None:
+        th.set_guess(guess)
+    if rtol is not None:
+        th.set_solver(rtol=rtol)
     th.step(0.0, cfg.dt, nsteps)
     return th
 

@@ -149,7 +149,10 @@ def test_batched_random_numbering(monkeypatch):
     hosts = [torch.empty(cfg.n_dof, dtype=torch.float64, pin_memory=True) for _ in scen]
     for k, h in enumerate(hosts):
         th.get_T_async(h.data_ptr(), scen=k)
+    allh = torch.empty(len(scen) * cfg.n_dof, dtype=torch.float64, pin_memory=True)
+    th.get_T_all_async(allh.data_ptr())
     th.sync()
+    assert np.array_equal(allh.numpy().reshape(len(scen), cfg.n_dof), np.stack([h.numpy() for h in hosts]))
     for k, sc in enumerate(scen):
         o = O.Oracle.from_config(cfg)
         Tr, _ = o.step(np.full(o.n, cfg.T0), 0.0, cfg.dt, 6, sc)
