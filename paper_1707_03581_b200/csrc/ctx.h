@@ -225,7 +225,7 @@ int cgb_launch_step(Ctx &c, int step, double dt, const double *x0 = nullptr);
 
 // reorder.cu (internal numbering, state transfers in the caller's numbering)
 int order_probe(Ctx &c, bool *good, int *max_runs, int *max_window);
-int rcm_order(Ctx &c, std::vector<int32_t> &new_to_old);
+int rcm_order(Ctx &c, const std::vector<char> &is_iface, bool rooted, std::vector<int32_t> &new_to_old);
 int gather_T(Ctx &c, int scen, int64_t off, int64_t cnt, const double *T, double *out, cudaStream_t st);
 int scatter_T(Ctx &c, int scen, int64_t off, int64_t cnt, double *T, const double *in, cudaStream_t st);
 int gather_all(Ctx &c, const double *T, double *out, cudaStream_t st);

@@ -7,8 +7,8 @@
 // level structure of a breadth-first order) meets that; a scattered one does not.  At create
 // the library therefore probes the caller's numbering with the same window test and, when it
 // fails, renumbers each part by reverse Cuthill-McKee on the volume pattern (breadth-first
-// level sets from a pseudo-peripheral node, neighbours by increasing degree).  Fixed nodes
-// stay in [0, nf) and moving ones in [nf, N).
+// level sets from a pseudo-peripheral node, neighbours by increasing degree; a variant rooted
+// at the interface nodes is selectable).  Fixed nodes stay in [0, nf) and moving ones in [nf, N).
 //
 // The ABI keeps the caller's numbering: thermo_set_T / thermo_get_T / thermo_get_T_async
 // scatter and gather through the permutation (and, for S > 1 scenarios, between the N x SP
@@ -64,9 +64,18 @@ int order_probe(Ctx &c, bool *good, int *max_runs, int *max_window) {
     return 0;
 }
 
-// Reverse Cuthill-McKee of each part from the device volume pattern.  new_to_old[i] = the
-// caller's (coupled) index of internal node i.
-int rcm_order(Ctx &c, std::vector<int32_t> &new_to_old) {
+// Cuthill-McKee numbering of each part from the device volume pattern (breadth-first level
+// sets, neighbours by increasing degree).
+//   rooted = false (default): reverse Cuthill-McKee from a pseudo-peripheral node (George-Liu).
+//     Narrow levels: every 256-row chunk's column window fits the windowed kernel (KIND 2).
+//   rooted = true: level 0 = the part's interface nodes (ordered by a Cuthill-McKee sweep of the
+//     surface graph), then the levels away from the interface; the interface rows form one
+//     contiguous block as in lattice order, but the levels are wider (shells around the rail
+//     top) and the windows of cfg 2/3 exceed the KIND 2 stage budget (KIND 1 is chosen).
+//     Measured (random numbering, B200, per CG iteration vs lattice order): default cfg 2
+//     1.17x / cfg 3 1.09x (KIND 2); rooted 1.10x / 1.09x (KIND 1).  DESIGN.md §6.
+// new_to_old[i] = the caller's (coupled) index of internal node i.
+int rcm_order(Ctx &c, const std::vector<char> &is_iface, bool rooted, std::vector<int32_t> &new_to_old) {
     const int64_t N = c.N;
     std::vector<int64_t> sp(c.nslices + 1);
     std::vector<int32_t> col(c.nnz_pad);
@@ -83,24 +92,23 @@ int rcm_order(Ctx &c, std::vector<int32_t> &new_to_old) {
         for (int k = 0; k < w; ++k) d += nb(i, k) != (int32_t)i;
         deg[i] = d;
     }
+    auto by_degree = [&](int32_t a, int32_t b) { return deg[a] != deg[b] ? deg[a] < deg[b] : a < b; };
     std::vector<int32_t> level(N, -1), order;
     order.reserve(N);
-    std::vector<int32_t> cand;
-    // breadth-first levels from r (marks `level`), returns the last level's nodes; the nodes
-    // visited are appended to `seen` so their marks can be reset
-    auto bfs_levels = [&](int32_t r, std::vector<int32_t> &seen, std::vector<int32_t> &last) {
+    // breadth-first levels from r over the nodes with allowed(v) (marks `level`; the visited
+    // nodes go to `seen` so the marks can be reset); returns the eccentricity, `last` = last level
+    auto bfs_levels = [&](int32_t r, auto allowed, std::vector<int32_t> &seen, std::vector<int32_t> &last) {
         seen.clear();
         seen.push_back(r);
         level[r] = 0;
-        size_t head = 0;
         int L = 0;
-        while (head < seen.size()) {
-            const int32_t u = seen[head++];
+        for (size_t head = 0; head < seen.size(); ++head) {
+            const int32_t u = seen[head];
             L = level[u];
             const int w = width(u);
             for (int k = 0; k < w; ++k) {
                 const int32_t v = nb(u, k);
-                if (v != u && level[v] < 0) {
+                if (v != u && level[v] < 0 && allowed(v)) {
                     level[v] = level[u] + 1;
                     seen.push_back(v);
                 }
@@ -111,53 +119,71 @@ int rcm_order(Ctx &c, std::vector<int32_t> &new_to_old) {
             if (level[v] == L) last.push_back(v);
         return L;
     };
+    // pseudo-peripheral node of r's component (restricted to allowed)
+    auto peripheral = [&](int32_t r, auto allowed) {
+        std::vector<int32_t> seen, last;
+        int ecc = bfs_levels(r, allowed, seen, last);
+        for (int rep = 0; rep < 8; ++rep) {
+            int32_t x = last[0];
+            for (int32_t v : last)
+                if (by_degree(v, x)) x = v;
+            for (int32_t v : seen) level[v] = -1;
+            const int e2 = bfs_levels(x, allowed, seen, last);
+            if (e2 <= ecc) break;
+            r = x;
+            ecc = e2;
+        }
+        for (int32_t v : seen) level[v] = -1;
+        return r;
+    };
     std::vector<char> done(N, 0);
-    std::vector<int32_t> seen, last, nbuf;
+    std::vector<int32_t> nbuf;
+    // Cuthill-McKee sweep: order[head..] grows by the unvisited allowed neighbours of each node
+    auto sweep = [&](size_t head, auto allowed) {
+        for (; head < order.size(); ++head) {
+            const int32_t u = order[head];
+            nbuf.clear();
+            const int w = width(u);
+            for (int k = 0; k < w; ++k) {
+                const int32_t v = nb(u, k);
+                if (v != u && !done[v] && allowed(v)) {
+                    done[v] = 1;
+                    nbuf.push_back(v);
+                }
+            }
+            std::sort(nbuf.begin(), nbuf.end(), by_degree);
+            order.insert(order.end(), nbuf.begin(), nbuf.end());
+        }
+    };
+    auto any = [](int32_t) { return true; };
+    auto on_iface = [&](int32_t v) { return is_iface[v] != 0; };
     for (int part = 0; part < 2; ++part) {
         const int64_t lo = part ? c.nf : 0, hi = part ? N : c.nf;
         const size_t part_begin = order.size();
-        for (int64_t s = lo; s < hi; ++s) {
-            if (done[s]) continue;
-            // pseudo-peripheral start (George-Liu): repeat from a minimum-degree node of the
-            // last level while the eccentricity grows
-            int32_t r = (int32_t)s;
-            int ecc = bfs_levels(r, seen, last);
-            for (int rep = 0; rep < 8; ++rep) {
-                int32_t x = last[0];
-                for (int32_t v : last)
-                    if (deg[v] < deg[x] || (deg[v] == deg[x] && v < x)) x = v;
-                for (int32_t v : seen) level[v] = -1;
-                const int e2 = bfs_levels(x, seen, last);
-                if (e2 <= ecc) break;
-                r = x;
-                ecc = e2;
+        if (rooted) {   // level 0: the interface nodes, surface component by surface component
+            for (int64_t s = lo; s < hi; ++s) {
+                if (done[s] || !is_iface[s]) continue;
+                const int32_t r = peripheral((int32_t)s, on_iface);
+                const size_t b = order.size();
+                order.push_back(r);
+                done[r] = 1;
+                sweep(b, on_iface);
             }
-            for (int32_t v : seen) level[v] = -1;
-            // Cuthill-McKee from r: unvisited neighbours by increasing degree (then index)
-            const size_t comp_begin = order.size();
+            sweep(part_begin, any);   // levels away from the interface
+        }
+        for (int64_t s = lo; s < hi; ++s) {   // (remaining) components from a pseudo-peripheral node
+            if (done[s]) continue;
+            const int32_t r = peripheral((int32_t)s, any);
+            const size_t b = order.size();
             order.push_back(r);
             done[r] = 1;
-            for (size_t head = comp_begin; head < order.size(); ++head) {
-                const int32_t u = order[head];
-                nbuf.clear();
-                const int w = width(u);
-                for (int k = 0; k < w; ++k) {
-                    const int32_t v = nb(u, k);
-                    if (v != u && !done[v]) {
-                        done[v] = 1;
-                        nbuf.push_back(v);
-                    }
-                }
-                std::sort(nbuf.begin(), nbuf.end(),
-                          [&](int32_t a, int32_t b) { return deg[a] != deg[b] ? deg[a] < deg[b] : a < b; });
-                order.insert(order.end(), nbuf.begin(), nbuf.end());
-            }
+            sweep(b, any);
         }
         if ((int64_t)(order.size() - part_begin) != hi - lo) {
             c.err = "reordering: volume pattern couples the two parts";
             return -1;
         }
-        std::reverse(order.begin() + part_begin, order.end());   // reverse Cuthill-McKee
+        if (!rooted) std::reverse(order.begin() + part_begin, order.end());   // reverse Cuthill-McKee
     }
     new_to_old.swap(order);
     return 0;

@@ -188,7 +188,8 @@ extern "C" int thermo_create_mesh(void **out, const thermo_mesh *fixed, const th
             return THERMO_EINVAL;
         }
     // THERMO_REORDER (tuning / test hook): unset = renumber only if the caller's numbering fails
-    // the window test, 0 = never, 1 = always (reverse Cuthill-McKee)
+    // the window test, 0 = never, 1 = always (reverse Cuthill-McKee), 2 = always (Cuthill-McKee
+    // rooted at the interface nodes; reorder.cu)
     const char *ro = getenv("THERMO_REORDER");
     const int reorder_mode = ro ? atoi(ro) : -1;
     HostMesh hm;
@@ -239,13 +240,16 @@ extern "C" int thermo_create_mesh(void **out, const thermo_mesh *fixed, const th
             c->probe_window = probe_window;
             int rc = thermo::assemble_create(*c, hm.xyz.data(), hm.tets.data(), hm.faces.data(), hm.fkey.data());
             if (!rc && attempt == 0 && reorder_mode != 0) {
-                // window test of the caller's numbering; renumber (RCM) and start over if it fails
+                // window test of the caller's numbering; renumber (Cuthill-McKee) and start over if it fails
                 bool good = true;
                 rc = thermo::order_probe(*c, &good, &probe_runs, &probe_window);
                 c->probe_runs = probe_runs;
                 c->probe_window = probe_window;
-                if (!rc && (!good || reorder_mode == 1)) {
-                    rc = thermo::rcm_order(*c, new_to_old);
+                if (!rc && (!good || reorder_mode >= 1)) {
+                    std::vector<char> is_iface(N, 0);
+                    for (const auto *v : {&hm.fA, &hm.fB})
+                        for (int32_t e : *v) is_iface[e] = 1;
+                    rc = thermo::rcm_order(*c, is_iface, reorder_mode == 2, new_to_old);
                     if (!rc) {
                         free_ctx(c);
                         permute_host_mesh(hm, new_to_old, old_to_new);

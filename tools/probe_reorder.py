@@ -1,6 +1,6 @@
 """Numbering-independence probe: device time per CG iteration of the lattice-ordered config
 against the same config with its nodes randomly renumbered (inputs.permute_config), which the
-library renumbers internally (reverse Cuthill-McKee) at create.
+library renumbers internally (reverse Cuthill-McKee; THERMO_REORDER=2: rooted at the interface) at create.
 
     python tools/probe_reorder.py cfg2 cfg3 [K]
 """
