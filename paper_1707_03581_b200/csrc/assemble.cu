@@ -385,10 +385,10 @@ int assemble_create(Ctx &c, const double *xyz, const int32_t *tets, const int32_
     CK(cudaMalloc(&c.d_R, sizeof(double) * (nnz_pad + 1)));
     CK(cudaMalloc(&c.d_val, sizeof(double) * (nnz_pad + 1)));
     CK(cudaMalloc(&c.d_diagpos, sizeof(int64_t) * N));
-    CK(cudaMalloc(&c.d_ML, sizeof(double) * N));
-    CK(cudaMalloc(&c.d_benv, sizeof(double) * N));
-    CK(cudaMalloc(&c.d_Dvol, sizeof(double) * N));
-    CK(cudaMalloc(&c.d_Dinv, sizeof(double) * N));
+    CK(cudaMalloc(&c.d_ML, sizeof(double) * (N + 16)));   // +16: 16-byte bulk copies of row ranges
+    CK(cudaMalloc(&c.d_benv, sizeof(double) * (N + 16)));
+    CK(cudaMalloc(&c.d_Dvol, sizeof(double) * (N + 16)));
+    CK(cudaMalloc(&c.d_Dinv, sizeof(double) * (N + 16)));
     CK(cudaMemsetAsync(c.d_benv, 0, sizeof(double) * N, st));
     k_row_fill<<<nb(c.nslices * 32, 128), 128, 0, st>>>(c.d_tinc_ptr, c.d_tinc, c.d_tets, c.d_xyz, N,
                                                         c.d_slice_ptr, c.nu, c.rho_cp, c.d_col, c.d_A,

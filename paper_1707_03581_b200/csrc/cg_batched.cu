@@ -543,6 +543,8 @@ __global__ void k_dinv_broadcast(const double *Dinv, int64_t N, int S, int SP, d
 int cgb_setup(Ctx &c) {
     if (c.S > CGB_MAXS) { c.err = "at most 64 scenarios per context"; return -1; }
     if (int rc = build_if_of_row(c)) return rc;
+    if (int rc = sbcg_setup(c)) return rc;
+    if (c.sb_on) return 0;   // windowed SpMM kernel (cg_spmm.cu)
     int per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cgb_step, CGB_BLOCK, 0));
     if (per_sm < 1) { c.err = "batched CG kernel cannot be resident"; return -3; }
@@ -554,6 +556,7 @@ int cgb_setup(Ctx &c) {
 }
 
 int cgb_prepare(Ctx &c) {
+    if (c.sb_on) return 0;   // the SpMM kernel reads the volume D^{-1} and the interface rows' own
     const int64_t n = c.N * c.SP;
     k_dinv_broadcast<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(c.d_Dinv, c.N, c.S, c.SP, c.d_DinvS);
     CK(cudaGetLastError());
@@ -561,6 +564,7 @@ int cgb_prepare(Ctx &c) {
 }
 
 int cgb_launch_step(Ctx &c, int step, double dt, const double *x0) {
+    if (c.sb_on) return sbcg_launch_step(c, step, dt, x0);
     CGBParams P;
     memset(&P, 0, sizeof P);
     P.N = c.N;

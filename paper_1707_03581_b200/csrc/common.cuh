@@ -45,6 +45,18 @@ __device__ __forceinline__ unsigned long long gtimer() {
     return t;
 }
 
+__device__ __forceinline__ double ld_cg1(const double *p) {
+    double v;
+    asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+
+// order this thread's generic-proxy shared-memory accesses before later async-proxy (TMA)
+// accesses of the same memory (and vice versa)
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 __device__ __forceinline__ double2 ld_cg2(const double2 *p) {
     double2 v;
     asm volatile("ld.global.cg.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
@@ -230,7 +242,8 @@ struct IfaceParams {
     double *if_b;             // [S][n_if] dt-free friction source eta/2 int phi
     double *if_phi;           // [S][n_if] int_{Gamma_R} phi
     double *Dinv;             // S == 1: [N] Jacobi inverse diagonal, interface rows rewritten
-    double *if_dinv;          // (unused)
+    double *if_dinv;          // S > 1: [k][s] per-scenario Jacobi inverse diagonal of the interface rows
+    double *if_d;             // S > 1: [k][s] per-scenario Jacobi diagonal of the interface rows
     int step;                 // time step of this assembly: an overflow records the first one in
                               // status[4] (the overlap mode assembles one step ahead of the solve)
     double *DinvS;            // S > 1: [N][SP] per-scenario Jacobi inverse diagonal

@@ -30,7 +30,9 @@ struct Ctx {
 
     int64_t nf = 0, nm = 0, N = 0;
     int S = 1;
-    int SP = 1;                      // row stride of the state / workspace block vectors (N x SP)
+    int SP = 1;                      // scenario columns of the state / workspace block vectors (>= S)
+    int CW = 1;                      // block layout [SP / CW][N][CW]: CW = SP (row-major N x SP) or 32
+                                     // (column groups of the windowed SpMM kernel, cg_spmm.cu)
     double *d_DinvS = nullptr;       // S > 1: per-scenario Jacobi inverse diagonal [N][SP]
     double nu = 0, rho_cp = 0, alpha = 0;
     int iface_tag_f = 0, iface_tag_m = 0;
@@ -76,6 +78,7 @@ struct Ctx {
     int32_t *d_slice_if = nullptr;   // [nslices + 1]
     int32_t *d_ell_cnt = nullptr, *d_ell_col = nullptr;
     double *d_ell_val = nullptr, *d_if_b = nullptr, *d_if_phi = nullptr, *d_if_dinv = nullptr;
+    double *d_if_d = nullptr;        // S > 1 (windowed SpMM): per-scenario diagonal of the interface rows
     double plane_n[3] = {0, 0, 1}, e1[3] = {1, 0, 0}, e2[3] = {0, 1, 0};
     double min_edge = 0.0;
 
@@ -166,6 +169,16 @@ struct Ctx {
     int32_t *d_pcnt_s = nullptr;
     double ms_iface = 0.0, ms_solve = 0.0;
 
+    // windowed SpMM batched kernel (cg_spmm.cu)
+    bool sb_on = false;
+    int sb_G = 1, sb_nstages = 0;
+    uint32_t sb_stage = 0, sb_col_off = 0, sb_win_off = 0, sb_own_off = 0, sb_aux_off = 0;
+    size_t sb_smem = 0;
+    double *d_sb_partials = nullptr, *d_sb_totals = nullptr;
+    int32_t *d_sb_if_ptr = nullptr, *d_sb_if_k = nullptr;   // interface rows per CTA
+    void *d_sb_recs = nullptr;                              // packed chunk metadata per CTA
+    int32_t *d_sb_rec_ptr = nullptr;
+
     // internal numbering (reorder.cu): nullptr / empty = the caller's numbering
     int32_t *d_int_of_ext = nullptr;      // [N] internal index of the caller's node e
     std::vector<int32_t> h_ext_of_int;    // [N] the caller's index of internal node i
@@ -222,6 +235,10 @@ int sdc_step(Ctx &c, double tn, double dt, int step_index);   // single-rate SDC
 int cgb_setup(Ctx &c);
 int cgb_prepare(Ctx &c);   // broadcast the volume D^{-1} into DinvS (after build_operator)
 int cgb_launch_step(Ctx &c, int step, double dt, const double *x0 = nullptr);
+
+// cg_spmm.cu (S > 1: windowed SpMM kernel, selected by cgb_setup when the windows fit)
+int sbcg_setup(Ctx &c);
+int sbcg_launch_step(Ctx &c, int step, double dt, const double *x0);
 
 // reorder.cu (internal numbering, state transfers in the caller's numbering)
 int order_probe(Ctx &c, bool *good, int *max_runs, int *max_window);

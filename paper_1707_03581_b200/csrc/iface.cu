@@ -483,7 +483,11 @@ __global__ void __launch_bounds__(32 * ROW_WPB) k_rows(IfaceParams P) {
         } else if (P.S == 1) {
             P.Dinv[row] = dinv;
         } else {
-            P.DinvS[(int64_t)row * P.SP + s] = dinv;
+            if (P.DinvS) P.DinvS[(int64_t)row * P.SP + s] = dinv;   // gather kernel (cg_batched.cu)
+            if (P.if_d) {                                           // windowed SpMM kernel (cg_spmm.cu)
+                P.if_dinv[row_index(P, s, k)] = dinv;
+                P.if_d[row_index(P, s, k)] = P.Dvol[row] + dself;
+            }
         }
     }
 }
@@ -879,6 +883,7 @@ void iface_params(Ctx &c, IfaceParams &P, const double *step_sc, double dt, int 
     P.if_phi = buf ? c.d_if_phi_b : c.d_if_phi;
     P.Dinv = buf ? c.d_Dinv_b : c.d_Dinv;
     P.if_dinv = c.d_if_dinv;
+    P.if_d = c.d_if_d;
     P.DinvS = c.d_DinvS;
     P.SP = c.SP;
     P.status = c.d_status;

@@ -11,8 +11,8 @@
 // at the interface nodes is selectable).  Fixed nodes stay in [0, nf) and moving ones in [nf, N).
 //
 // The ABI keeps the caller's numbering: thermo_set_T / thermo_get_T / thermo_get_T_async
-// scatter and gather through the permutation (and, for S > 1 scenarios, between the N x SP
-// row-major state block and one contiguous field per scenario), and thermo_get_interface maps
+// scatter and gather through the permutation (and, for S > 1 scenarios, between the state block
+// [SP / CW][N][CW] and one contiguous field per scenario), and thermo_get_interface maps
 // its row and column indices back.
 #include <algorithm>
 #include <cstdio>
@@ -189,29 +189,32 @@ int rcm_order(Ctx &c, const std::vector<char> &is_iface, bool rooted, std::vecto
     return 0;
 }
 
-// out[k] = T[map(off + k) * SP + scen], map = int_of_ext (nullptr: identity)
-__global__ void k_gather_T(const double *__restrict__ T, int SP, int scen, const int32_t *__restrict__ map,
+// Element (row i, scenario s) of a block vector with the layout [SP / CW][N][CW].
+__device__ __forceinline__ int64_t blk(int64_t N, int CW, int64_t i, int s) {
+    return ((int64_t)(s / CW) * N + i) * CW + s % CW;
+}
+
+// out[k] = T[map(off + k), scen], map = int_of_ext (nullptr: identity)
+__global__ void k_gather_T(const double *__restrict__ T, int64_t N, int CW, int scen, const int32_t *__restrict__ map,
                            int64_t off, int64_t cnt, double *__restrict__ out) {
     const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (k >= cnt) return;
     const int64_t e = off + k;
-    const int64_t i = map ? map[e] : e;
-    out[k] = T[i * SP + scen];
+    out[k] = T[blk(N, CW, map ? map[e] : e, scen)];
 }
 
-// T[map(off + k) * SP + scen] = in[k]
-__global__ void k_scatter_T(double *__restrict__ T, int SP, int scen, const int32_t *__restrict__ map, int64_t off,
-                            int64_t cnt, const double *__restrict__ in) {
+// T[map(off + k), scen] = in[k]
+__global__ void k_scatter_T(double *__restrict__ T, int64_t N, int CW, int scen, const int32_t *__restrict__ map,
+                            int64_t off, int64_t cnt, const double *__restrict__ in) {
     const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (k >= cnt) return;
     const int64_t e = off + k;
-    const int64_t i = map ? map[e] : e;
-    T[i * SP + scen] = in[k];
+    T[blk(N, CW, map ? map[e] : e, scen)] = in[k];
 }
 
-// All scenarios at once: out[s][e] = T[map(e) * SP + s] for e < N, s < S (a transpose of the
-// row-major N x SP block through 32 x 32 shared-memory tiles; identity map: both sides coalesced)
-__global__ void k_gather_all(const double *__restrict__ T, int S, int SP, const int32_t *__restrict__ map, int64_t N,
+// All scenarios at once: out[s][e] = T[map(e), s] for e < N, s < S (a transpose of the block
+// through 32 x 32 shared-memory tiles; identity map: both sides coalesced)
+__global__ void k_gather_all(const double *__restrict__ T, int S, int CW, const int32_t *__restrict__ map, int64_t N,
                              double *__restrict__ out) {
     __shared__ double tile[32][33];
     const int64_t e0 = blockIdx.x * 32ll;
@@ -220,7 +223,7 @@ __global__ void k_gather_all(const double *__restrict__ T, int S, int SP, const 
     for (int r = ty; r < 32; r += 8) {
         const int64_t e = e0 + r;
         const int s = s0 + tx;
-        if (e < N && s < S) tile[r][tx] = T[(map ? (int64_t)map[e] : e) * SP + s];
+        if (e < N && s < S) tile[r][tx] = T[blk(N, CW, map ? (int64_t)map[e] : e, s)];
     }
     __syncthreads();
     for (int r = ty; r < 32; r += 8) {
@@ -232,21 +235,21 @@ __global__ void k_gather_all(const double *__restrict__ T, int S, int SP, const 
 
 int gather_T(Ctx &c, int scen, int64_t off, int64_t cnt, const double *T, double *out, cudaStream_t st) {
     if (cnt <= 0) return 0;
-    k_gather_T<<<(unsigned)((cnt + 255) / 256), 256, 0, st>>>(T, c.SP, scen, c.d_int_of_ext, off, cnt, out);
+    k_gather_T<<<(unsigned)((cnt + 255) / 256), 256, 0, st>>>(T, c.N, c.CW, scen, c.d_int_of_ext, off, cnt, out);
     CK(cudaGetLastError());
     return 0;
 }
 
 int scatter_T(Ctx &c, int scen, int64_t off, int64_t cnt, double *T, const double *in, cudaStream_t st) {
     if (cnt <= 0) return 0;
-    k_scatter_T<<<(unsigned)((cnt + 255) / 256), 256, 0, st>>>(T, c.SP, scen, c.d_int_of_ext, off, cnt, in);
+    k_scatter_T<<<(unsigned)((cnt + 255) / 256), 256, 0, st>>>(T, c.N, c.CW, scen, c.d_int_of_ext, off, cnt, in);
     CK(cudaGetLastError());
     return 0;
 }
 
 int gather_all(Ctx &c, const double *T, double *out, cudaStream_t st) {
     dim3 grid((unsigned)((c.N + 31) / 32), (unsigned)((c.S + 31) / 32)), block(32, 8);
-    k_gather_all<<<grid, block, 0, st>>>(T, c.S, c.SP, c.d_int_of_ext, c.N, out);
+    k_gather_all<<<grid, block, 0, st>>>(T, c.S, c.CW, c.d_int_of_ext, c.N, out);
     CK(cudaGetLastError());
     return 0;
 }

@@ -76,7 +76,8 @@ static void free_ctx(Ctx *c) {
                     c->d_ell_cnt_s, c->d_ell_col_s, c->d_ell_val_s, c->d_if_b_s, c->d_if_phi_s, c->d_rhs,
                     c->d_pairs_s, c->d_pcnt_s, c->d_star_own, c->d_own_ptr, c->d_own_idx, c->d_x0, c->d_Thist, c->d_z2, c->d_q2,
                     c->d_ell_cnt_b, c->d_ell_col_b, c->d_ell_val_b, c->d_if_b_b, c->d_if_phi_b, c->d_Dinv_b,
-                    c->d_step_sc_spec, c->d_spec_status, c->d_int_of_ext, c->d_stage[0], c->d_stage[1]};
+                    c->d_step_sc_spec, c->d_spec_status, c->d_int_of_ext, c->d_stage[0], c->d_stage[1],
+                    c->d_if_d, c->d_sb_partials, c->d_sb_totals, c->d_sb_if_ptr, c->d_sb_if_k, c->d_sb_recs, c->d_sb_rec_ptr};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     for (cudaEvent_t e : c->events) cudaEventDestroy(e);
@@ -273,10 +274,12 @@ extern "C" int thermo_create_mesh(void **out, const thermo_mesh *fixed, const th
                 if (ok) ok &= cudaMemcpy(c->d_int_of_ext, old_to_new.data(), sizeof(int32_t) * N,
                                          cudaMemcpyHostToDevice) == cudaSuccess;
             }
-            // vectors padded by 16 entries: window bulk copies may read up to one element past N
+            // vectors padded by two rows + 16 entries: window bulk copies may read up to one
+            // (even-rounded) row past N
+            c->CW = c->SP;   // row-major N x SP until the batched kernel chooses column groups
             for (double **p : {&c->d_T[0], &c->d_T[1], &c->d_z, &c->d_p[0], &c->d_p[1], &c->d_q}) {
-                ok &= cudaMalloc(p, sizeof(double) * (NS + 16)) == cudaSuccess;
-                if (ok) cudaMemsetAsync(*p, 0, sizeof(double) * (NS + 16), c->stream);
+                ok &= cudaMalloc(p, sizeof(double) * (NS + 2 * c->SP + 16)) == cudaSuccess;
+                if (ok) cudaMemsetAsync(*p, 0, sizeof(double) * (NS + 2 * c->SP + 16), c->stream);
             }
             ok &= cudaMalloc(&c->d_status, sizeof(int) * 8) == cudaSuccess;
             ok &= cudaMalloc(&c->d_fail_relres, sizeof(double)) == cudaSuccess;
@@ -636,9 +639,9 @@ extern "C" int thermo_step(void *ctx, double t, double dt, int32_t nsteps) {
         const bool extrap = c->guess > 0;
         const int64_t NS = c->N * c->SP;
         if (extrap && !c->d_x0) {
-            API_CK(cudaMalloc(&c->d_x0, sizeof(double) * (NS + 16)));
+            API_CK(cudaMalloc(&c->d_x0, sizeof(double) * (NS + 2 * c->SP + 16)));
             API_CK(cudaMemsetAsync(c->d_x0, 0, sizeof(double) * (NS + 16), c->stream));
-            API_CK(cudaMalloc(&c->d_Thist, sizeof(double) * (NS + 16)));
+            API_CK(cudaMalloc(&c->d_Thist, sizeof(double) * (NS + 2 * c->SP + 16)));
             API_CK(cudaMemsetAsync(c->d_Thist, 0, sizeof(double) * (NS + 16), c->stream));
         }
         int64_t launches = 0;
@@ -781,21 +784,6 @@ extern "C" int thermo_step(void *ctx, double t, double dt, int32_t nsteps) {
                 c->ms_solve += b;
             }
         }
-        if (status[0]) {
-            const int f = status[2];
-            c->failed_step = f;
-            c->failed_scen = status[3];
-            c->failed_relres = status[0] == 1 ? frel : NAN;
-            c->cur = (c->cur + f) & 1;
-            c->steps_done += f;
-            c->hist = 0;
-            c->last_nsteps = f;
-            if (status[0] == 2)
-                return fail(c, THERMO_EGEOM, "interface row capacity exceeded at step " + std::to_string(f));
-            char buf[160];
-            snprintf(buf, sizeof buf, "CG did not converge at step %d (scenario %d), relres %.3e", f, status[3], frel);
-            return fail(c, THERMO_ENOCONV, buf);
-        }
         if (c->d_trace) {   // phase split of the last solve (debug aid)
             unsigned long long tr[1024];
             API_CK(cudaMemcpy(tr, c->d_trace, sizeof tr, cudaMemcpyDeviceToHost));
@@ -803,7 +791,21 @@ extern "C" int thermo_step(void *ctx, double t, double dt, int32_t nsteps) {
             for (int j = 0; j < S; ++j) it = std::max(it, (int)c->h_iters[(size_t)(nsteps - 1) * S + j]);
             double s_ns = 0, u_ns = 0;
             const char *tv = getenv("THERMO_CG_TRACE");
-            if (c->cg_fused && tv && atoi(tv) == 2) {   // 4 stamps per iteration after phase 0
+            if (S > 1 && c->sb_on && tv && atoi(tv) == 3) {   // batched SpMM kernel, 6 stamps per iteration
+                // phase 0: start, sweep+pass.. (4 stamps in reduce incl. the trailing one) -- layout:
+                // [0] start, [1] P0 partials, [2] P0 sync1, [3] P0 end; per iteration: sweep end,
+                // pass end... see cg_spmm.cu: sweep, iface, partials, sync1, (reduce end), U end
+                double d[6] = {0, 0, 0, 0, 0, 0};
+                int m = 0;
+                for (int k = 0; k + 1 < it && 4 + 6 * k + 6 < 1000; ++k, ++m)
+                    for (int j = 0; j < 6; ++j) d[j] += (double)(tr[4 + 6 * k + j] - tr[3 + 6 * k + j]);
+                if (m > 0)
+                    fprintf(stderr, "[thermo trace] SpMM per iteration: sweep %.1f, iface pass %.1f, CTA partials %.1f, "
+                            "grid sync 1 %.1f, totals + sync 2 %.1f, U + sync %.1f us (%d iters)\n",
+                            d[0] * 1e-3 / m, d[1] * 1e-3 / m, d[2] * 1e-3 / m, d[3] * 1e-3 / m, d[4] * 1e-3 / m,
+                            d[5] * 1e-3 / m, m);
+                it = 0;
+            } else if (c->cg_fused && tv && atoi(tv) == 2) {   // 4 stamps per iteration after phase 0
                 double d[4] = {0, 0, 0, 0};
                 int m = 0;
                 for (int k = 0; k + 1 < it && 2 + 4 * k + 4 < 1000; ++k, ++m)
@@ -826,6 +828,21 @@ extern "C" int thermo_step(void *ctx, double t, double dt, int32_t nsteps) {
             if (it > 0)
                 fprintf(stderr, "[thermo trace] phase0 %.1f us, S %.1f us/iter, U %.1f us/iter (%d iters)\n",
                         (tr[1] - tr[0]) * 1e-3, s_ns * 1e-3 / it, u_ns * 1e-3 / it, it);
+        }
+        if (status[0]) {
+            const int f = status[2];
+            c->failed_step = f;
+            c->failed_scen = status[3];
+            c->failed_relres = status[0] == 1 ? frel : NAN;
+            c->cur = (c->cur + f) & 1;
+            c->steps_done += f;
+            c->hist = 0;
+            c->last_nsteps = f;
+            if (status[0] == 2)
+                return fail(c, THERMO_EGEOM, "interface row capacity exceeded at step " + std::to_string(f));
+            char buf[160];
+            snprintf(buf, sizeof buf, "CG did not converge at step %d (scenario %d), relres %.3e", f, status[3], frel);
+            return fail(c, THERMO_ENOCONV, buf);
         }
         c->failed_step = -1;
         c->failed_scen = -1;
@@ -1002,7 +1019,7 @@ extern "C" int thermo_get_stats(const void *ctx, thermo_stats *out) {
     out->order_max_runs = c->probe_runs;
     out->order_max_window = c->probe_window;
     out->solve_variant = c->S == 1 ? c->cg_variant : -1;
-    out->solve_kind = c->S == 1 ? c->cg_kind : -1;
+    out->solve_kind = c->S == 1 ? c->cg_kind : (c->sb_on ? 3 : -1);   // 3: batched windowed SpMM
     out->solve_max_runs = c->cg_max_runs;
     out->solve_window = c->cg_win_cap;
     return THERMO_OK;

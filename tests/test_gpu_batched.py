@@ -58,7 +58,9 @@ def test_batched_equals_single_runs(guess):
         ts = Thermo.from_config(cfg, scenarios=[scen[k]])
         ts.set_guess(guess)
         ts.step(0.0, 1.0, 6)
-        assert rel(tb.get_T(scen=k), ts.get_T()) < 1e-12
+        # both stop at rtol 1e-12; the reduction trees differ (and so may the last iteration
+        # count), so they agree to the solver tolerance, not bitwise (reading R17)
+        assert rel(tb.get_T(scen=k), ts.get_T()) < 1e-11
 
 
 def test_cfg4_sampled_scenarios():
