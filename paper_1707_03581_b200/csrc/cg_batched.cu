@@ -556,7 +556,7 @@ int cgb_setup(Ctx &c) {
 }
 
 int cgb_prepare(Ctx &c) {
-    if (c.sb_on) return 0;   // the SpMM kernel reads the volume D^{-1} and the interface rows' own
+    if (c.sb_on) return sbcg_prepare(c);   // row-major copy of the rebuilt operator (cg_spmm.cu)
     const int64_t n = c.N * c.SP;
     k_dinv_broadcast<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(c.d_Dinv, c.N, c.S, c.SP, c.d_DinvS);
     CK(cudaGetLastError());

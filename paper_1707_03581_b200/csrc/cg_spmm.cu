@@ -60,7 +60,8 @@ namespace thermo {
 #define SB_NCW 8                        // consumer warps
 #define SB_RPW (32 / SB_NCW)            // rows of a slice per consumer warp (two per half-warp pass)
 #define SB_NPW 2                        // producer warps (chunks k = p mod 2; ring slots likewise)
-#define SB_THREADS ((SB_NCW + SB_NPW) * 32)
+#define SB_NIW 2                        // interface warps (gather the interface rows during the sweep)
+#define SB_THREADS ((SB_NCW + SB_NPW + SB_NIW) * 32)
 #define SB_NV 7                         // reduction values per column (S phase)
 #define SB_MAXS 64
 #define SB_M (SB_NV * SB_MAXS)          // partial slots per CTA
@@ -74,14 +75,16 @@ struct SBParams {
     int S, SP, CW, G;
     int Gw;                        // CTAs working in the sweeps: (grid / G) * G; CTA b -> group b % G
     const int64_t *slice_ptr;
-    const uint16_t *lcol;          // window-local columns (W = 1 chunks)
-    const double *val;
+    const uint16_t *lcol;          // window-local columns, row-major per slice (sbcg_prepare)
+    const double *val;             // K~_vol values, row-major per slice: [32 rows][w8] (w8 = width
+                                   // rounded up to 8, padding: value 0, column = the row itself)
     const struct SBRec *recs;      // per CTA, in sweep order: the chunk metadata (host-packed)
     const int32_t *rec_ptr;        // [Gw + 1]
     const double *ML, *benv, *Dinv;
     const int32_t *if_of_row;      // [nslices * 32] interface index of a row, -1 if none
     const int32_t *if_rows;        // [n_if] row of each interface node
     const int32_t *if_cta_ptr, *if_cta_k;   // [Gw + 1] / list: interface rows in the slices of CTA b
+    double *ai;                    // [list][SB_CW] interface sums of the current sweep
     int n_if, nA, cap;
     const int32_t *ell_cnt, *ell_col;
     const double *ell_val, *if_b, *if_phi, *if_d, *if_dinv;   // [k][c][s] / [k][s]
@@ -97,6 +100,7 @@ struct SBParams {
     int maxit, step;
     int nstages;
     uint32_t stage_bytes, col_off, win_off, own_off, aux_off;
+    uint32_t meta_off;             // metadata batch buffers (after the ring and the reduction scratch)
     unsigned long long *trace;
     int trace_fine;   // THERMO_CG_TRACE=3: stamps after the sweep, the interface pass, the CTA
                       // partials and the first grid barrier of every reduction (CTA 0)
@@ -115,6 +119,7 @@ struct SBRing {
     uint64_t *mbar;     // [2] metadata batch buffers
     SBRec *meta;        // [2][SB_RB]
     uint32_t mph;       // phase bits of mbar[0..1]
+    int *ictr;          // interface units claimed in this sweep (sb_iface_gather)
 };
 
 // Metadata of one chunk (one slice of the CTA's column group), packed on the host per CTA in
@@ -137,6 +142,66 @@ struct SBRow {
     int64_t i;
 };
 
+// Interface rows of this CTA's slices (its own column group), in two parts:
+//  * gather (the SB_NIW interface warps, during the sweep): ai = sum_e val_e w[col_e] of every
+//    (interface row, column), two rows in flight per half-warp, every load of a round issued
+//    before the next dependent round (count; entries; gathers) -> P.ai;
+//  * finish (all warps, after the sweep): body(k, i, g, l, ai) adds the volume part the sweep
+//    stored for the row and completes it.
+__device__ __forceinline__ void sb_iface_gather(const SBParams &P, const double *w, int *ctr) {
+    // units (interface rows of the CTA's list) are claimed four at a time per warp from a
+    // shared counter: the interface warps start during the sweep, every warp helps after it.
+    // Each unit's sum has a fixed order (the entries'), so the values are reproducible; only
+    // which warp computes them varies.
+    const int lane = threadIdx.x & 31, h = lane >> 4, l = lane & 15;
+    const int g = blockIdx.x % P.G;
+    const int j0 = P.if_cta_ptr[blockIdx.x], j1 = P.if_cta_ptr[blockIdx.x + 1];
+    const int sc = g * P.CW + l;
+    const bool col = l < P.CW && sc < P.S;
+    while (true) {   // warp-uniform: the warp claims four units, two per half-warp
+        int jb = 0;
+        if (lane == 0) jb = j0 + atomicAdd(ctr, 4);
+        jb = __shfl_sync(0xffffffffu, jb, 0);
+        if (jb >= j1) break;
+        const int j = jb + 2 * h;
+        int k[2], cnt[2];
+        double a[2] = {0.0, 0.0};
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            k[u] = j + u < j1 ? P.if_cta_k[j + u] : -1;
+            cnt[u] = (k[u] >= 0 && col) ? P.ell_cnt[(int64_t)k[u] * P.S + sc] : 0;
+        }
+        const int cmax = max(cnt[0], cnt[1]);
+        for (int c0 = 0; c0 < cmax; c0 += 8) {
+            int jc[2][8];
+            double v[2][8], y[2][8];
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const int ce = min(c0 + e, max(cnt[u] - 1, 0));
+                    const int64_t ix = ((int64_t)max(k[u], 0) * P.cap + ce) * P.S + (col ? sc : 0);
+                    jc[u][e] = cnt[u] ? P.ell_col[ix] : 0;
+                    v[u][e] = cnt[u] ? P.ell_val[ix] : 0.0;
+                }
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+#pragma unroll
+                for (int e = 0; e < 8; ++e) y[u][e] = cnt[u] ? ld_cg1(w + brow(P, g, jc[u][e]) + l) : 0.0;
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+#pragma unroll
+                for (int e = 0; e < 8; ++e)
+                    if (c0 + e < cnt[u]) a[u] = fma(v[u][e], y[u][e], a[u]);
+        }
+        if (l < P.CW) {
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+                if (k[u] >= 0) P.ai[(int64_t)(j + u) * SB_CW + l] = a[u];
+        }
+    }
+}
+
 // One sweep over the slices of this CTA's column group g = b % G (slices b / G + k Gw / G,
 // a static order).  Stage = [hdr | values | 16-bit window columns | window of w (runs) | own
 // rows of ownv | D^{-1} of the slice's rows | interface index of the slice's rows].  Consumers
@@ -151,6 +216,11 @@ __device__ __forceinline__ void sb_sweep(const SBParams &P, SBRing &R, const dou
     if ((int)blockIdx.x >= P.Gw) return;
     const int g = blockIdx.x % P.G;
     const uint32_t base = R.n;   // ring slot of this sweep's chunk 0 (the same in every warp)
+    if (warp >= SB_NCW + SB_NPW) {   // ---------------- interface warps
+        if (P.n_if) sb_iface_gather(P, w, R.ictr);
+        R.n = base + (uint32_t)(P.rec_ptr[2 * blockIdx.x + 2] - P.rec_ptr[2 * blockIdx.x]) + 1u;
+        return;
+    }
     if (warp >= SB_NCW) {   // ---------------- producers: warp SB_NCW + p takes chunks k = p (mod 2)
         const int pw = warp - SB_NCW;
         const int r0i = P.rec_ptr[2 * blockIdx.x + pw], r1i = P.rec_ptr[2 * blockIdx.x + pw + 1];
@@ -278,25 +348,35 @@ __device__ __forceinline__ void sb_sweep(const SBParams &P, SBRing &R, const dou
             ok_[pp] = x.i < P.N && lok && !(P.debug & 1);
         }
         if (ok_[0] || ok_[1]) {
+            // wd = row width rounded to 8 (row-major slice): per block of 8 entries one 16-byte
+            // broadcast load of the columns and four of the values per row
             for (int k = 0; k < wd; k += 8) {
-                int cc[SB_RPW / 2][8];
-                double vv[SB_RPW / 2][8], yy[SB_RPW / 2][8];
+                uint4 cq[SB_RPW / 2];
+                double2 vq[SB_RPW / 2][4];
+                double yy[SB_RPW / 2][8];
 #pragma unroll
-                for (int pp = 0; pp < SB_RPW / 2; ++pp)
+                for (int pp = 0; pp < SB_RPW / 2; ++pp) {
+                    const int e = rr_[pp] * wd + k;
+                    cq[pp] = *reinterpret_cast<const uint4 *>(lc + e);
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) vq[pp][u] = reinterpret_cast<const double2 *>(vals + e)[u];
+                }
+#pragma unroll
+                for (int pp = 0; pp < SB_RPW / 2; ++pp) {
+                    const uint32_t w4[4] = {cq[pp].x, cq[pp].y, cq[pp].z, cq[pp].w};
 #pragma unroll
                     for (int u = 0; u < 8; ++u) {
-                        const int e = 32 * min(k + u, wd - 1) + rr_[pp];
-                        cc[pp][u] = lc[e];
-                        vv[pp][u] = k + u < wd ? vals[e] : 0.0;
+                        const int cidx = (int)((w4[u >> 1] >> (16 * (u & 1))) & 0xffffu);
+                        yy[pp][u] = win[cidx * P.CW + l];
                     }
+                }
 #pragma unroll
                 for (int pp = 0; pp < SB_RPW / 2; ++pp)
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) yy[pp][u] = win[cc[pp][u] * P.CW + l];
-#pragma unroll
-                for (int pp = 0; pp < SB_RPW / 2; ++pp)
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) rw[pp].acc = fma(vv[pp][u], yy[pp][u], rw[pp].acc);
+                    for (int u = 0; u < 4; ++u) {
+                        rw[pp].acc = fma(vq[pp][u].x, yy[pp][2 * u], rw[pp].acc);
+                        rw[pp].acc = fma(vq[pp][u].y, yy[pp][2 * u + 1], rw[pp].acc);
+                    }
             }
         }
 #pragma unroll
@@ -307,7 +387,7 @@ __device__ __forceinline__ void sb_sweep(const SBParams &P, SBRing &R, const dou
                 x.pw = win[(lown + r) * P.CW + l];
                 x.own = own[r * P.CW + l];
                 x.dinv = dv[r];
-                x.diag = vals[r];
+                x.diag = vals[r * wd];   // entry 0 of the row: the diagonal
                 x.ik = ifr[r];
             }
         }
@@ -320,62 +400,25 @@ __device__ __forceinline__ void sb_sweep(const SBParams &P, SBRing &R, const dou
     }
 }
 
-// Interface rows of this CTA's slices (its own column group), after its volume sweep: a
-// half-warp per (interface row, column), two rows in flight, every load of a row issued before
-// the next dependent round (count; entries; gathers).  body(k, i, g, l, iface_sum) finishes the
-// row; the sweep stored the row's volume part for it.
 template <class Body>
-__device__ __forceinline__ void sb_iface_pass(const SBParams &P, const double *w, Body &&body) {
+__device__ __forceinline__ void sb_iface_finish(const SBParams &P, const double *w, int *ctr, Body &&body) {
     if ((int)blockIdx.x >= P.Gw || !P.n_if) return;
-    __syncthreads();   // the sweep's stores of this CTA's volume parts are visible
+    sb_iface_gather(P, w, ctr);   // the units the interface warps have not claimed yet
+    __syncthreads();   // the sweep's volume parts and the gathered interface sums are visible
+    if (threadIdx.x == 0) *ctr = 0;   // for the next sweep (after the reduction's barriers)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int h = lane >> 4, l = lane & 15;
     if (l >= P.CW) return;
     const int g = blockIdx.x % P.G;
     const int j0 = P.if_cta_ptr[blockIdx.x], j1 = P.if_cta_ptr[blockIdx.x + 1];
     const int nhw = 2 * (blockDim.x >> 5), hw = 2 * warp + h;
-    const int sc = g * P.CW + l;
-    const bool col = sc < P.S;
-    for (int j = j0 + hw; j < j1; j += 2 * nhw) {
-        int k[2], i[2], cnt[2];
-        double a[2] = {0.0, 0.0};
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-            const int jj = j + u * nhw;
-            k[u] = jj < j1 ? P.if_cta_k[jj] : -1;
-            i[u] = k[u] >= 0 ? P.if_rows[k[u]] : 0;
-            cnt[u] = (k[u] >= 0 && col) ? P.ell_cnt[(int64_t)k[u] * P.S + sc] : 0;
-        }
-        const int cmax = max(cnt[0], cnt[1]);
-        for (int c0 = 0; c0 < cmax; c0 += 8) {
-            int jc[2][8];
-            double v[2][8], y[2][8];
-#pragma unroll
-            for (int u = 0; u < 2; ++u)
-#pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    const int ce = min(c0 + e, max(cnt[u] - 1, 0));
-                    const int64_t ix = ((int64_t)max(k[u], 0) * P.cap + ce) * P.S + (col ? sc : 0);
-                    jc[u][e] = cnt[u] ? P.ell_col[ix] : 0;
-                    v[u][e] = cnt[u] ? P.ell_val[ix] : 0.0;
-                }
-#pragma unroll
-            for (int u = 0; u < 2; ++u)
-#pragma unroll
-                for (int e = 0; e < 8; ++e) y[u][e] = ld_cg1(w + brow(P, g, jc[u][e]) + l);
-#pragma unroll
-            for (int u = 0; u < 2; ++u)
-#pragma unroll
-                for (int e = 0; e < 8; ++e)
-                    if (c0 + e < cnt[u]) a[u] = fma(v[u][e], y[u][e], a[u]);
-        }
-#pragma unroll
-        for (int u = 0; u < 2; ++u)
-            if (k[u] >= 0) body(k[u], (int64_t)i[u], g, l, a[u]);
+    for (int j = j0 + hw; j < j1; j += nhw) {
+        const int k = P.if_cta_k[j];
+        body(k, (int64_t)P.if_rows[k], g, l, ld_cg1(P.ai + (int64_t)j * SB_CW + l));
     }
 }
 
-// CTA sums of NV values per column (lane (h, l) of a consumer warp holds column g * CW + l of its
+// CTA sums of NV values per column (lane (h, l) of every warp holds column g * CW + l of its
 // CTA's group in acc[v]; both halves) -> partials[cta][v * 64 + column]; grid barrier; the total
 // of every (v, column) by one warp, over the CTAs of the column's group in a fixed order
 // (distributed over the grid); grid barrier; totals -> tot (every CTA the same bits).
@@ -390,17 +433,16 @@ __device__ __forceinline__ void sb_reduce(const SBParams &P, const double (&acc)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int M = NV * SB_MAXS;
     __syncthreads();   // the ring is idle: red aliases its stages
-    if (warp < SB_NCW) {
+    const int nwb = blockDim.x >> 5;   // every warp: the consumers' rows and the interface rows
 #pragma unroll
-        for (int v = 0; v < NV; ++v) red[(warp * NV + v) * 32 + lane] = acc[v];
-    }
+    for (int v = 0; v < NV; ++v) red[(warp * NV + v) * 32 + lane] = acc[v];
     __syncthreads();
     if ((int)blockIdx.x < P.Gw) {
         const int g = blockIdx.x % P.G;
         for (int j = threadIdx.x; j < NV * P.CW; j += blockDim.x) {
             const int v = j / P.CW, l = j - v * P.CW;
             double x = 0.0;
-            for (int w = 0; w < SB_NCW; ++w) x += red[(w * NV + v) * 32 + l] + red[(w * NV + v) * 32 + 16 + l];
+            for (int w = 0; w < nwb; ++w) x += red[(w * NV + v) * 32 + l] + red[(w * NV + v) * 32 + 16 + l];
             P.partials[(int64_t)blockIdx.x * SB_M + v * SB_MAXS + g * P.CW + l] = x;
         }
     }
@@ -424,14 +466,14 @@ __device__ __forceinline__ void sb_reduce(const SBParams &P, const double (&acc)
     __syncthreads();
 }
 
-// 10 warps: <= 168 registers (3 warps on one SM sub-partition)
+// 12 warps: <= 168 registers (3 warps on each SM sub-partition)
 __global__ void __launch_bounds__(SB_THREADS, 1) k_sbcg_step(SBParams P) {
     extern __shared__ __align__(128) unsigned char sb_smem[];
     __shared__ uint64_t bar_full[SB_MAXSTAGES], bar_empty[SB_MAXSTAGES], bar_meta[2 * SB_NPW];
     __shared__ double s_tot[SB_M];
     __shared__ double s_alpha[SB_MAXS], s_beta[SB_MAXS], s_rho[SB_MAXS], s_rr[SB_MAXS], s_tol2[SB_MAXS],
         s_bb[SB_MAXS];
-    __shared__ int s_conv[SB_MAXS], s_itc[SB_MAXS], s_any;
+    __shared__ int s_conv[SB_MAXS], s_itc[SB_MAXS], s_any, s_ictr;
     // an earlier step failed, or the interface of this or an earlier step overflowed
     if (P.status[0] || (P.status[1] && P.status[4] <= P.step)) {
         if (!P.status[0] && blockIdx.x == 0 && threadIdx.x == 0) {
@@ -448,11 +490,12 @@ __global__ void __launch_bounds__(SB_THREADS, 1) k_sbcg_step(SBParams P) {
             mbar_init(&bar_empty[k], SB_NCW);
         }
         for (int k = 0; k < 2 * SB_NPW; ++k) mbar_init(&bar_meta[k], 1);
+        s_ictr = 0;
         fence_mbar_init();
     }
     __syncthreads();
     SBRing R{bar_full, bar_empty, sb_smem, 0u, bar_meta,
-             reinterpret_cast<SBRec *>(sb_smem + (size_t)P.nstages * P.stage_bytes), 0u};
+             reinterpret_cast<SBRec *>(sb_smem + P.meta_off), 0u, &s_ictr};
     double *red = reinterpret_cast<double *>(sb_smem);   // aliases the ring between sweeps
     const bool tr_on = P.trace && blockIdx.x == 0 && threadIdx.x == 0;
     int ntr = 0;
@@ -481,7 +524,7 @@ __global__ void __launch_bounds__(SB_THREADS, 1) k_sbcg_step(SBParams P) {
             if (x.ik >= 0) P.z[brow(P, g, x.i) + l] = x.acc;   // volume part; finished by the interface pass
             else fin0(x.i, g, l, x.acc, x.own, 0.0, x.dinv);
         });
-        sb_iface_pass(P, x0, [&](int k, int64_t i, int g, int l, double ai) {
+        sb_iface_finish(P, x0, &s_ictr, [&](int k, int64_t i, int g, int l, double ai) {
             const int sc = g * P.CW + l;
             const int64_t e = brow(P, g, i) + l;
             const double ax = ld_cg1(P.z + e) + ai, Ti = ld_cg1(P.T_in + e);
@@ -541,7 +584,7 @@ __global__ void __launch_bounds__(SB_THREADS, 1) k_sbcg_step(SBParams P) {
                 else finS(x.i, g, l, x.acc, x.pw, x.own, x.diag, x.dinv);
             });
             sb_stamp(P, ntr);
-            sb_iface_pass(P, P.p, [&](int k, int64_t i, int g, int l, double ai) {
+            sb_iface_finish(P, P.p, &s_ictr, [&](int k, int64_t i, int g, int l, double ai) {
                 const int sc = g * P.CW + l;
                 const int64_t e = brow(P, g, i) + l;
                 const double qv = ld_cg1(P.q + e) + ai, pi = ld_cg1(P.p + e), zz = ld_cg1(P.z + e);
@@ -635,6 +678,30 @@ __global__ void __launch_bounds__(SB_THREADS, 1) k_sbcg_step(SBParams P) {
     }
 }
 
+// Row-major copy of each slice of the sliced-ELL operator (after every rebuild of K~_vol):
+// entry k of row r at ptr8[s] + r w8 + k; padding entries: value 0, the row's own window slot.
+__global__ void k_sb_rowmajor(const int64_t *__restrict__ sp, const int64_t *__restrict__ sp8,
+                              const double *__restrict__ val, const uint16_t *__restrict__ lcol,
+                              const int32_t *__restrict__ lown, int64_t nslices, double *__restrict__ val8,
+                              uint16_t *__restrict__ lcol8) {
+    const int64_t s = blockIdx.x;
+    if (s >= nslices) return;
+    const int w = (int)((sp[s + 1] - sp[s]) / 32), w8 = (int)((sp8[s + 1] - sp8[s]) / 32);
+    for (int t = threadIdx.x; t < 32 * w8; t += blockDim.x) {
+        const int r = t / w8, k = t - r * w8;
+        const int64_t src = sp[s] + 32 * (int64_t)k + r;
+        val8[sp8[s] + t] = k < w ? val[src] : 0.0;
+        lcol8[sp8[s] + t] = k < w ? lcol[src] : (uint16_t)(lown[s] + r);
+    }
+}
+
+int sbcg_prepare(Ctx &c) {
+    k_sb_rowmajor<<<(unsigned)c.nslices, 128, 0, c.stream>>>(c.d_slice_ptr, c.d_sb_ptr8, c.d_val, c.d_lcol,
+                                                              c.d_chunk_lown, c.nslices, c.d_sb_val8, c.d_sb_lcol8);
+    CK(cudaGetLastError());
+    return 0;
+}
+
 // ---------------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------------
@@ -672,8 +739,15 @@ int sbcg_setup(Ctx &c) {
         if (verbose) fprintf(stderr, "[thermo cgb] windows do not fit (runs %d, flags %d): gather kernel\n", stats[1], stats[2]);
         return 0;
     }
+    // row-major copy of the matrix per slice, widths rounded up to 8 (sbcg_prepare fills it)
+    std::vector<int64_t> sp8(c.nslices + 1, 0);
+    for (int64_t s = 0; s < c.nslices; ++s) sp8[s + 1] = sp8[s] + 32 * (((sp[s + 1] - sp[s]) / 32 + 7) & ~(int64_t)7);
     int64_t emax = 0;
-    for (int64_t s = 0; s < c.nslices; ++s) emax = std::max(emax, sp[s + 1] - sp[s]);
+    for (int64_t s = 0; s < c.nslices; ++s) emax = std::max(emax, sp8[s + 1] - sp8[s]);
+    CK(cudaMalloc(&c.d_sb_ptr8, sizeof(int64_t) * (c.nslices + 1)));
+    CK(cudaMemcpy(c.d_sb_ptr8, sp8.data(), sizeof(int64_t) * (c.nslices + 1), cudaMemcpyHostToDevice));
+    CK(cudaMalloc(&c.d_sb_val8, sizeof(double) * (size_t)(sp8[c.nslices] + 1)));
+    CK(cudaMalloc(&c.d_sb_lcol8, sizeof(uint16_t) * (size_t)(sp8[c.nslices] + 8)));
     const int wc = (stats[0] + 2) & ~1;
     const size_t col_off = a16(SB_HDR + (size_t)emax * 8);
     const size_t win_off = a16(col_off + (size_t)emax * 2);
@@ -684,9 +758,10 @@ int sbcg_setup(Ctx &c) {
     int ns = (int)std::min<size_t>(SB_MAXSTAGES, budget / stage);
     if (const char *e = getenv("THERMO_CGB_STAGES")) ns = std::min(ns, std::max(2, atoi(e)));
     ns -= ns % SB_NPW;   // every ring slot belongs to one producer
-    // the reduction scratch aliases the ring: SB_NCW x 7 x 32 doubles; two metadata batch buffers
-    // follow the ring
-    const size_t smem = std::max((size_t)ns * stage, (size_t)SB_NCW * SB_NV * 32 * 8) + 2 * SB_NPW * SB_RB * sizeof(SBRec);
+    // the reduction scratch aliases the ring: (all warps) x 7 x 32 doubles; the metadata batch
+    // buffers follow the ring
+    const size_t meta_off = a16(std::max((size_t)ns * stage, (size_t)(SB_THREADS / 32) * SB_NV * 32 * 8));
+    const size_t smem = meta_off + 2 * SB_NPW * SB_RB * sizeof(SBRec);
     if (ns < 2) {
         if (verbose) fprintf(stderr, "[thermo cgb] stage %zu B too large: gather kernel\n", stage);
         return 0;
@@ -714,6 +789,7 @@ int sbcg_setup(Ctx &c) {
             ptr[b + 1] = ptr[b] + (int32_t)lists[b].size();
             ks.insert(ks.end(), lists[b].begin(), lists[b].end());
         }
+        CK(cudaMalloc(&c.d_sb_ai, sizeof(double) * SB_CW * (ks.size() + 1)));
         CK(cudaMalloc(&c.d_sb_if_ptr, sizeof(int32_t) * (Gw + 1)));
         CK(cudaMalloc(&c.d_sb_if_k, sizeof(int32_t) * (ks.size() + 1)));
         CK(cudaMemcpy(c.d_sb_if_ptr, ptr.data(), sizeof(int32_t) * (Gw + 1), cudaMemcpyHostToDevice));
@@ -735,8 +811,8 @@ int sbcg_setup(Ctx &c) {
                     if (k % SB_NPW != pw) continue;
                     SBRec r;
                     memset(&r, 0, sizeof r);
-                    r.e0 = sp[sl];
-                    r.cnt = (int)(sp[sl + 1] - sp[sl]);
+                    r.e0 = sp8[sl];
+                    r.cnt = (int)(sp8[sl + 1] - sp8[sl]);
                     r.lown = lo[sl];
                     r.nruns = nr[sl];
                     r.s = (int)sl;
@@ -761,6 +837,7 @@ int sbcg_setup(Ctx &c) {
     c.sb_col_off = (uint32_t)col_off;
     c.sb_win_off = (uint32_t)win_off;
     c.sb_own_off = (uint32_t)own_off;
+    c.sb_meta_off = (uint32_t)meta_off;
     c.sb_aux_off = (uint32_t)aux_off;
     c.sb_nstages = ns;
     c.sb_smem = smem;
@@ -785,8 +862,8 @@ int sbcg_launch_step(Ctx &c, int step, double dt, const double *x0) {
     P.G = c.sb_G;
     P.Gw = (c.cg_grid / P.G) * P.G;
     P.slice_ptr = c.d_slice_ptr;
-    P.lcol = c.d_lcol;
-    P.val = c.d_val;
+    P.lcol = c.d_sb_lcol8;
+    P.val = c.d_sb_val8;
     P.recs = (const SBRec *)c.d_sb_recs;
     P.rec_ptr = c.d_sb_rec_ptr;
     P.ML = c.d_ML;
@@ -796,6 +873,7 @@ int sbcg_launch_step(Ctx &c, int step, double dt, const double *x0) {
     P.if_rows = c.d_if_rows;
     P.if_cta_ptr = c.d_sb_if_ptr;
     P.if_cta_k = c.d_sb_if_k;
+    P.ai = c.d_sb_ai;
     P.n_if = c.n_if;
     P.nA = c.nA;
     P.cap = c.cap;
@@ -828,6 +906,7 @@ int sbcg_launch_step(Ctx &c, int step, double dt, const double *x0) {
     P.col_off = c.sb_col_off;
     P.win_off = c.sb_win_off;
     P.own_off = c.sb_own_off;
+    P.meta_off = c.sb_meta_off;
     P.debug = getenv("THERMO_CGB_DEBUG") ? atoi(getenv("THERMO_CGB_DEBUG")) : 0;
     P.aux_off = c.sb_aux_off;
     P.trace = c.d_trace;

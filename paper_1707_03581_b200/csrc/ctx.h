@@ -172,12 +172,16 @@ struct Ctx {
     // windowed SpMM batched kernel (cg_spmm.cu)
     bool sb_on = false;
     int sb_G = 1, sb_nstages = 0;
-    uint32_t sb_stage = 0, sb_col_off = 0, sb_win_off = 0, sb_own_off = 0, sb_aux_off = 0;
+    uint32_t sb_stage = 0, sb_col_off = 0, sb_win_off = 0, sb_own_off = 0, sb_aux_off = 0, sb_meta_off = 0;
     size_t sb_smem = 0;
     double *d_sb_partials = nullptr, *d_sb_totals = nullptr;
     int32_t *d_sb_if_ptr = nullptr, *d_sb_if_k = nullptr;   // interface rows per CTA
     void *d_sb_recs = nullptr;                              // packed chunk metadata per CTA
     int32_t *d_sb_rec_ptr = nullptr;
+    double *d_sb_ai = nullptr;                              // interface sums of a sweep
+    int64_t *d_sb_ptr8 = nullptr;                           // row-major operator copy per slice
+    double *d_sb_val8 = nullptr;
+    uint16_t *d_sb_lcol8 = nullptr;
 
     // internal numbering (reorder.cu): nullptr / empty = the caller's numbering
     int32_t *d_int_of_ext = nullptr;      // [N] internal index of the caller's node e
@@ -239,6 +243,7 @@ int cgb_launch_step(Ctx &c, int step, double dt, const double *x0 = nullptr);
 // cg_spmm.cu (S > 1: windowed SpMM kernel, selected by cgb_setup when the windows fit)
 int sbcg_setup(Ctx &c);
 int sbcg_launch_step(Ctx &c, int step, double dt, const double *x0);
+int sbcg_prepare(Ctx &c);   // after every rebuild of K~_vol
 
 // reorder.cu (internal numbering, state transfers in the caller's numbering)
 int order_probe(Ctx &c, bool *good, int *max_runs, int *max_window);

@@ -77,7 +77,7 @@ static void free_ctx(Ctx *c) {
                     c->d_pairs_s, c->d_pcnt_s, c->d_star_own, c->d_own_ptr, c->d_own_idx, c->d_x0, c->d_Thist, c->d_z2, c->d_q2,
                     c->d_ell_cnt_b, c->d_ell_col_b, c->d_ell_val_b, c->d_if_b_b, c->d_if_phi_b, c->d_Dinv_b,
                     c->d_step_sc_spec, c->d_spec_status, c->d_int_of_ext, c->d_stage[0], c->d_stage[1],
-                    c->d_if_d, c->d_sb_partials, c->d_sb_totals, c->d_sb_if_ptr, c->d_sb_if_k, c->d_sb_recs, c->d_sb_rec_ptr};
+                    c->d_if_d, c->d_sb_partials, c->d_sb_totals, c->d_sb_if_ptr, c->d_sb_if_k, c->d_sb_recs, c->d_sb_rec_ptr, c->d_sb_ptr8, c->d_sb_val8, c->d_sb_lcol8, c->d_sb_ai};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     for (cudaEvent_t e : c->events) cudaEventDestroy(e);

@@ -61,6 +61,10 @@ def test_batched_equals_single_runs(guess):
         # both stop at rtol 1e-12; the reduction trees differ (and so may the last iteration
         # count), so they agree to the solver tolerance, not bitwise (reading R17)
         assert rel(tb.get_T(scen=k), ts.get_T()) < 1e-11
+        # same CG iterations per step (+-1): the batched dot products are those of column k
+        ib = tb.step_iters().reshape(6, -1)[:, k]
+        isg = ts.step_iters().reshape(6, -1)[:, 0]
+        assert np.abs(ib.astype(int) - isg.astype(int)).max() <= 1, (ib, isg)
 
 
 def test_cfg4_sampled_scenarios():
