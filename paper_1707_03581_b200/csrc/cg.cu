@@ -694,6 +694,7 @@ __global__ void __launch_bounds__(cg_threads(KIND, W, NG), KIND == 0 ? 2 : 1) k_
     });
     P.ownv = nullptr;
     cta_reduce_store<4>(red0, red_smem, P.partials, 0);
+    fence_proxy_async_global();   // plain stores before the next TMA reads
     grid.sync();
     if (tr_on) P.trace[ntr++] = gtimer();
     double tot0[4];
@@ -778,6 +779,7 @@ __global__ void __launch_bounds__(cg_threads(KIND, W, NG), KIND == 0 ? 2 : 1) k_
             const int slot = 4 + 7 * sn;
             cta_reduce_store<7>(red, red_smem, P.partials, slot);
             if (fine && ntr < 1000) P.trace[ntr++] = gtimer();
+            fence_proxy_async_global();   // plain stores before the next TMA reads
             grid.sync();
             if (tr_on && ntr < 1000) P.trace[ntr++] = gtimer();
             double t7[7];
@@ -841,6 +843,7 @@ __global__ void __launch_bounds__(cg_threads(KIND, W, NG), KIND == 0 ? 2 : 1) k_
             });
             P.ownv = nullptr;
             cta_reduce_store<7>(red, red_smem, P.partials, 4);
+            fence_proxy_async_global();   // plain stores before the next TMA reads
             grid.sync();
             if (tr_on && ntr < 1000) P.trace[ntr++] = gtimer();
             double t7[7];
@@ -901,6 +904,7 @@ __global__ void __launch_bounds__(cg_threads(KIND, W, NG), KIND == 0 ? 2 : 1) k_
                     p[i] = fma(beta, p[i], zn);
                 }
             }
+            fence_proxy_async_global();   // plain stores before the next TMA reads
             grid.sync();
             if (tr_on && ntr < 1000) P.trace[ntr++] = gtimer();
             rho = rz_new;

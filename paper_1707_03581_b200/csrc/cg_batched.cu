@@ -102,11 +102,11 @@ __device__ __forceinline__ void cgb_reduce(double (&v)[NV][2], double *sm, doubl
         for (; g + 8 <= G; g += 8) {   // loads issued together, adds in the serial order
             double v[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) v[u] = partials[(int64_t)(g + u) * CGB_NV * 64 + t];
+            for (int u = 0; u < 8; ++u) v[u] = ld_cg1(partials + (int64_t)(g + u) * CGB_NV * 64 + t);   // L2, not a stale L1 line
 #pragma unroll
             for (int u = 0; u < 8; ++u) a += v[u];
         }
-        for (; g < G; ++g) a += partials[(int64_t)g * CGB_NV * 64 + t];
+        for (; g < G; ++g) a += ld_cg1(partials + (int64_t)g * CGB_NV * 64 + t);
         sm[t] = a;
     }
     __syncthreads();

@@ -57,6 +57,13 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// order this thread's generic-proxy global writes before async-proxy (TMA bulk copy) reads of the
+// same memory issued after a later barrier (every grid barrier after which vectors written by
+// plain stores are streamed by cp.async.bulk)
+__device__ __forceinline__ void fence_proxy_async_global() {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 __device__ __forceinline__ double2 ld_cg2(const double2 *p) {
     double2 v;
     asm volatile("ld.global.cg.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
@@ -168,7 +175,7 @@ __device__ __forceinline__ void grid_total(const double *partials, int G, int sl
         for (; g0 + 32 * 8 <= G; g0 += 32 * 8) {
             double a[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) a[u] = partials[(g0 + 32 * u + lane) * THERMO_NRED + slot + j];
+            for (int u = 0; u < 8; ++u) a[u] = ld_cg1(partials + (g0 + 32 * u + lane) * THERMO_NRED + slot + j);
 #pragma unroll
             for (int u = 0; u < 8; ++u) x += a[u];
         }
@@ -176,7 +183,9 @@ __device__ __forceinline__ void grid_total(const double *partials, int G, int sl
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             const int g = g0 + 32 * u + lane;
-            a[u] = g < G ? partials[g * THERMO_NRED + slot + j] : 0.0;
+            // through L2: the partials are rewritten by other CTAs every reduction of the launch, and an
+            // L1 line of this SM could still hold the previous reduction's value
+            a[u] = g < G ? ld_cg1(partials + g * THERMO_NRED + slot + j) : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) x += a[u];

@@ -220,7 +220,9 @@ extern "C" int thermo_create_mesh(void **out, const thermo_mesh *fixed, const th
             c->nm = hm.nm;
             c->N = c->nf + c->nm;
             c->S = n_scen;
-            c->SP = n_scen == 1 ? 1 : (n_scen + 1) & ~1;
+            // scenario columns: even (16-byte rows); above 16 a multiple of 16 (the column groups of
+            // the windowed SpMM kernel, cg_spmm.cu)
+            c->SP = n_scen == 1 ? 1 : n_scen > 16 ? (n_scen + 15) & ~15 : (n_scen + 1) & ~1;
             c->nu = nu;
             c->rho_cp = rho_cp;
             c->alpha = alpha_iface;

@@ -79,3 +79,25 @@ def test_cfg4_sampled_scenarios():
     for k in (0, 37, 63):
         Tr, st = o.step(np.full(o.n, cfg.T0), 0.0, cfg.dt, n, cfg.scenarios[k])
         assert rel(th.get_T(scen=k), Tr) <= TOL, k
+
+
+@pytest.mark.parametrize("S", [3, 20])
+def test_windowed_spmm_kernel_matches_gather_kernel(monkeypatch, S):
+    """The opt-in windowed-SpMM batched kernel (THERMO_CGB=2, cg_spmm.cu: column groups of 16,
+    padding columns for S = 20) against the default gather kernel and the oracle."""
+    from paper_1707_03581_b200.thermo import Thermo
+    cfg = I.make_config("medium", jitter=0.1)
+    scen = [_scen(k) for k in range(S)]
+    out = {}
+    for mode in ("2", "1"):
+        monkeypatch.setenv("THERMO_CGB", mode)
+        th = Thermo.from_config(cfg, scenarios=scen)
+        th.step(0.0, 1.0, 6)
+        if mode == "2":
+            assert th.stats()["solve_kind"] == 3
+        out[mode] = np.stack([th.get_T(scen=k) for k in range(S)])
+    for k in range(S):
+        assert rel(out["2"][k], out["1"][k]) < 1e-11, k
+    for k in (0, S - 1):
+        Tr, _ = O.Oracle.from_config(cfg).step(np.full(cfg.n_dof, cfg.T0), 0.0, 1.0, 6, scen[k])
+        assert rel(out["2"][k], Tr) <= 1e-9
