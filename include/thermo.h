@@ -17,7 +17,14 @@
  * The interface terms are re-integrated every step on the exact intersection of the two
  * non-matching surface triangulations at the stock's current offset, and the
  * coupled system is solved monolithically by Jacobi-preconditioned CG in fp64 until
- * ||b - K~ x||_2 <= rtol ||b||_2 (default 1e-12), from x0 = T^n.
+ * ||b - K~ x||_2 <= rtol ||b||_2 (default 1e-12).  CG starts from the quadratic extrapolation
+ * of the last committed states by default (thermo_set_guess; order 0 = x0 = T^n): the start
+ * changes the iterations, not the system or the stopping rule.
+ *
+ * Node numbering: the caller's numbering (per part, as passed to thermo_create_mesh) is what
+ * every entry point reads and writes.  Internally the library may renumber each part
+ * (reverse Cuthill-McKee) when the caller's numbering does not suit the windowed solve kernel
+ * (thermo_get_stats: reordered); this is invisible at the ABI.
  *
  * Everything runs in hand-written sm_100a CUDA kernels on the caller's stream; there is no
  * CPU fallback.  Several independent scenarios (different motion / friction laws) may be
@@ -41,13 +48,20 @@
 extern "C" {
 #endif
 
+/* Opaque context handle: owns all device memory of one coupled problem (thermo_create_mesh ..
+ * thermo_destroy).  One context per host thread. */
+typedef struct thermo_ctx thermo_ctx;
+
 enum {
     THERMO_OK = 0,
     THERMO_EINVAL = -1,   /* bad argument: sizes, indices, inverted tet, non-planar interface */
     THERMO_ENOMEM = -2,   /* device or host allocation failed */
     THERMO_ECUDA = -3,    /* CUDA runtime error (message has the CUDA error string) */
     THERMO_ENOCONV = -4,  /* CG did not reach rtol within maxit; see thermo_get_stats */
-    THERMO_EGEOM = -5     /* interface capacity exceeded or intersection area inconsistent */
+    THERMO_EGEOM = -5     /* interface storage capacity exceeded.  No check of |Gamma_R| against the
+                             stock-bottom area: a stock overhanging the rail is valid partial
+                             contact (reading R30); |Gamma_R| of every step is
+                             reported (thermo_get_stats: iface_area) */
 };
 
 /* One part's tetrahedral P1 mesh.
@@ -85,7 +99,7 @@ typedef struct {
  *  cuda_stream: a cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream) or NULL for
  *  the legacy default stream; every later call enqueues its work on this stream.
  * On failure *out is NULL; message via thermo_last_error(NULL). */
-int thermo_create_mesh(void **out, const thermo_mesh *fixed, const thermo_mesh *moving,
+int thermo_create_mesh(thermo_ctx **out, const thermo_mesh *fixed, const thermo_mesh *moving,
                        int32_t iface_tag_fixed, int32_t iface_tag_moving,
                        double nu, double rho_cp, double alpha_iface,
                        int32_t n_scen, const thermo_scenario *scen, double T_init,
@@ -97,7 +111,7 @@ int thermo_create_mesh(void **out, const thermo_mesh *fixed, const thermo_mesh *
  * device.  alpha = 0 removes the condition.  For part 1 grad_T must be orthogonal to every
  * scenario's motion direction (b_env of the stock is then time-independent), else EINVAL.
  * Interface tags cannot carry Robin data (EINVAL). */
-int thermo_set_bc(void *ctx, int32_t part, int32_t tag, double alpha, double T_ref,
+int thermo_set_bc(thermo_ctx *ctx, int32_t part, int32_t tag, double alpha, double T_ref,
                   const double grad_T[3]);
 
 /* Advance every scenario by nsteps implicit-Euler steps of size dt from time t:
@@ -106,14 +120,14 @@ int thermo_set_bc(void *ctx, int32_t part, int32_t tag, double alpha, double T_r
  * end to report status.  Returns THERMO_ENOCONV if some scenario's CG did not converge
  * within maxit (steps before the failing one are committed; the failing step and its
  * residual are in thermo_get_stats), THERMO_EGEOM if the interface storage overflowed. */
-int thermo_step(void *ctx, double t, double dt, int32_t nsteps);
+int thermo_step(thermo_ctx *ctx, double t, double dt, int32_t nsteps);
 
 /* Copy the temperature of one scenario and part (0 fixed, 1 moving, -1 both: fixed nodes
  * first) into out[n]; n must equal the node count of the selection (EINVAL otherwise).
  * out_on_device != 0: out is a device pointer (e.g. a torch tensor's data_ptr()), the copy
  * is asynchronous on the context stream.  Otherwise out is host memory and the call
  * synchronises the stream. */
-int thermo_get_T(void *ctx, int32_t scen, int32_t part, double *out, int64_t n,
+int thermo_get_T(thermo_ctx *ctx, int32_t scen, int32_t part, double *out, int64_t n,
                  int32_t out_on_device);
 
 /* Asynchronous variant of thermo_get_T for host memory: enqueues the copy of the current state
@@ -122,20 +136,20 @@ int thermo_get_T(void *ctx, int32_t scen, int32_t part, double *out, int64_t n,
  * overwrite the buffer being copied waits for the copy on the device).  host_out should be
  * pinned (e.g. cudaHostAlloc / a pinned torch tensor) for a real overlap; its contents are valid
  * after thermo_sync().  Same selection rules and errors as thermo_get_T. */
-int thermo_get_T_async(void *ctx, int32_t scen, int32_t part, double *host_out, int64_t n);
+int thermo_get_T_async(thermo_ctx *ctx, int32_t scen, int32_t part, double *host_out, int64_t n);
 
 /* Asynchronous copy of every scenario's whole field (both parts, the caller's numbering) into
  * host_out[n_scen][n_nodes_fixed + n_nodes_moving], scenario-major, as one transfer: the
  * batched state block (N x SP, row-major on the device) is transposed by one kernel on the copy
  * stream into a staging buffer first.  n must equal n_scen * N.  Valid after thermo_sync().
  * EINVAL on a NULL pointer or a wrong n. */
-int thermo_get_T_all_async(void *ctx, double *host_out, int64_t n);
+int thermo_get_T_all_async(thermo_ctx *ctx, double *host_out, int64_t n);
 
 /* Wait for all work of the context: its stream and every pending asynchronous copy. */
-int thermo_sync(void *ctx);
+int thermo_sync(thermo_ctx *ctx);
 
 /* Overwrite the temperature of one scenario and part (same selection rules as get_T). */
-int thermo_set_T(void *ctx, int32_t scen, int32_t part, const double *in, int64_t n,
+int thermo_set_T(thermo_ctx *ctx, int32_t scen, int32_t part, const double *in, int64_t n,
                  int32_t in_on_device);
 
 /* Time-stepping method for thermo_step:
@@ -150,7 +164,7 @@ int thermo_set_T(void *ctx, int32_t scen, int32_t part, const double *in, int64_
  *     at every node of every sweep (reading R29).  Implicit-Euler predictor through
  *     M equidistant no-left nodes; P is ignored.  M = 1 is implicit Euler.
  * EINVAL for other methods, M or P outside [1, 8], K < 0, or methods 1-2 with n_scen > 1. */
-int thermo_set_method(void *ctx, int32_t method, int32_t M, int32_t P, int32_t K);
+int thermo_set_method(thermo_ctx *ctx, int32_t method, int32_t M, int32_t P, int32_t K);
 
 /* Replace the temperature by the stationary state of the machine at rest (the
  * initial data of the paper's 3-D runs; readings R19, R28):
@@ -164,11 +178,11 @@ int thermo_set_method(void *ctx, int32_t method, int32_t M, int32_t P, int32_t K
  * ENOCONV if the solve did not converge (the temperature is then unchanged), EGEOM on
  * interface overflow.  Iterations / residual / |Gamma_R| are reported by thermo_get_stats
  * as a one-step run. */
-int thermo_stationary(void *ctx, double t, int32_t with_interface);
+int thermo_stationary(thermo_ctx *ctx, double t, int32_t with_interface);
 
 /* CG stopping rule ||r||_2 <= rtol ||b||_2 (default 1e-12) and iteration cap
  * (default 0 = min(10 N, 10000)).  EINVAL if rtol <= 0 or maxit < 0. */
-int thermo_set_solver(void *ctx, double rtol, int32_t maxit);
+int thermo_set_solver(thermo_ctx *ctx, double rtol, int32_t maxit);
 
 /* Initial guess x0 of the implicit-Euler CG solves (every scenario of a batched context alike):
  *   order 0:  x0 = T^n (reading R17; what the oracle does);
@@ -180,7 +194,7 @@ int thermo_set_solver(void *ctx, double rtol, int32_t maxit);
  * solve still stops at ||b - K~ x||_2 <= rtol ||b||_2, so results agree with x0 = T^n to the
  * solver tolerance, and the extrapolation saves iterations.
  * EINVAL for other orders. */
-int thermo_set_guess(void *ctx, int32_t order);
+int thermo_set_guess(thermo_ctx *ctx, int32_t order);
 
 /* Inspection / test aid (not needed for stepping): runs the interface kernels of every
  * scenario at time t (stock offset s(t), friction eta(t)) for step size dt, exactly
@@ -196,7 +210,7 @@ int thermo_set_guess(void *ctx, int32_t order);
  * Order of the entries within a row is unspecified.  EINVAL for a bad scenario, dt <= 0,
  * non-finite t or NULL outputs; EGEOM on interface capacity overflow.  The solve data of the
  * next thermo_step are unaffected (it reassembles its own interface). */
-int thermo_get_interface(void *ctx, int32_t scen, double t, double dt, int32_t *rows, int32_t *cnt,
+int thermo_get_interface(thermo_ctx *ctx, int32_t scen, double t, double dt, int32_t *rows, int32_t *cnt,
                          int32_t *col, double *val, double *b);
 
 typedef struct {
@@ -239,18 +253,18 @@ typedef struct {
     int32_t reserved_;
 } thermo_stats;
 
-int thermo_get_stats(const void *ctx, thermo_stats *out);
+int thermo_get_stats(const thermo_ctx *ctx, thermo_stats *out);
 
 /* enable != 0: record CUDA events on the context stream around every interface and solve
  * kernel of thermo_step, so that thermo_get_stats reports ms_iface / ms_solve of the last
  * call (small overhead per step).  Default off. */
-int thermo_set_timing(void *ctx, int32_t enable);
+int thermo_set_timing(thermo_ctx *ctx, int32_t enable);
 
 /* Per-step CG iteration counts of the last thermo_step: out[nsteps * n_scen], step-major. */
-int thermo_get_step_iters(const void *ctx, int32_t *out, int64_t n);
+int thermo_get_step_iters(const thermo_ctx *ctx, int32_t *out, int64_t n);
 
-const char *thermo_last_error(const void *ctx);
-void thermo_destroy(void *ctx);
+const char *thermo_last_error(const thermo_ctx *ctx);
+void thermo_destroy(thermo_ctx *ctx);
 
 #ifdef __cplusplus
 }

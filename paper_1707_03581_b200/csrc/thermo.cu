@@ -171,7 +171,7 @@ static void permute_host_mesh(HostMesh &h, const std::vector<int32_t> &new_to_ol
         for (int32_t &e : *v) e = old_to_new[e];
 }
 
-extern "C" int thermo_create_mesh(void **out, const thermo_mesh *fixed, const thermo_mesh *moving,
+extern "C" int thermo_create_mesh(thermo_ctx **out, const thermo_mesh *fixed, const thermo_mesh *moving,
                                   int32_t iface_tag_fixed, int32_t iface_tag_moving, double nu,
                                   double rho_cp, double alpha_iface, int32_t n_scen,
                                   const thermo_scenario *scen, double T_init, void *cuda_stream) {
@@ -299,7 +299,7 @@ extern "C" int thermo_create_mesh(void **out, const thermo_mesh *fixed, const th
             }
             if (!rc && cudaStreamSynchronize(c->stream) != cudaSuccess) { c->err = "CUDA error during create"; rc = -3; }
             if (rc) { g_create_err = c->err; free_ctx(c); return THERMO_ECUDA; }
-            *out = c;
+            *out = reinterpret_cast<thermo_ctx *>(c);
             return THERMO_OK;
         } catch (const std::exception &e) {
             g_create_err = std::string("exception: ") + e.what();
@@ -311,7 +311,7 @@ extern "C" int thermo_create_mesh(void **out, const thermo_mesh *fixed, const th
     return THERMO_ECUDA;
 }
 
-extern "C" int thermo_set_bc(void *ctx, int32_t part, int32_t tag, double alpha, double T_ref,
+extern "C" int thermo_set_bc(thermo_ctx *ctx, int32_t part, int32_t tag, double alpha, double T_ref,
                              const double grad_T[3]) {
     Ctx *c = (Ctx *)ctx;
     if (!c) return THERMO_EINVAL;
@@ -372,7 +372,7 @@ __global__ void k_stat_rhs(const double *benv, int64_t N, const int32_t *if_of_r
     rhs[i] = k >= 0 ? benv[i] + if_b[k] : benv[i];
 }
 
-extern "C" int thermo_stationary(void *ctx, double t, int32_t with_interface) {
+extern "C" int thermo_stationary(thermo_ctx *ctx, double t, int32_t with_interface) {
     Ctx *c = (Ctx *)ctx;
     if (!c) return THERMO_EINVAL;
     if (!std::isfinite(t)) return fail(c, THERMO_EINVAL, "t must be finite");
@@ -448,7 +448,7 @@ extern "C" int thermo_stationary(void *ctx, double t, int32_t with_interface) {
     }
 }
 
-extern "C" int thermo_get_interface(void *ctx, int32_t scen, double t, double dt, int32_t *rows, int32_t *cnt,
+extern "C" int thermo_get_interface(thermo_ctx *ctx, int32_t scen, double t, double dt, int32_t *rows, int32_t *cnt,
                                     int32_t *col, double *val, double *b) {
     Ctx *c = (Ctx *)ctx;
     if (!c) return THERMO_EINVAL;
@@ -507,7 +507,7 @@ extern "C" int thermo_get_interface(void *ctx, int32_t scen, double t, double dt
     }
 }
 
-extern "C" int thermo_set_guess(void *ctx, int32_t order) {
+extern "C" int thermo_set_guess(thermo_ctx *ctx, int32_t order) {
     Ctx *c = (Ctx *)ctx;
     if (!c) return THERMO_EINVAL;
     if (order < 0 || order > 2) return fail(c, THERMO_EINVAL, "guess order must be 0, 1 or 2");
@@ -516,7 +516,7 @@ extern "C" int thermo_set_guess(void *ctx, int32_t order) {
     return THERMO_OK;
 }
 
-extern "C" int thermo_set_method(void *ctx, int32_t method, int32_t M, int32_t P, int32_t K) {
+extern "C" int thermo_set_method(thermo_ctx *ctx, int32_t method, int32_t M, int32_t P, int32_t K) {
     Ctx *c = (Ctx *)ctx;
     if (!c) return THERMO_EINVAL;
     if (method == 0) {
@@ -536,7 +536,7 @@ extern "C" int thermo_set_method(void *ctx, int32_t method, int32_t M, int32_t P
     return rc ? THERMO_ECUDA : THERMO_OK;
 }
 
-extern "C" int thermo_set_solver(void *ctx, double rtol, int32_t maxit) {
+extern "C" int thermo_set_solver(thermo_ctx *ctx, double rtol, int32_t maxit) {
     Ctx *c = (Ctx *)ctx;
     if (!c) return THERMO_EINVAL;
     if (!(rtol > 0) || maxit < 0) return fail(c, THERMO_EINVAL, "rtol must be > 0 and maxit >= 0");
@@ -545,7 +545,7 @@ extern "C" int thermo_set_solver(void *ctx, double rtol, int32_t maxit) {
     return THERMO_OK;
 }
 
-extern "C" int thermo_step(void *ctx, double t, double dt, int32_t nsteps) {
+extern "C" int thermo_step(thermo_ctx *ctx, double t, double dt, int32_t nsteps) {
     Ctx *c = (Ctx *)ctx;
     if (!c) return THERMO_EINVAL;
     if (!(dt > 0) || !std::isfinite(t) || nsteps < 0) return fail(c, THERMO_EINVAL, "dt must be > 0, nsteps >= 0");
@@ -913,7 +913,7 @@ static int queue_host_copy(Ctx *c, int scen, int64_t off, int64_t cnt, double *h
     return THERMO_OK;
 }
 
-extern "C" int thermo_get_T(void *ctx, int32_t scen, int32_t part, double *out, int64_t n,
+extern "C" int thermo_get_T(thermo_ctx *ctx, int32_t scen, int32_t part, double *out, int64_t n,
                             int32_t out_on_device) {
     Ctx *c = (Ctx *)ctx;
     if (!c || !out) return c ? fail(c, THERMO_EINVAL, "out is NULL") : THERMO_EINVAL;
@@ -931,7 +931,7 @@ extern "C" int thermo_get_T(void *ctx, int32_t scen, int32_t part, double *out, 
     return THERMO_OK;
 }
 
-extern "C" int thermo_get_T_async(void *ctx, int32_t scen, int32_t part, double *host_out, int64_t n) {
+extern "C" int thermo_get_T_async(thermo_ctx *ctx, int32_t scen, int32_t part, double *host_out, int64_t n) {
     Ctx *c = (Ctx *)ctx;
     if (!c || !host_out) return c ? fail(c, THERMO_EINVAL, "host_out is NULL") : THERMO_EINVAL;
     int64_t off, cnt;
@@ -939,14 +939,14 @@ extern "C" int thermo_get_T_async(void *ctx, int32_t scen, int32_t part, double 
     return queue_host_copy(c, scen, off, cnt, host_out);
 }
 
-extern "C" int thermo_get_T_all_async(void *ctx, double *host_out, int64_t n) {
+extern "C" int thermo_get_T_all_async(thermo_ctx *ctx, double *host_out, int64_t n) {
     Ctx *c = (Ctx *)ctx;
     if (!c || !host_out) return c ? fail(c, THERMO_EINVAL, "host_out is NULL") : THERMO_EINVAL;
     if (n != c->N * c->S) return fail(c, THERMO_EINVAL, "n must equal n_scen * n_nodes");
     return queue_host_copy(c, c->S == 1 ? 0 : -1, 0, n, host_out);
 }
 
-extern "C" int thermo_sync(void *ctx) {
+extern "C" int thermo_sync(thermo_ctx *ctx) {
     Ctx *c = (Ctx *)ctx;
     if (!c) return THERMO_EINVAL;
     if (c->copy_stream) {
@@ -957,7 +957,7 @@ extern "C" int thermo_sync(void *ctx) {
     return THERMO_OK;
 }
 
-extern "C" int thermo_set_T(void *ctx, int32_t scen, int32_t part, const double *in, int64_t n,
+extern "C" int thermo_set_T(thermo_ctx *ctx, int32_t scen, int32_t part, const double *in, int64_t n,
                             int32_t in_on_device) {
     Ctx *c = (Ctx *)ctx;
     if (!c || !in) return c ? fail(c, THERMO_EINVAL, "in is NULL") : THERMO_EINVAL;
@@ -982,7 +982,7 @@ extern "C" int thermo_set_T(void *ctx, int32_t scen, int32_t part, const double 
     return THERMO_OK;
 }
 
-extern "C" int thermo_get_stats(const void *ctx, thermo_stats *out) {
+extern "C" int thermo_get_stats(const thermo_ctx *ctx, thermo_stats *out) {
     const Ctx *c = (const Ctx *)ctx;
     if (!c || !out) return THERMO_EINVAL;
     memset(out, 0, sizeof *out);
@@ -1027,14 +1027,14 @@ extern "C" int thermo_get_stats(const void *ctx, thermo_stats *out) {
     return THERMO_OK;
 }
 
-extern "C" int thermo_set_timing(void *ctx, int32_t enable) {
+extern "C" int thermo_set_timing(thermo_ctx *ctx, int32_t enable) {
     Ctx *c = (Ctx *)ctx;
     if (!c) return THERMO_EINVAL;
     c->timing = enable != 0;
     return THERMO_OK;
 }
 
-extern "C" int thermo_get_step_iters(const void *ctx, int32_t *out, int64_t n) {
+extern "C" int thermo_get_step_iters(const thermo_ctx *ctx, int32_t *out, int64_t n) {
     const Ctx *c = (const Ctx *)ctx;
     if (!c || !out) return THERMO_EINVAL;
     int64_t m = (int64_t)c->h_iters.size();
@@ -1043,12 +1043,12 @@ extern "C" int thermo_get_step_iters(const void *ctx, int32_t *out, int64_t n) {
     return THERMO_OK;
 }
 
-extern "C" const char *thermo_last_error(const void *ctx) {
+extern "C" const char *thermo_last_error(const thermo_ctx *ctx) {
     const Ctx *c = (const Ctx *)ctx;
     return c ? c->err.c_str() : g_create_err.c_str();
 }
 
-extern "C" void thermo_destroy(void *ctx) {
+extern "C" void thermo_destroy(thermo_ctx *ctx) {
     Ctx *c = (Ctx *)ctx;
     if (!c) return;
     cudaStreamSynchronize(c->stream);

@@ -20,7 +20,7 @@
 #include "thermo.h"
 #include "box_mesh.h"
 
-static int check_profile(void *ctx, const mesh_t *f, const mesh_t *s, const char *what) {
+static int check_profile(thermo_ctx *ctx, const mesh_t *f, const mesh_t *s, const char *what) {
     const double Tbot = 22.5, T1 = 22.35, T2 = 22.025, Ttop = 20.875;   /* analytic, H1 = H2 = 0.1 */
     int n = f->nn + s->nn;
     double *T = malloc(sizeof(double) * n);
@@ -46,7 +46,7 @@ int main(void) {
     thermo_mesh mf = {f.nn, f.xyz, f.nt, f.tets, f.nf, f.faces, f.tags};
     thermo_mesh ms = {s.nn, s.xyz, s.nt, s.tets, s.nf, s.faces, s.tags};
     thermo_scenario sc = {0.0, 0.0, 1.0, {1.0, 0.0, 0.0}, 500.0, 0.0, 1.0};
-    void *ctx = NULL;
+    thermo_ctx *ctx = NULL;
     int rc = thermo_create_mesh(&ctx, &mf, &ms, 4, 4, 50.0, 3.6e6, 1000.0, 1, &sc, 24.0, NULL);
     if (rc) { fprintf(stderr, "create: %d %s\n", rc, thermo_last_error(NULL)); return 1; }
     const double g0[3] = {0.0, 0.0, 0.0};

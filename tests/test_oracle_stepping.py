@@ -193,3 +193,38 @@ def test_extrapolated_start(order):
     assert np.array_equal(Te, Tf2)
     with pytest.raises(ValueError):
         og.set_guess(3)
+
+
+def test_ie_residual_rows():
+    """or_ie_residual_rows (the checker of test_cfg2_full_run_invariants) against a dense
+    numpy build of the same system from the oracle's exported matrices (R3):
+    (i) the residual of a dense-Cholesky step vanishes to rounding; (ii) for a perturbed state
+    T1 + delta the residual rows equal (M_L - dt K) delta, row by row, on a subset of rows; (iii)
+    bnorm = ||M_L T0 + dt (b_env + b_G)||_2."""
+    c = I.make_config("cfg0")
+    o = O.Oracle.from_config(c)
+    sc = c.scenarios[0]
+    t, dt = 3.0, 2.0
+    T0 = I.initial_field(c)[0]
+    T1, _ = o.step(T0, t, dt, 1, sc, solver="cholesky")
+    s1, eta1 = I.scenario_scalars(sc, t + dt)
+    off = (s1 * sc.dir[0], s1 * sc.dir[1], s1 * sc.dir[2])
+    rows = np.arange(o.n, dtype=np.int64)
+    res, bnorm = o.residual_rows(dt, off, eta1, T0, T1, rows)
+    rp, col, A, B, ML, benv = o.volume()
+    irp, icol, ival, bG, area = o.interface(off, eta1)
+    n = o.n
+    K = np.zeros((n, n))
+    for i in range(n):
+        K[i, col[rp[i]:rp[i + 1]]] += A[rp[i]:rp[i + 1]] + B[rp[i]:rp[i + 1]]
+        K[i, icol[irp[i]:irp[i + 1]]] += ival[irp[i]:irp[i + 1]]
+    Kt = np.diag(ML) - dt * K
+    b = ML * T0 + dt * (benv + bG)
+    assert abs(bnorm - np.linalg.norm(b)) <= 1e-14 * np.linalg.norm(b)
+    assert np.linalg.norm(res) <= 1e-13 * bnorm
+    delta = np.sin(np.arange(n) * 0.37) * 0.01
+    sub = np.arange(0, n, 7, dtype=np.int64)
+    res2, _ = o.residual_rows(dt, off, eta1, T0, T1 + delta, sub)
+    ref = (Kt @ (T1 + delta) - b)[sub]
+    assert np.abs(res2 - ref).max() <= 1e-12 * np.abs(Kt @ delta).max()
+    assert np.abs(res2 - (Kt @ delta)[sub]).max() <= 1e-10 * np.abs(Kt @ delta).max()
