@@ -861,7 +861,15 @@ int or_stationary(or_sys *s, double t, int32_t with_interface, double s0, double
             relres = truerel = sqrt(rr / bb);
         }
     } else {
+        /* reading R17: the stopping rule holds for the TRUE residual ||b - K~ x||_2 (verified at
+         * exit).  Over the O(1/h) iterations of this unshifted operator the recursive residual
+         * drifts below the true one (configs[2]: recursive 9.9e-13, true 8.0e-12), so CG restarts
+         * from its result while the true residual misses rtol (at most 10 restarts). */
         it = pcg(s, 1.0, b, x, rtol, maxit > 0 ? maxit : 10 * n, &relres, &truerel);
+        for (int rs = 0; rs < 10 && it >= 0 && truerel > rtol; ++rs) {
+            int64_t it2 = pcg(s, 1.0, b, x, rtol, maxit > 0 ? maxit : 10 * n, &relres, &truerel);
+            it = it2 < 0 ? it2 : it + it2;
+        }
         if (it < 0) rc = -4;
     }
     s->mass = 1.0;

@@ -413,17 +413,29 @@ extern "C" int thermo_stationary(thermo_ctx *ctx, double t, int32_t with_interfa
         API_CK(cudaGetLastError());
         double *x0 = c->d_T[c->cur], *x = c->d_T[c->cur ^ 1];
         API_CK(guard_write(c, c->cur ^ 1));
-        if (thermo::cg_launch_solve(*c, x0, x, c->d_rhs, iface ? c->d_Dinv : c->d_Dinv_vol, iface, c->d_iters,
-                                    c->d_relres, 0))
-            return THERMO_ECUDA;
+        // The unshifted operator needs O(1/h) iterations, over which the recursive residual the
+        // stopping rule watches drifts from the true one (the oracle's configs[2] solve stopped at
+        // a recursive 9.9e-13 with a true 8e-12).  So the solve restarts from its result: a
+        // restart recomputes r0 = b - K~ x in its phase 0 and returns at once (0 iterations) iff
+        // the TRUE residual meets rtol; otherwise it iterates on (at most 10 restarts).
         int status[8];
-        int32_t it = 0;
+        int32_t it = 0, it_tot = 0;
         double rr = 0.0, area = 0.0;
-        API_CK(cudaMemcpyAsync(status, c->d_status, sizeof status, cudaMemcpyDeviceToHost, c->stream));
-        API_CK(cudaMemcpyAsync(&it, c->d_iters, sizeof it, cudaMemcpyDeviceToHost, c->stream));
-        API_CK(cudaMemcpyAsync(&rr, c->d_relres, sizeof rr, cudaMemcpyDeviceToHost, c->stream));
-        API_CK(cudaMemcpyAsync(&area, c->d_area, sizeof area, cudaMemcpyDeviceToHost, c->stream));
-        API_CK(cudaStreamSynchronize(c->stream));
+        const double *xs = x0;
+        for (int rs = 0; rs <= 10; ++rs) {
+            if (thermo::cg_launch_solve(*c, xs, x, c->d_rhs, iface ? c->d_Dinv : c->d_Dinv_vol, iface, c->d_iters,
+                                        c->d_relres, 0))
+                return THERMO_ECUDA;
+            API_CK(cudaMemcpyAsync(status, c->d_status, sizeof status, cudaMemcpyDeviceToHost, c->stream));
+            API_CK(cudaMemcpyAsync(&it, c->d_iters, sizeof it, cudaMemcpyDeviceToHost, c->stream));
+            API_CK(cudaMemcpyAsync(&rr, c->d_relres, sizeof rr, cudaMemcpyDeviceToHost, c->stream));
+            API_CK(cudaMemcpyAsync(&area, c->d_area, sizeof area, cudaMemcpyDeviceToHost, c->stream));
+            API_CK(cudaStreamSynchronize(c->stream));
+            it_tot += it;
+            if (status[0] || status[1] || it == 0) break;   // it == 0: phase 0 saw the true residual meet rtol
+            xs = x;   // restart in place from the current iterate
+        }
+        it = it_tot;
         c->h_iters.assign(1, it);
         c->h_relres.assign(1, rr);
         c->h_area.assign(1, iface ? area : 0.0);
