@@ -158,12 +158,16 @@ int thermo_set_T(thermo_ctx *ctx, int32_t scen, int32_t part, const double *in, 
  *     f^I(T) = (A + B_env) T implicit with one solve of (M_L - dt/M (A + B_env)) per standard
  *     interval, f^E(T, t) = K_G(t) T + b_G(t) explicit on P embedded sub-steps (Algorithms 1-2),
  *     equidistant no-left nodes, Table-1 quadrature.  The paper's 3-D runs use M = 3, P = 2,
- *     K = 0..2.  Requires a single scenario.
+ *     K = 0..2.
  *   method 2: single-rate SDC(M) with K sweeps with every term implicit -- the
  *     comparison method of the work-precision study, whose interface Jacobian is reassembled
  *     at every node of every sweep (reading R29).  Implicit-Euler predictor through
  *     M equidistant no-left nodes; P is ignored.  M = 1 is implicit Euler.
- * EINVAL for other methods, M or P outside [1, 8], K < 0, or methods 1-2 with n_scen > 1. */
+ * Methods 1-2 run on batched contexts too: every scenario advances with its own motion and
+ * friction law (node-time interface operators of every scenario in one launch set, the implicit
+ * stages as batched solves with per-column convergence).
+ * EINVAL for other methods, M or P outside [1, 8], K < 0, or a batched context on the opt-in
+ * windowed-SpMM kernel (THERMO_CGB=2). */
 int thermo_set_method(thermo_ctx *ctx, int32_t method, int32_t M, int32_t P, int32_t K);
 
 /* Replace the temperature by the stationary state of the machine at rest (the

@@ -63,6 +63,8 @@ struct CGBParams {
     const double *ell_val, *if_b, *if_phi;
     const double *T_in;
     const double *X0;          // optional initial guess (extrapolated states); nullptr: x0 = T_in
+    const double *rhs;         // optional explicit right-hand side block (SDC / MRSDC solves)
+    int use_iface;             // 0: no interface rows (the MRSDC implicit operator is volume only)
     double *T_out, *z, *pa, *pb, *q;
     double *partials;   // [G][CGB_NV][64]
     int *status;
@@ -208,8 +210,8 @@ __device__ __forceinline__ void unit_loop(const CGBParams &P, int64_t npairs, in
             if (iA < N) {
                 m_base = P.slice_ptr[s];
                 m_w = (int)((P.slice_ptr[s + 1] - m_base) >> 5);
-                m_ikA = P.if_of_row[iA];
-                m_ikB = iA + 1 < N ? P.if_of_row[iA + 1] : -1;
+                m_ikA = P.use_iface ? P.if_of_row[iA] : -1;
+                m_ikB = P.use_iface && iA + 1 < N ? P.if_of_row[iA + 1] : -1;
             }
         }
         const int64_t rem = (npairs - c0 + TW - 1) / TW;
@@ -372,10 +374,14 @@ __global__ void __launch_bounds__(CGB_BLOCK, 1) k_cgb_step(CGBParams P) {
             if (lane == 0 && ik < P.nA) v0[3][0] += P.if_phi[(int64_t)ik * P.S];
         }
         if (!lane_ok) return;
-        const double ml = P.ML[i], be = P.benv[i];
         double2 b, rr, zz;
-        b.x = fma(ml, Ti.x, P.dt * (be + bg.x));
-        b.y = fma(ml, Ti.y, P.dt * (be + bg.y));
+        if (P.rhs) {
+            b = reinterpret_cast<const double2 *>(P.rhs + i * P.SP)[lane];
+        } else {
+            const double ml = P.ML[i], be = P.benv[i];
+            b.x = fma(ml, Ti.x, P.dt * (be + bg.x));
+            b.y = fma(ml, Ti.y, P.dt * (be + bg.y));
+        }
         rr.x = b.x - ax.x;
         rr.y = b.y - ax.y;
         zz.x = col_ok[0] ? di.x * rr.x : 0.0;
@@ -528,7 +534,7 @@ __global__ void __launch_bounds__(CGB_BLOCK, 1) k_cgb_step(CGBParams P) {
                 }
             }
         }
-        if (lane == 0) P.area_out[P.step] = area;
+        if (lane == 0 && P.area_out) P.area_out[P.step] = area;
     }
 }
 
@@ -563,9 +569,7 @@ int cgb_prepare(Ctx &c) {
     return 0;
 }
 
-int cgb_launch_step(Ctx &c, int step, double dt, const double *x0) {
-    if (c.sb_on) return sbcg_launch_step(c, step, dt, x0);
-    CGBParams P;
+static void cgb_params(Ctx &c, CGBParams &P) {
     memset(&P, 0, sizeof P);
     P.N = c.N;
     P.nslices = c.nslices;
@@ -588,9 +592,6 @@ int cgb_launch_step(Ctx &c, int step, double dt, const double *x0) {
     P.ell_val = c.d_ell_val;
     P.if_b = c.d_if_b;
     P.if_phi = c.d_if_phi;
-    P.T_in = c.d_T[(c.cur + step) & 1];
-    P.X0 = x0;
-    P.T_out = c.d_T[(c.cur + step + 1) & 1];
     P.z = c.d_z;
     P.pa = c.d_p[0];
     P.pb = c.d_p[1];
@@ -598,14 +599,45 @@ int cgb_launch_step(Ctx &c, int step, double dt, const double *x0) {
     P.partials = c.d_partials;
     P.status = c.d_status;
     P.fail_relres = c.d_fail_relres;
+    P.rtol2 = c.rtol * c.rtol;
+    P.maxit = c.maxit > 0 ? c.maxit : (int)std::min<int64_t>(10 * c.N, 10000);
+    P.trace = c.d_trace;
+}
+
+// Solve with an explicit right-hand side block (SDC / MRSDC implicit stages, every scenario)
+int cgb_launch_solve(Ctx &c, const double *x0, double *x, const double *rhs, bool iface, int32_t *iters_out,
+                     double *relres_out, int slot) {
+    if (c.sb_on) { c.err = "SDC methods need the default batched kernel (THERMO_CGB != 2)"; return -1; }
+    CGBParams P;
+    cgb_params(c, P);
+    P.T_in = x0;
+    P.X0 = nullptr;
+    P.T_out = x;
+    P.rhs = rhs;
+    P.use_iface = iface ? 1 : 0;
+    P.iters_out = iters_out;
+    P.relres_out = relres_out;
+    P.area_out = nullptr;
+    P.dt = 0.0;
+    P.step = slot;
+    void *args[] = {&P};
+    CK(cudaLaunchCooperativeKernel((const void *)k_cgb_step, dim3(c.cg_grid), dim3(c.cg_block), args, 0, c.stream));
+    return 0;
+}
+
+int cgb_launch_step(Ctx &c, int step, double dt, const double *x0) {
+    if (c.sb_on) return sbcg_launch_step(c, step, dt, x0);
+    CGBParams P;
+    cgb_params(c, P);
+    P.T_in = c.d_T[(c.cur + step) & 1];
+    P.X0 = x0;
+    P.T_out = c.d_T[(c.cur + step + 1) & 1];
     P.iters_out = c.d_iters;
     P.relres_out = c.d_relres;
     P.area_out = c.d_area;
     P.dt = dt;
-    P.rtol2 = c.rtol * c.rtol;
-    P.maxit = c.maxit > 0 ? c.maxit : (int)std::min<int64_t>(10 * c.N, 10000);
     P.step = step;
-    P.trace = c.d_trace;
+    P.use_iface = 1;
     void *args[] = {&P};
     CK(cudaLaunchCooperativeKernel((const void *)k_cgb_step, dim3(c.cg_grid), dim3(c.cg_block), args, 0, c.stream));
     return 0;

@@ -151,6 +151,7 @@ struct Ctx {
     double *d_Dinv_vol = nullptr;         // 1 / diag(M_L - a (A + B_env)), untouched by the interface
     int32_t *d_if_of_row = nullptr;       // [N] interface index of a row or -1
     double *d_mr = nullptr;               // MRSDC node states and caches (see mrsdc.cu)
+    double *d_benvS = nullptr;            // S > 1: b_env broadcast over the scenario columns
     size_t mr_vectors = 0;
     int32_t *d_mr_iters = nullptr;        // per implicit solve of the last step
     double *d_mr_relres = nullptr;
@@ -239,6 +240,10 @@ int sdc_step(Ctx &c, double tn, double dt, int step_index);   // single-rate SDC
 int cgb_setup(Ctx &c);
 int cgb_prepare(Ctx &c);   // broadcast the volume D^{-1} into DinvS (after build_operator)
 int cgb_launch_step(Ctx &c, int step, double dt, const double *x0 = nullptr);
+// Solve (M_L - a K_vol [- a K_G]) X = RHS for every scenario from X0 (explicit right-hand side
+// block, operator in d_val, Jacobi block d_DinvS); iterations / residuals to [slot][S].
+int cgb_launch_solve(Ctx &c, const double *x0, double *x, const double *rhs, bool iface, int32_t *iters_out,
+                     double *relres_out, int slot);
 
 // cg_spmm.cu (S > 1: windowed SpMM kernel, selected by cgb_setup when the windows fit)
 int sbcg_setup(Ctx &c);

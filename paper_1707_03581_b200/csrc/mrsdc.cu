@@ -39,82 +39,101 @@ struct MrW {            // one row of a weight family (by value)
 
 static inline unsigned nbk(int64_t n, int t = 256) { return (unsigned)((n + t - 1) / t); }
 
-// y_i = sum_j (A + B_env)_ij x_j + sgn * addv_i   (sliced ELL, thread per row)
-__global__ void k_vol_apply(const int64_t *slice_ptr, const int32_t *col, const double *KV, int64_t N,
-                            const double *x, const double *addv, double sgn, double *y) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= N) return;
-    const int64_t s = i >> 5;
+// Every kernel below works on S scenario columns: a block vector holds element (row i, scenario
+// s) at i * SP + s (SP >= S; S = SP = 1 for a single run), node vectors follow each other at a
+// stride of ldf elements, compact interface vectors (f^E on the interface rows) hold (k, s) at
+// k * SP + s, and the node-time interface operators of scenario s and slot q are batch entry
+// b = s * ns + q of the slot-major interface arrays ([b][c][k], [b][k]).  One thread per (row,
+// scenario); padding columns s >= S are left alone.
+
+// y = (A + B_env) x + sgn * addv   (sliced ELL)
+__global__ void k_vol_apply(const int64_t *slice_ptr, const int32_t *col, const double *KV, int64_t N, int S,
+                            int SP, const double *x, const double *addv, double sgn, double *y) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= N * S) return;
+    const int64_t i = t / S;
+    const int sc = (int)(t - i * S);
+    const int64_t sl = i >> 5;
     const int lane = (int)(i & 31);
-    const int64_t b0 = slice_ptr[s], w = (slice_ptr[s + 1] - b0) >> 5;
+    const int64_t b0 = slice_ptr[sl], w = (slice_ptr[sl + 1] - b0) >> 5;
     double acc = 0.0;
-    for (int64_t k = 0; k < w; ++k) acc = fma(KV[b0 + 32 * k + lane], x[col[b0 + 32 * k + lane]], acc);
-    if (addv) acc = fma(sgn, addv[i], acc);
-    y[i] = acc;
+    for (int64_t k = 0; k < w; ++k)
+        acc = fma(KV[b0 + 32 * k + lane], x[(int64_t)col[b0 + 32 * k + lane] * SP + sc], acc);
+    if (addv) acc = fma(sgn, addv[i * SP + sc], acc);
+    y[i * SP + sc] = acc;
 }
 
-// compact f^E on the interface rows of node-time slot s (slot-major arrays [s][c][k], [s][k]):
-// y[k] = b_G[k] + sum_c K_G[k][c] x[col]
-__global__ void k_fe_apply(int n_if, int s, int cap, const int32_t *cnt, const int32_t *ecol, const double *evals,
-                           const double *bG, const double *x, double *y) {
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= n_if) return;
-    double acc = bG[(int64_t)s * n_if + k];
-    const int m = cnt[(int64_t)s * n_if + k];
+// compact f^E on the interface rows at node-time slot q of every scenario:
+// y[k][s] = b_G[k] + sum_c K_G[k][c] x[col][s]   (operators of batch entry s * ns + q)
+__global__ void k_fe_apply(int n_if, int q, int ns, int S, int SP, int cap, const int32_t *cnt, const int32_t *ecol,
+                           const double *evals, const double *bG, const double *x, double *y) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= (int64_t)n_if * S) return;
+    const int k = (int)(t / S), sc = (int)(t - (int64_t)k * S);
+    const int64_t bt = (int64_t)sc * ns + q;
+    double acc = bG[bt * n_if + k];
+    const int m = cnt[bt * n_if + k];
     for (int c = 0; c < m; ++c) {
-        const int64_t e = ((int64_t)s * cap + c) * n_if + k;
-        acc = fma(evals[e], x[ecol[e]], acc);
+        const int64_t e = (bt * cap + c) * n_if + k;
+        acc = fma(evals[e], x[(int64_t)ecol[e] * SP + sc], acc);
     }
-    y[k] = acc;
+    y[(int64_t)k * SP + sc] = acc;
 }
 
 // right-hand side of an implicit solve.
 //  predictor:  rhs = M_L Tprev + a g
 //  sweep:      rhs = M_L Tprev - a f^I(T^k_m) + I_{m-1}^m,
 //              I_{m-1}^m = sum_j s_mj (f^I(T_j) + g) + sum_p shat_mp f^E(T_mp)
-__global__ void k_mr_rhs(int64_t N, int64_t ldf, const double *ML, const double *Tprev, const double *benv,
-                         const double *KvTk, double a, const double *FI, const double *FE, const int32_t *if_of_row,
-                         int n_if, int M, int P, MrW w, double *rhs) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= N) return;
-    double r = ML[i] * Tprev[i];
+__global__ void k_mr_rhs(int64_t N, int S, int SP, int64_t ldf, const double *ML, const double *Tprev,
+                         const double *benv, const double *KvTk, double a, const double *FI, const double *FE,
+                         const int32_t *if_of_row, int n_if, int M, int P, MrW w, double *rhs) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= N * S) return;
+    const int64_t i = t / S;
+    const int sc = (int)(t - i * S);
+    const int64_t e = i * SP + sc;
+    double r = ML[i] * Tprev[e];
     if (!KvTk) {
         r = fma(a, benv[i], r);
     } else {
         double I = 0.0;
-        for (int j = 0; j < M; ++j) I = fma(w.a[j], FI[(int64_t)j * ldf + i], I);
+        for (int j = 0; j < M; ++j) I = fma(w.a[j], FI[(int64_t)j * ldf + e], I);
         const int k = if_of_row[i];
         if (k >= 0)
-            for (int p = 0; p < P; ++p) I = fma(w.b[p], FE[(int64_t)p * n_if + k], I);
-        r = fma(-a, KvTk[i], r) + I;
+            for (int p = 0; p < P; ++p) I = fma(w.b[p], FE[((int64_t)p * n_if + k) * SP + sc], I);
+        r = fma(-a, KvTk[e], r) + I;
     }
-    rhs[i] = r;
+    rhs[e] = r;
 }
 
 // one embedded explicit-Euler sub-step (Algorithm 1 / 2 inner loop)
 //  predictor: T = Tprev + dtp (fs + fe_new) / M_L
 //  sweep:     T = Tprev + (dtp fs + dtp (fe_new - fe_old) + I_{m,p-1}^p) / M_L,
 //             I_{m,p-1}^p = sum_j st_j (f^I(T_j) + g) + sum_q se_q f^E(T_mq)
-__global__ void k_mr_emb(int64_t N, int64_t ldf, const double *ML, const double *Tprev, const double *fs,
-                         const double *fe_new, const double *fe_old, double dtp, const double *FI, const double *FE,
-                         const int32_t *if_of_row, int n_if, int M, int P, MrW w, double *Tout) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= N) return;
+__global__ void k_mr_emb(int64_t N, int S, int SP, int64_t ldf, const double *ML, const double *Tprev,
+                         const double *fs, const double *fe_new, const double *fe_old, double dtp, const double *FI,
+                         const double *FE, const int32_t *if_of_row, int n_if, int M, int P, MrW w, double *Tout) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= N * S) return;
+    const int64_t i = t / S;
+    const int sc = (int)(t - i * S);
+    const int64_t e = i * SP + sc;
     const int k = if_of_row[i];
+    const int64_t ek = (int64_t)k * SP + sc;
     double num;
     if (!fe_old) {
-        num = dtp * (fs[i] + (k >= 0 ? fe_new[k] : 0.0));
+        num = dtp * (fs[e] + (k >= 0 ? fe_new[ek] : 0.0));
     } else {
         double I = 0.0;
-        for (int j = 0; j < M; ++j) I = fma(w.a[j], FI[(int64_t)j * ldf + i], I);
+        for (int j = 0; j < M; ++j) I = fma(w.a[j], FI[(int64_t)j * ldf + e], I);
         double fe = 0.0;
         if (k >= 0) {
-            for (int q = 0; q < P; ++q) I = fma(w.b[q], FE[(int64_t)q * n_if + k], I);
-            fe = fe_new[k] - fe_old[k];
+            for (int q = 0; q < P; ++q) I = fma(w.b[q], FE[((int64_t)q * n_if + k) * SP + sc], I);
+            fe = fe_new[ek] - fe_old[ek];
         }
-        num = dtp * fs[i] + dtp * fe + I;
+        num = dtp * fs[e] + dtp * fe + I;
     }
-    Tout[i] = Tprev[i] + num / ML[i];
+    Tout[e] = Tprev[e] + num / ML[i];
 }
 
 // right-hand side of a single-rate SDC solve (every term implicit, reading R29):
@@ -122,28 +141,38 @@ __global__ void k_mr_emb(int64_t N, int64_t ldf, const double *ML, const double 
 //  sweep:  rhs = M_L Tprev - a K(tau_m) T^k_m + sum_j s_mj F(T^k_j, tau_j)
 //          K(tau_m) T^k_m = KvTk + (FE_m - b_G(tau_m)) on the interface rows,
 //          F(T^k_j, tau_j) = FI_j + FE_j (FI_j = (A + B_env) T^k_j + b_env, FE_j = K_G T^k_j + b_G)
-__global__ void k_sdc_rhs(int64_t N, int64_t ldf, const double *ML, const double *Tprev, const double *benv,
-                          const double *KvTk, double a, const double *FI, const double *FE, int nif,
-                          const double *bG, int ns, const int32_t *if_of_row, int M, int mcur, MrW w, double *rhs) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= N) return;
+__global__ void k_sdc_rhs(int64_t N, int S, int SP, int64_t ldf, const double *ML, const double *Tprev,
+                          const double *benv, const double *KvTk, double a, const double *FI, const double *FE,
+                          int nif, const double *bG, int ns, const int32_t *if_of_row, int M, int mcur, MrW w,
+                          double *rhs) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= N * S) return;
+    const int64_t i = t / S;
+    const int sc = (int)(t - i * S);
+    const int64_t e = i * SP + sc;
     const int k = nif ? if_of_row[i] : -1;
-    const double bGm = k >= 0 ? bG[(int64_t)mcur * nif + k] : 0.0;   // b_G(tau_m), slot m
-    double r = ML[i] * Tprev[i];
+    const double bGm = k >= 0 ? bG[((int64_t)sc * ns + mcur) * nif + k] : 0.0;   // b_G(tau_m), slot m
+    double r = ML[i] * Tprev[e];
     if (!KvTk) {
         r = fma(a, k >= 0 ? benv[i] + bGm : benv[i], r);
     } else {
-        double KT = KvTk[i];
-        if (k >= 0) KT += FE[(int64_t)(mcur - 1) * nif + k] - bGm;
+        double KT = KvTk[e];
+        if (k >= 0) KT += FE[((int64_t)(mcur - 1) * nif + k) * SP + sc] - bGm;
         double I = 0.0;
         for (int j = 0; j < M; ++j) {
-            double Fj = FI[(int64_t)j * ldf + i];
-            if (k >= 0) Fj += FE[(int64_t)j * nif + k];
+            double Fj = FI[(int64_t)j * ldf + e];
+            if (k >= 0) Fj += FE[((int64_t)j * nif + k) * SP + sc];
             I = fma(w.a[j], Fj, I);
         }
         r = fma(-a, KT, r) + I;
     }
-    rhs[i] = r;
+    rhs[e] = r;
+}
+
+// g = b_env as a block (every scenario column the same), for the "+ g" forms of k_vol_apply
+__global__ void k_bcast_rows(const double *v, int64_t N, int SP, double *vS) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t < N * SP) vS[t] = v[t / SP];
 }
 
 __global__ void k_if_of_row(const int32_t *if_rows, int n_if, int32_t *map) {
@@ -242,42 +271,49 @@ struct MrPtr {
 };
 
 int mrsdc_setup(Ctx &c) {
-    const int M = c.mr_M, P = c.mr_P;
+    const int M = c.mr_M, P = c.mr_P, S = c.S, SP = c.SP;
     const int64_t N = c.N, nif = std::max(c.n_if, 1);
     const int64_t Np = (N + 31) & ~(int64_t)31;   // 256-byte aligned vectors (TMA windows, 16-B loads)
     const size_t nfull = 2 * (size_t)M + 2 * (size_t)M * (P - 1) + M + 4;   // TS (1..M) x2, interior TE x2, FI, 4 temps
     const size_t ncomp = (size_t)M * P + 2;
     if (c.d_mr) cudaFree(c.d_mr);
-    CK(cudaMalloc(&c.d_mr, sizeof(double) * (nfull * Np + ncomp * nif + 64)));
-    CK(cudaMemsetAsync(c.d_mr, 0, sizeof(double) * (nfull * Np + ncomp * nif + 64), c.stream));
+    const size_t bytes = sizeof(double) * ((nfull * Np + ncomp * nif) * SP + 64);
+    CK(cudaMalloc(&c.d_mr, bytes));
+    CK(cudaMemsetAsync(c.d_mr, 0, bytes, c.stream));
     c.mr_vectors = nfull;
     if (int rc = build_if_of_row(c)) return rc;
-    // interface operators at the M P + 1 node times of a step
+    // interface operators at the M P + 1 node times of a step, every scenario (batch entry
+    // scenario * nslot + slot)
     const int nslot = M * P + 1;
-    if (c.mr_nslots < nslot && c.n_if) {
+    const int64_t nb = (int64_t)nslot * S;
+    if (c.mr_nslots < nb && c.n_if) {
         for (void *p : {(void *)c.d_ell_cnt_s, (void *)c.d_ell_col_s, (void *)c.d_ell_val_s, (void *)c.d_if_b_s,
                         (void *)c.d_if_phi_s, (void *)c.d_pairs_s, (void *)c.d_pcnt_s})
             if (p) cudaFree(p);
-        // pair records of all node times at once (one launch set per step, slot = blockIdx.y)
-        CK(cudaMalloc(&c.d_pairs_s, sizeof(PairRec) * (size_t)nslot * (c.nTA + c.nTB) * c.pcap));
-        CK(cudaMalloc(&c.d_pcnt_s, sizeof(int32_t) * (size_t)nslot * (c.nTA + c.nTB)));
-        CK(cudaMalloc(&c.d_ell_cnt_s, sizeof(int32_t) * nslot * nif));
-        CK(cudaMalloc(&c.d_ell_col_s, sizeof(int32_t) * (size_t)nslot * c.cap * nif));
-        CK(cudaMalloc(&c.d_ell_val_s, sizeof(double) * (size_t)nslot * c.cap * nif));
-        CK(cudaMalloc(&c.d_if_b_s, sizeof(double) * nslot * nif));
-        CK(cudaMalloc(&c.d_if_phi_s, sizeof(double) * nslot * nif));
-        c.mr_nslots = nslot;
+        // pair records of all node times at once (one launch set per step, batch = blockIdx.y)
+        CK(cudaMalloc(&c.d_pairs_s, sizeof(PairRec) * (size_t)nb * (c.nTA + c.nTB) * c.pcap));
+        CK(cudaMalloc(&c.d_pcnt_s, sizeof(int32_t) * (size_t)nb * (c.nTA + c.nTB)));
+        CK(cudaMalloc(&c.d_ell_cnt_s, sizeof(int32_t) * nb * nif));
+        CK(cudaMalloc(&c.d_ell_col_s, sizeof(int32_t) * (size_t)nb * c.cap * nif));
+        CK(cudaMalloc(&c.d_ell_val_s, sizeof(double) * (size_t)nb * c.cap * nif));
+        CK(cudaMalloc(&c.d_if_b_s, sizeof(double) * nb * nif));
+        CK(cudaMalloc(&c.d_if_phi_s, sizeof(double) * nb * nif));
+        c.mr_nslots = (int)nb;
     }
-    if (!c.d_mr_iters) {
-        CK(cudaMalloc(&c.d_mr_iters, sizeof(int32_t) * MR_MAX * (MR_MAX + 64)));
-        CK(cudaMalloc(&c.d_mr_relres, sizeof(double) * MR_MAX * (MR_MAX + 64)));
-    }
+    // iterations / residual of every implicit solve of a step (solve-major, S per solve)
+    const size_t nsol = (size_t)M * (c.mr_K + 1) + 8;
+    if (c.d_mr_iters) cudaFree(c.d_mr_iters);
+    if (c.d_mr_relres) cudaFree(c.d_mr_relres);
+    CK(cudaMalloc(&c.d_mr_iters, sizeof(int32_t) * nsol * S));
+    CK(cudaMalloc(&c.d_mr_relres, sizeof(double) * nsol * S));
+    if (S > 1 && cgb_prepare(c)) return -3;
     return 0;
 }
 
 static MrPtr mr_pointers(Ctx &c, double *T0) {
     const int M = c.mr_M, P = c.mr_P;
-    const int64_t N = (c.N + 31) & ~(int64_t)31, nif = std::max(c.n_if, 1);   // padded vector stride
+    const int64_t SP = c.SP;
+    const int64_t N = ((c.N + 31) & ~(int64_t)31) * SP, nif = std::max(c.n_if, 1) * SP;   // padded block strides
     MrPtr q;
     double *p = c.d_mr;
     q.TSo[0] = q.TSn[0] = T0;
@@ -302,6 +338,46 @@ static MrPtr mr_pointers(Ctx &c, double *T0) {
     return q;
 }
 
+// time scalars (offset, eta, s) of every scenario at the node times t_n + q dt / nq, q = 0..nq:
+// sc[(s * (nq + 1) + q) * 4 ..] (batch entry s * (nq + 1) + q of assemble_slots) followed by the
+// node-major copy sc[off + (q * S + s) * 4 ..] (one launch per node for the SDC reassembly)
+static void node_scalars(const Ctx &c, double tn, double dt, int nq, std::vector<double> &sc) {
+    const int S = c.S, ns = nq + 1;
+    sc.assign(8 * (size_t)S * ns, 0.0);
+    const size_t off = 4 * (size_t)S * ns;
+    for (int s = 0; s < S; ++s) {
+        const Scen &sn = c.scen[s];
+        for (int q = 0; q < ns; ++q) {
+            const double tq = tn + dt * (double)q / (double)nq;
+            const double sv = sn.s0 + sn.amp * std::sin(2.0 * M_PI * tq / sn.period);
+            const double v[4] = {sv * sn.d2[0], sv * sn.d2[1],
+                                 sn.eta0 * (1.0 + sn.eta_amp * std::sin(2.0 * M_PI * tq / sn.eta_period)), sv};
+            for (int j = 0; j < 4; ++j) {
+                sc[4 * ((size_t)s * ns + q) + j] = v[j];
+                sc[off + 4 * ((size_t)q * S + s) + j] = v[j];
+            }
+        }
+    }
+}
+
+static int ensure_step_scalars(Ctx &c, size_t n) {   // d_step_sc with room for n doubles
+    if ((int64_t)(n / 4) <= c.step_cap) return 0;
+    for (void *p : {(void *)c.d_step_sc, (void *)c.d_iters, (void *)c.d_relres, (void *)c.d_area})
+        if (p) cudaFree(p);
+    c.step_cap = (int64_t)(n / 4);
+    CK(cudaMalloc(&c.d_step_sc, sizeof(double) * n));
+    CK(cudaMalloc(&c.d_iters, sizeof(int32_t) * (size_t)c.step_cap * c.S));
+    CK(cudaMalloc(&c.d_relres, sizeof(double) * (size_t)c.step_cap * c.S));
+    CK(cudaMalloc(&c.d_area, sizeof(double) * (size_t)c.step_cap));
+    return 0;
+}
+
+// implicit solve number `slot` of a step: (M_L - a K_vol [- a K_G]) x = rhs from x0, every scenario
+static int mr_solve(Ctx &c, const double *x0, double *x, const double *rhs, const double *Dinv, bool iface, int slot) {
+    if (c.S == 1) return cg_launch_solve(c, x0, x, rhs, Dinv, iface, c.d_mr_iters, c.d_mr_relres, slot);
+    return cgb_launch_solve(c, x0, x, rhs, iface, c.d_mr_iters, c.d_mr_relres, slot);
+}
+
 // K_G, b_G unscaled (dt = -1, Jacobi rows untouched) at the node times of d_step_sc[0..ns), all
 // in one launch set with the slot as the batch index (layout [k][c][slot]).
 static int assemble_slots(Ctx &c, int ns) {
@@ -309,7 +385,7 @@ static int assemble_slots(Ctx &c, int ns) {
     IfaceParams Pf;
     memset(&Pf, 0, sizeof Pf);
     iface_params(c, Pf, c.d_step_sc, -1.0);
-    Pf.S = ns;
+    Pf.S = ns * c.S;   // batch entry scenario * ns + slot
     Pf.pairs = c.d_pairs_s;
     Pf.pcnt = c.d_pcnt_s;
     Pf.ell_cnt = c.d_ell_cnt_s;
@@ -323,82 +399,76 @@ static int assemble_slots(Ctx &c, int ns) {
 }
 
 int mrsdc_step(Ctx &c, double tn, double dt, int step_index) {
-    const int M = c.mr_M, P = c.mr_P, K = c.mr_K;
+    const int M = c.mr_M, P = c.mr_P, K = c.mr_K, S = c.S, SP = c.SP;
     const int64_t N = c.N;
     const int nif = c.n_if;
     const double a = dt / M, dtp = dt / (M * P);
-    const int64_t ldf = (N + 31) & ~(int64_t)31;
+    const int64_t ldf = ((N + 31) & ~(int64_t)31) * SP, nifs = (int64_t)std::max(nif, 1) * SP;
     cudaStream_t st = c.stream;
     if (c.built_dt != a) {
         if (build_operator(c, a)) return -3;
     }
+    if (S > 1 && cgb_prepare(c)) return -3;   // Jacobi block = volume diagonal (implicit part only)
+    const double *gS = c.d_benv;   // g per (row, scenario)
+    if (S > 1) {
+        if (!c.d_benvS) CK(cudaMalloc(&c.d_benvS, sizeof(double) * (size_t)N * SP));
+        k_bcast_rows<<<nbk(N * SP), 256, 0, st>>>(c.d_benv, N, SP, c.d_benvS);
+        CK(cudaGetLastError());
+        gS = c.d_benvS;
+    }
     MrTables W;
     mr_tables(M, P, tn, dt, W);
-    // ---- interface operators K_G, b_G at the node times t_n + q dt/(MP), q = 0..MP
+    // ---- interface operators K_G, b_G at the node times t_n + q dt/(MP), q = 0..MP, every scenario
     const int nslot = M * P + 1;
-    std::vector<double> sc(4 * (size_t)nslot);
-    const Scen &sn = c.scen[0];
-    for (int q = 0; q < nslot; ++q) {
-        const double tq = tn + dt * (double)q / (double)(M * P);
-        const double sv = sn.s0 + sn.amp * std::sin(2.0 * M_PI * tq / sn.period);
-        sc[4 * q + 0] = sv * sn.d2[0];
-        sc[4 * q + 1] = sv * sn.d2[1];
-        sc[4 * q + 2] = sn.eta0 * (1.0 + sn.eta_amp * std::sin(2.0 * M_PI * tq / sn.eta_period));
-        sc[4 * q + 3] = sv;
-    }
-    if ((int64_t)nslot > c.step_cap) {
-        for (void *p : {(void *)c.d_step_sc, (void *)c.d_iters, (void *)c.d_relres, (void *)c.d_area})
-            if (p) cudaFree(p);
-        c.step_cap = nslot;
-        CK(cudaMalloc(&c.d_step_sc, sizeof(double) * 4 * (size_t)nslot));
-        CK(cudaMalloc(&c.d_iters, sizeof(int32_t) * (size_t)nslot));
-        CK(cudaMalloc(&c.d_relres, sizeof(double) * (size_t)nslot));
-        CK(cudaMalloc(&c.d_area, sizeof(double) * (size_t)nslot));
-    }
+    std::vector<double> sc;
+    node_scalars(c, tn, dt, M * P, sc);
+    if (ensure_step_scalars(c, sc.size())) return -3;
     CK(cudaMemcpyAsync(c.d_step_sc, sc.data(), sizeof(double) * sc.size(), cudaMemcpyHostToDevice, st));
     if (assemble_slots(c, nslot)) return -3;
     double *T0 = c.d_T[c.cur];
     MrPtr q = mr_pointers(c, T0);
     auto fe_apply = [&](int slot, const double *x, double *y) -> int {
         if (!nif) return 0;
-        k_fe_apply<<<nbk(nif), 256, 0, st>>>(nif, slot, c.cap, c.d_ell_cnt_s, c.d_ell_col_s, c.d_ell_val_s,
-                                             c.d_if_b_s, x, y);
+        k_fe_apply<<<nbk((int64_t)nif * S), 256, 0, st>>>(nif, slot, nslot, S, SP, c.cap, c.d_ell_cnt_s,
+                                                          c.d_ell_col_s, c.d_ell_val_s, c.d_if_b_s, x, y);
         CK(cudaGetLastError());
         return 0;
     };
     auto vol_apply = [&](const double *x, const double *addv, double sgn, double *y) -> int {
-        k_vol_apply<<<nbk(N), 256, 0, st>>>(c.d_slice_ptr, c.d_col, c.d_KV, N, x, addv, sgn, y);
+        k_vol_apply<<<nbk(N * S), 256, 0, st>>>(c.d_slice_ptr, c.d_col, c.d_KV, N, S, SP, x, addv, sgn, y);
         CK(cudaGetLastError());
         return 0;
     };
     int solve_no = 0;
     auto solve = [&](const double *x0, double *x, const double *rhs) -> int {
-        const int slot = solve_no++;
-        return cg_launch_solve(c, x0, x, rhs, c.d_Dinv_vol, false, c.d_mr_iters, c.d_mr_relres, slot);
+        return mr_solve(c, x0, x, rhs, c.d_Dinv_vol, false, solve_no++);
     };
+    // g = b_env enters f^I + g per row (one value for every scenario): a block copy for the
+    // vol_apply "+ addv" forms
     MrW w0;
     memset(&w0, 0, sizeof w0);
     // ---- Algorithm 1: predictor
     for (int m = 1; m <= M; ++m) {
-        k_mr_rhs<<<nbk(N), 256, 0, st>>>(N, ldf, c.d_ML, q.TSo[m - 1], c.d_benv, nullptr, a, nullptr, nullptr,
-                                         c.d_if_of_row, nif, M, P, w0, q.rhs);
+        k_mr_rhs<<<nbk(N * S), 256, 0, st>>>(N, S, SP, ldf, c.d_ML, q.TSo[m - 1], c.d_benv, nullptr, a, nullptr,
+                                             nullptr, c.d_if_of_row, nif, M, P, w0, q.rhs);
         CK(cudaGetLastError());
         if (solve(q.TSo[m - 1], q.Tstar, q.rhs)) return -3;
-        if (vol_apply(q.Tstar, c.d_benv, 1.0, q.fs)) return -3;   // f* = f^I(T*) + g
+        if (vol_apply(q.Tstar, gS, 1.0, q.fs)) return -3;   // f* = f^I(T*) + g
         for (int p = 1; p <= P; ++p) {
             if (fe_apply((m - 1) * P + p - 1, q.TEo[m - 1][p - 1], q.fe_new)) return -3;
-            k_mr_emb<<<nbk(N), 256, 0, st>>>(N, ldf, c.d_ML, q.TEo[m - 1][p - 1], q.fs, q.fe_new, nullptr, dtp, nullptr,
-                                             nullptr, c.d_if_of_row, nif, M, P, w0, q.TEo[m - 1][p]);
+            k_mr_emb<<<nbk(N * S), 256, 0, st>>>(N, S, SP, ldf, c.d_ML, q.TEo[m - 1][p - 1], q.fs, q.fe_new, nullptr,
+                                                 dtp, nullptr, nullptr, c.d_if_of_row, nif, M, P, w0,
+                                                 q.TEo[m - 1][p]);
             CK(cudaGetLastError());
         }
     }
     // ---- Algorithm 2: K correction sweeps
     for (int k = 0; k < K; ++k) {
         for (int j = 1; j <= M; ++j)
-            if (vol_apply(q.TSo[j], c.d_benv, 1.0, q.FI + (size_t)(j - 1) * ldf)) return -3;   // f^I(T^k_j) + g
+            if (vol_apply(q.TSo[j], gS, 1.0, q.FI + (size_t)(j - 1) * ldf)) return -3;   // f^I(T^k_j) + g
         for (int m = 1; m <= M; ++m)
             for (int p = 1; p <= P; ++p)
-                if (fe_apply((m - 1) * P + p, q.TEo[m - 1][p], q.FE + (size_t)((m - 1) * P + p - 1) * std::max(nif, 1)))
+                if (fe_apply((m - 1) * P + p, q.TEo[m - 1][p], q.FE + (size_t)((m - 1) * P + p - 1) * nifs))
                     return -3;
         for (int m = 1; m <= M; ++m) {
             MrW wr;
@@ -406,9 +476,9 @@ int mrsdc_step(Ctx &c, double tn, double dt, int step_index) {
             for (int j = 0; j < M; ++j) wr.a[j] = W.s[m - 1][j];
             for (int p = 0; p < P; ++p) wr.b[p] = W.shat[m - 1][p];
             if (vol_apply(q.TSo[m], nullptr, 0.0, q.KvTk)) return -3;                 // f^I(T^k_m)
-            const double *FEm = q.FE + (size_t)(m - 1) * P * std::max(nif, 1);
-            k_mr_rhs<<<nbk(N), 256, 0, st>>>(N, ldf, c.d_ML, q.TSn[m - 1], c.d_benv, q.KvTk, a, q.FI, FEm, c.d_if_of_row,
-                                             nif, M, P, wr, q.rhs);
+            const double *FEm = q.FE + (size_t)(m - 1) * P * nifs;
+            k_mr_rhs<<<nbk(N * S), 256, 0, st>>>(N, S, SP, ldf, c.d_ML, q.TSn[m - 1], c.d_benv, q.KvTk, a, q.FI,
+                                                 FEm, c.d_if_of_row, nif, M, P, wr, q.rhs);
             CK(cudaGetLastError());
             if (solve(q.TSo[m], q.Tstar, q.rhs)) return -3;
             if (vol_apply(q.Tstar, q.KvTk, -1.0, q.fs)) return -3;                    // f^I(T*) - f^I(T^k_m)
@@ -420,8 +490,9 @@ int mrsdc_step(Ctx &c, double tn, double dt, int step_index) {
                 const int slot = (m - 1) * P + p - 1;
                 if (fe_apply(slot, q.TEn[m - 1][p - 1], q.fe_new)) return -3;
                 if (fe_apply(slot, q.TEo[m - 1][p - 1], q.fe_old)) return -3;
-                k_mr_emb<<<nbk(N), 256, 0, st>>>(N, ldf, c.d_ML, q.TEn[m - 1][p - 1], q.fs, q.fe_new, q.fe_old, dtp, q.FI,
-                                                 FEm, c.d_if_of_row, nif, M, P, we, q.TEn[m - 1][p]);
+                k_mr_emb<<<nbk(N * S), 256, 0, st>>>(N, S, SP, ldf, c.d_ML, q.TEn[m - 1][p - 1], q.fs, q.fe_new,
+                                                     q.fe_old, dtp, q.FI, FEm, c.d_if_of_row, nif, M, P, we,
+                                                     q.TEn[m - 1][p]);
                 CK(cudaGetLastError());
             }
         }
@@ -436,7 +507,7 @@ int mrsdc_step(Ctx &c, double tn, double dt, int step_index) {
         }
     }
     // ---- commit T(t_{n+1}) = T_M
-    CK(cudaMemcpyAsync(c.d_T[c.cur ^ 1], q.TSo[M], sizeof(double) * N, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(c.d_T[c.cur ^ 1], q.TSo[M], sizeof(double) * N * SP, cudaMemcpyDeviceToDevice, st));
     c.mr_solves = solve_no;
     (void)step_index;
     return 0;
@@ -447,82 +518,75 @@ int mrsdc_step(Ctx &c, double tn, double dt, int step_index) {
 // interface Jacobian is reassembled at that node (the overhead the paper attributes to
 // single-rate SDC).  Uses the MRSDC storage with P = 1 (slots = node times).
 int sdc_step(Ctx &c, double tn, double dt, int step_index) {
-    const int M = c.mr_M, K = c.mr_K;
+    const int M = c.mr_M, K = c.mr_K, S = c.S, SP = c.SP;
     const int64_t N = c.N;
-    const int nif = c.n_if, nifs = std::max(nif, 1);
+    const int nif = c.n_if;
+    const int64_t nifs = (int64_t)std::max(nif, 1) * SP;
     const double a = dt / M;
-    const int64_t ldf = (N + 31) & ~(int64_t)31;
+    const int64_t ldf = ((N + 31) & ~(int64_t)31) * SP;
     cudaStream_t st = c.stream;
     if (c.built_dt != a) {
         if (build_operator(c, a)) return -3;
     }
+    if (S > 1 && cgb_prepare(c)) return -3;   // Jacobi block: volume diagonal, interface rows per node below
+    const double *gS = c.d_benv;   // g per (row, scenario)
+    if (S > 1) {
+        if (!c.d_benvS) CK(cudaMalloc(&c.d_benvS, sizeof(double) * (size_t)N * SP));
+        k_bcast_rows<<<nbk(N * SP), 256, 0, st>>>(c.d_benv, N, SP, c.d_benvS);
+        CK(cudaGetLastError());
+        gS = c.d_benvS;
+    }
     MrTables W;
     mr_tables(M, 1, tn, dt, W);
     const int nslot = M + 1;   // slot m = node tau_m (slot 0 = t_n, unused)
-    std::vector<double> sc(4 * (size_t)2 * nslot);
-    const Scen &sn = c.scen[0];
-    for (int q = 0; q < nslot; ++q) {
-        const double tq = tn + dt * (double)q / (double)M;
-        const double sv = sn.s0 + sn.amp * std::sin(2.0 * M_PI * tq / sn.period);
-        sc[4 * q + 0] = sv * sn.d2[0];
-        sc[4 * q + 1] = sv * sn.d2[1];
-        sc[4 * q + 2] = sn.eta0 * (1.0 + sn.eta_amp * std::sin(2.0 * M_PI * tq / sn.eta_period));
-        sc[4 * q + 3] = sv;
-    }
-    if ((int64_t)nslot > c.step_cap) {
-        for (void *p : {(void *)c.d_step_sc, (void *)c.d_iters, (void *)c.d_relres, (void *)c.d_area})
-            if (p) cudaFree(p);
-        c.step_cap = nslot;
-        CK(cudaMalloc(&c.d_step_sc, sizeof(double) * 4 * (size_t)nslot));
-        CK(cudaMalloc(&c.d_iters, sizeof(int32_t) * (size_t)nslot));
-        CK(cudaMalloc(&c.d_relres, sizeof(double) * (size_t)nslot));
-        CK(cudaMalloc(&c.d_area, sizeof(double) * (size_t)nslot));
-    }
-    CK(cudaMemcpyAsync(c.d_step_sc, sc.data(), sizeof(double) * 4 * nslot, cudaMemcpyHostToDevice, st));
+    std::vector<double> sc;
+    node_scalars(c, tn, dt, M, sc);
+    if (ensure_step_scalars(c, sc.size())) return -3;
+    CK(cudaMemcpyAsync(c.d_step_sc, sc.data(), sizeof(double) * sc.size(), cudaMemcpyHostToDevice, st));
     // unscaled K_G, b_G at the node times (for F(T^k_j, tau_j) in the quadrature), one launch set
     if (assemble_slots(c, nslot)) return -3;
-    // implicit Jacobian M_L - a K(tau_m): interface rows reassembled into the solve arrays
+    // implicit Jacobian M_L - a K(tau_m): interface rows of every scenario reassembled into the
+    // solve arrays (node-major scalars after the slot-major ones)
     auto reassemble = [&](int m) -> int {
         if (!nif) return 0;
         IfaceParams Pf;
         memset(&Pf, 0, sizeof Pf);
-        iface_params(c, Pf, c.d_step_sc + 4 * m, a);
+        iface_params(c, Pf, c.d_step_sc + 4 * (size_t)S * nslot + 4 * (size_t)m * S, a);
         return iface_launch(c, Pf);
     };
     double *T0 = c.d_T[c.cur];
     MrPtr q = mr_pointers(c, T0);
     auto fe_apply = [&](int slot, const double *x, double *y) -> int {
         if (!nif) return 0;
-        k_fe_apply<<<nbk(nif), 256, 0, st>>>(nif, slot, c.cap, c.d_ell_cnt_s, c.d_ell_col_s, c.d_ell_val_s,
-                                             c.d_if_b_s, x, y);
+        k_fe_apply<<<nbk((int64_t)nif * S), 256, 0, st>>>(nif, slot, nslot, S, SP, c.cap, c.d_ell_cnt_s,
+                                                          c.d_ell_col_s, c.d_ell_val_s, c.d_if_b_s, x, y);
         CK(cudaGetLastError());
         return 0;
     };
     auto vol_apply = [&](const double *x, const double *addv, double sgn, double *y) -> int {
-        k_vol_apply<<<nbk(N), 256, 0, st>>>(c.d_slice_ptr, c.d_col, c.d_KV, N, x, addv, sgn, y);
+        k_vol_apply<<<nbk(N * S), 256, 0, st>>>(c.d_slice_ptr, c.d_col, c.d_KV, N, S, SP, x, addv, sgn, y);
         CK(cudaGetLastError());
         return 0;
     };
     int solve_no = 0;
     auto solve = [&](const double *x0, double *x, const double *rhs) -> int {
-        const int slot = solve_no++;
-        return cg_launch_solve(c, x0, x, rhs, c.d_Dinv, nif > 0, c.d_mr_iters, c.d_mr_relres, slot);
+        return mr_solve(c, x0, x, rhs, c.d_Dinv, nif > 0, solve_no++);
     };
     MrW w0;
     memset(&w0, 0, sizeof w0);
     // ---- predictor: implicit Euler from node to node
     for (int m = 1; m <= M; ++m) {
         if (reassemble(m)) return -3;
-        k_sdc_rhs<<<nbk(N), 256, 0, st>>>(N, ldf, c.d_ML, q.TSo[m - 1], c.d_benv, nullptr, a, nullptr, nullptr, nif,
-                                          c.d_if_b_s, nslot, c.d_if_of_row, M, m, w0, q.rhs);
+        k_sdc_rhs<<<nbk(N * S), 256, 0, st>>>(N, S, SP, ldf, c.d_ML, q.TSo[m - 1], c.d_benv, nullptr, a, nullptr,
+                                              nullptr, nif, c.d_if_b_s, nslot, c.d_if_of_row, M, m, w0, q.rhs);
         CK(cudaGetLastError());
         if (solve(q.TSo[m - 1], q.TSo[m], q.rhs)) return -3;
     }
     // ---- K sweeps
     for (int k = 0; k < K; ++k) {
         for (int j = 1; j <= M; ++j) {
-            if (vol_apply(q.TSo[j], c.d_benv, 1.0, q.FI + (size_t)(j - 1) * ldf)) return -3;   // (A + B) T + b_env
-            if (fe_apply(j, q.TSo[j], q.FE + (size_t)(j - 1) * nifs)) return -3;              // K_G T + b_G
+            if (vol_apply(q.TSo[j], gS, 1.0, q.FI + (size_t)(j - 1) * ldf)) return -3;   // (A + B) T + b_env
+            if (fe_apply(j, q.TSo[j], q.FE + (size_t)(j - 1) * nifs)) return -3;               // K_G T + b_G
         }
         for (int m = 1; m <= M; ++m) {
             MrW wr;
@@ -530,14 +594,14 @@ int sdc_step(Ctx &c, double tn, double dt, int step_index) {
             for (int j = 0; j < M; ++j) wr.a[j] = W.s[m - 1][j];
             if (vol_apply(q.TSo[m], nullptr, 0.0, q.KvTk)) return -3;   // (A + B_env) T^k_m
             if (reassemble(m)) return -3;
-            k_sdc_rhs<<<nbk(N), 256, 0, st>>>(N, ldf, c.d_ML, q.TSn[m - 1], c.d_benv, q.KvTk, a, q.FI, q.FE, nif,
-                                              c.d_if_b_s, nslot, c.d_if_of_row, M, m, wr, q.rhs);
+            k_sdc_rhs<<<nbk(N * S), 256, 0, st>>>(N, S, SP, ldf, c.d_ML, q.TSn[m - 1], c.d_benv, q.KvTk, a, q.FI,
+                                                  q.FE, nif, c.d_if_b_s, nslot, c.d_if_of_row, M, m, wr, q.rhs);
             CK(cudaGetLastError());
             if (solve(q.TSo[m], q.TSn[m], q.rhs)) return -3;
         }
         for (int m = 1; m <= M; ++m) std::swap(q.TSo[m], q.TSn[m]);
     }
-    CK(cudaMemcpyAsync(c.d_T[c.cur ^ 1], q.TSo[M], sizeof(double) * N, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(c.d_T[c.cur ^ 1], q.TSo[M], sizeof(double) * N * SP, cudaMemcpyDeviceToDevice, st));
     c.mr_solves = solve_no;
     (void)step_index;
     return 0;

@@ -77,7 +77,7 @@ static void free_ctx(Ctx *c) {
                     c->d_pairs_s, c->d_pcnt_s, c->d_star_own, c->d_own_ptr, c->d_own_idx, c->d_x0, c->d_Thist, c->d_z2, c->d_q2,
                     c->d_ell_cnt_b, c->d_ell_col_b, c->d_ell_val_b, c->d_if_b_b, c->d_if_phi_b, c->d_Dinv_b,
                     c->d_step_sc_spec, c->d_spec_status, c->d_int_of_ext, c->d_stage[0], c->d_stage[1],
-                    c->d_if_d, c->d_sb_partials, c->d_sb_totals, c->d_sb_if_ptr, c->d_sb_if_k, c->d_sb_recs, c->d_sb_rec_ptr, c->d_sb_ptr8, c->d_sb_val8, c->d_sb_lcol8, c->d_sb_ai};
+                    c->d_if_d, c->d_sb_partials, c->d_sb_totals, c->d_sb_if_ptr, c->d_sb_if_k, c->d_sb_recs, c->d_sb_rec_ptr, c->d_sb_ptr8, c->d_sb_val8, c->d_sb_lcol8, c->d_sb_ai, c->d_benvS};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     for (cudaEvent_t e : c->events) cudaEventDestroy(e);
@@ -539,7 +539,8 @@ extern "C" int thermo_set_method(thermo_ctx *ctx, int32_t method, int32_t M, int
         return fail(c, THERMO_EINVAL, "method must be 0 (implicit Euler), 1 (MRSDC) or 2 (single-rate SDC)");
     if (method == 2) P = 1;
     if (M < 1 || M > 8 || P < 1 || P > 8 || K < 0) return fail(c, THERMO_EINVAL, "SDC needs 1 <= M, P <= 8, K >= 0");
-    if (c->S != 1) return fail(c, THERMO_EINVAL, "SDC methods run a single scenario");
+    if (c->S > 1 && c->sb_on)
+        return fail(c, THERMO_EINVAL, "batched SDC methods run on the default batched kernel (unset THERMO_CGB=2)");
     c->method = method;
     c->mr_M = M;
     c->mr_P = P;
@@ -605,8 +606,8 @@ extern "C" int thermo_step(thermo_ctx *ctx, double t, double dt, int32_t nsteps)
         API_CK(cudaMemsetAsync(c->d_status + 4, 0x7f, sizeof(int), c->stream));   // no overflow step yet
         if (c->method >= 1) {   // MRSDC / single-rate SDC: one step at a time, status checked per step
             c->spec_valid = false;   // these steps reuse the first interface buffer set
-            c->h_iters.assign((size_t)nsteps, 0);
-            c->h_relres.assign((size_t)nsteps, 0.0);
+            c->h_iters.assign((size_t)nsteps * S, 0);
+            c->h_relres.assign((size_t)nsteps * S, 0.0);
             c->h_area.assign(nsteps, 0.0);
             c->ms_iface = c->ms_solve = 0.0;
             for (int n = 0; n < nsteps; ++n) {
@@ -616,21 +617,22 @@ extern "C" int thermo_step(thermo_ctx *ctx, double t, double dt, int32_t nsteps)
                                     : thermo::sdc_step(*c, t + (double)n * dt, dt, n)))
                     return THERMO_ECUDA;
                 int status[8];
-                std::vector<int32_t> it(c->mr_solves);
-                std::vector<double> rr(c->mr_solves);
+                std::vector<int32_t> it((size_t)c->mr_solves * S);   // [solve][scenario]
+                std::vector<double> rr((size_t)c->mr_solves * S);
                 API_CK(cudaMemcpyAsync(status, c->d_status, sizeof status, cudaMemcpyDeviceToHost, c->stream));
                 API_CK(cudaMemcpyAsync(it.data(), c->d_mr_iters, sizeof(int32_t) * it.size(), cudaMemcpyDeviceToHost, c->stream));
                 API_CK(cudaMemcpyAsync(rr.data(), c->d_mr_relres, sizeof(double) * rr.size(), cudaMemcpyDeviceToHost, c->stream));
                 API_CK(cudaStreamSynchronize(c->stream));
                 c->last_nsteps = n + 1;
-                for (int j = 0; j < c->mr_solves; ++j) {
-                    c->h_iters[n] += it[j];
-                    c->h_relres[n] = std::max(c->h_relres[n], rr[j]);
-                }
+                for (int j = 0; j < c->mr_solves; ++j)
+                    for (int q = 0; q < S; ++q) {
+                        c->h_iters[(size_t)n * S + q] += it[(size_t)j * S + q];
+                        c->h_relres[(size_t)n * S + q] = std::max(c->h_relres[(size_t)n * S + q], rr[(size_t)j * S + q]);
+                    }
                 if (status[0] || status[1]) {
                     c->failed_step = n;
-                    c->failed_scen = 0;
-                    c->failed_relres = c->h_relres[n];
+                    c->failed_scen = status[0] ? status[3] : 0;
+                    c->failed_relres = c->h_relres[(size_t)n * S + std::max(0, std::min(S - 1, c->failed_scen))];
                     c->last_nsteps = n;
                     return fail(c, status[1] ? THERMO_EGEOM : THERMO_ENOCONV,
                                 (c->method == 1 ? "MRSDC step " : "SDC step ") + std::to_string(n) +
