@@ -105,3 +105,25 @@ def test_batched_sdc_methods_every_column_vs_oracle(method, M, P, K):
         ts.set_T(T0)
         ts.step(1.0, cfg.dt, nsteps)
         assert rel(tb.get_T(scen=k), ts.get_T()) <= 1e-11, k
+
+
+def test_batched_work_precision_harness():
+    """tools/work_precision_batched.py on a small batch: every method class runs
+    batched; errors fall with dt for each class, the corrected SDC methods beat implicit Euler at
+    equal dt, and one batched run advances all variants together."""
+    import importlib.util
+    import os
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools",
+                        "work_precision_batched.py")
+    spec = importlib.util.spec_from_file_location("wpb", path)
+    wpb = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(wpb)
+    rows, head = wpb.work_precision(S=4, t_end=8.0, dts=(2.0, 1.0), sweeps=(1, 2))
+    by = {}
+    for r in rows:
+        by.setdefault(r["method"], {})[r["dt"]] = r["err_max"]
+    assert set(by) == {"implicit Euler", "SDC(3) k=1", "SDC(3) k=2", "MRSDC(3,2) k=1", "MRSDC(3,2) k=2"}
+    for m, e in by.items():
+        assert e[1.0] < e[2.0], (m, e)
+    for m in ("SDC(3) k=2", "MRSDC(3,2) k=2"):
+        assert by[m][1.0] < by["implicit Euler"][1.0], (m, by)
