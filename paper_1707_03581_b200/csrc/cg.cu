@@ -33,6 +33,7 @@
 #include <vector>
 
 #include "ctx.h"
+#include "cg_params.h"
 
 namespace cg = cooperative_groups;
 
@@ -54,50 +55,8 @@ namespace thermo {
 #define CG_GAP_LARGE 512  // fewer, longer window copies: cfg 3 403 -> 399 us per iteration, while
                           // cfg 2 is 1 % slower with them (55.3 -> 56.0 us)
 
-struct CGParams {
-    int64_t N, nslices, nchunks;
-    const int64_t *slice_ptr;
-    const int32_t *col;
-    const uint16_t *lcol;      // KIND 2: chunk-local 16-bit columns (same layout as col)
-    const double *val;
-    const double *ML, *benv, *Dinv;
-    int n_if, nA;
-    const int32_t *if_rows, *slice_if, *ell_cnt, *ell_col;
-    const double *ell_val, *if_b, *if_phi;
-    const double *T_in;
-    const double *X0;          // optional initial guess (extrapolated state); nullptr: x0 = T_in
-    const double *rhs;         // optional explicit right-hand side (MRSDC implicit solves)
-    double *T_out, *z, *pa, *pb, *q;
-    double *z2, *q2;           // FUSED: second buffer set of z and q' (p uses pa / pb)
-    double *partials;
-    int *status;
-    double *fail_relres;
-    int32_t *iters_out;
-    double *relres_out, *area_out;
-    double dt, rtol2;
-    int maxit, step;
-    int stage_entries;         // TMA: matrix entries per stage
-    int nstages;               // TMA: ring stages (<= 8)
-    int64_t u_rows;            // TMA: rows per update-phase chunk (4 streams per stage)
-    int win_cap;               // KIND 2: window entries per vector per stage
-    const int32_t *chunk_hi;   // TMA: largest column index referenced by each chunk
-    const int2 *chunk_runs;    // KIND 2: [nchunks][CG_MAXR] (start, length) of the window runs
-    const int32_t *chunk_nruns;
-    const int32_t *chunk_lown;  // KIND 2: window-local index of the chunk's first row
-    const double *pf[4];       // vectors whose leading edge is prefetched into L2
-    int npf;
-    const double *wv[3];       // KIND 2: vectors staged through the window (nwv <= nwin)
-    int nwv;
-    int nwin;                  // KIND 2: window slots of the stage layout (1, FUSED: 3)
-    const double *ownv;        // KIND 2: vector of which only the chunk's own rows are staged
-                               // (after the window, W * 32 rows)
-    unsigned long long *trace; // optional: %globaltimer after every grid barrier (CTA 0)
-    int trace_fine;            // fused kernel: also at the iteration start, sweep end, CTA reduction
-    int prefetch;              // L2 leading-edge prefetch (THERMO_CG_PREFETCH=1; measured slower on cfg3)
-    int debug;                 // THERMO_CG_DEBUG bits (measurement only, results invalid):
-                               // 1 consumers skip the row work, 2 no window copies, 4 no prefetch,
-                               // 8 no q' store
-};
+// CGParams: cg_params.h
+
 
 // Prefetch into L2 the leading edge of the column window of a chunk whose largest column
 // index is hi_col: rows [hi_col - len + 1, hi_col] of each vector in pf (len = rows of the
@@ -1187,7 +1146,7 @@ int cg_setup(Ctx &c) {
         if (g >= 1 && g < c.cg_grid) c.cg_grid = g;
     }
     CK(cudaMalloc(&c.d_partials, sizeof(double) * THERMO_NRED * c.cg_grid));
-    return 0;
+    return cl_setup(c);   // small problems: the single-cluster latency solve (cg_cluster.cu)
 }
 
 int cg_launch_solve(Ctx &c, const double *x0, double *x, const double *rhs, const double *Dinv, bool iface,
@@ -1242,6 +1201,7 @@ int cg_launch_solve(Ctx &c, const double *x0, double *x, const double *rhs, cons
     P.chunk_nruns = c.d_chunk_nruns;
     P.chunk_lown = c.d_chunk_lown;
     P.trace = nullptr;
+    if (c.cl_on) return cl_launch(c, P, false, 0);
     void *args[] = {&P};
     CK(cudaLaunchCooperativeKernel(variant_kernel(c.cg_variant), dim3(c.cg_grid), dim3(c.cg_block), args,
                                    c.cg_smem, c.stream));
@@ -1302,6 +1262,7 @@ int cg_launch_step(Ctx &c, int step, double dt, const double *x0, int buf, bool 
     P.trace_fine = c.d_trace && getenv("THERMO_CG_TRACE") && atoi(getenv("THERMO_CG_TRACE")) == 2;
     P.debug = c.cg_debug;
     P.prefetch = c.cg_prefetch;
+    if (c.cl_on) return cl_launch(c, P, ovl, buf);
     void *args[] = {&P};
     if (ovl) {   // cooperative launch that records ev_cg[step & 1] once all of its CTAs have begun
         cudaLaunchAttribute at[2];

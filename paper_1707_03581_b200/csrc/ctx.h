@@ -108,6 +108,10 @@ struct Ctx {
     int32_t *d_chunk_lown = nullptr;
     unsigned long long *d_trace = nullptr;   // THERMO_CG_TRACE=1: barrier timestamps of the last solve
     int cg_win_cap = 0, cg_nstages = 1, cg_max_runs = 0;
+    bool cl_on = false;              // single-cluster latency solve (cg_cluster.cu) for small N
+    double *d_cl_ai = nullptr;       // its interface sums (2 n_if)
+    int64_t cl_rows = 0;
+    size_t cl_smem = 0;
     int64_t cg_u_rows = 0;
     int *d_chunk_ctr = nullptr;
 
@@ -194,6 +198,10 @@ struct Ctx {
     double *d_stage[2] = {nullptr, nullptr};
     int64_t ver[2] = {0, 0}, stage_ver[2] = {-1, -1};
 
+    // pinned host staging of a call's time scalars and status readback (thermo.cu: pin_reserve)
+    void *h_pin = nullptr;
+    size_t h_pin_bytes = 0;
+
     // stats of the last thermo_step
     int last_nsteps = 0;
     int64_t last_launches = 0;       // kernels launched by the last implicit-Euler thermo_step
@@ -218,6 +226,10 @@ int iface_launch(Ctx &c, const IfaceParams &p, cudaStream_t stream = nullptr);
 
 // cg.cu
 int cg_setup(Ctx &c);
+// cg_cluster.cu (single-cluster latency solve; cl_setup decides, cl_launch replaces the grid launch)
+struct CGParams;
+int cl_setup(Ctx &c);
+int cl_launch(Ctx &c, CGParams &P, bool ovl, int buf);
 // chunk windows of the current pattern (W slices per chunk, runs merged below `gap`);
 // stats: [0] max window entries, [1] max runs, [2] flags (too many entries / window too wide)
 void chunk_windows_launch(Ctx &c, int W, int gap, int2 *runs, int32_t *nruns, int32_t *lown, uint16_t *lcol,

@@ -34,6 +34,19 @@ struct DevBuf {
     ~DevBuf() { if (p) cudaFree(p); }
 };
 
+// Pinned host staging of the per-call scalars and status (>= bytes): transfers from / to
+// pinned memory are asynchronous DMA; from pageable memory every copy stalls the host.
+static cudaError_t pin_reserve(Ctx *c, size_t bytes) {
+    if (bytes <= c->h_pin_bytes) return cudaSuccess;
+    if (c->h_pin) cudaFreeHost(c->h_pin);
+    c->h_pin = nullptr;
+    c->h_pin_bytes = 0;
+    const size_t nb = std::max(bytes, (size_t)64 * 1024);
+    cudaError_t e = cudaHostAlloc(&c->h_pin, nb, cudaHostAllocDefault);
+    if (e == cudaSuccess) c->h_pin_bytes = nb;
+    return e;
+}
+
 static int fail(Ctx *c, int code, const std::string &msg) {
     c->err = msg;
     return code;
@@ -77,9 +90,10 @@ static void free_ctx(Ctx *c) {
                     c->d_pairs_s, c->d_pcnt_s, c->d_star_own, c->d_own_ptr, c->d_own_idx, c->d_x0, c->d_Thist, c->d_z2, c->d_q2,
                     c->d_ell_cnt_b, c->d_ell_col_b, c->d_ell_val_b, c->d_if_b_b, c->d_if_phi_b, c->d_Dinv_b,
                     c->d_step_sc_spec, c->d_spec_status, c->d_int_of_ext, c->d_stage[0], c->d_stage[1],
-                    c->d_if_d, c->d_sb_partials, c->d_sb_totals, c->d_sb_if_ptr, c->d_sb_if_k, c->d_sb_recs, c->d_sb_rec_ptr, c->d_sb_ptr8, c->d_sb_val8, c->d_sb_lcol8, c->d_sb_ai, c->d_benvS};
+                    c->d_if_d, c->d_sb_partials, c->d_sb_totals, c->d_sb_if_ptr, c->d_sb_if_k, c->d_sb_recs, c->d_sb_rec_ptr, c->d_sb_ptr8, c->d_sb_val8, c->d_sb_lcol8, c->d_sb_ai, c->d_benvS, c->d_cl_ai};
     for (void *p : ptrs)
         if (p) cudaFree(p);
+    if (c->h_pin) cudaFreeHost(c->h_pin);
     for (cudaEvent_t e : c->events) cudaEventDestroy(e);
     for (cudaEvent_t e : c->events_if) cudaEventDestroy(e);
     if (c->if_stream) {
@@ -586,8 +600,15 @@ extern "C" int thermo_step(thermo_ctx *ctx, double t, double dt, int32_t nsteps)
             API_CK(cudaMalloc(&c->d_relres, sizeof(double) * S * (size_t)nsteps));
             API_CK(cudaMalloc(&c->d_area, sizeof(double) * (size_t)nsteps));
         }
-        // time scalars, fully implicit: everything at t' = t + (n+1) dt (reading R3)
-        std::vector<double> sc(4 * (size_t)S * nsteps);
+        // time scalars, fully implicit: everything at t' = t + (n+1) dt (reading R3); staged in
+        // pinned memory after the status block of the readback (below)
+        const size_t n_sc = 4 * (size_t)S * nsteps, n_st = (size_t)nsteps * S;
+        const size_t off_sc = 0, off_st = (n_sc * 8 + 63) & ~(size_t)63;     // [status 8 int | frel]
+        const size_t off_it = off_st + 64, off_rr = off_it + ((n_st * 4 + 63) & ~(size_t)63);
+        const size_t off_ar = off_rr + n_st * 8, pin_bytes = off_ar + (size_t)nsteps * 8 + 64;
+        API_CK(pin_reserve(c, pin_bytes));
+        unsigned char *pin = reinterpret_cast<unsigned char *>(c->h_pin);
+        double *sc = reinterpret_cast<double *>(pin + off_sc);
         for (int n = 0; n < nsteps; ++n) {
             const double tp = t + (double)(n + 1) * dt;
             for (int s = 0; s < S; ++s) {
@@ -601,7 +622,7 @@ extern "C" int thermo_step(thermo_ctx *ctx, double t, double dt, int32_t nsteps)
                 o[3] = sv;
             }
         }
-        API_CK(cudaMemcpyAsync(c->d_step_sc, sc.data(), sizeof(double) * sc.size(), cudaMemcpyHostToDevice, c->stream));
+        API_CK(cudaMemcpyAsync(c->d_step_sc, sc, sizeof(double) * n_sc, cudaMemcpyHostToDevice, c->stream));
         API_CK(cudaMemsetAsync(c->d_status, 0, sizeof(int) * 8, c->stream));
         API_CK(cudaMemsetAsync(c->d_status + 4, 0x7f, sizeof(int), c->stream));   // no overflow step yet
         if (c->method >= 1) {   // MRSDC / single-rate SDC: one step at a time, status checked per step
@@ -773,17 +794,23 @@ extern "C" int thermo_step(thermo_ctx *ctx, double t, double dt, int32_t nsteps)
         }
         c->last_launches = launches;
         if (c->timing) API_CK(cudaEventRecord(c->events[2 * nsteps], c->stream));
-        int status[8];
-        c->h_iters.assign((size_t)nsteps * S, 0);
-        c->h_relres.assign((size_t)nsteps * S, 0.0);
-        c->h_area.assign(nsteps, 0.0);
-        API_CK(cudaMemcpyAsync(status, c->d_status, sizeof status, cudaMemcpyDeviceToHost, c->stream));
-        API_CK(cudaMemcpyAsync(c->h_iters.data(), c->d_iters, sizeof(int32_t) * c->h_iters.size(), cudaMemcpyDeviceToHost, c->stream));
-        API_CK(cudaMemcpyAsync(c->h_relres.data(), c->d_relres, sizeof(double) * c->h_relres.size(), cudaMemcpyDeviceToHost, c->stream));
-        API_CK(cudaMemcpyAsync(c->h_area.data(), c->d_area, sizeof(double) * c->h_area.size(), cudaMemcpyDeviceToHost, c->stream));
-        double frel = 0.0;
-        API_CK(cudaMemcpyAsync(&frel, c->d_fail_relres, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        // status readback: asynchronous copies into the pinned block, one synchronisation
+        int *pst = reinterpret_cast<int *>(pin + off_st);
+        double *pfr = reinterpret_cast<double *>(pin + off_st + 32);
+        int32_t *pit = reinterpret_cast<int32_t *>(pin + off_it);
+        double *prr = reinterpret_cast<double *>(pin + off_rr), *par = reinterpret_cast<double *>(pin + off_ar);
+        API_CK(cudaMemcpyAsync(pst, c->d_status, sizeof(int) * 8, cudaMemcpyDeviceToHost, c->stream));
+        API_CK(cudaMemcpyAsync(pit, c->d_iters, sizeof(int32_t) * n_st, cudaMemcpyDeviceToHost, c->stream));
+        API_CK(cudaMemcpyAsync(prr, c->d_relres, sizeof(double) * n_st, cudaMemcpyDeviceToHost, c->stream));
+        API_CK(cudaMemcpyAsync(par, c->d_area, sizeof(double) * nsteps, cudaMemcpyDeviceToHost, c->stream));
+        API_CK(cudaMemcpyAsync(pfr, c->d_fail_relres, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
         API_CK(cudaStreamSynchronize(c->stream));
+        int status[8];
+        memcpy(status, pst, sizeof status);
+        const double frel = *pfr;
+        c->h_iters.assign(pit, pit + n_st);
+        c->h_relres.assign(prr, prr + n_st);
+        c->h_area.assign(par, par + nsteps);
         c->last_nsteps = nsteps;
         c->ms_iface = c->ms_solve = 0.0;
         if (c->timing) {
@@ -807,7 +834,18 @@ extern "C" int thermo_step(thermo_ctx *ctx, double t, double dt, int32_t nsteps)
             for (int j = 0; j < S; ++j) it = std::max(it, (int)c->h_iters[(size_t)(nsteps - 1) * S + j]);
             double s_ns = 0, u_ns = 0;
             const char *tv = getenv("THERMO_CG_TRACE");
-            if (S > 1 && c->sb_on && tv && atoi(tv) == 3) {   // batched SpMM kernel, 6 stamps per iteration
+            if (S == 1 && c->cl_on) {   // cluster solve: stamps after S + reduction and after U + sync
+                double sa = 0, ua = 0;
+                const int m = std::min(it, 499);
+                for (int k = 0; k < m; ++k) {
+                    sa += (double)(tr[2 + 2 * k] - tr[1 + 2 * k]);
+                    ua += (double)(tr[3 + 2 * k] - tr[2 + 2 * k]);
+                }
+                if (m > 0)
+                    fprintf(stderr, "[thermo trace] cluster solve: phase0 %.2f us, S + reduction %.2f us, U + sync %.2f us "
+                            "per iteration (%d iters)\n", (tr[1] - tr[0]) * 1e-3, sa * 1e-3 / m, ua * 1e-3 / m, m);
+                it = 0;
+            } else if (S > 1 && c->sb_on && tv && atoi(tv) == 3) {   // batched SpMM kernel, 6 stamps per iteration
                 // phase 0: start, sweep+pass.. (4 stamps in reduce incl. the trailing one) -- layout:
                 // [0] start, [1] P0 partials, [2] P0 sync1, [3] P0 end; per iteration: sweep end,
                 // pass end... see cg_spmm.cu: sweep, iface, partials, sync1, (reduce end), U end
