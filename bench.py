@@ -287,6 +287,8 @@ def run_thermo(args):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic,
                      "kernel": ("k_cg_step (persistent Jacobi-PCG, one launch per step)" if S == 1 else
+                                "k_sbcg_step (persistent batched Jacobi-PCG, windowed SpMM over column groups "
+                                "of 16 scenarios, one launch per step)" if st.get("solve_kind") == 3 else
                                 "k_cgb_step (persistent batched Jacobi-PCG over all scenarios, one launch per step)"),
                      "peak_kind": peak_kind, "achieved_vs_8TBs": achieved / 8000.0,
                      "solve_share_of_step": st["ms_solve"] / ms,

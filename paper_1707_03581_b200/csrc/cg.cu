@@ -411,6 +411,11 @@ __device__ __forceinline__ void sweep(const CGParams &P, Ring &R, Body &&body) {
             const int64_t e1 = __shfl_sync(0xffffffffu, cur.ptr, W);
             if (lane == 0) mbar_wait(&R.empty[st], ph ^ 1u);
             __syncwarp();
+            // the consumers' generic-proxy reads of this stage (released through the empty
+            // barrier) before this warp's async-proxy bulk writes into it: without the fence a
+            // copy can land while a consumer's shared-memory load of the previous chunk is still
+            // outstanding (seen as rare stale values in the batched kernel, cg_spmm.cu)
+            fence_proxy_async_smem();
             unsigned char *sb = R.stage + (size_t)st * R.stage_bytes;
             int *hdr = reinterpret_cast<int *>(sb);
             if (lane <= W) {
@@ -533,6 +538,7 @@ __device__ __forceinline__ void sweep_u(const CGParams &P, Ring &R, const double
             }
             if (lane == 0) {
                 mbar_wait(&R.empty[st], ph ^ 1u);
+                fence_proxy_async_smem();   // consumers' reads of the stage before the bulk writes
                 unsigned char *sb = R.stage + (size_t)st * R.stage_bytes;
                 int *hdr = reinterpret_cast<int *>(sb);
                 hdr[31] = (int)ch;

@@ -551,6 +551,10 @@ int cgb_setup(Ctx &c) {
     if (int rc = build_if_of_row(c)) return rc;
     if (int rc = sbcg_setup(c)) return rc;
     if (c.sb_on) return 0;   // windowed SpMM kernel (cg_spmm.cu)
+    return cgb_gather_setup(c);
+}
+
+int cgb_gather_setup(Ctx &c) {
     int per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cgb_step, CGB_BLOCK, 0));
     if (per_sm < 1) { c.err = "batched CG kernel cannot be resident"; return -3; }
@@ -607,7 +611,7 @@ static void cgb_params(Ctx &c, CGBParams &P) {
 // Solve with an explicit right-hand side block (SDC / MRSDC implicit stages, every scenario)
 int cgb_launch_solve(Ctx &c, const double *x0, double *x, const double *rhs, bool iface, int32_t *iters_out,
                      double *relres_out, int slot) {
-    if (c.sb_on) { c.err = "SDC methods need the default batched kernel (THERMO_CGB != 2)"; return -1; }
+    if (c.sb_on) { c.err = "internal: explicit-rhs solve on the windowed SpMM kernel (sbcg_disable first)"; return -1; }
     CGBParams P;
     cgb_params(c, P);
     P.T_in = x0;

@@ -108,7 +108,11 @@ struct SBParams {
     int trace_fine;   // THERMO_CG_TRACE=3: stamps after the sweep, the interface pass, the CTA
                       // partials and the first grid barrier of every reduction (CTA 0)
     int debug;   // THERMO_CGB_DEBUG bits (measurement only, results invalid): 1 consumers skip the
-                 // row sums, 2 no window copies, 4 no epilogue (post)
+                 // row sums, 2 no window copies, 4 no epilogue (post), 8 no copies at all; (results
+                 // valid:) 16 no interface gathers during the sweep; with -DSB_STAGE_CHECKS: 64
+                 // consumers check the values they kept for their own rows against global memory
+                 // (sb_check_light), 128 every value of every stage (sb_check), mismatches printed
+    int *dbg;    // [4] mismatch counter of sb_check
 };
 
 __device__ __forceinline__ int64_t brow(const SBParams &P, int g, int64_t i) {   // first element of row i, group g
@@ -205,6 +209,75 @@ __device__ __forceinline__ void sb_iface_gather(const SBParams &P, const double 
     }
 }
 
+#ifdef SB_STAGE_CHECKS   // compiled in for diagnosis only: the checks change the consumers' code
+// Debug (THERMO_CGB_DEBUG bit 128): compare what a consumer warp reads from a stage with the
+// global memory the producer copied it from -- matrix values and columns (constant), the window
+// rows of w, the own rows of ownv, D^{-1} -- and print the first mismatches.
+__device__ __noinline__ void sb_check(const SBParams &P, uint32_t k, const unsigned char *sb, const double *w,
+                                      const double *ownv, int64_t s, int wd, int g) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, h = lane >> 4, l = lane & 15;
+    const SBRec &rec = P.recs[P.rec_ptr[blockIdx.x] + k];
+    const double *vals = reinterpret_cast<const double *>(sb + SB_HDR);
+    const uint16_t *lc = reinterpret_cast<const uint16_t *>(sb + P.col_off);
+    const double *win = reinterpret_cast<const double *>(sb + P.win_off);
+    const double *own = reinterpret_cast<const double *>(sb + P.own_off);
+    const double *dv = reinterpret_cast<const double *>(sb + P.aux_off);
+    auto report = [&](int kind, int r, int e, int cidx, int64_t grow, double a, double b) {
+        const int c = atomicAdd(P.dbg, 1);
+        if (c < 16)
+            printf("[sbchk] kind %d step %d cta %d chunk %u slice %lld (rec %d) row %d e %d cidx %d grow %lld l %d "
+                   "stage %.17g global %.17g\n", kind, P.step, (int)blockIdx.x, k, (long long)s, rec.s, r, e, cidx,
+                   (long long)grow, l, a, b);
+    };
+    if (rec.s != s) report(0, -1, -1, -1, -1, 0.0, 0.0);
+    for (int pp = 0; pp < SB_RPW / 2; ++pp) {
+        const int r = warp * SB_RPW + 2 * pp + h;
+        const int64_t i = 32 * s + r;
+        if (i >= P.N || l >= P.CW) continue;
+        for (int kk = 0; kk < wd; ++kk) {
+            const int e = r * wd + kk;
+            const double gv = P.val[rec.e0 + e];
+            if (__double_as_longlong(vals[e]) != __double_as_longlong(gv)) report(1, r, e, -1, -1, vals[e], gv);
+            const int cidx = lc[e];
+            if (cidx != P.lcol[rec.e0 + e]) report(2, r, e, cidx, -1, cidx, P.lcol[rec.e0 + e]);
+            int off = 0;
+            int64_t grow = -1;
+            for (int q = 0; q < rec.nruns; ++q) {
+                if (cidx < off + rec.run[q].y) { grow = rec.run[q].x + cidx - off; break; }
+                off += rec.run[q].y;
+            }
+            if (grow < 0) { report(3, r, e, cidx, grow, 0.0, 0.0); continue; }
+            const double a = win[cidx * P.CW + l], b = ld_cg1(w + brow(P, g, grow) + l);
+            if (__double_as_longlong(a) != __double_as_longlong(b)) report(4, r, e, cidx, grow, a, b);
+        }
+        const double a = own[r * P.CW + l], b = ld_cg1(ownv + brow(P, g, i) + l);
+        if (__double_as_longlong(a) != __double_as_longlong(b)) report(5, r, -1, -1, i, a, b);
+        if (__double_as_longlong(dv[r]) != __double_as_longlong(P.Dinv[i])) report(6, r, -1, -1, i, dv[r], P.Dinv[i]);
+    }
+}
+
+// Debug (bit 64, cheap, after the release): the values a consumer kept from the stage for its
+// own rows (p of the row from the window, ownv, D^{-1}, the diagonal) against global memory.
+__device__ __noinline__ void sb_check_light(const SBParams &P, uint32_t k, const double *w, const double *ownv,
+                                            int64_t s, int wd, int g, int r, double pw, double ow, double dinv,
+                                            double diag) {
+    const int l = threadIdx.x & 15;
+    const int64_t i = 32 * s + r;
+    const SBRec &rec = P.recs[P.rec_ptr[blockIdx.x] + k];
+    const double v[4] = {ld_cg1(w + brow(P, g, i) + l), ld_cg1(ownv + brow(P, g, i) + l), P.Dinv[i],
+                         P.val[rec.e0 + r * wd]};
+    const double u[4] = {pw, ow, dinv, diag};
+    for (int q = 0; q < 4; ++q)
+        if (__double_as_longlong(u[q]) != __double_as_longlong(v[q])) {
+            const int c = atomicAdd(P.dbg, 1);
+            if (c < 16)
+                printf("[sbchk-light] kind %d step %d cta %d chunk %u slice %lld row %d l %d stage %.17g global %.17g\n",
+                       q, P.step, (int)blockIdx.x, k, (long long)s, r, l, u[q], v[q]);
+        }
+}
+
+#endif
+
 // One sweep over the slices of this CTA's column group g = b % G (slices b / G + k Gw / G,
 // a static order).  Stage = [hdr | values | 16-bit window columns | window of w (runs) | own
 // rows of ownv | D^{-1} of the slice's rows | interface index of the slice's rows].  Consumers
@@ -294,6 +367,11 @@ __device__ __forceinline__ void sb_sweep(const SBParams &P, SBRing &R, const dou
                 mbar_arrive(&R.full[st]);
             } else if (lane == 0) {
                 mbar_wait(&R.empty[st], ph ^ 1u);
+#ifndef SB_EXPERIMENT_EARLY_RELEASE
+                // generic-proxy reads of this stage by the consumers (released through the empty
+                // barrier) before the async-proxy writes into it (PTX: a proxy fence between them)
+                fence_proxy_async_smem();
+#endif
                 hdr[0] = (int)(cnt >> 5);
                 hdr[1] = lown;
                 hdr[31] = s;
@@ -306,6 +384,9 @@ __device__ __forceinline__ void sb_sweep(const SBParams &P, SBRing &R, const dou
                 bulk_g2s_nohint(sb + P.aux_off + 256, P.if_of_row + r0, 128u, &R.full[st]);
             }
             __syncwarp();
+#ifndef SB_EXPERIMENT_EARLY_RELEASE
+            if (len) fence_proxy_async_smem();   // the same for the lanes copying the window
+#endif
             if (len && !(P.debug & 10))
                 bulk_g2s_nohint(sb + P.win_off + (size_t)woff * P.CW * 8, w + brow(P, g, run.x),
                                 (uint32_t)len * (uint32_t)P.CW * 8u, &R.full[st]);
@@ -397,12 +478,32 @@ __device__ __forceinline__ void sb_sweep(const SBParams &P, SBRing &R, const dou
                 x.ik = ifr[r];
             }
         }
+#ifdef SB_STAGE_CHECKS
+        if (P.debug & 128) sb_check(P, R.n - base, sb, w, ownv, s, wd, g);
+        if (P.debug & 64)
+#pragma unroll
+            for (int pp = 0; pp < SB_RPW / 2; ++pp)
+                if (ok_[pp])
+                    sb_check_light(P, R.n - base, w, ownv, s, wd, g, rr_[pp], rw[pp].pw, rw[pp].own, rw[pp].dinv,
+                                   rw[pp].diag);
+#endif
+#ifdef SB_EXPERIMENT_EARLY_RELEASE   // the round-2 order (measurement of the race only)
         __syncwarp();
-        if (lane == 0) mbar_arrive(&R.empty[st]);   // the stage is free again
-        ++R.n;
+        if (lane == 0) mbar_arrive(&R.empty[st]);
+#endif
+        // the epilogue (global stores) consumes every value read from the stage; only then is
+        // the stage released.  Released right after the loads, the producer's next bulk copy into
+        // the stage could overtake a still outstanding shared-memory load (the arrive does not
+        // wait for them): about one cfg-4 run in three had one stale row somewhere
+        // (tools/diag_spmm_race.py; located with the SB_STAGE_CHECKS build)
 #pragma unroll
         for (int pp = 0; pp < SB_RPW / 2; ++pp)
             if (rw[pp].i < P.N && lok && !(P.debug & 5)) post(rw[pp], g, l);
+#ifndef SB_EXPERIMENT_EARLY_RELEASE
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&R.empty[st]);   // the stage is free again
+#endif
+        ++R.n;
     }
 }
 
@@ -721,13 +822,10 @@ static size_t a16(size_t x) { return (x + 15) & ~(size_t)15; }
 // numbering / sizes do not fit (the gather kernel of cg_batched.cu is used then).
 int sbcg_setup(Ctx &c) {
     c.sb_on = false;
-    // THERMO_CGB=2 selects this kernel; the default is the gather kernel (cg_batched.cu).  Measured
-    // on configs[4]: 152 vs 179 us per CG iteration, and bitwise equal to the gather kernel over
-    // 500 steps in most runs -- but about one full run in four (after other contexts ran in the
-    // process) ends up to 2e-6 away from the oracle in one column group, a rare race not yet
-    // found; so it stays opt-in.
+    // the default batched kernel; THERMO_CGB=1 selects the gather kernel (cg_batched.cu), which
+    // is also the fallback when the numbering or the sizes do not fit (below)
     const char *ev = getenv("THERMO_CGB");
-    if (!ev || atoi(ev) != 2) return 0;
+    if (ev && atoi(ev) == 1) return 0;
     if (c.S > SB_MAXS) return 0;
     const int CW = c.SP > SB_CW ? SB_CW : c.SP;
     const int G = c.SP / CW;
@@ -843,6 +941,8 @@ int sbcg_setup(Ctx &c) {
     }
     CK(cudaMalloc(&c.d_sb_partials, sizeof(double) * SB_M * (size_t)c.num_sms));
     CK(cudaMalloc(&c.d_sb_totals, sizeof(double) * 2 * SB_M));
+    CK(cudaMalloc(&c.d_sb_dbg, sizeof(int) * 4));
+    CK(cudaMemset(c.d_sb_dbg, 0, sizeof(int) * 4));
     if (!c.d_if_d && c.n_if) CK(cudaMalloc(&c.d_if_d, sizeof(double) * (size_t)c.S * c.n_if));
     c.sb_on = true;
     c.CW = CW;
@@ -863,6 +963,31 @@ int sbcg_setup(Ctx &c) {
         fprintf(stderr, "[thermo cgb] windowed SpMM: CW %d, G %d, window cap %d rows (max runs %d), stage %zu B, "
                         "%d stages, smem %zu B\n", CW, G, wc, stats[1], stage, ns, smem);
     return 0;
+}
+
+// [G][N][CW] column groups -> [N][SP] rows (the gather kernel's layout)
+__global__ void k_sb_to_rows(const double *__restrict__ in, int64_t N, int CW, int SP, double *__restrict__ out) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= N * SP) return;
+    const int64_t i = t / SP;
+    const int s = (int)(t % SP);
+    out[t] = in[((int64_t)(s / CW) * N + i) * CW + s % CW];
+}
+
+// Switch a batched context from this kernel to the gather kernel (the SDC methods run on the
+// latter): the current state moves to the row layout; the extrapolation history is dropped.
+int sbcg_disable(Ctx &c) {
+    if (!c.sb_on) return 0;
+    const int64_t n = c.N * c.SP;
+    double *cur = c.d_T[c.cur];
+    k_sb_to_rows<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(cur, c.N, c.CW, c.SP, c.d_q);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(cur, c.d_q, sizeof(double) * n, cudaMemcpyDeviceToDevice, c.stream));
+    c.sb_on = false;
+    c.CW = c.SP;
+    c.hist = 0;
+    if (int rc = cgb_gather_setup(c)) return rc;
+    return c.built_dt > 0.0 ? cgb_prepare(c) : 0;
 }
 
 int sbcg_launch_step(Ctx &c, int step, double dt, const double *x0) {
@@ -925,6 +1050,7 @@ int sbcg_launch_step(Ctx &c, int step, double dt, const double *x0) {
     P.aux_off = c.sb_aux_off;
     P.trace = c.d_trace;
     P.trace_fine = getenv("THERMO_CG_TRACE") && atoi(getenv("THERMO_CG_TRACE")) == 3;
+    P.dbg = c.d_sb_dbg;
     void *args[] = {&P};
     CK(cudaLaunchCooperativeKernel((const void *)k_sbcg_step, dim3(c.cg_grid), dim3(SB_THREADS), args, c.sb_smem,
                                    c.stream));

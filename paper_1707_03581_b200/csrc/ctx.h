@@ -183,6 +183,7 @@ struct Ctx {
     int32_t *d_sb_if_ptr = nullptr, *d_sb_if_k = nullptr;   // interface rows per CTA
     void *d_sb_recs = nullptr;                              // packed chunk metadata per CTA
     int32_t *d_sb_rec_ptr = nullptr;
+    int *d_sb_dbg = nullptr;                                // sb_check mismatch counter (debug)
     double *d_sb_ai = nullptr;                              // interface sums of a sweep
     int64_t *d_sb_ptr8 = nullptr;                           // row-major operator copy per slice
     double *d_sb_val8 = nullptr;
@@ -258,7 +259,9 @@ int cgb_launch_solve(Ctx &c, const double *x0, double *x, const double *rhs, boo
                      double *relres_out, int slot);
 
 // cg_spmm.cu (S > 1: windowed SpMM kernel, selected by cgb_setup when the windows fit)
+int cgb_gather_setup(Ctx &c);   // grid and buffers of the gather kernel
 int sbcg_setup(Ctx &c);
+int sbcg_disable(Ctx &c);   // switch a batched context to the gather kernel (state re-laid out)
 int sbcg_launch_step(Ctx &c, int step, double dt, const double *x0);
 int sbcg_prepare(Ctx &c);   // after every rebuild of K~_vol
 

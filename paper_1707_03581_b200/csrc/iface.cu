@@ -883,7 +883,7 @@ void iface_params(Ctx &c, IfaceParams &P, const double *step_sc, double dt, int 
     P.if_phi = buf ? c.d_if_phi_b : c.d_if_phi;
     P.Dinv = buf ? c.d_Dinv_b : c.d_Dinv;
     P.if_dinv = c.d_if_dinv;
-    P.if_d = c.d_if_d;
+    P.if_d = c.sb_on ? c.d_if_d : nullptr;   // per-scenario d, 1/d of the windowed SpMM kernel
     P.DinvS = c.d_DinvS;
     P.SP = c.SP;
     P.status = c.d_status;

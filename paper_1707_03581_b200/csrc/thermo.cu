@@ -90,7 +90,7 @@ static void free_ctx(Ctx *c) {
                     c->d_pairs_s, c->d_pcnt_s, c->d_star_own, c->d_own_ptr, c->d_own_idx, c->d_x0, c->d_Thist, c->d_z2, c->d_q2,
                     c->d_ell_cnt_b, c->d_ell_col_b, c->d_ell_val_b, c->d_if_b_b, c->d_if_phi_b, c->d_Dinv_b,
                     c->d_step_sc_spec, c->d_spec_status, c->d_int_of_ext, c->d_stage[0], c->d_stage[1],
-                    c->d_if_d, c->d_sb_partials, c->d_sb_totals, c->d_sb_if_ptr, c->d_sb_if_k, c->d_sb_recs, c->d_sb_rec_ptr, c->d_sb_ptr8, c->d_sb_val8, c->d_sb_lcol8, c->d_sb_ai, c->d_benvS, c->d_cl_ai};
+                    c->d_if_d, c->d_sb_partials, c->d_sb_totals, c->d_sb_if_ptr, c->d_sb_if_k, c->d_sb_recs, c->d_sb_rec_ptr, c->d_sb_ptr8, c->d_sb_val8, c->d_sb_lcol8, c->d_sb_ai, c->d_benvS, c->d_cl_ai, c->d_sb_dbg};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (c->h_pin) cudaFreeHost(c->h_pin);
@@ -553,8 +553,9 @@ extern "C" int thermo_set_method(thermo_ctx *ctx, int32_t method, int32_t M, int
         return fail(c, THERMO_EINVAL, "method must be 0 (implicit Euler), 1 (MRSDC) or 2 (single-rate SDC)");
     if (method == 2) P = 1;
     if (M < 1 || M > 8 || P < 1 || P > 8 || K < 0) return fail(c, THERMO_EINVAL, "SDC needs 1 <= M, P <= 8, K >= 0");
-    if (c->S > 1 && c->sb_on)
-        return fail(c, THERMO_EINVAL, "batched SDC methods run on the default batched kernel (unset THERMO_CGB=2)");
+    // the batched SDC methods run on the gather kernel: a context on the windowed SpMM kernel
+    // moves its state over (and stays there)
+    if (c->S > 1 && c->sb_on && thermo::sbcg_disable(*c)) return THERMO_ECUDA;
     c->method = method;
     c->mr_M = M;
     c->mr_P = P;
