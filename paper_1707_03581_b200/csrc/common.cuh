@@ -210,20 +210,24 @@ struct BinGrid {      // uniform bin grid over one surface triangulation (2-D, o
     const int32_t *ids;   // triangle ids, ascending within a bin
 };
 
-struct PairRec {       // one overlapping (rail-top, stock-bottom) triangle pair, one side's view
-    int other;         // triangle of the other surface
+struct PairRec {       // one overlapping (rail-top F, stock-bottom G) triangle pair, both sides' view
+    int other;         // the rail-top triangle F (records are listed under their stock triangle G)
     int pad_;
-    double own[6];     // int phi_own_a phi_own_b, symmetric 3x3 (00 01 02 11 12 22)
-    double cross[9];   // int phi_own_a phi_other_b, [a*3 + b]
-    double b[3];       // int phi_own_a
+    double ownF[6];    // int phi_F,a phi_F,b over F cap G, symmetric 3x3 (00 01 02 11 12 22)
+    double ownG[6];    // int phi_G,a phi_G,b
+    double cross[9];   // int phi_F,a phi_G,b, [a*3 + b]
+    double bF[3];      // int phi_F,a
+    double bG[3];      // int phi_G,a
 };
 
 struct IfaceParams {
     int nTA, nTB;         // rail-top / stock-bottom triangles
     int pcap;             // pair records per triangle
     int cmax;             // contributions per interface row (6 x records of its star)
-    PairRec *pairs;       // [(side A: S*nTA | side B: S*nTB) * pcap]
-    int32_t *pcnt;        // [S*nTA + S*nTB]
+    PairRec *pairs;       // [S*nTB * pcap] records of each stock-bottom triangle (one per pair)
+    int32_t *pcnt;        // [S*nTA + S*nTB]: rail side: refs of each rail-top triangle; stock side: records
+    int32_t *refs;        // [S*nTA * pcap] per rail-top triangle: its pairs' record indices g*pcap + slot
+                          // (within the scenario), ascending after k_refsort
     int n_if;             // interface rows: [0, nA) rail top (fixed), [nA, n_if) stock bottom
     int nA;
     int S;                // scenarios

@@ -67,6 +67,7 @@ struct Ctx {
     int n_if = 0, nA = 0, nTA = 0, nTB = 0, cap = 0, pcap = 0, cmax = 0;
     PairRec *d_pairs = nullptr;
     int32_t *d_pcnt = nullptr;
+    int32_t *d_refs = nullptr;           // rail-side record references (k_pairs / k_refsort)
     int32_t *d_if_rows = nullptr;
     double2 *d_uv = nullptr;
     int32_t *d_star_ptr = nullptr, *d_star_tri = nullptr;
@@ -172,6 +173,7 @@ struct Ctx {
     int copy_pending[2] = {0, 0};
     PairRec *d_pairs_s = nullptr;        // pair records of the SDC node-time slots
     int32_t *d_pcnt_s = nullptr;
+    int32_t *d_refs_s = nullptr;
     double ms_iface = 0.0, ms_solve = 0.0;
 
     // windowed SpMM batched kernel (cg_spmm.cu)

@@ -89,12 +89,12 @@ __device__ __forceinline__ int bin_coord(double v, double v0, double inv_h, int 
 
 // ------------------------------------------------------------------------------ K2a: pairs
 
-// Integrals over one overlap polygon F cap (G + o) (both triangles given in the fixed frame),
-// seen from side `ownIsF`: own[] = int phi_own_a phi_own_b (symmetric, 00 01 02 11 12 22),
-// cross[a*3+b] = int phi_own_a phi_other_b, b[a] = int phi_own_a.  The polygon is always F
-// clipped by G and every product is formed in the same order from both sides, so the F-side
-// and G-side records of a pair hold bitwise-transposed cross blocks.
-__device__ bool pair_integrals(const double2 F[3], const double2 G[3], bool ownIsF, PairRec &r) {
+// Integrals over one overlap polygon F cap (G + o) (both triangles given in the fixed frame), for
+// both sides at once: ownF = int phi_F,a phi_F,b, ownG = int phi_G,a phi_G,b (symmetric, 00 01 02
+// 11 12 22), cross[a*3+b] = int phi_F,a phi_G,b, bF / bG = int phi_F,a / phi_G,a.  The polygon is F
+// clipped by G; the G side's cross block is the transpose (x*y == y*x in IEEE arithmetic, so it
+// equals bitwise what a G-side evaluation of the same products would give).
+__device__ bool pair_integrals(const double2 F[3], const double2 G[3], PairRec &r) {
     double2 poly[IF_MAXV];
     const int nv = clip_tri(F, G, poly);
     if (nv < 3) return false;
@@ -106,60 +106,62 @@ __device__ bool pair_integrals(const double2 F[3], const double2 G[3], bool ownI
         l[2] = cross2(T[1].x - T[0].x, T[1].y - T[0].y, y.x - T[0].x, y.y - T[0].y) * inv;
         l[0] = 1.0 - l[1] - l[2];
     };
-    auto vtx = [&](double2 y, double own[3], double oth[3]) {
-        double lf[3], lg[3];
-        bc(F, invF, y, lf);
-        bc(G, invG, y, lg);
+    double R[27];   // ownF[6] ownG[6] cross[9] bF[3] bG[3]
 #pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            own[a] = ownIsF ? lf[a] : lg[a];
-            oth[a] = ownIsF ? lg[a] : lf[a];
-        }
-    };
-    double R[18];   // own[6] cross[9] b[3]
-#pragma unroll
-    for (int q = 0; q < 18; ++q) R[q] = 0.0;
-    double o0[3], t0[3], o1[3], t1[3], o2[3], t2[3];
-    vtx(poly[0], o0, t0);
-    vtx(poly[1], o1, t1);
+    for (int q = 0; q < 27; ++q) R[q] = 0.0;
+    double f0[3], g0[3], f1[3], g1[3], f2[3], g2[3];
+    bc(F, invF, poly[0], f0);
+    bc(G, invG, poly[0], g0);
+    bc(F, invF, poly[1], f1);
+    bc(G, invG, poly[1], g1);
     double area = 0.0;
     for (int f = 1; f + 1 < nv; ++f) {
         const double2 p0 = poly[0], p1 = poly[f], p2 = poly[f + 1];
-        vtx(p2, o2, t2);
+        bc(F, invF, p2, f2);
+        bc(G, invG, p2, g2);
         const double ar = 0.5 * cross2(p1.x - p0.x, p1.y - p0.y, p2.x - p0.x, p2.y - p0.y);
         if (ar > 0.0) {
             area += ar;
             const double w12 = ar * (1.0 / 12.0), w3 = ar * (1.0 / 3.0);
-            double so[3], st[3];
+            double sf[3], sg[3];
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
-                so[a] = o0[a] + o1[a] + o2[a];
-                st[a] = t0[a] + t1[a] + t2[a];
+                sf[a] = f0[a] + f1[a] + f2[a];
+                sg[a] = g0[a] + g1[a] + g2[a];
             }
             int q = 0;
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
-                R[15 + a] += w3 * so[a];
+                R[21 + a] += w3 * sf[a];
+                R[24 + a] += w3 * sg[a];
 #pragma unroll
-                for (int b = a; b < 3; ++b, ++q)
-                    R[q] += w12 * (o0[a] * o0[b] + o1[a] * o1[b] + o2[a] * o2[b] + so[a] * so[b]);
+                for (int b = a; b < 3; ++b, ++q) {
+                    R[q] += w12 * (f0[a] * f0[b] + f1[a] * f1[b] + f2[a] * f2[b] + sf[a] * sf[b]);
+                    R[6 + q] += w12 * (g0[a] * g0[b] + g1[a] * g1[b] + g2[a] * g2[b] + sg[a] * sg[b]);
+                }
 #pragma unroll
                 for (int b = 0; b < 3; ++b)
-                    R[6 + a * 3 + b] += w12 * (o0[a] * t0[b] + o1[a] * t1[b] + o2[a] * t2[b] + so[a] * st[b]);
+                    R[12 + a * 3 + b] += w12 * (f0[a] * g0[b] + f1[a] * g1[b] + f2[a] * g2[b] + sf[a] * sg[b]);
             }
         }
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
-            o1[a] = o2[a];
-            t1[a] = t2[a];
+            f1[a] = f2[a];
+            g1[a] = g2[a];
         }
     }
 #pragma unroll
-    for (int q = 0; q < 6; ++q) r.own[q] = R[q];
+    for (int q = 0; q < 6; ++q) {
+        r.ownF[q] = R[q];
+        r.ownG[q] = R[6 + q];
+    }
 #pragma unroll
-    for (int q = 0; q < 9; ++q) r.cross[q] = R[6 + q];
+    for (int q = 0; q < 9; ++q) r.cross[q] = R[12 + q];
 #pragma unroll
-    for (int q = 0; q < 3; ++q) r.b[q] = R[15 + q];
+    for (int q = 0; q < 3; ++q) {
+        r.bF[q] = R[21 + q];
+        r.bG[q] = R[24 + q];
+    }
     return area > 0.0;
 }
 
@@ -173,57 +175,52 @@ __device__ __forceinline__ int warp_excl_scan(int v, int lane) {
     return x - v;
 }
 
-// Warp per (PAIR_TPW consecutive own triangles of side `side`, scenario s).
-//  1. candidates: per triangle, the candidates of all bins under its box (in the other
-//     surface's frame) are flattened (bins row-major, ascending ids) and spread over the
-//     lanes; box-overlapping ones, each counted in one bin only, are appended to a per-warp
-//     shared-memory queue in that order (ballot prefix).  A triangle whose box misses the
-//     other surface's union box has none (most rail triangles: the stock covers a part of it).
+// Warp per (PAIR_TPW consecutive stock-bottom triangles G, scenario s); every overlapping pair is
+// clipped once, from the stock side (round 1 clipped it once per side).
+//  1. candidates: per G, the rail-top triangles of all bins under its box (in the rail frame) are
+//     flattened (bins row-major, ascending ids) and spread over the lanes; box-overlapping ones,
+//     each counted in one bin only, are appended to a per-warp shared-memory queue in that order
+//     (ballot prefix).
 //  2. integrals: the queue is clipped 32 pairs at a time, one pair per lane, so the lanes stay
-//     busy across triangles; a hit's record slot is its rank among its own triangle's hits.
-// Records per triangle therefore come out in candidate order, the same for every run.
-#define PAIR_TPW 4
+//     busy across triangles; a hit's record slot is its rank among its own G's hits (records of
+//     a G come out in candidate order, the same for every run).  The rail triangle F gets a
+//     reference g * pcap + slot appended to its list (an integer atomic: the list order varies,
+//     k_refsort sorts it).
+#define PAIR_TPW 8
 #define PAIR_WPB 4
 
-// Both surfaces in one launch: blocks [0, nbA) take the rail-top triangles (side 0), the rest
-// the stock-bottom triangles (side 1), so the two passes run concurrently.
-__global__ void __launch_bounds__(32 * PAIR_WPB, 4) k_pairs(IfaceParams P, int nbA) {
+__global__ void __launch_bounds__(32 * PAIR_WPB, 3) k_pairs(IfaceParams P) {
     extern __shared__ int pair_q_all[];   // [PAIR_WPB][PAIR_TPW * pcap]
     __shared__ int pair_cnt_all[PAIR_WPB][PAIR_TPW];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const unsigned lt = (1u << lane) - 1u;
-    const int side = (int)blockIdx.x < nbA ? 0 : 1;
-    const int bx = side == 0 ? (int)blockIdx.x : (int)blockIdx.x - nbA;
-    const int nT = side == 0 ? P.nTA : P.nTB;
-    const int t0 = (bx * PAIR_WPB + wib) * PAIR_TPW;
+    const int nT = P.nTB;
+    const int t0 = (blockIdx.x * PAIR_WPB + wib) * PAIR_TPW;
     const int s = blockIdx.y;
     if (t0 >= nT) return;
     int *q = pair_q_all + wib * PAIR_TPW * P.pcap;
     int *qcnt = pair_cnt_all[wib];
     const int qcap = PAIR_TPW * P.pcap;
     const double ox = P.step_sc[4 * s + 0], oy = P.step_sc[4 * s + 1];
-    const int4 *own_tri = side == 0 ? P.triA : P.triB;
-    const int4 *oth_tri = side == 0 ? P.triB : P.triA;
-    const double4 *oth_box = side == 0 ? P.boxB : P.boxA;
-    const BinGrid &G = side == 0 ? P.binB : P.binA;
-    const double sx_own = side == 0 ? 0.0 : ox, sy_own = side == 0 ? 0.0 : oy;
-    const double sx_oth = side == 0 ? ox : 0.0, sy_oth = side == 0 ? oy : 0.0;
-    const int64_t rid0 = (side == 0 ? 0 : (int64_t)P.nTA * P.S) + (int64_t)s * nT;
+    const BinGrid &G = P.binA;
+    const int64_t gid0 = (int64_t)s * nT;          // stock triangles of this scenario
+    int32_t *rcnt = P.pcnt + (int64_t)s * P.nTA;   // reference counts of its rail triangles
+    int32_t *refs = P.refs + (int64_t)s * P.nTA * P.pcap;
 
-    // lane j < PAIR_TPW: query box of triangle t0 + j in the other surface's frame
+    // lane j < PAIR_TPW: query box of stock triangle t0 + j in the rail frame
     double qlx_l = 1.0, qhx_l = 0.0, qly_l = 1.0, qhy_l = 0.0;
     if (lane < PAIR_TPW && t0 + lane < nT) {
-        const int4 T = own_tri[t0 + lane];
+        const int4 T = P.triB[t0 + lane];
         const int tv[3] = {T.x, T.y, T.z};
         double lox = 1e300, loy = 1e300, hix = -1e300, hiy = -1e300;
         for (int v = 0; v < 3; ++v) {
             const double2 u = P.uv[tv[v]];
-            const double px = u.x + sx_own, py = u.y + sy_own;
+            const double px = u.x + ox, py = u.y + oy;
             lox = fmin(lox, px); hix = fmax(hix, px);
             loy = fmin(loy, py); hiy = fmax(hiy, py);
         }
-        qlx_l = lox - sx_oth; qhx_l = hix - sx_oth; qly_l = loy - sy_oth; qhy_l = hiy - sy_oth;
-        if (qlx_l > G.hx || qhx_l < G.lx || qly_l > G.hy || qhy_l < G.ly) {   // misses the surface
+        qlx_l = lox; qhx_l = hix; qly_l = loy; qhy_l = hiy;
+        if (qlx_l > G.hx || qhx_l < G.lx || qly_l > G.hy || qhy_l < G.ly) {   // off the rail top
             qlx_l = 1.0; qhx_l = 0.0;
         }
     }
@@ -260,7 +257,7 @@ __global__ void __launch_bounds__(32 * PAIR_WPB, 4) k_pairs(IfaceParams P, int n
                 int u = -1;
                 if (idx < total) {
                     u = G.ids[G.ptr[binq] + (idx - offq)];
-                    const double4 ub = oth_box[u];
+                    const double4 ub = P.boxA[u];
                     const int bx = bx0 + (b0 + qq) % nbx, by = by0 + (b0 + qq) / nbx;
                     cand = !(ub.x > qhx || ub.z < qlx || ub.y > qhy || ub.w < qly) &&
                            bin_coord(fmax(qlx, ub.x), G.x0, G.inv_h, G.nx) == bx &&
@@ -288,15 +285,15 @@ __global__ void __launch_bounds__(32 * PAIR_WPB, 4) k_pairs(IfaceParams P, int n
             const int e = q[r];
             j = e & 7;
             u = e >> 3;
-            const int4 T = own_tri[t0 + j], W = oth_tri[u];
+            const int4 T = P.triB[t0 + j], W = P.triA[u];
             const int tv[3] = {T.x, T.y, T.z}, wv[3] = {W.x, W.y, W.z};
-            double2 Tp[3], Up[3];
+            double2 Gp[3], Fp[3];
             for (int v = 0; v < 3; ++v) {
                 const double2 a = P.uv[tv[v]], b = P.uv[wv[v]];
-                Tp[v] = make_double2(a.x + sx_own, a.y + sy_own);
-                Up[v] = make_double2(b.x + sx_oth, b.y + sy_oth);
+                Gp[v] = make_double2(a.x + ox, a.y + oy);
+                Fp[v] = b;
             }
-            hit = side == 0 ? pair_integrals(Tp, Up, true, rec) : pair_integrals(Up, Tp, false, rec);
+            hit = pair_integrals(Fp, Gp, rec);
         }
         const unsigned hm = __ballot_sync(0xffffffffu, hit);
         const unsigned grp = __match_any_sync(0xffffffffu, valid ? j : 8 + lane);
@@ -304,7 +301,10 @@ __global__ void __launch_bounds__(32 * PAIR_WPB, 4) k_pairs(IfaceParams P, int n
             const int pos = qcnt[j] + __popc(hm & grp & lt);
             if (pos < P.pcap) {
                 rec.other = u;
-                P.pairs[(rid0 + t0 + j) * P.pcap + pos] = rec;
+                P.pairs[(gid0 + t0 + j) * P.pcap + pos] = rec;
+                const int rp = atomicAdd(&rcnt[u], 1);
+                if (rp < P.pcap) refs[(int64_t)u * P.pcap + rp] = (t0 + j) * P.pcap + pos;
+                else ok = false;
             } else {
                 ok = false;
             }
@@ -317,7 +317,33 @@ __global__ void __launch_bounds__(32 * PAIR_WPB, 4) k_pairs(IfaceParams P, int n
         atomicOr(&P.status[1], 1);
         atomicMin(&P.status[4], P.step);
     }
-    if (lane < PAIR_TPW && t0 + lane < nT) P.pcnt[rid0 + t0 + lane] = min(qcnt[lane], P.pcap);
+    if (lane < PAIR_TPW && t0 + lane < nT) P.pcnt[(int64_t)P.S * P.nTA + gid0 + t0 + lane] = min(qcnt[lane], P.pcap);
+}
+
+// Thread per (rail-top triangle F, scenario s): sort F's references ascending (insertion sort,
+// <= pcap entries), so that k_rows reads them in an order independent of the atomics' timing.
+__global__ void k_refsort(IfaceParams P) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= P.nTA) return;
+    const int64_t tid = (int64_t)blockIdx.y * P.nTA + t;
+    int n = P.pcnt[tid];
+    if (n <= 1) return;
+    n = min(n, P.pcap);
+    P.pcnt[tid] = n;
+    int32_t *r = P.refs + tid * P.pcap;
+    int v[64];
+    if (n > 64) return;   // pcap > 64 is refused at setup
+    for (int i = 0; i < n; ++i) v[i] = r[i];
+    for (int i = 1; i < n; ++i) {
+        const int x = v[i];
+        int k = i - 1;
+        while (k >= 0 && v[k] > x) {
+            v[k + 1] = v[k];
+            --k;
+        }
+        v[k + 1] = x;
+    }
+    for (int i = 0; i < n; ++i) r[i] = v[i];
 }
 
 // ------------------------------------------------------------------------------ K2b: rows
@@ -351,7 +377,7 @@ __global__ void __launch_bounds__(32 * ROW_WPB) k_rows(IfaceParams P) {
     RowSmem &W = sm_all[wib];
     const bool sideA = k < P.nA;
     const int nT = sideA ? P.nTA : P.nTB;
-    const int64_t base_rec = sideA ? 0 : (int64_t)P.nTA * P.S;
+    const int64_t base_cnt = sideA ? 0 : (int64_t)P.nTA * P.S;   // pcnt: rail refs | stock records
     const int4 *own_tri = sideA ? P.triA : P.triB;
     const int4 *oth_tri = sideA ? P.triB : P.triA;
     const int32_t row = P.if_rows[k];
@@ -364,7 +390,7 @@ __global__ void __launch_bounds__(32 * ROW_WPB) k_rows(IfaceParams P) {
         so_l = P.star_own[st0 + lane];
         const int4 T = own_tri[t_l];
         a_l = (T.x == k) ? 0 : ((T.y == k) ? 1 : 2);
-        np_l = P.pcnt[base_rec + (int64_t)s * nT + t_l];
+        np_l = P.pcnt[base_cnt + (int64_t)s * nT + t_l];
     }
     const int roff = warp_excl_scan(np_l, lane);
     const int R = __shfl_sync(0xffffffffu, roff + np_l, 31);
@@ -397,19 +423,30 @@ __global__ void __launch_bounds__(32 * ROW_WPB) k_rows(IfaceParams P) {
         int cc[6];
         double cv[6];
         if (valid) {
-            const PairRec &rec = P.pairs[(base_rec + (int64_t)s * nT + tq) * P.pcap + (r - oq)];
+            // rail rows reach their pairs through the sorted references, stock rows directly
+            int64_t ridx;
+            int oth;
+            if (sideA) {
+                const int key = P.refs[((int64_t)s * P.nTA + tq) * P.pcap + (r - oq)];
+                ridx = (int64_t)s * P.nTB * P.pcap + key;
+                oth = key / P.pcap;
+            } else {
+                ridx = ((int64_t)s * P.nTB + tq) * P.pcap + (r - oq);
+                oth = P.pairs[ridx].other;
+            }
+            const PairRec &rec = P.pairs[ridx];
             const int4 Tq = own_tri[tq];
-            const int4 Wq = oth_tri[rec.other];
+            const int4 Wq = oth_tri[oth];
             const int sym[3][3] = {{0, 1, 2}, {1, 3, 4}, {2, 4, 5}};
             const int tv[3] = {Tq.x, Tq.y, Tq.z}, wv[3] = {Wq.x, Wq.y, Wq.z};
 #pragma unroll
             for (int b = 0; b < 3; ++b) {
                 cc[b] = P.if_rows[tv[b]];
-                cv[b] = scale * rec.own[sym[aq][b]];          // -dt * (-alpha int phi phi)
+                cv[b] = scale * (sideA ? rec.ownF[sym[aq][b]] : rec.ownG[sym[aq][b]]);   // -dt * (-alpha int phi phi)
                 cc[3 + b] = P.if_rows[wv[b]];
-                cv[3 + b] = -scale * rec.cross[aq * 3 + b];   // -dt * (+alpha int phi phi)
+                cv[3 + b] = -scale * (sideA ? rec.cross[aq * 3 + b] : rec.cross[b * 3 + aq]);   // -dt * (+alpha ...)
             }
-            phi += rec.b[aq];
+            phi += sideA ? rec.bF[aq] : rec.bG[aq];
         }
 #pragma unroll
         for (int qq = 0; qq < 6; ++qq) {
@@ -832,7 +869,9 @@ int iface_setup(Ctx &c, const double *X, const std::vector<int32_t> &fA, const s
     if (max_star > 32) { c.err = "interface node with more than 32 surface triangles"; return -1; }
     if (c.cap > ROW_HS / 2) { c.err = "interface rows too dense for the row merge (capacity > 128)"; return -5; }
     c.cmax = 6 * max_star * c.pcap;
-    CK(cudaMalloc(&c.d_pairs, sizeof(PairRec) * (size_t)c.S * (c.nTA + c.nTB) * c.pcap));
+    if (c.pcap > 64) { c.err = "interface triangles overlap too many triangles of the other surface (> 62)"; return -5; }
+    CK(cudaMalloc(&c.d_pairs, sizeof(PairRec) * (size_t)c.S * c.nTB * c.pcap));
+    CK(cudaMalloc(&c.d_refs, sizeof(int32_t) * (size_t)c.S * c.nTA * c.pcap));
     CK(cudaMalloc(&c.d_pcnt, sizeof(int32_t) * (size_t)c.S * (c.nTA + c.nTB)));
 
     const int64_t S = c.S, nif = c.n_if;
@@ -854,6 +893,7 @@ void iface_params(Ctx &c, IfaceParams &P, const double *step_sc, double dt, int 
     P.pcap = c.pcap;
     P.pairs = c.d_pairs;
     P.pcnt = c.d_pcnt;
+    P.refs = c.d_refs;
     P.cmax = c.cmax;
     P.n_if = c.n_if;
     P.nA = c.nA;
@@ -895,8 +935,11 @@ int iface_launch(Ctx &c, const IfaceParams &P, cudaStream_t stream) {
     const size_t qsm = sizeof(int) * (size_t)PAIR_WPB * PAIR_TPW * c.pcap;
     cudaStream_t st = stream ? stream : c.stream;
     // blockIdx.y = scenario (batched mode) or node time (the slots of the SDC methods): P.S of them
-    const int nbA = (c.nTA + tpb - 1) / tpb, nbB = (c.nTB + tpb - 1) / tpb;
-    k_pairs<<<dim3((unsigned)(nbA + nbB), (unsigned)P.S), 32 * PAIR_WPB, qsm, st>>>(P, nbA);
+    CK(cudaMemsetAsync(P.pcnt, 0, sizeof(int32_t) * (size_t)P.S * c.nTA, st));   // rail reference counts
+    const int nbB = (c.nTB + tpb - 1) / tpb;
+    k_pairs<<<dim3((unsigned)nbB, (unsigned)P.S), 32 * PAIR_WPB, qsm, st>>>(P);
+    CK(cudaGetLastError());
+    k_refsort<<<dim3((unsigned)((c.nTA + 127) / 128), (unsigned)P.S), 128, 0, st>>>(P);
     CK(cudaGetLastError());
     k_rows<<<dim3((unsigned)((c.n_if + ROW_WPB - 1) / ROW_WPB), (unsigned)P.S), 32 * ROW_WPB, 0, st>>>(P);
     CK(cudaGetLastError());

@@ -288,10 +288,11 @@ int mrsdc_setup(Ctx &c) {
     const int64_t nb = (int64_t)nslot * S;
     if (c.mr_nslots < nb && c.n_if) {
         for (void *p : {(void *)c.d_ell_cnt_s, (void *)c.d_ell_col_s, (void *)c.d_ell_val_s, (void *)c.d_if_b_s,
-                        (void *)c.d_if_phi_s, (void *)c.d_pairs_s, (void *)c.d_pcnt_s})
+                        (void *)c.d_if_phi_s, (void *)c.d_pairs_s, (void *)c.d_pcnt_s, (void *)c.d_refs_s})
             if (p) cudaFree(p);
         // pair records of all node times at once (one launch set per step, batch = blockIdx.y)
-        CK(cudaMalloc(&c.d_pairs_s, sizeof(PairRec) * (size_t)nb * (c.nTA + c.nTB) * c.pcap));
+        CK(cudaMalloc(&c.d_pairs_s, sizeof(PairRec) * (size_t)nb * c.nTB * c.pcap));
+        CK(cudaMalloc(&c.d_refs_s, sizeof(int32_t) * (size_t)nb * c.nTA * c.pcap));
         CK(cudaMalloc(&c.d_pcnt_s, sizeof(int32_t) * (size_t)nb * (c.nTA + c.nTB)));
         CK(cudaMalloc(&c.d_ell_cnt_s, sizeof(int32_t) * nb * nif));
         CK(cudaMalloc(&c.d_ell_col_s, sizeof(int32_t) * (size_t)nb * c.cap * nif));
@@ -388,6 +389,7 @@ static int assemble_slots(Ctx &c, int ns) {
     Pf.S = ns * c.S;   // batch entry scenario * ns + slot
     Pf.pairs = c.d_pairs_s;
     Pf.pcnt = c.d_pcnt_s;
+    Pf.refs = c.d_refs_s;
     Pf.ell_cnt = c.d_ell_cnt_s;
     Pf.ell_col = c.d_ell_col_s;
     Pf.ell_val = c.d_ell_val_s;

@@ -83,7 +83,7 @@ static void free_ctx(Ctx *c) {
                     c->d_binB_ptr, c->d_binB_ids, c->d_slice_if, c->d_ell_cnt, c->d_ell_col, c->d_ell_val,
                     c->d_if_b, c->d_if_phi, c->d_if_dinv, c->d_T[0], c->d_T[1], c->d_z, c->d_p[0], c->d_p[1],
                     c->d_q, c->d_partials, c->d_status, c->d_fail_relres, c->d_step_sc, c->d_iters,
-                    c->d_relres, c->d_area, c->d_pairs, c->d_pcnt, c->d_chunk_hi, c->d_chunk_ctr, c->d_lcol, c->d_chunk_runs,
+                    c->d_relres, c->d_area, c->d_pairs, c->d_pcnt, c->d_refs, c->d_refs_s, c->d_chunk_hi, c->d_chunk_ctr, c->d_lcol, c->d_chunk_runs,
                     c->d_chunk_nruns, c->d_chunk_lown, c->d_trace, c->d_DinvS, c->d_slice_if_zero,
                     c->d_KV, c->d_Dinv_vol, c->d_if_of_row, c->d_mr, c->d_mr_iters, c->d_mr_relres,
                     c->d_ell_cnt_s, c->d_ell_col_s, c->d_ell_val_s, c->d_if_b_s, c->d_if_phi_s, c->d_rhs,
