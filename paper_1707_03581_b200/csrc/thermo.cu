@@ -957,9 +957,15 @@ static int queue_host_copy(Ctx *c, int scen, int64_t off, int64_t cnt, double *h
                                      : thermo::gather_all(*c, c->d_T[b], c->d_stage[b], c->copy_stream);
             if (rc) return THERMO_ECUDA;
             c->stage_ver[b] = c->ver[b];
+            // only the gather kernel reads the state buffer: a later step may overwrite it as
+            // soon as that kernel is done, while the DMA still drains the staging buffer (the
+            // next gather into it is ordered behind the DMA on the copy stream)
+            API_CK(cudaEventRecord(c->ev_copy[b], c->copy_stream));
+            c->copy_pending[b] = 1;
         }
         API_CK(cudaMemcpyAsync(host_out, c->d_stage[b] + (scen < 0 ? 0 : (int64_t)scen * c->N + off),
                                sizeof(double) * cnt, cudaMemcpyDeviceToHost, c->copy_stream));
+        return THERMO_OK;
     }
     API_CK(cudaEventRecord(c->ev_copy[b], c->copy_stream));
     c->copy_pending[b] = 1;
