@@ -251,10 +251,14 @@ typedef struct {
     int32_t order_max_window;        /*   ... and max window entries of a chunk */
     int32_t solve_variant;           /* CG kernel variant chosen at create (S = 1): kind 2 =
                                         windowed TMA sweep */
-    int32_t solve_kind;
+    int32_t solve_kind;              /* sweep kind of the streaming grid kernel (S = 1: 0-2), 3: the
+                                        batched windowed-SpMM kernel, -1: the batched gather kernel */
     int32_t solve_max_runs;          /* kind 2: max column-window runs of a chunk (internal order) */
     int32_t solve_window;            /* kind 2: max column-window entries of a chunk */
-    int32_t reserved_;
+    int32_t latency_path;            /* S = 1, small problems: 0 = the streaming grid kernel solves,
+                                        1 = the single-cluster kernel, 2 = the resident-operator
+                                        kernel (operator and vectors in shared memory, one grid
+                                        barrier per CG iteration) */
 } thermo_stats;
 
 int thermo_get_stats(const thermo_ctx *ctx, thermo_stats *out);

@@ -11,7 +11,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "build")
 LIB = os.path.join(HERE, "libthermo.so")
-SOURCES = ["assemble.cu", "iface.cu", "cg.cu", "cg_cluster.cu", "cg_batched.cu", "cg_spmm.cu", "mrsdc.cu", "reorder.cu", "thermo.cu"]
+SOURCES = ["assemble.cu", "iface.cu", "cg.cu", "cg_cluster.cu", "cg_resident.cu", "cg_batched.cu", "cg_spmm.cu", "mrsdc.cu", "reorder.cu", "thermo.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
          "-Xcompiler", "-fPIC", "-I" + os.path.join(ROOT, "include"), "--expt-relaxed-constexpr"]

@@ -434,6 +434,7 @@ int build_operator(Ctx &c, double dt, double mu) {
     if (!c.d_KV) CK(cudaMalloc(&c.d_KV, sizeof(double) * (c.nnz_pad + 1)));
     k_build_kv<<<nb(c.nnz_pad), 256, 0, st>>>(c.d_A, c.d_R, c.nnz_pad, c.d_KV);
     CK(cudaGetLastError());
+    ++c.op_ver;   // the interface rows' Jacobi diagonals assembled ahead (ahead mode) are stale
     c.built_dt = mu == 1.0 ? dt : -1.0;   // anything but the implicit-Euler operator: rebuild next step
     return 0;
 }

@@ -1207,6 +1207,7 @@ int cg_launch_solve(Ctx &c, const double *x0, double *x, const double *rhs, cons
     P.chunk_nruns = c.d_chunk_nruns;
     P.chunk_lown = c.d_chunk_lown;
     P.trace = nullptr;
+    if (c.rs_on) return rs_launch(c, P, false, 0);
     if (c.cl_on) return cl_launch(c, P, false, 0);
     void *args[] = {&P};
     CK(cudaLaunchCooperativeKernel(variant_kernel(c.cg_variant), dim3(c.cg_grid), dim3(c.cg_block), args,
@@ -1214,7 +1215,7 @@ int cg_launch_solve(Ctx &c, const double *x0, double *x, const double *rhs, cons
     return 0;
 }
 
-int cg_launch_step(Ctx &c, int step, double dt, const double *x0, int buf, bool ovl) {
+int cg_launch_step(Ctx &c, int step, double dt, const double *x0, int buf, bool ovl, int ah_slot) {
     CGParams P;
     memset(&P, 0, sizeof P);
     P.N = c.N;
@@ -1268,6 +1269,19 @@ int cg_launch_step(Ctx &c, int step, double dt, const double *x0, int buf, bool 
     P.trace_fine = c.d_trace && getenv("THERMO_CG_TRACE") && atoi(getenv("THERMO_CG_TRACE")) == 2;
     P.debug = c.cg_debug;
     P.prefetch = c.cg_prefetch;
+    if (c.rs_on) {
+        if (ah_slot >= 0) {   // ahead mode: this step's interface rows sit in slot ah_slot
+            const int64_t nif = c.n_if;
+            P.ell_cnt = c.d_ah_ell_cnt + ah_slot * nif;
+            P.ell_col = c.d_ah_ell_col + (int64_t)ah_slot * c.cap * nif;
+            P.ell_val = c.d_ah_ell_val + (int64_t)ah_slot * c.cap * nif;
+            P.if_b = c.d_ah_if_b + ah_slot * nif;
+            P.if_phi = c.d_ah_if_phi + ah_slot * nif;
+            P.if_dinv_s = c.d_ah_dinv + ah_slot * nif;
+            P.Dinv = c.d_Dinv_vol;
+        }
+        return rs_launch(c, P, ovl, buf);
+    }
     if (c.cl_on) return cl_launch(c, P, ovl, buf);
     void *args[] = {&P};
     if (ovl) {   // cooperative launch that records ev_cg[step & 1] once all of its CTAs have begun

@@ -49,6 +49,12 @@ struct CGParams {
     int prefetch;              // L2 leading-edge prefetch (THERMO_CG_PREFETCH=1; measured slower on cfg3)
     const int32_t *if_of_row;  // cluster kernel: interface index of a row (-1: none)
     int64_t cl_rows;           // cluster kernel: shared-memory rows per vector
+    int rs_ell;                // resident kernel: ELL capacity of an interface row
+    const int64_t *rs_part;    // resident kernel: [grid + 1] first slice of every CTA
+    const double *if_dinv_s;   // resident kernel, ahead mode: Jacobi inverse diagonal of the interface rows of
+                               // this step's slot ([n_if]; Dinv then holds the volume-only diagonal)
+    unsigned *gbar, *gbar_next;   // resident kernel: grid-barrier arrive counter of this launch (zero at its
+                                  // start) and the one it zeroes for the next launch
     int debug;                 // THERMO_CG_DEBUG bits (measurement only, results invalid):
                                // 1 consumers skip the row work, 2 no window copies, 4 no prefetch,
                                // 8 no q' store

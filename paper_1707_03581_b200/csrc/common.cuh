@@ -264,6 +264,8 @@ struct IfaceParams {
     int no_dinv;              // 1: leave the Jacobi diagonal alone (MRSDC: f^E is explicit)
     int slot_major;           // 1: batch index = node-time slot, arrays laid out slot by slot
                               // ([s][c][k], [s][k]) so per-slot row loops stay coalesced
+    int step_per_slot;        // 1: batch entry s belongs to time step `step + s` (the ahead mode assembles
+                              // the interfaces of consecutive steps in one launch set)
     int *status;              // status[1] |= overflow
 };
 

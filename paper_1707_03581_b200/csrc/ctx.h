@@ -113,6 +113,24 @@ struct Ctx {
     double *d_cl_ai = nullptr;       // its interface sums (2 n_if)
     int64_t cl_rows = 0;
     size_t cl_smem = 0;
+    bool rs_on = false;              // resident-operator latency solve (cg_resident.cu)
+    int64_t *d_rs_part[2] = {nullptr, nullptr};        // slice blocks of its CTAs (full grid, overlap grid)
+    size_t rs_smem = 0;
+    unsigned *d_gbar = nullptr;      // its two grid-barrier arrive counters (alternating between launches)
+    int rs_parity = 0;
+    // Ahead mode (with the resident solve, implicit Euler): the interface of a step depends only on
+    // its time, so the interfaces of the next ah_slots step times are assembled in ONE launch set
+    // (batch entry = step, slot-major buffers) and the solves run back to back; slots left over
+    // at the end of a call belong to the presumed next call (same dt, t = the end of this one)
+    bool ah_on = false, ah_valid = false;
+    int ah_slots = 0, ah_next = 0, ah_count = 0;
+    double ah_dt = 0.0;
+    uint64_t ah_opver = 0, op_ver = 0;    // op_ver: rebuilds of the volume operator / Jacobi diagonal
+    std::vector<double> ah_tp;            // step time of every assembled slot
+    void *d_ah_pairs = nullptr;
+    int32_t *d_ah_refs = nullptr, *d_ah_pcnt = nullptr, *d_ah_ell_cnt = nullptr, *d_ah_ell_col = nullptr;
+    double *d_ah_ell_val = nullptr, *d_ah_if_b = nullptr, *d_ah_if_phi = nullptr, *d_ah_dinv = nullptr,
+           *d_ah_d = nullptr, *d_ah_sc = nullptr;
     int64_t cg_u_rows = 0;
     int *d_chunk_ctr = nullptr;
 
@@ -233,12 +251,17 @@ int cg_setup(Ctx &c);
 struct CGParams;
 int cl_setup(Ctx &c);
 int cl_launch(Ctx &c, CGParams &P, bool ovl, int buf);
+// cg_resident.cu (resident-operator latency solve; rs_setup decides after overlap_setup, rs_launch
+// replaces the grid / cluster launch)
+int rs_setup(Ctx &c);
+int rs_launch(Ctx &c, CGParams &P, bool ovl, int buf);
 // chunk windows of the current pattern (W slices per chunk, runs merged below `gap`);
 // stats: [0] max window entries, [1] max runs, [2] flags (too many entries / window too wide)
 void chunk_windows_launch(Ctx &c, int W, int gap, int2 *runs, int32_t *nruns, int32_t *lown, uint16_t *lcol,
                           int *d_stats);
 // x0: initial guess (extrapolated state, see thermo.cu), nullptr = the committed state T^n
-int cg_launch_step(Ctx &c, int step, double dt, const double *x0 = nullptr, int buf = 0, bool ovl = false);
+int cg_launch_step(Ctx &c, int step, double dt, const double *x0 = nullptr, int buf = 0, bool ovl = false,
+                   int ah_slot = -1);   // ah_slot >= 0: the interface rows of that slot of the ahead buffers
 int overlap_setup(Ctx &c);   // second interface buffer set, side stream, reduced CG grid
 // Solve (M_L - a K_vol [- a K_G]) x = rhs from x0 with the operator currently in d_val (a =
 // built_dt); iface = false: no interface rows.  Iterations / residual to iters_out[slot].

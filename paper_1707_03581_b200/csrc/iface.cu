@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(32 * PAIR_WPB, 3) k_pairs(IfaceParams P) {
     }
     if (!__all_sync(0xffffffffu, ok) && lane == 0) {
         atomicOr(&P.status[1], 1);
-        atomicMin(&P.status[4], P.step);
+        atomicMin(&P.status[4], P.step + (P.step_per_slot ? (int)blockIdx.y : 0));
     }
     if (lane < PAIR_TPW && t0 + lane < nT) P.pcnt[(int64_t)P.S * P.nTA + gid0 + t0 + lane] = min(qcnt[lane], P.pcap);
 }
@@ -510,7 +510,7 @@ __global__ void __launch_bounds__(32 * ROW_WPB) k_rows(IfaceParams P) {
     if (lane == 0) {
         if (!ok) {
             atomicOr(&P.status[1], 1);
-            atomicMin(&P.status[4], P.step);
+            atomicMin(&P.status[4], P.step + (P.step_per_slot ? s : 0));
         }
         P.ell_cnt[row_index(P, s, k)] = ok ? count : 0;
         P.if_phi[row_index(P, s, k)] = phi;

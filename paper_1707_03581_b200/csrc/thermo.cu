@@ -90,7 +90,8 @@ static void free_ctx(Ctx *c) {
                     c->d_pairs_s, c->d_pcnt_s, c->d_star_own, c->d_own_ptr, c->d_own_idx, c->d_x0, c->d_Thist, c->d_z2, c->d_q2,
                     c->d_ell_cnt_b, c->d_ell_col_b, c->d_ell_val_b, c->d_if_b_b, c->d_if_phi_b, c->d_Dinv_b,
                     c->d_step_sc_spec, c->d_spec_status, c->d_int_of_ext, c->d_stage[0], c->d_stage[1],
-                    c->d_if_d, c->d_sb_partials, c->d_sb_totals, c->d_sb_if_ptr, c->d_sb_if_k, c->d_sb_recs, c->d_sb_rec_ptr, c->d_sb_ptr8, c->d_sb_val8, c->d_sb_lcol8, c->d_sb_ai, c->d_benvS, c->d_cl_ai, c->d_sb_dbg};
+                    c->d_if_d, c->d_sb_partials, c->d_sb_totals, c->d_sb_if_ptr, c->d_sb_if_k, c->d_sb_recs, c->d_sb_rec_ptr, c->d_sb_ptr8, c->d_sb_val8, c->d_sb_lcol8, c->d_sb_ai, c->d_benvS, c->d_cl_ai, c->d_sb_dbg, c->d_gbar, c->d_rs_part[0], c->d_rs_part[1], c->d_ah_pairs, c->d_ah_refs, c->d_ah_pcnt, c->d_ah_ell_cnt, c->d_ah_ell_col,
+                    c->d_ah_ell_val, c->d_ah_if_b, c->d_ah_if_phi, c->d_ah_dinv, c->d_ah_d, c->d_ah_sc};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (c->h_pin) cudaFreeHost(c->h_pin);
@@ -307,6 +308,7 @@ extern "C" int thermo_create_mesh(thermo_ctx **out, const thermo_mesh *fixed, co
             rc = thermo::assemble_robin(*c);
             if (!rc) rc = c->S == 1 ? thermo::cg_setup(*c) : thermo::cgb_setup(*c);
             if (!rc) rc = thermo::overlap_setup(*c);
+            if (!rc && c->S == 1) rc = thermo::rs_setup(*c);   // after the overlap grid is known
             if (!rc && getenv("THERMO_CG_TRACE")) {
                 if (cudaMalloc(&c->d_trace, sizeof(unsigned long long) * 1024) != cudaSuccess) rc = -3;
                 else cudaMemsetAsync(c->d_trace, 0, sizeof(unsigned long long) * 1024, c->stream);
@@ -606,7 +608,11 @@ extern "C" int thermo_step(thermo_ctx *ctx, double t, double dt, int32_t nsteps)
         const size_t n_sc = 4 * (size_t)S * nsteps, n_st = (size_t)nsteps * S;
         const size_t off_sc = 0, off_st = (n_sc * 8 + 63) & ~(size_t)63;     // [status 8 int | frel]
         const size_t off_it = off_st + 64, off_rr = off_it + ((n_st * 4 + 63) & ~(size_t)63);
-        const size_t off_ar = off_rr + n_st * 8, pin_bytes = off_ar + (size_t)nsteps * 8 + 64;
+        const size_t off_ar = off_rr + n_st * 8;
+        // ahead mode: time scalars of every batch of slots this call may assemble
+        const size_t off_ah = (off_ar + (size_t)nsteps * 8 + 63) & ~(size_t)63;
+        const size_t ah_bytes = c->ah_on ? ((size_t)nsteps / c->ah_slots + 2) * c->ah_slots * 32 : 0;
+        const size_t pin_bytes = off_ah + ah_bytes + 64;
         API_CK(pin_reserve(c, pin_bytes));
         unsigned char *pin = reinterpret_cast<unsigned char *>(c->h_pin);
         double *sc = reinterpret_cast<double *>(pin + off_sc);
@@ -683,8 +689,72 @@ extern "C" int thermo_step(thermo_ctx *ctx, double t, double dt, int32_t nsteps)
             API_CK(cudaMemsetAsync(c->d_Thist, 0, sizeof(double) * (NS + 16), c->stream));
         }
         int64_t launches = 0;
-        const bool ovl = c->overlap && S == 1;
+        const bool ahead = c->ah_on && S == 1;   // (implicit Euler: the SDC methods returned above)
+        const bool ovl = c->overlap && S == 1 && !ahead;
         bool spec_launched = false;
+        int ah_batches = 0;
+        // ahead mode: the slot that holds the interface of step n -- the next assembled slot if its
+        // step time is this step's (bitwise), else a new batch: this call's steps from n on, then the
+        // first steps of the presumed next call (t' = t + nsteps dt, evaluated with its expressions)
+        auto ahead_slot = [&](int n, int *slot) -> int {
+            const double tp = t + (double)(n + 1) * dt;
+            if (c->ah_valid && c->ah_dt == dt && c->ah_opver == c->op_ver && c->ah_next < c->ah_count &&
+                c->ah_tp[c->ah_next] == tp) {
+                *slot = c->ah_next++;
+                return 0;
+            }
+            const int M = c->ah_slots;
+            double *hs = reinterpret_cast<double *>(pin + off_ah) + (size_t)ah_batches * M * 4;
+            ++ah_batches;
+            c->ah_tp.assign(M, 0.0);
+            const thermo::Scen &q = c->scen[0];
+            for (int j = 0; j < M; ++j) {
+                double tq;
+                if (n + j < nsteps) {
+                    tq = t + (double)(n + j + 1) * dt;
+                } else {
+                    const double ts = t + (double)nsteps * dt;
+                    tq = ts + (double)(n + j - nsteps + 1) * dt;
+                }
+                const double sv = q.s0 + q.amp * std::sin(2.0 * M_PI * tq / q.period);
+                const double eta = q.eta0 * (1.0 + q.eta_amp * std::sin(2.0 * M_PI * tq / q.eta_period));
+                hs[4 * j + 0] = sv * q.d2[0];
+                hs[4 * j + 1] = sv * q.d2[1];
+                hs[4 * j + 2] = eta;
+                hs[4 * j + 3] = sv;
+                c->ah_tp[j] = tq;
+            }
+            if (cudaMemcpyAsync(c->d_ah_sc, hs, sizeof(double) * 4 * M, cudaMemcpyHostToDevice, c->stream) != cudaSuccess)
+                return -1;
+            thermo::IfaceParams P;
+            memset(&P, 0, sizeof P);
+            thermo::iface_params(*c, P, c->d_ah_sc, dt, 0);
+            P.S = M;
+            P.pairs = reinterpret_cast<thermo::PairRec *>(c->d_ah_pairs);
+            P.pcnt = c->d_ah_pcnt;
+            P.refs = c->d_ah_refs;
+            P.ell_cnt = c->d_ah_ell_cnt;
+            P.ell_col = c->d_ah_ell_col;
+            P.ell_val = c->d_ah_ell_val;
+            P.if_b = c->d_ah_if_b;
+            P.if_phi = c->d_ah_if_phi;
+            P.if_dinv = c->d_ah_dinv;
+            P.if_d = c->d_ah_d;
+            P.DinvS = nullptr;
+            P.Dinv = nullptr;
+            P.slot_major = 1;
+            P.step = n;             // slot j: step n + j (an overflow is reported at its own step)
+            P.step_per_slot = 1;
+            if (thermo::iface_launch(*c, P, c->stream)) return -1;
+            launches += c->n_if ? 3 : 0;
+            c->ah_valid = true;
+            c->ah_dt = dt;
+            c->ah_opver = c->op_ver;
+            c->ah_count = M;
+            c->ah_next = 1;
+            *slot = 0;
+            return 0;
+        };
         if (ovl) {
             // the side stream runs one step ahead: interface(n + 1) into buffer set (n + 1) & 1
             // while the solve of step n reads set n & 1; interface(n + 1) waits for the solve of
@@ -751,11 +821,17 @@ extern "C" int thermo_step(thermo_ctx *ctx, double t, double dt, int32_t nsteps)
                 API_CK(cudaGetLastError());
                 ++launches;
             }
-            if (ovl) API_CK(cudaStreamWaitEvent(c->stream, c->ev_if[bs(n)], 0));
-            else if (launch_iface(n, c->stream)) return THERMO_ECUDA;
+            int ah_slot = -1;
+            if (ahead) {
+                if (ahead_slot(n, &ah_slot)) return THERMO_ECUDA;
+            } else if (ovl) {
+                API_CK(cudaStreamWaitEvent(c->stream, c->ev_if[bs(n)], 0));
+            } else if (launch_iface(n, c->stream)) {
+                return THERMO_ECUDA;
+            }
             if (c->timing) API_CK(cudaEventRecord(c->events[2 * n + 1], c->stream));
             const double *x0 = avail > 0 ? c->d_x0 : nullptr;
-            if ((S == 1 ? thermo::cg_launch_step(*c, n, dt, x0, ovl ? bs(n) : 0, ovl)
+            if ((S == 1 ? thermo::cg_launch_step(*c, n, dt, x0, ovl ? bs(n) : 0, ovl, ah_slot)
                         : thermo::cgb_launch_step(*c, n, dt, x0)))
                 return THERMO_ECUDA;
             launches += 1;
@@ -835,7 +911,18 @@ extern "C" int thermo_step(thermo_ctx *ctx, double t, double dt, int32_t nsteps)
             for (int j = 0; j < S; ++j) it = std::max(it, (int)c->h_iters[(size_t)(nsteps - 1) * S + j]);
             double s_ns = 0, u_ns = 0;
             const char *tv = getenv("THERMO_CG_TRACE");
-            if (S == 1 && c->cl_on) {   // cluster solve: stamps after S + reduction and after U + sync
+            if (S == 1 && c->rs_on) {   // resident solve: stamps after the sweep + CTA sums and after the barrier + totals
+                double sa = 0, ua = 0;
+                const int m = std::min(it, 499);
+                for (int k = 0; k < m; ++k) {
+                    sa += (double)(tr[2 + 2 * k] - tr[1 + 2 * k]);
+                    ua += (double)(tr[3 + 2 * k] - tr[2 + 2 * k]);
+                }
+                if (m > 0)
+                    fprintf(stderr, "[thermo trace] resident solve: phase0 %.2f us, sweep + CTA sums %.2f us, barrier + totals %.2f us "
+                            "per iteration (%d iters)\n", (tr[1] - tr[0]) * 1e-3, sa * 1e-3 / m, ua * 1e-3 / m, m);
+                it = 0;
+            } else if (S == 1 && c->cl_on) {   // cluster solve: stamps after S + reduction and after U + sync
                 double sa = 0, ua = 0;
                 const int m = std::min(it, 499);
                 for (int k = 0; k < m; ++k) {
@@ -884,6 +971,9 @@ extern "C" int thermo_step(thermo_ctx *ctx, double t, double dt, int32_t nsteps)
                 fprintf(stderr, "[thermo trace] phase0 %.1f us, S %.1f us/iter, U %.1f us/iter (%d iters)\n",
                         (tr[1] - tr[0]) * 1e-3, s_ns * 1e-3 / it, u_ns * 1e-3 / it, it);
         }
+        // ahead mode: an overflow in a slot (of this call or of the presumed next one) or a failed
+        // step ends the assembled time line; the next call assembles from its own first step
+        if (ahead && (status[0] || status[1])) c->ah_valid = false;
         if (status[0]) {
             const int f = status[2];
             c->failed_step = f;
@@ -1081,6 +1171,7 @@ extern "C" int thermo_get_stats(const thermo_ctx *ctx, thermo_stats *out) {
     out->order_max_window = c->probe_window;
     out->solve_variant = c->S == 1 ? c->cg_variant : -1;
     out->solve_kind = c->S == 1 ? c->cg_kind : (c->sb_on ? 3 : -1);   // 3: batched windowed SpMM
+    out->latency_path = c->S == 1 ? (c->rs_on ? 2 : (c->cl_on ? 1 : 0)) : 0;
     out->solve_max_runs = c->cg_max_runs;
     out->solve_window = c->cg_win_cap;
     return THERMO_OK;

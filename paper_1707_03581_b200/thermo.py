@@ -55,7 +55,7 @@ class Stats(ctypes.Structure):
                 ("reordered", ctypes.c_int32), ("order_max_runs", ctypes.c_int32),
                 ("order_max_window", ctypes.c_int32), ("solve_variant", ctypes.c_int32),
                 ("solve_kind", ctypes.c_int32), ("solve_max_runs", ctypes.c_int32),
-                ("solve_window", ctypes.c_int32), ("reserved_", ctypes.c_int32)]
+                ("solve_window", ctypes.c_int32), ("latency_path", ctypes.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

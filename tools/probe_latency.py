@@ -1,7 +1,8 @@
 """Latency probe for paper-scale problems (16,626 DoF; look-ahead factor P:189-194):
 device time per implicit-Euler step and per CG iteration of small configurations with the
-single-cluster solve (default for N <= 65,536) and with the persistent grid kernel
-(THERMO_CG_CLUSTER=0), one step per call as a digital twin would run.
+resident-operator solve (default where the operator fits in shared memory), the single-cluster
+solve (THERMO_CG_CLUSTER=1) and the persistent streaming grid kernel (THERMO_CG_CLUSTER=0), one
+step per call as a digital twin would run.
 
     python tools/probe_latency.py [K]
 """
@@ -16,8 +17,10 @@ from paper_1707_03581_b200.thermo import Thermo  # noqa: E402
 
 K = int(sys.argv[1]) if len(sys.argv) > 1 else 50
 for name, jit in (("cfg0", None), ("small", 0.1), ("medium", 0.1), ("cfg1", None)):
-    for mode in ("cluster", "grid"):
-        os.environ["THERMO_CG_CLUSTER"] = "1" if mode == "cluster" else "0"
+    for mode in ("resident", "cluster", "grid"):
+        os.environ.pop("THERMO_CG_CLUSTER", None)
+        if mode != "resident":
+            os.environ["THERMO_CG_CLUSTER"] = "1" if mode == "cluster" else "0"
         cfg = I.make_config(name, jitter=jit)
         th = Thermo.from_config(cfg)
         th.set_timing(True)
@@ -38,7 +41,7 @@ for name, jit in (("cfg0", None), ("small", 0.1), ("medium", 0.1), ("cfg1", None
         e1.record(s)
         torch.cuda.synchronize()
         ms1 = e0.elapsed_time(e1) / K
-        print(f"{name:7s} N={cfg.n_dof:6d} {mode:7s}: {ms * 1e3:7.1f} us/step ({st['ms_solve'] / K * 1e3:6.1f} solve, "
+        print(f"{name:7s} N={cfg.n_dof:6d} {mode:8s} (path {st['latency_path']}): {ms * 1e3:7.1f} us/step ({st['ms_solve'] / K * 1e3:6.1f} solve, "
               f"{st['ms_solve'] / max(st['total_iters'], 1) * 1e3:5.2f} us/iter, {its:4.1f} iters), "
               f"{ms1 * 1e3:7.1f} us/step one step per call; look-ahead {cfg.dt / (ms * 1e-3):7.0f}", flush=True)
         th.close()
