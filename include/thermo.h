@@ -119,7 +119,14 @@ int thermo_set_bc(thermo_ctx *ctx, int32_t part, int32_t tag, double alpha, doub
  * Work is enqueued on the context stream; the call synchronises that stream once at the
  * end to report status.  Returns THERMO_ENOCONV if some scenario's CG did not converge
  * within maxit (steps before the failing one are committed; the failing step and its
- * residual are in thermo_get_stats), THERMO_EGEOM if the interface storage overflowed. */
+ * residual are in thermo_get_stats), THERMO_EGEOM if the interface storage overflowed.
+ * Scheduling (no effect on the result beyond rounding of the reductions): the interface
+ * operator of a step depends only on its time, so the library may assemble it early -- on a
+ * side stream during the previous solve (overlap mode), or for the next 16 step times in one
+ * launch set (ahead mode, with the resident-operator solve of small single-scenario problems);
+ * operators assembled for times the caller then does not step to are discarded.  A call that
+ * continues the previous call's time line with the same dt (t = the previous t + nsteps dt,
+ * bitwise) reuses what was assembled for it. */
 int thermo_step(thermo_ctx *ctx, double t, double dt, int32_t nsteps);
 
 /* Copy the temperature of one scenario and part (0 fixed, 1 moving, -1 both: fixed nodes
@@ -166,8 +173,9 @@ int thermo_set_T(thermo_ctx *ctx, int32_t scen, int32_t part, const double *in, 
  * Methods 1-2 run on batched contexts too: every scenario advances with its own motion and
  * friction law (node-time interface operators of every scenario in one launch set, the implicit
  * stages as batched solves with per-column convergence).
- * EINVAL for other methods, M or P outside [1, 8], K < 0, or a batched context on the opt-in
- * windowed-SpMM kernel (THERMO_CGB=2). */
+ * (A batched context whose implicit-Euler solves run on the windowed-SpMM kernel, the default,
+ * moves its state to the gather kernel's row layout at this call: the SDC stages run there.)
+ * EINVAL for other methods, M or P outside [1, 8] or K < 0. */
 int thermo_set_method(thermo_ctx *ctx, int32_t method, int32_t M, int32_t P, int32_t K);
 
 /* Replace the temperature by the stationary state of the machine at rest (the
