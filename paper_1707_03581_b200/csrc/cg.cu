@@ -638,9 +638,11 @@ __global__ void __launch_bounds__(cg_threads(KIND, W, NG), KIND == 0 ? 2 : 1) k_
         const int64_t i = 32 * s + lane;
         const int64_t ii = i < N ? i : N - 1;
         // own-row loads first: their latency overlaps the row sum
-        const double be = P.benv[ii], ml = P.ML[ii], di = P.Dinv[ii];
+        const double be = P.benv[ii], ml = P.ML[ii], dv = P.Dinv[ii];
         const double Ti = P.X0 ? src.own2(P.T_in, ii) : src.own1(P.T_in, ii);
         const int ik = iface_index_r(P, ib, ie, i, lane);
+        // ahead mode: the Jacobi diagonal of an interface row comes with its step's slot
+        const double di = ik >= 0 && P.if_dinv_s ? P.if_dinv_s[ik] : dv;
         double ax = src.template dot<false>(w, x0, nullptr, 0.0);
         if (ik >= 0) ax += ell_row<false>(P, ik, x0, nullptr, 0.0);
         if (i < N) {
@@ -1269,19 +1271,17 @@ int cg_launch_step(Ctx &c, int step, double dt, const double *x0, int buf, bool 
     P.trace_fine = c.d_trace && getenv("THERMO_CG_TRACE") && atoi(getenv("THERMO_CG_TRACE")) == 2;
     P.debug = c.cg_debug;
     P.prefetch = c.cg_prefetch;
-    if (c.rs_on) {
-        if (ah_slot >= 0) {   // ahead mode: this step's interface rows sit in slot ah_slot
-            const int64_t nif = c.n_if;
-            P.ell_cnt = c.d_ah_ell_cnt + ah_slot * nif;
-            P.ell_col = c.d_ah_ell_col + (int64_t)ah_slot * c.cap * nif;
-            P.ell_val = c.d_ah_ell_val + (int64_t)ah_slot * c.cap * nif;
-            P.if_b = c.d_ah_if_b + ah_slot * nif;
-            P.if_phi = c.d_ah_if_phi + ah_slot * nif;
-            P.if_dinv_s = c.d_ah_dinv + ah_slot * nif;
-            P.Dinv = c.d_Dinv_vol;
-        }
-        return rs_launch(c, P, ovl, buf);
+    if (ah_slot >= 0) {   // ahead mode: this step's interface rows sit in slot ah_slot
+        const int64_t nif = c.n_if;
+        P.ell_cnt = c.d_ah_ell_cnt + ah_slot * nif;
+        P.ell_col = c.d_ah_ell_col + (int64_t)ah_slot * c.cap * nif;
+        P.ell_val = c.d_ah_ell_val + (int64_t)ah_slot * c.cap * nif;
+        P.if_b = c.d_ah_if_b + ah_slot * nif;
+        P.if_phi = c.d_ah_if_phi + ah_slot * nif;
+        P.if_dinv_s = c.d_ah_dinv + ah_slot * nif;
+        P.Dinv = c.d_Dinv_vol;
     }
+    if (c.rs_on) return rs_launch(c, P, ovl, buf);
     if (c.cl_on) return cl_launch(c, P, ovl, buf);
     void *args[] = {&P};
     if (ovl) {   // cooperative launch that records ev_cg[step & 1] once all of its CTAs have begun

@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_cg_cluster(CGParams P) {
         }
         bi = P.rhs ? P.rhs[i] : fma(P.ML[i], P.T_in[i], P.dt * bi);
         const double r = bi - ax;
-        const double zi = P.Dinv[i] * r;
+        const double zi = (ik >= 0 && P.if_dinv_s ? P.if_dinv_s[ik] : P.Dinv[i]) * r;   // (ahead mode: per-slot diagonal)
         zs[l] = zi;
         ps[l] = zi;
         pg[i] = zi;

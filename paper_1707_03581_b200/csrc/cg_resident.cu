@@ -445,32 +445,45 @@ int rs_setup(Ctx &c) {
         if (!c.d_rs_part[gi]) CK(cudaMalloc(&c.d_rs_part[gi], sizeof(int64_t) * (c.num_sms + 1)));
         CK(cudaMemcpy(c.d_rs_part[gi], parts[gi].data(), sizeof(int64_t) * parts[gi].size(), cudaMemcpyHostToDevice));
     }
-    // ahead mode (ctx.h): slot-major buffers for the interfaces of the next ah_slots steps
-    c.ah_on = false;
-    const char *ea = getenv("THERMO_AHEAD");   // 0: off; n >= 2: slots
-    const int slots = ea ? atoi(ea) : 16;
-    if (c.n_if > 0 && slots >= 2 && !c.d_ah_sc) {
-        const size_t M = (size_t)std::min(slots, 64), nif = (size_t)c.n_if;
-        CK(cudaMalloc(&c.d_ah_pairs, sizeof(PairRec) * M * c.nTB * c.pcap));
-        CK(cudaMalloc(&c.d_ah_refs, sizeof(int32_t) * M * c.nTA * c.pcap));
-        CK(cudaMalloc(&c.d_ah_pcnt, sizeof(int32_t) * M * (c.nTA + c.nTB)));
-        CK(cudaMalloc(&c.d_ah_ell_cnt, sizeof(int32_t) * M * nif));
-        CK(cudaMalloc(&c.d_ah_ell_col, sizeof(int32_t) * M * c.cap * nif));
-        CK(cudaMalloc(&c.d_ah_ell_val, sizeof(double) * M * c.cap * nif));
-        CK(cudaMalloc(&c.d_ah_if_b, sizeof(double) * M * nif));
-        CK(cudaMalloc(&c.d_ah_if_phi, sizeof(double) * M * nif));
-        CK(cudaMalloc(&c.d_ah_dinv, sizeof(double) * M * nif));
-        CK(cudaMalloc(&c.d_ah_d, sizeof(double) * M * nif));
-        CK(cudaMalloc(&c.d_ah_sc, sizeof(double) * 4 * M));
-        c.ah_slots = (int)M;
-        c.ah_on = true;
-        c.ah_valid = false;
-    }
     c.rs_on = true;
     c.rs_smem = smem;
     if (getenv("THERMO_CG_VERBOSE"))
-        fprintf(stderr, "[thermo cg] resident solve: %d CTAs x %d threads (overlap grid %d), interface ELL %d, smem %zu B, "
-                        "ahead slots %d\n", rs_grid(c, false), RS_THREADS, rs_grid(c, true), ell, smem, c.ah_on ? c.ah_slots : 0);
+        fprintf(stderr, "[thermo cg] resident solve: %d CTAs x %d threads (overlap grid %d), interface ELL %d, smem %zu B"
+                        "\n", rs_grid(c, false), RS_THREADS, rs_grid(c, true), ell, smem);
+    return 0;
+}
+
+// Ahead mode (ctx.h, DESIGN 7.2): slot-major buffers for the interfaces of the next ah_slots step
+// times.  On with the resident solve, and for the sizes that do not overlap the interface assembly
+// with the previous solve (the overlap mode hides it completely where it is on); the slot count
+// is limited by memory (<= 2 GB of pair records and rows).  THERMO_AHEAD: 0 off, n >= 2 slots.
+int ahead_setup(Ctx &c) {
+    c.ah_on = false;
+    if (c.S != 1 || c.n_if == 0 || !(c.rs_on || !c.overlap)) return 0;
+    const char *ea = getenv("THERMO_AHEAD");
+    int slots = ea ? atoi(ea) : 16;
+    const size_t nif = (size_t)c.n_if;
+    const size_t per_slot = sizeof(PairRec) * (size_t)c.nTB * c.pcap + sizeof(int32_t) * (size_t)c.nTA * c.pcap +
+                            sizeof(int32_t) * (size_t)(c.nTA + c.nTB) + nif * ((size_t)c.cap * 12 + 36);
+    slots = (int)std::min<size_t>((size_t)std::min(slots, 64), ((size_t)2 << 30) / std::max<size_t>(per_slot, 1));
+    if (slots < 2 || c.d_ah_sc) return 0;
+    const size_t M = (size_t)slots;
+    CK(cudaMalloc(&c.d_ah_pairs, sizeof(PairRec) * M * c.nTB * c.pcap));
+    CK(cudaMalloc(&c.d_ah_refs, sizeof(int32_t) * M * c.nTA * c.pcap));
+    CK(cudaMalloc(&c.d_ah_pcnt, sizeof(int32_t) * M * (c.nTA + c.nTB)));
+    CK(cudaMalloc(&c.d_ah_ell_cnt, sizeof(int32_t) * M * nif));
+    CK(cudaMalloc(&c.d_ah_ell_col, sizeof(int32_t) * M * c.cap * nif));
+    CK(cudaMalloc(&c.d_ah_ell_val, sizeof(double) * M * c.cap * nif));
+    CK(cudaMalloc(&c.d_ah_if_b, sizeof(double) * M * nif));
+    CK(cudaMalloc(&c.d_ah_if_phi, sizeof(double) * M * nif));
+    CK(cudaMalloc(&c.d_ah_dinv, sizeof(double) * M * nif));
+    CK(cudaMalloc(&c.d_ah_d, sizeof(double) * M * nif));
+    CK(cudaMalloc(&c.d_ah_sc, sizeof(double) * 4 * M));
+    c.ah_slots = slots;
+    c.ah_on = true;
+    c.ah_valid = false;
+    if (getenv("THERMO_CG_VERBOSE"))
+        fprintf(stderr, "[thermo] ahead mode: %d slots of %.1f MB\n", slots, per_slot / 1048576.0);
     return 0;
 }
 

@@ -118,7 +118,8 @@ struct Ctx {
     size_t rs_smem = 0;
     unsigned *d_gbar = nullptr;      // its two grid-barrier arrive counters (alternating between launches)
     int rs_parity = 0;
-    // Ahead mode (with the resident solve, implicit Euler): the interface of a step depends only on
+    // Ahead mode (single scenario, implicit Euler; with the resident solve, and for the sizes without
+    // the overlap mode): the interface of a step depends only on
     // its time, so the interfaces of the next ah_slots step times are assembled in ONE launch set
     // (batch entry = step, slot-major buffers) and the solves run back to back; slots left over
     // at the end of a call belong to the presumed next call (same dt, t = the end of this one)
@@ -255,6 +256,7 @@ int cl_launch(Ctx &c, CGParams &P, bool ovl, int buf);
 // replaces the grid / cluster launch)
 int rs_setup(Ctx &c);
 int rs_launch(Ctx &c, CGParams &P, bool ovl, int buf);
+int ahead_setup(Ctx &c);   // after rs_setup: buffers of the ahead mode
 // chunk windows of the current pattern (W slices per chunk, runs merged below `gap`);
 // stats: [0] max window entries, [1] max runs, [2] flags (too many entries / window too wide)
 void chunk_windows_launch(Ctx &c, int W, int gap, int2 *runs, int32_t *nruns, int32_t *lown, uint16_t *lcol,

@@ -309,6 +309,7 @@ extern "C" int thermo_create_mesh(thermo_ctx **out, const thermo_mesh *fixed, co
             if (!rc) rc = c->S == 1 ? thermo::cg_setup(*c) : thermo::cgb_setup(*c);
             if (!rc) rc = thermo::overlap_setup(*c);
             if (!rc && c->S == 1) rc = thermo::rs_setup(*c);   // after the overlap grid is known
+            if (!rc && c->S == 1) rc = thermo::ahead_setup(*c);
             if (!rc && getenv("THERMO_CG_TRACE")) {
                 if (cudaMalloc(&c->d_trace, sizeof(unsigned long long) * 1024) != cudaSuccess) rc = -3;
                 else cudaMemsetAsync(c->d_trace, 0, sizeof(unsigned long long) * 1024, c->stream);

@@ -156,3 +156,23 @@ def test_ahead_mode_operator_rebuild_invalidates_slots(monkeypatch):
         th.step(3 * cfg.dt, cfg.dt, 3)
         out[ahead] = th.get_T()
     assert np.array_equal(out["16"], out["0"])
+
+
+def test_ahead_mode_with_streaming_kernel_cfg2(monkeypatch):
+    """Sizes without the overlap mode (N > 2^18) run the ahead mode with the streaming grid kernel
+    (the interface rows' Jacobi diagonal comes with the step's slot): bitwise the step-by-step
+    assembly, at a fraction of its interface time per step."""
+    cfg = I.make_config("cfg2")
+    out = {}
+    for ahead in ("16", "0"):
+        monkeypatch.setenv("THERMO_AHEAD", ahead)
+        th = _thermo(cfg)
+        th.set_timing(True)
+        th.step(0.0, cfg.dt, 2)
+        th.step(2 * cfg.dt, cfg.dt, 18)     # 2 slots of the first batch left over + a second batch
+        st = th.stats()
+        assert st["latency_path"] == 0 and st["failed_step"] == -1
+        out[ahead] = (th.get_T(), st["ms_iface"] / 18, th.step_iters().copy())
+    assert np.array_equal(out["16"][0], out["0"][0])
+    assert np.array_equal(out["16"][2], out["0"][2])
+    assert out["16"][1] < 0.7 * out["0"][1], (out["16"][1], out["0"][1])
