@@ -1217,7 +1217,8 @@ int cg_launch_solve(Ctx &c, const double *x0, double *x, const double *rhs, cons
     return 0;
 }
 
-int cg_launch_step(Ctx &c, int step, double dt, const double *x0, int buf, bool ovl, int ah_slot) {
+int cg_launch_step(Ctx &c, int step, double dt, const double *x0, int buf, bool ovl, int ah_slot, int xorder,
+                   bool xsave) {
     CGParams P;
     memset(&P, 0, sizeof P);
     P.N = c.N;
@@ -1281,7 +1282,12 @@ int cg_launch_step(Ctx &c, int step, double dt, const double *x0, int buf, bool 
         P.if_dinv_s = c.d_ah_dinv + ah_slot * nif;
         P.Dinv = c.d_Dinv_vol;
     }
-    if (c.rs_on) return rs_launch(c, P, ovl, buf);
+    if (c.rs_on) {
+        P.xorder = xorder;   // extrapolated start formed inside the kernel (no k_extrap launch)
+        P.xsave = xsave ? 1 : 0;
+        P.Th = c.d_Thist;
+        return rs_launch(c, P, ovl, buf);
+    }
     if (c.cl_on) return cl_launch(c, P, ovl, buf);
     void *args[] = {&P};
     if (ovl) {   // cooperative launch that records ev_cg[step & 1] once all of its CTAs have begun

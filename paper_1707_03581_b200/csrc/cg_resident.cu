@@ -226,7 +226,15 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_cg_resident(CGParams P) {
 
     // ---- phase 0: r0 = b - K~ x0, z0 = D^{-1} r0, p0 = z0; b = M_L T^n + dt (b_env + b_G) or rhs
     double red0[4] = {0.0, 0.0, 0.0, 0.0};   // b.b, r.r, r.z, |Gamma_R|
-    sweep([&](int j) { return __ldg(x0 + j); },
+    // x0 at column j: T^n (or the given X0), or the extrapolation of the last committed states
+    // formed here with the expressions of k_extrap (thermo.cu) -- T^{n-1} still sits in T_out, which
+    // is only written at the end of the launch, after every CTA has passed phase 0
+    auto gx = [&](int64_t j) -> double {
+        if (P.xorder == 0) return __ldg(x0 + j);
+        const double a = ld_cg1(P.T_in + j), d = a - ld_cg1(P.T_out + j);
+        return P.xorder >= 2 ? fma(3.0, d, ld_cg1(P.Th + j)) : a + d;
+    };
+    sweep([&](int j) { return gx(j); },
           [&](int l, double ax) {
               const int64_t i = r0 + l;
               const int ik = iks[l];
@@ -238,7 +246,7 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_cg_resident(CGParams P) {
               bi = P.rhs ? P.rhs[i] : fma(P.ML[i], P.T_in[i], P.dt * bi);
               const double r = bi - ax;
               const double zi = (ik >= 0 && P.if_dinv_s ? P.if_dinv_s[ik] : P.Dinv[i]) * r;
-              xs[l] = x0[i];
+              xs[l] = gx(i);
               zs[l] = zi;
               ps[l] = zi;
               qs[l] = 0.0;
@@ -317,7 +325,10 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_cg_resident(CGParams P) {
     }
     __syncthreads();
     // the last update of x is still to be applied (alpha = 0 after an exit on the direct r.r test)
-    for (int l = t; l < nloc; l += RS_THREADS) P.T_out[r0 + l] = fma(alpha, ps[l], xs[l]);
+    for (int l = t; l < nloc; l += RS_THREADS) {
+        if (P.xsave) P.Th[r0 + l] = P.T_out[r0 + l];   // history shift: T^{n-1} before it is overwritten
+        P.T_out[r0 + l] = fma(alpha, ps[l], xs[l]);
+    }
     if (rank == 0 && t == 0) {
         const double rel = tot0[0] > 0.0 ? sqrt(rr / tot0[0]) : sqrt(rr);
         P.iters_out[P.step] = it;

@@ -815,7 +815,8 @@ extern "C" int thermo_step(thermo_ctx *ctx, double t, double dt, int32_t nsteps)
             API_CK(guard_write(c, (c->cur + n + 1) & 1));
             // states behind T^n available for the extrapolated guess
             const int avail = extrap ? std::min(c->hist + n, c->guess) : 0;
-            if (avail > 0) {
+            const bool fold = S == 1 && c->rs_on;   // the resident kernel forms the guess in its phase 0
+            if (avail > 0 && !fold) {
                 k_extrap<<<(unsigned)((NS + 255) / 256), 256, 0, c->stream>>>(
                     c->d_T[(c->cur + n) & 1], c->d_T[(c->cur + n + 1) & 1], c->d_Thist, c->d_x0, NS, avail,
                     c->guess >= 2);
@@ -831,8 +832,9 @@ extern "C" int thermo_step(thermo_ctx *ctx, double t, double dt, int32_t nsteps)
                 return THERMO_ECUDA;
             }
             if (c->timing) API_CK(cudaEventRecord(c->events[2 * n + 1], c->stream));
-            const double *x0 = avail > 0 ? c->d_x0 : nullptr;
-            if ((S == 1 ? thermo::cg_launch_step(*c, n, dt, x0, ovl ? bs(n) : 0, ovl, ah_slot)
+            const double *x0 = avail > 0 && !fold ? c->d_x0 : nullptr;
+            if ((S == 1 ? thermo::cg_launch_step(*c, n, dt, x0, ovl ? bs(n) : 0, ovl, ah_slot, fold ? avail : 0,
+                                                 fold && avail > 0 && c->guess >= 2)
                         : thermo::cgb_launch_step(*c, n, dt, x0)))
                 return THERMO_ECUDA;
             launches += 1;
