@@ -227,6 +227,9 @@ struct Ctx {
     // stats of the last thermo_step
     int last_nsteps = 0;
     int64_t last_launches = 0;       // kernels launched by the last implicit-Euler thermo_step
+    bool status_clean = false;   // d_status is in its initial state (see thermo_step)
+    bool rep_pending = false;    // h_iters / h_relres / h_area of the last implicit-Euler call not fetched yet
+    int rep_nsteps = 0;
     std::vector<int32_t> h_iters;
     std::vector<double> h_relres, h_area;
     int64_t steps_done = 0;

@@ -82,7 +82,7 @@ static void free_ctx(Ctx *c) {
                     c->d_star_tri, c->d_triA, c->d_triB, c->d_boxA, c->d_boxB, c->d_binA_ptr, c->d_binA_ids,
                     c->d_binB_ptr, c->d_binB_ids, c->d_slice_if, c->d_ell_cnt, c->d_ell_col, c->d_ell_val,
                     c->d_if_b, c->d_if_phi, c->d_if_dinv, c->d_T[0], c->d_T[1], c->d_z, c->d_p[0], c->d_p[1],
-                    c->d_q, c->d_partials, c->d_status, c->d_fail_relres, c->d_step_sc, c->d_iters,
+                    c->d_q, c->d_partials, c->d_status, c->d_step_sc, c->d_iters,
                     c->d_relres, c->d_area, c->d_pairs, c->d_pcnt, c->d_refs, c->d_refs_s, c->d_chunk_hi, c->d_chunk_ctr, c->d_lcol, c->d_chunk_runs,
                     c->d_chunk_nruns, c->d_chunk_lown, c->d_trace, c->d_DinvS, c->d_slice_if_zero,
                     c->d_KV, c->d_Dinv_vol, c->d_if_of_row, c->d_mr, c->d_mr_iters, c->d_mr_relres,
@@ -298,8 +298,9 @@ extern "C" int thermo_create_mesh(thermo_ctx **out, const thermo_mesh *fixed, co
                 ok &= cudaMalloc(p, sizeof(double) * (NS + 2 * c->SP + 16)) == cudaSuccess;
                 if (ok) cudaMemsetAsync(*p, 0, sizeof(double) * (NS + 2 * c->SP + 16), c->stream);
             }
-            ok &= cudaMalloc(&c->d_status, sizeof(int) * 8) == cudaSuccess;
-            ok &= cudaMalloc(&c->d_fail_relres, sizeof(double)) == cudaSuccess;
+            // [status 8 int | achieved relative residual of a failed solve]: one readback copy
+            ok &= cudaMalloc(&c->d_status, sizeof(int) * 8 + sizeof(double)) == cudaSuccess;
+            c->d_fail_relres = reinterpret_cast<double *>(c->d_status + 8);
             if (!ok) { g_create_err = "device allocation failed"; free_ctx(c); return THERMO_ENOMEM; }
             k_fill_value<<<(unsigned)((NS + 255) / 256), 256, 0, c->stream>>>(c->d_T[0], NS, T_init);
             cudaMemsetAsync(c->d_p[0], 0, sizeof(double) * NS, c->stream);
@@ -412,6 +413,8 @@ extern "C" int thermo_stationary(thermo_ctx *ctx, double t, int32_t with_interfa
         }
         if (!c->d_rhs) API_CK(cudaMalloc(&c->d_rhs, sizeof(double) * (N + 16)));
         API_CK(cudaMemsetAsync(c->d_status, 0, sizeof(int) * 8, c->stream));
+        c->status_clean = false;   // (thermo_step skips its reset only after a clean implicit-Euler call)
+        c->rep_pending = false;
         const bool iface = with_interface && c->n_if > 0;
         if (iface) {   // K_G, b_G, Jacobi rows at the stock position and friction of time t
             const thermo::Scen &q = c->scen[0];
@@ -504,6 +507,8 @@ extern "C" int thermo_get_interface(thermo_ctx *ctx, int32_t scen, double t, dou
         double *d_sc = (double *)sc_buf.p;
         API_CK(cudaMemcpyAsync(d_sc, sc.data(), sizeof(double) * sc.size(), cudaMemcpyHostToDevice, c->stream));
         API_CK(cudaMemsetAsync(c->d_status, 0, sizeof(int) * 8, c->stream));
+        c->status_clean = false;   // (thermo_step skips its reset only after a clean implicit-Euler call)
+        c->rep_pending = false;
         thermo::IfaceParams P;
         memset(&P, 0, sizeof P);
         thermo::iface_params(*c, P, d_sc, dt);
@@ -576,6 +581,22 @@ extern "C" int thermo_set_solver(thermo_ctx *ctx, double rtol, int32_t maxit) {
     return THERMO_OK;
 }
 
+// The per-step report of the last implicit-Euler call (iterations, relative residuals, |Gamma_R|),
+// copied from the device when first asked for.
+static int fetch_report(Ctx *c) {
+    if (!c->rep_pending) return THERMO_OK;
+    c->rep_pending = false;
+    const size_t n_st = (size_t)c->rep_nsteps * c->S;
+    c->h_iters.resize(n_st);
+    c->h_relres.resize(n_st);
+    c->h_area.resize(c->rep_nsteps);
+    API_CK(cudaMemcpyAsync(c->h_iters.data(), c->d_iters, sizeof(int32_t) * n_st, cudaMemcpyDeviceToHost, c->stream));
+    API_CK(cudaMemcpyAsync(c->h_relres.data(), c->d_relres, sizeof(double) * n_st, cudaMemcpyDeviceToHost, c->stream));
+    API_CK(cudaMemcpyAsync(c->h_area.data(), c->d_area, sizeof(double) * c->rep_nsteps, cudaMemcpyDeviceToHost, c->stream));
+    API_CK(cudaStreamSynchronize(c->stream));
+    return THERMO_OK;
+}
+
 extern "C" int thermo_step(thermo_ctx *ctx, double t, double dt, int32_t nsteps) {
     Ctx *c = (Ctx *)ctx;
     if (!c) return THERMO_EINVAL;
@@ -630,9 +651,17 @@ extern "C" int thermo_step(thermo_ctx *ctx, double t, double dt, int32_t nsteps)
                 o[3] = sv;
             }
         }
-        API_CK(cudaMemcpyAsync(c->d_step_sc, sc, sizeof(double) * n_sc, cudaMemcpyHostToDevice, c->stream));
-        API_CK(cudaMemsetAsync(c->d_status, 0, sizeof(int) * 8, c->stream));
-        API_CK(cudaMemsetAsync(c->d_status + 4, 0x7f, sizeof(int), c->stream));   // no overflow step yet
+        // (ahead mode: every batch of slots carries its own scalars)
+        if (!(c->ah_on && c->method == 0))
+            API_CK(cudaMemcpyAsync(c->d_step_sc, sc, sizeof(double) * n_sc, cudaMemcpyHostToDevice, c->stream));
+        // the status words are still in their initial state if the last call was a clean
+        // implicit-Euler call (its readback showed it) and nothing else ran since
+        if (!c->status_clean) {
+            API_CK(cudaMemsetAsync(c->d_status, 0, sizeof(int) * 8, c->stream));
+            API_CK(cudaMemsetAsync(c->d_status + 4, 0x7f, sizeof(int), c->stream));   // no overflow step yet
+        }
+        c->status_clean = false;
+        c->rep_pending = false;   // the report arrays are rewritten by this call
         if (c->method >= 1) {   // MRSDC / single-rate SDC: one step at a time, status checked per step
             c->spec_valid = false;   // these steps reuse the first interface buffer set
             c->h_iters.assign((size_t)nsteps * S, 0);
@@ -877,20 +906,20 @@ extern "C" int thermo_step(thermo_ctx *ctx, double t, double dt, int32_t nsteps)
         // status readback: asynchronous copies into the pinned block, one synchronisation
         int *pst = reinterpret_cast<int *>(pin + off_st);
         double *pfr = reinterpret_cast<double *>(pin + off_st + 32);
-        int32_t *pit = reinterpret_cast<int32_t *>(pin + off_it);
-        double *prr = reinterpret_cast<double *>(pin + off_rr), *par = reinterpret_cast<double *>(pin + off_ar);
-        API_CK(cudaMemcpyAsync(pst, c->d_status, sizeof(int) * 8, cudaMemcpyDeviceToHost, c->stream));
-        API_CK(cudaMemcpyAsync(pit, c->d_iters, sizeof(int32_t) * n_st, cudaMemcpyDeviceToHost, c->stream));
-        API_CK(cudaMemcpyAsync(prr, c->d_relres, sizeof(double) * n_st, cudaMemcpyDeviceToHost, c->stream));
-        API_CK(cudaMemcpyAsync(par, c->d_area, sizeof(double) * nsteps, cudaMemcpyDeviceToHost, c->stream));
-        API_CK(cudaMemcpyAsync(pfr, c->d_fail_relres, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        // [status | fail_relres] in one copy; the per-step report (iterations, residuals, |Gamma_R|)
+        // is fetched when somebody asks for it (fetch_report) -- a caller stepping in real time
+        // pays for one small transfer per call
+        API_CK(cudaMemcpyAsync(pst, c->d_status, sizeof(int) * 8 + sizeof(double), cudaMemcpyDeviceToHost, c->stream));
         API_CK(cudaStreamSynchronize(c->stream));
         int status[8];
         memcpy(status, pst, sizeof status);
         const double frel = *pfr;
-        c->h_iters.assign(pit, pit + n_st);
-        c->h_relres.assign(prr, prr + n_st);
-        c->h_area.assign(par, par + nsteps);
+        c->rep_pending = true;
+        c->rep_nsteps = nsteps;
+        c->status_clean = !status[0] && !status[1] && !status[2] && !status[3] && status[4] == 0x7f7f7f7f;
+        if (status[0] || c->d_trace) {
+            if (int rc = fetch_report(c)) return rc;
+        }
         c->last_nsteps = nsteps;
         c->ms_iface = c->ms_solve = 0.0;
         if (c->timing) {
@@ -1137,6 +1166,7 @@ extern "C" int thermo_set_T(thermo_ctx *ctx, int32_t scen, int32_t part, const d
 extern "C" int thermo_get_stats(const thermo_ctx *ctx, thermo_stats *out) {
     const Ctx *c = (const Ctx *)ctx;
     if (!c || !out) return THERMO_EINVAL;
+    if (fetch_report(const_cast<Ctx *>(c))) return THERMO_ECUDA;   // (a cache of device-side results)
     memset(out, 0, sizeof *out);
     out->n_fixed = c->nf;
     out->n_moving = c->nm;
@@ -1190,6 +1220,7 @@ extern "C" int thermo_set_timing(thermo_ctx *ctx, int32_t enable) {
 extern "C" int thermo_get_step_iters(const thermo_ctx *ctx, int32_t *out, int64_t n) {
     const Ctx *c = (const Ctx *)ctx;
     if (!c || !out) return THERMO_EINVAL;
+    if (fetch_report(const_cast<Ctx *>(c))) return THERMO_ECUDA;
     int64_t m = (int64_t)c->h_iters.size();
     if (n < m) m = n;
     for (int64_t k = 0; k < m; ++k) out[k] = c->h_iters[k];
