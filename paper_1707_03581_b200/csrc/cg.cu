@@ -1217,8 +1217,8 @@ int cg_launch_solve(Ctx &c, const double *x0, double *x, const double *rhs, cons
     return 0;
 }
 
-int cg_launch_step(Ctx &c, int step, double dt, const double *x0, int buf, bool ovl, int ah_slot, int xorder,
-                   bool xsave) {
+int cg_launch_step(Ctx &c, int step, double dt, const double *x0, int buf, bool ovl, int ah_slot, int xhist,
+                   int xguess, int nst) {
     CGParams P;
     memset(&P, 0, sizeof P);
     P.N = c.N;
@@ -1283,9 +1283,12 @@ int cg_launch_step(Ctx &c, int step, double dt, const double *x0, int buf, bool 
         P.Dinv = c.d_Dinv_vol;
     }
     if (c.rs_on) {
-        P.xorder = xorder;   // extrapolated start formed inside the kernel (no k_extrap launch)
-        P.xsave = xsave ? 1 : 0;
+        P.xhist = xhist;     // extrapolated start formed inside the kernel (no k_extrap launch)
+        P.xguess = xguess;
+        P.xsave = xguess >= 2 ? 1 : 0;
         P.Th = c.d_Thist;
+        P.nst = nst;
+        P.Tin_w = c.d_T[(c.cur + step) & 1];
         return rs_launch(c, P, ovl, buf);
     }
     if (c.cl_on) return cl_launch(c, P, ovl, buf);

@@ -51,10 +51,13 @@ struct CGParams {
     int64_t cl_rows;           // cluster kernel: shared-memory rows per vector
     int rs_ell;                // resident kernel: ELL capacity of an interface row
     const int64_t *rs_part;    // resident kernel: [grid + 1] first slice of every CTA
-    int xorder, xsave;         // resident kernel: the extrapolated start formed in phase 0 (order 1 / 2; 0: x0 = X0
-                               // or T_in) from T_in = T^n, T_out's old content T^{n-1} and Th = T^{n-2}; xsave:
-                               // shift the history (Th <- T^{n-1}) at the end of the launch
+    int xhist, xguess, xsave;  // resident kernel: the extrapolated start formed in phase 0 -- order min(xhist + step
+                               // in launch, xguess) (0: x0 = X0 or T^n) from T^n, T_out's old content T^{n-1} and
+                               // Th = T^{n-2}; xsave: shift the history (Th <- T^{n-1}) at the end of a step
     double *Th;
+    int nst;                   // resident kernel: steps of this launch (ahead mode: their interfaces in
+                               // consecutive slots from ell_cnt / ell_col / ... on; the state buffers alternate)
+    double *Tin_w;             // = T_in, writable: the output buffer of the odd steps of a launch
     const double *if_dinv_s;   // resident kernel, ahead mode: Jacobi inverse diagonal of the interface rows of
                                // this step's slot ([n_if]; Dinv then holds the volume-only diagonal)
     unsigned *gbar, *gbar_next;   // resident kernel: grid-barrier arrive counter of this launch (zero at its

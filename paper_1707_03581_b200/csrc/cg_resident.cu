@@ -111,24 +111,50 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_cg_resident(CGParams P) {
         iks[l] = ik;
         // the list order only decides where a row's entries sit in shared memory
         if (ik >= 0) ifl[atomicAdd(&s_nifl, 1)] = l;
-        const int sl = l >> 5;
-        ds[l] = vs[sbase[sl] + (l & 31)];   // entry 0 of the row: the volume diagonal (assembly order)
     }
     __syncthreads();
     const int nifl = s_nifl;
     int *ics = reinterpret_cast<int *>(ivs + (((size_t)nifl * ell + 1) & ~(size_t)1));
+    const bool tr_on = P.trace && rank == 0 && t == 0;
+    unsigned nbar = 0;
+    // ---- the steps of this launch (ahead mode: consecutive steps whose interfaces sit in
+    // consecutive slots; otherwise one).  Step sti reads the state buffer the previous step wrote.
+    for (int sti = 0; sti < P.nst; ++sti) {
+    const int step = P.step + sti;
+    if (sti > 0 && P.status[1] && P.status[4] <= step) {   // interface overflow at this step (known before the launch)
+        if (rank == 0 && t == 0) {
+            P.status[0] = 2;
+            P.status[2] = step;
+        }
+        break;
+    }
+    const double *const Tin = (sti & 1) ? P.T_out : P.T_in;
+    double *const Tout = (sti & 1) ? P.Tin_w : P.T_out;
+    const int64_t so_if = (int64_t)sti * P.n_if;               // this step's slot behind the first one
+    const int32_t *const ell_cnt = P.ell_cnt + so_if;
+    const int32_t *const ell_col = P.ell_col + so_if * ell;
+    const double *const ell_val = P.ell_val + so_if * ell;
+    const double *const if_b = P.if_b + so_if, *const if_phi = P.if_phi + so_if;
+    const double *const if_dinv_s = P.if_dinv_s ? P.if_dinv_s + so_if : nullptr;
+    const int xorder = min(P.xhist + sti, P.xguess);   // states behind T^n available / wanted for the start
+    const int xsave = P.xsave;
+    for (int l = t; l < nloc; l += RS_THREADS) {
+        const int sl = l >> 5;
+        ds[l] = vs[sbase[sl] + (l & 31)];   // entry 0 of the row: the volume diagonal (assembly order)
+    }
+    __syncthreads();
     // this step's interface entries of the own interface rows -> shared memory (slot-major ELL
     // [c][k] in global memory; [j][c] here), and the interface self term on the diagonal
     for (int jb = 0; jb < nifl; jb += RS_THREADS >> 3) {   // warp-uniform trip count (shuffles inside)
         const int j = jb + (t >> 3);
         const bool on = j < nifl;
         const int l = on ? ifl[j] : 0, k = on ? iks[l] : 0;
-        const int cnt = on ? min(__ldg(P.ell_cnt + k), ell) : 0;
+        const int cnt = on ? min(__ldg(ell_cnt + k), ell) : 0;
         double self = 0.0;
         for (int c = t & 7; c < cnt; c += 8) {
             const int64_t e = (int64_t)c * P.n_if + k;
-            const int jc = __ldg(P.ell_col + e);
-            const double v = __ldg(P.ell_val + e);
+            const int jc = __ldg(ell_col + e);
+            const double v = __ldg(ell_val + e);
             ics[j * ell + c] = jc;
             ivs[j * ell + c] = v;
             if (jc == r0 + l) self += v;
@@ -141,11 +167,9 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_cg_resident(CGParams P) {
         }
     }
     __syncthreads();
-    const bool tr_on = P.trace && rank == 0 && t == 0;
-    int ntr = 0;
+    int ntr = 0;   // (the trace of the launch's last step survives)
     if (tr_on) P.trace[ntr++] = gtimer();
-    const double *const x0 = P.X0 ? P.X0 : P.T_in;
-    unsigned nbar = 0;
+    const double *const x0 = P.X0 ? P.X0 : Tin;
 
     // One pass over the CTA's rows: (K~ w)_l for every own row l with w_j = gv(j), then fin(l, sum)
     // by one thread per row.  A volume row is summed by 4 threads (entries q, q + 4, ...), an
@@ -230,9 +254,9 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_cg_resident(CGParams P) {
     // formed here with the expressions of k_extrap (thermo.cu) -- T^{n-1} still sits in T_out, which
     // is only written at the end of the launch, after every CTA has passed phase 0
     auto gx = [&](int64_t j) -> double {
-        if (P.xorder == 0) return __ldg(x0 + j);
-        const double a = ld_cg1(P.T_in + j), d = a - ld_cg1(P.T_out + j);
-        return P.xorder >= 2 ? fma(3.0, d, ld_cg1(P.Th + j)) : a + d;
+        if (xorder == 0) return ld_cg1(x0 + j);
+        const double a = ld_cg1(Tin + j), d = a - ld_cg1(Tout + j);
+        return xorder >= 2 ? fma(3.0, d, ld_cg1(P.Th + j)) : a + d;
     };
     sweep([&](int j) { return gx(j); },
           [&](int l, double ax) {
@@ -240,12 +264,12 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_cg_resident(CGParams P) {
               const int ik = iks[l];
               double bi = P.benv[i];
               if (ik >= 0) {
-                  bi += P.if_b[ik];
-                  if (ik < P.nA) red0[3] += P.if_phi[ik];
+                  bi += if_b[ik];
+                  if (ik < P.nA) red0[3] += if_phi[ik];
               }
-              bi = P.rhs ? P.rhs[i] : fma(P.ML[i], P.T_in[i], P.dt * bi);
+              bi = P.rhs ? P.rhs[i] : fma(P.ML[i], ld_cg1(Tin + i), P.dt * bi);
               const double r = bi - ax;
-              const double zi = (ik >= 0 && P.if_dinv_s ? P.if_dinv_s[ik] : P.Dinv[i]) * r;
+              const double zi = (ik >= 0 && if_dinv_s ? if_dinv_s[ik] : P.Dinv[i]) * r;
               xs[l] = gx(i);
               zs[l] = zi;
               ps[l] = zi;
@@ -326,21 +350,25 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_cg_resident(CGParams P) {
     __syncthreads();
     // the last update of x is still to be applied (alpha = 0 after an exit on the direct r.r test)
     for (int l = t; l < nloc; l += RS_THREADS) {
-        if (P.xsave) P.Th[r0 + l] = P.T_out[r0 + l];   // history shift: T^{n-1} before it is overwritten
-        P.T_out[r0 + l] = fma(alpha, ps[l], xs[l]);
+        if (xsave && xorder > 0) P.Th[r0 + l] = Tout[r0 + l];   // history shift: T^{n-1} before it is overwritten
+        Tout[r0 + l] = fma(alpha, ps[l], xs[l]);
     }
     if (rank == 0 && t == 0) {
         const double rel = tot0[0] > 0.0 ? sqrt(rr / tot0[0]) : sqrt(rr);
-        P.iters_out[P.step] = it;
-        P.relres_out[P.step] = rel;
-        P.area_out[P.step] = tot0[3];
+        P.iters_out[step] = it;
+        P.relres_out[step] = rel;
+        P.area_out[step] = tot0[3];
         if (!conv) {
             P.status[0] = 1;
-            P.status[2] = P.step;
+            P.status[2] = step;
             P.status[3] = 0;
             *P.fail_relres = rel;
         }
     }
+    if (!conv) break;   // (the same decision in every CTA: identical totals)
+    // the next step gathers this step's state (and the shifted history) from every CTA
+    if (sti + 1 < P.nst) rs_barrier(P.gbar, ++nbar * (unsigned)nct);
+    }   // steps of the launch
 }
 
 // CTAs of a launch: one per SM (the overlap mode leaves some SMs to the interface kernels), but
@@ -502,6 +530,7 @@ int ahead_setup(Ctx &c) {
 // smaller grid, and record its launch-completion event).
 int rs_launch(Ctx &c, CGParams &P, bool ovl, int buf) {
     P.rs_ell = std::max(c.cap, 1);
+    if (P.nst < 1) P.nst = 1;
     P.rs_part = c.d_rs_part[ovl ? 1 : 0];
     P.if_of_row = c.d_if_of_row;
     P.z2 = c.d_z2;

@@ -266,9 +266,9 @@ void chunk_windows_launch(Ctx &c, int W, int gap, int2 *runs, int32_t *nruns, in
                           int *d_stats);
 // x0: initial guess (extrapolated state, see thermo.cu), nullptr = the committed state T^n
 int cg_launch_step(Ctx &c, int step, double dt, const double *x0 = nullptr, int buf = 0, bool ovl = false,
-                   int ah_slot = -1, int xorder = 0, bool xsave = false);
-// ah_slot >= 0: the interface rows of that slot of the ahead buffers; xorder / xsave (resident kernel): the
-// extrapolated start of that order and the history shift done inside the solve kernel
+                   int ah_slot = -1, int xhist = 0, int xguess = 0, int nst = 1);
+// ah_slot >= 0: the interface rows of that slot of the ahead buffers; resident kernel: xhist / xguess = states
+// behind T^n available / wanted for the extrapolated start formed inside the kernel, nst = steps of the launch
 int overlap_setup(Ctx &c);   // second interface buffer set, side stream, reduced CG grid
 // Solve (M_L - a K_vol [- a K_G]) x = rhs from x0 with the operator currently in d_val (a =
 // built_dt); iface = false: no interface rows.  Iterations / residual to iters_out[slot].

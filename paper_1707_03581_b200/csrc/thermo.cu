@@ -720,6 +720,8 @@ extern "C" int thermo_step(thermo_ctx *ctx, double t, double dt, int32_t nsteps)
         }
         int64_t launches = 0;
         const bool ahead = c->ah_on && S == 1;   // (implicit Euler: the SDC methods returned above)
+        // steps per launch of the resident solve (THERMO_RS_STEPS: 1 = one launch per step)
+        const int rs_steps_max = getenv("THERMO_RS_STEPS") ? std::max(1, atoi(getenv("THERMO_RS_STEPS"))) : 16;
         const bool ovl = c->overlap && S == 1 && !ahead;
         bool spec_launched = false;
         int ah_batches = 0;
@@ -861,12 +863,31 @@ extern "C" int thermo_step(thermo_ctx *ctx, double t, double dt, int32_t nsteps)
                 return THERMO_ECUDA;
             }
             if (c->timing) API_CK(cudaEventRecord(c->events[2 * n + 1], c->stream));
+            // resident solve in ahead mode: the following steps whose interfaces sit in the next
+            // slots run in the same launch (the operator is loaded once, no launch gaps; the state
+            // buffers alternate inside the kernel)
+            int g = 1;
+            if (ahead && fold) {
+                while (n + g < nsteps && g < rs_steps_max && c->ah_next < c->ah_count &&
+                       c->ah_tp[c->ah_next] == t + (double)(n + g + 1) * dt) {
+                    ++c->ah_next;
+                    API_CK(guard_write(c, (c->cur + n + g + 1) & 1));
+                    ++g;
+                }
+            }
             const double *x0 = avail > 0 && !fold ? c->d_x0 : nullptr;
-            if ((S == 1 ? thermo::cg_launch_step(*c, n, dt, x0, ovl ? bs(n) : 0, ovl, ah_slot, fold ? avail : 0,
-                                                 fold && avail > 0 && c->guess >= 2)
+            if ((S == 1 ? thermo::cg_launch_step(*c, n, dt, x0, ovl ? bs(n) : 0, ovl, ah_slot,
+                                                 fold && extrap ? c->hist + n : 0, fold && extrap ? c->guess : 0, g)
                         : thermo::cgb_launch_step(*c, n, dt, x0)))
                 return THERMO_ECUDA;
             launches += 1;
+            for (int j = 1; j < g; ++j) {   // the launch's later steps: their time is booked on its first
+                if (c->timing) {
+                    API_CK(cudaEventRecord(c->events[2 * (n + j)], c->stream));
+                    API_CK(cudaEventRecord(c->events[2 * (n + j) + 1], c->stream));
+                }
+            }
+            n += g - 1;
             if (ovl) API_CK(cudaEventRecord(c->ev_done[bs(n)], c->stream));
             if (ovl && n + 1 < nsteps && side_iface(n + 1)) return THERMO_ECUDA;
         }
