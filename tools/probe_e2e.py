@@ -1,9 +1,9 @@
-"""End-to-end probe of the batched configuration: where the one-step-per-call loop with a host
-copy of every step's fields loses time against the device-only run.
+"""End-to-end probe: where the one-step-per-call loop with a host copy of every step's fields
+loses time against the device-only run (bench.py's e2e loop).
 
-    python tools/probe_e2e.py [K]
+    python tools/probe_e2e.py [K] [config]          (default: 20, cfg4)
 prints ms per step of (a) one K-step call, (b) K one-step calls, (c) K one-step calls each followed
-by thermo_get_T_all_async (bench.py's e2e loop), and the D2H rate of the pinned host buffer.
+by thermo_get_T_all_async, and the D2H rate of the pinned host buffer.
 """
 import sys
 import time
@@ -12,10 +12,16 @@ import torch
 
 sys.path.insert(0, ".")
 from paper_1707_03581_b200 import inputs as I  # noqa: E402
+import os  # noqa: E402
+import paper_1707_03581_b200.thermo as _T  # noqa: E402
 from paper_1707_03581_b200.thermo import Thermo  # noqa: E402
 
+if os.environ.get("DIAG_LIB"):   # another build of libthermo.so (A/B on one box)
+    _T.load(os.environ["DIAG_LIB"])
+
 K = int(sys.argv[1]) if len(sys.argv) > 1 else 20
-cfg = I.make_config("cfg4")
+name = sys.argv[2] if len(sys.argv) > 2 else "cfg4"
+cfg = I.make_config(name)
 stream = torch.cuda.current_stream()
 th = Thermo.from_config(cfg, stream=stream.cuda_stream)
 t = 0.0
@@ -25,7 +31,6 @@ hosts = [torch.empty(th.S * cfg.n_dof, dtype=torch.float64, pin_memory=True) for
 
 
 def timed(fn):
-    global t
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     w0 = time.perf_counter()
@@ -58,11 +63,12 @@ def k_calls_copy():
     th.sync()
 
 
-for name, fn in (("one K-step call", one_call), ("K one-step calls", k_calls),
-                 ("K one-step calls + get_T_all_async", k_calls_copy)):
+for label, fn in (("one K-step call", one_call), ("K one-step calls", k_calls),
+                  ("K one-step calls + get_T_all_async", k_calls_copy)):
     fn()   # warm
     ev, wall = timed(fn)
-    print(f"{name:38s}: {ev:.3f} ms/step (events), {wall:.3f} ms/step (wall)")
+    it = th.step_iters()
+    print(f"{name} {label:38s}: {ev:.3f} ms/step (events), {wall:.3f} ms/step (wall); iterations of the last call {it.ravel()[:12].tolist()}", flush=True)
 dev = torch.empty(th.S * cfg.n_dof, dtype=torch.float64, device="cuda")
 torch.cuda.synchronize()
 w0 = time.perf_counter()
