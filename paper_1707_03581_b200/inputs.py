@@ -332,12 +332,15 @@ def make_config(name: str, n_scen: Optional[int] = None, jitter: Optional[float]
     """Build one named configuration.
 
     cfg0..cfg4 are BASELINE.json configs[0..4]; "small" and "medium" are extra parity
-    sizes (same geometry as cfg 0/1, several SELL slices + a ragged tail).  `jitter`
-    overrides the configuration's node jitter (fraction of h)."""
-    if name in ("cfg0", "small", "medium", "cfg1", "cfg4"):
+    sizes (same geometry as cfg 0/1, several SELL slices + a ragged tail); "paper" has the DoF
+    count of the paper's machine model (16,626 DoF; here 16,870) on the same geometry, for
+    the look-ahead measurements.  `jitter` overrides the configuration's node jitter (fraction
+    of h)."""
+    if name in ("cfg0", "small", "medium", "paper", "cfg1", "cfg4"):
         cells = {"cfg0": ((16, 4, 2), (5, 3, 2)),
                  "small": ((32, 8, 4), (10, 6, 3)),
                  "medium": ((64, 16, 8), (20, 12, 6)),
+                 "paper": ((72, 18, 9), (24, 14, 7)),
                  "cfg1": ((128, 32, 16), (40, 24, 12)),
                  "cfg4": ((128, 32, 16), (40, 24, 12))}[name]
         fixed, moving = rail_pair(*cells, jitter=0.0 if jitter is None else jitter)
@@ -353,7 +356,7 @@ def make_config(name: str, n_scen: Optional[int] = None, jitter: Optional[float]
             dt, nsteps = 0.5, 1000
         else:
             scen = [Scenario(0.375, 0.375, 60.0, 500.0, 0.5, 20.0)]
-            dt, nsteps = 0.5, {"small": 50, "medium": 30}[name]
+            dt, nsteps = 0.5, {"small": 50, "medium": 30, "paper": 30}[name]
         return Config(name, fixed, moving, NU, RHO_CP, ALPHA_IFACE, _std_robin(), scen,
                       24.0, dt, nsteps, description=f"rail pair {cells}")
     if name in ("cfg2", "cfg3"):

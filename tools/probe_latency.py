@@ -16,7 +16,7 @@ from paper_1707_03581_b200 import inputs as I  # noqa: E402
 from paper_1707_03581_b200.thermo import Thermo  # noqa: E402
 
 K = int(sys.argv[1]) if len(sys.argv) > 1 else 50
-for name, jit in (("cfg0", None), ("small", 0.1), ("medium", 0.1), ("cfg1", None)):
+for name, jit in (("cfg0", None), ("small", 0.1), ("medium", 0.1), ("paper", 0.1), ("cfg1", None)):
     for mode in ("resident", "cluster", "grid"):
         os.environ.pop("THERMO_CG_CLUSTER", None)
         if mode != "resident":
