@@ -35,7 +35,7 @@ def rel(a, b):
     return float(np.abs(a - b).max() / np.abs(b).max())
 
 
-@pytest.mark.parametrize("name,jitter", [("cfg0", None), ("small", 0.1), ("medium", 0.1)])
+@pytest.mark.parametrize("name,jitter", [("cfg0", None), ("small", 0.1), ("medium", 0.1), ("paper", 0.1)])
 def test_resident_solve_selected_parity_and_reproducible(monkeypatch, name, jitter):
     """Default path on small problems = the resident kernel: whole field vs the oracle, vs the
     streaming grid kernel (same iteration counts +-1), and bitwise equal from run to run."""
