@@ -374,7 +374,8 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_cg_resident(CGParams P) {
 // CTAs of a launch: one per SM (the overlap mode leaves some SMs to the interface kernels), but
 // never more than slices -- fewer arrivals make the barrier of a tiny problem cheaper
 static int rs_grid(const Ctx &c, bool ovl) {
-    const int g = ovl && c.cg_grid_ovl > 0 ? c.cg_grid_ovl : c.num_sms;
+    int g = ovl && c.cg_grid_ovl > 0 ? c.cg_grid_ovl : c.num_sms;
+    if (const char *e = getenv("THERMO_RS_CTAS")) g = std::max(1, std::min(g, atoi(e)));   // tuning hook
     return (int)std::max<int64_t>(1, std::min<int64_t>(g, c.nslices));
 }
 
