@@ -592,7 +592,6 @@ __global__ void __launch_bounds__(SB_THREADS, 1) k_sbcg_step(SBParams P) {
         return;
     }
     cg::grid_group grid = cg::this_grid();
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) {
         for (int k = 0; k < P.nstages; ++k) {
             mbar_init(&bar_full[k], 1);
